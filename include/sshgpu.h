@@ -1,0 +1,147 @@
+/*
+ * sshgpu.h — C-ABI of the B200-native SSH (Sketch, Shingle & Hash) hot path.
+ *
+ * One shared library, libsshgpu.so (sm_100a, static cudart), exports these
+ * entry points.  Signatures use plain pointers and sizes only: device
+ * pointers are caller-owned (the Python host allocates them with PyTorch),
+ * `stream` is a cudaStream_t passed as void*, and every call is
+ * stream-ordered.  Functions return SSH_OK (0) or a negative error code;
+ * ssh_last_error() returns a thread-local message for the last failure.
+ *
+ * Each entry point names the reference function it replaces
+ * (/root/reference/pkg/src/sshts/<file>:<line>).  The reference itself has
+ * no C ABI — it is a Python package — so the "binding a maintainer would
+ * add" is a ctypes stub; paper_1610_07328_b200/_native.py
+ * is exactly that binding.
+ */
+#ifndef SSHGPU_H
+#define SSHGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSHGPU_ABI_VERSION 1
+
+enum {
+    SSH_OK = 0,
+    SSH_ERR_INVALID = -1,     /* bad argument (message names it)            */
+    SSH_ERR_CUDA = -2,        /* CUDA runtime failure                        */
+    SSH_ERR_OOM = -3,         /* device allocation failed                    */
+    SSH_ERR_UNSUPPORTED = -4, /* parameter outside the device path's range   */
+    SSH_ERR_STATE = -5        /* call order violated (e.g. params not set)   */
+};
+
+/* Pipeline parameters: SshParams (index.py:32-56) + K (concatenation order,
+ * wmh.py:107-125) + the series length and the DTW radius
+ * r = int(round(band * m)) (dtw.py:38-39), resolved by the host. */
+typedef struct ssh_params {
+    int32_t m;      /* series length t                            */
+    int32_t W;      /* filter length                              */
+    int32_t delta;  /* filter step                                */
+    int32_t n;      /* shingle length (device path: 1..20)        */
+    int32_t L;      /* number of tables (SshParams.d)             */
+    int32_t K;      /* CWS samples concatenated per table key     */
+    uint64_t seed;  /* master seed (filter + CWS)                 */
+    int32_t radius; /* Sakoe-Chiba radius r                       */
+    int32_t reserved;
+} ssh_params;
+
+typedef struct ssh_ctx ssh_ctx;     /* per device: params, filter, CWS tables */
+typedef struct ssh_index ssh_index; /* per shard: L CSR bucket tables          */
+
+const char *ssh_last_error(void);
+int ssh_abi_version(void);
+
+/* Context for `device`; owns the uploaded filter and CWS tables. */
+int ssh_ctx_create(int device, ssh_ctx **out);
+int ssh_ctx_destroy(ssh_ctx *ctx);
+
+/* Upload parameters and host tables (all HOST pointers):
+ *   filter  f64[W]              make_filter (sketch.py:36-43), index.py:162
+ *   tab_r, tab_lnc, tab_beta    f64[2^n][L*K], layout [token][slot]: the CWS
+ *                               variates r, ln c, beta of wmh.py:60-72
+ *   ln_w    f64[max_count+1]    np.log(count) of wmh.py:72 (entry 0 unused)
+ * Replaces the stateless variate evaluation inside _cws_keys (wmh.py:52-81):
+ * the device never evaluates log(), so keys are bit-identical to the
+ * reference for the host's numpy. */
+int ssh_ctx_set_params(ssh_ctx *ctx, const ssh_params *p, const double *filter,
+                       const double *tab_r, const double *tab_lnc, const double *tab_beta,
+                       const double *ln_w, int32_t max_count);
+
+/* Sizes derived from the parameters. */
+int ssh_num_sketch_bits(const ssh_ctx *ctx);   /* N_B  (sketch.py:46-48)      */
+int ssh_sketch_words(const ssh_ctx *ctx);      /* ceil(N_B/64)                */
+int ssh_tokens_per_series(const ssh_ctx *ctx); /* N_B - n + 1                 */
+
+/* K1 — sketch_matrix (sketch.py:69-89) / sketch_values (sketch.py:51-61).
+ * X: f32[N][ld] device.  bits: u64[N][words], bit i of a row = window i
+ * has dot >= 0 (+1).  stats (device i64[2] or NULL, accumulated):
+ * [0] windows re-evaluated in exact f64, [1] windows with |dot| < 1e-9. */
+int ssh_sketch(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *bits,
+               int64_t *stats, void *stream);
+
+/* K2 — tokenize_bits + np.unique(return_counts) (shingle.py:56-75,
+ * index.py:118).  Per series: distinct tokens ascending with counts, in rows
+ * of T = N_B-n+1 slots; set_len[i] = number of distinct tokens. */
+int ssh_shingle(ssh_ctx *ctx, const uint64_t *bits, int64_t N, uint32_t *tokens,
+                uint16_t *counts, int32_t *set_len, void *stream);
+
+/* K3 — _cws_keys + signature(concat=K) (wmh.py:52-81, 107-125).
+ * keys: u64[N][L*K] raw slot keys (or NULL); sig: u64[N][L] folded keys. */
+int ssh_cws(ssh_ctx *ctx, const uint32_t *tokens, const uint16_t *counts,
+            const int32_t *set_len, int64_t N, uint64_t *keys, uint64_t *sig, void *stream);
+
+/* K1->K3 fused — compute_signatures (index.py:123-138) with the K fold and
+ * query_signature (index.py:175-181).  sig: u64[N][L]. */
+int ssh_signatures(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *sig,
+                   int64_t *stats, void *stream);
+
+/* K4 — _tables_from_signatures (index.py:141-156): per table a stable
+ * radix sort of (key, id) -> CSR (sorted unique keys, offsets, ids ascending
+ * within each bucket).  Ids are id_base + row.  Synchronises `stream` once
+ * to read back bucket counts. */
+int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int64_t id_base,
+                    ssh_index **out, void *stream);
+int ssh_index_destroy(ssh_index *idx);
+int ssh_index_num_buckets(const ssh_index *idx, int table, int64_t *n_buckets);
+int64_t ssh_index_size(const ssh_index *idx);
+/* Copy table `table` to HOST arrays: keys u64[nb], offsets i64[nb+1],
+ * ids i64[N] (global ids).  The reference's dict view (index.py:151-154). */
+int ssh_index_export(const ssh_index *idx, int table, uint64_t *keys, int64_t *offsets,
+                     int64_t *ids, void *stream);
+
+/* K6 — probe_candidates (index.py:184-190) for a batch: membership bitmap
+ * u32[nq][ceil(N/32)] of the deduplicated bucket union (bit = local row),
+ * and n_cand[nq] = |R|.  qsig: u64[nq][L] device. */
+int ssh_probe(ssh_ctx *ctx, const ssh_index *idx, const uint64_t *qsig, int32_t nq,
+              uint32_t *bitmap, int64_t *n_cand, void *stream);
+
+/* K5..K10 — query_index (index.py:204-273) for a batch of nq queries:
+ * hash, probe, LB_Kim/LB_Keogh/LB_Keogh2-gated banded DTW (fp32) and exact
+ * fp64 rescoring of the top-k boundary set.  X: f32[N][m] device (the
+ * shard), Q: f32[nq][m] device.  Outputs (device): ids i64[nq][k] (global,
+ * -1 padded), d2 f64[nq][k] squared DTW (bit-identical to dtw.py:83-121),
+ * n_out i32[nq], n_cand i64[nq] (|R|), counters i64[nq][5] =
+ * [kim_pruned, keogh_pruned, keogh2_pruned, dtw_computed, dtw_abandoned]
+ * (SearchStats, dtw.py:50-72; batch-order semantics),
+ * status i32[nq] = 0 "ok", 1 "no-candidates", 2 "fallback" (index.py:99). */
+#define SSH_QUERY_FALLBACK_ON_EMPTY 1 /* empty R -> exact search over the shard
+                                         (query_index(fallback_on_empty=True),
+                                         index.py:239-243) */
+int ssh_query_batch(ssh_ctx *ctx, const ssh_index *idx, const float *X, const float *Q,
+                    int32_t nq, int32_t k, int32_t flags, int64_t *ids, double *d2,
+                    int32_t *n_out, int64_t *n_cand, int64_t *counters, int32_t *status,
+                    void *stream);
+
+/* Exact f64 banded DTW (dtw.py:83-121, FMA-free, no abandon) of npair
+ * (query row, series row) pairs; rows index X / Q.  d2: f64[npair]. */
+int ssh_dtw_exact(ssh_ctx *ctx, const float *X, const float *Q, const int32_t *qrow,
+                  const int64_t *xrow, int64_t npair, double *d2, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSHGPU_H */

@@ -1,0 +1,39 @@
+"""B200-native SSH (Sketch, Shingle & Hash) index-build and query path.
+
+Drop-in for the reference package's hot path (sshts.index: build_index,
+query_index).  All compute runs in libsshgpu.so (hand-written
+sm_100a CUDA behind the C-ABI in include/sshgpu.h); there is no CPU
+fallback.
+"""
+
+from .core import (
+    ConfigError,
+    DataFormatError,
+    Dataset,
+    IndexLoadError,
+    SshError,
+    TimeSeries,
+    z_normalize,
+    z_normalize_dataset,
+    z_normalize_rows,
+    z_normalize_values,
+)
+from .cws import make_filter
+from .index import (
+    QueryResult,
+    QueryStats,
+    RandomFilter,
+    SearchStats,
+    SshIndex,
+    SshParams,
+    WarpingParams,
+    build_index,
+    compute_signatures,
+    num_sketch_bits,
+    probe_candidates,
+    query_index,
+    query_index_batch,
+    query_signature,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,96 @@
+// common.cuh — shared device/host helpers for libsshgpu (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/sshgpu.h"
+
+#define SSH_MAX_W 256
+#define SSH_MAX_N 20          // table-based CWS: 2^n x S variates resident in HBM
+#define SSH_MAX_SLOTS 256     // K*L
+#define SSH_SALT_KEY 0xEB44ACCAB455D165ULL
+
+// --------------------------------------------------------------- errors
+void ssh_set_error(const char *fmt, ...);
+int ssh_cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define SSH_CUDA(call)                                                           \
+    do {                                                                         \
+        cudaError_t _e = (call);                                                 \
+        if (_e != cudaSuccess) return ssh_cuda_fail(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+
+#define SSH_CHECK_LAUNCH() SSH_CUDA(cudaGetLastError())
+
+#define SSH_REQUIRE(cond, code, ...)       \
+    do {                                   \
+        if (!(cond)) {                     \
+            ssh_set_error(__VA_ARGS__);    \
+            return (code);                 \
+        }                                  \
+    } while (0)
+
+// --------------------------------------------------------------- context
+struct ssh_ctx {
+    int device = 0;
+    int num_sms = 148;
+    bool have_params = false;
+    ssh_params p{};
+    int nb = 0;      // sketch bits per series
+    int words = 0;   // u64 words per bit row
+    int T = 0;       // tokens per series
+    int S = 0;       // K*L slots
+    int max_count = 0;
+    float screen_c = 0.f;  // |dot32 - dot64| <= screen_c * max|x|  (sketch.cu)
+    float h_w32[SSH_MAX_W];  // filter rounded to f32 (host copy, passed as kernel params)
+    double *d_w64 = nullptr;  // filter f64[W]
+    float *d_w32 = nullptr;   // filter rounded to f32
+    double *d_r = nullptr, *d_lnc = nullptr, *d_beta = nullptr, *d_lna1 = nullptr;
+    double *d_lnw = nullptr;  // ln(count)
+    size_t tab_entries = 0;
+    // scratch reused across calls (grown on demand)
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+};
+
+struct ssh_index {
+    int L = 0;
+    int64_t N = 0;
+    int64_t id_base = 0;
+    int device = 0;
+    uint64_t *keys = nullptr;     // concatenated unique keys, table j at kbase[j]
+    uint32_t *offsets = nullptr;  // concatenated offsets, table j at kbase[j] + j (nb+1 entries)
+    uint32_t *ids = nullptr;      // L x N local row ids
+    int64_t *h_nb = nullptr;      // host: buckets per table
+    int64_t *h_kbase = nullptr;   // host: bucket base per table
+    int64_t *d_nb = nullptr;      // device copies
+    int64_t *d_kbase = nullptr;
+    int64_t total_buckets = 0;
+};
+
+// grow ctx scratch; returns pointer or nullptr (error set)
+void *ssh_scratch(ssh_ctx *ctx, size_t bytes, cudaStream_t st);
+
+// ----------------------------------------------------------- device math
+__host__ __device__ __forceinline__ uint64_t ssh_mix64(uint64_t x) {
+    // splitmix64 finalizer (wmh.py:34-44)
+    uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+static inline int ssh_div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// kernel launchers implemented per translation unit
+int ssh_launch_sketch(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *bits,
+                      int64_t *stats, cudaStream_t st);
+int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *tok_in,
+                           const uint16_t *cnt_in, const int32_t *len_in, int64_t N,
+                           uint32_t *tok_out, uint16_t *cnt_out, int32_t *len_out,
+                           uint64_t *keys_out, uint64_t *sig_out, int mode, cudaStream_t st);
+int ssh_launch_lna1(ssh_ctx *ctx, cudaStream_t st);
+
+enum { SIG_MODE_SHINGLE = 1, SIG_MODE_CWS_FROM_SETS = 2, SIG_MODE_FUSED = 3 };

@@ -1,0 +1,381 @@
+// tables.cu — K4: LSH bucket tables (index.py:141-156, _tables_from_signatures).
+//
+// Reference: per table j, order = argsort(sig[:, j], kind="stable"); buckets
+// are runs of equal keys, ids ascending inside a bucket.  Device: per table,
+// an LSD radix sort of (key u64, row u32) with 8-bit digits (8 passes, all L
+// tables in one launch per pass via blockIdx.y), stable by construction
+// (per-warp ordered ranking with __match_any_sync), tiles staged in shared
+// memory so each digit run is written contiguously.  Then a run-length pass
+// emits CSR: sorted unique keys, u32 offsets, u32 rows.  Bytes per
+// (series, table): 8 B key read + 8 B key + 4 B row written per pass.
+#include "common.cuh"
+
+#define RS_THREADS 256
+#define RS_WARPS (RS_THREADS / 32)
+#define RS_ITEMS 12
+#define RS_TILE (RS_THREADS * RS_ITEMS)
+#define RS_BINS 256
+
+// sig [N][L] row-major -> keys [L][N], rows [L][N] = 0..N-1
+__global__ void rs_transpose(const uint64_t *__restrict__ sig, int64_t N, int L,
+                             uint64_t *__restrict__ keys, uint32_t *__restrict__ rows) {
+    __shared__ uint64_t tile[32][33];
+    int64_t r0 = (int64_t)blockIdx.x * 32;
+    int j0 = blockIdx.y * 32;
+    int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int yy = ty; yy < 32; yy += 8) {
+        int64_t r = r0 + yy;
+        int j = j0 + tx;
+        if (r < N && j < L) tile[yy][tx] = sig[r * L + j];
+    }
+    __syncthreads();
+    for (int yy = ty; yy < 32; yy += 8) {
+        int j = j0 + yy;
+        int64_t r = r0 + tx;
+        if (r < N && j < L) {
+            keys[(int64_t)j * N + r] = tile[tx][yy];
+            rows[(int64_t)j * N + r] = (uint32_t)r;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+rs_hist(const uint64_t *__restrict__ keys, int64_t N, int shift, int ntiles,
+        uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[RS_BINS];
+    const int j = blockIdx.y;
+    const int tile = blockIdx.x;
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t *k = keys + (int64_t)j * N;
+    int64_t base = (int64_t)tile * RS_TILE;
+#pragma unroll 4
+    for (int it = 0; it < RS_ITEMS; it++) {
+        int64_t i = base + it * RS_THREADS + threadIdx.x;
+        if (i < N) atomicAdd(&h[(k[i] >> shift) & 0xFF], 1u);
+    }
+    __syncthreads();
+    // digit-major layout: hist[j][digit][tile]
+    hist[((int64_t)j * RS_BINS + threadIdx.x) * ntiles + tile] = h[threadIdx.x];
+}
+
+// exclusive scan of hist[j][*] (RS_BINS * ntiles entries), one block per table
+__global__ void __launch_bounds__(1024) rs_scan(uint32_t *__restrict__ hist, int ntiles) {
+    __shared__ uint32_t part[1024];
+    const int j = blockIdx.x;
+    uint32_t *h = hist + (int64_t)j * RS_BINS * ntiles;
+    const int64_t n = (int64_t)RS_BINS * ntiles;
+    const int64_t chunk = (n + 1023) / 1024;
+    int64_t b = threadIdx.x * chunk, e = min(n, b + chunk);
+    uint32_t s = 0;
+    for (int64_t i = b; i < e; i++) s += h[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        uint32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+    for (int64_t i = b; i < e; i++) {
+        uint32_t v = h[i];
+        h[i] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+rs_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ rin, int64_t N,
+           int shift, int ntiles, const uint32_t *__restrict__ gofs, uint64_t *__restrict__ kout,
+           uint32_t *__restrict__ rout) {
+    __shared__ uint32_t wcnt[RS_WARPS][RS_BINS];
+    __shared__ uint32_t dstart[RS_BINS];
+    __shared__ uint64_t skey[RS_TILE];
+    __shared__ uint32_t srow[RS_TILE];
+    const int j = blockIdx.y;
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int e = threadIdx.x; e < RS_WARPS * RS_BINS; e += RS_THREADS) (&wcnt[0][0])[e] = 0;
+    __syncthreads();
+    const uint64_t *k = kin + (int64_t)j * N;
+    const uint32_t *r = rin + (int64_t)j * N;
+    // warp w owns the contiguous sub-tile [w*32*ITEMS, (w+1)*32*ITEMS) of the tile
+    const int64_t wbase = (int64_t)tile * RS_TILE + (int64_t)w * 32 * RS_ITEMS;
+    uint64_t key[RS_ITEMS];
+    uint32_t row[RS_ITEMS];
+    uint32_t rank[RS_ITEMS];
+#pragma unroll
+    for (int it = 0; it < RS_ITEMS; it++) {
+        int64_t i = wbase + it * 32 + lane;
+        bool valid = i < N;
+        key[it] = valid ? k[i] : 0ULL;
+        row[it] = valid ? r[i] : 0u;
+        unsigned d = valid ? (unsigned)((key[it] >> shift) & 0xFF) : RS_BINS;
+        unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        unsigned before = valid ? wcnt[w][d] : 0u;
+        rank[it] = before + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wcnt[w][d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // exclusive prefix over warps per digit; digit totals
+    {
+        const int d = threadIdx.x;
+        uint32_t run = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS_WARPS; ww++) {
+            uint32_t t = wcnt[ww][d];
+            wcnt[ww][d] = run;
+            run += t;
+        }
+        dstart[d] = run;
+    }
+    __syncthreads();
+    // exclusive scan over digits (256 entries, one thread each)
+    {
+        const int d = threadIdx.x;
+        uint32_t v = dstart[d];
+        // warp-level inclusive scan then cross-warp fixup
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        __shared__ uint32_t wsum[RS_WARPS];
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        uint32_t add = 0;
+        for (int ww = 0; ww < w; ww++) add += wsum[ww];
+        __syncthreads();
+        dstart[d] = x - v + add;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < RS_ITEMS; it++) {
+        int64_t i = wbase + it * 32 + lane;
+        if (i < N) {
+            unsigned d = (unsigned)((key[it] >> shift) & 0xFF);
+            uint32_t pos = dstart[d] + wcnt[w][d] + rank[it];
+            skey[pos] = key[it];
+            srow[pos] = row[it];
+        }
+    }
+    __syncthreads();
+    const int64_t tbase = (int64_t)tile * RS_TILE;
+    const int nvalid = (int)min((int64_t)RS_TILE, N - tbase);
+    const uint32_t *go = gofs + (int64_t)j * RS_BINS * ntiles;
+    for (int e = threadIdx.x; e < nvalid; e += RS_THREADS) {
+        uint64_t kk = skey[e];
+        unsigned d = (unsigned)((kk >> shift) & 0xFF);
+        int64_t dst = (int64_t)go[(int64_t)d * ntiles + tile] + (e - dstart[d]);
+        kout[(int64_t)j * N + dst] = kk;
+        rout[(int64_t)j * N + dst] = srow[e];
+    }
+}
+
+// run starts per tile: count flags
+__global__ void __launch_bounds__(RS_THREADS)
+rle_count(const uint64_t *__restrict__ keys, int64_t N, int ntiles, uint32_t *__restrict__ bcnt) {
+    const int j = blockIdx.y, tile = blockIdx.x;
+    const uint64_t *k = keys + (int64_t)j * N;
+    uint32_t c = 0;
+    for (int it = 0; it < RS_ITEMS; it++) {
+        int64_t i = (int64_t)tile * RS_TILE + it * RS_THREADS + threadIdx.x;
+        if (i < N && (i == 0 || k[i] != k[i - 1])) c++;
+    }
+    __shared__ uint32_t red[RS_WARPS];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int w = 0; w < RS_WARPS; w++) s += red[w];
+        bcnt[(int64_t)j * ntiles + tile] = s;
+    }
+}
+
+// per table: exclusive scan of tile counts; nb[j] = total
+__global__ void rle_scan(uint32_t *__restrict__ bcnt, int ntiles, int64_t *__restrict__ nb) {
+    const int j = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    uint32_t *b = bcnt + (int64_t)j * ntiles;
+    uint32_t run = 0;
+    for (int t = 0; t < ntiles; t++) {
+        uint32_t v = b[t];
+        b[t] = run;
+        run += v;
+    }
+    nb[j] = run;
+}
+
+__global__ void __launch_bounds__(RS_THREADS)
+rle_emit(const uint64_t *__restrict__ keys, int64_t N, int ntiles, const uint32_t *__restrict__ bofs,
+         const int64_t *__restrict__ kbase, const int64_t *__restrict__ nb,
+         uint64_t *__restrict__ ukeys, uint32_t *__restrict__ offsets) {
+    const int j = blockIdx.y, tile = blockIdx.x;
+    const uint64_t *k = keys + (int64_t)j * N;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ uint32_t wsum[RS_WARPS];
+    __shared__ uint32_t running;
+    if (threadIdx.x == 0) running = bofs[(int64_t)j * ntiles + tile];
+    __syncthreads();
+    uint64_t *uk = ukeys + kbase[j];
+    uint32_t *of = offsets + kbase[j] + j;
+    for (int it = 0; it < RS_ITEMS; it++) {
+        int64_t i = (int64_t)tile * RS_TILE + it * RS_THREADS + threadIdx.x;
+        bool f = i < N && (i == 0 || k[i] != k[i - 1]);
+        unsigned m = __ballot_sync(0xFFFFFFFFu, f);
+        if (lane == 0) wsum[w] = __popc(m);
+        __syncthreads();
+        uint32_t before = running;
+        for (int ww = 0; ww < w; ww++) before += wsum[ww];
+        if (f) {
+            uint32_t pos = before + __popc(m & ((1u << lane) - 1u));
+            uk[pos] = k[i];
+            of[pos] = (uint32_t)i;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t s = 0;
+            for (int ww = 0; ww < RS_WARPS; ww++) s += wsum[ww];
+            running += s;
+        }
+        __syncthreads();
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) of[nb[j]] = (uint32_t)N;
+}
+
+extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int64_t id_base,
+                               ssh_index **out, void *stream) {
+    SSH_REQUIRE(ctx && out, SSH_ERR_INVALID, "ssh_index_build: NULL argument");
+    SSH_REQUIRE(ctx->have_params, SSH_ERR_STATE, "ssh_index_build: ssh_ctx_set_params not called");
+    SSH_REQUIRE(N >= 1 && N < (int64_t)0xFFFFFFFF, SSH_ERR_INVALID,
+                "ssh_index_build: N=%lld outside [1, 2^32-1)", (long long)N);
+    SSH_REQUIRE(sig != nullptr, SSH_ERR_INVALID, "ssh_index_build: sig is NULL");
+    SSH_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int L = ctx->p.L;
+    const int ntiles = ssh_div_up(N, RS_TILE);
+    ssh_index *ix = new ssh_index();
+    ix->L = L; ix->N = N; ix->id_base = id_base; ix->device = ctx->device;
+    // scratch: keys A/B, rows A/B, hist
+    size_t kbytes = sizeof(uint64_t) * (size_t)L * N;
+    size_t rbytes = sizeof(uint32_t) * (size_t)L * N;
+    size_t hbytes = sizeof(uint32_t) * (size_t)L * RS_BINS * ntiles;
+    size_t total = 2 * kbytes + rbytes + hbytes + 256;  // kA, kB, rB, hist
+    unsigned char *scr = nullptr;
+    int rc = SSH_OK;
+    cudaError_t e;
+    uint64_t *kA, *kB;
+    uint32_t *rA, *rB, *hist;
+    e = cudaMallocAsync((void **)&scr, total, st);
+    if (e != cudaSuccess) { delete ix; return ssh_cuda_fail(e, "cudaMallocAsync(index scratch)", __FILE__, __LINE__); }
+    e = cudaMallocAsync((void **)&ix->ids, rbytes, st);
+    if (e != cudaSuccess) { cudaFreeAsync(scr, st); delete ix; return ssh_cuda_fail(e, "cudaMallocAsync(ids)", __FILE__, __LINE__); }
+    kA = (uint64_t *)scr;
+    kB = (uint64_t *)(scr + kbytes);
+    rB = (uint32_t *)(scr + 2 * kbytes);
+    hist = (uint32_t *)(scr + 2 * kbytes + rbytes);
+    rA = ix->ids;  // 8 passes (even): the sorted rows land back in rA = ix->ids
+    {
+        dim3 g((unsigned)ssh_div_up(N, 32), (unsigned)ssh_div_up(L, 32));
+        rs_transpose<<<g, 256, 0, st>>>(sig, N, L, kA, rA);
+    }
+    uint64_t *kin = kA, *kout = kB;
+    uint32_t *rin = rA, *rout = rB;
+    dim3 grid((unsigned)ntiles, (unsigned)L);
+    for (int pass = 0; pass < 8; pass++) {
+        int shift = 8 * pass;
+        rs_hist<<<grid, RS_THREADS, 0, st>>>(kin, N, shift, ntiles, hist);
+        rs_scan<<<L, 1024, 0, st>>>(hist, ntiles);
+        rs_scatter<<<grid, RS_THREADS, 0, st>>>(kin, rin, N, shift, ntiles, hist, kout, rout);
+        uint64_t *tk = kin; kin = kout; kout = tk;
+        uint32_t *tr = rin; rin = rout; rout = tr;
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "radix sort", __FILE__, __LINE__); goto fail; }
+    // after 8 passes: sorted keys in kin (= kA), rows in rin (= rA = ix->ids)
+    // run-length encode -> CSR
+    e = cudaMallocAsync((void **)&ix->d_nb, sizeof(int64_t) * 2 * L, st);
+    if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "cudaMallocAsync(nb)", __FILE__, __LINE__); goto fail; }
+    ix->d_kbase = ix->d_nb + L;
+    rle_count<<<grid, RS_THREADS, 0, st>>>(kin, N, ntiles, hist);
+    rle_scan<<<L, 32, 0, st>>>(hist, ntiles, ix->d_nb);
+    ix->h_nb = new int64_t[2 * L];
+    ix->h_kbase = ix->h_nb + L;
+    e = cudaMemcpyAsync(ix->h_nb, ix->d_nb, sizeof(int64_t) * L, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "bucket count readback", __FILE__, __LINE__); goto fail; }
+    {
+        int64_t tot = 0;
+        for (int j = 0; j < L; j++) { ix->h_kbase[j] = tot; tot += ix->h_nb[j]; }
+        ix->total_buckets = tot;
+        e = cudaMemcpyAsync(ix->d_kbase, ix->h_kbase, sizeof(int64_t) * L, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMallocAsync((void **)&ix->keys, sizeof(uint64_t) * tot, st);
+        if (e == cudaSuccess) e = cudaMallocAsync((void **)&ix->offsets, sizeof(uint32_t) * (tot + L), st);
+        if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "CSR allocation", __FILE__, __LINE__); goto fail; }
+        rle_emit<<<grid, RS_THREADS, 0, st>>>(kin, N, ntiles, hist, ix->d_kbase, ix->d_nb,
+                                              ix->keys, ix->offsets);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "rle_emit", __FILE__, __LINE__); goto fail; }
+    }
+    cudaFreeAsync(scr, st);
+    *out = ix;
+    return SSH_OK;
+fail:
+    cudaFreeAsync(scr, st);
+    cudaStreamSynchronize(st);
+    ssh_index_destroy(ix);
+    return rc;
+}
+
+extern "C" int ssh_index_destroy(ssh_index *ix) {
+    if (!ix) return SSH_OK;
+    cudaSetDevice(ix->device);
+    cudaDeviceSynchronize();
+    cudaFree(ix->keys);
+    cudaFree(ix->offsets);
+    cudaFree(ix->ids);
+    cudaFree(ix->d_nb);
+    delete[] ix->h_nb;
+    delete ix;
+    return SSH_OK;
+}
+
+extern "C" int ssh_index_num_buckets(const ssh_index *ix, int table, int64_t *nb) {
+    SSH_REQUIRE(ix && nb, SSH_ERR_INVALID, "ssh_index_num_buckets: NULL argument");
+    SSH_REQUIRE(table >= 0 && table < ix->L, SSH_ERR_INVALID, "table %d out of range", table);
+    *nb = ix->h_nb[table];
+    return SSH_OK;
+}
+
+extern "C" int64_t ssh_index_size(const ssh_index *ix) { return ix ? ix->N : -1; }
+
+extern "C" int ssh_index_export(const ssh_index *ix, int table, uint64_t *keys, int64_t *offsets,
+                                int64_t *ids, void *stream) {
+    SSH_REQUIRE(ix && keys && offsets && ids, SSH_ERR_INVALID, "ssh_index_export: NULL argument");
+    SSH_REQUIRE(table >= 0 && table < ix->L, SSH_ERR_INVALID, "table %d out of range", table);
+    SSH_CUDA(cudaSetDevice(ix->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t nb = ix->h_nb[table], kb = ix->h_kbase[table], N = ix->N;
+    uint32_t *of = new uint32_t[nb + 1];
+    uint32_t *rw = new uint32_t[N];
+    cudaError_t e = cudaMemcpyAsync(keys, ix->keys + kb, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(of, ix->offsets + kb + table, sizeof(uint32_t) * (nb + 1), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(rw, ix->ids + (int64_t)table * N, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) {
+        for (int64_t b = 0; b <= nb; b++) offsets[b] = of[b];
+        for (int64_t i = 0; i < N; i++) ids[i] = (int64_t)rw[i] + ix->id_base;
+    }
+    delete[] of;
+    delete[] rw;
+    if (e != cudaSuccess) return ssh_cuda_fail(e, "ssh_index_export", __FILE__, __LINE__);
+    return SSH_OK;
+}

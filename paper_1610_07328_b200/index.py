@@ -1,0 +1,510 @@
+"""Drop-in device implementation of the reference index API (index.py:32-273).
+
+Same names, dataclasses, validation messages and error types as the
+reference `sshts.index`; `SshParams` gains `K` (the CWS concatenation order
+of wmh.signature(concat=K), wmh.py:107-125; default 1 = reference
+build_index behaviour).  Every stage runs in libsshgpu.so on an sm_100 GPU:
+
+  build_index       -> ssh_signatures (K1-K3) + ssh_index_build (K4)
+  query_signature   -> ssh_signatures on the query
+  probe_candidates  -> ssh_probe (K6)
+  query_index(_batch) -> ssh_query_batch (K5-K10)
+
+PyTorch is used only for device memory and the current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from . import cws
+from .core import ConfigError, Dataset, SshError, TimeSeries, _is_torch
+
+MAX_SHINGLE_BITS = 64
+DEVICE_MAX_SHINGLE_BITS = 20
+
+
+def num_sketch_bits(m: int, W: int, delta: int) -> int:
+    """floor((m - W) / delta) + 1 (sketch.py:46-48)."""
+    return (m - W) // delta + 1
+
+
+@dataclass(frozen=True)
+class WarpingParams:
+    """Sakoe-Chiba constraint |i - j| <= radius, radius = round(band * m) (dtw.py:28-39)."""
+
+    band: float = 0.05
+
+    def __post_init__(self):
+        if not 0.0 <= self.band <= 1.0:
+            raise ValueError(f"warping band must be in [0, 1], got {self.band}")
+
+    def radius(self, m: int) -> int:
+        return int(round(self.band * m))
+
+
+@dataclass(frozen=True)
+class SearchStats:
+    """Cascade counters (dtw.py:50-72)."""
+
+    candidates: int
+    kim_pruned: int
+    keogh_pruned: int
+    keogh2_pruned: int
+    dtw_computed: int
+    dtw_abandoned: int
+
+    @property
+    def pruned(self) -> int:
+        return self.kim_pruned + self.keogh_pruned + self.keogh2_pruned
+
+    @property
+    def pruned_fraction(self) -> float:
+        return 0.0 if self.candidates == 0 else self.pruned / self.candidates
+
+    def fraction(self, bound: str) -> float:
+        return 0.0 if self.candidates == 0 else getattr(self, f"{bound}_pruned") / self.candidates
+
+
+@dataclass(frozen=True)
+class RandomFilter:
+    weights: np.ndarray  # (W,) float64
+    seed: int
+
+    @property
+    def W(self) -> int:
+        return self.weights.shape[0]
+
+
+@dataclass(frozen=True)
+class SshParams:
+    """W, delta, n, d (= L tables), seed, band (index.py:32-71) + K."""
+
+    W: int = 30
+    delta: int = 5
+    n: int = 15
+    d: int = 20
+    seed: int = 0
+    band: float = 0.05
+    K: int = 1
+
+    def __post_init__(self):
+        if self.W < 1:
+            raise ConfigError(f"filter length W must be >= 1, got {self.W}")
+        if self.delta < 1:
+            raise ConfigError(f"step size delta must be >= 1, got {self.delta}")
+        if not 1 <= self.n <= MAX_SHINGLE_BITS:
+            raise ConfigError(f"shingle length n must be in [1, {MAX_SHINGLE_BITS}], got {self.n}")
+        if self.d < 1:
+            raise ConfigError(f"table count d must be >= 1, got {self.d}")
+        if self.seed < 0:
+            raise ConfigError(f"seed must be non-negative, got {self.seed}")
+        if not 0.0 <= self.band <= 1.0:
+            raise ConfigError(f"warping band must be in [0, 1], got {self.band}")
+        if self.K < 1:
+            raise ConfigError(f"concat order K must be >= 1, got {self.K}")
+
+    def validate_for_length(self, t: int) -> None:
+        if t < self.W:
+            raise ConfigError(f"series length t={t} violates t >= W (W={self.W})")
+        nb = num_sketch_bits(t, self.W, self.delta)
+        if nb < self.n:
+            raise ConfigError(
+                f"sketch length floor((t-W)/delta)+1 = {nb} violates >= n "
+                f"(t={t}, W={self.W}, delta={self.delta}, n={self.n})"
+            )
+        if self.n > DEVICE_MAX_SHINGLE_BITS:
+            raise ConfigError(
+                f"shingle length n={self.n} exceeds the device limit {DEVICE_MAX_SHINGLE_BITS} "
+                "(CWS variates are tabulated over the 2^n token universe)")
+
+    def warping(self) -> WarpingParams:
+        return WarpingParams(band=self.band)
+
+    @property
+    def L(self) -> int:
+        return self.d
+
+
+@dataclass(frozen=True)
+class QueryStats:
+    n_indexed: int
+    candidates: int
+    cascade: SearchStats
+
+    @property
+    def hash_pruned_fraction(self) -> float:
+        return 1.0 - self.candidates / self.n_indexed
+
+    @property
+    def bound_pruned_fraction(self) -> float:
+        return self.cascade.pruned / self.n_indexed
+
+    @property
+    def total_pruned_fraction(self) -> float:
+        return 1.0 - self.cascade.dtw_computed / self.n_indexed
+
+
+@dataclass(frozen=True)
+class QueryResult:
+    ids: list
+    distances: list
+    stats: QueryStats
+    timings: dict
+    status: str = "ok"  # "ok" | "no-candidates" | "fallback"
+    warning: str | None = None
+
+
+# ------------------------------------------------------------ device context
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _device_index(device) -> int:
+    torch = _torch()
+    if device is None:
+        if not torch.cuda.is_available():
+            raise SshError("no CUDA device available: the SSH device path needs an sm_100 GPU "
+                           "(there is no CPU fallback)")
+        return torch.cuda.current_device()
+    return torch.device(device).index if not isinstance(device, int) else device
+
+
+class DeviceContext:
+    """One ssh_ctx per (device, parameters, series length)."""
+
+    def __init__(self, device: int, params: SshParams, m: int):
+        self.device = device
+        self.params = params
+        self.m = m
+        L = nat.lib()
+        h = ctypes.c_void_p()
+        nat.check(L.ssh_ctx_create(device, ctypes.byref(h)), "ssh_ctx_create")
+        self.handle = h
+        w = cws.make_filter(params.W, params.seed)
+        self.filter = RandomFilter(weights=w, seed=params.seed)
+        S = params.K * params.d
+        r, lnc, beta = cws.tables(params.n, S, params.seed)
+        nb = num_sketch_bits(m, params.W, params.delta)
+        max_count = nb - params.n + 1
+        lnw = cws.ln_counts(max_count)
+        p = nat.ssh_params(m=m, W=params.W, delta=params.delta, n=params.n, L=params.d, K=params.K,
+                           seed=params.seed, radius=params.warping().radius(m), reserved=0)
+        self.cparams = p
+        nat.check(L.ssh_ctx_set_params(h, ctypes.byref(p), nat.ptr(np.ascontiguousarray(w)),
+                                       nat.ptr(r), nat.ptr(lnc), nat.ptr(beta), nat.ptr(lnw),
+                                       max_count), "ssh_ctx_set_params")
+        self.nb = L.ssh_num_sketch_bits(h)
+        self.words = L.ssh_sketch_words(h)
+        self.T = L.ssh_tokens_per_series(h)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                nat.lib().ssh_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_ctx_cache: dict = {}
+_ctx_lock = threading.Lock()
+
+
+def get_context(device: int, params: SshParams, m: int) -> DeviceContext:
+    key = (device, params, m)
+    with _ctx_lock:
+        c = _ctx_cache.get(key)
+        if c is None:
+            if len(_ctx_cache) >= 4:
+                _ctx_cache.pop(next(iter(_ctx_cache)))
+            c = DeviceContext(device, params, m)
+            _ctx_cache[key] = c
+        return c
+
+
+def _stream_ptr(device: int):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _as_device_f32(values, device: int):
+    torch = _torch()
+    if _is_torch(values):
+        t = values.to(device=f"cuda:{device}", dtype=torch.float32)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(f"cuda:{device}")
+    return t.contiguous()
+
+
+# ------------------------------------------------------------------ index
+
+class _TablesHandle:
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            if self.handle:
+                nat.lib().ssh_index_destroy(self.handle)
+        except Exception:
+            pass
+
+
+@dataclass(eq=False)
+class SshIndex:
+    """params, filter, tables, dataset, signatures, normalized (index.py:103-110)
+    plus the device state: X (f32 series), signature tensor, CSR tables."""
+
+    params: SshParams
+    filter: RandomFilter
+    dataset: Dataset
+    normalized: bool
+    device: int
+    X: object  # torch float32 (N, m) on device
+    sig_dev: object  # torch int64 (N, L) on device (uint64 bit patterns)
+    id_base: int = 0
+    _tables: object = None
+    _tables_host: list | None = field(default=None, repr=False)
+    _sig_host: np.ndarray | None = field(default=None, repr=False)
+
+    @property
+    def n_series(self) -> int:
+        return int(self.X.shape[0])
+
+    @property
+    def length(self) -> int:
+        return int(self.X.shape[1])
+
+    @property
+    def signatures(self) -> np.ndarray:
+        """(N, d) uint64 (index.py:109), copied from the device on first use."""
+        if self._sig_host is None:
+            self._sig_host = self.sig_dev.cpu().numpy().view(np.uint64)
+        return self._sig_host
+
+    def table_csr(self, j: int):
+        """Table j as host CSR: (keys uint64[nb], offsets int64[nb+1], ids int64[N])."""
+        L = nat.lib()
+        nb = ctypes.c_int64()
+        nat.check(L.ssh_index_num_buckets(self._tables.handle, j, ctypes.byref(nb)))
+        keys = np.empty(nb.value, dtype=np.uint64)
+        offsets = np.empty(nb.value + 1, dtype=np.int64)
+        ids = np.empty(self.n_series, dtype=np.int64)
+        nat.check(L.ssh_index_export(self._tables.handle, j, nat.ptr(keys), nat.ptr(offsets),
+                                     nat.ptr(ids), _stream_ptr(self.device)), "ssh_index_export")
+        return keys, offsets, ids
+
+    @property
+    def tables(self) -> list:
+        """The reference's list[dict[key, ids ascending]] (index.py:141-156), materialised lazily."""
+        if self._tables_host is None:
+            out = []
+            for j in range(self.params.d):
+                keys, offsets, ids = self.table_csr(j)
+                out.append({int(k): ids[offsets[b]:offsets[b + 1]] for b, k in enumerate(keys)})
+            self._tables_host = out
+        return self._tables_host
+
+    def context(self) -> DeviceContext:
+        return get_context(self.device, self.params, self.length)
+
+
+def _check_params_length(params: SshParams, m: int):
+    params.validate_for_length(m)
+
+
+def compute_signatures_device(ctx: DeviceContext, X, stats=None):
+    """(N, L) int64 device tensor of signatures (K1-K3 fused)."""
+    torch = _torch()
+    N = int(X.shape[0])
+    sig = torch.empty((N, ctx.params.d), dtype=torch.int64, device=X.device)
+    if N:
+        nat.check(nat.lib().ssh_signatures(ctx.handle, nat.ptr(X), N, int(X.stride(0)), nat.ptr(sig),
+                                           nat.ptr(stats), _stream_ptr(ctx.device)), "ssh_signatures")
+    return sig
+
+
+def build_index(dataset, params: SshParams, normalized: bool = True, threads: int = 1,
+                device=None, id_base: int = 0) -> SshIndex:
+    """Hash every series into d tables (index.py:159-172).  `threads` is
+    accepted for API compatibility; the device path is always parallel."""
+    if not isinstance(dataset, Dataset):
+        dataset = Dataset(values=dataset)
+    params.validate_for_length(dataset.length)
+    dev = _device_index(device)
+    ctx = get_context(dev, params, dataset.length)
+    X = _as_device_f32(dataset.values, dev)
+    sig = compute_signatures_device(ctx, X)
+    handle = ctypes.c_void_p()
+    nat.check(nat.lib().ssh_index_build(ctx.handle, nat.ptr(sig), int(X.shape[0]), int(id_base),
+                                        ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_build")
+    return SshIndex(params=params, filter=ctx.filter, dataset=dataset, normalized=normalized,
+                    device=dev, X=X, sig_dev=sig, id_base=id_base, _tables=_TablesHandle(handle))
+
+
+def compute_signatures(values, params: SshParams, weights=None, threads: int = 1, device=None):
+    """(N, d) uint64 signature matrix (index.py:123-138, with the K fold)."""
+    ds = values if isinstance(values, Dataset) else Dataset(values=values)
+    params.validate_for_length(ds.length)
+    dev = _device_index(device)
+    ctx = get_context(dev, params, ds.length)
+    if weights is not None and not np.array_equal(np.asarray(weights, dtype=np.float64),
+                                                  ctx.filter.weights):
+        raise ConfigError("custom filter weights are not supported on device; "
+                          "the filter is make_filter(W, seed)")
+    X = _as_device_f32(ds.values, dev)
+    return compute_signatures_device(ctx, X).cpu().numpy().view(np.uint64)
+
+
+def _query_values(q) -> np.ndarray:
+    if isinstance(q, TimeSeries):
+        return q.values
+    if _is_torch(q):
+        return q.detach().double().cpu().numpy()
+    return np.asarray(q, dtype=np.float64)
+
+
+def query_signature(index: SshIndex, q) -> np.ndarray:
+    """(d,) uint64 signature of one query (index.py:175-181)."""
+    qv = _query_values(q)
+    torch = _torch()
+    Q = _as_device_f32(qv.reshape(1, -1), index.device)
+    sig = compute_signatures_device(index.context(), Q)
+    return sig.cpu().numpy().view(np.uint64)[0]
+
+
+def probe_candidates(index: SshIndex, qsig) -> np.ndarray:
+    """Deduplicated union of the d probed buckets, ascending ids (index.py:184-190)."""
+    torch = _torch()
+    qs = torch.from_numpy(np.ascontiguousarray(np.asarray(qsig, dtype=np.uint64).view(np.int64))
+                          .reshape(1, -1)).to(f"cuda:{index.device}")
+    N = index.n_series
+    NW = (N + 31) // 32
+    bm = torch.empty((1, NW), dtype=torch.int32, device=qs.device)
+    nc = torch.empty(1, dtype=torch.int64, device=qs.device)
+    nat.check(nat.lib().ssh_probe(index.context().handle, index._tables.handle, nat.ptr(qs), 1,
+                                  nat.ptr(bm), nat.ptr(nc), _stream_ptr(index.device)), "ssh_probe")
+    words = bm.cpu().numpy().view(np.uint32)[0]
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:N]
+    return np.nonzero(bits)[0].astype(np.int64) + index.id_base
+
+
+@dataclass
+class BatchResult:
+    """Raw device-batch output (host numpy)."""
+
+    ids: np.ndarray       # (nq, k) int64, -1 padded
+    d2: np.ndarray        # (nq, k) float64 squared DTW
+    n_out: np.ndarray     # (nq,) int32
+    n_cand: np.ndarray    # (nq,) int64
+    counters: np.ndarray  # (nq, 5) int64
+    seconds: float
+
+
+def query_batch_device(index: SshIndex, Q, k: int, fallback_on_empty: bool = False):
+    """Run ssh_query_batch on a device tensor Q (nq, m) f32; returns device tensors."""
+    torch = _torch()
+    nq = int(Q.shape[0])
+    dev = Q.device
+    ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    d2 = torch.empty((nq, k), dtype=torch.float64, device=dev)
+    n_out = torch.empty(nq, dtype=torch.int32, device=dev)
+    n_cand = torch.empty(nq, dtype=torch.int64, device=dev)
+    counters = torch.empty((nq, 5), dtype=torch.int64, device=dev)
+    status = torch.empty(nq, dtype=torch.int32, device=dev)
+    flags = nat.SSH_QUERY_FALLBACK_ON_EMPTY if fallback_on_empty else 0
+    nat.check(nat.lib().ssh_query_batch(
+        index.context().handle, index._tables.handle, nat.ptr(index.X), nat.ptr(Q), nq, k, flags,
+        nat.ptr(ids), nat.ptr(d2), nat.ptr(n_out), nat.ptr(n_cand), nat.ptr(counters),
+        nat.ptr(status), _stream_ptr(index.device)), "ssh_query_batch")
+    return ids, d2, n_out, n_cand, counters, status
+
+
+def _validate_k(index: SshIndex, k: int):
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    n = index.n_series
+    warning = None
+    if k > n:
+        warning = f"k={k} exceeds index size {n}; returning at most {n} series"
+        k = n
+    return k, warning
+
+
+def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = False) -> list:
+    """query_index for every row of Q (nq, m) in one device batch."""
+    if _is_torch(Q):
+        Qd = Q.to(device=f"cuda:{index.device}", dtype=_torch().float32).contiguous()
+        if Qd.ndim == 1:
+            Qd = Qd.reshape(1, -1)
+    else:
+        Qh = np.asarray(Q, dtype=np.float64)
+        if Qh.ndim == 1:
+            Qh = Qh.reshape(1, -1)
+        if not np.all(np.isfinite(Qh)):
+            raise ValueError("series values contains non-finite values")
+        Qd = _as_device_f32(Qh, index.device)
+    if Qd.shape[1] != index.length:
+        raise ValueError(f"query length {Qd.shape[1]} does not match indexed length {index.length}")
+    k, warning = _validate_k(index, k)
+    t0 = time.perf_counter()
+    ids, d2, n_out, n_cand, counters, status = query_batch_device(index, Qd, k, fallback_on_empty)
+    status = status.cpu().numpy()
+    ids = ids.cpu().numpy()
+    d2 = d2.cpu().numpy()
+    n_out = n_out.cpu().numpy()
+    n_cand = n_cand.cpu().numpy()
+    counters = counters.cpu().numpy()
+    dt = time.perf_counter() - t0
+    nq = Qd.shape[0]
+    N = index.n_series
+    out = []
+    for i in range(nq):
+        n = int(n_out[i])
+        c = counters[i]
+        cascade = SearchStats(candidates=int(n_cand[i]), kim_pruned=int(c[0]), keogh_pruned=int(c[1]),
+                              keogh2_pruned=int(c[2]), dtw_computed=int(c[3]), dtw_abandoned=int(c[4]))
+        timings = {"batch": dt, "per_query": dt / max(1, nq)}
+        if status[i] == 1:
+            stats = QueryStats(n_indexed=N, candidates=0, cascade=SearchStats(0, 0, 0, 0, 0, 0))
+            out.append(QueryResult([], [], stats, timings, status="no-candidates", warning=warning))
+            continue
+        stats = QueryStats(n_indexed=N, candidates=int(n_cand[i]), cascade=cascade)
+        out.append(QueryResult(ids=[int(v) for v in ids[i, :n]],
+                               distances=[float(v) for v in np.sqrt(d2[i, :n])],
+                               stats=stats, timings=timings,
+                               status="fallback" if status[i] == 2 else "ok", warning=warning))
+    return out
+
+
+def query_index(index: SshIndex, q, k: int, fallback_on_empty: bool = False) -> QueryResult:
+    """Probe the d tables, then rerank the candidate union exactly by DTW (index.py:204-273)."""
+    qv = _query_values(q)
+    if qv.shape[0] != index.length:
+        raise ValueError(f"query length {qv.shape[0]} does not match indexed length {index.length}")
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    return query_index_batch(index, qv.reshape(1, -1), k, fallback_on_empty)[0]
+
+
+def dtw_exact_pairs(index: SshIndex, Q, qrow, xrow) -> np.ndarray:
+    """Exact f64 DTW^2 of (Q[qrow[e]], X[xrow[e]]) pairs via ssh_dtw_exact."""
+    torch = _torch()
+    Qd = _as_device_f32(Q, index.device) if not _is_torch(Q) else Q
+    qr = torch.as_tensor(np.asarray(qrow, dtype=np.int32)).to(Qd.device)
+    xr = torch.as_tensor(np.asarray(xrow, dtype=np.int64)).to(Qd.device)
+    out = torch.empty(qr.shape[0], dtype=torch.float64, device=Qd.device)
+    nat.check(nat.lib().ssh_dtw_exact(index.context().handle, nat.ptr(index.X), nat.ptr(Qd),
+                                      nat.ptr(qr), nat.ptr(xr), int(qr.shape[0]), nat.ptr(out),
+                                      _stream_ptr(index.device)), "ssh_dtw_exact")
+    return out.cpu().numpy()
