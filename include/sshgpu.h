@@ -54,6 +54,8 @@ typedef struct ssh_index ssh_index; /* per shard: L CSR bucket tables          *
 
 const char *ssh_last_error(void);
 int ssh_abi_version(void);
+/* Kernels launched by this library so far (process-wide, monotonic). */
+int64_t ssh_launch_count(void);
 
 /* Context for `device`; owns the uploaded filter and CWS tables. */
 int ssh_ctx_create(int device, ssh_ctx **out);
@@ -70,6 +72,14 @@ int ssh_ctx_destroy(ssh_ctx *ctx);
 int ssh_ctx_set_params(ssh_ctx *ctx, const ssh_params *p, const double *filter,
                        const double *tab_r, const double *tab_lnc, const double *tab_beta,
                        const double *ln_w, int32_t max_count);
+
+/* Optional per-phase device timing of ssh_query_batch (CUDA events; adds no
+ * host syncs beyond the batch's own).  ssh_ctx_profile fills up to n values:
+ * [0] hash ms, [1] probe ms, [2] seed ms, [3] LB filter ms, [4] fp32 DTW ms,
+ * [5] rescore+top-k ms, [6] DTW cells evaluated, [7] DTW launches' lanes,
+ * [8] survivors, [9] rescored pairs — accumulated since profiling was enabled. */
+int ssh_ctx_set_profiling(ssh_ctx *ctx, int on);
+int ssh_ctx_profile(const ssh_ctx *ctx, double *out, int n);
 
 /* Sizes derived from the parameters. */
 int ssh_num_sketch_bits(const ssh_ctx *ctx);   /* N_B  (sketch.py:46-48)      */
@@ -112,6 +122,13 @@ int64_t ssh_index_size(const ssh_index *idx);
  * ids i64[N] (global ids).  The reference's dict view (index.py:151-154). */
 int ssh_index_export(const ssh_index *idx, int table, uint64_t *keys, int64_t *offsets,
                      int64_t *ids, void *stream);
+
+/* Rerank summaries of the shard (device): PAA segment means of every row
+ * (32-sample segments, f64 sums stored f32) and max|x|.  They feed the
+ * LB_PAA bound of ssh_query_batch; build_index computes them right after
+ * the tables (ssh_query_batch computes them lazily if absent).  X is the
+ * shard the index was built over, f32[N][ld] device. */
+int ssh_index_summarize(ssh_ctx *ctx, ssh_index *idx, const float *X, int64_t ld, void *stream);
 
 /* K6 — probe_candidates (index.py:184-190) for a batch: membership bitmap
  * u32[nq][ceil(N/32)] of the deduplicated bucket union (bit = local row),

@@ -88,6 +88,9 @@ def lib():
         sigs = {
             "ssh_last_error": ([], ctypes.c_char_p),
             "ssh_abi_version": ([], ctypes.c_int),
+            "ssh_launch_count": ([], i64),
+            "ssh_ctx_set_profiling": ([P, ctypes.c_int], ctypes.c_int),
+            "ssh_ctx_profile": ([P, P, ctypes.c_int], ctypes.c_int),
             "ssh_ctx_create": ([ctypes.c_int, PP], ctypes.c_int),
             "ssh_ctx_destroy": ([P], ctypes.c_int),
             "ssh_ctx_set_params": ([P, ctypes.POINTER(ssh_params), P, P, P, P, P, i32], ctypes.c_int),
@@ -104,6 +107,7 @@ def lib():
             "ssh_index_size": ([P], i64),
             "ssh_index_export": ([P, ctypes.c_int, P, P, P, P], ctypes.c_int),
             "ssh_probe": ([P, P, P, i32, P, P, P], ctypes.c_int),
+            "ssh_index_summarize": ([P, P, P, i64, P], ctypes.c_int),
             "ssh_query_batch": ([P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P], ctypes.c_int),
             "ssh_dtw_exact": ([P, P, P, P, P, i64, P, P], ctypes.c_int),
         }
@@ -116,10 +120,11 @@ def lib():
 
 
 EXPORTED = [
-    "ssh_last_error", "ssh_abi_version", "ssh_ctx_create", "ssh_ctx_destroy", "ssh_ctx_set_params",
+    "ssh_last_error", "ssh_abi_version", "ssh_launch_count", "ssh_ctx_set_profiling",
+    "ssh_ctx_profile", "ssh_ctx_create", "ssh_ctx_destroy", "ssh_ctx_set_params",
     "ssh_num_sketch_bits", "ssh_sketch_words", "ssh_tokens_per_series", "ssh_sketch", "ssh_shingle",
     "ssh_cws", "ssh_signatures", "ssh_index_build", "ssh_index_destroy", "ssh_index_num_buckets",
-    "ssh_index_size", "ssh_index_export", "ssh_probe", "ssh_query_batch", "ssh_dtw_exact",
+    "ssh_index_size", "ssh_index_export", "ssh_index_summarize", "ssh_probe", "ssh_query_batch", "ssh_dtw_exact",
 ]
 
 

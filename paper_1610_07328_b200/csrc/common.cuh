@@ -22,7 +22,12 @@ int ssh_cuda_fail(cudaError_t e, const char *what, const char *file, int line);
         if (_e != cudaSuccess) return ssh_cuda_fail(_e, #call, __FILE__, __LINE__); \
     } while (0)
 
-#define SSH_CHECK_LAUNCH() SSH_CUDA(cudaGetLastError())
+void ssh_count_launch();
+#define SSH_CHECK_LAUNCH()          \
+    do {                            \
+        ssh_count_launch();         \
+        SSH_CUDA(cudaGetLastError()); \
+    } while (0)
 
 #define SSH_REQUIRE(cond, code, ...)       \
     do {                                   \
@@ -50,13 +55,40 @@ struct ssh_ctx {
     double *d_r = nullptr, *d_lnc = nullptr, *d_beta = nullptr, *d_lna1 = nullptr;
     double *d_lnw = nullptr;  // ln(count)
     size_t tab_entries = 0;
-    // scratch reused across calls (grown on demand)
-    void *scratch = nullptr;
-    size_t scratch_bytes = 0;
+    // profiling (ssh_ctx_set_profiling)
+    int profile = 0;
+    double prof[16] = {0};
+    unsigned long long *d_cells = nullptr;  // device counter: DTW cells evaluated
+    // named grow-only scratch slots reused across calls (stream-ordered)
+    void *slot_ptr[32] = {nullptr};
+    size_t slot_bytes[32] = {0};
+};
+
+enum {
+    SLOT_BITS = 0,       // ssh_signatures: packed sketch bits
+    SLOT_RS_KEYS_A,      // ssh_index_build radix sort
+    SLOT_RS_KEYS_B,
+    SLOT_RS_ROWS_B,
+    SLOT_RS_HIST,
+    SLOT_Q_FIXED,        // ssh_query_batch: per-query fixed-size arrays
+    SLOT_Q_BITMAP,
+    SLOT_Q_SURV,
+    SLOT_Q_SURV_LB,
+    SLOT_Q_W2,
+    SLOT_Q_D2,
+    SLOT_Q_RESC,
+    SLOT_Q_D64,
+    SLOT_Q_HIST,
+    SLOT_COUNT
 };
 
 struct ssh_index {
     int L = 0;
+    // rerank summaries (ssh_index_summarize): PAA segment means of every row
+    float *paa = nullptr;  // [N][nseg]
+    int nseg = 0;
+    float paa_delta = 0.f;  // bound on |stored mean - exact mean|
+    unsigned *d_maxabs = nullptr;
     int64_t N = 0;
     int64_t id_base = 0;
     int device = 0;
@@ -70,8 +102,10 @@ struct ssh_index {
     int64_t total_buckets = 0;
 };
 
-// grow ctx scratch; returns pointer or nullptr (error set)
-void *ssh_scratch(ssh_ctx *ctx, size_t bytes, cudaStream_t st);
+// grow-only named scratch slot; returns pointer or nullptr (error set)
+void *ssh_slot(ssh_ctx *ctx, int slot, size_t bytes, cudaStream_t st);
+
+#define SSH_PAA_SEG 32  // samples per PAA segment (rerank lower bound)
 
 // ----------------------------------------------------------- device math
 __host__ __device__ __forceinline__ uint64_t ssh_mix64(uint64_t x) {

@@ -6,7 +6,34 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
 static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void ssh_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" int64_t ssh_launch_count(void) { return g_launches.load(); }
+
+extern "C" int ssh_ctx_set_profiling(ssh_ctx *ctx, int on) {
+    SSH_REQUIRE(ctx != nullptr, SSH_ERR_INVALID, "ssh_ctx_set_profiling: ctx is NULL");
+    SSH_CUDA(cudaSetDevice(ctx->device));
+    if (on && !ctx->d_cells) SSH_CUDA(cudaMalloc(&ctx->d_cells, sizeof(unsigned long long)));
+    if (ctx->d_cells) SSH_CUDA(cudaMemset(ctx->d_cells, 0, sizeof(unsigned long long)));
+    for (int i = 0; i < 16; i++) ctx->prof[i] = 0.0;
+    ctx->profile = on;
+    return SSH_OK;
+}
+
+extern "C" int ssh_ctx_profile(const ssh_ctx *ctx, double *out, int n) {
+    SSH_REQUIRE(ctx && out, SSH_ERR_INVALID, "ssh_ctx_profile: NULL argument");
+    for (int i = 0; i < n && i < 16; i++) out[i] = ctx->prof[i];
+    if (n > 6 && ctx->d_cells) {
+        unsigned long long c = 0;
+        SSH_CUDA(cudaMemcpy(&c, ctx->d_cells, sizeof(c), cudaMemcpyDeviceToHost));
+        out[6] = (double)c;
+    }
+    return SSH_OK;
+}
 
 void ssh_set_error(const char *fmt, ...) {
     va_list ap;
@@ -24,23 +51,20 @@ int ssh_cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
 extern "C" const char *ssh_last_error(void) { return g_err; }
 extern "C" int ssh_abi_version(void) { return SSHGPU_ABI_VERSION; }
 
-void *ssh_scratch(ssh_ctx *ctx, size_t bytes, cudaStream_t st) {
-    if (bytes <= ctx->scratch_bytes) return ctx->scratch;
-    if (ctx->scratch) {
-        cudaStreamSynchronize(st);
-        cudaFree(ctx->scratch);
-        ctx->scratch = nullptr;
-        ctx->scratch_bytes = 0;
-    }
-    size_t want = bytes + bytes / 4;
-    cudaError_t e = cudaMalloc(&ctx->scratch, want);
+void *ssh_slot(ssh_ctx *ctx, int slot, size_t bytes, cudaStream_t st) {
+    if (bytes <= ctx->slot_bytes[slot]) return ctx->slot_ptr[slot];
+    if (ctx->slot_ptr[slot]) cudaFreeAsync(ctx->slot_ptr[slot], st);
+    ctx->slot_ptr[slot] = nullptr;
+    ctx->slot_bytes[slot] = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    cudaError_t e = cudaMallocAsync(&ctx->slot_ptr[slot], want, st);
     if (e != cudaSuccess) {
-        ssh_cuda_fail(e, "cudaMalloc(scratch)", __FILE__, __LINE__);
-        ctx->scratch = nullptr;
+        ssh_cuda_fail(e, "cudaMallocAsync(scratch slot)", __FILE__, __LINE__);
+        ctx->slot_ptr[slot] = nullptr;
         return nullptr;
     }
-    ctx->scratch_bytes = want;
-    return ctx->scratch;
+    ctx->slot_bytes[slot] = want;
+    return ctx->slot_ptr[slot];
 }
 
 extern "C" int ssh_ctx_create(int device, ssh_ctx **out) {
@@ -55,6 +79,13 @@ extern "C" int ssh_ctx_create(int device, ssh_ctx **out) {
     SSH_REQUIRE(prop.major == 10, SSH_ERR_UNSUPPORTED,
                 "ssh_ctx_create: device %d is sm_%d%d; libsshgpu is built for sm_100a only",
                 device, prop.major, prop.minor);
+    // keep freed stream-ordered allocations cached in the device pool
+    // (the query batch and the table build allocate scratch per call)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     ssh_ctx *c = new (std::nothrow) ssh_ctx();
     SSH_REQUIRE(c != nullptr, SSH_ERR_OOM, "ssh_ctx_create: host allocation failed");
     c->device = device;
@@ -75,7 +106,10 @@ extern "C" int ssh_ctx_destroy(ssh_ctx *ctx) {
     if (!ctx) return SSH_OK;
     cudaSetDevice(ctx->device);
     free_tables(ctx);
-    if (ctx->scratch) cudaFree(ctx->scratch);
+    cudaDeviceSynchronize();
+    for (int i = 0; i < 32; i++)
+        if (ctx->slot_ptr[i]) cudaFree(ctx->slot_ptr[i]);
+    if (ctx->d_cells) cudaFree(ctx->d_cells);
     delete ctx;
     return SSH_OK;
 }
@@ -195,7 +229,7 @@ extern "C" int ssh_signatures(ssh_ctx *ctx, const float *X, int64_t N, int64_t l
     if (N == 0) return SSH_OK;
     SSH_REQUIRE(X && sig, SSH_ERR_INVALID, "ssh_signatures: NULL pointer");
     cudaStream_t st = (cudaStream_t)stream;
-    uint64_t *bits = (uint64_t *)ssh_scratch(ctx, sizeof(uint64_t) * (size_t)N * ctx->words, st);
+    uint64_t *bits = (uint64_t *)ssh_slot(ctx, SLOT_BITS, sizeof(uint64_t) * (size_t)N * ctx->words, st);
     if (!bits) return SSH_ERR_OOM;
     int rc = ssh_launch_sketch(ctx, X, N, ld, bits, stats, st);
     if (rc) return rc;

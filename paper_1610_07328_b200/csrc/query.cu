@@ -7,19 +7,26 @@
 // A14).  Distances are the reference's f64 values (dtw.py:83-121, FMA-free).
 //
 // Device pipeline per query batch (all queries in flight at once):
-//   probe      binary search of each query key in each table's sorted keys
-//   bitmap     membership bitmap of R (warp-aggregated atomicOr over buckets)
-//   seeds      up to S0 distinct members taken from the smallest probed
-//              buckets first; their fp32 DTW gives tau_q >= true k-th best
-//   lb_filter  LB_Kim then early-abandoning LB_Keogh (fp32) of every member
-//              against thr_q = tau_q (1 + eps); survivors listed per query
-//   dtw32      lane-per-candidate banded DTW (fp32, row-min abandon at thr_q)
-//   select     T_k = k-th smallest fp32 DTW; rescoring set = d32 <= T_k(1+eps)
-//   dtw64      exact f64 DTW (__dsub_rn/__dmul_rn/__dadd_rn, reference order)
-//   topk       sort by (d64, id) -> ids / d2
+//   probe     binary search of each query key in each table's sorted keys
+//   bitmap    membership bitmap of R (warp-aggregated atomicOr over buckets)
+//   seeds     LB_PAA (segment-mean envelope bound, from the L2-resident PAA
+//             summary of the shard) of every member -> per-query histogram
+//             -> the S0 members with the smallest LB_PAA; their fp32 DTW
+//             gives thr0 >= the exact k-th best
+//   filter    per member: LB_PAA, LB_Kim, then early-abandoning LB_Keogh
+//             (query envelope) against thr0; survivors keep their LB_Keogh
+//   waves     wave 1 = the W1 smallest-LB survivors (fp32 DTW) -> thr1;
+//             wave 2 = remaining survivors with LB <= thr1.  The fp32 DTW
+//             abandons on row-min + the remaining rows' LB_Keogh terms
+//             (the UCR-suite cumulative bound)
+//   rescore   T_k = k-th smallest fp32 DTW; every candidate with
+//             d32 <= T_k (1 + eps) is re-evaluated in exact f64
+//             (__dsub_rn/__dmul_rn/__dadd_rn in reference order)
+//   top-k     (d64, id) order -> ids / squared distances
 // eps = (8m + 64) 2^-24 bounds the relative error of every fp32 bound and
-// DTW value against the f64 reference values, so no member of
-// the exact top-k is ever pruned, abandoned or left unrescored.
+// DTW value against the f64 reference values; bounds built on
+// stored segment means subtract an explicit absolute error term.  No member
+// of the exact top-k is ever pruned, abandoned or left unrescored.
 #include <math.h>
 
 #include <algorithm>
@@ -28,14 +35,74 @@
 #include "common.cuh"
 
 #define Q_SURV_CAP0 4096
-#define LB_THREADS 256
-#define LB_WARPS (LB_THREADS / 32)
-#define LB_WORDS 64
+#define Q_SEED_CAND 4096
+#define MB_THREADS 256
+#define MB_WARPS (MB_THREADS / 32)
+#define MB_SLICE_WORDS 256
+#define NBINS 2048
+#define U32_EPS (1.0f / 16777216.0f)
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
     return v;
+}
+
+__device__ __forceinline__ unsigned lb_bin(float v) { return min(__float_as_uint(v) >> 20, (unsigned)(NBINS - 1)); }
+
+__device__ int block_sum(int c, int *red) {
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w];
+    return s;
+}
+
+// count of entries (over up to two arrays) whose bit pattern is <= v
+template <typename U>
+__device__ int block_count_le2(const U *a, int na, const U *b, int nb, U v, int *red) {
+    int c = 0;
+    for (int e = threadIdx.x; e < na; e += blockDim.x) c += a[e] <= v;
+    for (int e = threadIdx.x; e < nb; e += blockDim.x) c += b[e] <= v;
+    return block_sum(c, red);
+}
+
+// smallest v with count(<= v) >= kk over the two arrays (non-negative float/double bits)
+template <typename U>
+__device__ U block_kth2(const U *a, int na, const U *b, int nb, int kk, U hi, int *red) {
+    U lo = 0;
+    while (lo < hi) {
+        U mid = lo + (hi - lo) / 2;
+        if (block_count_le2<U>(a, na, b, nb, mid, red) >= kk) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+template <typename K>
+__device__ void block_sort_pairs(K *key, uint32_t *val, int P2) {
+    for (int k = 2; k <= P2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int idx = threadIdx.x; idx < (P2 >> 1); idx += blockDim.x) {
+                int i = 2 * idx - (idx & (j - 1));
+                int l = i + j;
+                K a = key[i], b = key[l];
+                uint32_t va = val[i], vb = val[l];
+                bool gt = (a > b) || (a == b && va > vb);
+                bool up = (i & k) == 0;
+                if (gt == up) {
+                    key[i] = b; key[l] = a;
+                    val[i] = vb; val[l] = va;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__device__ __forceinline__ float thr_from(float t, float eps) {
+    return isinf(t) ? INFINITY : (float)((double)t * (1.0 + (double)eps));
 }
 
 // ------------------------------------------------------------------ probe
@@ -64,7 +131,7 @@ __global__ void probe_kernel(const uint64_t *__restrict__ qsig, int nq, int L,
     }
 }
 
-// membership bitmap: blockIdx.y = q*L + j
+// membership bitmap: blockIdx.x = q*L + j, blockIdx.y strides the bucket
 __global__ void bitmap_kernel(const uint32_t *__restrict__ ids, const uint64_t *__restrict__ bstart,
                               const uint32_t *__restrict__ blen, int L, int64_t NW,
                               uint32_t *__restrict__ bitmap) {
@@ -123,9 +190,13 @@ __global__ void count_kernel(uint32_t *__restrict__ bitmap, int64_t NW, int64_t 
     }
 }
 
-// query envelope (dtw.py:124-151 semantics: max/min over [i-r, i+r])
-__global__ void envelope_kernel(const float *__restrict__ Q, int m, int r, float *__restrict__ U,
-                                float *__restrict__ Lo) {
+// query envelope (dtw.py:124-151 semantics: max/min over [i-r, i+r]) and its
+// per-segment max/min for the PAA bound
+__global__ void envelope_kernel(const float *__restrict__ Q, int m, int r, int nseg,
+                                float *__restrict__ U, float *__restrict__ Lo,
+                                float *__restrict__ Useg, float *__restrict__ Lseg) {
+    extern __shared__ float esm[];
+    float *su = esm, *sl = esm + m;
     const int q = blockIdx.x;
     const float *y = Q + (int64_t)q * m;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -136,110 +207,361 @@ __global__ void envelope_kernel(const float *__restrict__ Q, int m, int r, float
             mx = fmaxf(mx, v);
             mn = fminf(mn, v);
         }
+        su[i] = mx;
+        sl[i] = mn;
         U[(int64_t)q * m + i] = mx;
         Lo[(int64_t)q * m + i] = mn;
     }
+    __syncthreads();
+    for (int s = threadIdx.x; s < nseg; s += blockDim.x) {
+        int a = s * SSH_PAA_SEG, b = min(m, a + SSH_PAA_SEG);
+        float mx = su[a], mn = sl[a];
+        for (int i = a + 1; i < b; i++) {
+            mx = fmaxf(mx, su[i]);
+            mn = fminf(mn, sl[i]);
+        }
+        Useg[(int64_t)q * nseg + s] = mx;
+        Lseg[(int64_t)q * nseg + s] = mn;
+    }
 }
 
-// seeds: distinct members from the smallest non-empty probed buckets first
-__global__ void seed_kernel(const uint32_t *__restrict__ ids, const uint64_t *__restrict__ bstart,
-                            const uint32_t *__restrict__ blen, int L, int S0, int64_t N,
-                            const int *__restrict__ is_fallback, uint32_t *__restrict__ seeds,
-                            int *__restrict__ nseed) {
-    const int q = blockIdx.x;
-    const int lane = threadIdx.x;
-    extern __shared__ uint32_t hset[];  // 2*S0 hash slots, then L used-flags
-    const int H = 2 * S0;
-    uint32_t *used = hset + H;
-    for (int e = lane; e < H; e += 32) hset[e] = 0xFFFFFFFFu;
-    for (int j = lane; j < L; j += 32) used[j] = blen[(int64_t)q * L + j] == 0;
-    __syncwarp();
-    uint32_t *out = seeds + (int64_t)q * S0;
-    int cnt = 0;
-    if (is_fallback[q]) {
-        int n = (int)((int64_t)S0 < N ? (int64_t)S0 : N);
-        for (int e = lane; e < S0; e += 32) out[e] = e < n ? (uint32_t)e : 0xFFFFFFFFu;
-        if (lane == 0) nseed[q] = n;
-        return;
-    }
-    const unsigned lt = (1u << lane) - 1u;
-    while (cnt < S0) {
-        // smallest unused non-empty bucket (ties -> lowest table)
-        uint64_t mn = ~0ULL;
-        for (int j = lane; j < L; j += 32)
-            if (!used[j]) {
-                uint64_t key = ((uint64_t)blen[(int64_t)q * L + j] << 16) | (uint64_t)j;
-                mn = key < mn ? key : mn;
+// ------------------------------------------------------ shard summaries
+// PAA segment means (f64 sum, stored f32) of every row + max|x| over the shard
+__global__ void paa_kernel(const float *__restrict__ X, int64_t N, int m, int64_t ld, int nseg,
+                           float *__restrict__ paa, unsigned *__restrict__ maxabs) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    float mx = 0.f;
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < N; row += nw) {
+        const float *x = X + row * ld;
+        for (int s = lane; s < nseg; s += 32) {
+            int a = s * SSH_PAA_SEG, b = min(m, a + SSH_PAA_SEG);
+            double sum = 0.0;
+            for (int i = a; i < b; i++) {
+                float v = x[i];
+                sum += (double)v;
+                mx = fmaxf(mx, fabsf(v));
             }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            uint64_t o2 = __shfl_xor_sync(0xFFFFFFFFu, mn, o);
-            mn = o2 < mn ? o2 : mn;
+            paa[row * nseg + s] = (float)(sum / (double)(b - a));
         }
-        if (mn == ~0ULL) break;
-        int jsel = (int)(mn & 0xFFFF);
-        uint32_t len = (uint32_t)(mn >> 16);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if (lane == 0) atomicMax(maxabs, __float_as_uint(mx));
+}
+
+extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t ld,
+                                   void *stream) {
+    SSH_REQUIRE(ctx && ix && X, SSH_ERR_INVALID, "ssh_index_summarize: NULL argument");
+    SSH_REQUIRE(ctx->have_params, SSH_ERR_STATE, "ssh_index_summarize: params not set");
+    SSH_REQUIRE(ld >= ctx->p.m, SSH_ERR_INVALID, "ssh_index_summarize: ld < m");
+    SSH_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int m = ctx->p.m;
+    const int nseg = (m + SSH_PAA_SEG - 1) / SSH_PAA_SEG;
+    if (!ix->paa) {
+        SSH_CUDA(cudaMallocAsync((void **)&ix->paa, sizeof(float) * (size_t)ix->N * nseg, st));
+        SSH_CUDA(cudaMallocAsync((void **)&ix->d_maxabs, sizeof(unsigned), st));
+    }
+    ix->nseg = nseg;
+    SSH_CUDA(cudaMemsetAsync(ix->d_maxabs, 0, sizeof(unsigned), st));
+    int grid = (int)std::min<int64_t>((ix->N + 7) / 8, (int64_t)ctx->num_sms * 16);
+    paa_kernel<<<grid, 256, 0, st>>>(X, ix->N, m, ld, nseg, ix->paa, ix->d_maxabs);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
+// --------------------------------------------------- member stream kernel
+// One CTA per (query, slice of MB_SLICE_WORDS bitmap words).  A warp turns 32
+// words into a member list in shared memory, evaluates LB_PAA lane-per-member
+// (L2-resident summaries), and
+//   MODE_HIST    histograms LB_PAA (seed threshold),
+//   MODE_COLLECT lists members with LB_PAA below the per-query threshold,
+//   MODE_FILTER  keeps members with LB_PAA <= thr and runs LB_Kim + the
+//                early-abandoning LB_Keogh warp-cooperatively; survivors are
+//                appended with their LB_Keogh value.
+enum { MODE_HIST = 0, MODE_COLLECT = 1, MODE_FILTER = 2 };
+
+struct MemberArgs {
+    const float *X;
+    const float *Q;
+    const float *U, *Lo, *Useg, *Lseg;
+    const float *paa;
+    const unsigned *maxabs;
+    const uint32_t *bitmap;
+    const float *thr;
+    const uint32_t *ts;
+    uint32_t *hist;
+    uint32_t *out;
+    float *out_lb;
+    int *out_cnt;
+    long long *counters;
+    int64_t NW;
+    int m, nseg, cap;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(MB_THREADS) members_kernel(MemberArgs a) {
+    extern __shared__ __align__(16) unsigned char msm[];
+    const int q = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int m = a.m, nseg = a.nseg;
+    float *sUs = reinterpret_cast<float *>(msm);
+    float *sLs = sUs + nseg;
+    uint32_t *lists = reinterpret_cast<uint32_t *>(sLs + nseg);  // MB_WARPS x 1024
+    uint32_t *shist = lists + MB_WARPS * 1024;                   // NBINS (HIST)
+    float *su = reinterpret_cast<float *>(lists + MB_WARPS * 1024);  // m (FILTER)
+    float *sl = su + m;
+    for (int s = threadIdx.x; s < nseg; s += MB_THREADS) {
+        sUs[s] = a.Useg[(int64_t)q * nseg + s];
+        sLs[s] = a.Lseg[(int64_t)q * nseg + s];
+    }
+    if (MODE == MODE_HIST)
+        for (int b = threadIdx.x; b < NBINS; b += MB_THREADS) shist[b] = 0u;
+    if (MODE == MODE_FILTER)
+        for (int i = threadIdx.x; i < m; i += MB_THREADS) {
+            su[i] = a.U[(int64_t)q * m + i];
+            sl[i] = a.Lo[(int64_t)q * m + i];
+        }
+    __syncthreads();
+    // |stored mean - exact mean| <= 2u max|x|; products/sums: relative (2 nseg + 8) u
+    const float delta = 2.f * U32_EPS * __uint_as_float(*a.maxabs) + 1e-30f;
+    const float shrink = 1.f - (2.f * nseg + 8.f) * U32_EPS;
+    const float lastlen = (float)(m - (nseg - 1) * SSH_PAA_SEG);
+    const float T = MODE == MODE_FILTER ? a.thr[q] : 0.f;
+    const uint32_t TS = MODE == MODE_COLLECT ? a.ts[q] : 0u;
+    const float q0 = a.Q[(int64_t)q * m], ql = a.Q[(int64_t)q * m + m - 1];
+    const uint32_t *bm = a.bitmap + (int64_t)q * a.NW;
+    uint32_t *list = lists + w * 1024;
+    int paa_pr = 0, kim = 0, keo = 0;
+    const int64_t s0 = (int64_t)blockIdx.x * MB_SLICE_WORDS;
+    const int64_t s1 = min(a.NW, s0 + MB_SLICE_WORDS);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t wb = s0 + 32 * w; wb < s1; wb += 32 * MB_WARPS) {
+        const int64_t wd = wb + lane;
+        uint32_t word = wd < s1 ? bm[wd] : 0u;
+        int c = __popc(word);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        int pos = incl - c;
+        while (word) {
+            int b = __ffs(word) - 1;
+            word &= word - 1;
+            list[pos++] = (uint32_t)(wd * 32 + b);
+        }
         __syncwarp();
-        if (lane == 0) used[jsel] = 1;
-        __syncwarp();
-        const uint32_t *b = ids + bstart[(int64_t)q * L + jsel];
-        for (uint32_t base = 0; base < len && cnt < S0; base += 32) {
-            uint32_t e = base + lane;
-            bool ins = false;
+        // stage A: LB_PAA, lane per member
+        int kept = 0;
+        for (int base = 0; base < total; base += 32) {
+            const int e = base + lane;
+            bool keep = false;
             uint32_t row = 0;
-            if (e < len) {
-                row = b[e];
-                uint32_t h = (row * 2654435761u) % (uint32_t)H;
-                while (true) {
-                    uint32_t prev = atomicCAS(&hset[h], 0xFFFFFFFFu, row);
-                    if (prev == 0xFFFFFFFFu) { ins = true; break; }
-                    if (prev == row) break;
-                    h = (h + 1) % (uint32_t)H;
+            if (e < total) {
+                row = list[e];
+                const float *p = a.paa + (int64_t)row * nseg;
+                float acc = 0.f;
+                for (int s = 0; s < nseg; s++) {
+                    float xb = __ldg(p + s);
+                    float ev = fmaxf(fmaxf(xb - sUs[s] - delta, sLs[s] - xb - delta), 0.f);
+                    float len = s + 1 < nseg ? (float)SSH_PAA_SEG : lastlen;
+                    acc = fmaf(len * ev, ev, acc);
+                }
+                const float lb = acc * shrink;
+                if (MODE == MODE_HIST) {
+                    atomicAdd(&shist[lb_bin(lb)], 1u);
+                } else if (MODE == MODE_COLLECT) {
+                    if (__float_as_uint(lb) < TS) {
+                        int p2 = atomicAdd(&a.out_cnt[q], 1);
+                        if (p2 < a.cap) {
+                            a.out[(int64_t)q * a.cap + p2] = row;
+                            a.out_lb[(int64_t)q * a.cap + p2] = lb;
+                        }
+                    }
+                } else {
+                    keep = !(lb > T);
+                    paa_pr += !keep;
                 }
             }
-            unsigned msk = __ballot_sync(0xFFFFFFFFu, ins);
-            int pos = cnt + __popc(msk & lt);
-            if (ins && pos < S0) out[pos] = row;
-            cnt = min(S0, cnt + __popc(msk));
-            __syncwarp();
+            if (MODE == MODE_FILTER) {
+                unsigned msk = __ballot_sync(0xFFFFFFFFu, keep);
+                if (keep) list[kept + __popc(msk & lt)] = row;
+                kept += __popc(msk);
+                __syncwarp();
+            }
+        }
+        if (MODE == MODE_FILTER) {
+            // stage B: LB_Kim + early-abandoning LB_Keogh, warp per member
+            for (int e = 0; e < kept; e++) {
+                const uint32_t row = list[e];
+                const float *x = a.X + (int64_t)row * m;
+                if (m >= 2) {
+                    float d0 = x[0] - q0, dl = x[m - 1] - ql;
+                    if (fmaf(dl, dl, d0 * d0) > T) { kim++; continue; }
+                }
+                float acc = 0.f, tot = 0.f;
+                bool pruned = false;
+                for (int base = 0; base < m; base += 128) {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        int i = base + k * 32 + lane;
+                        if (i < m) {
+                            float cv = __ldg(x + i);
+                            float v = fmaxf(fmaxf(cv - su[i], sl[i] - cv), 0.f);
+                            acc = fmaf(v, v, acc);
+                        }
+                    }
+                    tot = warp_sum(acc);
+                    if (tot > T) { pruned = true; break; }
+                }
+                if (pruned) { keo++; continue; }
+                if (lane == 0) {
+                    int p2 = atomicAdd(&a.out_cnt[q], 1);
+                    if (p2 < a.cap) {
+                        a.out[(int64_t)q * a.cap + p2] = row;
+                        a.out_lb[(int64_t)q * a.cap + p2] = tot;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (MODE == MODE_HIST) {
+        __syncthreads();
+        for (int b = threadIdx.x; b < NBINS; b += MB_THREADS) {
+            uint32_t v = shist[b];
+            if (v) atomicAdd(&a.hist[(int64_t)q * NBINS + b], v);
         }
     }
-    for (int e = cnt + lane; e < S0; e += 32) out[e] = 0xFFFFFFFFu;
-    if (lane == 0) nseed[q] = cnt;
+    if (MODE == MODE_FILTER) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) paa_pr += __shfl_xor_sync(0xFFFFFFFFu, paa_pr, o);
+        if (lane == 0) {
+            long long k1 = kim, k2 = (long long)keo + paa_pr;
+            if (k1) atomicAdd((unsigned long long *)&a.counters[q * 5 + 0], (unsigned long long)k1);
+            if (k2) atomicAdd((unsigned long long *)&a.counters[q * 5 + 1], (unsigned long long)k2);
+        }
+    }
+}
+
+// per query: LB_PAA bin threshold holding >= S0 members
+__global__ void seed_thresh_kernel(const uint32_t *__restrict__ hist, int S0, uint32_t *__restrict__ ts) {
+    __shared__ uint32_t part[NBINS / 8];
+    const int q = blockIdx.x;
+    const uint32_t *h = hist + (int64_t)q * NBINS;
+    uint32_t s = 0;
+    for (int b = 0; b < 8; b++) s += h[threadIdx.x * 8 + b];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t cum = 0;
+        uint32_t out = 0xFFFFFFFFu;
+        for (int t = 0; t < NBINS / 8 && out == 0xFFFFFFFFu; t++) {
+            if (cum + part[t] >= (uint32_t)S0) {
+                for (int b = 0; b < 8; b++) {
+                    cum += h[t * 8 + b];
+                    if (cum >= (uint32_t)S0) {
+                        int bin = t * 8 + b;
+                        out = bin + 1 >= NBINS ? 0xFFFFFFFFu : ((uint32_t)(bin + 1) << 20);
+                        break;
+                    }
+                }
+            } else {
+                cum += part[t];
+            }
+        }
+        ts[q] = out;
+    }
+}
+
+// per query: the S0 collected members with the smallest LB_PAA -> seeds
+__global__ void seed_select_kernel(const uint32_t *__restrict__ cand, const float *__restrict__ cand_lb,
+                                   const int *__restrict__ cand_cnt, int cap, int S0,
+                                   uint32_t *__restrict__ seeds, int *__restrict__ nseed) {
+    __shared__ int red[32];
+    __shared__ int npos;
+    const int q = blockIdx.x;
+    uint32_t *out = seeds + (int64_t)q * S0;
+    const int n = min(cand_cnt[q], cap);
+    const uint32_t *bits = reinterpret_cast<const uint32_t *>(cand_lb + (int64_t)q * cap);
+    uint32_t V = 0xFFFFFFFFu;
+    if (n > S0) V = block_kth2<uint32_t>(bits, n, nullptr, 0, S0, 0x7F800000u, red);
+    if (threadIdx.x == 0) npos = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += blockDim.x)
+        if (n <= S0 || bits[e] < V) out[atomicAdd(&npos, 1)] = cand[(int64_t)q * cap + e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += blockDim.x)
+        if (n > S0 && bits[e] == V) {
+            int p = atomicAdd(&npos, 1);
+            if (p < S0) out[p] = cand[(int64_t)q * cap + e];
+        }
+    __syncthreads();
+    const int c = min(npos, S0);
+    for (int e = c + threadIdx.x; e < S0; e += blockDim.x) out[e] = 0xFFFFFFFFu;
+    if (threadIdx.x == 0) nseed[q] = c;
 }
 
 // ------------------------------------------------------------ fp32 DTW
-// lane-per-candidate banded DTW; band[k][lane] in shared memory, query padded
-// with +inf outside [0, m) so out-of-band cells are +inf without branches.
+// Lane-per-candidate banded DTW; band[k][lane] in shared memory, the query
+// padded with +inf outside [0, m) so out-of-band cells are +inf without
+// branches.  With a finite threshold the lane abandons once
+//   row_min + sum_{i' > i} LB_Keogh_i'(x, env(q)) - slack > thr
+// (every remaining row contributes at least its envelope excursion).
 __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const float *__restrict__ Q,
+                             const float *__restrict__ U, const float *__restrict__ Lo,
                              const uint32_t *__restrict__ list, int64_t list_stride,
                              const int *__restrict__ list_cnt, int cap, const float *__restrict__ thr,
                              float *__restrict__ out, unsigned long long *__restrict__ abandoned,
-                             int warps) {
+                             int warps, unsigned long long *__restrict__ cells) {
     extern __shared__ float dsm[];
     const int q = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int B = 2 * r + 2;
-    float *ypad = dsm;                           // m + 2r
-    float *band = dsm + ((m + 2 * r + 3) & ~3) + (size_t)w * B * 32;
+    const int ypadn = (m + 2 * r + 3) & ~3;
+    float *ypad = dsm;  // m + 2r
+    float *su = dsm + ypadn;
+    float *sl = su + m;
+    float *band = sl + m + (size_t)w * B * 32;
     const float *y = Q + (int64_t)q * m;
     for (int j = threadIdx.x; j < m + 2 * r; j += blockDim.x) {
         int jj = j - r;
         ypad[j] = (jj >= 0 && jj < m) ? y[jj] : INFINITY;
     }
+    const float T = thr ? thr[q] : INFINITY;
+    const bool cb = !isinf(T) && U != nullptr;
+    if (cb)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            su[i] = U[(int64_t)q * m + i];
+            sl[i] = Lo[(int64_t)q * m + i];
+        }
     __syncthreads();
     const int cnt = min(list_cnt ? list_cnt[q] : (int)list_stride, cap);
     const int e = (blockIdx.x * warps + w) * 32 + lane;
     if ((blockIdx.x * warps + w) * 32 >= cnt) return;
     uint32_t row = e < cnt ? list[(int64_t)q * list_stride + e] : 0xFFFFFFFFu;
     bool valid = row != 0xFFFFFFFFu;
-    const float T = thr ? thr[q] : INFINITY;
+    const float *x = X + (int64_t)(valid ? row : 0) * m;
+    float rem = 0.f, slack = 0.f;
+    if (cb) {
+        for (int i = 0; i < m; i++) {
+            float cv = x[i];
+            float v = fmaxf(fmaxf(cv - su[i], sl[i] - cv), 0.f);
+            rem = fmaf(v, v, rem);
+        }
+        slack = rem * (float)(2 * m + 8) * U32_EPS;
+    }
     for (int k = 0; k < B; k++) band[k * 32 + lane] = INFINITY;
     band[r * 32 + lane] = 0.f;
-    const float *x = X + (int64_t)(valid ? row : 0) * m;
     bool alive = valid;
+    int rows = 0;
     for (int i = 0; i < m; i++) {
         if (!__any_sync(0xFFFFFFFFu, alive)) break;
+        rows += alive;
         const float xi = x[i];
         float left = INFINITY;
         float diag = band[lane];
@@ -255,12 +577,24 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
             left = c;
             diag = up;
         }
-        if (alive && rmin > T) alive = false;
+        float bound = rmin;
+        if (cb) {
+            float v = fmaxf(fmaxf(xi - su[i], sl[i] - xi), 0.f);
+            rem = fmaf(-v, v, rem);
+            bound = rmin + fmaxf(rem - slack, 0.f);
+        }
+        if (alive && bound > T) alive = false;
     }
     if (e < cnt) {
         float res = (valid && alive) ? band[r * 32 + lane] : INFINITY;
         out[(int64_t)q * list_stride + e] = res;
         if (abandoned && valid && !alive) atomicAdd(&abandoned[q], 1ULL);
+    }
+    if (cells) {
+        unsigned long long c = (unsigned long long)rows * (unsigned long long)(2 * r + 1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        if (lane == 0 && c) atomicAdd(cells, c);
     }
 }
 
@@ -321,170 +655,146 @@ __global__ void dtw64_kernel(const float *__restrict__ X, int m, int r, const fl
     else out[e] = res;
 }
 
-// ------------------------------------------------------- LB filter
-__global__ void __launch_bounds__(LB_THREADS)
-lb_filter_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
-                 const float *__restrict__ U, const float *__restrict__ Lo,
-                 const uint32_t *__restrict__ bitmap, int64_t NW, const float *__restrict__ thr,
-                 uint32_t *__restrict__ surv, int cap, int *__restrict__ surv_cnt,
-                 long long *__restrict__ counters) {
-    extern __shared__ float lsm[];
-    float *su = lsm, *sl = lsm + m;
-    const int q = blockIdx.y;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < m; i += LB_THREADS) {
-        su[i] = U[(int64_t)q * m + i];
-        sl[i] = Lo[(int64_t)q * m + i];
-    }
-    __syncthreads();
-    const float T = thr[q];
-    const float q0 = Q[(int64_t)q * m], ql = Q[(int64_t)q * m + m - 1];
-    const uint32_t *bm = bitmap + (int64_t)q * NW;
-    int kim = 0, keo = 0;
-    const int64_t w0 = (int64_t)blockIdx.x * LB_WORDS;
-    const int64_t w1 = min(NW, w0 + LB_WORDS);
-    for (int64_t wd = w0 + w; wd < w1; wd += LB_WARPS) {
-        uint32_t bits = bm[wd];
-        while (bits) {
-            int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int64_t row = wd * 32 + b;
-            const float *x = X + row * m;
-            if (m >= 2) {
-                float d0 = x[0] - q0, dl = x[m - 1] - ql;
-                float kv = fmaf(dl, dl, d0 * d0);
-                if (kv > T) { kim++; continue; }
-            }
-            float acc = 0.f, tot = 0.f;
-            bool pruned = false;
-            for (int base = 0; base < m; base += 128) {
-#pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    int i = base + e * 32 + lane;
-                    if (i < m) {
-                        float c = x[i];
-                        float a = c - su[i], bb = sl[i] - c;
-                        float v = fmaxf(fmaxf(a, bb), 0.f);
-                        acc = fmaf(v, v, acc);
-                    }
-                }
-                tot = warp_sum(acc);
-                if (tot > T) { pruned = true; break; }
-            }
-            if (pruned) { keo++; continue; }
-            if (lane == 0) {
-                int pos = atomicAdd(&surv_cnt[q], 1);
-                if (pos < cap) surv[(int64_t)q * cap + pos] = (uint32_t)row;
-            }
-        }
-    }
-    if (lane == 0 && (kim | keo)) {
-        if (kim) atomicAdd((unsigned long long *)&counters[q * 5 + 0], (unsigned long long)kim);
-        if (keo) atomicAdd((unsigned long long *)&counters[q * 5 + 1], (unsigned long long)keo);
-    }
-}
-
-// ------------------------------------------------------- block sort helper
-template <typename K>
-__device__ void block_sort_pairs(K *key, uint32_t *val, int P2) {
-    for (int k = 2; k <= P2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int idx = threadIdx.x; idx < (P2 >> 1); idx += blockDim.x) {
-                int i = 2 * idx - (idx & (j - 1));
-                int l = i + j;
-                K a = key[i], b = key[l];
-                uint32_t va = val[i], vb = val[l];
-                bool gt = (a > b) || (a == b && va > vb);
-                bool up = (i & k) == 0;
-                if (gt == up) {
-                    key[i] = b; key[l] = a;
-                    val[i] = vb; val[l] = va;
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-// tau_q = k-th smallest seed DTW (seeds are distinct rows of R)
+// ------------------------------------------------------- thresholds / waves
+// thr0 from the seed DTWs (k-th smallest of distinct seeds)
 __global__ void tau_kernel(const float *__restrict__ sd32, int S0, const int *__restrict__ nseed,
                            int k, float eps, float *__restrict__ thr) {
-    extern __shared__ float tsm[];
-    float *key = tsm;
-    uint32_t *val = reinterpret_cast<uint32_t *>(tsm + S0);
+    __shared__ int red[32];
     const int q = blockIdx.x;
     const int ns = nseed[q];
-    for (int e = threadIdx.x; e < S0; e += blockDim.x) {
-        key[e] = e < ns ? sd32[(int64_t)q * S0 + e] : INFINITY;
-        val[e] = e;
+    const uint32_t *bits = reinterpret_cast<const uint32_t *>(sd32 + (int64_t)q * S0);
+    float t = INFINITY;
+    if (k <= ns) {
+        int nfin = block_count_le2<uint32_t>(bits, ns, nullptr, 0, 0x7F7FFFFFu, red);
+        if (nfin >= k) t = __uint_as_float(block_kth2<uint32_t>(bits, ns, nullptr, 0, k, 0x7F7FFFFFu, red));
     }
+    if (threadIdx.x == 0) thr[q] = thr_from(t, eps);
+}
+
+// wave 1: move the W1 smallest-LB survivors into w1 (taken entries: lb = -1)
+__global__ void wave1_kernel(const uint32_t *__restrict__ surv, float *__restrict__ surv_lb,
+                             const int *__restrict__ surv_cnt, int cap, int W1,
+                             uint32_t *__restrict__ w1, int *__restrict__ w1cnt) {
+    __shared__ uint32_t h[NBINS];
+    __shared__ int npos, cut;
+    const int q = blockIdx.x;
+    const int cnt = min(surv_cnt[q], cap);
+    float *lb = surv_lb + (int64_t)q * cap;
+    const uint32_t *rows = surv + (int64_t)q * cap;
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) h[b] = 0u;
+    if (threadIdx.x == 0) npos = 0;
     __syncthreads();
-    block_sort_pairs<float>(key, val, S0);
+    if (cnt > W1)
+        for (int e = threadIdx.x; e < cnt; e += blockDim.x) atomicAdd(&h[lb_bin(lb[e])], 1u);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        float t = (k <= ns) ? key[k - 1] : INFINITY;
-        thr[q] = isinf(t) ? INFINITY : (float)((double)t * (1.0 + (double)eps));
+        int c = 0, b = NBINS;
+        if (cnt > W1) {
+            for (b = 0; b < NBINS; b++) {
+                if (c + (int)h[b] >= W1) break;
+                c += h[b];
+            }
+        }
+        cut = b;
     }
-}
-
-// block-wide count of entries with key-bits <= v (non-negative floats/doubles
-// order like their bit patterns)
-template <typename U>
-__device__ int block_count_le(const U *bits, int n, U v, int *red) {
-    int c = 0;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) c += bits[e] <= v;
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
     __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
-    __syncthreads();
-    int s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w];
-    return s;
-}
-
-// smallest v with count(bits <= v) >= kk (kk >= 1, kk <= n)
-template <typename U>
-__device__ U block_kth(const U *bits, int n, int kk, U hi, int *red) {
-    U lo = 0;
-    while (lo < hi) {
-        U mid = lo + (hi - lo) / 2;
-        if (block_count_le<U>(bits, n, mid, red) >= kk) hi = mid; else lo = mid + 1;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+        float v = lb[e];
+        if ((int)lb_bin(v) < cut) {
+            w1[(int64_t)q * W1 + atomicAdd(&npos, 1)] = rows[e];
+            lb[e] = -1.f;
+        }
     }
-    return lo;
+    __syncthreads();
+    if (cut < NBINS)
+        for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+            float v = lb[e];
+            if (v >= 0.f && (int)lb_bin(v) == cut) {
+                int p = atomicAdd(&npos, 1);
+                if (p < W1) {
+                    w1[(int64_t)q * W1 + p] = rows[e];
+                    lb[e] = -1.f;
+                }
+            }
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) w1cnt[q] = min(npos, W1);
 }
 
-// rescoring set: d32 <= T_k (1 + eps), T_k = k-th smallest finite survivor d32
-__global__ void select_kernel(const uint32_t *__restrict__ surv, const float *__restrict__ d32,
-                              const int *__restrict__ surv_cnt, int cap, int k, float eps,
-                              uint32_t *__restrict__ resc, int *__restrict__ resc_cnt) {
+// tighten thr with the wave-1 DTWs: thr1 = min(thr0, kth(d32_w1) (1 + eps))
+__global__ void tau1_kernel(const float *__restrict__ d1, int W1, const int *__restrict__ w1cnt,
+                            int k, float eps, float *__restrict__ thr) {
+    __shared__ int red[32];
+    const int q = blockIdx.x;
+    const int n = w1cnt[q];
+    const uint32_t *bits = reinterpret_cast<const uint32_t *>(d1 + (int64_t)q * W1);
+    if (n < k) return;
+    int nfin = block_count_le2<uint32_t>(bits, n, nullptr, 0, 0x7F7FFFFFu, red);
+    if (nfin < k) return;
+    float t = __uint_as_float(block_kth2<uint32_t>(bits, n, nullptr, 0, k, 0x7F7FFFFFu, red));
+    if (threadIdx.x == 0) thr[q] = fminf(thr[q], thr_from(t, eps));
+}
+
+// wave 2: remaining survivors with LB_Keogh <= thr1
+__global__ void wave2_kernel(const uint32_t *__restrict__ surv, const float *__restrict__ surv_lb,
+                             const int *__restrict__ surv_cnt, int cap, const float *__restrict__ thr,
+                             uint32_t *__restrict__ w2, int *__restrict__ w2cnt,
+                             long long *__restrict__ counters) {
     __shared__ int red[32];
     __shared__ int npos;
     const int q = blockIdx.x;
     const int cnt = min(surv_cnt[q], cap);
-    const uint32_t *bits = reinterpret_cast<const uint32_t *>(d32 + (int64_t)q * cap);
-    const uint32_t INF = 0x7F800000u;
-    const int nfin = block_count_le<uint32_t>(bits, cnt, INF - 1, red);
-    const int kk = min(k, nfin);
-    float bound = -1.f;
-    if (kk > 0) {
-        uint32_t t = block_kth<uint32_t>(bits, cnt, kk, INF - 1, red);
-        bound = (float)((double)__uint_as_float(t) * (1.0 + (double)eps));
-    }
+    const float T = thr[q];
     if (threadIdx.x == 0) npos = 0;
     __syncthreads();
+    int pr = 0;
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-        float v = d32[(int64_t)q * cap + e];
-        if (v <= bound) {
+        float v = surv_lb[(int64_t)q * cap + e];
+        if (v < 0.f) continue;
+        if (v <= T) {
             int p = atomicAdd(&npos, 1);
-            resc[(int64_t)q * cap + p] = surv[(int64_t)q * cap + e];
+            w2[(int64_t)q * cap + p] = surv[(int64_t)q * cap + e];
+        } else {
+            pr++;
         }
     }
+    int tot = block_sum(pr, red);
+    if (threadIdx.x == 0) {
+        w2cnt[q] = npos;
+        if (tot) counters[q * 5 + 1] += tot;
+    }
+}
+
+// rescoring set over both waves: d32 <= T_k (1 + eps)
+__global__ void select_kernel(const uint32_t *__restrict__ w1, const float *__restrict__ d1,
+                              const int *__restrict__ c1, int W1, const uint32_t *__restrict__ w2,
+                              const float *__restrict__ d2, const int *__restrict__ c2, int cap,
+                              int k, float eps, uint32_t *__restrict__ resc, int RS,
+                              int *__restrict__ resc_cnt) {
+    __shared__ int red[32];
+    __shared__ int npos;
+    const int q = blockIdx.x;
+    const int na = c1[q], nb = min(c2[q], cap);
+    const uint32_t *ba = reinterpret_cast<const uint32_t *>(d1 + (int64_t)q * W1);
+    const uint32_t *bb = reinterpret_cast<const uint32_t *>(d2 + (int64_t)q * cap);
+    const int nfin = block_count_le2<uint32_t>(ba, na, bb, nb, 0x7F7FFFFFu, red);
+    const int kk = min(k, nfin);
+    float bound = -1.f;
+    if (kk > 0)
+        bound = thr_from(__uint_as_float(block_kth2<uint32_t>(ba, na, bb, nb, kk, 0x7F7FFFFFu, red)), eps);
+    if (threadIdx.x == 0) npos = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < na; e += blockDim.x)
+        if (d1[(int64_t)q * W1 + e] <= bound) resc[(int64_t)q * RS + atomicAdd(&npos, 1)] = w1[(int64_t)q * W1 + e];
+    for (int e = threadIdx.x; e < nb; e += blockDim.x)
+        if (d2[(int64_t)q * cap + e] <= bound) resc[(int64_t)q * RS + atomicAdd(&npos, 1)] = w2[(int64_t)q * cap + e];
     __syncthreads();
     if (threadIdx.x == 0) resc_cnt[q] = npos;
 }
 
 // exact top-k by (d64, id) of the rescored set; P2 >= k power of two
 __global__ void topk_kernel(const uint32_t *__restrict__ resc, const double *__restrict__ d64,
-                            const int *__restrict__ resc_cnt, int cap, int P2, int k,
+                            const int *__restrict__ resc_cnt, int RS, int P2, int k,
                             int64_t id_base, const long long *__restrict__ n_cand,
                             long long *__restrict__ out_ids, double *__restrict__ out_d2,
                             int *__restrict__ n_out) {
@@ -494,34 +804,24 @@ __global__ void topk_kernel(const uint32_t *__restrict__ resc, const double *__r
     __shared__ int red[32];
     __shared__ int npos;
     const int q = blockIdx.x;
-    const int cnt = n_cand[q] > 0 ? min(resc_cnt[q], cap) : 0;
+    const int cnt = n_cand[q] > 0 ? min(resc_cnt[q], RS) : 0;
     const int n = min(k, cnt);
-    const uint64_t *bits = reinterpret_cast<const uint64_t *>(d64 + (int64_t)q * cap);
-    const uint32_t *ids = resc + (int64_t)q * cap;
-    // V = n-th smallest d64; then the smallest ids among entries equal to V
-    uint64_t V = 0;
+    const uint64_t *bits = reinterpret_cast<const uint64_t *>(d64 + (int64_t)q * RS);
+    const uint32_t *ids = resc + (int64_t)q * RS;
+    uint64_t V = 0x7FF0000000000000ULL;
     uint32_t idcut = 0xFFFFFFFFu;
     if (n > 0 && cnt > n) {
-        V = block_kth<uint64_t>(bits, cnt, n, 0x7FF0000000000000ULL, red);
-        int nless = V ? block_count_le<uint64_t>(bits, cnt, V - 1, red) : 0;
+        V = block_kth2<uint64_t>(bits, cnt, nullptr, 0, n, 0x7FF0000000000000ULL, red);
+        int nless = V ? block_count_le2<uint64_t>(bits, cnt, nullptr, 0, V - 1, red) : 0;
         int need = n - nless;
-        // idcut = need-th smallest id among entries with bits == V
         uint32_t lo = 0, hi = 0xFFFFFFFFu;
-        while (lo < hi) {
+        while (lo < hi) {  // need-th smallest id among entries equal to V
             uint32_t mid = lo + (hi - lo) / 2;
             int c = 0;
             for (int e = threadIdx.x; e < cnt; e += blockDim.x) c += (bits[e] == V && ids[e] <= mid);
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-            __syncthreads();
-            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
-            __syncthreads();
-            int s = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w];
-            if (s >= need) hi = mid; else lo = mid + 1;
+            if (block_sum(c, red) >= need) hi = mid; else lo = mid + 1;
         }
         idcut = lo;
-    } else {
-        V = 0x7FF0000000000000ULL;
     }
     if (threadIdx.x == 0) npos = 0;
     for (int e = threadIdx.x; e < P2; e += blockDim.x) {
@@ -531,8 +831,7 @@ __global__ void topk_kernel(const uint32_t *__restrict__ resc, const double *__r
     __syncthreads();
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
         uint64_t b = bits[e];
-        bool take = (cnt <= n) || b < V || (b == V && ids[e] <= idcut);
-        if (take) {
+        if (cnt <= n || b < V || (b == V && ids[e] <= idcut)) {
             int p = atomicAdd(&npos, 1);
             if (p < P2) {
                 key[p] = __longlong_as_double((long long)b);
@@ -549,14 +848,15 @@ __global__ void topk_kernel(const uint32_t *__restrict__ resc, const double *__r
     if (threadIdx.x == 0) n_out[q] = n;
 }
 
-__global__ void finalize_counters(const int *__restrict__ surv_cnt,
+__global__ void finalize_counters(const int *__restrict__ nseed, const int *__restrict__ w1cnt,
+                                  const int *__restrict__ w2cnt,
                                   const unsigned long long *__restrict__ abandoned, int nq,
                                   const long long *__restrict__ n_cand,
                                   const int *__restrict__ is_fb, long long *__restrict__ counters,
                                   int *__restrict__ status) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
-    counters[q * 5 + 3] = surv_cnt[q];
+    counters[q * 5 + 3] = (long long)nseed[q] + w1cnt[q] + w2cnt[q];
     counters[q * 5 + 4] = (long long)abandoned[q];
     status[q] = n_cand[q] == 0 ? 1 : (is_fb[q] ? 2 : 0);
 }
@@ -581,6 +881,83 @@ struct Arena {
     }
 };
 
+// bump carving of one ctx slot (a first pass with base == nullptr sizes it)
+struct Carver {
+    unsigned char *base = nullptr;
+    size_t off = 0;
+    template <typename T>
+    T *take(size_t n) {
+        off = (off + 255) & ~(size_t)255;
+        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += std::max<size_t>(n, 1) * sizeof(T);
+        return p;
+    }
+};
+
+struct QueryBufs {
+    uint64_t *qsig, *qbits, *bstart;
+    uint32_t *blen, *seeds, *w1, *ts, *cand;
+    int *isfb, *nseed, *scnt, *c1, *c2, *rcnt, *ccnt;
+    float *U, *Lo, *Useg, *Lseg, *sd32, *thr, *d1, *cand_lb;
+    unsigned long long *aband;
+
+    void carve(Carver &c, int nc, int L, int words, int S0, int W1, int m, int nseg) {
+        qsig = c.take<uint64_t>((size_t)nc * L);
+        qbits = c.take<uint64_t>((size_t)nc * words);
+        bstart = c.take<uint64_t>((size_t)nc * L);
+        blen = c.take<uint32_t>((size_t)nc * L);
+        seeds = c.take<uint32_t>((size_t)nc * S0);
+        w1 = c.take<uint32_t>((size_t)nc * W1);
+        ts = c.take<uint32_t>(nc);
+        cand = c.take<uint32_t>((size_t)nc * Q_SEED_CAND);
+        isfb = c.take<int>(nc);
+        nseed = c.take<int>(nc);
+        scnt = c.take<int>(nc);
+        c1 = c.take<int>(nc);
+        c2 = c.take<int>(nc);
+        rcnt = c.take<int>(nc);
+        ccnt = c.take<int>(nc);
+        U = c.take<float>((size_t)nc * m);
+        Lo = c.take<float>((size_t)nc * m);
+        Useg = c.take<float>((size_t)nc * nseg);
+        Lseg = c.take<float>((size_t)nc * nseg);
+        sd32 = c.take<float>((size_t)nc * S0);
+        thr = c.take<float>(nc);
+        d1 = c.take<float>((size_t)nc * W1);
+        cand_lb = c.take<float>((size_t)nc * Q_SEED_CAND);
+        aband = c.take<unsigned long long>(nc);
+    }
+};
+
+struct PhaseTimer {
+    ssh_ctx *ctx;
+    cudaStream_t st;
+    cudaEvent_t ev[8];
+    int n = 0;
+    bool on;
+    PhaseTimer(ssh_ctx *c, cudaStream_t s) : ctx(c), st(s), on(c->profile != 0) {
+        if (on)
+            for (int i = 0; i < 8; i++) cudaEventCreate(&ev[i]);
+    }
+    void mark() {
+        if (on && n < 8) cudaEventRecord(ev[n++], st);
+    }
+    void flush() {
+        if (!on || n == 0) return;
+        cudaEventSynchronize(ev[n - 1]);
+        for (int i = 1; i < n; i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            ctx->prof[i - 1] += ms;
+        }
+        n = 0;
+    }
+    ~PhaseTimer() {
+        if (on)
+            for (int i = 0; i < 8; i++) cudaEventDestroy(ev[i]);
+    }
+};
+
 int next_pow2(int v) {
     int p = 32;
     while (p < v) p <<= 1;
@@ -589,12 +966,15 @@ int next_pow2(int v) {
 
 float rescore_eps(int m) { return (float)((8.0 * m + 64.0) * ldexp(1.0, -24)); }
 
+size_t dtw32_smem(int m, int r, int warps) {
+    size_t yb = (size_t)((m + 2 * r + 3) & ~3) * 4 + (size_t)2 * m * 4;
+    return yb + (size_t)(2 * r + 2) * 32 * 4 * warps;
+}
+
 int dtw32_warps(int m, int r, size_t *smem) {
-    size_t yb = (size_t)((m + 2 * r + 3) & ~3) * 4;
-    size_t per = (size_t)(2 * r + 2) * 32 * 4;
     int w = 4;
-    while (w > 1 && yb + per * w > 200 * 1024) w--;
-    *smem = yb + per * w;
+    while (w > 1 && dtw32_smem(m, r, w) > 200 * 1024) w--;
+    *smem = dtw32_smem(m, r, w);
     return w;
 }
 
@@ -605,19 +985,28 @@ int dtw64_threads(int r, size_t *smem) {
     *smem = per * t;
     return t;
 }
+
+size_t members_smem(int mode, int m, int nseg) {
+    size_t b = (size_t)2 * nseg * 4 + (size_t)MB_WARPS * 1024 * 4;
+    if (mode == MODE_HIST) b += NBINS * 4;
+    if (mode == MODE_FILTER) b += (size_t)2 * m * 4;
+    return b;
+}
 }  // namespace
 
-static int launch_dtw32(const float *X, int m, int r, const float *Q, const uint32_t *list,
-                        int64_t stride, const int *cnt, int cap, int maxcnt, const float *thr,
-                        float *out, unsigned long long *aband, int nq, cudaStream_t st) {
+static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const float *U,
+                        const float *Lo, const uint32_t *list, int64_t stride, const int *cnt,
+                        int cap, int maxcnt, const float *thr, float *out,
+                        unsigned long long *aband, int nq, cudaStream_t st) {
+    const int m = ctx->p.m, r = ctx->p.radius;
     size_t smem;
     int warps = dtw32_warps(m, r, &smem);
     SSH_REQUIRE(smem <= 227 * 1024, SSH_ERR_UNSUPPORTED, "DTW band too wide (r=%d)", r);
     SSH_CUDA(cudaFuncSetAttribute(dtw32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (maxcnt <= 0) return SSH_OK;
     dim3 grid((unsigned)ssh_div_up(maxcnt, 32 * warps), (unsigned)nq);
-    dtw32_kernel<<<grid, 32 * warps, smem, st>>>(X, m, r, Q, list, stride, cnt, cap, thr, out, aband,
-                                                 warps);
+    dtw32_kernel<<<grid, 32 * warps, smem, st>>>(X, m, r, Q, U, Lo, list, stride, cnt, cap, thr, out,
+                                                 aband, warps, ctx->profile ? ctx->d_cells : nullptr);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
@@ -631,6 +1020,17 @@ static int launch_dtw64_list(const float *X, int m, int r, const float *Q, const
     if (maxcnt <= 0) return SSH_OK;
     dim3 grid((unsigned)ssh_div_up(maxcnt, t), (unsigned)nq);
     dtw64_kernel<<<grid, t, smem, st>>>(X, m, r, Q, nullptr, list, stride, cnt, nullptr, 0, out);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
+template <int MODE>
+static int launch_members(const MemberArgs &a, int nq, cudaStream_t st) {
+    size_t smem = members_smem(MODE, a.m, a.nseg);
+    SSH_CUDA(cudaFuncSetAttribute(members_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    dim3 g((unsigned)ssh_div_up(a.NW, MB_SLICE_WORDS), (unsigned)nq);
+    members_kernel<MODE><<<g, MB_THREADS, smem, st>>>(a);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
@@ -659,9 +1059,9 @@ static int qsig_batch(ssh_ctx *ctx, const float *Q, int nq, uint64_t *qsig, uint
                                   nullptr, nullptr, qsig, SIG_MODE_FUSED, st);
 }
 
-static int probe_and_bitmap(ssh_ctx *ctx, const ssh_index *ix, const uint64_t *qsig, int nq,
-                            int fallback, uint64_t *bstart, uint32_t *blen, uint32_t *bitmap,
-                            long long *n_cand, int *is_fb, cudaStream_t st) {
+static int probe_and_bitmap(const ssh_index *ix, const uint64_t *qsig, int nq, int fallback,
+                            uint64_t *bstart, uint32_t *blen, uint32_t *bitmap, long long *n_cand,
+                            int *is_fb, cudaStream_t st) {
     const int L = ix->L;
     const int64_t N = ix->N, NW = (N + 31) / 32;
     probe_kernel<<<ssh_div_up((int64_t)nq * L, 128), 128, 0, st>>>(
@@ -689,7 +1089,15 @@ extern "C" int ssh_probe(ssh_ctx *ctx, const ssh_index *ix, const uint64_t *qsig
     uint32_t *blen = A.get<uint32_t>((size_t)nq * ix->L);
     int *isfb = A.get<int>(nq);
     if (A.err) return ssh_cuda_fail(A.err, "ssh_probe scratch", __FILE__, __LINE__);
-    return probe_and_bitmap(ctx, ix, qsig, nq, 0, bstart, blen, bitmap, (long long *)n_cand, isfb, st);
+    return probe_and_bitmap(ix, qsig, nq, 0, bstart, blen, bitmap, (long long *)n_cand, isfb, st);
+}
+
+static int max_of(const int *d, int n, cudaStream_t st, int *out) {
+    std::vector<int> h(n);
+    SSH_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    SSH_CUDA(cudaStreamSynchronize(st));
+    *out = n ? *std::max_element(h.begin(), h.end()) : 0;
+    return SSH_OK;
 }
 
 extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X, const float *Q,
@@ -707,97 +1115,143 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                 "ssh_query_batch: NULL pointer");
     SSH_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = (cudaStream_t)stream;
-    const int m = ctx->p.m, r = ctx->p.radius, L = ix->L;
+    ssh_index *mix = const_cast<ssh_index *>(ix);
+    if (!mix->paa) {
+        int rc = ssh_index_summarize(ctx, mix, X, ctx->p.m, stream);
+        if (rc) return rc;
+    }
+    const int m = ctx->p.m, r = ctx->p.radius, L = ix->L, nseg = ix->nseg;
     const int64_t N = ix->N, NW = (N + 31) / 32;
     const float eps = rescore_eps(m);
     const int S0 = ((std::max(64, 2 * k) + 31) / 32) * 32;
+    const int W1 = S0;
     const int fallback = (flags & SSH_QUERY_FALLBACK_ON_EMPTY) ? 1 : 0;
     // query chunk: keep the membership bitmaps under ~1 GiB
     int qc = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(nq, 32768),
                                                          ((int64_t)1 << 28) / std::max<int64_t>(1, NW)));
     SSH_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 5 * (size_t)nq, st));
     int cap = Q_SURV_CAP0;
+    PhaseTimer pt(ctx, st);
     for (int q0 = 0; q0 < nq; q0 += qc) {
         const int nc = std::min(qc, nq - q0);
         const float *Qc = Q + (int64_t)q0 * m;
         long long *ncand = (long long *)n_cand + q0;
         long long *cnt5 = (long long *)counters + (int64_t)q0 * 5;
-        Arena A;
-        A.st = st;
-        uint64_t *qsig = A.get<uint64_t>((size_t)nc * L);
-        uint64_t *qbits = A.get<uint64_t>((size_t)nc * ctx->words);
-        uint64_t *bstart = A.get<uint64_t>((size_t)nc * L);
-        uint32_t *blen = A.get<uint32_t>((size_t)nc * L);
-        uint32_t *bitmap = A.get<uint32_t>((size_t)nc * NW);
-        int *isfb = A.get<int>(nc);
-        float *U = A.get<float>((size_t)nc * m);
-        float *Lo = A.get<float>((size_t)nc * m);
-        uint32_t *seeds = A.get<uint32_t>((size_t)nc * S0);
-        int *nseed = A.get<int>(nc);
-        float *sd32 = A.get<float>((size_t)nc * S0);
-        float *thr = A.get<float>(nc);
-        int *scnt = A.get<int>(nc);
-        int *rcnt = A.get<int>(nc);
-        unsigned long long *aband = A.get<unsigned long long>(nc);
-        if (A.err) return ssh_cuda_fail(A.err, "query scratch", __FILE__, __LINE__);
-        int rc = qsig_batch(ctx, Qc, nc, qsig, qbits, st);
+        Carver sizer;
+        QueryBufs B;
+        B.carve(sizer, nc, L, ctx->words, S0, W1, m, nseg);
+        Carver cv;
+        cv.base = (unsigned char *)ssh_slot(ctx, SLOT_Q_FIXED, sizer.off, st);
+        if (!cv.base) return SSH_ERR_OOM;
+        B.carve(cv, nc, L, ctx->words, S0, W1, m, nseg);
+        uint32_t *bitmap = (uint32_t *)ssh_slot(ctx, SLOT_Q_BITMAP, sizeof(uint32_t) * (size_t)nc * NW, st);
+        uint32_t *hist = (uint32_t *)ssh_slot(ctx, SLOT_Q_HIST, sizeof(uint32_t) * (size_t)nc * NBINS, st);
+        if (!bitmap || !hist) return SSH_ERR_OOM;
+        SSH_CUDA(cudaMemsetAsync(B.aband, 0, sizeof(unsigned long long) * nc, st));
+        pt.mark();
+        // K5: query signatures
+        int rc = qsig_batch(ctx, Qc, nc, B.qsig, B.qbits, st);
         if (rc) return rc;
-        rc = probe_and_bitmap(ctx, ix, qsig, nc, fallback, bstart, blen, bitmap, ncand, isfb, st);
+        pt.mark();
+        // K6: probe + candidate bitmap
+        rc = probe_and_bitmap(ix, B.qsig, nc, fallback, B.bstart, B.blen, bitmap, ncand, B.isfb, st);
         if (rc) return rc;
-        envelope_kernel<<<nc, 256, 0, st>>>(Qc, m, r, U, Lo);
-        seed_kernel<<<nc, 32, sizeof(uint32_t) * (2 * S0 + L), st>>>(ix->ids, bstart, blen, L, S0, N, isfb,
-                                                               seeds, nseed);
+        pt.mark();
+        // seeds: the S0 members with the smallest LB_PAA -> fp32 DTW -> thr0
+        envelope_kernel<<<nc, 256, 2 * m * sizeof(float), st>>>(Qc, m, r, nseg, B.U, B.Lo, B.Useg, B.Lseg);
+        ssh_count_launch();
+        MemberArgs ma;
+        ma.X = X; ma.Q = Qc; ma.U = B.U; ma.Lo = B.Lo; ma.Useg = B.Useg; ma.Lseg = B.Lseg;
+        ma.paa = ix->paa; ma.maxabs = ix->d_maxabs; ma.bitmap = bitmap; ma.thr = B.thr; ma.ts = B.ts;
+        ma.hist = hist; ma.counters = cnt5; ma.NW = NW; ma.m = m; ma.nseg = nseg;
+        ma.out = nullptr; ma.out_lb = nullptr; ma.out_cnt = nullptr; ma.cap = 0;
+        SSH_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)nc * NBINS, st));
+        rc = launch_members<MODE_HIST>(ma, nc, st);
+        if (rc) return rc;
+        seed_thresh_kernel<<<nc, NBINS / 8, 0, st>>>(hist, S0, B.ts);
         SSH_CHECK_LAUNCH();
-        rc = launch_dtw32(X, m, r, Qc, seeds, S0, nseed, S0, S0, nullptr, sd32, nullptr, nc, st);
+        SSH_CUDA(cudaMemsetAsync(B.ccnt, 0, sizeof(int) * nc, st));
+        ma.out = B.cand; ma.out_lb = B.cand_lb; ma.out_cnt = B.ccnt; ma.cap = Q_SEED_CAND;
+        rc = launch_members<MODE_COLLECT>(ma, nc, st);
         if (rc) return rc;
-        tau_kernel<<<nc, 256, (sizeof(float) + sizeof(uint32_t)) * S0, st>>>(sd32, S0, nseed, k, eps, thr);
+        seed_select_kernel<<<nc, 256, 0, st>>>(B.cand, B.cand_lb, B.ccnt, Q_SEED_CAND, S0, B.seeds,
+                                               B.nseed);
         SSH_CHECK_LAUNCH();
-        // LB filter (retried with a larger per-query capacity on overflow)
+        rc = launch_dtw32(ctx, X, Qc, nullptr, nullptr, B.seeds, S0, B.nseed, S0, S0, nullptr, B.sd32,
+                          nullptr, nc, st);
+        if (rc) return rc;
+        tau_kernel<<<nc, 256, 0, st>>>(B.sd32, S0, B.nseed, k, eps, B.thr);
+        SSH_CHECK_LAUNCH();
+        pt.mark();
+        // K7: member filter (retried with a larger per-query capacity on overflow)
         uint32_t *surv = nullptr;
-        std::vector<int> hcnt(nc);
-        SSH_CUDA(cudaFuncSetAttribute(lb_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(8 * m)));
-        for (int attempt = 0;; attempt++) {
-            surv = A.get<uint32_t>((size_t)nc * cap);
-            if (A.err) return ssh_cuda_fail(A.err, "survivor buffer", __FILE__, __LINE__);
-            SSH_CUDA(cudaMemsetAsync(scnt, 0, sizeof(int) * nc, st));
+        float *slb = nullptr;
+        int maxs = 0;
+        for (;;) {
+            surv = (uint32_t *)ssh_slot(ctx, SLOT_Q_SURV, sizeof(uint32_t) * (size_t)nc * cap, st);
+            slb = (float *)ssh_slot(ctx, SLOT_Q_SURV_LB, sizeof(float) * (size_t)nc * cap, st);
+            if (!surv || !slb) return SSH_ERR_OOM;
+            SSH_CUDA(cudaMemsetAsync(B.scnt, 0, sizeof(int) * nc, st));
             SSH_CUDA(cudaMemsetAsync(cnt5, 0, sizeof(long long) * 5 * nc, st));
-            dim3 g((unsigned)ssh_div_up(NW, LB_WORDS), (unsigned)nc);
-            lb_filter_kernel<<<g, LB_THREADS, 8 * m, st>>>(X, m, Qc, U, Lo, bitmap, NW, thr, surv, cap,
-                                                         scnt, cnt5);
-            SSH_CHECK_LAUNCH();
-            SSH_CUDA(cudaMemcpyAsync(hcnt.data(), scnt, sizeof(int) * nc, cudaMemcpyDeviceToHost, st));
-            SSH_CUDA(cudaStreamSynchronize(st));
-            int mx = *std::max_element(hcnt.begin(), hcnt.end());
-            if (mx <= cap) break;
-            cap = next_pow2(mx);
+            ma.out = surv; ma.out_lb = slb; ma.out_cnt = B.scnt; ma.cap = cap;
+            rc = launch_members<MODE_FILTER>(ma, nc, st);
+            if (rc) return rc;
+            rc = max_of(B.scnt, nc, st, &maxs);
+            if (rc) return rc;
+            if (maxs <= cap) break;
+            cap = next_pow2(maxs);
         }
-        int maxs = *std::max_element(hcnt.begin(), hcnt.end());
-        float *d32 = A.get<float>((size_t)nc * cap);
-        uint32_t *resc = A.get<uint32_t>((size_t)nc * cap);
-        double *d64 = A.get<double>((size_t)nc * cap);
-        if (A.err) return ssh_cuda_fail(A.err, "rerank buffers", __FILE__, __LINE__);
-        SSH_CUDA(cudaMemsetAsync(aband, 0, sizeof(unsigned long long) * nc, st));
-        rc = launch_dtw32(X, m, r, Qc, surv, cap, scnt, cap, maxs, thr, d32, aband, nc, st);
-        if (rc) return rc;
-        select_kernel<<<nc, 256, 0, st>>>(surv, d32, scnt, cap, k, eps, resc, rcnt);
+        pt.mark();
+        // K8: DTW waves in LB order
+        uint32_t *w2 = (uint32_t *)ssh_slot(ctx, SLOT_Q_W2, sizeof(uint32_t) * (size_t)nc * cap, st);
+        float *d2 = (float *)ssh_slot(ctx, SLOT_Q_D2, sizeof(float) * (size_t)nc * cap, st);
+        if (!w2 || !d2) return SSH_ERR_OOM;
+        wave1_kernel<<<nc, 256, 0, st>>>(surv, slb, B.scnt, cap, W1, B.w1, B.c1);
         SSH_CHECK_LAUNCH();
-        std::vector<int> hr(nc);
-        SSH_CUDA(cudaMemcpyAsync(hr.data(), rcnt, sizeof(int) * nc, cudaMemcpyDeviceToHost, st));
-        SSH_CUDA(cudaStreamSynchronize(st));
-        int maxr = *std::max_element(hr.begin(), hr.end());
-        rc = launch_dtw64_list(X, m, r, Qc, resc, cap, rcnt, maxr, d64, nc, st);
+        rc = launch_dtw32(ctx, X, Qc, B.U, B.Lo, B.w1, W1, B.c1, W1, std::min(W1, maxs), B.thr, B.d1,
+                          B.aband, nc, st);
+        if (rc) return rc;
+        tau1_kernel<<<nc, 256, 0, st>>>(B.d1, W1, B.c1, k, eps, B.thr);
+        SSH_CHECK_LAUNCH();
+        wave2_kernel<<<nc, 256, 0, st>>>(surv, slb, B.scnt, cap, B.thr, w2, B.c2, cnt5);
+        SSH_CHECK_LAUNCH();
+        int max2 = 0;
+        rc = max_of(B.c2, nc, st, &max2);
+        if (rc) return rc;
+        rc = launch_dtw32(ctx, X, Qc, B.U, B.Lo, w2, cap, B.c2, cap, max2, B.thr, d2, B.aband, nc, st);
+        if (rc) return rc;
+        pt.mark();
+        // K9/K10: rescoring set, exact f64 DTW, top-k by (d64, id)
+        const int RS = W1 + cap;
+        uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)nc * RS, st);
+        double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)nc * RS, st);
+        if (!resc || !d64) return SSH_ERR_OOM;
+        select_kernel<<<nc, 256, 0, st>>>(B.w1, B.d1, B.c1, W1, w2, d2, B.c2, cap, k, eps, resc, RS, B.rcnt);
+        SSH_CHECK_LAUNCH();
+        int maxr = 0;
+        rc = max_of(B.rcnt, nc, st, &maxr);
+        if (rc) return rc;
+        rc = launch_dtw64_list(X, m, r, Qc, resc, RS, B.rcnt, maxr, d64, nc, st);
         if (rc) return rc;
         const int P2k = next_pow2(k);
         size_t stk = (size_t)P2k * (sizeof(double) + sizeof(uint32_t));
         SSH_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stk));
-        topk_kernel<<<nc, 256, stk, st>>>(resc, d64, rcnt, cap, P2k, k, ix->id_base, ncand,
+        topk_kernel<<<nc, 256, stk, st>>>(resc, d64, B.rcnt, RS, P2k, k, ix->id_base, ncand,
                                           (long long *)out_ids + (int64_t)q0 * k,
                                           out_d2 + (int64_t)q0 * k, n_out + q0);
         SSH_CHECK_LAUNCH();
-        finalize_counters<<<ssh_div_up(nc, 128), 128, 0, st>>>(scnt, aband, nc, ncand, isfb, cnt5,
-                                                               status + q0);
+        finalize_counters<<<ssh_div_up(nc, 128), 128, 0, st>>>(B.nseed, B.c1, B.c2, B.aband, nc, ncand,
+                                                               B.isfb, cnt5, status + q0);
         SSH_CHECK_LAUNCH();
+        pt.mark();
+        if (ctx->profile) {
+            pt.flush();
+            std::vector<int> h(nc);
+            cudaMemcpy(h.data(), B.scnt, sizeof(int) * nc, cudaMemcpyDeviceToHost);
+            for (int v : h) ctx->prof[8] += v;
+            cudaMemcpy(h.data(), B.rcnt, sizeof(int) * nc, cudaMemcpyDeviceToHost);
+            for (int v : h) ctx->prof[9] += v;
+        }
     }
     return SSH_OK;
 }

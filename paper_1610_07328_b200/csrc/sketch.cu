@@ -255,7 +255,7 @@ static bool try_poly(ssh_ctx *ctx, const float *X, SketchGeom &g, const SketchW 
     if (per_sm < 1) per_sm = 1;
     int64_t ntiles = (g.N + g.ST - 1) / g.ST;
     int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * per_sm);
-    kern<<<grid, SK_THREADS, smem, st>>>(X, g, wp, ctx->d_w64, bits, (long long *)stats);
+    kern<<<grid, SK_THREADS, smem, st>>>(X, g, wp, ctx->d_w64, bits, (long long *)stats); ssh_count_launch();
     e = cudaGetLastError();
     *rc = e == cudaSuccess ? SSH_OK : ssh_cuda_fail(e, "sketch_poly_kernel", __FILE__, __LINE__);
     return true;

@@ -262,37 +262,33 @@ extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int
     const int ntiles = ssh_div_up(N, RS_TILE);
     ssh_index *ix = new ssh_index();
     ix->L = L; ix->N = N; ix->id_base = id_base; ix->device = ctx->device;
-    // scratch: keys A/B, rows A/B, hist
+    // scratch: keys A/B, rows B, hist (ctx slots, reused across builds); rows A = ix->ids
     size_t kbytes = sizeof(uint64_t) * (size_t)L * N;
     size_t rbytes = sizeof(uint32_t) * (size_t)L * N;
     size_t hbytes = sizeof(uint32_t) * (size_t)L * RS_BINS * ntiles;
-    size_t total = 2 * kbytes + rbytes + hbytes + 256;  // kA, kB, rB, hist
-    unsigned char *scr = nullptr;
     int rc = SSH_OK;
     cudaError_t e;
-    uint64_t *kA, *kB;
-    uint32_t *rA, *rB, *hist;
-    e = cudaMallocAsync((void **)&scr, total, st);
-    if (e != cudaSuccess) { delete ix; return ssh_cuda_fail(e, "cudaMallocAsync(index scratch)", __FILE__, __LINE__); }
+    uint64_t *kA = (uint64_t *)ssh_slot(ctx, SLOT_RS_KEYS_A, kbytes, st);
+    uint64_t *kB = (uint64_t *)ssh_slot(ctx, SLOT_RS_KEYS_B, kbytes, st);
+    uint32_t *rB = (uint32_t *)ssh_slot(ctx, SLOT_RS_ROWS_B, rbytes, st);
+    uint32_t *hist = (uint32_t *)ssh_slot(ctx, SLOT_RS_HIST, hbytes, st);
+    uint32_t *rA;
+    if (!kA || !kB || !rB || !hist) { delete ix; return SSH_ERR_OOM; }
     e = cudaMallocAsync((void **)&ix->ids, rbytes, st);
-    if (e != cudaSuccess) { cudaFreeAsync(scr, st); delete ix; return ssh_cuda_fail(e, "cudaMallocAsync(ids)", __FILE__, __LINE__); }
-    kA = (uint64_t *)scr;
-    kB = (uint64_t *)(scr + kbytes);
-    rB = (uint32_t *)(scr + 2 * kbytes);
-    hist = (uint32_t *)(scr + 2 * kbytes + rbytes);
+    if (e != cudaSuccess) { delete ix; return ssh_cuda_fail(e, "cudaMallocAsync(ids)", __FILE__, __LINE__); }
     rA = ix->ids;  // 8 passes (even): the sorted rows land back in rA = ix->ids
     {
         dim3 g((unsigned)ssh_div_up(N, 32), (unsigned)ssh_div_up(L, 32));
-        rs_transpose<<<g, 256, 0, st>>>(sig, N, L, kA, rA);
+        rs_transpose<<<g, 256, 0, st>>>(sig, N, L, kA, rA); ssh_count_launch();
     }
     uint64_t *kin = kA, *kout = kB;
     uint32_t *rin = rA, *rout = rB;
     dim3 grid((unsigned)ntiles, (unsigned)L);
     for (int pass = 0; pass < 8; pass++) {
         int shift = 8 * pass;
-        rs_hist<<<grid, RS_THREADS, 0, st>>>(kin, N, shift, ntiles, hist);
-        rs_scan<<<L, 1024, 0, st>>>(hist, ntiles);
-        rs_scatter<<<grid, RS_THREADS, 0, st>>>(kin, rin, N, shift, ntiles, hist, kout, rout);
+        rs_hist<<<grid, RS_THREADS, 0, st>>>(kin, N, shift, ntiles, hist); ssh_count_launch();
+        rs_scan<<<L, 1024, 0, st>>>(hist, ntiles); ssh_count_launch();
+        rs_scatter<<<grid, RS_THREADS, 0, st>>>(kin, rin, N, shift, ntiles, hist, kout, rout); ssh_count_launch();
         uint64_t *tk = kin; kin = kout; kout = tk;
         uint32_t *tr = rin; rin = rout; rout = tr;
     }
@@ -303,8 +299,8 @@ extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int
     e = cudaMallocAsync((void **)&ix->d_nb, sizeof(int64_t) * 2 * L, st);
     if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "cudaMallocAsync(nb)", __FILE__, __LINE__); goto fail; }
     ix->d_kbase = ix->d_nb + L;
-    rle_count<<<grid, RS_THREADS, 0, st>>>(kin, N, ntiles, hist);
-    rle_scan<<<L, 32, 0, st>>>(hist, ntiles, ix->d_nb);
+    rle_count<<<grid, RS_THREADS, 0, st>>>(kin, N, ntiles, hist); ssh_count_launch();
+    rle_scan<<<L, 32, 0, st>>>(hist, ntiles, ix->d_nb); ssh_count_launch();
     ix->h_nb = new int64_t[2 * L];
     ix->h_kbase = ix->h_nb + L;
     e = cudaMemcpyAsync(ix->h_nb, ix->d_nb, sizeof(int64_t) * L, cudaMemcpyDeviceToHost, st);
@@ -320,14 +316,13 @@ extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int
         if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "CSR allocation", __FILE__, __LINE__); goto fail; }
         rle_emit<<<grid, RS_THREADS, 0, st>>>(kin, N, ntiles, hist, ix->d_kbase, ix->d_nb,
                                               ix->keys, ix->offsets);
+        ssh_count_launch();
         e = cudaGetLastError();
         if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "rle_emit", __FILE__, __LINE__); goto fail; }
     }
-    cudaFreeAsync(scr, st);
     *out = ix;
     return SSH_OK;
 fail:
-    cudaFreeAsync(scr, st);
     cudaStreamSynchronize(st);
     ssh_index_destroy(ix);
     return rc;
@@ -341,6 +336,8 @@ extern "C" int ssh_index_destroy(ssh_index *ix) {
     cudaFree(ix->offsets);
     cudaFree(ix->ids);
     cudaFree(ix->d_nb);
+    cudaFree(ix->paa);
+    cudaFree(ix->d_maxabs);
     delete[] ix->h_nb;
     delete ix;
     return SSH_OK;

@@ -1,0 +1,105 @@
+"""Sharded index over the GPUs of one node (one process per GPU).
+
+The database shards by series id (contiguous ranges): every
+rank builds its own bucket tables over its rows with global ids, so the
+build needs no collective.  Queries are replicated; each rank answers the
+batch over its shard (R_g, exact local top-k by (d2, id)), and the global
+answer is the (d2, id) merge of the per-rank lists, which equals the exact
+top-k of R = U_g R_g.  The exchange is one all_gather of the per-rank top-k
+(d2 f64, id i64) and one all_reduce(sum) of |R_g| and the cascade counters,
+all batched over the whole query batch.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def init_from_env(backend: str = "nccl"):
+    """Initialise torch.distributed from RANK/WORLD_SIZE/MASTER_* if present."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
+    return rank, world, local
+
+
+def shard_range(N: int, rank: int, world: int):
+    """Contiguous id range [lo, hi) of `rank` (balanced to within one row)."""
+    base, extra = divmod(N, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def merge_topk_local(ids, d2, k: int):
+    """(d2, id)-lexicographic top-k of concatenated candidate lists.
+
+    ids/d2: (nq, C) tensors, id -1 / d2 inf for empty slots.  Returns
+    (ids (nq, k), d2 (nq, k), n (nq,))."""
+    torch = _torch()
+    big = torch.iinfo(torch.int64).max
+    idk = torch.where(ids < 0, torch.full_like(ids, big), ids)
+    o1 = torch.argsort(idk, dim=1, stable=True)
+    d2s = torch.gather(d2, 1, o1)
+    ids1 = torch.gather(ids, 1, o1)
+    o2 = torch.argsort(d2s, dim=1, stable=True)
+    d2o = torch.gather(d2s, 1, o2)[:, :k]
+    ido = torch.gather(ids1, 1, o2)[:, :k]
+    n = (ido >= 0).sum(dim=1).to(torch.int32)
+    return ido, d2o, n
+
+
+def merge_across_ranks(ids, d2, n_cand, counters, k: int, group=None):
+    """All-gather per-rank top-k and merge; all-reduce |R_g| and counters.
+
+    ids (nq, k) int64 global ids (-1 pad), d2 (nq, k) f64 (inf pad),
+    n_cand (nq,) int64, counters (nq, 5) int64 — all on the rank's device
+    (CPU tensors under gloo)."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if world == 1:
+        return ids, d2, n_cand, counters
+    nq = ids.shape[0]
+    g_ids = torch.empty((world * nq, k), dtype=ids.dtype, device=ids.device)
+    g_d2 = torch.empty((world * nq, k), dtype=d2.dtype, device=d2.device)
+    dist.all_gather_into_tensor(g_ids, ids.contiguous(), group=group)
+    dist.all_gather_into_tensor(g_d2, d2.contiguous(), group=group)
+    cat_ids = g_ids.view(world, nq, k).permute(1, 0, 2).reshape(nq, world * k)
+    cat_d2 = g_d2.view(world, nq, k).permute(1, 0, 2).reshape(nq, world * k)
+    red = torch.cat([n_cand.view(nq, 1), counters], dim=1).contiguous()
+    dist.all_reduce(red, op=dist.ReduceOp.SUM, group=group)
+    mids, md2, _ = merge_topk_local(cat_ids, cat_d2, k)
+    return mids, md2, red[:, 0].contiguous(), red[:, 1:].contiguous()
+
+
+def merge_numpy(parts, k: int):
+    """Reference merge for tests: parts = [(ids, d2)] per rank -> (ids, d2)."""
+    ids = np.concatenate([p[0] for p in parts], axis=1)
+    d2 = np.concatenate([p[1] for p in parts], axis=1)
+    out_i = np.full((ids.shape[0], k), -1, dtype=np.int64)
+    out_d = np.full((ids.shape[0], k), np.inf)
+    for q in range(ids.shape[0]):
+        sel = ids[q] >= 0
+        order = np.lexsort((ids[q][sel], d2[q][sel]))[:k]
+        out_i[q, :order.shape[0]] = ids[q][sel][order]
+        out_d[q, :order.shape[0]] = d2[q][sel][order]
+    return out_i, out_d

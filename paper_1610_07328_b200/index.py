@@ -348,8 +348,11 @@ def build_index(dataset, params: SshParams, normalized: bool = True, threads: in
     handle = ctypes.c_void_p()
     nat.check(nat.lib().ssh_index_build(ctx.handle, nat.ptr(sig), int(X.shape[0]), int(id_base),
                                         ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_build")
+    tables = _TablesHandle(handle)
+    nat.check(nat.lib().ssh_index_summarize(ctx.handle, handle, nat.ptr(X), int(X.stride(0)),
+                                            _stream_ptr(dev)), "ssh_index_summarize")
     return SshIndex(params=params, filter=ctx.filter, dataset=dataset, normalized=normalized,
-                    device=dev, X=X, sig_dev=sig, id_base=id_base, _tables=_TablesHandle(handle))
+                    device=dev, X=X, sig_dev=sig, id_base=id_base, _tables=tables)
 
 
 def compute_signatures(values, params: SshParams, weights=None, threads: int = 1, device=None):

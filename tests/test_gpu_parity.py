@@ -1,0 +1,362 @@
+"""Device parity: every stage of the CUDA path against the CPU oracle (itself
+pinned to the reference's golden vectors) and the golden digests.
+
+Bit-exact: sketch bits, shingle sets, CWS slot keys, signatures, bucket
+tables (CSR), candidate sets R.  Top-k: identical ids, squared distances
+bit-identical to the reference's f64 DTW (the device rescoring is exact)."""
+
+import ctypes
+import hashlib
+
+import numpy as np
+import pytest
+
+from fixture_data import CASES, case_data
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def csr_digest(tables):
+    h = hashlib.sha256()
+    for keys, offsets, ids in tables:
+        for b, key in enumerate(keys):
+            h.update(np.uint64(key).tobytes())
+            h.update(np.ascontiguousarray(ids[offsets[b]:offsets[b + 1]], dtype=np.int64).tobytes())
+        h.update(b"|")
+    return h.hexdigest()
+
+
+def params(band=0.05, K=4, **kw):
+    import paper_1610_07328_b200 as ssh
+
+    d = dict(W=80, delta=3, n=15, d=20, seed=0, band=band, K=K)
+    d.update(kw)
+    return ssh.SshParams(**d)
+
+
+def unpack_bits(words, nb):
+    b = np.unpackbits(words.view(np.uint8), axis=1, bitorder="little")[:, :nb]
+    return np.where(b > 0, 1, -1).astype(np.int8)
+
+
+def _stage_ctx(p, m):
+    from paper_1610_07328_b200.index import get_context
+
+    return get_context(0, p, m)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_sketch_bits_golden(cuda, golden, name):
+    import torch
+
+    from paper_1610_07328_b200 import _native as nat
+    from paper_1610_07328_b200.index import _stream_ptr
+
+    X, _, _, band = case_data(name)
+    p = params(band)
+    ctx = _stage_ctx(p, X.shape[1])
+    Xd = torch.from_numpy(X).cuda()
+    bits = torch.zeros((X.shape[0], ctx.words), dtype=torch.int64, device="cuda")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    nat.check(nat.lib().ssh_sketch(ctx.handle, nat.ptr(Xd), X.shape[0], X.shape[1], nat.ptr(bits),
+                                   nat.ptr(stats), _stream_ptr(0)))
+    got = unpack_bits(bits.cpu().numpy().view(np.uint64), ctx.nb)
+    assert sha(got) == golden["cases"][name]["bits_sha"]
+    assert int(stats[1]) == golden["cases"][name]["n_dot_below_1e9"]
+
+
+def test_sketch_recheck_near_zero(cuda):
+    """Windows whose dot is exactly 0 (sign(0) = +1) and tiny: the f32 screen
+    must defer to the exact f64 sequence."""
+    import torch
+
+    from paper_1610_07328_b200 import _native as nat
+    from paper_1610_07328_b200.index import _stream_ptr
+
+    p = params(0.05)
+    m = 512
+    ctx = _stage_ctx(p, m)
+    rng = np.random.default_rng(4)
+    X = np.zeros((64, m), dtype=np.float32)
+    X[1:20] = rng.standard_normal((19, m)).astype(np.float32) * 1e-3
+    X[20:40] = rng.standard_normal((20, m)).astype(np.float32)
+    X[40:] = (rng.integers(-2, 3, size=(24, m))).astype(np.float32)  # small integers: exact cancellations
+    Xd = torch.from_numpy(X).cuda()
+    bits = torch.zeros((64, ctx.words), dtype=torch.int64, device="cuda")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    nat.check(nat.lib().ssh_sketch(ctx.handle, nat.ptr(Xd), 64, m, nat.ptr(bits), nat.ptr(stats), _stream_ptr(0)))
+    got = unpack_bits(bits.cpu().numpy().view(np.uint64), ctx.nb)
+    want, dots = O.sketch_matrix(X, O.make_filter(80, 0), 3, return_dots=True)
+    assert np.array_equal(got, want)
+    assert got[0].tolist() == [1] * ctx.nb  # all-zero series: every dot is 0 -> +1
+    assert int(stats[1]) == int((np.abs(dots) < 1e-9).sum())
+
+
+@pytest.mark.parametrize("name", ["rw512", "rw2048"])
+def test_shingle_and_cws_stages(cuda, name):
+    import torch
+
+    from paper_1610_07328_b200 import _native as nat
+    from paper_1610_07328_b200.index import _stream_ptr
+
+    X, _, _, band = case_data(name)
+    p = params(band)
+    N, m = X.shape
+    ctx = _stage_ctx(p, m)
+    L = nat.lib()
+    st = _stream_ptr(0)
+    Xd = torch.from_numpy(X).cuda()
+    bits = torch.zeros((N, ctx.words), dtype=torch.int64, device="cuda")
+    nat.check(L.ssh_sketch(ctx.handle, nat.ptr(Xd), N, m, nat.ptr(bits), None, st))
+    T = ctx.T
+    tok = torch.zeros((N, T), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((N, T), dtype=torch.int16, device="cuda")
+    ln = torch.zeros(N, dtype=torch.int32, device="cuda")
+    nat.check(L.ssh_shingle(ctx.handle, nat.ptr(bits), N, nat.ptr(tok), nat.ptr(cnt), nat.ptr(ln), st))
+    S = p.K * p.d
+    keys = torch.zeros((N, S), dtype=torch.int64, device="cuda")
+    sig = torch.zeros((N, p.d), dtype=torch.int64, device="cuda")
+    nat.check(L.ssh_cws(ctx.handle, nat.ptr(tok), nat.ptr(cnt), nat.ptr(ln), N, nat.ptr(keys), nat.ptr(sig), st))
+    torch.cuda.synchronize()
+    obits = O.sketch_matrix(X, O.make_filter(80, 0), 3)
+    tabs = O.get_tables(15, S, 0, T)
+    tokh, cnth, lnh = tok.cpu().numpy().view(np.uint32), cnt.cpu().numpy().view(np.uint16), ln.cpu().numpy()
+    keysh = keys.cpu().numpy().view(np.uint64)
+    for i in range(0, N, max(1, N // 40)):
+        ot, oc = O.shingle(obits[i], 15)
+        D = int(lnh[i])
+        assert tokh[i, :D].tolist() == ot.tolist() and cnth[i, :D].tolist() == oc.tolist()
+        assert keysh[i].tolist() == O.cws_keys_tab(ot, oc, S, tabs).tolist()
+    osig = O.signatures(X, 80, 3, 15, 20, 4, 0, threads=8)
+    assert np.array_equal(sig.cpu().numpy().view(np.uint64), osig)
+
+
+def test_cws_large_counts(cuda, golden):
+    """Synthetic weighted sets with counts up to 699 through ssh_cws (count>1 path)."""
+    import torch
+
+    from paper_1610_07328_b200 import _native as nat
+    from paper_1610_07328_b200.index import _stream_ptr
+
+    p = params(0.10)
+    ctx = _stage_ctx(p, 2048)  # T = 643 slots per row
+    T = ctx.T
+    sets = [cw for cw in golden["cws"] if cw["seed"] == 0 and max(cw["counts"]) <= T and len(cw["tokens"]) <= T]
+    N = len(sets)
+    tok = np.zeros((N, T), dtype=np.uint32)
+    cnt = np.zeros((N, T), dtype=np.uint16)
+    ln = np.zeros(N, dtype=np.int32)
+    for i, cw in enumerate(sets):
+        D = len(cw["tokens"])
+        tok[i, :D] = cw["tokens"]
+        cnt[i, :D] = cw["counts"]
+        ln[i] = D
+    td, cd, ld = (torch.from_numpy(a.view(v)).cuda() for a, v in ((tok, np.int32), (cnt, np.int16), (ln, np.int32)))
+    keys = torch.zeros((N, 80), dtype=torch.int64, device="cuda")
+    sig = torch.zeros((N, 20), dtype=torch.int64, device="cuda")
+    nat.check(nat.lib().ssh_cws(ctx.handle, nat.ptr(td), nat.ptr(cd), nat.ptr(ld), N, nat.ptr(keys),
+                                nat.ptr(sig), _stream_ptr(0)))
+    got = keys.cpu().numpy().view(np.uint64)
+    for i, cw in enumerate(sets):
+        assert got[i].tolist() == cw["keys"]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("K", [1, 4])
+def test_build_index_golden(cuda, golden, name, K):
+    import paper_1610_07328_b200 as ssh
+
+    X, _, _, band = case_data(name)
+    c = golden["cases"][name]
+    idx = ssh.build_index(ssh.Dataset(X), params(band, K=K))
+    assert sha(idx.signatures) == c[f"sig_k{K}_sha"]
+    assert csr_digest([idx.table_csr(j) for j in range(20)]) == c[f"tables_k{K}_sha"]
+    assert [len(t) for t in idx.tables] == c[f"tables_k{K}_nbuckets"]
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("K", [1, 4])
+def test_query_golden(cuda, golden, name, K):
+    """ids and distances bit-identical to the reference's query_index."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data(name)
+    c = golden["cases"][name]
+    idx = ssh.build_index(ssh.Dataset(X), params(band, K=K))
+    res = ssh.query_index_batch(idx, Q, 10)
+    for qi, (r, g) in enumerate(zip(res, c[f"queries_k{K}"])):
+        assert r.status == g["status"]
+        assert r.stats.candidates == g["candidates"], qi
+        assert r.ids == g["ids"], qi
+        assert r.distances == g["distances"], qi
+        assert ssh.query_signature(idx, Q[qi]).tolist() == c[f"qsig_k{K}"][qi]
+
+
+def test_probe_candidates_exact(cuda):
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw512")
+    idx = ssh.build_index(ssh.Dataset(X), params(band, K=4))
+    oidx = O.build_index(X, 80, 3, 15, 20, 4, 0, band)
+    for q in Q[:6]:
+        qs = ssh.query_signature(idx, q)
+        got = ssh.probe_candidates(idx, qs)
+        want = []
+        for j, (ukeys, offsets, ids) in enumerate(oidx.csr):
+            b = np.searchsorted(ukeys, qs[j])
+            if b < len(ukeys) and ukeys[b] == qs[j]:
+                want.append(ids[offsets[b]:offsets[b + 1]])
+        want = np.unique(np.concatenate(want)) if want else np.empty(0, np.int64)
+        assert np.array_equal(got, want)
+
+
+def test_no_candidates_and_fallback(cuda, golden):
+    import paper_1610_07328_b200 as ssh
+
+    X, _, _, band = case_data("rw512")
+    idx = ssh.build_index(ssh.Dataset(X[:200]), params(band, K=1))
+    q = np.array(golden["empty"]["query"])
+    r0 = ssh.query_index(idx, q, 10)
+    assert r0.status == "no-candidates" and r0.ids == [] and r0.stats.candidates == 0
+    r1 = ssh.query_index(idx, q, 10, fallback_on_empty=True)
+    assert r1.status == "fallback"
+    assert r1.ids == golden["empty"]["fallback_ids"]
+    # the golden query is float64; the device path indexes/queries float32 values
+    np.testing.assert_allclose(r1.distances, golden["empty"]["fallback_distances"], rtol=1e-6)
+    q32 = q.astype(np.float32)
+    ids, d2 = O.brute_force_topk_over(X[:200], np.arange(200), q32, O.radius(band, 512), 10)
+    assert r1.ids == ids.tolist() and r1.distances == np.sqrt(d2).tolist()
+
+
+def test_k_larger_than_n_and_validation(cuda):
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw512")
+    idx = ssh.build_index(ssh.Dataset(X[:30]), params(band, K=1))
+    r = ssh.query_index(idx, X[3], 50)
+    assert r.warning and "exceeds index size 30" in r.warning
+    assert len(r.ids) == r.stats.candidates <= 30
+    assert r.ids[0] == 3 and r.distances[0] == 0.0  # self-retrieval
+    with pytest.raises(ValueError, match="does not match indexed length"):
+        ssh.query_index(idx, X[0, :100], 5)
+    with pytest.raises(ValueError, match="k must be >= 1"):
+        ssh.query_index(idx, X[0], 0)
+
+
+def test_duplicates_tie_break_by_id(cuda):
+    """Identical series -> identical distances; ties break toward the lower id."""
+    import paper_1610_07328_b200 as ssh
+
+    X, _, _, band = case_data("rw512")
+    base = X[:50].copy()
+    Xd = np.concatenate([base, base, base])  # ids i, i+50, i+100 identical
+    idx = ssh.build_index(ssh.Dataset(Xd), params(band, K=1))
+    oidx = O.build_index(Xd, 80, 3, 15, 20, 1, 0, band)
+    Q = np.stack([base[7], base[20] + 0.01])
+    res = ssh.query_index_batch(idx, Q, 10)
+    ores = O.query_batch(oidx, Q, 10)
+    for i, r in enumerate(res):
+        n = int(ores["n"][i])
+        assert r.ids == ores["ids"][i][:n].tolist()
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist()
+    assert res[0].ids[:3] == [7, 57, 107]
+
+
+def test_constant_and_edge_shapes(cuda):
+    """Flat (z-normalised to zero) series, N=1, and m == W (one sketch bit, n=1)."""
+    import paper_1610_07328_b200 as ssh
+
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal((40, 128)).astype(np.float32)
+    X[5] = 0.0
+    X[6] = 0.0
+    idx = ssh.build_index(ssh.Dataset(X), ssh.SshParams(W=16, delta=2, n=6, d=6, band=0.1, K=2))
+    oidx = O.build_index(X, 16, 2, 6, 6, 2, 0, 0.1)
+    assert np.array_equal(idx.signatures, oidx.sig)
+    r = ssh.query_index(idx, X[5], 3)
+    assert r.ids[:2] == [5, 6] and r.distances[:2] == [0.0, 0.0]
+    one = ssh.build_index(ssh.Dataset(X[:1]), ssh.SshParams(W=16, delta=2, n=6, d=6, band=0.1))
+    assert ssh.query_index(one, X[0], 5).ids == [0]
+    # m == W: N_B = 1, n must be 1
+    Y = rng.standard_normal((20, 30)).astype(np.float32)
+    p = ssh.SshParams(W=30, delta=5, n=1, d=4, band=0.2, K=1)
+    idy = ssh.build_index(ssh.Dataset(Y), p)
+    oy = O.build_index(Y, 30, 5, 1, 4, 1, 0, 0.2)
+    assert np.array_equal(idy.signatures, oy.sig)
+    ores = O.query_batch(oy, Y[:3], 4)
+    for i, r in enumerate(ssh.query_index_batch(idy, Y[:3], 4)):
+        n = int(ores["n"][i])
+        assert r.ids == ores["ids"][i][:n].tolist()
+
+
+@pytest.mark.parametrize("W,delta,n,band,K,d", [(30, 5, 15, 0.05, 1, 20), (30, 2, 10, 0.1, 2, 8),
+                                                 (17, 1, 12, 0.03, 3, 5)])
+def test_other_parameters_vs_oracle(cuda, W, delta, n, band, K, d):
+    """Non-default (W, delta) exercise the generic sketch kernel and other radii."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, _ = case_data("rw512")
+    X, Q = X[:400], Q[:5]
+    idx = ssh.build_index(ssh.Dataset(X), ssh.SshParams(W=W, delta=delta, n=n, d=d, band=band, K=K))
+    oidx = O.build_index(X, W, delta, n, d, K, 0, band)
+    assert np.array_equal(idx.signatures, oidx.sig)
+    ores = O.query_batch(oidx, Q, 10)
+    for i, r in enumerate(ssh.query_index_batch(idx, Q, 10)):
+        nn = int(ores["n"][i])
+        assert r.stats.candidates == int(ores["n_cand"][i])
+        assert r.ids == ores["ids"][i][:nn].tolist()
+        assert r.distances == np.sqrt(ores["d2"][i][:nn]).tolist()
+
+
+def test_dtw_exact_pairs(cuda, golden):
+    """ssh_dtw_exact == reference _dtw_band_sq bits (FMA-free f64)."""
+    import paper_1610_07328_b200 as ssh
+    from paper_1610_07328_b200.index import dtw_exact_pairs
+
+    X, Q, _, band = case_data("rw1024")
+    idx = ssh.build_index(ssh.Dataset(X), params(band, K=4))
+    rng = np.random.default_rng(2)
+    qrow = rng.integers(0, Q.shape[0], 64)
+    xrow = rng.integers(0, X.shape[0], 64)
+    got = dtw_exact_pairs(idx, Q, qrow, xrow)
+    r = O.radius(band, X.shape[1])
+    want = np.array([O.dtw_sq(X[b], Q[a], r) for a, b in zip(qrow, xrow)])
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.slow
+def test_full_scale_cfg1_sampled(cuda):
+    """configs[1] shape (N=1,000,000): sampled signature parity, the tables of
+    the device signatures, and 16 queries' top-10 against the oracle cascade."""
+    import torch
+
+    import paper_1610_07328_b200 as ssh
+    from paper_1610_07328_b200 import datagen
+
+    X, Q, src, p = datagen.workload(1, device="cuda", nq=16)
+    params_ = ssh.SshParams(**p)
+    idx = ssh.build_index(ssh.Dataset(X), params_)
+    res = ssh.query_index_batch(idx, Q, 10)
+    Xh = X.cpu().numpy()
+    sig = idx.signatures
+    rng = np.random.default_rng(0)
+    rows = rng.choice(Xh.shape[0], 10000, replace=False)
+    osig = O.signatures(Xh[rows], 80, 3, 15, 20, 4, 0, threads=16)
+    assert np.array_equal(sig[rows], osig)
+    # tables built on the device == reference table construction over the same signatures
+    ocsr = O.tables_from_signatures(sig)
+    for j in (0, 9, 19):
+        k, o, i = idx.table_csr(j)
+        assert np.array_equal(k, ocsr[j][0]) and np.array_equal(o, ocsr[j][1]) and np.array_equal(i, ocsr[j][2])
+    oidx = O.OracleIndex(Xh, 80, 3, 15, 20, 4, 0, p["band"], O.make_filter(80, 0), sig, ocsr)
+    ores = O.query_batch(oidx, Q, 10, threads=16)
+    for i, r in enumerate(res):
+        n = int(ores["n"][i])
+        assert r.stats.candidates == int(ores["n_cand"][i])
+        assert r.ids == ores["ids"][i][:n].tolist()
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist()
