@@ -598,6 +598,116 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
     }
 }
 
+// Register-resident band (radius R compile-time): band[k], k = j - i + R, lives
+// in registers and is updated in place k-ascending (diag = old band[k], up =
+// old band[k+1], left = new band[k-1]).  The query is staged in 4 copies
+// shifted by 0..3 samples so every LDS.128 (warp-uniform broadcast) feeds 4
+// cells; x_i is prefetched 4 rows at a time.  Per cell: FADD + FMNMX3 + FFMA
+// + 1/2 FMNMX3 (row min) + 1/4 LDS.128.
+template <int R>
+__global__ void __launch_bounds__(128)
+dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
+              const float *__restrict__ U, const float *__restrict__ Lo,
+              const uint32_t *__restrict__ list, int64_t list_stride,
+              const int *__restrict__ list_cnt, int cap, const float *__restrict__ thr,
+              float *__restrict__ out, unsigned long long *__restrict__ abandoned, int warps,
+              unsigned long long *__restrict__ cells) {
+    constexpr int NB = 2 * R + 1;
+    constexpr int NT = (NB + 3) / 4;
+    extern __shared__ __align__(16) float rsm[];
+    const int q = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int YP = ((m + 2 * R + 8) + 3) & ~3;
+    float *yc = rsm;           // 4 x YP
+    float *su = rsm + 4 * YP;  // m
+    float *sl = su + m;        // m
+    const float *y = Q + (int64_t)q * m;
+    for (int t = threadIdx.x; t < 4 * YP; t += blockDim.x) {
+        int c = t / YP, jj = (t - c * YP) + c - R;
+        yc[t] = (jj >= 0 && jj < m) ? y[jj] : INFINITY;
+    }
+    const float T = thr ? thr[q] : INFINITY;
+    const bool cb = !isinf(T) && U != nullptr;
+    if (cb)
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            su[i] = U[(int64_t)q * m + i];
+            sl[i] = Lo[(int64_t)q * m + i];
+        }
+    __syncthreads();
+    const int cnt = min(list_cnt ? list_cnt[q] : (int)list_stride, cap);
+    const int e = (blockIdx.x * warps + w) * 32 + lane;
+    if ((blockIdx.x * warps + w) * 32 >= cnt) return;
+    const uint32_t row = e < cnt ? list[(int64_t)q * list_stride + e] : 0xFFFFFFFFu;
+    const bool valid = row != 0xFFFFFFFFu;
+    const float *x = X + (int64_t)(valid ? row : 0) * m;
+    const bool vec = (m & 3) == 0;
+    float rem = 0.f, slack = 0.f;
+    if (cb) {
+        for (int i = 0; i < m; i++) {
+            float cv = x[i];
+            float v = fmaxf(fmaxf(cv - su[i], sl[i] - cv), 0.f);
+            rem = fmaf(v, v, rem);
+        }
+        slack = rem * (float)(2 * m + 8) * U32_EPS;
+    }
+    float band[NB];
+#pragma unroll
+    for (int k = 0; k < NB; k++) band[k] = INFINITY;
+    band[R] = 0.f;
+    bool alive = valid;
+    int rows = 0;
+    float4 xv = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < m; i++) {
+        if (!__any_sync(0xFFFFFFFFu, alive)) break;
+        rows += alive;
+        const int c = i & 3;
+        float xi;
+        if (vec) {
+            if (c == 0) xv = __ldg(reinterpret_cast<const float4 *>(x + i));
+            xi = c == 0 ? xv.x : c == 1 ? xv.y : c == 2 ? xv.z : xv.w;
+        } else {
+            xi = __ldg(x + i);
+        }
+        const float4 *yr = reinterpret_cast<const float4 *>(yc + c * YP + (i - c));
+        float left = INFINITY, diag = band[0], rmin = INFINITY;
+#pragma unroll
+        for (int t = 0; t < NT; t++) {
+            const float4 yv = yr[t];
+            const float ys[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int k = 4 * t + u;
+                if (k < NB) {
+                    const float up = (k + 1 < NB) ? band[k + 1] : INFINITY;
+                    const float d = xi - ys[u];
+                    const float cv = fmaf(d, d, fminf(fminf(diag, up), left));
+                    band[k] = cv;
+                    rmin = fminf(rmin, cv);
+                    left = cv;
+                    diag = up;
+                }
+            }
+        }
+        float bound = rmin;
+        if (cb) {
+            float v = fmaxf(fmaxf(xi - su[i], sl[i] - xi), 0.f);
+            rem = fmaf(-v, v, rem);
+            bound = rmin + fmaxf(rem - slack, 0.f);
+        }
+        if (alive && bound > T) alive = false;
+    }
+    if (e < cnt) {
+        out[(int64_t)q * list_stride + e] = (valid && alive) ? band[R] : INFINITY;
+        if (abandoned && valid && !alive) atomicAdd(&abandoned[q], 1ULL);
+    }
+    if (cells) {
+        unsigned long long cc = (unsigned long long)rows * (unsigned long long)NB;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cc += __shfl_xor_sync(0xFFFFFFFFu, cc, o);
+        if (lane == 0 && cc) atomicAdd(cells, cc);
+    }
+}
+
 // ------------------------------------------------------------ fp64 DTW
 // exact reference arithmetic (dtw.py:100-113): d = x - y; d = d*d; c = d + min(...)
 __global__ void dtw64_kernel(const float *__restrict__ X, int m, int r, const float *__restrict__ Q,
@@ -994,11 +1104,37 @@ size_t members_smem(int mode, int m, int nseg) {
 }
 }  // namespace
 
+template <int R>
+static int launch_dtw32r(ssh_ctx *ctx, const float *X, const float *Q, const float *U,
+                         const float *Lo, const uint32_t *list, int64_t stride, const int *cnt,
+                         int cap, int maxcnt, const float *thr, float *out,
+                         unsigned long long *aband, int nq, cudaStream_t st) {
+    const int m = ctx->p.m;
+    const int warps = 4;
+    const int YP = ((m + 2 * R + 8) + 3) & ~3;
+    size_t smem = (size_t)(4 * YP + 2 * m) * sizeof(float);
+    SSH_CUDA(cudaFuncSetAttribute(dtw32r_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (maxcnt <= 0) return SSH_OK;
+    dim3 grid((unsigned)ssh_div_up(maxcnt, 32 * warps), (unsigned)nq);
+    dtw32r_kernel<R><<<grid, 32 * warps, smem, st>>>(X, m, Q, U, Lo, list, stride, cnt, cap, thr, out,
+                                                     aband, warps, ctx->profile ? ctx->d_cells : nullptr);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
 static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const float *U,
                         const float *Lo, const uint32_t *list, int64_t stride, const int *cnt,
                         int cap, int maxcnt, const float *thr, float *out,
                         unsigned long long *aband, int nq, cudaStream_t st) {
     const int m = ctx->p.m, r = ctx->p.radius;
+#define DTWR(RR)                                                                                  \
+    case RR:                                                                                      \
+        return launch_dtw32r<RR>(ctx, X, Q, U, Lo, list, stride, cnt, cap, maxcnt, thr, out, aband, nq, st);
+    switch (r) {
+        DTWR(3) DTWR(6) DTWR(13) DTWR(26) DTWR(51)
+        default: break;
+    }
+#undef DTWR
     size_t smem;
     int warps = dtw32_warps(m, r, &smem);
     SSH_REQUIRE(smem <= 227 * 1024, SSH_ERR_UNSUPPORTED, "DTW band too wide (r=%d)", r);
