@@ -139,8 +139,8 @@ extern "C" int ssh_ctx_set_params(ssh_ctx *ctx, const ssh_params *p, const doubl
     int T = nb - p->n + 1;
     SSH_REQUIRE(max_count >= T, SSH_ERR_INVALID,
                 "ln_w table must cover counts up to %d (got max_count=%d)", T, max_count);
-    SSH_REQUIRE(T <= 4096, SSH_ERR_UNSUPPORTED,
-                "tokens per series %d exceeds the device limit 4096 (series too long)", T);
+    SSH_REQUIRE(T <= 4095, SSH_ERR_UNSUPPORTED,
+                "tokens per series %d exceeds the device limit 4095 (series too long)", T);
     SSH_CUDA(cudaSetDevice(ctx->device));
     free_tables(ctx);
     ctx->have_params = false;

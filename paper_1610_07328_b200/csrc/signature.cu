@@ -1,22 +1,29 @@
 // signature.cu — K2 shingle + K3 consistent weighted sampling (one warp per series).
 //
 // K2 (shingle.py:56-75, index.py:118): tokens t_i = bits[i..i+n-1] with the
-// first bit most significant, then the distinct tokens ascending with their
-// counts (np.unique(return_counts=True)).  A warp extracts its series' T
-// tokens from the packed bit row (word shuffles + __brev), bitonic-sorts
-// them in shared memory and run-length encodes with ballots.
+// first bit most significant, and their multiplicities.  A warp extracts its
+// series' T tokens from the packed bit row (word shuffles + __brev) and
+// counts them in a per-warp shared-memory hash set (atomicCAS/atomicAdd),
+// then compacts the distinct (token, count) pairs with ballots.  The stage
+// API (ssh_shingle) additionally bitonic-sorts them to reproduce
+// np.unique's ascending order; the fused build path does not need the order.
 //
 // K3 (wmh.py:52-81 + signature(concat=K) wmh.py:107-125): for every slot s
 // of S = K*L, argmin over the distinct tokens of
 //     ln_a = ln_c - r*(floor(ln_w/r + beta) - beta) - r
-// (first occurrence = lowest token on ties), key = mix64(tok ^ mix64(t ^ SALT_KEY)),
-// then the K-fold acc = mix64(acc ^ key).  The variates come from host tables
-// (np.log bits); the device does only IEEE div/add/sub/mul/floor in the
-// reference order with explicit _rn intrinsics, so keys are bit-exact.
-// Count-1 tokens (76-84% of all) use the precomputed ln_a1 table (one 8-byte
-// gather per (token, slot)); larger counts evaluate the full formula.
+// with ties broken toward the lowest token (np.argmin's first occurrence over
+// the sorted tokens), key = mix64(tok ^ mix64(t ^ SALT_KEY)), then the K-fold
+// acc = mix64(acc ^ key).  The variates come from host tables (np.log bits);
+// the device does only IEEE operations in the reference order with explicit
+// _rn intrinsics, so keys are bit-exact:
+//   * count-1 tokens (76-84% of all) read the precomputed ln_a1 table;
+//   * larger counts need t = floor(fl(fl(ln_w / r) + beta)).  It is taken from
+//     an approximate quotient (rcp.approx + two Newton steps, relative error
+//     < 2^-48) whenever that sum is farther than 1e-12 (relative) from an
+//     integer, which pins the floor; otherwise the exact IEEE division is
+//     evaluated.  ln_y and ln_a then follow with _rn operations.
 // Lanes own slots s = lane + 32*i, so every gather is a contiguous 256-byte
-// segment of the [token][slot] table (L2-resident: 2^15 x 80 x 8 B = 21 MB).
+// segment of the [token][slot] tables (L2-resident: 2^15 x 80 x 8 B = 21 MB).
 #include <float.h>
 
 #include <algorithm>
@@ -24,7 +31,7 @@
 #include "common.cuh"
 
 #define SG_WARPS 8
-#define SG_NS_MAX (SSH_MAX_SLOTS / 32)
+#define SG_EMPTY 0xFFFFFFFFu
 
 struct SigArgs {
     const uint64_t *bits;
@@ -38,7 +45,7 @@ struct SigArgs {
     uint64_t *sig_out;
     const double *lna1, *tr, *tlnc, *tbeta, *lnw;
     int64_t N;
-    int words, nb, n, T, P2, S, L, K;
+    int words, nb, n, T, P2, H, S, L, K;
     int warp_smem;  // bytes per warp
 };
 
@@ -65,47 +72,186 @@ int ssh_launch_lna1(ssh_ctx *ctx, cudaStream_t st) {
 }
 
 struct WarpSmem {
-    uint32_t *sortbuf;  // P2
-    uint32_t *utok;     // T
-    uint16_t *ucnt;     // T
-    uint16_t *ustart;   // T+1
-    uint16_t *list1;    // T  indices of count-1 tokens
-    uint16_t *listm;    // T  indices of count>1 tokens
     uint64_t *keys;     // S
+    uint32_t *hkey;     // H   (hash set; aliases the sort buffer)
+    uint32_t *hcnt;     // H
+    uint32_t *sortbuf;  // P2  (ssh_shingle only)
+    uint32_t *utok;     // T   distinct tokens (stage API)
+    uint32_t *ukey;     // T   packed (token << 12 | count), aliases utok
+    uint16_t *ucnt;     // T
+    uint16_t *ustart;   // T+1 (ssh_shingle only)
 };
+
+__host__ __device__ __forceinline__ int warp_smem_bytes(int S, int P2, int H, int T) {
+    int region = 8 * H > 4 * P2 ? 8 * H : 4 * P2;
+    int b = 8 * S + region + 4 * T + 2 * T + 2 * (T + 1);
+    return (b + 15) & ~15;
+}
 
 __device__ __forceinline__ WarpSmem carve(unsigned char *base, const SigArgs &a) {
     WarpSmem w;
     unsigned char *p = base;
     w.keys = reinterpret_cast<uint64_t *>(p); p += 8 * a.S;
-    w.sortbuf = reinterpret_cast<uint32_t *>(p); p += 4 * a.P2;
+    w.hkey = reinterpret_cast<uint32_t *>(p);
+    w.hcnt = w.hkey + a.H;
+    w.sortbuf = w.hkey;
+    p += (8 * a.H > 4 * a.P2) ? 8 * a.H : 4 * a.P2;
     w.utok = reinterpret_cast<uint32_t *>(p); p += 4 * a.T;
+    w.ukey = w.utok;
     w.ucnt = reinterpret_cast<uint16_t *>(p); p += 2 * a.T;
-    w.ustart = reinterpret_cast<uint16_t *>(p); p += 2 * (a.T + 1);
-    w.list1 = reinterpret_cast<uint16_t *>(p); p += 2 * a.T;
-    w.listm = reinterpret_cast<uint16_t *>(p);
+    w.ustart = reinterpret_cast<uint16_t *>(p);
     return w;
 }
 
-// Tokens of one series -> distinct sorted tokens + counts in smem; returns D.
-__device__ int warp_shingle(const SigArgs &a, int64_t row, const WarpSmem &w, int lane) {
-    const uint64_t *brow = a.bits + row * a.words;
-    uint64_t myword = lane < a.words ? brow[lane] : 0ULL;
-    const uint32_t nmask = (a.n == 32) ? 0xFFFFFFFFu : ((1u << a.n) - 1u);
+// token i of the packed bit row: bits i..i+n-1, first bit most significant
+__device__ __forceinline__ uint32_t token_at(uint64_t myword, int i, int words, int n) {
+    const int wi = min(i >> 6, 31);
+    const int sh = i & 63;
+    uint64_t w0 = __shfl_sync(0xFFFFFFFFu, myword, wi);
+    uint64_t w1 = __shfl_sync(0xFFFFFFFFu, myword, min(wi + 1, 31));
+    if (wi + 1 >= words) w1 = 0ULL;
+    uint64_t v = sh ? ((w0 >> sh) | (w1 << (64 - sh))) : w0;
+    const uint32_t nmask = (n == 32) ? 0xFFFFFFFFu : ((1u << n) - 1u);
+    return __brev((uint32_t)v & nmask) >> (32 - n);
+}
+
+// Warp bitonic sort of 32*V u32 keys held V per lane (element e = lane*V + v).
+template <int V>
+__device__ __forceinline__ void warp_sort_regs(uint32_t (&x)[V], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * V; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= V) {
+                const int lj = j / V;
+                const bool lower = (lane & lj) == 0;
+#pragma unroll
+                for (int v = 0; v < V; v++) {
+                    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x[v], lj);
+                    const bool up = ((lane * V + v) & k) == 0;
+                    x[v] = (lower == up) ? min(x[v], y) : max(x[v], y);
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < V; v++) {
+                    if ((v & j) == 0) {
+                        const bool up = ((lane * V + v) & k) == 0;
+                        const uint32_t p = x[v], q = x[v + j];
+                        x[v] = up ? min(p, q) : max(p, q);
+                        x[v + j] = up ? max(p, q) : min(p, q);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void sort_keys_regs(uint32_t *keys, int D, int lane) {
+    uint32_t x[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        const int e = lane * V + v;
+        x[v] = e < D ? keys[e] : 0xFFFFFFFFu;
+    }
+    __syncwarp();
+    warp_sort_regs<V>(x, lane);
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        const int e = lane * V + v;
+        if (e < D) keys[e] = x[v];
+    }
+    __syncwarp();
+}
+
+// ascending sort of D packed keys in smem (buf: scratch of P2 >= D entries)
+__device__ void sort_keys(uint32_t *keys, int D, uint32_t *buf, int P2, int lane) {
+    if (D <= 1) return;
+    if (D <= 32) { sort_keys_regs<1>(keys, D, lane); return; }
+    if (D <= 64) { sort_keys_regs<2>(keys, D, lane); return; }
+    if (D <= 128) { sort_keys_regs<4>(keys, D, lane); return; }
+    if (D <= 256) { sort_keys_regs<8>(keys, D, lane); return; }
+    int P = 512;
+    while (P < D) P <<= 1;
+    for (int e = lane; e < P; e += 32) buf[e] = e < D ? keys[e] : 0xFFFFFFFFu;
+    __syncwarp();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int idx = lane; idx < (P >> 1); idx += 32) {
+                int i = 2 * idx - (idx & (j - 1));
+                int l = i + j;
+                uint32_t x = buf[i], y = buf[l];
+                bool up = (i & k) == 0;
+                if ((x > y) == up) {
+                    buf[i] = y;
+                    buf[l] = x;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    for (int e = lane; e < D; e += 32) keys[e] = buf[e];
+    __syncwarp();
+}
+
+// Distinct tokens + counts via the per-warp hash set, as packed keys
+// (token << 12 | count) sorted ascending (= np.unique order); returns D.
+// The hash table is left empty again for the next series.
+__device__ int warp_dedup(const SigArgs &a, int64_t row, const WarpSmem &w, int lane) {
+    const uint64_t myword = lane < a.words ? a.bits[row * a.words + lane] : 0ULL;
+    const uint32_t hmask = (uint32_t)a.H - 1u;
+    const unsigned lt0 = (1u << lane) - 1u;
+    for (int base = 0; base < a.T; base += 32) {
+        const int i = base + lane;
+        const uint32_t t0 = token_at(myword, i, a.words, a.n);  // all lanes shuffle
+        const uint32_t tok = i < a.T ? t0 : SG_EMPTY;
+        // identical tokens of this round insert once (runs are common)
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, tok);
+        if (tok != SG_EMPTY && (peers & lt0) == 0) {
+            const uint32_t add = __popc(peers);
+            uint32_t h = (tok * 0x9E3779B1u) & hmask;
+            while (true) {
+                uint32_t prev = atomicCAS(&w.hkey[h], SG_EMPTY, tok);
+                if (prev == SG_EMPTY || prev == tok) {
+                    atomicAdd(&w.hcnt[h], add);
+                    break;
+                }
+                h = (h + 1) & hmask;
+            }
+        }
+    }
+    __syncwarp();
+    int D = 0;
+    for (int base = 0; base < a.H; base += 32) {
+        const int h = base + lane;
+        const uint32_t k = w.hkey[h];
+        const bool occ = k != SG_EMPTY;
+        const unsigned msk = __ballot_sync(0xFFFFFFFFu, occ);
+        if (occ) {
+            w.ukey[D + __popc(msk & lt0)] = (k << 12) | w.hcnt[h];
+            w.hkey[h] = SG_EMPTY;
+            w.hcnt[h] = 0u;
+        }
+        D += __popc(msk);
+    }
+    __syncwarp();
+    sort_keys(w.ukey, D, w.hkey, a.H, lane);
+    if (D > 256) {  // the smem sort used the hash table as scratch
+        for (int h = lane; h < a.H; h += 32) w.hkey[h] = SG_EMPTY;
+        __syncwarp();
+    }
+    return D;
+}
+
+// Sorted distinct tokens + counts (np.unique order) for the stage API; returns D.
+__device__ int warp_shingle_sorted(const SigArgs &a, int64_t row, const WarpSmem &w, int lane) {
+    const uint64_t myword = lane < a.words ? a.bits[row * a.words + lane] : 0ULL;
     for (int base = 0; base < a.P2; base += 32) {
-        int i = base + lane;
-        int wi = min(i >> 6, 31);
-        int sh = i & 63;
-        uint64_t w0 = __shfl_sync(0xFFFFFFFFu, myword, wi);
-        uint64_t w1 = __shfl_sync(0xFFFFFFFFu, myword, min(wi + 1, 31));
-        if (wi + 1 >= a.words) w1 = 0ULL;
-        uint64_t v = sh ? ((w0 >> sh) | (w1 << (64 - sh))) : w0;
-        uint32_t fwd = (uint32_t)v & nmask;                  // bit j = sketch bit i+j
-        uint32_t tok = __brev(fwd) >> (32 - a.n);             // first bit most significant
+        const int i = base + lane;
+        const uint32_t tok = token_at(myword, i, a.words, a.n);
         w.sortbuf[i] = i < a.T ? tok : 0xFFFFFFFFu;
     }
     __syncwarp();
-    // bitonic sort (ascending) of P2 entries
     for (int k = 2; k <= a.P2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int idx = lane; idx < (a.P2 >> 1); idx += 32) {
@@ -121,7 +267,6 @@ __device__ int warp_shingle(const SigArgs &a, int64_t row, const WarpSmem &w, in
             __syncwarp();
         }
     }
-    // run-length encode
     int D = 0;
     const unsigned lt = (1u << lane) - 1u;
     for (int base = 0; base < a.T; base += 32) {
@@ -143,110 +288,150 @@ __device__ int warp_shingle(const SigArgs &a, int64_t row, const WarpSmem &w, in
         w.ucnt[d] = (uint16_t)(e - w.ustart[d]);
     }
     __syncwarp();
+    // restore the hash-set invariant (sortbuf aliases it)
+    for (int h = lane; h < a.H; h += 32) {
+        w.hkey[h] = SG_EMPTY;
+        w.hcnt[h] = 0u;
+    }
+    __syncwarp();
     return D;
 }
 
-__device__ __forceinline__ void upd(double v, int d, double &best, int &bd) {
-    if (v < best || (v == best && d < bd)) {
-        best = v;
+// t = floor(fl(fl(lw / r) + b)) exactly (see header): approximate quotient,
+// exact IEEE division only when the sum is within 1e-12 of an integer.
+__device__ __forceinline__ double cws_t(double lw, double r, double b) {
+    double rc;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(r));
+    double e = fma(-r, rc, 1.0);
+    rc = fma(rc, e, rc);
+    e = fma(-r, rc, 1.0);
+    rc = fma(rc, e, rc);
+    const double s1 = fma(lw, rc, b);
+    const double fl = floor(s1);
+    const double tol = s1 * 1e-12;
+    if (s1 - fl > tol && (fl + 1.0) - s1 > tol) return fl;
+    return floor(__dadd_rn(__ddiv_rn(lw, r), b));
+}
+
+__device__ __forceinline__ double cws_lna(double t, double r, double lnc, double b) {
+    const double lny = __dmul_rn(r, __dsub_rn(t, b));
+    return __dsub_rn(__dsub_rn(lnc, lny), r);
+}
+
+// argmin over the D distinct tokens (packed keys in ascending token order),
+// K-fold, signature row.  Count-1 and count>1 tokens run in separate
+// branch-free loops (index lists keep ascending order); the count-1 loop keeps
+// U independent min-chains per slot so the compare/select chain does not
+// serialise on latency.  Chains are merged by (value, index): ties go to the
+// lower index = lower token, i.e. np.argmin's first occurrence.
+__device__ __forceinline__ void take_min(double v, int d, double &bv, int &bd) {
+    if (v < bv || (v == bv && d < bd)) {
+        bv = v;
         bd = d;
     }
 }
 
-// CWS argmin over the D distinct tokens in smem, K-fold, write signature row.
+template <int NS>
 __device__ void warp_cws(const SigArgs &a, int64_t row, const WarpSmem &w, int D, int lane) {
+    constexpr int U = 4;
     const int S = a.S;
-    const int NS = (S + 31) >> 5;
-    // split count-1 / count>1 token indices (ascending)
+    // split indices: count-1 into list1 (ustart storage), count>1 into listm (ucnt storage)
+    uint16_t *list1 = w.ustart;
+    uint16_t *listm = w.ucnt;
     int n1 = 0, nm = 0;
     const unsigned lt = (1u << lane) - 1u;
     for (int base = 0; base < D; base += 32) {
-        int d = base + lane;
-        bool valid = d < D;
-        bool one = valid && w.ucnt[d] == 1;
-        bool many = valid && !one;
-        unsigned m1 = __ballot_sync(0xFFFFFFFFu, one);
-        unsigned mm = __ballot_sync(0xFFFFFFFFu, many);
-        if (one) w.list1[n1 + __popc(m1 & lt)] = (uint16_t)d;
-        if (many) w.listm[nm + __popc(mm & lt)] = (uint16_t)d;
+        const int d = base + lane;
+        const uint32_t key = d < D ? w.ukey[d] : 0u;
+        const bool one = d < D && (key & 0xFFFu) == 1u;
+        const bool many = d < D && (key & 0xFFFu) > 1u;
+        const unsigned m1 = __ballot_sync(0xFFFFFFFFu, one);
+        const unsigned mm = __ballot_sync(0xFFFFFFFFu, many);
+        if (one) list1[n1 + __popc(m1 & lt)] = (uint16_t)d;
+        if (many) listm[nm + __popc(mm & lt)] = (uint16_t)d;
         n1 += __popc(m1);
         nm += __popc(mm);
     }
     __syncwarp();
-    double best[SG_NS_MAX];
-    int bd[SG_NS_MAX];
+    double best[U][NS];
+    int bd[U][NS];
 #pragma unroll
-    for (int i = 0; i < SG_NS_MAX; i++) {
-        best[i] = (double)INFINITY;
-        bd[i] = 0x7FFFFFFF;
-    }
-    // count-1 tokens: one gather of the precomputed ln_a1 per (token, slot)
-    int e = 0;
-    for (; e + 4 <= n1; e += 4) {
-        int d0 = w.list1[e], d1 = w.list1[e + 1], d2 = w.list1[e + 2], d3 = w.list1[e + 3];
-        const double *p0 = a.lna1 + (size_t)w.utok[d0] * S;
-        const double *p1 = a.lna1 + (size_t)w.utok[d1] * S;
-        const double *p2 = a.lna1 + (size_t)w.utok[d2] * S;
-        const double *p3 = a.lna1 + (size_t)w.utok[d3] * S;
+    for (int u = 0; u < U; u++)
 #pragma unroll
-        for (int i = 0; i < SG_NS_MAX; i++) {
-            if (i < NS) {
-                int s = lane + 32 * i;
-                if (s < S) {
-                    double v0 = __ldg(p0 + s), v1 = __ldg(p1 + s), v2 = __ldg(p2 + s),
-                           v3 = __ldg(p3 + s);
-                    upd(v0, d0, best[i], bd[i]);
-                    upd(v1, d1, best[i], bd[i]);
-                    upd(v2, d2, best[i], bd[i]);
-                    upd(v3, d3, best[i], bd[i]);
-                }
+        for (int i = 0; i < NS; i++) {
+            best[u][i] = (double)INFINITY;
+            bd[u][i] = 0x7FFFFFFF;
+        }
+    // count-1 tokens: one ln_a1 gather per (token, slot), U chains
+    for (int e0 = 0; e0 < n1; e0 += U) {
+        int dd[U];
+        double va[U][NS];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const bool ok = e0 + u < n1;
+            dd[u] = ok ? list1[e0 + u] : 0;
+            const size_t base = (size_t)(w.ukey[dd[u]] >> 12) * S;
+#pragma unroll
+            for (int i = 0; i < NS; i++) {
+                const int s = lane + 32 * i;
+                va[u][i] = (ok && s < S) ? __ldg(a.lna1 + base + s) : (double)INFINITY;
             }
         }
-    }
-    for (; e < n1; e++) {
-        int d0 = w.list1[e];
-        const double *p0 = a.lna1 + (size_t)w.utok[d0] * S;
 #pragma unroll
-        for (int i = 0; i < SG_NS_MAX; i++) {
-            int s = lane + 32 * i;
-            if (i < NS && s < S) upd(__ldg(p0 + s), d0, best[i], bd[i]);
-        }
+        for (int u = 0; u < U; u++)
+#pragma unroll
+            for (int i = 0; i < NS; i++) {
+                const bool l = va[u][i] < best[u][i];
+                best[u][i] = l ? va[u][i] : best[u][i];
+                bd[u][i] = l ? dd[u] : bd[u][i];
+            }
     }
-    // count>1 tokens: full formula, reference op order (wmh.py:74-76)
+    // count>1 tokens: full formula (wmh.py:74-76), one more chain
+    double bestm[NS];
+    int bdm[NS];
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+        bestm[i] = (double)INFINITY;
+        bdm[i] = 0x7FFFFFFF;
+    }
     for (int f = 0; f < nm; f++) {
-        int d0 = w.listm[f];
-        size_t base = (size_t)w.utok[d0] * S;
-        double lw = __ldg(a.lnw + w.ucnt[d0]);
+        const int d = listm[f];
+        const uint32_t key = w.ukey[d];
+        const size_t base = (size_t)(key >> 12) * S;
+        const double lw = __ldg(a.lnw + (key & 0xFFFu));
 #pragma unroll
-        for (int i = 0; i < SG_NS_MAX; i++) {
-            int s = lane + 32 * i;
-            if (i < NS && s < S) {
-                double r = __ldg(a.tr + base + s);
-                double lnc = __ldg(a.tlnc + base + s);
-                double b = __ldg(a.tbeta + base + s);
-                double t = floor(__dadd_rn(__ddiv_rn(lw, r), b));
-                double lny = __dmul_rn(r, __dsub_rn(t, b));
-                double v = __dsub_rn(__dsub_rn(lnc, lny), r);
-                upd(v, d0, best[i], bd[i]);
+        for (int i = 0; i < NS; i++) {
+            const int s = lane + 32 * i;
+            if (s < S) {
+                const double r = __ldg(a.tr + base + s);
+                const double lnc = __ldg(a.tlnc + base + s), b = __ldg(a.tbeta + base + s);
+                const double v = cws_lna(cws_t(lw, r, b), r, lnc, b);
+                const bool l = v < bestm[i];  // ascending indices: strict < keeps the first
+                bestm[i] = l ? v : bestm[i];
+                bdm[i] = l ? d : bdm[i];
             }
         }
     }
-    // winners -> keys (wmh.py:79-81)
+    // merge chains, winners -> keys (wmh.py:79-81)
 #pragma unroll
-    for (int i = 0; i < SG_NS_MAX; i++) {
-        int s = lane + 32 * i;
-        if (i < NS && s < S) {
-            int d0 = bd[i];
-            uint32_t tok = w.utok[d0];
-            int c = w.ucnt[d0];
-            size_t ent = (size_t)tok * S + s;
-            double b = __ldg(a.tbeta + ent);
-            double r = __ldg(a.tr + ent);
-            double t = floor(__dadd_rn(__ddiv_rn(__ldg(a.lnw + c), r), b));
-            uint64_t tt = (uint64_t)(int64_t)t;
-            uint64_t key = ssh_mix64((uint64_t)tok ^ ssh_mix64(tt ^ SSH_SALT_KEY));
-            w.keys[s] = key;
-            if (a.keys_out) a.keys_out[row * S + s] = key;
+    for (int i = 0; i < NS; i++) {
+        const int s = lane + 32 * i;
+        double bv = bestm[i];
+        int bi = bdm[i];
+#pragma unroll
+        for (int u = 0; u < U; u++) take_min(best[u][i], bd[u][i], bv, bi);
+        if (s < S && D > 0) {
+            const uint32_t key = w.ukey[bi];
+            const uint32_t tok = key >> 12, cnt = key & 0xFFFu;
+            const size_t ent = (size_t)tok * S + s;
+            const double b = __ldg(a.tbeta + ent);
+            double t;
+            if (cnt == 1u) t = floor(b);  // fl(0/r + b) = b
+            else t = cws_t(__ldg(a.lnw + cnt), __ldg(a.tr + ent), b);
+            const uint64_t tt = (uint64_t)(int64_t)t;
+            const uint64_t k64 = ssh_mix64((uint64_t)tok ^ ssh_mix64(tt ^ SSH_SALT_KEY));
+            w.keys[s] = k64;
+            if (a.keys_out) a.keys_out[row * S + s] = k64;
         }
     }
     __syncwarp();
@@ -258,24 +443,29 @@ __device__ void warp_cws(const SigArgs &a, int64_t row, const WarpSmem &w, int D
     __syncwarp();
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(32 * SG_WARPS) shingle_cws_kernel(SigArgs a) {
+template <int MODE, int NS>
+__global__ void __launch_bounds__(32 * SG_WARPS, 3) shingle_cws_kernel(SigArgs a, int warps) {
     extern __shared__ __align__(16) unsigned char sg_smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     WarpSmem w = carve(sg_smem + (size_t)wid * a.warp_smem, a);
-    const int64_t nwarps = (int64_t)gridDim.x * SG_WARPS;
-    for (int64_t row = (int64_t)blockIdx.x * SG_WARPS + wid; row < a.N; row += nwarps) {
+    for (int h = lane; h < a.H; h += 32) {
+        w.hkey[h] = SG_EMPTY;
+        w.hcnt[h] = 0u;
+    }
+    __syncwarp();
+    const int64_t nwarps = (int64_t)gridDim.x * warps;
+    for (int64_t row = (int64_t)blockIdx.x * warps + wid; row < a.N; row += nwarps) {
         int D;
         if (MODE == SIG_MODE_CWS_FROM_SETS) {
             D = a.len_in[row];
-            for (int d = lane; d < D; d += 32) {
-                w.utok[d] = a.tok_in[row * a.T + d];
-                w.ucnt[d] = a.cnt_in[row * a.T + d];
-            }
+            for (int d = lane; d < D; d += 32)
+                w.ukey[d] = (a.tok_in[row * a.T + d] << 12) | (uint32_t)a.cnt_in[row * a.T + d];
             __syncwarp();
+        } else if (MODE == SIG_MODE_SHINGLE) {
+            D = warp_shingle_sorted(a, row, w, lane);
         } else {
-            D = warp_shingle(a, row, w, lane);
+            D = warp_dedup(a, row, w, lane);
         }
         if (MODE == SIG_MODE_SHINGLE) {
             for (int d = lane; d < a.T; d += 32) {
@@ -285,8 +475,43 @@ __global__ void __launch_bounds__(32 * SG_WARPS) shingle_cws_kernel(SigArgs a) {
             if (lane == 0) a.len_out[row] = D;
             __syncwarp();
         } else {
-            warp_cws(a, row, w, D, lane);
+            warp_cws<NS>(a, row, w, D, lane);
         }
+    }
+}
+
+template <int MODE, int NS>
+static int launch_sig(ssh_ctx *ctx, const SigArgs &a, int64_t N, cudaStream_t st) {
+    auto kern = shingle_cws_kernel<MODE, NS>;
+    int warps = SG_WARPS;
+    while (warps > 1 && (size_t)a.warp_smem * warps > 200 * 1024) warps--;
+    size_t smem = (size_t)a.warp_smem * warps;
+    SSH_REQUIRE(smem <= 220 * 1024, SSH_ERR_UNSUPPORTED,
+                "signature kernel needs %zu bytes of shared memory (T=%d)", smem, a.T);
+    SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t nblk = (N + warps - 1) / warps;
+    const int grid = (int)std::min<int64_t>(nblk, (int64_t)ctx->num_sms * per_sm);
+    kern<<<grid, 32 * warps, smem, st>>>(a, warps);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
+template <int MODE>
+static int launch_sig_ns(ssh_ctx *ctx, const SigArgs &a, int64_t N, cudaStream_t st) {
+    switch ((a.S + 31) / 32) {
+        case 1: return launch_sig<MODE, 1>(ctx, a, N, st);
+        case 2: return launch_sig<MODE, 2>(ctx, a, N, st);
+        case 3: return launch_sig<MODE, 3>(ctx, a, N, st);
+        case 4: return launch_sig<MODE, 4>(ctx, a, N, st);
+        case 5: return launch_sig<MODE, 5>(ctx, a, N, st);
+        case 6: return launch_sig<MODE, 6>(ctx, a, N, st);
+        case 7: return launch_sig<MODE, 7>(ctx, a, N, st);
+        default: return launch_sig<MODE, 8>(ctx, a, N, st);
     }
 }
 
@@ -304,29 +529,10 @@ int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *t
     int P2 = 32;
     while (P2 < ctx->T) P2 <<= 1;
     a.P2 = P2;
+    a.H = P2;  // D <= T <= P2/2 + 1: load factor <= ~1/2
     a.S = ctx->S; a.L = ctx->p.L; a.K = ctx->p.K;
-    int ws = 8 * a.S + 4 * P2 + 4 * a.T + 2 * a.T + 2 * (a.T + 1) + 2 * a.T + 2 * a.T;
-    ws = (ws + 15) & ~15;
-    a.warp_smem = ws;
-    size_t smem = (size_t)ws * SG_WARPS;
-    SSH_REQUIRE(smem <= 220 * 1024, SSH_ERR_UNSUPPORTED,
-                "signature kernel needs %zu bytes of shared memory (T=%d)", smem, a.T);
-    int per_sm = 1;
-    int64_t nblk = (N + SG_WARPS - 1) / SG_WARPS;
-#define LAUNCH_SIG(MODE_)                                                                     \
-    do {                                                                                      \
-        auto kern = shingle_cws_kernel<MODE_>;                                                \
-        SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                      (int)smem));                                            \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * SG_WARPS, smem);    \
-        if (per_sm < 1) per_sm = 1;                                                           \
-        int grid = (int)std::min<int64_t>(nblk, (int64_t)ctx->num_sms * per_sm);                   \
-        kern<<<grid, 32 * SG_WARPS, smem, st>>>(a);                                           \
-        SSH_CHECK_LAUNCH();                                                                   \
-    } while (0)
-    if (mode == SIG_MODE_SHINGLE) LAUNCH_SIG(SIG_MODE_SHINGLE);
-    else if (mode == SIG_MODE_CWS_FROM_SETS) LAUNCH_SIG(SIG_MODE_CWS_FROM_SETS);
-    else LAUNCH_SIG(SIG_MODE_FUSED);
-#undef LAUNCH_SIG
-    return SSH_OK;
+    a.warp_smem = warp_smem_bytes(a.S, a.P2, a.H, a.T);
+    if (mode == SIG_MODE_SHINGLE) return launch_sig<SIG_MODE_SHINGLE, 1>(ctx, a, N, st);
+    if (mode == SIG_MODE_CWS_FROM_SETS) return launch_sig_ns<SIG_MODE_CWS_FROM_SETS>(ctx, a, N, st);
+    return launch_sig_ns<SIG_MODE_FUSED>(ctx, a, N, st);
 }
