@@ -181,8 +181,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches = lib.ssh_launch_count() - launches0
     clocks = sampler.stop()
-    build_ms = sum(a.elapsed_time(b) for a, b, _ in evs)
-    query_ms = sum(b.elapsed_time(c2) for _, b, c2 in evs)
+    build_each = [a.elapsed_time(b) for a, b, _ in evs]
+    query_each = [b.elapsed_time(c2) for _, b, c2 in evs]
+    build_ms = sum(build_each)
+    query_ms = sum(query_each)
     total_ms = evs[0][0].elapsed_time(evs[-1][2])
     t = torch.tensor([build_ms, query_ms, total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -217,6 +219,8 @@ def run_ours(args):
             },
             "queries_per_s": nq * args.steps / (query_ms / 1e3),
             "build_ms_per_step": build_ms / args.steps,
+            "build_ms_each": [round(v, 3) for v in build_each],
+            "query_ms_each": [round(v, 3) for v in query_each],
             "query_ms_per_step": query_ms / args.steps,
             "mean_candidates": mean_cand,
             "mean_counters": dict(zip(["kim_pruned", "keogh_pruned", "keogh2_pruned", "dtw_computed",
@@ -324,6 +328,12 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
                                  note="cell = FADD + FMNMX3 + FFMA (3 FP32-pipe instr); peak 148x128x f_max / 3")
     res["survivors"] = prof[8]
     res["rescored"] = prof[9]
+    res["lb_paa_pruned"] = prof[10]
+    res["lb_keogh_pruned_filter"] = prof[11]
+    res["members_visited"] = prof[12]
+    if prof[15] > 0:
+        res["thr0_over_dk"] = prof[13] / prof[15]
+        res["thr1_over_dk"] = prof[14] / prof[15]
     return res
 
 

@@ -58,7 +58,10 @@ struct ssh_ctx {
     // profiling (ssh_ctx_set_profiling)
     int profile = 0;
     double prof[16] = {0};
-    unsigned long long *d_cells = nullptr;  // device counter: DTW cells evaluated
+    unsigned long long *d_cells = nullptr;  // device counters: [0] DTW cells evaluated,
+                                            // [1] LB_PAA prunes, [2] LB_Keogh prunes,
+                                            // [3] members visited by the filter
+    int surv_cap = 4096;  // per-query survivor capacity (grows, remembered across batches)
     // named grow-only scratch slots reused across calls (stream-ordered)
     void *slot_ptr[32] = {nullptr};
     size_t slot_bytes[32] = {0};
@@ -79,6 +82,8 @@ enum {
     SLOT_Q_RESC,
     SLOT_Q_D64,
     SLOT_Q_HIST,
+    SLOT_Q_D32,
+    SLOT_Q_TOPK,
     SLOT_COUNT
 };
 

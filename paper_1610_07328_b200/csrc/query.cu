@@ -296,6 +296,7 @@ struct MemberArgs {
     float *out_lb;
     int *out_cnt;
     long long *counters;
+    unsigned long long *dbg;  // profiling counters (ctx->d_cells) or NULL
     int64_t NW;
     int m, nseg, cap;
 };
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(MB_THREADS) members_kernel(MemberArgs a) {
     const float q0 = a.Q[(int64_t)q * m], ql = a.Q[(int64_t)q * m + m - 1];
     const uint32_t *bm = a.bitmap + (int64_t)q * a.NW;
     uint32_t *list = lists + w * 1024;
-    int paa_pr = 0, kim = 0, keo = 0;
+    int paa_pr = 0, kim = 0, keo = 0, nvisit = 0;
     const int64_t s0 = (int64_t)blockIdx.x * MB_SLICE_WORDS;
     const int64_t s1 = min(a.NW, s0 + MB_SLICE_WORDS);
     const unsigned lt = (1u << lane) - 1u;
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(MB_THREADS) members_kernel(MemberArgs a) {
             if (lane >= o) incl += y;
         }
         const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        nvisit += lane == 0 ? total : 0;
         int pos = incl - c;
         while (word) {
             int b = __ffs(word) - 1;
@@ -440,10 +442,17 @@ __global__ void __launch_bounds__(MB_THREADS) members_kernel(MemberArgs a) {
     if (MODE == MODE_FILTER) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) paa_pr += __shfl_xor_sync(0xFFFFFFFFu, paa_pr, o);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nvisit += __shfl_xor_sync(0xFFFFFFFFu, nvisit, o);
         if (lane == 0) {
             long long k1 = kim, k2 = (long long)keo + paa_pr;
             if (k1) atomicAdd((unsigned long long *)&a.counters[q * 5 + 0], (unsigned long long)k1);
             if (k2) atomicAdd((unsigned long long *)&a.counters[q * 5 + 1], (unsigned long long)k2);
+            if (a.dbg) {
+                atomicAdd(&a.dbg[1], (unsigned long long)paa_pr);
+                atomicAdd(&a.dbg[2], (unsigned long long)keo);
+                atomicAdd(&a.dbg[3], (unsigned long long)nvisit);
+            }
         }
     }
 }
@@ -507,17 +516,36 @@ __global__ void seed_select_kernel(const uint32_t *__restrict__ cand, const floa
 }
 
 // ------------------------------------------------------------ fp32 DTW
+// Candidate list of one DTW launch: per query the entries
+// [off_q, min(cnt_q, off_q + wave)) of rows[q][*]; an entry whose lower bound
+// lbs[q][e] exceeds thr_q is skipped (result +inf).
+struct DtwList {
+    const uint32_t *rows;
+    int64_t stride;
+    const int *cnt;     // per-query entry count (NULL: stride)
+    const int *off;     // per-query first entry (NULL: 0)
+    int wave;           // entries per query in this launch
+    const float *lbs;   // per-entry lower bound (NULL: none)
+    float *out;         // result at the same index
+    unsigned long long *abandoned;  // per query (NULL ok)
+    int *computed;      // per query DTWs evaluated (NULL ok)
+};
+
+__device__ __forceinline__ void dtw_list_range(const DtwList &L, int q, int &start, int &end) {
+    start = L.off ? L.off[q] : 0;
+    const int total = L.cnt ? L.cnt[q] : (int)L.stride;
+    end = min(total, start + L.wave);
+}
+
 // Lane-per-candidate banded DTW; band[k][lane] in shared memory, the query
 // padded with +inf outside [0, m) so out-of-band cells are +inf without
 // branches.  With a finite threshold the lane abandons once
 //   row_min + sum_{i' > i} LB_Keogh_i'(x, env(q)) - slack > thr
 // (every remaining row contributes at least its envelope excursion).
 __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const float *__restrict__ Q,
-                             const float *__restrict__ U, const float *__restrict__ Lo,
-                             const uint32_t *__restrict__ list, int64_t list_stride,
-                             const int *__restrict__ list_cnt, int cap, const float *__restrict__ thr,
-                             float *__restrict__ out, unsigned long long *__restrict__ abandoned,
-                             int warps, unsigned long long *__restrict__ cells) {
+                             const float *__restrict__ U, const float *__restrict__ Lo, DtwList L,
+                             const float *__restrict__ thr, int warps,
+                             unsigned long long *__restrict__ cells) {
     extern __shared__ float dsm[];
     const int q = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -540,11 +568,16 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
             sl[i] = Lo[(int64_t)q * m + i];
         }
     __syncthreads();
-    const int cnt = min(list_cnt ? list_cnt[q] : (int)list_stride, cap);
-    const int e = (blockIdx.x * warps + w) * 32 + lane;
-    if ((blockIdx.x * warps + w) * 32 >= cnt) return;
-    uint32_t row = e < cnt ? list[(int64_t)q * list_stride + e] : 0xFFFFFFFFu;
-    bool valid = row != 0xFFFFFFFFu;
+    int start, end;
+    dtw_list_range(L, q, start, end);
+    const int e = start + (blockIdx.x * warps + w) * 32 + lane;
+    if (start + (blockIdx.x * warps + w) * 32 >= end) return;
+    uint32_t row = e < end ? L.rows[(int64_t)q * L.stride + e] : 0xFFFFFFFFu;
+    bool valid = row != 0xFFFFFFFFu && (!L.lbs || !(L.lbs[(int64_t)q * L.stride + e] > T));
+    {
+        const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+        if (L.computed && lane == 0 && vm) atomicAdd(&L.computed[q], __popc(vm));
+    }
     const float *x = X + (int64_t)(valid ? row : 0) * m;
     float rem = 0.f, slack = 0.f;
     if (cb) {
@@ -585,10 +618,10 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
         }
         if (alive && bound > T) alive = false;
     }
-    if (e < cnt) {
+    if (e < end) {
         float res = (valid && alive) ? band[r * 32 + lane] : INFINITY;
-        out[(int64_t)q * list_stride + e] = res;
-        if (abandoned && valid && !alive) atomicAdd(&abandoned[q], 1ULL);
+        L.out[(int64_t)q * L.stride + e] = res;
+        if (L.abandoned && valid && !alive) atomicAdd(&L.abandoned[q], 1ULL);
     }
     if (cells) {
         unsigned long long c = (unsigned long long)rows * (unsigned long long)(2 * r + 1);
@@ -607,11 +640,8 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
 template <int R>
 __global__ void __launch_bounds__(128)
 dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
-              const float *__restrict__ U, const float *__restrict__ Lo,
-              const uint32_t *__restrict__ list, int64_t list_stride,
-              const int *__restrict__ list_cnt, int cap, const float *__restrict__ thr,
-              float *__restrict__ out, unsigned long long *__restrict__ abandoned, int warps,
-              unsigned long long *__restrict__ cells) {
+              const float *__restrict__ U, const float *__restrict__ Lo, DtwList L,
+              const float *__restrict__ thr, int warps, unsigned long long *__restrict__ cells) {
     constexpr int NB = 2 * R + 1;
     constexpr int NT = (NB + 3) / 4;
     extern __shared__ __align__(16) float rsm[];
@@ -634,11 +664,16 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
             sl[i] = Lo[(int64_t)q * m + i];
         }
     __syncthreads();
-    const int cnt = min(list_cnt ? list_cnt[q] : (int)list_stride, cap);
-    const int e = (blockIdx.x * warps + w) * 32 + lane;
-    if ((blockIdx.x * warps + w) * 32 >= cnt) return;
-    const uint32_t row = e < cnt ? list[(int64_t)q * list_stride + e] : 0xFFFFFFFFu;
-    const bool valid = row != 0xFFFFFFFFu;
+    int start, end;
+    dtw_list_range(L, q, start, end);
+    const int e = start + (blockIdx.x * warps + w) * 32 + lane;
+    if (start + (blockIdx.x * warps + w) * 32 >= end) return;
+    const uint32_t row = e < end ? L.rows[(int64_t)q * L.stride + e] : 0xFFFFFFFFu;
+    const bool valid = row != 0xFFFFFFFFu && (!L.lbs || !(L.lbs[(int64_t)q * L.stride + e] > T));
+    {
+        const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
+        if (L.computed && lane == 0 && vm) atomicAdd(&L.computed[q], __popc(vm));
+    }
     const float *x = X + (int64_t)(valid ? row : 0) * m;
     const bool vec = (m & 3) == 0;
     float rem = 0.f, slack = 0.f;
@@ -696,9 +731,9 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
         }
         if (alive && bound > T) alive = false;
     }
-    if (e < cnt) {
-        out[(int64_t)q * list_stride + e] = (valid && alive) ? band[R] : INFINITY;
-        if (abandoned && valid && !alive) atomicAdd(&abandoned[q], 1ULL);
+    if (e < end) {
+        L.out[(int64_t)q * L.stride + e] = (valid && alive) ? band[R] : INFINITY;
+        if (L.abandoned && valid && !alive) atomicAdd(&L.abandoned[q], 1ULL);
     }
     if (cells) {
         unsigned long long cc = (unsigned long long)rows * (unsigned long long)NB;
@@ -781,125 +816,131 @@ __global__ void tau_kernel(const float *__restrict__ sd32, int S0, const int *__
     if (threadIdx.x == 0) thr[q] = thr_from(t, eps);
 }
 
-// wave 1: move the W1 smallest-LB survivors into w1 (taken entries: lb = -1)
-__global__ void wave1_kernel(const uint32_t *__restrict__ surv, float *__restrict__ surv_lb,
-                             const int *__restrict__ surv_cnt, int cap, int W1,
-                             uint32_t *__restrict__ w1, int *__restrict__ w1cnt) {
+// Per query: survivors reordered by LB_Keogh bin (float bits >> 20, ~12% wide)
+// with a counting sort.  Within a bin the order is arbitrary; the wave loop
+// only relies on bins being non-decreasing.
+__global__ void __launch_bounds__(1024)
+lbsort_kernel(const uint32_t *__restrict__ surv, const float *__restrict__ slb,
+              const int *__restrict__ surv_cnt, int cap, uint32_t *__restrict__ srow,
+              float *__restrict__ slbs) {
     __shared__ uint32_t h[NBINS];
-    __shared__ int npos, cut;
     const int q = blockIdx.x;
     const int cnt = min(surv_cnt[q], cap);
-    float *lb = surv_lb + (int64_t)q * cap;
-    const uint32_t *rows = surv + (int64_t)q * cap;
     for (int b = threadIdx.x; b < NBINS; b += blockDim.x) h[b] = 0u;
-    if (threadIdx.x == 0) npos = 0;
     __syncthreads();
-    if (cnt > W1)
-        for (int e = threadIdx.x; e < cnt; e += blockDim.x) atomicAdd(&h[lb_bin(lb[e])], 1u);
+    const float *lb = slb + (int64_t)q * cap;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) atomicAdd(&h[lb_bin(lb[e])], 1u);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int c = 0, b = NBINS;
-        if (cnt > W1) {
-            for (b = 0; b < NBINS; b++) {
-                if (c + (int)h[b] >= W1) break;
-                c += h[b];
-            }
-        }
-        cut = b;
+    // exclusive scan of NBINS (= 2 per thread at 1024 threads)
+    __shared__ uint32_t part[1024];
+    const int per = NBINS / blockDim.x;
+    uint32_t loc = 0;
+    for (int i = 0; i < per; i++) loc += h[threadIdx.x * per + i];
+    part[threadIdx.x] = loc;
+    __syncthreads();
+    for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+        uint32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[threadIdx.x] - loc;
+    for (int i = 0; i < per; i++) {
+        uint32_t c = h[threadIdx.x * per + i];
+        h[threadIdx.x * per + i] = run;
+        run += c;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-        float v = lb[e];
-        if ((int)lb_bin(v) < cut) {
-            w1[(int64_t)q * W1 + atomicAdd(&npos, 1)] = rows[e];
-            lb[e] = -1.f;
-        }
+        const float v = lb[e];
+        const uint32_t p = atomicAdd(&h[lb_bin(v)], 1u);
+        srow[(int64_t)q * cap + p] = surv[(int64_t)q * cap + e];
+        slbs[(int64_t)q * cap + p] = v;
     }
-    __syncthreads();
-    if (cut < NBINS)
-        for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-            float v = lb[e];
-            if (v >= 0.f && (int)lb_bin(v) == cut) {
-                int p = atomicAdd(&npos, 1);
-                if (p < W1) {
-                    w1[(int64_t)q * W1 + p] = rows[e];
-                    lb[e] = -1.f;
-                }
-            }
-        }
-    __syncthreads();
-    if (threadIdx.x == 0) w1cnt[q] = min(npos, W1);
 }
 
-// tighten thr with the wave-1 DTWs: thr1 = min(thr0, kth(d32_w1) (1 + eps))
-__global__ void tau1_kernel(const float *__restrict__ d1, int W1, const int *__restrict__ w1cnt,
-                            int k, float eps, float *__restrict__ thr) {
+// After a wave: fold its fp32 DTWs into the per-query k smallest (topk),
+// tighten thr = min(thr, kth (1 + eps)), advance the wave start and decide
+// whether the query is done (next entry's LB bin above thr's bin => every
+// remaining LB exceeds thr).  Sets *active if any query continues.
+__global__ void wave_update_kernel(const float *__restrict__ d32, const float *__restrict__ slbs,
+                                   const int *__restrict__ cnt, int cap, int wave, int k, float eps,
+                                   float *__restrict__ topk, float *__restrict__ thr,
+                                   int *__restrict__ pos, int *__restrict__ done,
+                                   int *__restrict__ active) {
     __shared__ int red[32];
     const int q = blockIdx.x;
-    const int n = w1cnt[q];
-    const uint32_t *bits = reinterpret_cast<const uint32_t *>(d1 + (int64_t)q * W1);
-    if (n < k) return;
-    int nfin = block_count_le2<uint32_t>(bits, n, nullptr, 0, 0x7F7FFFFFu, red);
-    if (nfin < k) return;
-    float t = __uint_as_float(block_kth2<uint32_t>(bits, n, nullptr, 0, k, 0x7F7FFFFFu, red));
-    if (threadIdx.x == 0) thr[q] = fminf(thr[q], thr_from(t, eps));
-}
-
-// wave 2: remaining survivors with LB_Keogh <= thr1
-__global__ void wave2_kernel(const uint32_t *__restrict__ surv, const float *__restrict__ surv_lb,
-                             const int *__restrict__ surv_cnt, int cap, const float *__restrict__ thr,
-                             uint32_t *__restrict__ w2, int *__restrict__ w2cnt,
-                             long long *__restrict__ counters) {
-    __shared__ int red[32];
-    __shared__ int npos;
-    const int q = blockIdx.x;
-    const int cnt = min(surv_cnt[q], cap);
-    const float T = thr[q];
-    if (threadIdx.x == 0) npos = 0;
-    __syncthreads();
-    int pr = 0;
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-        float v = surv_lb[(int64_t)q * cap + e];
-        if (v < 0.f) continue;
-        if (v <= T) {
-            int p = atomicAdd(&npos, 1);
-            w2[(int64_t)q * cap + p] = surv[(int64_t)q * cap + e];
-        } else {
-            pr++;
+    if (done[q]) return;
+    const int start = pos[q];
+    const int total = min(cnt[q], cap);
+    const int end = min(total, start + wave);
+    const uint32_t *wb = reinterpret_cast<const uint32_t *>(d32 + (int64_t)q * cap + start);
+    uint32_t *tb = reinterpret_cast<uint32_t *>(topk + (int64_t)q * k);
+    const int nw = end - start;
+    const int nfin = block_count_le2<uint32_t>(tb, k, wb, nw, 0x7F7FFFFFu, red);
+    float T = thr[q];
+    if (nfin >= k) {
+        const uint32_t kv = block_kth2<uint32_t>(tb, k, wb, nw, k, 0x7F7FFFFFu, red);
+        // new topk: values < kv, padded with kv
+        __shared__ int npos;
+        __shared__ uint32_t tmp[2048];
+        if (threadIdx.x == 0) npos = 0;
+        __syncthreads();
+        for (int e = threadIdx.x; e < k; e += blockDim.x)
+            if (tb[e] < kv) tmp[atomicAdd(&npos, 1)] = tb[e];
+        for (int e = threadIdx.x; e < nw; e += blockDim.x)
+            if (wb[e] < kv) tmp[atomicAdd(&npos, 1)] = wb[e];
+        __syncthreads();
+        const int c = npos;
+        for (int e = threadIdx.x; e < k; e += blockDim.x) tb[e] = e < c ? tmp[e] : kv;
+        T = fminf(T, thr_from(__uint_as_float(kv), eps));
+    } else {
+        // fewer than k finite values so far: append the wave's finite values
+        __shared__ int npos2;
+        if (threadIdx.x == 0) {
+            int c = 0;
+            for (int e = 0; e < k; e++) c += tb[e] <= 0x7F7FFFFFu;
+            npos2 = c;
         }
+        __syncthreads();
+        for (int e = threadIdx.x; e < nw; e += blockDim.x)
+            if (wb[e] <= 0x7F7FFFFFu) tb[atomicAdd(&npos2, 1)] = wb[e];
     }
-    int tot = block_sum(pr, red);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        w2cnt[q] = npos;
-        if (tot) counters[q * 5 + 1] += tot;
+        thr[q] = T;
+        pos[q] = end;
+        const bool fin = end >= total || lb_bin(slbs[(int64_t)q * cap + end]) > lb_bin(T);
+        done[q] = fin;
+        if (!fin) atomicOr(active, 1);
     }
 }
 
-// rescoring set over both waves: d32 <= T_k (1 + eps)
-__global__ void select_kernel(const uint32_t *__restrict__ w1, const float *__restrict__ d1,
-                              const int *__restrict__ c1, int W1, const uint32_t *__restrict__ w2,
-                              const float *__restrict__ d2, const int *__restrict__ c2, int cap,
-                              int k, float eps, uint32_t *__restrict__ resc, int RS,
-                              int *__restrict__ resc_cnt) {
+// rescoring set over every wave: d32 <= T_k (1 + eps)
+__global__ void select_kernel(const uint32_t *__restrict__ srow, const float *__restrict__ d32,
+                              const int *__restrict__ pos, int cap, int k, float eps,
+                              uint32_t *__restrict__ resc, int *__restrict__ resc_cnt,
+                              long long *__restrict__ counters, const int *__restrict__ cnt,
+                              const int *__restrict__ computed) {
     __shared__ int red[32];
     __shared__ int npos;
     const int q = blockIdx.x;
-    const int na = c1[q], nb = min(c2[q], cap);
-    const uint32_t *ba = reinterpret_cast<const uint32_t *>(d1 + (int64_t)q * W1);
-    const uint32_t *bb = reinterpret_cast<const uint32_t *>(d2 + (int64_t)q * cap);
-    const int nfin = block_count_le2<uint32_t>(ba, na, bb, nb, 0x7F7FFFFFu, red);
+    const int n = pos[q];
+    const uint32_t *b = reinterpret_cast<const uint32_t *>(d32 + (int64_t)q * cap);
+    const int nfin = block_count_le2<uint32_t>(b, n, nullptr, 0, 0x7F7FFFFFu, red);
     const int kk = min(k, nfin);
     float bound = -1.f;
-    if (kk > 0)
-        bound = thr_from(__uint_as_float(block_kth2<uint32_t>(ba, na, bb, nb, kk, 0x7F7FFFFFu, red)), eps);
+    if (kk > 0) bound = thr_from(__uint_as_float(block_kth2<uint32_t>(b, n, nullptr, 0, kk, 0x7F7FFFFFu, red)), eps);
     if (threadIdx.x == 0) npos = 0;
     __syncthreads();
-    for (int e = threadIdx.x; e < na; e += blockDim.x)
-        if (d1[(int64_t)q * W1 + e] <= bound) resc[(int64_t)q * RS + atomicAdd(&npos, 1)] = w1[(int64_t)q * W1 + e];
-    for (int e = threadIdx.x; e < nb; e += blockDim.x)
-        if (d2[(int64_t)q * cap + e] <= bound) resc[(int64_t)q * RS + atomicAdd(&npos, 1)] = w2[(int64_t)q * cap + e];
+    for (int e = threadIdx.x; e < n; e += blockDim.x)
+        if (d32[(int64_t)q * cap + e] <= bound) resc[(int64_t)q * cap + atomicAdd(&npos, 1)] = srow[(int64_t)q * cap + e];
     __syncthreads();
-    if (threadIdx.x == 0) resc_cnt[q] = npos;
+    if (threadIdx.x == 0) {
+        resc_cnt[q] = npos;
+        // survivors never evaluated were excluded by LB_Keogh > thr
+        counters[q * 5 + 1] += min(cnt[q], cap) - computed[q];
+    }
 }
 
 // exact top-k by (d64, id) of the rescored set; P2 >= k power of two
@@ -958,15 +999,14 @@ __global__ void topk_kernel(const uint32_t *__restrict__ resc, const double *__r
     if (threadIdx.x == 0) n_out[q] = n;
 }
 
-__global__ void finalize_counters(const int *__restrict__ nseed, const int *__restrict__ w1cnt,
-                                  const int *__restrict__ w2cnt,
+__global__ void finalize_counters(const int *__restrict__ nseed, const int *__restrict__ computed,
                                   const unsigned long long *__restrict__ abandoned, int nq,
                                   const long long *__restrict__ n_cand,
                                   const int *__restrict__ is_fb, long long *__restrict__ counters,
                                   int *__restrict__ status) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
-    counters[q * 5 + 3] = (long long)nseed[q] + w1cnt[q] + w2cnt[q];
+    counters[q * 5 + 3] = (long long)nseed[q] + computed[q];
     counters[q * 5 + 4] = (long long)abandoned[q];
     status[q] = n_cand[q] == 0 ? 1 : (is_fb[q] ? 2 : 0);
 }
@@ -1007,7 +1047,7 @@ struct Carver {
 struct QueryBufs {
     uint64_t *qsig, *qbits, *bstart;
     uint32_t *blen, *seeds, *w1, *ts, *cand;
-    int *isfb, *nseed, *scnt, *c1, *c2, *rcnt, *ccnt;
+    int *isfb, *nseed, *scnt, *c1, *c2, *rcnt, *ccnt, *done, *active;
     float *U, *Lo, *Useg, *Lseg, *sd32, *thr, *d1, *cand_lb;
     unsigned long long *aband;
 
@@ -1027,6 +1067,8 @@ struct QueryBufs {
         c2 = c.take<int>(nc);
         rcnt = c.take<int>(nc);
         ccnt = c.take<int>(nc);
+        done = c.take<int>(nc);
+        active = c.take<int>(1);
         U = c.take<float>((size_t)nc * m);
         Lo = c.take<float>((size_t)nc * m);
         Useg = c.take<float>((size_t)nc * nseg);
@@ -1106,30 +1148,28 @@ size_t members_smem(int mode, int m, int nseg) {
 
 template <int R>
 static int launch_dtw32r(ssh_ctx *ctx, const float *X, const float *Q, const float *U,
-                         const float *Lo, const uint32_t *list, int64_t stride, const int *cnt,
-                         int cap, int maxcnt, const float *thr, float *out,
-                         unsigned long long *aband, int nq, cudaStream_t st) {
+                         const float *Lo, const DtwList &L, const float *thr, int nq,
+                         cudaStream_t st) {
     const int m = ctx->p.m;
     const int warps = 4;
     const int YP = ((m + 2 * R + 8) + 3) & ~3;
     size_t smem = (size_t)(4 * YP + 2 * m) * sizeof(float);
     SSH_CUDA(cudaFuncSetAttribute(dtw32r_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (maxcnt <= 0) return SSH_OK;
-    dim3 grid((unsigned)ssh_div_up(maxcnt, 32 * warps), (unsigned)nq);
-    dtw32r_kernel<R><<<grid, 32 * warps, smem, st>>>(X, m, Q, U, Lo, list, stride, cnt, cap, thr, out,
-                                                     aband, warps, ctx->profile ? ctx->d_cells : nullptr);
+    if (L.wave <= 0) return SSH_OK;
+    dim3 grid((unsigned)ssh_div_up(L.wave, 32 * warps), (unsigned)nq);
+    dtw32r_kernel<R><<<grid, 32 * warps, smem, st>>>(X, m, Q, U, Lo, L, thr, warps,
+                                                     ctx->profile ? ctx->d_cells : nullptr);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
 
+// fp32 DTW of a candidate list (register band for the common radii, shared-memory band otherwise)
 static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const float *U,
-                        const float *Lo, const uint32_t *list, int64_t stride, const int *cnt,
-                        int cap, int maxcnt, const float *thr, float *out,
-                        unsigned long long *aband, int nq, cudaStream_t st) {
+                        const float *Lo, const DtwList &L, const float *thr, int nq,
+                        cudaStream_t st) {
     const int m = ctx->p.m, r = ctx->p.radius;
-#define DTWR(RR)                                                                                  \
-    case RR:                                                                                      \
-        return launch_dtw32r<RR>(ctx, X, Q, U, Lo, list, stride, cnt, cap, maxcnt, thr, out, aband, nq, st);
+#define DTWR(RR) \
+    case RR: return launch_dtw32r<RR>(ctx, X, Q, U, Lo, L, thr, nq, st);
     switch (r) {
         DTWR(3) DTWR(6) DTWR(13) DTWR(26) DTWR(51)
         default: break;
@@ -1139,10 +1179,10 @@ static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const floa
     int warps = dtw32_warps(m, r, &smem);
     SSH_REQUIRE(smem <= 227 * 1024, SSH_ERR_UNSUPPORTED, "DTW band too wide (r=%d)", r);
     SSH_CUDA(cudaFuncSetAttribute(dtw32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (maxcnt <= 0) return SSH_OK;
-    dim3 grid((unsigned)ssh_div_up(maxcnt, 32 * warps), (unsigned)nq);
-    dtw32_kernel<<<grid, 32 * warps, smem, st>>>(X, m, r, Q, U, Lo, list, stride, cnt, cap, thr, out,
-                                                 aband, warps, ctx->profile ? ctx->d_cells : nullptr);
+    if (L.wave <= 0) return SSH_OK;
+    dim3 grid((unsigned)ssh_div_up(L.wave, 32 * warps), (unsigned)nq);
+    dtw32_kernel<<<grid, 32 * warps, smem, st>>>(X, m, r, Q, U, Lo, L, thr, warps,
+                                                 ctx->profile ? ctx->d_cells : nullptr);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
@@ -1266,7 +1306,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     int qc = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(nq, 32768),
                                                          ((int64_t)1 << 28) / std::max<int64_t>(1, NW)));
     SSH_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 5 * (size_t)nq, st));
-    int cap = Q_SURV_CAP0;
+    int cap = std::max(Q_SURV_CAP0, ctx->surv_cap);
     PhaseTimer pt(ctx, st);
     for (int q0 = 0; q0 < nq; q0 += qc) {
         const int nc = std::min(qc, nq - q0);
@@ -1300,6 +1340,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         ma.X = X; ma.Q = Qc; ma.U = B.U; ma.Lo = B.Lo; ma.Useg = B.Useg; ma.Lseg = B.Lseg;
         ma.paa = ix->paa; ma.maxabs = ix->d_maxabs; ma.bitmap = bitmap; ma.thr = B.thr; ma.ts = B.ts;
         ma.hist = hist; ma.counters = cnt5; ma.NW = NW; ma.m = m; ma.nseg = nseg;
+        ma.dbg = nullptr;
         ma.out = nullptr; ma.out_lb = nullptr; ma.out_cnt = nullptr; ma.cap = 0;
         SSH_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)nc * NBINS, st));
         rc = launch_members<MODE_HIST>(ma, nc, st);
@@ -1313,11 +1354,18 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         seed_select_kernel<<<nc, 256, 0, st>>>(B.cand, B.cand_lb, B.ccnt, Q_SEED_CAND, S0, B.seeds,
                                                B.nseed);
         SSH_CHECK_LAUNCH();
-        rc = launch_dtw32(ctx, X, Qc, nullptr, nullptr, B.seeds, S0, B.nseed, S0, S0, nullptr, B.sd32,
-                          nullptr, nc, st);
+        {
+            DtwList dl{B.seeds, S0, B.nseed, nullptr, S0, nullptr, B.sd32, nullptr, nullptr};
+            rc = launch_dtw32(ctx, X, Qc, nullptr, nullptr, dl, nullptr, nc, st);
+        }
         if (rc) return rc;
         tau_kernel<<<nc, 256, 0, st>>>(B.sd32, S0, B.nseed, k, eps, B.thr);
         SSH_CHECK_LAUNCH();
+        std::vector<float> thr0h;
+        if (ctx->profile) {
+            thr0h.resize(nc);
+            cudaMemcpyAsync(thr0h.data(), B.thr, sizeof(float) * nc, cudaMemcpyDeviceToHost, st);
+        }
         pt.mark();
         // K7: member filter (retried with a larger per-query capacity on overflow)
         uint32_t *surv = nullptr;
@@ -1330,39 +1378,49 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             SSH_CUDA(cudaMemsetAsync(B.scnt, 0, sizeof(int) * nc, st));
             SSH_CUDA(cudaMemsetAsync(cnt5, 0, sizeof(long long) * 5 * nc, st));
             ma.out = surv; ma.out_lb = slb; ma.out_cnt = B.scnt; ma.cap = cap;
+            ma.dbg = ctx->profile ? ctx->d_cells : nullptr;
             rc = launch_members<MODE_FILTER>(ma, nc, st);
             if (rc) return rc;
             rc = max_of(B.scnt, nc, st, &maxs);
             if (rc) return rc;
             if (maxs <= cap) break;
-            cap = next_pow2(maxs);
+            cap = next_pow2(maxs + maxs / 4);
+            ctx->surv_cap = cap;
         }
         pt.mark();
-        // K8: DTW waves in LB order
-        uint32_t *w2 = (uint32_t *)ssh_slot(ctx, SLOT_Q_W2, sizeof(uint32_t) * (size_t)nc * cap, st);
-        float *d2 = (float *)ssh_slot(ctx, SLOT_Q_D2, sizeof(float) * (size_t)nc * cap, st);
-        if (!w2 || !d2) return SSH_ERR_OOM;
-        wave1_kernel<<<nc, 256, 0, st>>>(surv, slb, B.scnt, cap, W1, B.w1, B.c1);
+        // K8: DTW waves in LB order (survivors bucket-sorted by LB; growing waves)
+        uint32_t *srow = (uint32_t *)ssh_slot(ctx, SLOT_Q_W2, sizeof(uint32_t) * (size_t)nc * cap, st);
+        float *slbs = (float *)ssh_slot(ctx, SLOT_Q_D2, sizeof(float) * (size_t)nc * cap, st);
+        float *d32 = (float *)ssh_slot(ctx, SLOT_Q_D32, sizeof(float) * (size_t)nc * cap, st);
+        uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)nc * cap, st);
+        double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)nc * cap, st);
+        float *topk = (float *)ssh_slot(ctx, SLOT_Q_TOPK, sizeof(float) * (size_t)nc * k, st);
+        if (!srow || !slbs || !d32 || !resc || !d64 || !topk) return SSH_ERR_OOM;
+        lbsort_kernel<<<nc, 1024, 0, st>>>(surv, slb, B.scnt, cap, srow, slbs);
         SSH_CHECK_LAUNCH();
-        rc = launch_dtw32(ctx, X, Qc, B.U, B.Lo, B.w1, W1, B.c1, W1, std::min(W1, maxs), B.thr, B.d1,
-                          B.aband, nc, st);
-        if (rc) return rc;
-        tau1_kernel<<<nc, 256, 0, st>>>(B.d1, W1, B.c1, k, eps, B.thr);
-        SSH_CHECK_LAUNCH();
-        wave2_kernel<<<nc, 256, 0, st>>>(surv, slb, B.scnt, cap, B.thr, w2, B.c2, cnt5);
-        SSH_CHECK_LAUNCH();
-        int max2 = 0;
-        rc = max_of(B.c2, nc, st, &max2);
-        if (rc) return rc;
-        rc = launch_dtw32(ctx, X, Qc, B.U, B.Lo, w2, cap, B.c2, cap, max2, B.thr, d2, B.aband, nc, st);
-        if (rc) return rc;
+        SSH_CUDA(cudaMemsetAsync(topk, 0xFF, sizeof(float) * (size_t)nc * k, st));  // NaN bits > any finite
+        SSH_CUDA(cudaMemsetAsync(B.c1, 0, sizeof(int) * nc, st));    // wave start
+        SSH_CUDA(cudaMemsetAsync(B.c2, 0, sizeof(int) * nc, st));    // DTWs evaluated
+        SSH_CUDA(cudaMemsetAsync(B.done, 0, sizeof(int) * nc, st));
+        int wave = W1;
+        for (int it = 0; maxs > 0; it++) {
+            SSH_CUDA(cudaMemsetAsync(B.active, 0, sizeof(int), st));
+            DtwList dl{srow, cap, B.scnt, B.c1, std::min(wave, maxs), slbs, d32, B.aband, B.c2};
+            rc = launch_dtw32(ctx, X, Qc, B.U, B.Lo, dl, B.thr, nc, st);
+            if (rc) return rc;
+            wave_update_kernel<<<nc, 256, 0, st>>>(d32, slbs, B.scnt, cap, std::min(wave, maxs), k, eps,
+                                                   topk, B.thr, B.c1, B.done, B.active);
+            SSH_CHECK_LAUNCH();
+            int act = 0;
+            SSH_CUDA(cudaMemcpyAsync(&act, B.active, sizeof(int), cudaMemcpyDeviceToHost, st));
+            SSH_CUDA(cudaStreamSynchronize(st));
+            if (!act) break;
+            wave = std::min(wave * 2, 1 << 14);
+        }
         pt.mark();
         // K9/K10: rescoring set, exact f64 DTW, top-k by (d64, id)
-        const int RS = W1 + cap;
-        uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)nc * RS, st);
-        double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)nc * RS, st);
-        if (!resc || !d64) return SSH_ERR_OOM;
-        select_kernel<<<nc, 256, 0, st>>>(B.w1, B.d1, B.c1, W1, w2, d2, B.c2, cap, k, eps, resc, RS, B.rcnt);
+        const int RS = cap;
+        select_kernel<<<nc, 256, 0, st>>>(srow, d32, B.c1, cap, k, eps, resc, B.rcnt, cnt5, B.scnt, B.c2);
         SSH_CHECK_LAUNCH();
         int maxr = 0;
         rc = max_of(B.rcnt, nc, st, &maxr);
@@ -1376,7 +1434,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                                           (long long *)out_ids + (int64_t)q0 * k,
                                           out_d2 + (int64_t)q0 * k, n_out + q0);
         SSH_CHECK_LAUNCH();
-        finalize_counters<<<ssh_div_up(nc, 128), 128, 0, st>>>(B.nseed, B.c1, B.c2, B.aband, nc, ncand,
+        finalize_counters<<<ssh_div_up(nc, 128), 128, 0, st>>>(B.nseed, B.c2, B.aband, nc, ncand,
                                                                B.isfb, cnt5, status + q0);
         SSH_CHECK_LAUNCH();
         pt.mark();
@@ -1387,6 +1445,19 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             for (int v : h) ctx->prof[8] += v;
             cudaMemcpy(h.data(), B.rcnt, sizeof(int) * nc, cudaMemcpyDeviceToHost);
             for (int v : h) ctx->prof[9] += v;
+            // threshold quality: thr0 / d_k and thr1 / d_k (d_k = exact k-th squared distance)
+            std::vector<float> thr1h(nc);
+            std::vector<double> dk((size_t)nc * k);
+            cudaMemcpy(thr1h.data(), B.thr, sizeof(float) * nc, cudaMemcpyDeviceToHost);
+            cudaMemcpy(dk.data(), out_d2 + (int64_t)q0 * k, sizeof(double) * nc * k, cudaMemcpyDeviceToHost);
+            for (int q = 0; q < nc; q++) {
+                double d = dk[(size_t)q * k + k - 1];
+                if (d > 0 && std::isfinite(d) && std::isfinite(thr0h[q])) {
+                    ctx->prof[13] += thr0h[q] / d;
+                    ctx->prof[14] += thr1h[q] / d;
+                    ctx->prof[15] += 1;
+                }
+            }
         }
     }
     return SSH_OK;
