@@ -116,6 +116,11 @@ int ssh_signatures(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t
  * to read back bucket counts. */
 int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int64_t id_base,
                     ssh_index **out, void *stream);
+/* K1 -> K4 fused — build_index (index.py:159-172): signatures (written to
+ * sig_out u64[N][L] when non-NULL), bucket tables and the shard's rerank
+ * summary (PAA means, emitted by the sketch kernel while it stages X). */
+int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, int64_t id_base,
+                    uint64_t *sig_out, ssh_index **out, void *stream);
 int ssh_index_destroy(ssh_index *idx);
 int ssh_index_num_buckets(const ssh_index *idx, int table, int64_t *n_buckets);
 int64_t ssh_index_size(const ssh_index *idx);

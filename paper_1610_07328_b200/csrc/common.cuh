@@ -54,6 +54,7 @@ struct ssh_ctx {
     float *d_w32 = nullptr;   // filter rounded to f32
     double *d_r = nullptr, *d_lnc = nullptr, *d_beta = nullptr, *d_lna1 = nullptr;
     double *d_lnw = nullptr;  // ln(count)
+    void *d_rank = nullptr;   // per-slot rank of ln_a1 by (value, token): u16 (n <= 16) or u32
     size_t tab_entries = 0;
     // profiling (ssh_ctx_set_profiling)
     int profile = 0;
@@ -84,6 +85,7 @@ enum {
     SLOT_Q_HIST,
     SLOT_Q_D32,
     SLOT_Q_TOPK,
+    SLOT_SIG,
     SLOT_COUNT
 };
 
@@ -125,11 +127,15 @@ static inline int ssh_div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / 
 
 // kernel launchers implemented per translation unit
 int ssh_launch_sketch(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *bits,
-                      int64_t *stats, cudaStream_t st);
+                      int64_t *stats, cudaStream_t st, float *paa = nullptr,
+                      unsigned *maxabs = nullptr);
 int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *tok_in,
                            const uint16_t *cnt_in, const int32_t *len_in, int64_t N,
                            uint32_t *tok_out, uint16_t *cnt_out, int32_t *len_out,
                            uint64_t *keys_out, uint64_t *sig_out, int mode, cudaStream_t st);
 int ssh_launch_lna1(ssh_ctx *ctx, cudaStream_t st);
+int ssh_build_ranks(ssh_ctx *ctx, cudaStream_t st);
+int ssh_sort_columns(ssh_ctx *ctx, const uint64_t *rowmajor, int64_t N, int L, uint32_t *rows_out,
+                     uint64_t **keys_sorted, cudaStream_t st);
 
 enum { SIG_MODE_SHINGLE = 1, SIG_MODE_CWS_FROM_SETS = 2, SIG_MODE_FUSED = 3 };

@@ -103,6 +103,8 @@ static void free_tables(ssh_ctx *c) {
     cudaFree(c->d_w64); cudaFree(c->d_w32);
     cudaFree(c->d_r); cudaFree(c->d_lnc); cudaFree(c->d_beta); cudaFree(c->d_lna1);
     cudaFree(c->d_lnw);
+    cudaFree(c->d_rank);
+    c->d_rank = nullptr;
     c->d_w64 = nullptr; c->d_w32 = nullptr; c->d_r = c->d_lnc = c->d_beta = c->d_lna1 = nullptr;
     c->d_lnw = nullptr;
 }
@@ -182,7 +184,10 @@ extern "C" int ssh_ctx_set_params(ssh_ctx *ctx, const ssh_params *p, const doubl
     SSH_CUDA(cudaMemcpy(ctx->d_beta, tab_beta, sizeof(double) * ent, cudaMemcpyHostToDevice));
     SSH_CUDA(cudaMemcpy(ctx->d_lnw, ln_w, sizeof(double) * (max_count + 1),
                         cudaMemcpyHostToDevice));
+    SSH_CUDA(cudaMalloc(&ctx->d_rank, (p->n <= 16 ? 2 : 4) * ent));
     int rc = ssh_launch_lna1(ctx, 0);
+    if (rc) return rc;
+    rc = ssh_build_ranks(ctx, 0);
     if (rc) return rc;
     SSH_CUDA(cudaDeviceSynchronize());
     ctx->have_params = true;

@@ -44,6 +44,7 @@ struct SigArgs {
     uint64_t *keys_out;
     uint64_t *sig_out;
     const double *lna1, *tr, *tlnc, *tbeta, *lnw;
+    const void *rank;  // per-slot rank of ln_a1: u16 (n <= 16) or u32
     int64_t N;
     int words, nb, n, T, P2, H, S, L, K;
     int warp_smem;  // bytes per warp
@@ -331,10 +332,11 @@ __device__ __forceinline__ void take_min(double v, int d, double &bv, int &bd) {
     }
 }
 
-template <int NS>
+template <int NS, typename RT>
 __device__ void warp_cws(const SigArgs &a, int64_t row, const WarpSmem &w, int D, int lane) {
     constexpr int U = 4;
     const int S = a.S;
+    const RT *rank = reinterpret_cast<const RT *>(a.rank);
     // split indices: count-1 into list1 (ustart storage), count>1 into listm (ucnt storage)
     uint16_t *list1 = w.ustart;
     uint16_t *listm = w.ucnt;
@@ -353,19 +355,16 @@ __device__ void warp_cws(const SigArgs &a, int64_t row, const WarpSmem &w, int D
         nm += __popc(mm);
     }
     __syncwarp();
-    double best[U][NS];
-    int bd[U][NS];
+    // count-1 tokens: ln_a1 ranks are a total order by (value, token), so the
+    // argmin is an integer min over (rank << 12 | index); U independent chains.
+    uint32_t bk[U][NS];  // rank < 2^20, index < 2^12
 #pragma unroll
     for (int u = 0; u < U; u++)
 #pragma unroll
-        for (int i = 0; i < NS; i++) {
-            best[u][i] = (double)INFINITY;
-            bd[u][i] = 0x7FFFFFFF;
-        }
-    // count-1 tokens: one ln_a1 gather per (token, slot), U chains
+        for (int i = 0; i < NS; i++) bk[u][i] = 0xFFFFFFFFu;
     for (int e0 = 0; e0 < n1; e0 += U) {
         int dd[U];
-        double va[U][NS];
+        uint32_t rv[U][NS];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const bool ok = e0 + u < n1;
@@ -374,17 +373,31 @@ __device__ void warp_cws(const SigArgs &a, int64_t row, const WarpSmem &w, int D
 #pragma unroll
             for (int i = 0; i < NS; i++) {
                 const int s = lane + 32 * i;
-                va[u][i] = (ok && s < S) ? __ldg(a.lna1 + base + s) : (double)INFINITY;
+                rv[u][i] = (ok && s < S) ? (uint32_t)__ldg(rank + base + s) : 0xFFFFFu;
             }
         }
 #pragma unroll
         for (int u = 0; u < U; u++)
 #pragma unroll
             for (int i = 0; i < NS; i++) {
-                const bool l = va[u][i] < best[u][i];
-                best[u][i] = l ? va[u][i] : best[u][i];
-                bd[u][i] = l ? dd[u] : bd[u][i];
+                bk[u][i] = min(bk[u][i], (rv[u][i] << 12) | (uint32_t)dd[u]);
             }
+    }
+    double best[1][NS];
+    int bd[1][NS];
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+        uint32_t k0 = bk[0][i];
+#pragma unroll
+        for (int u = 1; u < U; u++) k0 = min(k0, bk[u][i]);
+        const int s = lane + 32 * i;
+        if (n1 > 0 && s < S) {
+            bd[0][i] = (int)(k0 & 0xFFFu);
+            best[0][i] = __ldg(a.lna1 + (size_t)(w.ukey[bd[0][i]] >> 12) * S + s);
+        } else {
+            bd[0][i] = 0x7FFFFFFF;
+            best[0][i] = (double)INFINITY;
+        }
     }
     // count>1 tokens: full formula (wmh.py:74-76), one more chain
     double bestm[NS];
@@ -418,8 +431,7 @@ __device__ void warp_cws(const SigArgs &a, int64_t row, const WarpSmem &w, int D
         const int s = lane + 32 * i;
         double bv = bestm[i];
         int bi = bdm[i];
-#pragma unroll
-        for (int u = 0; u < U; u++) take_min(best[u][i], bd[u][i], bv, bi);
+        take_min(best[0][i], bd[0][i], bv, bi);
         if (s < S && D > 0) {
             const uint32_t key = w.ukey[bi];
             const uint32_t tok = key >> 12, cnt = key & 0xFFFu;
@@ -475,7 +487,8 @@ __global__ void __launch_bounds__(32 * SG_WARPS, 3) shingle_cws_kernel(SigArgs a
             if (lane == 0) a.len_out[row] = D;
             __syncwarp();
         } else {
-            warp_cws<NS>(a, row, w, D, lane);
+            if (a.n <= 16) warp_cws<NS, uint16_t>(a, row, w, D, lane);
+            else warp_cws<NS, uint32_t>(a, row, w, D, lane);
         }
     }
 }
@@ -525,6 +538,7 @@ int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *t
     a.keys_out = keys_out; a.sig_out = sig_out;
     a.lna1 = ctx->d_lna1; a.tr = ctx->d_r; a.tlnc = ctx->d_lnc; a.tbeta = ctx->d_beta;
     a.lnw = ctx->d_lnw;
+    a.rank = ctx->d_rank;
     a.N = N; a.words = ctx->words; a.nb = ctx->nb; a.n = ctx->p.n; a.T = ctx->T;
     int P2 = 32;
     while (P2 < ctx->T) P2 <<= 1;

@@ -8,6 +8,8 @@
 // memory so each digit run is written contiguously.  Then a run-length pass
 // emits CSR: sorted unique keys, u32 offsets, u32 rows.  Bytes per
 // (series, table): 8 B key read + 8 B key + 4 B row written per pass.
+#include <algorithm>
+
 #include "common.cuh"
 
 #define RS_THREADS 256
@@ -249,6 +251,87 @@ rle_emit(const uint64_t *__restrict__ keys, int64_t N, int ntiles, const uint32_
     if (tile == ntiles - 1 && threadIdx.x == 0) of[nb[j]] = (uint32_t)N;
 }
 
+// Stable LSD radix sort (8 x 8-bit passes) of the L columns of a row-major
+// [N][L] u64 matrix, each column independently; rows_out [L][N] receives the
+// original row of every sorted position, *keys_sorted the sorted keys [L][N]
+// (a ctx scratch slot).  Ties keep ascending row order.
+int ssh_sort_columns(ssh_ctx *ctx, const uint64_t *rowmajor, int64_t N, int L, uint32_t *rows_out,
+                     uint64_t **keys_sorted, cudaStream_t st) {
+    const int ntiles = ssh_div_up(N, RS_TILE);
+    size_t kbytes = sizeof(uint64_t) * (size_t)L * N;
+    size_t rbytes = sizeof(uint32_t) * (size_t)L * N;
+    size_t hbytes = sizeof(uint32_t) * (size_t)L * RS_BINS * ntiles;
+    uint64_t *kA = (uint64_t *)ssh_slot(ctx, SLOT_RS_KEYS_A, kbytes, st);
+    uint64_t *kB = (uint64_t *)ssh_slot(ctx, SLOT_RS_KEYS_B, kbytes, st);
+    uint32_t *rB = (uint32_t *)ssh_slot(ctx, SLOT_RS_ROWS_B, rbytes, st);
+    uint32_t *hist = (uint32_t *)ssh_slot(ctx, SLOT_RS_HIST, hbytes, st);
+    if (!kA || !kB || !rB || !hist) return SSH_ERR_OOM;
+    uint32_t *rA = rows_out;  // 8 passes (even): the sorted rows land back in rA
+    {
+        dim3 g((unsigned)ssh_div_up(N, 32), (unsigned)ssh_div_up(L, 32));
+        rs_transpose<<<g, 256, 0, st>>>(rowmajor, N, L, kA, rA); ssh_count_launch();
+    }
+    uint64_t *kin = kA, *kout = kB;
+    uint32_t *rin = rA, *rout = rB;
+    dim3 grid((unsigned)ntiles, (unsigned)L);
+    for (int pass = 0; pass < 8; pass++) {
+        int shift = 8 * pass;
+        rs_hist<<<grid, RS_THREADS, 0, st>>>(kin, N, shift, ntiles, hist); ssh_count_launch();
+        rs_scan<<<L, 1024, 0, st>>>(hist, ntiles); ssh_count_launch();
+        rs_scatter<<<grid, RS_THREADS, 0, st>>>(kin, rin, N, shift, ntiles, hist, kout, rout); ssh_count_launch();
+        uint64_t *tk = kin; kin = kout; kout = tk;
+        uint32_t *tr = rin; rin = rout; rout = tr;
+    }
+    SSH_CUDA(cudaGetLastError());
+    *keys_sorted = kin;
+    return SSH_OK;
+}
+
+// Per-slot ranks of ln_a1 (order by (value, token)): rank[token][slot].
+__global__ void lna1_orderable_kernel(const double *__restrict__ lna1, size_t n, uint64_t *__restrict__ keys) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        uint64_t b = (uint64_t)__double_as_longlong(lna1[e]);
+        keys[e] = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+    }
+}
+
+template <typename RT>
+__global__ void rank_scatter_kernel(const uint32_t *__restrict__ rows, int64_t T, int S, RT *__restrict__ rank) {
+    const int64_t n = T * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / T, p = e - j * T;
+        rank[(int64_t)rows[e] * S + j] = (RT)p;
+    }
+}
+
+int ssh_build_ranks(ssh_ctx *ctx, cudaStream_t st) {
+    const int64_t T = (int64_t)1 << ctx->p.n;
+    const int S = ctx->S;
+    const size_t n = (size_t)T * S;
+    uint64_t *keys = nullptr;
+    uint32_t *rows = nullptr;
+    SSH_CUDA(cudaMalloc(&keys, sizeof(uint64_t) * n));
+    SSH_CUDA(cudaMalloc(&rows, sizeof(uint32_t) * n));
+    int grid = (int)std::min<size_t>((n + 255) / 256, (size_t)ctx->num_sms * 16);
+    lna1_orderable_kernel<<<grid, 256, 0, st>>>(ctx->d_lna1, n, keys);
+    SSH_CHECK_LAUNCH();
+    uint64_t *sorted = nullptr;
+    int rc = ssh_sort_columns(ctx, keys, T, S, rows, &sorted, st);
+    if (rc == SSH_OK) {
+        if (ctx->p.n <= 16) {
+            rank_scatter_kernel<uint16_t><<<grid, 256, 0, st>>>(rows, T, S, (uint16_t *)ctx->d_rank);
+        } else {
+            rank_scatter_kernel<uint32_t><<<grid, 256, 0, st>>>(rows, T, S, (uint32_t *)ctx->d_rank);
+        }
+        ssh_count_launch();
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = ssh_cuda_fail(e, "ssh_build_ranks", __FILE__, __LINE__);
+    }
+    cudaFree(keys);
+    cudaFree(rows);
+    return rc;
+}
+
 extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int64_t id_base,
                                ssh_index **out, void *stream) {
     SSH_REQUIRE(ctx && out, SSH_ERR_INVALID, "ssh_index_build: NULL argument");
@@ -262,39 +345,18 @@ extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int
     const int ntiles = ssh_div_up(N, RS_TILE);
     ssh_index *ix = new ssh_index();
     ix->L = L; ix->N = N; ix->id_base = id_base; ix->device = ctx->device;
-    // scratch: keys A/B, rows B, hist (ctx slots, reused across builds); rows A = ix->ids
-    size_t kbytes = sizeof(uint64_t) * (size_t)L * N;
-    size_t rbytes = sizeof(uint32_t) * (size_t)L * N;
-    size_t hbytes = sizeof(uint32_t) * (size_t)L * RS_BINS * ntiles;
     int rc = SSH_OK;
     cudaError_t e;
-    uint64_t *kA = (uint64_t *)ssh_slot(ctx, SLOT_RS_KEYS_A, kbytes, st);
-    uint64_t *kB = (uint64_t *)ssh_slot(ctx, SLOT_RS_KEYS_B, kbytes, st);
-    uint32_t *rB = (uint32_t *)ssh_slot(ctx, SLOT_RS_ROWS_B, rbytes, st);
-    uint32_t *hist = (uint32_t *)ssh_slot(ctx, SLOT_RS_HIST, hbytes, st);
-    uint32_t *rA;
-    if (!kA || !kB || !rB || !hist) { delete ix; return SSH_ERR_OOM; }
+    uint64_t *kin = nullptr;
+    size_t rbytes = sizeof(uint32_t) * (size_t)L * N;
     e = cudaMallocAsync((void **)&ix->ids, rbytes, st);
     if (e != cudaSuccess) { delete ix; return ssh_cuda_fail(e, "cudaMallocAsync(ids)", __FILE__, __LINE__); }
-    rA = ix->ids;  // 8 passes (even): the sorted rows land back in rA = ix->ids
+    rc = ssh_sort_columns(ctx, sig, N, L, ix->ids, &kin, st);
+    if (rc) goto fail;
     {
-        dim3 g((unsigned)ssh_div_up(N, 32), (unsigned)ssh_div_up(L, 32));
-        rs_transpose<<<g, 256, 0, st>>>(sig, N, L, kA, rA); ssh_count_launch();
-    }
-    uint64_t *kin = kA, *kout = kB;
-    uint32_t *rin = rA, *rout = rB;
+    uint32_t *hist = (uint32_t *)ctx->slot_ptr[SLOT_RS_HIST];
     dim3 grid((unsigned)ntiles, (unsigned)L);
-    for (int pass = 0; pass < 8; pass++) {
-        int shift = 8 * pass;
-        rs_hist<<<grid, RS_THREADS, 0, st>>>(kin, N, shift, ntiles, hist); ssh_count_launch();
-        rs_scan<<<L, 1024, 0, st>>>(hist, ntiles); ssh_count_launch();
-        rs_scatter<<<grid, RS_THREADS, 0, st>>>(kin, rin, N, shift, ntiles, hist, kout, rout); ssh_count_launch();
-        uint64_t *tk = kin; kin = kout; kout = tk;
-        uint32_t *tr = rin; rin = rout; rout = tr;
-    }
-    e = cudaGetLastError();
-    if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "radix sort", __FILE__, __LINE__); goto fail; }
-    // after 8 passes: sorted keys in kin (= kA), rows in rin (= rA = ix->ids)
+    // sorted keys in kin, rows in ix->ids
     // run-length encode -> CSR
     e = cudaMallocAsync((void **)&ix->d_nb, sizeof(int64_t) * 2 * L, st);
     if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "cudaMallocAsync(nb)", __FILE__, __LINE__); goto fail; }
@@ -319,6 +381,7 @@ extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int
         ssh_count_launch();
         e = cudaGetLastError();
         if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "rle_emit", __FILE__, __LINE__); goto fail; }
+    }
     }
     *out = ix;
     return SSH_OK;
@@ -374,5 +437,45 @@ extern "C" int ssh_index_export(const ssh_index *ix, int table, uint64_t *keys, 
     delete[] of;
     delete[] rw;
     if (e != cudaSuccess) return ssh_cuda_fail(e, "ssh_index_export", __FILE__, __LINE__);
+    return SSH_OK;
+}
+
+// K1 -> K4 in one call: build_index (index.py:159-172).  The sketch kernel
+// also emits the shard's PAA rerank summary while the series are staged.
+extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, int64_t id_base,
+                               uint64_t *sig_out, ssh_index **out, void *stream) {
+    SSH_REQUIRE(ctx && X && out, SSH_ERR_INVALID, "ssh_build_index: NULL argument");
+    SSH_REQUIRE(ctx->have_params, SSH_ERR_STATE, "ssh_build_index: ssh_ctx_set_params not called");
+    SSH_REQUIRE(N >= 1 && ld >= ctx->p.m, SSH_ERR_INVALID, "ssh_build_index: bad shape N=%lld ld=%lld",
+                (long long)N, (long long)ld);
+    SSH_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nseg = (ctx->p.m + SSH_PAA_SEG - 1) / SSH_PAA_SEG;
+    uint64_t *bits = (uint64_t *)ssh_slot(ctx, SLOT_BITS, sizeof(uint64_t) * (size_t)N * ctx->words, st);
+    uint64_t *sig = sig_out ? sig_out
+                            : (uint64_t *)ssh_slot(ctx, SLOT_SIG, sizeof(uint64_t) * (size_t)N * ctx->p.L, st);
+    if (!bits || !sig) return SSH_ERR_OOM;
+    float *paa = nullptr;
+    unsigned *maxabs = nullptr;
+    SSH_CUDA(cudaMallocAsync((void **)&paa, sizeof(float) * (size_t)N * nseg, st));
+    cudaError_t e = cudaMallocAsync((void **)&maxabs, sizeof(unsigned), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(maxabs, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(paa, st);
+        return ssh_cuda_fail(e, "ssh_build_index summaries", __FILE__, __LINE__);
+    }
+    int rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st, paa, maxabs);
+    if (rc == SSH_OK)
+        rc = ssh_launch_shingle_cws(ctx, bits, nullptr, nullptr, nullptr, N, nullptr, nullptr, nullptr,
+                                    nullptr, sig, SIG_MODE_FUSED, st);
+    if (rc == SSH_OK) rc = ssh_index_build(ctx, sig, N, id_base, out, stream);
+    if (rc != SSH_OK) {
+        cudaFreeAsync(paa, st);
+        cudaFreeAsync(maxabs, st);
+        return rc;
+    }
+    (*out)->paa = paa;
+    (*out)->d_maxabs = maxabs;
+    (*out)->nseg = nseg;
     return SSH_OK;
 }

@@ -344,13 +344,13 @@ def build_index(dataset, params: SshParams, normalized: bool = True, threads: in
     dev = _device_index(device)
     ctx = get_context(dev, params, dataset.length)
     X = _as_device_f32(dataset.values, dev)
-    sig = compute_signatures_device(ctx, X)
+    torch = _torch()
+    sig = torch.empty((int(X.shape[0]), params.d), dtype=torch.int64, device=X.device)
     handle = ctypes.c_void_p()
-    nat.check(nat.lib().ssh_index_build(ctx.handle, nat.ptr(sig), int(X.shape[0]), int(id_base),
-                                        ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_build")
+    nat.check(nat.lib().ssh_build_index(ctx.handle, nat.ptr(X), int(X.shape[0]), int(X.stride(0)),
+                                        int(id_base), nat.ptr(sig), ctypes.byref(handle),
+                                        _stream_ptr(dev)), "ssh_build_index")
     tables = _TablesHandle(handle)
-    nat.check(nat.lib().ssh_index_summarize(ctx.handle, handle, nat.ptr(X), int(X.stride(0)),
-                                            _stream_ptr(dev)), "ssh_index_summarize")
     return SshIndex(params=params, filter=ctx.filter, dataset=dataset, normalized=normalized,
                     device=dev, X=X, sig_dev=sig, id_base=id_base, _tables=tables)
 
