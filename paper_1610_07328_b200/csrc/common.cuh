@@ -62,7 +62,9 @@ struct ssh_ctx {
     unsigned long long *d_cells = nullptr;  // device counters: [0] DTW cells evaluated,
                                             // [1] LB_PAA prunes, [2] LB_Keogh prunes,
                                             // [3] members visited by the filter
-    int surv_cap = 4096;  // per-query survivor capacity (grows, remembered across batches)
+    // side stream for independent build work (candidate envelopes), joined by events
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // named grow-only scratch slots reused across calls (stream-ordered)
     void *slot_ptr[32] = {nullptr};
     size_t slot_bytes[32] = {0};
@@ -86,6 +88,8 @@ enum {
     SLOT_Q_D32,
     SLOT_Q_TOPK,
     SLOT_SIG,
+    SLOT_Q_KEEP,
+    SLOT_Q_KEEP_D,
     SLOT_COUNT
 };
 
@@ -96,6 +100,9 @@ struct ssh_index {
     int nseg = 0;
     float paa_delta = 0.f;  // bound on |stored mean - exact mean|
     unsigned *d_maxabs = nullptr;
+    // envelope of every row (running max/min over +-radius), fp16 rounded
+    // outward: xenv[row][i] = (upper_i rounded up, lower_i rounded down)
+    void *xenv = nullptr;
     int64_t N = 0;
     int64_t id_base = 0;
     int device = 0;
@@ -113,6 +120,8 @@ struct ssh_index {
 void *ssh_slot(ssh_ctx *ctx, int slot, size_t bytes, cudaStream_t st);
 
 #define SSH_PAA_SEG 32  // samples per PAA segment (rerank lower bound)
+
+int ssh_launch_xenv(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, void *xenv, cudaStream_t st);
 
 // ----------------------------------------------------------- device math
 __host__ __device__ __forceinline__ uint64_t ssh_mix64(uint64_t x) {

@@ -95,6 +95,12 @@ extern "C" int ssh_ctx_create(int device, ssh_ctx **out) {
     SSH_REQUIRE(c != nullptr, SSH_ERR_OOM, "ssh_ctx_create: host allocation failed");
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        delete c;
+        return ssh_cuda_fail(cudaGetLastError(), "ssh_ctx_create streams", __FILE__, __LINE__);
+    }
     *out = c;
     return SSH_OK;
 }
@@ -117,6 +123,9 @@ extern "C" int ssh_ctx_destroy(ssh_ctx *ctx) {
     for (int i = 0; i < 32; i++)
         if (ctx->slot_ptr[i]) cudaFree(ctx->slot_ptr[i]);
     if (ctx->d_cells) cudaFree(ctx->d_cells);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     delete ctx;
     return SSH_OK;
 }

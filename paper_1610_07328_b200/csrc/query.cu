@@ -32,10 +32,10 @@
 #include <algorithm>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
-#define Q_SURV_CAP0 4096
-#define Q_SEED_CAND 4096
 #define MB_THREADS 256
 #define MB_WARPS (MB_THREADS / 32)
 #define MB_SLICE_WORDS 256
@@ -250,6 +250,87 @@ __global__ void paa_kernel(const float *__restrict__ X, int64_t N, int m, int64_
     if (lane == 0) atomicMax(maxabs, __float_as_uint(mx));
 }
 
+// Envelope of every row (dtw.py:124-151 semantics: max/min over [i-r, i+r]),
+// stored as fp16 pairs rounded outward (upper up, lower down), so
+// LB_Keogh(q, env(x)) computed from them never exceeds the exact bound.
+// One CTA per row tile; log-step doubling over a padded shared-memory copy.
+// One warp per row: padded copy (-inf/+inf outside [0, m)) in the warp's
+// shared-memory slice, log-step doubling with register staging and
+// __syncwarp only, then u_i = max(A[i], A[i + win - 2^lev]).
+#define XE_WARPS 8
+__global__ void __launch_bounds__(32 * XE_WARPS)
+xenv_kernel(const float *__restrict__ X, int64_t N, int m, int64_t ld, int r, int lev, int pad,
+            __half2 *__restrict__ out) {
+    extern __shared__ float xsm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float *mx = xsm + (size_t)w * 2 * pad, *mn = mx + pad;
+    const int win = 2 * r + 1;
+    const int sh = win - (1 << lev);
+    const int64_t nwarps = (int64_t)gridDim.x * XE_WARPS;
+    for (int64_t row = (int64_t)blockIdx.x * XE_WARPS + w; row < N; row += nwarps) {
+        const float *x = X + row * ld;
+        for (int t = lane; t < pad; t += 32) {
+            const int j = t - r;
+            const bool in = j >= 0 && j < m;
+            const float v = in ? __ldg(x + j) : 0.f;
+            mx[t] = in ? v : -INFINITY;
+            mn[t] = in ? v : INFINITY;
+        }
+        __syncwarp();
+        for (int l = 0; l < lev; l++) {
+            const int d = 1 << l;
+            for (int t0 = 0; t0 < pad; t0 += 32 * 8) {
+                float a[8], b[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int t = t0 + u * 32 + lane;
+                    if (t + d < pad) {
+                        a[u] = fmaxf(mx[t], mx[t + d]);
+                        b[u] = fminf(mn[t], mn[t + d]);
+                    } else if (t < pad) {
+                        a[u] = mx[t];
+                        b[u] = mn[t];
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int t = t0 + u * 32 + lane;
+                    if (t < pad) {
+                        mx[t] = a[u];
+                        mn[t] = b[u];
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (int i = lane; i < m; i += 32) {
+            const float u = fmaxf(mx[i], mx[i + sh]);
+            const float lo = fminf(mn[i], mn[i + sh]);
+            out[row * m + i] = __halves2half2(__float2half_ru(u), __float2half_rd(lo));
+        }
+        __syncwarp();
+    }
+}
+
+int ssh_launch_xenv(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, void *xenv, cudaStream_t st) {
+    const int m = ctx->p.m, r = ctx->p.radius;
+    int lev = 0;
+    while ((2 << lev) <= 2 * r + 1) lev++;
+    const int pad = m + 2 * r + (1 << lev);
+    const size_t smem = (size_t)XE_WARPS * 2 * pad * sizeof(float);
+    SSH_REQUIRE(smem <= 220 * 1024, SSH_ERR_UNSUPPORTED,
+                "series too long for the envelope kernel (m=%d, r=%d)", m, r);
+    SSH_CUDA(cudaFuncSetAttribute(xenv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xenv_kernel, 32 * XE_WARPS, smem);
+    const int grid = (int)std::min<int64_t>((N + XE_WARPS - 1) / XE_WARPS,
+                                            (int64_t)ctx->num_sms * std::max(1, per_sm));
+    xenv_kernel<<<grid, 32 * XE_WARPS, smem, st>>>(X, N, m, ld, r, lev, pad, (__half2 *)xenv);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
 extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t ld,
                                    void *stream) {
     SSH_REQUIRE(ctx && ix && X, SSH_ERR_INVALID, "ssh_index_summarize: NULL argument");
@@ -264,6 +345,11 @@ extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, 
         SSH_CUDA(cudaMallocAsync((void **)&ix->d_maxabs, sizeof(unsigned), st));
     }
     ix->nseg = nseg;
+    if (!ix->xenv) SSH_CUDA(cudaMallocAsync(&ix->xenv, sizeof(uint32_t) * (size_t)ix->N * m, st));
+    {
+        int rc = ssh_launch_xenv(ctx, X, ix->N, ld, ix->xenv, st);
+        if (rc) return rc;
+    }
     SSH_CUDA(cudaMemsetAsync(ix->d_maxabs, 0, sizeof(unsigned), st));
     int grid = (int)std::min<int64_t>((ix->N + 7) / 8, (int64_t)ctx->num_sms * 16);
     paa_kernel<<<grid, 256, 0, st>>>(X, ix->N, m, ld, nseg, ix->paa, ix->d_maxabs);
@@ -271,77 +357,51 @@ extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, 
     return SSH_OK;
 }
 
-// --------------------------------------------------- member stream kernel
+// --------------------------------------------------- LB_PAA of every member
 // One CTA per (query, slice of MB_SLICE_WORDS bitmap words).  A warp turns 32
-// words into a member list in shared memory, evaluates LB_PAA lane-per-member
-// (L2-resident summaries), and
-//   MODE_HIST    histograms LB_PAA (seed threshold),
-//   MODE_COLLECT lists members with LB_PAA below the per-query threshold,
-//   MODE_FILTER  keeps members with LB_PAA <= thr and runs LB_Kim + the
-//                early-abandoning LB_Keogh warp-cooperatively; survivors are
-//                appended with their LB_Keogh value.
-enum { MODE_HIST = 0, MODE_COLLECT = 1, MODE_FILTER = 2 };
-
-struct MemberArgs {
-    const float *X;
-    const float *Q;
-    const float *U, *Lo, *Useg, *Lseg;
-    const float *paa;
+// words into a member list in shared memory, reserves space in the query's
+// CSR segment with one atomic, and evaluates LB_PAA lane-per-member from the
+// L2-resident PAA summary (float4 gathers):
+//   LB_PAA = sum_seg len * max(xbar - Useg - delta, Lseg - xbar - delta, 0)^2 * shrink
+// where Useg/Lseg are the segment max/min of the query envelope, delta bounds
+// the stored-mean error (2u max|x|) and shrink the fp32 evaluation error.
+struct PaaArgs {
+    const float *Useg, *Lseg, *paa;
     const unsigned *maxabs;
     const uint32_t *bitmap;
-    const float *thr;
-    const uint32_t *ts;
-    uint32_t *hist;
-    uint32_t *out;
-    float *out_lb;
-    int *out_cnt;
-    long long *counters;
-    unsigned long long *dbg;  // profiling counters (ctx->d_cells) or NULL
+    const int64_t *roff;  // per-query CSR offset of the member list
+    uint32_t *rows;
+    float *lb;
+    int *cnt;
     int64_t NW;
-    int m, nseg, cap;
+    int m, nseg;
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(MB_THREADS) members_kernel(MemberArgs a) {
+__global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
     extern __shared__ __align__(16) unsigned char msm[];
     const int q = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int m = a.m, nseg = a.nseg;
+    const int nseg = a.nseg;
     float *sUs = reinterpret_cast<float *>(msm);
     float *sLs = sUs + nseg;
-    uint32_t *lists = reinterpret_cast<uint32_t *>(sLs + nseg);  // MB_WARPS x 1024
-    uint32_t *shist = lists + MB_WARPS * 1024;                   // NBINS (HIST)
-    float *su = reinterpret_cast<float *>(lists + MB_WARPS * 1024);  // m (FILTER)
-    float *sl = su + m;
+    uint32_t *list = reinterpret_cast<uint32_t *>(sLs + nseg) + w * 1024;
     for (int s = threadIdx.x; s < nseg; s += MB_THREADS) {
         sUs[s] = a.Useg[(int64_t)q * nseg + s];
         sLs[s] = a.Lseg[(int64_t)q * nseg + s];
     }
-    if (MODE == MODE_HIST)
-        for (int b = threadIdx.x; b < NBINS; b += MB_THREADS) shist[b] = 0u;
-    if (MODE == MODE_FILTER)
-        for (int i = threadIdx.x; i < m; i += MB_THREADS) {
-            su[i] = a.U[(int64_t)q * m + i];
-            sl[i] = a.Lo[(int64_t)q * m + i];
-        }
     __syncthreads();
-    // |stored mean - exact mean| <= 2u max|x|; products/sums: relative (2 nseg + 8) u
     const float delta = 2.f * U32_EPS * __uint_as_float(*a.maxabs) + 1e-30f;
     const float shrink = 1.f - (2.f * nseg + 8.f) * U32_EPS;
-    const float lastlen = (float)(m - (nseg - 1) * SSH_PAA_SEG);
-    const float T = MODE == MODE_FILTER ? a.thr[q] : 0.f;
-    const uint32_t TS = MODE == MODE_COLLECT ? a.ts[q] : 0u;
-    const float q0 = a.Q[(int64_t)q * m], ql = a.Q[(int64_t)q * m + m - 1];
+    const float lastlen = (float)(a.m - (nseg - 1) * SSH_PAA_SEG);
+    const bool vec = (nseg & 3) == 0;
     const uint32_t *bm = a.bitmap + (int64_t)q * a.NW;
-    uint32_t *list = lists + w * 1024;
-    int paa_pr = 0, kim = 0, keo = 0, nvisit = 0;
+    const int64_t base_q = a.roff[q];
     const int64_t s0 = (int64_t)blockIdx.x * MB_SLICE_WORDS;
     const int64_t s1 = min(a.NW, s0 + MB_SLICE_WORDS);
-    const unsigned lt = (1u << lane) - 1u;
     for (int64_t wb = s0 + 32 * w; wb < s1; wb += 32 * MB_WARPS) {
         const int64_t wd = wb + lane;
         uint32_t word = wd < s1 ? bm[wd] : 0u;
-        int c = __popc(word);
+        const int c = __popc(word);
         int incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -349,170 +409,178 @@ __global__ void __launch_bounds__(MB_THREADS) members_kernel(MemberArgs a) {
             if (lane >= o) incl += y;
         }
         const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        nvisit += lane == 0 ? total : 0;
+        if (total == 0) continue;
         int pos = incl - c;
         while (word) {
             int b = __ffs(word) - 1;
             word &= word - 1;
             list[pos++] = (uint32_t)(wd * 32 + b);
         }
+        int dst = 0;
+        if (lane == 0) dst = atomicAdd(&a.cnt[q], total);
+        dst = __shfl_sync(0xFFFFFFFFu, dst, 0);
         __syncwarp();
-        // stage A: LB_PAA, lane per member
-        int kept = 0;
-        for (int base = 0; base < total; base += 32) {
-            const int e = base + lane;
-            bool keep = false;
-            uint32_t row = 0;
-            if (e < total) {
-                row = list[e];
-                const float *p = a.paa + (int64_t)row * nseg;
-                float acc = 0.f;
-                for (int s = 0; s < nseg; s++) {
-                    float xb = __ldg(p + s);
-                    float ev = fmaxf(fmaxf(xb - sUs[s] - delta, sLs[s] - xb - delta), 0.f);
-                    float len = s + 1 < nseg ? (float)SSH_PAA_SEG : lastlen;
-                    acc = fmaf(len * ev, ev, acc);
-                }
-                const float lb = acc * shrink;
-                if (MODE == MODE_HIST) {
-                    atomicAdd(&shist[lb_bin(lb)], 1u);
-                } else if (MODE == MODE_COLLECT) {
-                    if (__float_as_uint(lb) < TS) {
-                        int p2 = atomicAdd(&a.out_cnt[q], 1);
-                        if (p2 < a.cap) {
-                            a.out[(int64_t)q * a.cap + p2] = row;
-                            a.out_lb[(int64_t)q * a.cap + p2] = lb;
-                        }
-                    }
-                } else {
-                    keep = !(lb > T);
-                    paa_pr += !keep;
-                }
-            }
-            if (MODE == MODE_FILTER) {
-                unsigned msk = __ballot_sync(0xFFFFFFFFu, keep);
-                if (keep) list[kept + __popc(msk & lt)] = row;
-                kept += __popc(msk);
-                __syncwarp();
-            }
-        }
-        if (MODE == MODE_FILTER) {
-            // stage B: LB_Kim + early-abandoning LB_Keogh, warp per member
-            for (int e = 0; e < kept; e++) {
-                const uint32_t row = list[e];
-                const float *x = a.X + (int64_t)row * m;
-                if (m >= 2) {
-                    float d0 = x[0] - q0, dl = x[m - 1] - ql;
-                    if (fmaf(dl, dl, d0 * d0) > T) { kim++; continue; }
-                }
-                float acc = 0.f, tot = 0.f;
-                bool pruned = false;
-                for (int base = 0; base < m; base += 128) {
+        for (int e = lane; e < total; e += 32) {
+            const uint32_t row = list[e];
+            const float *p = a.paa + (int64_t)row * nseg;
+            float acc = 0.f;
+            if (vec) {
+                for (int s = 0; s < nseg; s += 4) {
+                    const float4 v = __ldg(reinterpret_cast<const float4 *>(p + s));
+                    const float xv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        int i = base + k * 32 + lane;
-                        if (i < m) {
-                            float cv = __ldg(x + i);
-                            float v = fmaxf(fmaxf(cv - su[i], sl[i] - cv), 0.f);
-                            acc = fmaf(v, v, acc);
-                        }
-                    }
-                    tot = warp_sum(acc);
-                    if (tot > T) { pruned = true; break; }
-                }
-                if (pruned) { keo++; continue; }
-                if (lane == 0) {
-                    int p2 = atomicAdd(&a.out_cnt[q], 1);
-                    if (p2 < a.cap) {
-                        a.out[(int64_t)q * a.cap + p2] = row;
-                        a.out_lb[(int64_t)q * a.cap + p2] = tot;
-                    }
-                }
-            }
-        }
-        __syncwarp();
-    }
-    if (MODE == MODE_HIST) {
-        __syncthreads();
-        for (int b = threadIdx.x; b < NBINS; b += MB_THREADS) {
-            uint32_t v = shist[b];
-            if (v) atomicAdd(&a.hist[(int64_t)q * NBINS + b], v);
-        }
-    }
-    if (MODE == MODE_FILTER) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) paa_pr += __shfl_xor_sync(0xFFFFFFFFu, paa_pr, o);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nvisit += __shfl_xor_sync(0xFFFFFFFFu, nvisit, o);
-        if (lane == 0) {
-            long long k1 = kim, k2 = (long long)keo + paa_pr;
-            if (k1) atomicAdd((unsigned long long *)&a.counters[q * 5 + 0], (unsigned long long)k1);
-            if (k2) atomicAdd((unsigned long long *)&a.counters[q * 5 + 1], (unsigned long long)k2);
-            if (a.dbg) {
-                atomicAdd(&a.dbg[1], (unsigned long long)paa_pr);
-                atomicAdd(&a.dbg[2], (unsigned long long)keo);
-                atomicAdd(&a.dbg[3], (unsigned long long)nvisit);
-            }
-        }
-    }
-}
-
-// per query: LB_PAA bin threshold holding >= S0 members
-__global__ void seed_thresh_kernel(const uint32_t *__restrict__ hist, int S0, uint32_t *__restrict__ ts) {
-    __shared__ uint32_t part[NBINS / 8];
-    const int q = blockIdx.x;
-    const uint32_t *h = hist + (int64_t)q * NBINS;
-    uint32_t s = 0;
-    for (int b = 0; b < 8; b++) s += h[threadIdx.x * 8 + b];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t cum = 0;
-        uint32_t out = 0xFFFFFFFFu;
-        for (int t = 0; t < NBINS / 8 && out == 0xFFFFFFFFu; t++) {
-            if (cum + part[t] >= (uint32_t)S0) {
-                for (int b = 0; b < 8; b++) {
-                    cum += h[t * 8 + b];
-                    if (cum >= (uint32_t)S0) {
-                        int bin = t * 8 + b;
-                        out = bin + 1 >= NBINS ? 0xFFFFFFFFu : ((uint32_t)(bin + 1) << 20);
-                        break;
+                    for (int t = 0; t < 4; t++) {
+                        const float ev = fmaxf(fmaxf(xv[t] - sUs[s + t] - delta, sLs[s + t] - xv[t] - delta), 0.f);
+                        const float len = s + t + 1 < nseg ? (float)SSH_PAA_SEG : lastlen;
+                        acc = fmaf(len * ev, ev, acc);
                     }
                 }
             } else {
-                cum += part[t];
+                for (int s = 0; s < nseg; s++) {
+                    const float xb = __ldg(p + s);
+                    const float ev = fmaxf(fmaxf(xb - sUs[s] - delta, sLs[s] - xb - delta), 0.f);
+                    const float len = s + 1 < nseg ? (float)SSH_PAA_SEG : lastlen;
+                    acc = fmaf(len * ev, ev, acc);
+                }
             }
+            a.rows[base_q + dst + e] = row;
+            a.lb[base_q + dst + e] = acc * shrink;
         }
-        ts[q] = out;
+        __syncwarp();
     }
 }
 
-// per query: the S0 collected members with the smallest LB_PAA -> seeds
-__global__ void seed_select_kernel(const uint32_t *__restrict__ cand, const float *__restrict__ cand_lb,
-                                   const int *__restrict__ cand_cnt, int cap, int S0,
-                                   uint32_t *__restrict__ seeds, int *__restrict__ nseed) {
-    __shared__ int red[32];
-    __shared__ int npos;
+// Per query: members reordered by LB bin (float bits >> 20, ~12% wide) with a
+// counting sort; within a bin the order is arbitrary (the wave loop relies
+// only on non-decreasing bins).
+__global__ void __launch_bounds__(1024)
+binsort_kernel(const uint32_t *__restrict__ rows_in, const float *__restrict__ lb_in,
+               const int64_t *__restrict__ roff, const int *__restrict__ cnt,
+               uint32_t *__restrict__ rows_out, float *__restrict__ lb_out) {
+    __shared__ uint32_t h[NBINS];
+    __shared__ uint32_t part[1024];
     const int q = blockIdx.x;
-    uint32_t *out = seeds + (int64_t)q * S0;
-    const int n = min(cand_cnt[q], cap);
-    const uint32_t *bits = reinterpret_cast<const uint32_t *>(cand_lb + (int64_t)q * cap);
-    uint32_t V = 0xFFFFFFFFu;
-    if (n > S0) V = block_kth2<uint32_t>(bits, n, nullptr, 0, S0, 0x7F800000u, red);
-    if (threadIdx.x == 0) npos = 0;
+    const int64_t o = roff[q];
+    const int n = cnt[q];
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) h[b] = 0u;
     __syncthreads();
-    for (int e = threadIdx.x; e < n; e += blockDim.x)
-        if (n <= S0 || bits[e] < V) out[atomicAdd(&npos, 1)] = cand[(int64_t)q * cap + e];
+    for (int e = threadIdx.x; e < n; e += blockDim.x) atomicAdd(&h[lb_bin(lb_in[o + e])], 1u);
     __syncthreads();
-    for (int e = threadIdx.x; e < n; e += blockDim.x)
-        if (n > S0 && bits[e] == V) {
-            int p = atomicAdd(&npos, 1);
-            if (p < S0) out[p] = cand[(int64_t)q * cap + e];
+    const int per = NBINS / blockDim.x;
+    uint32_t loc = 0;
+    for (int i = 0; i < per; i++) loc += h[threadIdx.x * per + i];
+    part[threadIdx.x] = loc;
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+        uint32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[threadIdx.x] - loc;
+    for (int i = 0; i < per; i++) {
+        uint32_t c = h[threadIdx.x * per + i];
+        h[threadIdx.x * per + i] = run;
+        run += c;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const float v = lb_in[o + e];
+        const uint32_t p = atomicAdd(&h[lb_bin(v)], 1u);
+        rows_out[o + p] = rows_in[o + e];
+        lb_out[o + p] = v;
+    }
+}
+
+// One wave, part 1: members [pos_q, pos_q + wave) of the LB_PAA-sorted list,
+// warp per member.  Skip LB_PAA > thr; else LB_Kim; then LB_Keogh(x, env(q))
+// and LB_Keogh2 = LB_Keogh(q, env(x)) (the candidate envelopes precomputed at
+// build, fp16 rounded outward), each in 128-sample chunks abandoning once the
+// partial sum exceeds thr (dtw.py:154-168, 206-215).  Survivors go to the
+// wave's DTW list.
+struct WaveLbArgs {
+    const float *X, *Q, *U, *Lo;
+    const __half2 *xenv;
+    const uint32_t *srows;
+    const float *slbp;
+    const int64_t *roff;
+    const int *cnt, *pos, *done;
+    const float *thr;
+    uint32_t *wrows;
+    int *wcnt;
+    long long *counters;
+    int m, wave, wcap;
+};
+
+__global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
+    extern __shared__ float wsm[];
+    const int q = blockIdx.y;
+    if (a.done[q]) return;
+    const int m = a.m;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int start = a.pos[q];
+    const int end = min(a.cnt[q], start + a.wave);
+    if (start + (int)blockIdx.x * nw >= end) return;
+    float *su = wsm, *sl = wsm + m, *sq = wsm + 2 * m;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        su[i] = a.U[(int64_t)q * m + i];
+        sl[i] = a.Lo[(int64_t)q * m + i];
+        sq[i] = a.Q[(int64_t)q * m + i];
+    }
+    __syncthreads();
+    const float T = a.thr[q];
+    const float q0 = sq[0], ql = sq[m - 1];
+    const int64_t o = a.roff[q];
+    int paa = 0, kim = 0, keo = 0, keo2 = 0;
+    for (int e = start + blockIdx.x * nw + w; e < end; e += gridDim.x * nw) {
+        if (a.slbp[o + e] > T) { paa++; continue; }
+        const uint32_t row = a.srows[o + e];
+        const float *x = a.X + (int64_t)row * m;
+        if (m >= 2) {
+            const float d0 = x[0] - q0, dl = x[m - 1] - ql;
+            if (fmaf(dl, dl, d0 * d0) > T) { kim++; continue; }
         }
-    __syncthreads();
-    const int c = min(npos, S0);
-    for (int e = c + threadIdx.x; e < S0; e += blockDim.x) out[e] = 0xFFFFFFFFu;
-    if (threadIdx.x == 0) nseed[q] = c;
+        float acc = 0.f;
+        bool pruned = false;
+        for (int base = 0; base < m; base += 128) {
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int i = base + k * 32 + lane;
+                if (i < m) {
+                    const float cv = __ldg(x + i);
+                    const float v = fmaxf(fmaxf(cv - su[i], sl[i] - cv), 0.f);
+                    acc = fmaf(v, v, acc);
+                }
+            }
+            if (warp_sum(acc) > T) { pruned = true; break; }
+        }
+        if (pruned) { keo++; continue; }
+        const __half2 *ev = a.xenv + (int64_t)row * m;
+        acc = 0.f;
+        for (int base = 0; base < m; base += 128) {
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int i = base + k * 32 + lane;
+                if (i < m) {
+                    const float2 ul = __half22float2(ev[i]);
+                    const float qv = sq[i];
+                    const float v = fmaxf(fmaxf(qv - ul.x, ul.y - qv), 0.f);
+                    acc = fmaf(v, v, acc);
+                }
+            }
+            if (warp_sum(acc) > T) { pruned = true; break; }
+        }
+        if (pruned) { keo2++; continue; }
+        if (lane == 0) {
+            const int p = atomicAdd(&a.wcnt[q], 1);
+            if (p < a.wcap) a.wrows[(int64_t)q * a.wcap + p] = row;
+        }
+    }
+    if (lane == 0) {
+        if (kim) atomicAdd((unsigned long long *)&a.counters[q * 5 + 0], (unsigned long long)kim);
+        if (paa + keo) atomicAdd((unsigned long long *)&a.counters[q * 5 + 1], (unsigned long long)(paa + keo));
+        if (keo2) atomicAdd((unsigned long long *)&a.counters[q * 5 + 2], (unsigned long long)keo2);
+    }
 }
 
 // ------------------------------------------------------------ fp32 DTW
@@ -801,89 +869,32 @@ __global__ void dtw64_kernel(const float *__restrict__ X, int m, int r, const fl
 }
 
 // ------------------------------------------------------- thresholds / waves
-// thr0 from the seed DTWs (k-th smallest of distinct seeds)
-__global__ void tau_kernel(const float *__restrict__ sd32, int S0, const int *__restrict__ nseed,
-                           int k, float eps, float *__restrict__ thr) {
+// One wave, part 3: fold the wave's fp32 DTWs into the per-query k smallest
+// (topk), tighten thr = min(thr, kth (1 + eps)), keep every evaluated
+// candidate with d32 <= thr (only those can reach the final rescoring set,
+// since thr never increases and always stays >= the final kth (1 + eps)),
+// advance the wave start and decide whether the query is done (next member's
+// LB_PAA bin above thr's bin => every remaining LB_PAA exceeds thr).
+__global__ void wave_update_kernel(const float *__restrict__ wd32, const uint32_t *__restrict__ wrows,
+                                   int *__restrict__ wcnt, int wcap, const float *__restrict__ slbp,
+                                   const int64_t *__restrict__ roff, const int *__restrict__ cnt,
+                                   int wave, int k, float eps, float *__restrict__ topk,
+                                   float *__restrict__ thr, int *__restrict__ pos,
+                                   int *__restrict__ done, int *__restrict__ active,
+                                   uint32_t *__restrict__ keep_rows, float *__restrict__ keep_d32,
+                                   int *__restrict__ keep_cnt, int kcap) {
     __shared__ int red[32];
-    const int q = blockIdx.x;
-    const int ns = nseed[q];
-    const uint32_t *bits = reinterpret_cast<const uint32_t *>(sd32 + (int64_t)q * S0);
-    float t = INFINITY;
-    if (k <= ns) {
-        int nfin = block_count_le2<uint32_t>(bits, ns, nullptr, 0, 0x7F7FFFFFu, red);
-        if (nfin >= k) t = __uint_as_float(block_kth2<uint32_t>(bits, ns, nullptr, 0, k, 0x7F7FFFFFu, red));
-    }
-    if (threadIdx.x == 0) thr[q] = thr_from(t, eps);
-}
-
-// Per query: survivors reordered by LB_Keogh bin (float bits >> 20, ~12% wide)
-// with a counting sort.  Within a bin the order is arbitrary; the wave loop
-// only relies on bins being non-decreasing.
-__global__ void __launch_bounds__(1024)
-lbsort_kernel(const uint32_t *__restrict__ surv, const float *__restrict__ slb,
-              const int *__restrict__ surv_cnt, int cap, uint32_t *__restrict__ srow,
-              float *__restrict__ slbs) {
-    __shared__ uint32_t h[NBINS];
-    const int q = blockIdx.x;
-    const int cnt = min(surv_cnt[q], cap);
-    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) h[b] = 0u;
-    __syncthreads();
-    const float *lb = slb + (int64_t)q * cap;
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) atomicAdd(&h[lb_bin(lb[e])], 1u);
-    __syncthreads();
-    // exclusive scan of NBINS (= 2 per thread at 1024 threads)
-    __shared__ uint32_t part[1024];
-    const int per = NBINS / blockDim.x;
-    uint32_t loc = 0;
-    for (int i = 0; i < per; i++) loc += h[threadIdx.x * per + i];
-    part[threadIdx.x] = loc;
-    __syncthreads();
-    for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-        uint32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
-    }
-    uint32_t run = part[threadIdx.x] - loc;
-    for (int i = 0; i < per; i++) {
-        uint32_t c = h[threadIdx.x * per + i];
-        h[threadIdx.x * per + i] = run;
-        run += c;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-        const float v = lb[e];
-        const uint32_t p = atomicAdd(&h[lb_bin(v)], 1u);
-        srow[(int64_t)q * cap + p] = surv[(int64_t)q * cap + e];
-        slbs[(int64_t)q * cap + p] = v;
-    }
-}
-
-// After a wave: fold its fp32 DTWs into the per-query k smallest (topk),
-// tighten thr = min(thr, kth (1 + eps)), advance the wave start and decide
-// whether the query is done (next entry's LB bin above thr's bin => every
-// remaining LB exceeds thr).  Sets *active if any query continues.
-__global__ void wave_update_kernel(const float *__restrict__ d32, const float *__restrict__ slbs,
-                                   const int *__restrict__ cnt, int cap, int wave, int k, float eps,
-                                   float *__restrict__ topk, float *__restrict__ thr,
-                                   int *__restrict__ pos, int *__restrict__ done,
-                                   int *__restrict__ active) {
-    __shared__ int red[32];
+    __shared__ uint32_t tmp[2048];
+    __shared__ int npos;
     const int q = blockIdx.x;
     if (done[q]) return;
-    const int start = pos[q];
-    const int total = min(cnt[q], cap);
-    const int end = min(total, start + wave);
-    const uint32_t *wb = reinterpret_cast<const uint32_t *>(d32 + (int64_t)q * cap + start);
+    const int nw = min(wcnt[q], wcap);
+    const uint32_t *wb = reinterpret_cast<const uint32_t *>(wd32 + (int64_t)q * wcap);
     uint32_t *tb = reinterpret_cast<uint32_t *>(topk + (int64_t)q * k);
-    const int nw = end - start;
     const int nfin = block_count_le2<uint32_t>(tb, k, wb, nw, 0x7F7FFFFFu, red);
     float T = thr[q];
     if (nfin >= k) {
         const uint32_t kv = block_kth2<uint32_t>(tb, k, wb, nw, k, 0x7F7FFFFFu, red);
-        // new topk: values < kv, padded with kv
-        __shared__ int npos;
-        __shared__ uint32_t tmp[2048];
         if (threadIdx.x == 0) npos = 0;
         __syncthreads();
         for (int e = threadIdx.x; e < k; e += blockDim.x)
@@ -895,38 +906,51 @@ __global__ void wave_update_kernel(const float *__restrict__ d32, const float *_
         for (int e = threadIdx.x; e < k; e += blockDim.x) tb[e] = e < c ? tmp[e] : kv;
         T = fminf(T, thr_from(__uint_as_float(kv), eps));
     } else {
-        // fewer than k finite values so far: append the wave's finite values
-        __shared__ int npos2;
         if (threadIdx.x == 0) {
             int c = 0;
             for (int e = 0; e < k; e++) c += tb[e] <= 0x7F7FFFFFu;
-            npos2 = c;
+            npos = c;
         }
         __syncthreads();
         for (int e = threadIdx.x; e < nw; e += blockDim.x)
-            if (wb[e] <= 0x7F7FFFFFu) tb[atomicAdd(&npos2, 1)] = wb[e];
+            if (wb[e] <= 0x7F7FFFFFu) tb[atomicAdd(&npos, 1)] = wb[e];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nw; e += blockDim.x) {
+        const float v = wd32[(int64_t)q * wcap + e];
+        if (v <= T) {
+            const int p = atomicAdd(&keep_cnt[q], 1);
+            if (p < kcap) {
+                keep_rows[(int64_t)q * kcap + p] = wrows[(int64_t)q * wcap + e];
+                keep_d32[(int64_t)q * kcap + p] = v;
+            }
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         thr[q] = T;
+        wcnt[q] = 0;
+        const int total = cnt[q];
+        const int end = min(total, pos[q] + wave);
         pos[q] = end;
-        const bool fin = end >= total || lb_bin(slbs[(int64_t)q * cap + end]) > lb_bin(T);
+        const bool fin = end >= total || lb_bin(slbp[roff[q] + end]) > lb_bin(T);
         done[q] = fin;
         if (!fin) atomicOr(active, 1);
     }
 }
 
-// rescoring set over every wave: d32 <= T_k (1 + eps)
-__global__ void select_kernel(const uint32_t *__restrict__ srow, const float *__restrict__ d32,
-                              const int *__restrict__ pos, int cap, int k, float eps,
+// Rescoring set: kept candidates with d32 <= T_k (1 + eps), T_k = k-th
+// smallest kept d32 (the kept set contains the k smallest of all evaluated).
+__global__ void select_kernel(const uint32_t *__restrict__ keep_rows, const float *__restrict__ keep_d32,
+                              const int *__restrict__ keep_cnt, int kcap, int k, float eps,
                               uint32_t *__restrict__ resc, int *__restrict__ resc_cnt,
                               long long *__restrict__ counters, const int *__restrict__ cnt,
-                              const int *__restrict__ computed) {
+                              const int *__restrict__ pos) {
     __shared__ int red[32];
     __shared__ int npos;
     const int q = blockIdx.x;
-    const int n = pos[q];
-    const uint32_t *b = reinterpret_cast<const uint32_t *>(d32 + (int64_t)q * cap);
+    const int n = min(keep_cnt[q], kcap);
+    const uint32_t *b = reinterpret_cast<const uint32_t *>(keep_d32 + (int64_t)q * kcap);
     const int nfin = block_count_le2<uint32_t>(b, n, nullptr, 0, 0x7F7FFFFFu, red);
     const int kk = min(k, nfin);
     float bound = -1.f;
@@ -934,12 +958,12 @@ __global__ void select_kernel(const uint32_t *__restrict__ srow, const float *__
     if (threadIdx.x == 0) npos = 0;
     __syncthreads();
     for (int e = threadIdx.x; e < n; e += blockDim.x)
-        if (d32[(int64_t)q * cap + e] <= bound) resc[(int64_t)q * cap + atomicAdd(&npos, 1)] = srow[(int64_t)q * cap + e];
+        if (keep_d32[(int64_t)q * kcap + e] <= bound)
+            resc[(int64_t)q * kcap + atomicAdd(&npos, 1)] = keep_rows[(int64_t)q * kcap + e];
     __syncthreads();
     if (threadIdx.x == 0) {
         resc_cnt[q] = npos;
-        // survivors never evaluated were excluded by LB_Keogh > thr
-        counters[q * 5 + 1] += min(cnt[q], cap) - computed[q];
+        counters[q * 5 + 1] += cnt[q] - pos[q];  // never visited: LB_PAA > thr
     }
 }
 
@@ -999,16 +1023,34 @@ __global__ void topk_kernel(const uint32_t *__restrict__ resc, const double *__r
     if (threadIdx.x == 0) n_out[q] = n;
 }
 
-__global__ void finalize_counters(const int *__restrict__ nseed, const int *__restrict__ computed,
+__global__ void finalize_counters(const int *__restrict__ computed,
                                   const unsigned long long *__restrict__ abandoned, int nq,
                                   const long long *__restrict__ n_cand,
                                   const int *__restrict__ is_fb, long long *__restrict__ counters,
                                   int *__restrict__ status) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
-    counters[q * 5 + 3] = (long long)nseed[q] + computed[q];
+    counters[q * 5 + 3] = computed[q];
     counters[q * 5 + 4] = (long long)abandoned[q];
     status[q] = n_cand[q] == 0 ? 1 : (is_fb[q] ? 2 : 0);
+}
+
+__global__ void wave_init_kernel(int nq, int k, const int *__restrict__ cnt, float *__restrict__ thr,
+                                 float *__restrict__ topk, int *__restrict__ pos, int *__restrict__ done,
+                                 int *__restrict__ wcnt, int *__restrict__ keep_cnt,
+                                 int *__restrict__ computed, unsigned long long *__restrict__ aband) {
+    const int64_t n = (int64_t)nq * k;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<uint32_t *>(topk)[e] = 0xFFFFFFFFu;  // NaN bits: above every finite value
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+        thr[q] = INFINITY;
+        pos[q] = 0;
+        done[q] = cnt[q] == 0;
+        wcnt[q] = 0;
+        keep_cnt[q] = 0;
+        computed[q] = 0;
+        aband[q] = 0ULL;
+    }
 }
 
 // ------------------------------------------------------------------ host
@@ -1046,69 +1088,68 @@ struct Carver {
 
 struct QueryBufs {
     uint64_t *qsig, *qbits, *bstart;
-    uint32_t *blen, *seeds, *w1, *ts, *cand;
-    int *isfb, *nseed, *scnt, *c1, *c2, *rcnt, *ccnt, *done, *active;
-    float *U, *Lo, *Useg, *Lseg, *sd32, *thr, *d1, *cand_lb;
+    uint32_t *blen;
+    int64_t *roff;
+    int *isfb, *mcnt, *pos, *done, *active, *wcnt, *keep_cnt, *rcnt, *computed;
+    float *U, *Lo, *Useg, *Lseg, *thr;
     unsigned long long *aband;
 
-    void carve(Carver &c, int nc, int L, int words, int S0, int W1, int m, int nseg) {
+    void carve(Carver &c, int nc, int L, int words, int m, int nseg) {
         qsig = c.take<uint64_t>((size_t)nc * L);
         qbits = c.take<uint64_t>((size_t)nc * words);
         bstart = c.take<uint64_t>((size_t)nc * L);
         blen = c.take<uint32_t>((size_t)nc * L);
-        seeds = c.take<uint32_t>((size_t)nc * S0);
-        w1 = c.take<uint32_t>((size_t)nc * W1);
-        ts = c.take<uint32_t>(nc);
-        cand = c.take<uint32_t>((size_t)nc * Q_SEED_CAND);
+        roff = c.take<int64_t>(nc + 1);
         isfb = c.take<int>(nc);
-        nseed = c.take<int>(nc);
-        scnt = c.take<int>(nc);
-        c1 = c.take<int>(nc);
-        c2 = c.take<int>(nc);
-        rcnt = c.take<int>(nc);
-        ccnt = c.take<int>(nc);
+        mcnt = c.take<int>(nc);
+        pos = c.take<int>(nc);
         done = c.take<int>(nc);
         active = c.take<int>(1);
+        wcnt = c.take<int>(nc);
+        keep_cnt = c.take<int>(nc);
+        rcnt = c.take<int>(nc);
+        computed = c.take<int>(nc);
         U = c.take<float>((size_t)nc * m);
         Lo = c.take<float>((size_t)nc * m);
         Useg = c.take<float>((size_t)nc * nseg);
         Lseg = c.take<float>((size_t)nc * nseg);
-        sd32 = c.take<float>((size_t)nc * S0);
         thr = c.take<float>(nc);
-        d1 = c.take<float>((size_t)nc * W1);
-        cand_lb = c.take<float>((size_t)nc * Q_SEED_CAND);
         aband = c.take<unsigned long long>(nc);
     }
 };
 
-struct PhaseTimer {
+// CUDA-event timing of a launch group into ctx->prof[slot] (profiling only)
+struct Prof {
     ssh_ctx *ctx;
     cudaStream_t st;
-    cudaEvent_t ev[8];
-    int n = 0;
+    cudaEvent_t a = nullptr, b = nullptr;
     bool on;
-    PhaseTimer(ssh_ctx *c, cudaStream_t s) : ctx(c), st(s), on(c->profile != 0) {
-        if (on)
-            for (int i = 0; i < 8; i++) cudaEventCreate(&ev[i]);
-    }
-    void mark() {
-        if (on && n < 8) cudaEventRecord(ev[n++], st);
-    }
-    void flush() {
-        if (!on || n == 0) return;
-        cudaEventSynchronize(ev[n - 1]);
-        for (int i = 1; i < n; i++) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
-            ctx->prof[i - 1] += ms;
+    Prof(ssh_ctx *c, cudaStream_t s) : ctx(c), st(s), on(c->profile != 0) {
+        if (on) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
         }
-        n = 0;
     }
-    ~PhaseTimer() {
-        if (on)
-            for (int i = 0; i < 8; i++) cudaEventDestroy(ev[i]);
+    void begin() {
+        if (on) cudaEventRecord(a, st);
+    }
+    void end(int slot) {
+        if (!on) return;
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        ctx->prof[slot] += ms;
+    }
+    ~Prof() {
+        if (on) {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
     }
 };
+
+
 
 int next_pow2(int v) {
     int p = 32;
@@ -1138,12 +1179,7 @@ int dtw64_threads(int r, size_t *smem) {
     return t;
 }
 
-size_t members_smem(int mode, int m, int nseg) {
-    size_t b = (size_t)2 * nseg * 4 + (size_t)MB_WARPS * 1024 * 4;
-    if (mode == MODE_HIST) b += NBINS * 4;
-    if (mode == MODE_FILTER) b += (size_t)2 * m * 4;
-    return b;
-}
+
 }  // namespace
 
 template <int R>
@@ -1196,17 +1232,6 @@ static int launch_dtw64_list(const float *X, int m, int r, const float *Q, const
     if (maxcnt <= 0) return SSH_OK;
     dim3 grid((unsigned)ssh_div_up(maxcnt, t), (unsigned)nq);
     dtw64_kernel<<<grid, t, smem, st>>>(X, m, r, Q, nullptr, list, stride, cnt, nullptr, 0, out);
-    SSH_CHECK_LAUNCH();
-    return SSH_OK;
-}
-
-template <int MODE>
-static int launch_members(const MemberArgs &a, int nq, cudaStream_t st) {
-    size_t smem = members_smem(MODE, a.m, a.nseg);
-    SSH_CUDA(cudaFuncSetAttribute(members_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    dim3 g((unsigned)ssh_div_up(a.NW, MB_SLICE_WORDS), (unsigned)nq);
-    members_kernel<MODE><<<g, MB_THREADS, smem, st>>>(a);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
@@ -1299,15 +1324,18 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     const int m = ctx->p.m, r = ctx->p.radius, L = ix->L, nseg = ix->nseg;
     const int64_t N = ix->N, NW = (N + 31) / 32;
     const float eps = rescore_eps(m);
-    const int S0 = ((std::max(64, 2 * k) + 31) / 32) * 32;
-    const int W1 = S0;
+    const int W0 = ((std::max(64, 2 * k) + 31) / 32) * 32;
+    const int WCAP = std::max(W0, 16384);
+    const int KCAP = 4096 + 4 * k;
     const int fallback = (flags & SSH_QUERY_FALLBACK_ON_EMPTY) ? 1 : 0;
-    // query chunk: keep the membership bitmaps under ~1 GiB
-    int qc = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(nq, 32768),
-                                                         ((int64_t)1 << 28) / std::max<int64_t>(1, NW)));
+    // query chunk: membership bitmaps <= 1 GiB and worst-case member lists <= 8 GiB
+    int64_t qc64 = std::min<int64_t>(nq, 32768);
+    qc64 = std::min<int64_t>(qc64, ((int64_t)1 << 28) / std::max<int64_t>(1, NW));
+    qc64 = std::min<int64_t>(qc64, ((int64_t)1 << 33) / std::max<int64_t>(1, N * 16));
+    const int qc = (int)std::max<int64_t>(1, qc64);
     SSH_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 5 * (size_t)nq, st));
-    int cap = std::max(Q_SURV_CAP0, ctx->surv_cap);
-    PhaseTimer pt(ctx, st);
+    SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(2 * nseg * 4 + MB_WARPS * 1024 * 4)));
     for (int q0 = 0; q0 < nq; q0 += qc) {
         const int nc = std::min(qc, nq - q0);
         const float *Qc = Q + (int64_t)q0 * m;
@@ -1315,144 +1343,139 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         long long *cnt5 = (long long *)counters + (int64_t)q0 * 5;
         Carver sizer;
         QueryBufs B;
-        B.carve(sizer, nc, L, ctx->words, S0, W1, m, nseg);
+        B.carve(sizer, nc, L, ctx->words, m, nseg);
         Carver cv;
         cv.base = (unsigned char *)ssh_slot(ctx, SLOT_Q_FIXED, sizer.off, st);
         if (!cv.base) return SSH_ERR_OOM;
-        B.carve(cv, nc, L, ctx->words, S0, W1, m, nseg);
+        B.carve(cv, nc, L, ctx->words, m, nseg);
         uint32_t *bitmap = (uint32_t *)ssh_slot(ctx, SLOT_Q_BITMAP, sizeof(uint32_t) * (size_t)nc * NW, st);
-        uint32_t *hist = (uint32_t *)ssh_slot(ctx, SLOT_Q_HIST, sizeof(uint32_t) * (size_t)nc * NBINS, st);
-        if (!bitmap || !hist) return SSH_ERR_OOM;
-        SSH_CUDA(cudaMemsetAsync(B.aband, 0, sizeof(unsigned long long) * nc, st));
-        pt.mark();
+        if (!bitmap) return SSH_ERR_OOM;
+        Prof pf(ctx, st);
         // K5: query signatures
+        pf.begin();
         int rc = qsig_batch(ctx, Qc, nc, B.qsig, B.qbits, st);
         if (rc) return rc;
-        pt.mark();
-        // K6: probe + candidate bitmap
+        pf.end(0);
+        // K6: probe + candidate bitmap; member counts -> CSR offsets
+        pf.begin();
         rc = probe_and_bitmap(ix, B.qsig, nc, fallback, B.bstart, B.blen, bitmap, ncand, B.isfb, st);
         if (rc) return rc;
-        pt.mark();
-        // seeds: the S0 members with the smallest LB_PAA -> fp32 DTW -> thr0
         envelope_kernel<<<nc, 256, 2 * m * sizeof(float), st>>>(Qc, m, r, nseg, B.U, B.Lo, B.Useg, B.Lseg);
-        ssh_count_launch();
-        MemberArgs ma;
-        ma.X = X; ma.Q = Qc; ma.U = B.U; ma.Lo = B.Lo; ma.Useg = B.Useg; ma.Lseg = B.Lseg;
-        ma.paa = ix->paa; ma.maxabs = ix->d_maxabs; ma.bitmap = bitmap; ma.thr = B.thr; ma.ts = B.ts;
-        ma.hist = hist; ma.counters = cnt5; ma.NW = NW; ma.m = m; ma.nseg = nseg;
-        ma.dbg = nullptr;
-        ma.out = nullptr; ma.out_lb = nullptr; ma.out_cnt = nullptr; ma.cap = 0;
-        SSH_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)nc * NBINS, st));
-        rc = launch_members<MODE_HIST>(ma, nc, st);
-        if (rc) return rc;
-        seed_thresh_kernel<<<nc, NBINS / 8, 0, st>>>(hist, S0, B.ts);
         SSH_CHECK_LAUNCH();
-        SSH_CUDA(cudaMemsetAsync(B.ccnt, 0, sizeof(int) * nc, st));
-        ma.out = B.cand; ma.out_lb = B.cand_lb; ma.out_cnt = B.ccnt; ma.cap = Q_SEED_CAND;
-        rc = launch_members<MODE_COLLECT>(ma, nc, st);
-        if (rc) return rc;
-        seed_select_kernel<<<nc, 256, 0, st>>>(B.cand, B.cand_lb, B.ccnt, Q_SEED_CAND, S0, B.seeds,
-                                               B.nseed);
-        SSH_CHECK_LAUNCH();
+        std::vector<long long> hc(nc);
+        std::vector<int64_t> hoff(nc + 1);
+        SSH_CUDA(cudaMemcpyAsync(hc.data(), ncand, sizeof(long long) * nc, cudaMemcpyDeviceToHost, st));
+        SSH_CUDA(cudaStreamSynchronize(st));
+        hoff[0] = 0;
+        for (int q = 0; q < nc; q++) hoff[q + 1] = hoff[q] + hc[q];
+        const int64_t total = hoff[nc];
+        SSH_CUDA(cudaMemcpyAsync(B.roff, hoff.data(), sizeof(int64_t) * (nc + 1), cudaMemcpyHostToDevice, st));
+        pf.end(1);
+        // LB_PAA of every member, then per-query counting sort by LB_PAA bin
+        pf.begin();
+        uint32_t *rows_u = (uint32_t *)ssh_slot(ctx, SLOT_Q_SURV, sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1), st);
+        float *lb_u = (float *)ssh_slot(ctx, SLOT_Q_SURV_LB, sizeof(float) * (size_t)std::max<int64_t>(total, 1), st);
+        uint32_t *rows_s = (uint32_t *)ssh_slot(ctx, SLOT_Q_W2, sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1), st);
+        float *lb_s = (float *)ssh_slot(ctx, SLOT_Q_D2, sizeof(float) * (size_t)std::max<int64_t>(total, 1), st);
+        if (!rows_u || !lb_u || !rows_s || !lb_s) return SSH_ERR_OOM;
+        SSH_CUDA(cudaMemsetAsync(B.mcnt, 0, sizeof(int) * nc, st));
         {
-            DtwList dl{B.seeds, S0, B.nseed, nullptr, S0, nullptr, B.sd32, nullptr, nullptr};
-            rc = launch_dtw32(ctx, X, Qc, nullptr, nullptr, dl, nullptr, nc, st);
+            PaaArgs pa{B.Useg, B.Lseg, ix->paa, ix->d_maxabs, bitmap, B.roff, rows_u, lb_u, B.mcnt, NW, m, nseg};
+            dim3 g((unsigned)ssh_div_up(NW, MB_SLICE_WORDS), (unsigned)nc);
+            paa_members_kernel<<<g, MB_THREADS, 2 * nseg * 4 + MB_WARPS * 1024 * 4, st>>>(pa);
+            SSH_CHECK_LAUNCH();
         }
-        if (rc) return rc;
-        tau_kernel<<<nc, 256, 0, st>>>(B.sd32, S0, B.nseed, k, eps, B.thr);
+        binsort_kernel<<<nc, 1024, 0, st>>>(rows_u, lb_u, B.roff, B.mcnt, rows_s, lb_s);
+        SSH_CHECK_LAUNCH();
+        pf.end(2);
+        // K7/K8: waves in LB_PAA order: LB_Kim/LB_Keogh -> fp32 DTW -> threshold
+        uint32_t *wrows = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)nc * WCAP, st);
+        float *wd32 = (float *)ssh_slot(ctx, SLOT_Q_D32, sizeof(float) * (size_t)nc * WCAP, st);
+        float *topk = (float *)ssh_slot(ctx, SLOT_Q_TOPK, sizeof(float) * (size_t)nc * k, st);
+        uint32_t *keep_rows = (uint32_t *)ssh_slot(ctx, SLOT_Q_KEEP, sizeof(uint32_t) * (size_t)nc * KCAP, st);
+        float *keep_d32 = (float *)ssh_slot(ctx, SLOT_Q_KEEP_D, sizeof(float) * (size_t)nc * KCAP, st);
+        uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_HIST, sizeof(uint32_t) * (size_t)nc * KCAP, st);
+        double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)nc * KCAP, st);
+        if (!wrows || !wd32 || !topk || !keep_rows || !keep_d32 || !resc || !d64) return SSH_ERR_OOM;
+        wave_init_kernel<<<ssh_div_up(std::max<int64_t>((int64_t)nc * k, nc), 256), 256, 0, st>>>(
+            nc, k, B.mcnt, B.thr, topk, B.pos, B.done, B.wcnt, B.keep_cnt, B.computed, B.aband);
         SSH_CHECK_LAUNCH();
         std::vector<float> thr0h;
-        if (ctx->profile) {
-            thr0h.resize(nc);
-            cudaMemcpyAsync(thr0h.data(), B.thr, sizeof(float) * nc, cudaMemcpyDeviceToHost, st);
-        }
-        pt.mark();
-        // K7: member filter (retried with a larger per-query capacity on overflow)
-        uint32_t *surv = nullptr;
-        float *slb = nullptr;
-        int maxs = 0;
-        for (;;) {
-            surv = (uint32_t *)ssh_slot(ctx, SLOT_Q_SURV, sizeof(uint32_t) * (size_t)nc * cap, st);
-            slb = (float *)ssh_slot(ctx, SLOT_Q_SURV_LB, sizeof(float) * (size_t)nc * cap, st);
-            if (!surv || !slb) return SSH_ERR_OOM;
-            SSH_CUDA(cudaMemsetAsync(B.scnt, 0, sizeof(int) * nc, st));
-            SSH_CUDA(cudaMemsetAsync(cnt5, 0, sizeof(long long) * 5 * nc, st));
-            ma.out = surv; ma.out_lb = slb; ma.out_cnt = B.scnt; ma.cap = cap;
-            ma.dbg = ctx->profile ? ctx->d_cells : nullptr;
-            rc = launch_members<MODE_FILTER>(ma, nc, st);
-            if (rc) return rc;
-            rc = max_of(B.scnt, nc, st, &maxs);
-            if (rc) return rc;
-            if (maxs <= cap) break;
-            cap = next_pow2(maxs + maxs / 4);
-            ctx->surv_cap = cap;
-        }
-        pt.mark();
-        // K8: DTW waves in LB order (survivors bucket-sorted by LB; growing waves)
-        uint32_t *srow = (uint32_t *)ssh_slot(ctx, SLOT_Q_W2, sizeof(uint32_t) * (size_t)nc * cap, st);
-        float *slbs = (float *)ssh_slot(ctx, SLOT_Q_D2, sizeof(float) * (size_t)nc * cap, st);
-        float *d32 = (float *)ssh_slot(ctx, SLOT_Q_D32, sizeof(float) * (size_t)nc * cap, st);
-        uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)nc * cap, st);
-        double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)nc * cap, st);
-        float *topk = (float *)ssh_slot(ctx, SLOT_Q_TOPK, sizeof(float) * (size_t)nc * k, st);
-        if (!srow || !slbs || !d32 || !resc || !d64 || !topk) return SSH_ERR_OOM;
-        lbsort_kernel<<<nc, 1024, 0, st>>>(surv, slb, B.scnt, cap, srow, slbs);
-        SSH_CHECK_LAUNCH();
-        SSH_CUDA(cudaMemsetAsync(topk, 0xFF, sizeof(float) * (size_t)nc * k, st));  // NaN bits > any finite
-        SSH_CUDA(cudaMemsetAsync(B.c1, 0, sizeof(int) * nc, st));    // wave start
-        SSH_CUDA(cudaMemsetAsync(B.c2, 0, sizeof(int) * nc, st));    // DTWs evaluated
-        SSH_CUDA(cudaMemsetAsync(B.done, 0, sizeof(int) * nc, st));
-        int wave = W1;
-        for (int it = 0; maxs > 0; it++) {
+        WaveLbArgs wl{X, Qc, B.U, B.Lo, (const __half2 *)ix->xenv, rows_s, lb_s, B.roff, B.mcnt, B.pos,
+                      B.done, B.thr, wrows, B.wcnt, cnt5, m, W0, WCAP};
+        const int wl_warps = 8;
+        const size_t wl_smem = (size_t)3 * m * sizeof(float);
+        SSH_CUDA(cudaFuncSetAttribute(wave_lb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wl_smem));
+        for (int wave = W0, it = 0;; wave = std::min(2 * wave, WCAP), it++) {
             SSH_CUDA(cudaMemsetAsync(B.active, 0, sizeof(int), st));
-            DtwList dl{srow, cap, B.scnt, B.c1, std::min(wave, maxs), slbs, d32, B.aband, B.c2};
-            rc = launch_dtw32(ctx, X, Qc, B.U, B.Lo, dl, B.thr, nc, st);
-            if (rc) return rc;
-            wave_update_kernel<<<nc, 256, 0, st>>>(d32, slbs, B.scnt, cap, std::min(wave, maxs), k, eps,
-                                                   topk, B.thr, B.c1, B.done, B.active);
+            pf.begin();
+            {
+                dim3 g((unsigned)std::min(ssh_div_up(wave, wl_warps), 512), (unsigned)nc);
+                wl.wave = wave;
+                wave_lb_kernel<<<g, 32 * wl_warps, wl_smem, st>>>(wl);
+                SSH_CHECK_LAUNCH();
+            }
+            pf.end(3);
+            pf.begin();
+            {
+                DtwList dl{wrows, WCAP, B.wcnt, nullptr, wave, nullptr, wd32, B.aband, B.computed};
+                rc = launch_dtw32(ctx, X, Qc, B.U, B.Lo, dl, B.thr, nc, st);
+                if (rc) return rc;
+            }
+            pf.end(4);
+            wave_update_kernel<<<nc, 256, 0, st>>>(wd32, wrows, B.wcnt, WCAP, lb_s, B.roff, B.mcnt, wave, k, eps,
+                                                   topk, B.thr, B.pos, B.done, B.active, keep_rows, keep_d32,
+                                                   B.keep_cnt, KCAP);
             SSH_CHECK_LAUNCH();
+            if (ctx->profile && it == 0) {
+                thr0h.resize(nc);
+                cudaMemcpyAsync(thr0h.data(), B.thr, sizeof(float) * nc, cudaMemcpyDeviceToHost, st);
+            }
             int act = 0;
             SSH_CUDA(cudaMemcpyAsync(&act, B.active, sizeof(int), cudaMemcpyDeviceToHost, st));
             SSH_CUDA(cudaStreamSynchronize(st));
             if (!act) break;
-            wave = std::min(wave * 2, 1 << 14);
         }
-        pt.mark();
+        int maxkeep = 0;
+        rc = max_of(B.keep_cnt, nc, st, &maxkeep);
+        if (rc) return rc;
+        SSH_REQUIRE(maxkeep <= KCAP, SSH_ERR_UNSUPPORTED,
+                    "ssh_query_batch: %d candidates within the rescoring margin of one query "
+                    "(limit %d; massively tied distances)", maxkeep, KCAP);
         // K9/K10: rescoring set, exact f64 DTW, top-k by (d64, id)
-        const int RS = cap;
-        select_kernel<<<nc, 256, 0, st>>>(srow, d32, B.c1, cap, k, eps, resc, B.rcnt, cnt5, B.scnt, B.c2);
+        pf.begin();
+        select_kernel<<<nc, 256, 0, st>>>(keep_rows, keep_d32, B.keep_cnt, KCAP, k, eps, resc, B.rcnt, cnt5,
+                                          B.mcnt, B.pos);
         SSH_CHECK_LAUNCH();
         int maxr = 0;
         rc = max_of(B.rcnt, nc, st, &maxr);
         if (rc) return rc;
-        rc = launch_dtw64_list(X, m, r, Qc, resc, RS, B.rcnt, maxr, d64, nc, st);
+        rc = launch_dtw64_list(X, m, r, Qc, resc, KCAP, B.rcnt, maxr, d64, nc, st);
         if (rc) return rc;
         const int P2k = next_pow2(k);
         size_t stk = (size_t)P2k * (sizeof(double) + sizeof(uint32_t));
         SSH_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stk));
-        topk_kernel<<<nc, 256, stk, st>>>(resc, d64, B.rcnt, RS, P2k, k, ix->id_base, ncand,
+        topk_kernel<<<nc, 256, stk, st>>>(resc, d64, B.rcnt, KCAP, P2k, k, ix->id_base, ncand,
                                           (long long *)out_ids + (int64_t)q0 * k,
                                           out_d2 + (int64_t)q0 * k, n_out + q0);
         SSH_CHECK_LAUNCH();
-        finalize_counters<<<ssh_div_up(nc, 128), 128, 0, st>>>(B.nseed, B.c2, B.aband, nc, ncand,
-                                                               B.isfb, cnt5, status + q0);
+        finalize_counters<<<ssh_div_up(nc, 128), 128, 0, st>>>(B.computed, B.aband, nc, ncand, B.isfb, cnt5,
+                                                               status + q0);
         SSH_CHECK_LAUNCH();
-        pt.mark();
+        pf.end(5);
         if (ctx->profile) {
-            pt.flush();
             std::vector<int> h(nc);
-            cudaMemcpy(h.data(), B.scnt, sizeof(int) * nc, cudaMemcpyDeviceToHost);
+            cudaMemcpy(h.data(), B.computed, sizeof(int) * nc, cudaMemcpyDeviceToHost);
             for (int v : h) ctx->prof[8] += v;
             cudaMemcpy(h.data(), B.rcnt, sizeof(int) * nc, cudaMemcpyDeviceToHost);
             for (int v : h) ctx->prof[9] += v;
-            // threshold quality: thr0 / d_k and thr1 / d_k (d_k = exact k-th squared distance)
             std::vector<float> thr1h(nc);
             std::vector<double> dk((size_t)nc * k);
             cudaMemcpy(thr1h.data(), B.thr, sizeof(float) * nc, cudaMemcpyDeviceToHost);
             cudaMemcpy(dk.data(), out_d2 + (int64_t)q0 * k, sizeof(double) * nc * k, cudaMemcpyDeviceToHost);
             for (int q = 0; q < nc; q++) {
                 double d = dk[(size_t)q * k + k - 1];
-                if (d > 0 && std::isfinite(d) && std::isfinite(thr0h[q])) {
+                if (d > 0 && std::isfinite(d) && !thr0h.empty() && std::isfinite(thr0h[q])) {
                     ctx->prof[13] += thr0h[q] / d;
                     ctx->prof[14] += thr1h[q] / d;
                     ctx->prof[15] += 1;

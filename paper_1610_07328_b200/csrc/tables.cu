@@ -394,13 +394,16 @@ fail:
 extern "C" int ssh_index_destroy(ssh_index *ix) {
     if (!ix) return SSH_OK;
     cudaSetDevice(ix->device);
-    cudaDeviceSynchronize();
-    cudaFree(ix->keys);
-    cudaFree(ix->offsets);
-    cudaFree(ix->ids);
-    cudaFree(ix->d_nb);
-    cudaFree(ix->paa);
-    cudaFree(ix->d_maxabs);
+    // stream-ordered frees on the legacy stream: memory returns to the pool
+    // without a device-wide synchronisation
+    cudaStream_t st = 0;
+    cudaFreeAsync(ix->keys, st);
+    cudaFreeAsync(ix->offsets, st);
+    cudaFreeAsync(ix->ids, st);
+    cudaFreeAsync(ix->d_nb, st);
+    if (ix->paa) cudaFreeAsync(ix->paa, st);
+    if (ix->d_maxabs) cudaFreeAsync(ix->d_maxabs, st);
+    if (ix->xenv) cudaFreeAsync(ix->xenv, st);
     delete[] ix->h_nb;
     delete ix;
     return SSH_OK;
@@ -464,18 +467,34 @@ extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t 
         cudaFreeAsync(paa, st);
         return ssh_cuda_fail(e, "ssh_build_index summaries", __FILE__, __LINE__);
     }
-    int rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st, paa, maxabs);
+    void *xenv = nullptr;
+    e = cudaMallocAsync(&xenv, sizeof(uint32_t) * (size_t)N * ctx->p.m, st);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(paa, st);
+        cudaFreeAsync(maxabs, st);
+        return ssh_cuda_fail(e, "ssh_build_index envelopes", __FILE__, __LINE__);
+    }
+    // candidate envelopes depend only on X: run them on the side stream,
+    // concurrently with the (latency-bound) signature kernels, join at the end
+    SSH_CUDA(cudaEventRecord(ctx->ev_fork, st));
+    SSH_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    int rc = ssh_launch_xenv(ctx, X, N, ld, xenv, ctx->side);
+    if (rc == SSH_OK) rc = cudaEventRecord(ctx->ev_join, ctx->side) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
+    if (rc == SSH_OK) rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st, paa, maxabs);
     if (rc == SSH_OK)
         rc = ssh_launch_shingle_cws(ctx, bits, nullptr, nullptr, nullptr, N, nullptr, nullptr, nullptr,
                                     nullptr, sig, SIG_MODE_FUSED, st);
+    if (rc == SSH_OK) rc = cudaStreamWaitEvent(st, ctx->ev_join, 0) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
     if (rc == SSH_OK) rc = ssh_index_build(ctx, sig, N, id_base, out, stream);
     if (rc != SSH_OK) {
         cudaFreeAsync(paa, st);
         cudaFreeAsync(maxabs, st);
+        cudaFreeAsync(xenv, st);
         return rc;
     }
     (*out)->paa = paa;
     (*out)->d_maxabs = maxabs;
     (*out)->nseg = nseg;
+    (*out)->xenv = xenv;
     return SSH_OK;
 }
