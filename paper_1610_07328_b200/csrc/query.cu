@@ -464,7 +464,15 @@ binsort_kernel(const uint32_t *__restrict__ rows_in, const float *__restrict__ l
     const int n = cnt[q];
     for (int b = threadIdx.x; b < NBINS; b += blockDim.x) h[b] = 0u;
     __syncthreads();
-    for (int e = threadIdx.x; e < n; e += blockDim.x) atomicAdd(&h[lb_bin(lb_in[o + e])], 1u);
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    // warp-aggregated counting: LB values cluster in few bins
+    for (int e0 = 0; e0 < n; e0 += blockDim.x) {
+        const int e = e0 + threadIdx.x;
+        const unsigned bin = e < n ? lb_bin(lb_in[o + e]) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+        if (e < n && (peers & lt) == 0) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+    }
     __syncthreads();
     const int per = NBINS / blockDim.x;
     uint32_t loc = 0;
@@ -484,11 +492,20 @@ binsort_kernel(const uint32_t *__restrict__ rows_in, const float *__restrict__ l
         run += c;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const float v = lb_in[o + e];
-        const uint32_t p = atomicAdd(&h[lb_bin(v)], 1u);
-        rows_out[o + p] = rows_in[o + e];
-        lb_out[o + p] = v;
+    for (int e0 = 0; e0 < n; e0 += blockDim.x) {
+        const int e = e0 + threadIdx.x;
+        const float v = e < n ? lb_in[o + e] : 0.f;
+        const unsigned bin = e < n ? lb_bin(v) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+        const int leader = __ffs(peers) - 1;
+        uint32_t basep = 0;
+        if (e < n && lane == leader) basep = atomicAdd(&h[bin], (uint32_t)__popc(peers));
+        basep = __shfl_sync(0xFFFFFFFFu, basep, leader);
+        if (e < n) {
+            const uint32_t p = basep + __popc(peers & lt);
+            rows_out[o + p] = rows_in[o + e];
+            lb_out[o + p] = v;
+        }
     }
 }
 
@@ -623,6 +640,9 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
     float *su = dsm + ypadn;
     float *sl = su + m;
     float *band = sl + m + (size_t)w * B * 32;
+    int start, end;
+    dtw_list_range(L, q, start, end);
+    if (start + (int)blockIdx.x * warps * 32 >= end) return;  // block-uniform: no work
     const float *y = Q + (int64_t)q * m;
     for (int j = threadIdx.x; j < m + 2 * r; j += blockDim.x) {
         int jj = j - r;
@@ -636,8 +656,6 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
             sl[i] = Lo[(int64_t)q * m + i];
         }
     __syncthreads();
-    int start, end;
-    dtw_list_range(L, q, start, end);
     const int e = start + (blockIdx.x * warps + w) * 32 + lane;
     if (start + (blockIdx.x * warps + w) * 32 >= end) return;
     uint32_t row = e < end ? L.rows[(int64_t)q * L.stride + e] : 0xFFFFFFFFu;
@@ -719,6 +737,9 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
     float *yc = rsm;           // 4 x YP
     float *su = rsm + 4 * YP;  // m
     float *sl = su + m;        // m
+    int start, end;
+    dtw_list_range(L, q, start, end);
+    if (start + (int)blockIdx.x * warps * 32 >= end) return;  // block-uniform: no work
     const float *y = Q + (int64_t)q * m;
     for (int t = threadIdx.x; t < 4 * YP; t += blockDim.x) {
         int c = t / YP, jj = (t - c * YP) + c - R;
@@ -732,8 +753,6 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
             sl[i] = Lo[(int64_t)q * m + i];
         }
     __syncthreads();
-    int start, end;
-    dtw_list_range(L, q, start, end);
     const int e = start + (blockIdx.x * warps + w) * 32 + lane;
     if (start + (blockIdx.x * warps + w) * 32 >= end) return;
     const uint32_t row = e < end ? L.rows[(int64_t)q * L.stride + e] : 0xFFFFFFFFu;
