@@ -329,9 +329,9 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
                                  note="cell = FADD + FMNMX3 + FFMA (3 FP32-pipe instr); peak 148x128x f_max / 3")
     res["dtw_evaluated"] = prof[8]
     res["rescored"] = prof[9]
-    res["lb_paa_pruned"] = prof[10]
-    res["lb_keogh_pruned_filter"] = prof[11]
-    res["members_visited"] = prof[12]
+    res["wave_lb_paa_skips"] = prof[10]
+    res["wave_lb_keogh_prunes"] = prof[11]
+    res["wave_members_visited"] = prof[12]
     if prof[15] > 0:
         res["thr0_over_dk"] = prof[13] / prof[15]
         res["thr1_over_dk"] = prof[14] / prof[15]

@@ -526,6 +526,7 @@ struct WaveLbArgs {
     uint32_t *wrows;
     int *wcnt;
     long long *counters;
+    unsigned long long *dbg;  // profiling: [1] LB_PAA skips, [2] LB_Keogh prunes, [3] visited
     int m, wave, wcap;
 };
 
@@ -548,8 +549,9 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
     const float T = a.thr[q];
     const float q0 = sq[0], ql = sq[m - 1];
     const int64_t o = a.roff[q];
-    int paa = 0, kim = 0, keo = 0, keo2 = 0;
+    int paa = 0, kim = 0, keo = 0, keo2 = 0, nvis = 0;
     for (int e = start + blockIdx.x * nw + w; e < end; e += gridDim.x * nw) {
+        nvis++;
         if (a.slbp[o + e] > T) { paa++; continue; }
         const uint32_t row = a.srows[o + e];
         const float *x = a.X + (int64_t)row * m;
@@ -597,6 +599,11 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
         if (kim) atomicAdd((unsigned long long *)&a.counters[q * 5 + 0], (unsigned long long)kim);
         if (paa + keo) atomicAdd((unsigned long long *)&a.counters[q * 5 + 1], (unsigned long long)(paa + keo));
         if (keo2) atomicAdd((unsigned long long *)&a.counters[q * 5 + 2], (unsigned long long)keo2);
+        if (a.dbg) {
+            atomicAdd(&a.dbg[1], (unsigned long long)paa);
+            atomicAdd(&a.dbg[2], (unsigned long long)keo);
+            atomicAdd(&a.dbg[3], (unsigned long long)nvis);
+        }
     }
 }
 
@@ -1421,7 +1428,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         SSH_CHECK_LAUNCH();
         std::vector<float> thr0h;
         WaveLbArgs wl{X, Qc, B.U, B.Lo, (const __half2 *)ix->xenv, rows_s, lb_s, B.roff, B.mcnt, B.pos,
-                      B.done, B.thr, wrows, B.wcnt, cnt5, m, W0, WCAP};
+                      B.done, B.thr, wrows, B.wcnt, cnt5, ctx->profile ? ctx->d_cells : nullptr, m, W0, WCAP};
         const int wl_warps = 8;
         const size_t wl_smem = (size_t)3 * m * sizeof(float);
         SSH_CUDA(cudaFuncSetAttribute(wave_lb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wl_smem));
