@@ -329,6 +329,15 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
                                  note="cell = FADD + FMNMX3 + FFMA (3 FP32-pipe instr); peak 148x128x f_max / 3")
     res["dtw_evaluated"] = prof[8]
     res["rescored"] = prof[9]
+    lb_bytes = prof[7]
+    lb_ms = prof[3]
+    if lb_ms > 0:
+        res["q3"]["roofline"] = dict(
+            bound="hbm", achieved=lb_bytes / lb_ms / 1e6, peak=hbm, unit="GB/s",
+            frac=lb_bytes / lb_ms / 1e6 / hbm, traffic=None, kernel="wave_lb_kernel",
+            note="algorithmic bytes = candidate row (f32) and envelope (fp16x2) chunks the "
+                 "LB_Kim/LB_Keogh/LB_Keogh2 cascade actually reads before abandoning (device counter)")
+    res["wave_lb_bytes"] = lb_bytes
     res["wave_lb_paa_skips"] = prof[10]
     res["wave_lb_keogh_prunes"] = prof[11]
     res["wave_members_visited"] = prof[12]

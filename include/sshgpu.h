@@ -76,7 +76,7 @@ int ssh_ctx_set_params(ssh_ctx *ctx, const ssh_params *p, const double *filter,
 /* Optional per-phase device timing of ssh_query_batch (CUDA events; adds no
  * host syncs beyond the batch's own).  ssh_ctx_profile fills up to n values:
  * [0] hash ms, [1] probe ms, [2] seed ms, [3] LB filter ms, [4] fp32 DTW ms,
- * [5] rescore+top-k ms, [6] DTW cells evaluated, [7] reserved,
+ * [5] rescore+top-k ms, [6] DTW cells evaluated, [7] bytes read by the wave LB,
  * [8] survivors, [9] rescored pairs, [10] LB_PAA prunes, [11] LB_Keogh prunes,
  * [12] members visited — accumulated since profiling was enabled. */
 int ssh_ctx_set_profiling(ssh_ctx *ctx, int on);

@@ -17,8 +17,8 @@ extern "C" int64_t ssh_launch_count(void) { return g_launches.load(); }
 extern "C" int ssh_ctx_set_profiling(ssh_ctx *ctx, int on) {
     SSH_REQUIRE(ctx != nullptr, SSH_ERR_INVALID, "ssh_ctx_set_profiling: ctx is NULL");
     SSH_CUDA(cudaSetDevice(ctx->device));
-    if (on && !ctx->d_cells) SSH_CUDA(cudaMalloc(&ctx->d_cells, 4 * sizeof(unsigned long long)));
-    if (ctx->d_cells) SSH_CUDA(cudaMemset(ctx->d_cells, 0, 4 * sizeof(unsigned long long)));
+    if (on && !ctx->d_cells) SSH_CUDA(cudaMalloc(&ctx->d_cells, 8 * sizeof(unsigned long long)));
+    if (ctx->d_cells) SSH_CUDA(cudaMemset(ctx->d_cells, 0, 8 * sizeof(unsigned long long)));
     for (int i = 0; i < 16; i++) ctx->prof[i] = 0.0;
     ctx->profile = on;
     return SSH_OK;
@@ -28,7 +28,7 @@ extern "C" int ssh_ctx_profile(const ssh_ctx *ctx, double *out, int n) {
     SSH_REQUIRE(ctx && out, SSH_ERR_INVALID, "ssh_ctx_profile: NULL argument");
     for (int i = 0; i < n && i < 16; i++) out[i] = ctx->prof[i];
     if (n > 6 && ctx->d_cells) {
-        unsigned long long c[4] = {0, 0, 0, 0};
+        unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         SSH_CUDA(cudaMemcpy(c, ctx->d_cells, sizeof(c), cudaMemcpyDeviceToHost));
         out[6] = (double)c[0];
         if (n > 12) {
@@ -36,6 +36,7 @@ extern "C" int ssh_ctx_profile(const ssh_ctx *ctx, double *out, int n) {
             out[11] = (double)c[2];
             out[12] = (double)c[3];
         }
+        if (n > 7) out[7] = (double)(c[4] + c[5]);  // bytes of rows/envelopes read by the wave LB
     }
     return SSH_OK;
 }

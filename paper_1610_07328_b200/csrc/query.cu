@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
     const float q0 = sq[0], ql = sq[m - 1];
     const int64_t o = a.roff[q];
     int paa = 0, kim = 0, keo = 0, keo2 = 0, nvis = 0;
+    long long nbytes = 0;
     for (int e = start + blockIdx.x * nw + w; e < end; e += gridDim.x * nw) {
         nvis++;
         if (a.slbp[o + e] > T) { paa++; continue; }
@@ -557,11 +558,13 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
         const float *x = a.X + (int64_t)row * m;
         if (m >= 2) {
             const float d0 = x[0] - q0, dl = x[m - 1] - ql;
+            nbytes += 8;
             if (fmaf(dl, dl, d0 * d0) > T) { kim++; continue; }
         }
         float acc = 0.f;
         bool pruned = false;
         for (int base = 0; base < m; base += 128) {
+            nbytes += 4 * min(128, m - base);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const int i = base + k * 32 + lane;
@@ -577,6 +580,7 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
         const __half2 *ev = a.xenv + (int64_t)row * m;
         acc = 0.f;
         for (int base = 0; base < m; base += 128) {
+            nbytes += 4 * min(128, m - base);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 const int i = base + k * 32 + lane;
@@ -603,6 +607,7 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
             atomicAdd(&a.dbg[1], (unsigned long long)paa);
             atomicAdd(&a.dbg[2], (unsigned long long)keo);
             atomicAdd(&a.dbg[3], (unsigned long long)nvis);
+            atomicAdd(&a.dbg[4], (unsigned long long)nbytes);
         }
     }
 }
