@@ -95,14 +95,19 @@ enum {
 
 struct ssh_index {
     int L = 0;
-    // rerank summaries (ssh_index_summarize): PAA segment means of every row
-    float *paa = nullptr;  // [N][nseg]
-    int nseg = 0;
-    float paa_delta = 0.f;  // bound on |stored mean - exact mean|
-    unsigned *d_maxabs = nullptr;
-    // envelope of every row (running max/min over +-radius), fp16 rounded
-    // outward: xenv[row][i] = (upper_i rounded up, lower_i rounded down)
-    void *xenv = nullptr;
+    // rerank summaries (ssh_index_summarize / ssh_build_index), one per row:
+    //  rec[row]   64 B: {lo, sc, x0, x_last} + u8 PAA codes of the segment
+    //             means (seg samples per segment, nseg <= SSH_REC_CODES)
+    //  codes[row] cstride B: u8 sample codes x8[mp] then (U8, L8)[mp] pairs of
+    //             the row's +-radius envelope
+    // Decoding is dec(c) = fmaf(c, sc, lo) (fp32); every code brackets its
+    // value exactly: dec(x8) <= x <= dec(x8 + 1), dec(U8) >= U, dec(L8) <= L,
+    // and dec(pc) <= segment mean <= dec(pc + 1).  Rows with non-finite
+    // values have sc = NaN, which turns every bound on them into 0.
+    void *rec = nullptr;
+    uint8_t *codes = nullptr;
+    int seg = 0, nseg = 0, mp = 0;
+    int64_t cstride = 0;
     int64_t N = 0;
     int64_t id_base = 0;
     int device = 0;
@@ -119,9 +124,10 @@ struct ssh_index {
 // grow-only named scratch slot; returns pointer or nullptr (error set)
 void *ssh_slot(ssh_ctx *ctx, int slot, size_t bytes, cudaStream_t st);
 
-#define SSH_PAA_SEG 32  // samples per PAA segment (rerank lower bound)
+#define SSH_REC_CODES 48  // PAA codes per 64-byte series record
 
-int ssh_launch_xenv(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, void *xenv, cudaStream_t st);
+// rerank summaries of N rows into ix (allocates rec/codes if needed)
+int ssh_launch_summaries(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t N, int64_t ld, cudaStream_t st);
 
 // ----------------------------------------------------------- device math
 __host__ __device__ __forceinline__ uint64_t ssh_mix64(uint64_t x) {
@@ -136,8 +142,7 @@ static inline int ssh_div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / 
 
 // kernel launchers implemented per translation unit
 int ssh_launch_sketch(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *bits,
-                      int64_t *stats, cudaStream_t st, float *paa = nullptr,
-                      unsigned *maxabs = nullptr);
+                      int64_t *stats, cudaStream_t st);
 int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *tok_in,
                            const uint16_t *cnt_in, const int32_t *len_in, int64_t N,
                            uint32_t *tok_out, uint16_t *cnt_out, int32_t *len_out,

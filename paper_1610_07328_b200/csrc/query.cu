@@ -191,14 +191,18 @@ __global__ void count_kernel(uint32_t *__restrict__ bitmap, int64_t NW, int64_t 
 }
 
 // query envelope (dtw.py:124-151 semantics: max/min over [i-r, i+r]) and its
-// per-segment max/min for the PAA bound
-__global__ void envelope_kernel(const float *__restrict__ Q, int m, int r, int nseg,
+// per-segment means for the PAA bound, rounded outward past the f64 error
+// (Useg >= mean U, Lseg <= mean L; by convexity of max(.,0)^2,
+// sum_seg max(x_i - U_i, 0)^2 >= len * max(mean x - mean U, 0)^2).
+__global__ void envelope_kernel(const float *__restrict__ Q, int m, int r, int seg, int nseg,
                                 float *__restrict__ U, float *__restrict__ Lo,
                                 float *__restrict__ Useg, float *__restrict__ Lseg) {
     extern __shared__ float esm[];
     float *su = esm, *sl = esm + m;
+    __shared__ float red[32];
     const int q = blockIdx.x;
     const float *y = Q + (int64_t)q * m;
+    float amax = 0.f;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         int lo = max(0, i - r), hi = min(m - 1, i + r);
         float mx = y[lo], mn = y[lo];
@@ -209,87 +213,171 @@ __global__ void envelope_kernel(const float *__restrict__ Q, int m, int r, int n
         }
         su[i] = mx;
         sl[i] = mn;
+        amax = fmaxf(amax, fmaxf(fabsf(mx), fabsf(mn)));
         U[(int64_t)q * m + i] = mx;
         Lo[(int64_t)q * m + i] = mn;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
     __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double mg = (double)red[0] * 0x1p-36;
     for (int s = threadIdx.x; s < nseg; s += blockDim.x) {
-        int a = s * SSH_PAA_SEG, b = min(m, a + SSH_PAA_SEG);
-        float mx = su[a], mn = sl[a];
-        for (int i = a + 1; i < b; i++) {
-            mx = fmaxf(mx, su[i]);
-            mn = fminf(mn, sl[i]);
+        const int a = s * seg, b = min(m, a + seg);
+        double su_ = 0.0, sl_ = 0.0;
+        for (int i = a; i < b; i++) {
+            su_ += (double)su[i];
+            sl_ += (double)sl[i];
         }
-        Useg[(int64_t)q * nseg + s] = mx;
-        Lseg[(int64_t)q * nseg + s] = mn;
+        Useg[(int64_t)q * nseg + s] = __double2float_ru(su_ / (double)(b - a) + mg);
+        Lseg[(int64_t)q * nseg + s] = __double2float_rd(sl_ / (double)(b - a) - mg);
     }
 }
 
 // ------------------------------------------------------ shard summaries
-// PAA segment means (f64 sum, stored f32) of every row + max|x| over the shard
-__global__ void paa_kernel(const float *__restrict__ X, int64_t N, int m, int64_t ld, int nseg,
-                           float *__restrict__ paa, unsigned *__restrict__ maxabs) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    float mx = 0.f;
-    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < N; row += nw) {
-        const float *x = X + row * ld;
-        for (int s = lane; s < nseg; s += 32) {
-            int a = s * SSH_PAA_SEG, b = min(m, a + SSH_PAA_SEG);
-            double sum = 0.0;
-            for (int i = a; i < b; i++) {
-                float v = x[i];
-                sum += (double)v;
-                mx = fmaxf(mx, fabsf(v));
-            }
-            paa[row * nseg + s] = (float)(sum / (double)(b - a));
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    if (lane == 0) atomicMax(maxabs, __float_as_uint(mx));
+// Rerank summaries of every row (layout in common.cuh): one warp per row.
+// The row is staged in the warp's shared-memory slice padded with -inf/+inf
+// outside [0, m); the per-row grid is lo = min x, sc ~ (max x - lo) / 254
+// with dec(255) >= max x verified; sample codes and PAA codes are chosen and
+// verified with the same fp32 dec() the query kernels use, so every stored
+// interval provably contains its value.  Then log-step doubling turns the
+// slice into running max/min and the envelope codes are written (upper code
+// rounded up, lower code rounded down: the fp32 LB_Keogh(q, env(x)) over
+// decoded codes never exceeds the exact one, dtw.py:124-151 envelope).
+__device__ __forceinline__ float sdec(int c, float sc, float lo) { return fmaf((float)c, sc, lo); }
+
+// c in [0, 254] with dec(c) <= v <= dec(c + 1)
+__device__ __forceinline__ int code_in(float v, float lo, float sc, float inv) {
+    int c = __float2int_rd((v - lo) * inv);
+    c = min(max(c, 0), 254);
+    for (int it = 0; it < 256 && c > 0 && sdec(c, sc, lo) > v; it++) c--;
+    for (int it = 0; it < 256 && c < 254 && sdec(c + 1, sc, lo) < v; it++) c++;
+    return c;
+}
+// smallest c in [0, 255] with dec(c) >= v (v <= dec(255))
+__device__ __forceinline__ int code_up(float v, float lo, float sc, float inv) {
+    int c = __float2int_ru((v - lo) * inv);
+    c = min(max(c, 0), 255);
+    for (int it = 0; it < 256 && c > 0 && sdec(c - 1, sc, lo) >= v; it++) c--;
+    for (int it = 0; it < 256 && c < 255 && sdec(c, sc, lo) < v; it++) c++;
+    return c;
+}
+// largest c in [0, 255] with dec(c) <= v (v >= lo)
+__device__ __forceinline__ int code_dn(float v, float lo, float sc, float inv) {
+    int c = __float2int_rd((v - lo) * inv);
+    c = min(max(c, 0), 255);
+    for (int it = 0; it < 256 && c < 255 && sdec(c + 1, sc, lo) <= v; it++) c++;
+    for (int it = 0; it < 256 && c > 0 && sdec(c, sc, lo) > v; it++) c--;
+    return c;
 }
 
-// Envelope of every row (dtw.py:124-151 semantics: max/min over [i-r, i+r]),
-// stored as fp16 pairs rounded outward (upper up, lower down), so
-// LB_Keogh(q, env(x)) computed from them never exceeds the exact bound.
-// One CTA per row tile; log-step doubling over a padded shared-memory copy.
-// One warp per row: padded copy (-inf/+inf outside [0, m)) in the warp's
-// shared-memory slice, log-step doubling with register staging and
-// __syncwarp only, then u_i = max(A[i], A[i + win - 2^lev]).
-#define XE_WARPS 8
-__global__ void __launch_bounds__(32 * XE_WARPS)
-xenv_kernel(const float *__restrict__ X, int64_t N, int m, int64_t ld, int r, int lev, int pad,
-            __half2 *__restrict__ out) {
+struct SumArgs {
+    const float *X;
+    int64_t N, ld, cstride;
+    int m, r, lev, pad, seg, nseg, mp;
+    uint4 *rec;
+    uint8_t *codes;
+};
+
+__global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
     extern __shared__ float xsm[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float *mx = xsm + (size_t)w * 2 * pad, *mn = mx + pad;
-    const int win = 2 * r + 1;
-    const int sh = win - (1 << lev);
-    const int64_t nwarps = (int64_t)gridDim.x * XE_WARPS;
-    for (int64_t row = (int64_t)blockIdx.x * XE_WARPS + w; row < N; row += nwarps) {
-        const float *x = X + row * ld;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int m = a.m, pad = a.pad;
+    float *mx = xsm + (size_t)w * (2 * pad + 16), *mn = mx + pad;
+    uint8_t *prec = reinterpret_cast<uint8_t *>(mn + pad);  // 64-byte record staging
+    const int win = 2 * a.r + 1;
+    const int sh = win - (1 << a.lev);
+    const int64_t nwarps = (int64_t)gridDim.x * nwb;
+    for (int64_t row = (int64_t)blockIdx.x * nwb + w; row < a.N; row += nwarps) {
+        const float *x = a.X + row * a.ld;
+        float vmin = INFINITY, vmax = -INFINITY;
+        bool fin = true;
         for (int t = lane; t < pad; t += 32) {
-            const int j = t - r;
+            const int j = t - a.r;
             const bool in = j >= 0 && j < m;
             const float v = in ? __ldg(x + j) : 0.f;
             mx[t] = in ? v : -INFINITY;
             mn[t] = in ? v : INFINITY;
+            if (in) {
+                fin = fin && isfinite(v);
+                vmin = fminf(vmin, v);
+                vmax = fmaxf(vmax, v);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            vmin = fminf(vmin, __shfl_xor_sync(0xFFFFFFFFu, vmin, o));
+            vmax = fmaxf(vmax, __shfl_xor_sync(0xFFFFFFFFu, vmax, o));
+        }
+        fin = __all_sync(0xFFFFFFFFu, fin);
+        __syncwarp();
+        const float lo = vmin;
+        float sc = (vmax - lo) * (1.0f / 254.0f);
+        if (fin && isfinite(sc)) {
+            for (int it = 0; it < 64 && sdec(255, sc, lo) < vmax; it++) sc = nextafterf(sc, INFINITY);
+        }
+        if (!fin || !isfinite(sc) || sdec(255, sc, lo) < vmax) sc = __int_as_float(0x7FC00000);  // NaN
+        const float inv = 1.0f / sc;
+        const float x0 = mx[a.r], xl = mx[a.r + m - 1];
+        // sample codes, 4 per lane per 128-sample chunk
+        uint8_t *cr = a.codes + row * a.cstride;
+        for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
+            uint32_t pk = 0;
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int i = i4 + t;
+                const int c = i < m ? code_in(mx[a.r + i], lo, sc, inv) : 0;
+                pk |= (uint32_t)c << (8 * t);
+            }
+            *reinterpret_cast<uint32_t *>(cr + i4) = pk;
+        }
+        // PAA codes of the segment means (f64 sums); an ambiguous mean (a grid
+        // point within the f64 error margin) gets the sentinel 255 = [lo, dec(256)]
+        const double amax = fmax(fabs((double)lo), fabs((double)vmax));
+        const double mg = amax * 0x1p-36;
+        for (int s = lane; s < SSH_REC_CODES; s += 32) {
+            int c = 0;
+            if (s < a.nseg) {
+                const int b0 = s * a.seg, b1 = min(m, b0 + a.seg);
+                double sum = 0.0;
+                for (int i = b0; i < b1; i++) sum += (double)mx[a.r + i];
+                const double md = sum / (double)(b1 - b0);
+                c = __double2int_rd((md - (double)lo) * (double)inv);
+                c = min(max(c, 0), 254);
+                for (int it = 0; it < 256 && c > 0 && (double)sdec(c, sc, lo) > md - mg; it++) c--;
+                for (int it = 0; it < 256 && c < 254 && (double)sdec(c + 1, sc, lo) < md - mg; it++) c++;
+                if (c > 0 && (double)sdec(c, sc, lo) > md - mg) c = 255;
+                else if (c < 254 && (double)sdec(c + 1, sc, lo) < md + mg) c = 255;
+            }
+            prec[16 + s] = (uint8_t)c;
+        }
+        if (lane == 0) {
+            float4 h = make_float4(lo, sc, x0, xl);
+            *reinterpret_cast<float4 *>(prec) = h;
         }
         __syncwarp();
-        for (int l = 0; l < lev; l++) {
+        if (lane < 4) a.rec[row * 4 + lane] = reinterpret_cast<const uint4 *>(prec)[lane];
+        // running max/min by log-step doubling
+        for (int l = 0; l < a.lev; l++) {
             const int d = 1 << l;
             for (int t0 = 0; t0 < pad; t0 += 32 * 8) {
-                float a[8], b[8];
+                float va[8], vb[8];
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
                     const int t = t0 + u * 32 + lane;
                     if (t + d < pad) {
-                        a[u] = fmaxf(mx[t], mx[t + d]);
-                        b[u] = fminf(mn[t], mn[t + d]);
+                        va[u] = fmaxf(mx[t], mx[t + d]);
+                        vb[u] = fminf(mn[t], mn[t + d]);
                     } else if (t < pad) {
-                        a[u] = mx[t];
-                        b[u] = mn[t];
+                        va[u] = mx[t];
+                        vb[u] = mn[t];
                     }
                 }
                 __syncwarp();
@@ -297,36 +385,65 @@ xenv_kernel(const float *__restrict__ X, int64_t N, int m, int64_t ld, int r, in
                 for (int u = 0; u < 8; u++) {
                     const int t = t0 + u * 32 + lane;
                     if (t < pad) {
-                        mx[t] = a[u];
-                        mn[t] = b[u];
+                        mx[t] = va[u];
+                        mn[t] = vb[u];
                     }
                 }
                 __syncwarp();
             }
         }
-        for (int i = lane; i < m; i += 32) {
-            const float u = fmaxf(mx[i], mx[i + sh]);
-            const float lo = fminf(mn[i], mn[i + sh]);
-            out[row * m + i] = __halves2half2(__float2half_ru(u), __float2half_rd(lo));
+        // envelope codes: (U8, L8) pairs, 4 samples per lane per chunk
+        for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
+            uint32_t p0 = 0, p1 = 0;
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int i = i4 + t;
+                int cu = 255, cl = 0;
+                if (i < m) {
+                    cu = code_up(fmaxf(mx[i], mx[i + sh]), lo, sc, inv);
+                    cl = code_dn(fminf(mn[i], mn[i + sh]), lo, sc, inv);
+                }
+                const uint32_t pr = (uint32_t)cu | ((uint32_t)cl << 8);
+                if (t < 2) p0 |= pr << (16 * t); else p1 |= pr << (16 * (t - 2));
+            }
+            *reinterpret_cast<uint2 *>(cr + a.mp + 2 * i4) = make_uint2(p0, p1);
         }
         __syncwarp();
     }
 }
 
-int ssh_launch_xenv(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, void *xenv, cudaStream_t st) {
+int ssh_launch_summaries(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t N, int64_t ld,
+                         cudaStream_t st) {
     const int m = ctx->p.m, r = ctx->p.radius;
+    const int seg = (m + SSH_REC_CODES - 1) / SSH_REC_CODES;
+    const int nseg = (m + seg - 1) / seg;
+    const int mp = ((m + 127) / 128) * 128;
     int lev = 0;
     while ((2 << lev) <= 2 * r + 1) lev++;
-    const int pad = m + 2 * r + (1 << lev);
-    const size_t smem = (size_t)XE_WARPS * 2 * pad * sizeof(float);
-    SSH_REQUIRE(smem <= 220 * 1024, SSH_ERR_UNSUPPORTED,
-                "series too long for the envelope kernel (m=%d, r=%d)", m, r);
-    SSH_CUDA(cudaFuncSetAttribute(xenv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int pad = ((m + 2 * r + (1 << lev)) + 3) & ~3;
+    const size_t per_warp = ((size_t)2 * pad + 16) * sizeof(float);
+    const int nwb = (int)std::min<size_t>(8, (200 * 1024) / per_warp);
+    SSH_REQUIRE(nwb >= 1, SSH_ERR_UNSUPPORTED, "series too long for the summaries kernel (m=%d, r=%d)", m, r);
+    if (!ix->rec) {
+        SSH_CUDA(cudaMallocAsync(&ix->rec, (size_t)64 * N, st));
+        cudaError_t e = cudaMallocAsync((void **)&ix->codes, (size_t)3 * mp * N, st);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(ix->rec, st);
+            ix->rec = nullptr;
+            return ssh_cuda_fail(e, "rerank summaries (3 m bytes per series)", __FILE__, __LINE__);
+        }
+    }
+    ix->seg = seg;
+    ix->nseg = nseg;
+    ix->mp = mp;
+    ix->cstride = (int64_t)3 * mp;
+    SumArgs a{X, N, ld, ix->cstride, m, r, lev, pad, seg, nseg, mp, (uint4 *)ix->rec, ix->codes};
+    const size_t smem = per_warp * nwb;
+    SSH_CUDA(cudaFuncSetAttribute(summaries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xenv_kernel, 32 * XE_WARPS, smem);
-    const int grid = (int)std::min<int64_t>((N + XE_WARPS - 1) / XE_WARPS,
-                                            (int64_t)ctx->num_sms * std::max(1, per_sm));
-    xenv_kernel<<<grid, 32 * XE_WARPS, smem, st>>>(X, N, m, ld, r, lev, pad, (__half2 *)xenv);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, summaries_kernel, 32 * nwb, smem);
+    const int grid = (int)std::min<int64_t>((N + nwb - 1) / nwb, (int64_t)ctx->num_sms * std::max(1, per_sm));
+    summaries_kernel<<<grid, 32 * nwb, smem, st>>>(a);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
@@ -337,63 +454,53 @@ extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, 
     SSH_REQUIRE(ctx->have_params, SSH_ERR_STATE, "ssh_index_summarize: params not set");
     SSH_REQUIRE(ld >= ctx->p.m, SSH_ERR_INVALID, "ssh_index_summarize: ld < m");
     SSH_CUDA(cudaSetDevice(ctx->device));
-    cudaStream_t st = (cudaStream_t)stream;
-    const int m = ctx->p.m;
-    const int nseg = (m + SSH_PAA_SEG - 1) / SSH_PAA_SEG;
-    if (!ix->paa) {
-        SSH_CUDA(cudaMallocAsync((void **)&ix->paa, sizeof(float) * (size_t)ix->N * nseg, st));
-        SSH_CUDA(cudaMallocAsync((void **)&ix->d_maxabs, sizeof(unsigned), st));
-    }
-    ix->nseg = nseg;
-    if (!ix->xenv) SSH_CUDA(cudaMallocAsync(&ix->xenv, sizeof(uint32_t) * (size_t)ix->N * m, st));
-    {
-        int rc = ssh_launch_xenv(ctx, X, ix->N, ld, ix->xenv, st);
-        if (rc) return rc;
-    }
-    SSH_CUDA(cudaMemsetAsync(ix->d_maxabs, 0, sizeof(unsigned), st));
-    int grid = (int)std::min<int64_t>((ix->N + 7) / 8, (int64_t)ctx->num_sms * 16);
-    paa_kernel<<<grid, 256, 0, st>>>(X, ix->N, m, ld, nseg, ix->paa, ix->d_maxabs);
-    SSH_CHECK_LAUNCH();
-    return SSH_OK;
+    return ssh_launch_summaries(ctx, ix, X, ix->N, ld, (cudaStream_t)stream);
 }
 
 // --------------------------------------------------- LB_PAA of every member
 // One CTA per (query, slice of MB_SLICE_WORDS bitmap words).  A warp turns 32
 // words into a member list in shared memory, reserves space in the query's
-// CSR segment with one atomic, and evaluates LB_PAA lane-per-member from the
-// L2-resident PAA summary (float4 gathers):
-//   LB_PAA = sum_seg len * max(xbar - Useg - delta, Lseg - xbar - delta, 0)^2 * shrink
-// where Useg/Lseg are the segment max/min of the query envelope, delta bounds
-// the stored-mean error (2u max|x|) and shrink the fp32 evaluation error.
+// CSR segment with one atomic, and evaluates lane-per-member the summary key
+// from the member's 64-byte record (L2-resident for shards up to ~2M rows):
+//   LB_PAA = shrink * sum_seg len * max(dec(c) - Useg, Lseg - dec(c+1), 0)^2
+//   LB_Kim = (x_0 - q_0)^2 + (x_last - q_last)^2            (dtw.py:154-160)
+//   key    = max(LB_PAA, LB_Kim), bit 0 = "LB_Kim is the larger" (the key is
+//            first lowered by >= 1 ulp, so setting the bit keeps it a bound)
+// shrink = 1 - (3 nseg + 8) u absorbs the fp32 evaluation error.
 struct PaaArgs {
-    const float *Useg, *Lseg, *paa;
-    const unsigned *maxabs;
+    const float *Useg, *Lseg, *Q;
+    const uint4 *rec;
     const uint32_t *bitmap;
     const int64_t *roff;  // per-query CSR offset of the member list
     uint32_t *rows;
     float *lb;
     int *cnt;
     int64_t NW;
-    int m, nseg;
+    int m, seg, nseg;
 };
+
+__device__ __forceinline__ float code_f(uint32_t w, int t) {
+    // byte t of w as an exact float (0x4B0000cc = 2^23 + cc)
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, (unsigned)t | 0x7440u)) - 8388608.f;
+}
 
 __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
     extern __shared__ __align__(16) unsigned char msm[];
+    __shared__ float sUs[SSH_REC_CODES], sLs[SSH_REC_CODES];
     const int q = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nseg = a.nseg;
-    float *sUs = reinterpret_cast<float *>(msm);
-    float *sLs = sUs + nseg;
-    uint32_t *list = reinterpret_cast<uint32_t *>(sLs + nseg) + w * 1024;
-    for (int s = threadIdx.x; s < nseg; s += MB_THREADS) {
-        sUs[s] = a.Useg[(int64_t)q * nseg + s];
-        sLs[s] = a.Lseg[(int64_t)q * nseg + s];
+    uint32_t *list = reinterpret_cast<uint32_t *>(msm) + w * 1024;
+    for (int s = threadIdx.x; s < SSH_REC_CODES; s += MB_THREADS) {
+        // unused segments contribute max(dec - inf, -inf - dec, 0) = 0
+        sUs[s] = s < nseg ? a.Useg[(int64_t)q * nseg + s] : INFINITY;
+        sLs[s] = s < nseg ? a.Lseg[(int64_t)q * nseg + s] : -INFINITY;
     }
     __syncthreads();
-    const float delta = 2.f * U32_EPS * __uint_as_float(*a.maxabs) + 1e-30f;
-    const float shrink = 1.f - (2.f * nseg + 8.f) * U32_EPS;
-    const float lastlen = (float)(a.m - (nseg - 1) * SSH_PAA_SEG);
-    const bool vec = (nseg & 3) == 0;
+    const float q0 = a.Q[(int64_t)q * a.m], ql = a.Q[(int64_t)q * a.m + a.m - 1];
+    const float shrink = 1.f - (3.f * nseg + 8.f) * U32_EPS;
+    const float segf = (float)a.seg;
+    const float lastlen = (float)(a.m - (nseg - 1) * a.seg);
     const uint32_t *bm = a.bitmap + (int64_t)q * a.NW;
     const int64_t base_q = a.roff[q];
     const int64_t s0 = (int64_t)blockIdx.x * MB_SLICE_WORDS;
@@ -422,29 +529,29 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
         __syncwarp();
         for (int e = lane; e < total; e += 32) {
             const uint32_t row = list[e];
-            const float *p = a.paa + (int64_t)row * nseg;
+            const uint4 *rp = a.rec + (int64_t)row * 4;
+            const uint4 h = __ldg(rp);
+            const uint4 c0 = __ldg(rp + 1), c1 = __ldg(rp + 2), c2 = __ldg(rp + 3);
+            const uint32_t cw[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
+            const float lo = __uint_as_float(h.x), sc = __uint_as_float(h.y);
             float acc = 0.f;
-            if (vec) {
-                for (int s = 0; s < nseg; s += 4) {
-                    const float4 v = __ldg(reinterpret_cast<const float4 *>(p + s));
-                    const float xv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int t = 0; t < 4; t++) {
-                        const float ev = fmaxf(fmaxf(xv[t] - sUs[s + t] - delta, sLs[s + t] - xv[t] - delta), 0.f);
-                        const float len = s + t + 1 < nseg ? (float)SSH_PAA_SEG : lastlen;
-                        acc = fmaf(len * ev, ev, acc);
-                    }
-                }
-            } else {
-                for (int s = 0; s < nseg; s++) {
-                    const float xb = __ldg(p + s);
-                    const float ev = fmaxf(fmaxf(xb - sUs[s] - delta, sLs[s] - xb - delta), 0.f);
-                    const float len = s + 1 < nseg ? (float)SSH_PAA_SEG : lastlen;
-                    acc = fmaf(len * ev, ev, acc);
-                }
+            for (int s = 0; s < SSH_REC_CODES; s++) {
+                const float cf = code_f(cw[s >> 2], s & 3);
+                const float xa = cf == 255.f ? lo : fmaf(cf, sc, lo);
+                const float xb = fmaf(cf + 1.f, sc, lo);
+                const float ev = fmaxf(fmaxf(xa - sUs[s], sLs[s] - xb), 0.f);
+                const float len = s == nseg - 1 ? lastlen : segf;
+                acc = fmaf(len * ev, ev, acc);
             }
+            const float paa = acc * shrink;
+            const float d0 = __uint_as_float(h.z) - q0, dl = __uint_as_float(h.w) - ql;
+            const float kim = a.m >= 2 ? fmaf(dl, dl, d0 * d0) : d0 * d0;
+            float key;
+            if (kim > paa) key = __uint_as_float(__float_as_uint(kim * (1.f - 2.f * U32_EPS)) | 1u);
+            else key = __uint_as_float(__float_as_uint(paa) & ~1u);
             a.rows[base_q + dst + e] = row;
-            a.lb[base_q + dst + e] = acc * shrink;
+            a.lb[base_q + dst + e] = key;
         }
         __syncwarp();
     }
@@ -509,15 +616,21 @@ binsort_kernel(const uint32_t *__restrict__ rows_in, const float *__restrict__ l
     }
 }
 
-// One wave, part 1: members [pos_q, pos_q + wave) of the LB_PAA-sorted list,
-// warp per member.  Skip LB_PAA > thr; else LB_Kim; then LB_Keogh(x, env(q))
-// and LB_Keogh2 = LB_Keogh(q, env(x)) (the candidate envelopes precomputed at
-// build, fp16 rounded outward), each in 128-sample chunks abandoning once the
+// One wave, part 1: members [pos_q, pos_q + wave) of the key-sorted list.
+// A warp takes 32 consecutive members (coalesced key/row loads, ballot of
+// key <= thr) and walks the live ones with the next member's first
+// 512-sample block of envelope codes prefetched while the current one is
+// evaluated.  Per member: LB_Keogh2 = LB_Keogh(q, env(x)) over the member's
+// envelope codes (dec(U8) >= U, dec(L8) <= L: each term is a lower bound of
+// the exact one), then LB_Keogh(x, env(q)) over its sample codes
+// (dec(c) <= x <= dec(c+1)), each abandoning after any 512-sample block whose
 // partial sum exceeds thr (dtw.py:154-168, 206-215).  Survivors go to the
 // wave's DTW list.
 struct WaveLbArgs {
-    const float *X, *Q, *U, *Lo;
-    const __half2 *xenv;
+    const float *Q, *U, *Lo;
+    const uint4 *rec;
+    const uint8_t *codes;
+    int64_t cstride;
     const uint32_t *srows;
     const float *slbp;
     const int64_t *roff;
@@ -526,85 +639,161 @@ struct WaveLbArgs {
     uint32_t *wrows;
     int *wcnt;
     long long *counters;
-    unsigned long long *dbg;  // profiling: [1] LB_PAA skips, [2] LB_Keogh prunes, [3] visited
-    int m, wave, wcap;
+    unsigned long long *dbg;  // profiling: [1] key skips, [2] LB_Keogh prunes, [3] visited, [4] bytes
+    int m, mp, wave, wcap;
 };
 
+#define WL_BLK 512  // samples per block of loads (4 chunks of 128, one per lane each)
+
+__device__ __forceinline__ void wl_load_env(const uint8_t *cr, int mp, int base, uint2 (&v)[4]) {
+    const uint2 *p = reinterpret_cast<const uint2 *>(cr + mp + 2 * base) + (threadIdx.x & 31);
+#pragma unroll
+    for (int c = 0; c < 4; c++) v[c] = base + 128 * c < mp ? __ldg(p + 32 * c) : make_uint2(0u, 0u);
+}
+
+// partial LB_Keogh2 of one 512-sample block (tails: sq = NaN -> term 0)
+__device__ __forceinline__ float wl_env_block(const uint2 (&v)[4], const float *sq, int base, int mp, float sc,
+                                              float lo) {
+    const int lane = threadIdx.x & 31;
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const int i0 = base + 128 * c + 4 * lane;
+        if (base + 128 * c < mp) {
+            const float4 q4 = *reinterpret_cast<const float4 *>(sq + i0);
+            const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const uint32_t wv = t < 2 ? v[c].x : v[c].y;
+                const int bu = 2 * (t & 1);
+                const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
+                const float d = fmaxf(fmaxf(qq[t] - ue, le - qq[t]), 0.f);
+                acc = fmaf(d, d, acc);
+            }
+        }
+    }
+    return acc;
+}
+
 __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
-    extern __shared__ float wsm[];
+    extern __shared__ __align__(16) float wsm[];
     const int q = blockIdx.y;
     if (a.done[q]) return;
-    const int m = a.m;
+    const int m = a.m, mp = a.mp;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int start = a.pos[q];
     const int end = min(a.cnt[q], start + a.wave);
-    if (start + (int)blockIdx.x * nw >= end) return;
-    float *su = wsm, *sl = wsm + m, *sq = wsm + 2 * m;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        su[i] = a.U[(int64_t)q * m + i];
-        sl[i] = a.Lo[(int64_t)q * m + i];
-        sq[i] = a.Q[(int64_t)q * m + i];
+    if (start + (int)blockIdx.x * nw * 32 >= end) return;
+    float *su = wsm, *sl = wsm + mp, *sq = wsm + 2 * mp;
+    for (int i = threadIdx.x; i < mp; i += blockDim.x) {
+        const bool in = i < m;
+        su[i] = in ? a.U[(int64_t)q * m + i] : INFINITY;
+        sl[i] = in ? a.Lo[(int64_t)q * m + i] : -INFINITY;
+        sq[i] = in ? a.Q[(int64_t)q * m + i] : __int_as_float(0x7FC00000);
     }
     __syncthreads();
     const float T = a.thr[q];
-    const float q0 = sq[0], ql = sq[m - 1];
     const int64_t o = a.roff[q];
     int paa = 0, kim = 0, keo = 0, keo2 = 0, nvis = 0;
     long long nbytes = 0;
-    for (int e = start + blockIdx.x * nw + w; e < end; e += gridDim.x * nw) {
-        nvis++;
-        if (a.slbp[o + e] > T) { paa++; continue; }
-        const uint32_t row = a.srows[o + e];
-        const float *x = a.X + (int64_t)row * m;
-        if (m >= 2) {
-            const float d0 = x[0] - q0, dl = x[m - 1] - ql;
-            nbytes += 8;
-            if (fmaf(dl, dl, d0 * d0) > T) { kim++; continue; }
+    for (int b0 = start + (blockIdx.x * nw + w) * 32; b0 < end; b0 += gridDim.x * nw * 32) {
+        const int e = b0 + lane;
+        float key = INFINITY;
+        uint32_t row = 0;
+        if (e < end) {
+            key = a.slbp[o + e];
+            row = a.srows[o + e];
+            nvis++;
+            if (key > T) {
+                if (__float_as_uint(key) & 1u) kim++; else paa++;
+            }
         }
-        float acc = 0.f;
-        bool pruned = false;
-        for (int base = 0; base < m; base += 128) {
-            nbytes += 4 * min(128, m - base);
+        unsigned live = __ballot_sync(0xFFFFFFFFu, e < end && key <= T);
+        if (!live) continue;
+        int j = __ffs(live) - 1;
+        live &= live - 1;
+        uint32_t rc = __shfl_sync(0xFFFFFFFFu, row, j);
+        float2 hc = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rc * 4));
+        uint2 vc[4];
+        wl_load_env(a.codes + (int64_t)rc * a.cstride, mp, 0, vc);
+        for (;;) {
+            // prefetch the next live member's header and first block
+            const bool more = live != 0;
+            uint32_t rn = 0;
+            float2 hn = make_float2(0.f, 0.f);
+            uint2 vn[4];
+            if (more) {
+                j = __ffs(live) - 1;
+                live &= live - 1;
+                rn = __shfl_sync(0xFFFFFFFFu, row, j);
+                hn = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rn * 4));
+                wl_load_env(a.codes + (int64_t)rn * a.cstride, mp, 0, vn);
+            }
+            const uint8_t *cr = a.codes + (int64_t)rc * a.cstride;
+            const float lo = hc.x, sc = hc.y;
+            bool pruned = false;
+            float acc = 0.f;
+            for (int base = 0; base < mp; base += WL_BLK) {
+                if (base) wl_load_env(cr, mp, base, vc);
+                nbytes += 2 * min(WL_BLK, mp - base);
+                acc += wl_env_block(vc, sq, base, mp, sc, lo);
+                if (warp_sum(acc) > T) { pruned = true; break; }
+            }
+            if (pruned) {
+                keo2++;
+            } else {
+                acc = 0.f;
+                for (int base = 0; base < mp && !pruned; base += WL_BLK) {
+                    uint32_t cw[4];
+                    const uint32_t *p = reinterpret_cast<const uint32_t *>(cr + base) + lane;
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int i = base + k * 32 + lane;
-                if (i < m) {
-                    const float cv = __ldg(x + i);
-                    const float v = fmaxf(fmaxf(cv - su[i], sl[i] - cv), 0.f);
-                    acc = fmaf(v, v, acc);
+                    for (int c = 0; c < 4; c++) cw[c] = base + 128 * c < mp ? __ldg(p + 32 * c) : 0u;
+                    nbytes += min(WL_BLK, mp - base);
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        const int i0 = base + 128 * c + 4 * lane;
+                        if (base + 128 * c < mp) {
+                            const float4 u4 = *reinterpret_cast<const float4 *>(su + i0);
+                            const float4 l4 = *reinterpret_cast<const float4 *>(sl + i0);
+                            const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                const float cf = code_f(cw[c], t);
+                                const float xa = fmaf(cf, sc, lo), xb = fmaf(cf + 1.f, sc, lo);
+                                const float d = fmaxf(fmaxf(xa - uu[t], ll[t] - xb), 0.f);
+                                acc = fmaf(d, d, acc);
+                            }
+                        }
+                    }
+                    if (warp_sum(acc) > T) pruned = true;
+                }
+                if (pruned) {
+                    keo++;
+                } else if (lane == 0) {
+                    const int p = atomicAdd(&a.wcnt[q], 1);
+                    if (p < a.wcap) a.wrows[(int64_t)q * a.wcap + p] = rc;
                 }
             }
-            if (warp_sum(acc) > T) { pruned = true; break; }
-        }
-        if (pruned) { keo++; continue; }
-        const __half2 *ev = a.xenv + (int64_t)row * m;
-        acc = 0.f;
-        for (int base = 0; base < m; base += 128) {
-            nbytes += 4 * min(128, m - base);
+            if (!more) break;
+            rc = rn;
+            hc = hn;
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int i = base + k * 32 + lane;
-                if (i < m) {
-                    const float2 ul = __half22float2(ev[i]);
-                    const float qv = sq[i];
-                    const float v = fmaxf(fmaxf(qv - ul.x, ul.y - qv), 0.f);
-                    acc = fmaf(v, v, acc);
-                }
-            }
-            if (warp_sum(acc) > T) { pruned = true; break; }
+            for (int c = 0; c < 4; c++) vc[c] = vn[c];
         }
-        if (pruned) { keo2++; continue; }
-        if (lane == 0) {
-            const int p = atomicAdd(&a.wcnt[q], 1);
-            if (p < a.wcap) a.wrows[(int64_t)q * a.wcap + p] = row;
-        }
+    }
+    // per-lane key counts, per-warp (lane-uniform) LB counts
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        paa += __shfl_xor_sync(0xFFFFFFFFu, paa, off);
+        kim += __shfl_xor_sync(0xFFFFFFFFu, kim, off);
+        nvis += __shfl_xor_sync(0xFFFFFFFFu, nvis, off);
     }
     if (lane == 0) {
         if (kim) atomicAdd((unsigned long long *)&a.counters[q * 5 + 0], (unsigned long long)kim);
         if (paa + keo) atomicAdd((unsigned long long *)&a.counters[q * 5 + 1], (unsigned long long)(paa + keo));
         if (keo2) atomicAdd((unsigned long long *)&a.counters[q * 5 + 2], (unsigned long long)keo2);
         if (a.dbg) {
-            atomicAdd(&a.dbg[1], (unsigned long long)paa);
+            atomicAdd(&a.dbg[1], (unsigned long long)(paa + kim));
             atomicAdd(&a.dbg[2], (unsigned long long)keo);
             atomicAdd(&a.dbg[3], (unsigned long long)nvis);
             atomicAdd(&a.dbg[4], (unsigned long long)nbytes);
@@ -1348,7 +1537,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     SSH_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = (cudaStream_t)stream;
     ssh_index *mix = const_cast<ssh_index *>(ix);
-    if (!mix->paa) {
+    if (!mix->rec) {
         int rc = ssh_index_summarize(ctx, mix, X, ctx->p.m, stream);
         if (rc) return rc;
     }
@@ -1366,7 +1555,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     const int qc = (int)std::max<int64_t>(1, qc64);
     SSH_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 5 * (size_t)nq, st));
     SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(2 * nseg * 4 + MB_WARPS * 1024 * 4)));
+                                  (int)(MB_WARPS * 1024 * 4)));
     for (int q0 = 0; q0 < nq; q0 += qc) {
         const int nc = std::min(qc, nq - q0);
         const float *Qc = Q + (int64_t)q0 * m;
@@ -1391,7 +1580,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         pf.begin();
         rc = probe_and_bitmap(ix, B.qsig, nc, fallback, B.bstart, B.blen, bitmap, ncand, B.isfb, st);
         if (rc) return rc;
-        envelope_kernel<<<nc, 256, 2 * m * sizeof(float), st>>>(Qc, m, r, nseg, B.U, B.Lo, B.Useg, B.Lseg);
+        envelope_kernel<<<nc, 256, 2 * m * sizeof(float), st>>>(Qc, m, r, ix->seg, nseg, B.U, B.Lo, B.Useg, B.Lseg);
         SSH_CHECK_LAUNCH();
         std::vector<long long> hc(nc);
         std::vector<int64_t> hoff(nc + 1);
@@ -1411,9 +1600,10 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         if (!rows_u || !lb_u || !rows_s || !lb_s) return SSH_ERR_OOM;
         SSH_CUDA(cudaMemsetAsync(B.mcnt, 0, sizeof(int) * nc, st));
         {
-            PaaArgs pa{B.Useg, B.Lseg, ix->paa, ix->d_maxabs, bitmap, B.roff, rows_u, lb_u, B.mcnt, NW, m, nseg};
+            PaaArgs pa{B.Useg, B.Lseg, Qc, (const uint4 *)ix->rec, bitmap, B.roff, rows_u, lb_u, B.mcnt, NW,
+                       m, ix->seg, nseg};
             dim3 g((unsigned)ssh_div_up(NW, MB_SLICE_WORDS), (unsigned)nc);
-            paa_members_kernel<<<g, MB_THREADS, 2 * nseg * 4 + MB_WARPS * 1024 * 4, st>>>(pa);
+            paa_members_kernel<<<g, MB_THREADS, MB_WARPS * 1024 * 4, st>>>(pa);
             SSH_CHECK_LAUNCH();
         }
         binsort_kernel<<<nc, 1024, 0, st>>>(rows_u, lb_u, B.roff, B.mcnt, rows_s, lb_s);
@@ -1432,16 +1622,17 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             nc, k, B.mcnt, B.thr, topk, B.pos, B.done, B.wcnt, B.keep_cnt, B.computed, B.aband);
         SSH_CHECK_LAUNCH();
         std::vector<float> thr0h;
-        WaveLbArgs wl{X, Qc, B.U, B.Lo, (const __half2 *)ix->xenv, rows_s, lb_s, B.roff, B.mcnt, B.pos,
-                      B.done, B.thr, wrows, B.wcnt, cnt5, ctx->profile ? ctx->d_cells : nullptr, m, W0, WCAP};
+        WaveLbArgs wl{Qc, B.U, B.Lo, (const uint4 *)ix->rec, ix->codes, ix->cstride, rows_s, lb_s, B.roff,
+                      B.mcnt, B.pos, B.done, B.thr, wrows, B.wcnt, cnt5,
+                      ctx->profile ? ctx->d_cells : nullptr, m, ix->mp, W0, WCAP};
         const int wl_warps = 8;
-        const size_t wl_smem = (size_t)3 * m * sizeof(float);
+        const size_t wl_smem = (size_t)3 * ix->mp * sizeof(float);
         SSH_CUDA(cudaFuncSetAttribute(wave_lb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wl_smem));
         for (int wave = W0, it = 0;; wave = std::min(2 * wave, WCAP), it++) {
             SSH_CUDA(cudaMemsetAsync(B.active, 0, sizeof(int), st));
             pf.begin();
             {
-                dim3 g((unsigned)std::min(ssh_div_up(wave, wl_warps), 512), (unsigned)nc);
+                dim3 g((unsigned)std::min(ssh_div_up(wave, 32 * wl_warps), 512), (unsigned)nc);
                 wl.wave = wave;
                 wave_lb_kernel<<<g, 32 * wl_warps, wl_smem, st>>>(wl);
                 SSH_CHECK_LAUNCH();

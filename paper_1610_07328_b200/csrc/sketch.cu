@@ -31,29 +31,7 @@ struct SketchGeom {
     int m, nb, words, G, ST, PB, P, W, delta;
     int64_t N, ld;
     float screen_c;
-    float *paa;         // optional: PAA segment means [N][nseg] (rerank summary)
-    unsigned *maxabs;   // optional: max |x| over all series (atomicMax of float bits)
-    int nseg;
 };
-
-// PAA segment means of the staged tile (f64 sums in sample order, stored f32)
-// and the tile's max|x|; one thread per (series, segment).
-__device__ __forceinline__ void tile_paa(const float *xs, const SketchGeom &g, int64_t s0, int ns,
-                                         const unsigned *tile_maxabs) {
-    if (!g.paa) return;
-    for (int it = threadIdx.x; it < ns * g.nseg; it += blockDim.x) {
-        const int s = it / g.nseg, seg = it - s * g.nseg;
-        const float *xr = xs + s * g.P;
-        const int a = seg * SSH_PAA_SEG, b = min(g.m, a + SSH_PAA_SEG);
-        double sum = 0.0;
-        for (int p = a; p < b; p++) {
-            const int bb = p % g.delta, j = p / g.delta;
-            sum += (double)xr[bb * g.PB + j + (j >> 3)];
-        }
-        g.paa[(s0 + s) * g.nseg + seg] = (float)(sum / (double)(b - a));
-    }
-    if (g.maxabs && threadIdx.x < ns) atomicMax(g.maxabs, tile_maxabs[threadIdx.x]);
-}
 
 __device__ __forceinline__ int poly_off(int j) { return j + (j >> 3); }
 
@@ -165,7 +143,6 @@ sketch_poly_kernel(const float *__restrict__ X, SketchGeom g, const SketchW wp,
         __syncthreads();
         stage_tile<DELTA>(X, g, s0, ns, xs, maxabs);
         __syncthreads();
-        tile_paa(xs, g, s0, ns, maxabs);
         const int item = threadIdx.x;
         if (item < ns * g.G) {
             const int s = item / g.G;
@@ -232,7 +209,6 @@ sketch_generic_kernel(const float *__restrict__ X, SketchGeom g, const SketchW w
         __syncthreads();
         stage_tile<0>(X, g, s0, ns, xs, maxabs);
         __syncthreads();
-        tile_paa(xs, g, s0, ns, maxabs);
         for (int item = threadIdx.x; item < ns * g.nb; item += SK_THREADS) {
             const int s = item / g.nb;
             const int i = item - s * g.nb;
@@ -286,12 +262,9 @@ static bool try_poly(ssh_ctx *ctx, const float *X, SketchGeom &g, const SketchW 
 }
 
 int ssh_launch_sketch(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *bits,
-                      int64_t *stats, cudaStream_t st, float *paa, unsigned *maxabs) {
+                      int64_t *stats, cudaStream_t st) {
     const ssh_params &p = ctx->p;
     SketchGeom g;
-    g.paa = paa;
-    g.maxabs = maxabs;
-    g.nseg = (p.m + SSH_PAA_SEG - 1) / SSH_PAA_SEG;
     g.m = p.m; g.nb = ctx->nb; g.words = ctx->words; g.W = p.W; g.delta = p.delta;
     g.N = N; g.ld = ld; g.screen_c = ctx->screen_c;
     g.G = (ctx->nb + SK_J - 1) / SK_J;

@@ -401,9 +401,8 @@ extern "C" int ssh_index_destroy(ssh_index *ix) {
     cudaFreeAsync(ix->offsets, st);
     cudaFreeAsync(ix->ids, st);
     cudaFreeAsync(ix->d_nb, st);
-    if (ix->paa) cudaFreeAsync(ix->paa, st);
-    if (ix->d_maxabs) cudaFreeAsync(ix->d_maxabs, st);
-    if (ix->xenv) cudaFreeAsync(ix->xenv, st);
+    if (ix->rec) cudaFreeAsync(ix->rec, st);
+    if (ix->codes) cudaFreeAsync(ix->codes, st);
     delete[] ix->h_nb;
     delete ix;
     return SSH_OK;
@@ -443,8 +442,9 @@ extern "C" int ssh_index_export(const ssh_index *ix, int table, uint64_t *keys, 
     return SSH_OK;
 }
 
-// K1 -> K4 in one call: build_index (index.py:159-172).  The sketch kernel
-// also emits the shard's PAA rerank summary while the series are staged.
+// K1 -> K4 in one call: build_index (index.py:159-172), plus the rerank
+// summaries of every row (they depend only on X: computed on the side stream,
+// concurrently with the latency-bound signature kernels, joined at the end).
 extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, int64_t id_base,
                                uint64_t *sig_out, ssh_index **out, void *stream) {
     SSH_REQUIRE(ctx && X && out, SSH_ERR_INVALID, "ssh_build_index: NULL argument");
@@ -453,48 +453,33 @@ extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t 
                 (long long)N, (long long)ld);
     SSH_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = (cudaStream_t)stream;
-    const int nseg = (ctx->p.m + SSH_PAA_SEG - 1) / SSH_PAA_SEG;
     uint64_t *bits = (uint64_t *)ssh_slot(ctx, SLOT_BITS, sizeof(uint64_t) * (size_t)N * ctx->words, st);
     uint64_t *sig = sig_out ? sig_out
                             : (uint64_t *)ssh_slot(ctx, SLOT_SIG, sizeof(uint64_t) * (size_t)N * ctx->p.L, st);
     if (!bits || !sig) return SSH_ERR_OOM;
-    float *paa = nullptr;
-    unsigned *maxabs = nullptr;
-    SSH_CUDA(cudaMallocAsync((void **)&paa, sizeof(float) * (size_t)N * nseg, st));
-    cudaError_t e = cudaMallocAsync((void **)&maxabs, sizeof(unsigned), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(maxabs, 0, sizeof(unsigned), st);
-    if (e != cudaSuccess) {
-        cudaFreeAsync(paa, st);
-        return ssh_cuda_fail(e, "ssh_build_index summaries", __FILE__, __LINE__);
-    }
-    void *xenv = nullptr;
-    e = cudaMallocAsync(&xenv, sizeof(uint32_t) * (size_t)N * ctx->p.m, st);
-    if (e != cudaSuccess) {
-        cudaFreeAsync(paa, st);
-        cudaFreeAsync(maxabs, st);
-        return ssh_cuda_fail(e, "ssh_build_index envelopes", __FILE__, __LINE__);
-    }
-    // candidate envelopes depend only on X: run them on the side stream,
-    // concurrently with the (latency-bound) signature kernels, join at the end
+    ssh_index summ;
+    summ.N = N;
     SSH_CUDA(cudaEventRecord(ctx->ev_fork, st));
     SSH_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    int rc = ssh_launch_xenv(ctx, X, N, ld, xenv, ctx->side);
+    int rc = ssh_launch_summaries(ctx, &summ, X, N, ld, ctx->side);
     if (rc == SSH_OK) rc = cudaEventRecord(ctx->ev_join, ctx->side) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
-    if (rc == SSH_OK) rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st, paa, maxabs);
+    if (rc == SSH_OK) rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st);
     if (rc == SSH_OK)
         rc = ssh_launch_shingle_cws(ctx, bits, nullptr, nullptr, nullptr, N, nullptr, nullptr, nullptr,
                                     nullptr, sig, SIG_MODE_FUSED, st);
     if (rc == SSH_OK) rc = cudaStreamWaitEvent(st, ctx->ev_join, 0) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
     if (rc == SSH_OK) rc = ssh_index_build(ctx, sig, N, id_base, out, stream);
     if (rc != SSH_OK) {
-        cudaFreeAsync(paa, st);
-        cudaFreeAsync(maxabs, st);
-        cudaFreeAsync(xenv, st);
+        cudaStreamWaitEvent(st, ctx->ev_join, 0);
+        if (summ.rec) cudaFreeAsync(summ.rec, st);
+        if (summ.codes) cudaFreeAsync(summ.codes, st);
         return rc;
     }
-    (*out)->paa = paa;
-    (*out)->d_maxabs = maxabs;
-    (*out)->nseg = nseg;
-    (*out)->xenv = xenv;
+    (*out)->rec = summ.rec;
+    (*out)->codes = summ.codes;
+    (*out)->seg = summ.seg;
+    (*out)->nseg = summ.nseg;
+    (*out)->mp = summ.mp;
+    (*out)->cstride = summ.cstride;
     return SSH_OK;
 }

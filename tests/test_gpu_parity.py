@@ -360,3 +360,43 @@ def test_full_scale_cfg1_sampled(cuda):
         assert r.stats.candidates == int(ores["n_cand"][i])
         assert r.ids == ores["ids"][i][:n].tolist()
         assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist()
+
+
+def _adversarial_sets():
+    rng = np.random.default_rng(11)
+    m = 256
+    ints = np.cumsum(rng.integers(-2, 3, size=(1500, m)), axis=1).astype(np.float32)  # grid-aligned values
+    steps = np.repeat(rng.integers(-3, 4, size=(1500, m // 32)), 32, axis=1).astype(np.float32)  # flat segments
+    offset = (np.cumsum(rng.standard_normal((1500, m)), axis=1) * 1e-2 + 4e3).astype(np.float32)  # tiny range, big offset
+    mixed = np.cumsum(rng.standard_normal((1500, m)), axis=1).astype(np.float32)
+    mixed[::7] *= 1e3
+    mixed[3::7] = 0.0
+    mixed[5::7, : m // 2] = 2.5
+    return {"ints": ints, "steps": steps, "offset": offset, "mixed": mixed}
+
+
+@pytest.mark.parametrize("kind", ["ints", "steps", "offset", "mixed"])
+def test_cascade_bounds_adversarial(cuda, kind):
+    """The u8-coded rerank summaries (LB_PAA / LB_Keogh / LB_Keogh2 over
+    bracketing codes) never prune a true top-k member: values on the code grid,
+    flat segments (PAA means on grid points), a range tiny against the offset,
+    mixed scales and constant rows; few tables and short shingles make R large
+    (most of the shard), queries include exact copies and near-duplicates."""
+    import paper_1610_07328_b200 as ssh
+
+    X = _adversarial_sets()[kind]
+    rng = np.random.default_rng(12)
+    src = rng.integers(0, X.shape[0], 12)
+    Q = X[src].copy()
+    Q[6:] += rng.standard_normal((6, X.shape[1])).astype(np.float32) * np.float32(0.3 * (np.abs(X[src[6:]]).max() + 1e-3))
+    p = ssh.SshParams(W=16, delta=2, n=4, d=3, band=0.08, K=1)
+    idx = ssh.build_index(ssh.Dataset(X), p)
+    oidx = O.build_index(X, 16, 2, 4, 3, 1, 0, 0.08)
+    ores = O.query_batch(oidx, Q, 10)
+    res = ssh.query_index_batch(idx, Q, 10, fallback_on_empty=True)
+    for i, r in enumerate(res):
+        n = int(ores["n"][i])
+        if n == 0:
+            continue
+        assert r.ids == ores["ids"][i][:n].tolist(), (kind, i)
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), (kind, i)
