@@ -309,8 +309,8 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     torch.cuda.synchronize()
     query_batch_device(index, Qd, K_TOP)
     torch.cuda.synchronize()
-    prof = (ctypes.c_double * 16)()
-    nat.check(lib.ssh_ctx_profile(ctx.handle, prof, 16))
+    prof = (ctypes.c_double * 24)()
+    nat.check(lib.ssh_ctx_profile(ctx.handle, prof, 24))
     nat.check(lib.ssh_ctx_set_profiling(ctx.handle, 0))
     names = ["hash (K5)", "probe+bitmap (K6)", "LB_PAA of all members + bin sort",
              "wave LB_Kim/LB_Keogh (K7)", "wave fp32 DTW (K8)", "rescore+top-k (K9/K10)"]
@@ -341,6 +341,8 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     res["wave_lb_paa_skips"] = prof[10]
     res["wave_lb_keogh_prunes"] = prof[11]
     res["wave_members_visited"] = prof[12]
+    res["waves"] = prof[16]
+    res["active_query_waves"] = prof[17]
     if prof[15] > 0:
         res["thr0_over_dk"] = prof[13] / prof[15]
         res["thr1_over_dk"] = prof[14] / prof[15]

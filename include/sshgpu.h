@@ -74,11 +74,15 @@ int ssh_ctx_set_params(ssh_ctx *ctx, const ssh_params *p, const double *filter,
                        const double *ln_w, int32_t max_count);
 
 /* Optional per-phase device timing of ssh_query_batch (CUDA events; adds no
- * host syncs beyond the batch's own).  ssh_ctx_profile fills up to n values:
- * [0] hash ms, [1] probe ms, [2] seed ms, [3] LB filter ms, [4] fp32 DTW ms,
- * [5] rescore+top-k ms, [6] DTW cells evaluated, [7] bytes read by the wave LB,
- * [8] survivors, [9] rescored pairs, [10] LB_PAA prunes, [11] LB_Keogh prunes,
- * [12] members visited — accumulated since profiling was enabled. */
+ * host syncs beyond the batch's own).  ssh_ctx_profile fills up to n (<= 24)
+ * values, accumulated since profiling was enabled:
+ * [0] query signatures ms, [1] probe + bitmap ms, [2] member keys + sort ms,
+ * [3] wave LB ms, [4] wave fp32 DTW ms, [5] rescore + top-k ms,
+ * [6] DTW cells evaluated (alive lane-rows x band), [7] bytes read by the
+ * wave LB, [8] fp32 DTWs started, [9] rescored pairs, [10] key prunes
+ * (LB_PAA / LB_Kim), [11] LB_Keogh prunes, [12] members visited,
+ * [13]/[14]/[15] sum of first-wave / final thr over the exact k-th distance
+ * and their count, [16] waves, [17] sum over waves of active queries. */
 int ssh_ctx_set_profiling(ssh_ctx *ctx, int on);
 int ssh_ctx_profile(const ssh_ctx *ctx, double *out, int n);
 

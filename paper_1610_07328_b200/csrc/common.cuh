@@ -58,7 +58,7 @@ struct ssh_ctx {
     size_t tab_entries = 0;
     // profiling (ssh_ctx_set_profiling)
     int profile = 0;
-    double prof[16] = {0};
+    double prof[24] = {0};
     unsigned long long *d_cells = nullptr;  // device counters: [0] DTW cells evaluated,
                                             // [1] LB_PAA prunes, [2] LB_Keogh prunes,
                                             // [3] members visited by the filter
@@ -90,6 +90,7 @@ enum {
     SLOT_SIG,
     SLOT_Q_KEEP,
     SLOT_Q_KEEP_D,
+    SLOT_Q_WLB,
     SLOT_COUNT
 };
 

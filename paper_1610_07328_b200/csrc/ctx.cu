@@ -19,14 +19,14 @@ extern "C" int ssh_ctx_set_profiling(ssh_ctx *ctx, int on) {
     SSH_CUDA(cudaSetDevice(ctx->device));
     if (on && !ctx->d_cells) SSH_CUDA(cudaMalloc(&ctx->d_cells, 8 * sizeof(unsigned long long)));
     if (ctx->d_cells) SSH_CUDA(cudaMemset(ctx->d_cells, 0, 8 * sizeof(unsigned long long)));
-    for (int i = 0; i < 16; i++) ctx->prof[i] = 0.0;
+    for (int i = 0; i < 24; i++) ctx->prof[i] = 0.0;
     ctx->profile = on;
     return SSH_OK;
 }
 
 extern "C" int ssh_ctx_profile(const ssh_ctx *ctx, double *out, int n) {
     SSH_REQUIRE(ctx && out, SSH_ERR_INVALID, "ssh_ctx_profile: NULL argument");
-    for (int i = 0; i < n && i < 16; i++) out[i] = ctx->prof[i];
+    for (int i = 0; i < n && i < 24; i++) out[i] = ctx->prof[i];
     if (n > 6 && ctx->d_cells) {
         unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         SSH_CUDA(cudaMemcpy(c, ctx->d_cells, sizeof(c), cudaMemcpyDeviceToHost));

@@ -28,6 +28,8 @@
 // stored segment means subtract an explicit absolute error term.  No member
 // of the exact top-k is ever pruned, abandoned or left unrescored.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -636,7 +638,9 @@ struct WaveLbArgs {
     const int64_t *roff;
     const int *cnt, *pos, *done;
     const float *thr;
-    uint32_t *wrows;
+    const int *act;  // active queries: block row y works on query act[y] (slot y)
+    uint32_t *wrows;  // per-slot wave lists [slot][wcap]
+    float2 *wlb;  // (LB_Keogh, LB_Keogh2) totals of each DTW-list entry
     int *wcnt;
     long long *counters;
     unsigned long long *dbg;  // profiling: [1] key skips, [2] LB_Keogh prunes, [3] visited, [4] bytes
@@ -677,8 +681,8 @@ __device__ __forceinline__ float wl_env_block(const uint2 (&v)[4], const float *
 
 __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
     extern __shared__ __align__(16) float wsm[];
-    const int q = blockIdx.y;
-    if (a.done[q]) return;
+    const int slot = blockIdx.y;
+    const int q = a.act[slot];
     const int m = a.m, mp = a.mp;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int start = a.pos[q];
@@ -732,12 +736,13 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
             const uint8_t *cr = a.codes + (int64_t)rc * a.cstride;
             const float lo = hc.x, sc = hc.y;
             bool pruned = false;
-            float acc = 0.f;
+            float acc = 0.f, tot2 = 0.f, tot1 = 0.f;
             for (int base = 0; base < mp; base += WL_BLK) {
                 if (base) wl_load_env(cr, mp, base, vc);
                 nbytes += 2 * min(WL_BLK, mp - base);
                 acc += wl_env_block(vc, sq, base, mp, sc, lo);
-                if (warp_sum(acc) > T) { pruned = true; break; }
+                tot2 = warp_sum(acc);
+                if (tot2 > T) { pruned = true; break; }
             }
             if (pruned) {
                 keo2++;
@@ -765,13 +770,17 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
                             }
                         }
                     }
-                    if (warp_sum(acc) > T) pruned = true;
+                    tot1 = warp_sum(acc);
+                    if (tot1 > T) pruned = true;
                 }
                 if (pruned) {
                     keo++;
                 } else if (lane == 0) {
-                    const int p = atomicAdd(&a.wcnt[q], 1);
-                    if (p < a.wcap) a.wrows[(int64_t)q * a.wcap + p] = rc;
+                    const int p = atomicAdd(&a.wcnt[slot], 1);
+                    if (p < a.wcap) {
+                        a.wrows[(int64_t)slot * a.wcap + p] = rc;
+                        a.wlb[(int64_t)slot * a.wcap + p] = make_float2(tot1, tot2);
+                    }
                 }
             }
             if (!more) break;
@@ -815,11 +824,12 @@ struct DtwList {
     float *out;         // result at the same index
     unsigned long long *abandoned;  // per query (NULL ok)
     int *computed;      // per query DTWs evaluated (NULL ok)
+    const int *act;     // block row y -> query act[y]; rows/lbs/out/cnt/off are per slot y (NULL: identity)
 };
 
-__device__ __forceinline__ void dtw_list_range(const DtwList &L, int q, int &start, int &end) {
-    start = L.off ? L.off[q] : 0;
-    const int total = L.cnt ? L.cnt[q] : (int)L.stride;
+__device__ __forceinline__ void dtw_list_range(const DtwList &L, int slot, int &start, int &end) {
+    start = L.off ? L.off[slot] : 0;
+    const int total = L.cnt ? L.cnt[slot] : (int)L.stride;
     end = min(total, start + L.wave);
 }
 
@@ -833,7 +843,7 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
                              const float *__restrict__ thr, int warps,
                              unsigned long long *__restrict__ cells) {
     extern __shared__ float dsm[];
-    const int q = blockIdx.y;
+    const int q = L.act ? L.act[blockIdx.y] : blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int B = 2 * r + 2;
     const int ypadn = (m + 2 * r + 3) & ~3;
@@ -841,8 +851,9 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
     float *su = dsm + ypadn;
     float *sl = su + m;
     float *band = sl + m + (size_t)w * B * 32;
+    const int slot = blockIdx.y;
     int start, end;
-    dtw_list_range(L, q, start, end);
+    dtw_list_range(L, slot, start, end);
     if (start + (int)blockIdx.x * warps * 32 >= end) return;  // block-uniform: no work
     const float *y = Q + (int64_t)q * m;
     for (int j = threadIdx.x; j < m + 2 * r; j += blockDim.x) {
@@ -859,8 +870,8 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
     __syncthreads();
     const int e = start + (blockIdx.x * warps + w) * 32 + lane;
     if (start + (blockIdx.x * warps + w) * 32 >= end) return;
-    uint32_t row = e < end ? L.rows[(int64_t)q * L.stride + e] : 0xFFFFFFFFu;
-    bool valid = row != 0xFFFFFFFFu && (!L.lbs || !(L.lbs[(int64_t)q * L.stride + e] > T));
+    uint32_t row = e < end ? L.rows[(int64_t)slot * L.stride + e] : 0xFFFFFFFFu;
+    bool valid = row != 0xFFFFFFFFu && (!L.lbs || !(L.lbs[(int64_t)slot * L.stride + e] > T));
     {
         const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
         if (L.computed && lane == 0 && vm) atomicAdd(&L.computed[q], __popc(vm));
@@ -907,7 +918,7 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
     }
     if (e < end) {
         float res = (valid && alive) ? band[r * 32 + lane] : INFINITY;
-        L.out[(int64_t)q * L.stride + e] = res;
+        L.out[(int64_t)slot * L.stride + e] = res;
         if (L.abandoned && valid && !alive) atomicAdd(&L.abandoned[q], 1ULL);
     }
     if (cells) {
@@ -932,14 +943,15 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
     constexpr int NB = 2 * R + 1;
     constexpr int NT = (NB + 3) / 4;
     extern __shared__ __align__(16) float rsm[];
-    const int q = blockIdx.y;
+    const int q = L.act ? L.act[blockIdx.y] : blockIdx.y;
+    const int slot = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int YP = ((m + 2 * R + 8) + 3) & ~3;
     float *yc = rsm;           // 4 x YP
     float *su = rsm + 4 * YP;  // m
     float *sl = su + m;        // m
     int start, end;
-    dtw_list_range(L, q, start, end);
+    dtw_list_range(L, slot, start, end);
     if (start + (int)blockIdx.x * warps * 32 >= end) return;  // block-uniform: no work
     const float *y = Q + (int64_t)q * m;
     for (int t = threadIdx.x; t < 4 * YP; t += blockDim.x) {
@@ -956,8 +968,8 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
     __syncthreads();
     const int e = start + (blockIdx.x * warps + w) * 32 + lane;
     if (start + (blockIdx.x * warps + w) * 32 >= end) return;
-    const uint32_t row = e < end ? L.rows[(int64_t)q * L.stride + e] : 0xFFFFFFFFu;
-    const bool valid = row != 0xFFFFFFFFu && (!L.lbs || !(L.lbs[(int64_t)q * L.stride + e] > T));
+    const uint32_t row = e < end ? L.rows[(int64_t)slot * L.stride + e] : 0xFFFFFFFFu;
+    const bool valid = row != 0xFFFFFFFFu && (!L.lbs || !(L.lbs[(int64_t)slot * L.stride + e] > T));
     {
         const unsigned vm = __ballot_sync(0xFFFFFFFFu, valid);
         if (L.computed && lane == 0 && vm) atomicAdd(&L.computed[q], __popc(vm));
@@ -1020,7 +1032,7 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
         if (alive && bound > T) alive = false;
     }
     if (e < end) {
-        L.out[(int64_t)q * L.stride + e] = (valid && alive) ? band[R] : INFINITY;
+        L.out[(int64_t)slot * L.stride + e] = (valid && alive) ? band[R] : INFINITY;
         if (L.abandoned && valid && !alive) atomicAdd(&L.abandoned[q], 1ULL);
     }
     if (cells) {
@@ -1028,6 +1040,255 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cc += __shfl_xor_sync(0xFFFFFFFFu, cc, o);
         if (lane == 0 && cc) atomicAdd(cells, cc);
+    }
+}
+
+// Register-band fp32 DTW of one wave's candidate list with in-block
+// compaction.  A block owns up to DW_ITEMS candidates of one query and runs
+// them through row passes [0,32), [32,64), [64,128), ... ; after each pass
+// the survivors' state (band registers, remaining bounds) is compacted in
+// shared memory and redistributed over the leading warps, so lanes whose
+// candidate was abandoned early do not idle until the slowest lane of their
+// warp finishes.  Rows stay warp-uniform (query reads are LDS.128
+// broadcasts from 4 shifted copies, as in dtw32r_kernel).
+// Abandon test after row i (UCR-suite cumulative bounds, dtw.py:206-215):
+//   rmin_i + max(remK_i - slackK, rem2_i - slack2, 0) > thr
+//   remK_i = LBK total - sum_{i' <= i} LB_Keogh term of row i'     (rows left)
+//   rem2_i = LBK2 total - sum_{j <= i + R} LB_Keogh2 term of col j (columns
+//            no path through row i has reached)
+// with the totals from the wave LB kernel (code-based terms; the exact-x row
+// terms subtracted here are never smaller, so remK stays a lower bound) and
+// slack = total * (2m + 8) u for the fp32 running sums.
+#define DW_WARPS 8
+#define DW_ITEMS (32 * DW_WARPS)
+
+struct DtwWave {
+    const uint32_t *rows;
+    const float2 *lbs;  // (LB_Keogh, LB_Keogh2) totals per entry
+    int64_t stride;
+    const int *cnt;
+    float *out;
+    unsigned long long *abandoned;
+    int *computed;
+    const uint4 *rec;
+    const uint8_t *codes;
+    int64_t cstride;
+    int mp;
+    const int *act;  // block row y -> query act[y]; rows/lbs/out/cnt per slot y
+};
+
+template <int R>
+__global__ void __launch_bounds__(DW_ITEMS, R <= 32 ? 2 : 1)
+dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, const float *__restrict__ U,
+              const float *__restrict__ Lo, DtwWave L, const float *__restrict__ thr,
+              unsigned long long *__restrict__ cells) {
+    constexpr int NB = 2 * R + 1;
+    extern __shared__ __align__(16) float wsm2[];
+    __shared__ int n_live, n_next;
+    const int slot = blockIdx.y;
+    const int q = L.act[slot];
+    const int lane = threadIdx.x & 31;
+    const int total = min(L.cnt[slot], (int)L.stride);
+    const int base = blockIdx.x * DW_ITEMS;
+    if (base >= total) return;
+    const int n0 = min(total - base, DW_ITEMS);
+    const int YP = ((m + 2 * R + 8) + 3) & ~3;
+    float *yc = wsm2;           // 4 x YP
+    float *su = yc + 4 * YP;    // m
+    float *sl = su + m;         // m
+    float *sband = sl + m;      // NB x DW_ITEMS
+    float *sremk = sband + NB * DW_ITEMS, *srem2 = sremk + DW_ITEMS;
+    float *sslk = srem2 + DW_ITEMS, *ssl2 = sslk + DW_ITEMS;
+    float *slo = ssl2 + DW_ITEMS, *ssc = slo + DW_ITEMS;
+    uint32_t *srow = reinterpret_cast<uint32_t *>(ssc + DW_ITEMS);
+    int *se = reinterpret_cast<int *>(srow + DW_ITEMS);
+    const float *y = Q + (int64_t)q * m;
+    for (int t = threadIdx.x; t < 4 * YP; t += blockDim.x) {
+        int c = t / YP, jj = (t - c * YP) + c - R;
+        yc[t] = (jj >= 0 && jj < m) ? y[jj] : INFINITY;
+    }
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        su[i] = U[(int64_t)q * m + i];
+        sl[i] = Lo[(int64_t)q * m + i];
+    }
+    const float T = thr[q];
+    const float slf = (float)(2 * m + 8) * U32_EPS;
+    if (threadIdx.x < n0) {
+        const int t = threadIdx.x, e = base + t;
+        const uint32_t row = L.rows[(int64_t)slot * L.stride + e];
+        const float2 lb = L.lbs[(int64_t)slot * L.stride + e];
+        const float2 h = __ldg(reinterpret_cast<const float2 *>(L.rec + (int64_t)row * 4));
+        L.out[(int64_t)slot * L.stride + e] = INFINITY;
+        srow[t] = row;
+        se[t] = e;
+        sremk[t] = lb.x;
+        srem2[t] = lb.y;
+        sslk[t] = lb.x * slf;
+        ssl2[t] = lb.y * slf;
+        slo[t] = h.x;
+        ssc[t] = h.y;
+#pragma unroll
+        for (int k = 0; k < NB; k++) sband[k * DW_ITEMS + t] = k == R ? 0.f : INFINITY;
+    }
+    if (threadIdx.x == 0) {
+        n_live = n0;
+        if (L.computed) atomicAdd(&L.computed[q], n0);
+    }
+    __syncthreads();
+    unsigned long long my_cells = 0;
+    unsigned long long my_ab = 0;
+    for (int a = 0; a < m;) {
+        const int b = min(m, a < 32 ? 32 : 2 * a);
+        const int nl = n_live;
+        if (nl == 0) break;
+        const int t = threadIdx.x;
+        const bool have = t < nl;
+        float band[NB];
+        uint32_t row = 0;
+        int e = 0;
+        float remk = 0.f, rem2 = 0.f, slk = 0.f, sl2 = 0.f, lo = 0.f, sc = 0.f;
+        if (have) {
+#pragma unroll
+            for (int k = 0; k < NB; k++) band[k] = sband[k * DW_ITEMS + t];
+            row = srow[t];
+            e = se[t];
+            remk = sremk[t];
+            rem2 = srem2[t];
+            slk = sslk[t];
+            sl2 = ssl2[t];
+            lo = slo[t];
+            sc = ssc[t];
+        } else {
+#pragma unroll
+            for (int k = 0; k < NB; k++) band[k] = INFINITY;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) n_next = 0;
+        __syncthreads();
+        if ((t & ~31) < nl) {
+            const float *x = X + (int64_t)row * m;
+            const uint8_t *env = L.codes + (int64_t)row * L.cstride + L.mp;
+            bool alive = have;
+            uint2 ev = make_uint2(0u, 0u);
+            if (a == 0 && have) {
+                // columns j < R leave the LB_Keogh2 remainder before row 0
+                for (int j = 0; j < min(R, m); j++) {
+                    if ((j & 3) == 0) ev = __ldg(reinterpret_cast<const uint2 *>(env + 2 * j));
+                    const uint32_t wv = (j & 2) ? ev.y : ev.x;
+                    const int bu = 2 * (j & 1);
+                    const float qj = yc[j + R];
+                    const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
+                    const float d = fmaxf(fmaxf(qj - ue, le - qj), 0.f);
+                    rem2 = fmaf(-d, d, rem2);
+                }
+            }
+            // 4 rows per step, interleaved with a one-cell lag (row i0+u works on
+            // band cell s-u at step s): all four need y[i0 + s - R], and the four
+            // dependency chains overlap.  Registers update in place: row u reads
+            // band[k] (row u-1's value from step s-1) and band[k+1] (written by
+            // row u-1 earlier in this step) before overwriting band[k].
+            const float4 *xp = reinterpret_cast<const float4 *>(x);
+            float4 xn = have ? __ldg(xp + (a >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            int rows = 0;
+            for (int i0 = a; i0 < b; i0 += 4) {
+                if (!__any_sync(0xFFFFFFFFu, alive)) break;
+                rows += alive ? 4 : 0;
+                const float4 xc = xn;
+                if (i0 + 4 < b) xn = __ldg(xp + (i0 >> 2) + 1);
+                // envelope codes of columns i0+R .. i0+R+3 (two aligned 4-column groups)
+                const int jb = (i0 + R) & ~3;
+                uint2 e0 = make_uint2(0u, 0u), e1 = make_uint2(0u, 0u);
+                if (jb < m) e0 = __ldg(reinterpret_cast<const uint2 *>(env + 2 * jb));
+                if (jb + 4 < m) e1 = __ldg(reinterpret_cast<const uint2 *>(env + 2 * jb + 8));
+                const float xr[4] = {xc.x, xc.y, xc.z, xc.w};
+                float lft[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+                float rmn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+                const float4 *yp = reinterpret_cast<const float4 *>(yc + i0);
+#pragma unroll
+                for (int s4 = 0; s4 < (NB + 3 + 3) / 4; s4++) {
+                    const float4 yv4 = yp[s4];
+                    const float yv[4] = {yv4.x, yv4.y, yv4.z, yv4.w};
+#pragma unroll
+                    for (int sv = 0; sv < 4; sv++) {
+                        const int st = 4 * s4 + sv;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int k = st - u;
+                            if (k >= 0 && k < NB) {
+                                const float up = (k + 1 < NB) ? band[k + 1] : INFINITY;
+                                const float d = xr[u] - yv[sv];
+                                const float cv = fmaf(d, d, fminf(fminf(band[k], up), lft[u]));
+                                band[k] = cv;
+                                lft[u] = cv;
+                                rmn[u] = fminf(rmn[u], cv);
+                            }
+                        }
+                    }
+                }
+                const float4 u4 = *reinterpret_cast<const float4 *>(su + i0);
+                const float4 l4 = *reinterpret_cast<const float4 *>(sl + i0);
+                const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+                bool cut = false;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const float v = fmaxf(fmaxf(xr[u] - uu[u], ll[u] - xr[u]), 0.f);
+                    remk = fmaf(-v, v, remk);
+                    const int jj = i0 + u + R;
+                    if (jj < m) {
+                        const int off = (R & 3) + u;  // column jj within the 8-column window
+                        const uint32_t wv = off < 2 ? e0.x : off < 4 ? e0.y : off < 6 ? e1.x : e1.y;
+                        const int bu = 2 * (off & 1);
+                        const float qj = yc[jj + R];
+                        const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
+                        const float dd = fmaxf(fmaxf(qj - ue, le - qj), 0.f);
+                        rem2 = fmaf(-dd, dd, rem2);
+                    }
+                    cut = cut || (rmn[u] + fmaxf(fmaxf(remk - slk, rem2 - sl2), 0.f) > T);
+                }
+                if (alive && cut) {
+                    alive = false;
+                    my_ab++;
+                }
+            }
+            my_cells += (unsigned long long)rows * NB;
+            const unsigned am = __ballot_sync(0xFFFFFFFFu, alive && b < m);
+            int dst = 0;
+            if (am) {
+                if (lane == 0) dst = atomicAdd(&n_next, __popc(am));
+                dst = __shfl_sync(0xFFFFFFFFu, dst, 0) + __popc(am & ((1u << lane) - 1u));
+            }
+            if (alive) {
+                if (b >= m) {
+                    L.out[(int64_t)slot * L.stride + e] = band[R];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NB; k++) sband[k * DW_ITEMS + dst] = band[k];
+                    srow[dst] = row;
+                    se[dst] = e;
+                    sremk[dst] = remk;
+                    srem2[dst] = rem2;
+                    sslk[dst] = slk;
+                    ssl2[dst] = sl2;
+                    slo[dst] = lo;
+                    ssc[dst] = sc;
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) n_live = n_next;
+        __syncthreads();
+        a = b;
+    }
+    if (cells || L.abandoned) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            my_cells += __shfl_xor_sync(0xFFFFFFFFu, my_cells, o);
+            my_ab += __shfl_xor_sync(0xFFFFFFFFu, my_ab, o);
+        }
+        if (lane == 0) {
+            if (cells && my_cells) atomicAdd(cells, my_cells);
+            if (L.abandoned && my_ab) atomicAdd(&L.abandoned[q], my_ab);
+        }
     }
 }
 
@@ -1095,7 +1356,8 @@ __global__ void dtw64_kernel(const float *__restrict__ X, int m, int r, const fl
 // since thr never increases and always stays >= the final kth (1 + eps)),
 // advance the wave start and decide whether the query is done (next member's
 // LB_PAA bin above thr's bin => every remaining LB_PAA exceeds thr).
-__global__ void wave_update_kernel(const float *__restrict__ wd32, const uint32_t *__restrict__ wrows,
+__global__ void wave_update_kernel(const int *__restrict__ act, const float *__restrict__ wd32,
+                                   const uint32_t *__restrict__ wrows,
                                    int *__restrict__ wcnt, int wcap, const float *__restrict__ slbp,
                                    const int64_t *__restrict__ roff, const int *__restrict__ cnt,
                                    int wave, int k, float eps, float *__restrict__ topk,
@@ -1106,10 +1368,10 @@ __global__ void wave_update_kernel(const float *__restrict__ wd32, const uint32_
     __shared__ int red[32];
     __shared__ uint32_t tmp[2048];
     __shared__ int npos;
-    const int q = blockIdx.x;
-    if (done[q]) return;
-    const int nw = min(wcnt[q], wcap);
-    const uint32_t *wb = reinterpret_cast<const uint32_t *>(wd32 + (int64_t)q * wcap);
+    const int slot = blockIdx.x;
+    const int q = act[slot];
+    const int nw = min(wcnt[slot], wcap);
+    const uint32_t *wb = reinterpret_cast<const uint32_t *>(wd32 + (int64_t)slot * wcap);
     uint32_t *tb = reinterpret_cast<uint32_t *>(topk + (int64_t)q * k);
     const int nfin = block_count_le2<uint32_t>(tb, k, wb, nw, 0x7F7FFFFFu, red);
     float T = thr[q];
@@ -1137,11 +1399,11 @@ __global__ void wave_update_kernel(const float *__restrict__ wd32, const uint32_
     }
     __syncthreads();
     for (int e = threadIdx.x; e < nw; e += blockDim.x) {
-        const float v = wd32[(int64_t)q * wcap + e];
+        const float v = wd32[(int64_t)slot * wcap + e];
         if (v <= T) {
             const int p = atomicAdd(&keep_cnt[q], 1);
             if (p < kcap) {
-                keep_rows[(int64_t)q * kcap + p] = wrows[(int64_t)q * wcap + e];
+                keep_rows[(int64_t)q * kcap + p] = wrows[(int64_t)slot * wcap + e];
                 keep_d32[(int64_t)q * kcap + p] = v;
             }
         }
@@ -1149,7 +1411,7 @@ __global__ void wave_update_kernel(const float *__restrict__ wd32, const uint32_
     __syncthreads();
     if (threadIdx.x == 0) {
         thr[q] = T;
-        wcnt[q] = 0;
+        wcnt[slot] = 0;
         const int total = cnt[q];
         const int end = min(total, pos[q] + wave);
         pos[q] = end;
@@ -1157,6 +1419,26 @@ __global__ void wave_update_kernel(const float *__restrict__ wd32, const uint32_
         done[q] = fin;
         if (!fin) atomicOr(active, 1);
     }
+}
+
+// compact list of the queries still in the wave loop (order irrelevant)
+__global__ void compact_active_kernel(const int *__restrict__ done, int nq, int *__restrict__ act,
+                                      int *__restrict__ nact) {
+    __shared__ int n;
+    if (threadIdx.x == 0) n = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int q0 = 0; q0 < nq; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        const bool a = q < nq && !done[q];
+        const unsigned bm = __ballot_sync(0xFFFFFFFFu, a);
+        int base = 0;
+        if (lane == 0 && bm) base = atomicAdd(&n, __popc(bm));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (a) act[base + __popc(bm & ((1u << lane) - 1u))] = q;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *nact = n;
 }
 
 // Rescoring set: kept candidates with d32 <= T_k (1 + eps), T_k = k-th
@@ -1310,7 +1592,7 @@ struct QueryBufs {
     uint64_t *qsig, *qbits, *bstart;
     uint32_t *blen;
     int64_t *roff;
-    int *isfb, *mcnt, *pos, *done, *active, *wcnt, *keep_cnt, *rcnt, *computed;
+    int *isfb, *mcnt, *pos, *done, *active, *wcnt, *keep_cnt, *rcnt, *computed, *act, *nact;
     float *U, *Lo, *Useg, *Lseg, *thr;
     unsigned long long *aband;
 
@@ -1325,6 +1607,8 @@ struct QueryBufs {
         pos = c.take<int>(nc);
         done = c.take<int>(nc);
         active = c.take<int>(1);
+        nact = c.take<int>(1);
+        act = c.take<int>(nc);
         wcnt = c.take<int>(nc);
         keep_cnt = c.take<int>(nc);
         rcnt = c.take<int>(nc);
@@ -1344,6 +1628,7 @@ struct Prof {
     cudaStream_t st;
     cudaEvent_t a = nullptr, b = nullptr;
     bool on;
+    float last = 0.f;
     Prof(ssh_ctx *c, cudaStream_t s) : ctx(c), st(s), on(c->profile != 0) {
         if (on) {
             cudaEventCreate(&a);
@@ -1360,6 +1645,7 @@ struct Prof {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, a, b);
         ctx->prof[slot] += ms;
+        last = ms;
     }
     ~Prof() {
         if (on) {
@@ -1419,6 +1705,28 @@ static int launch_dtw32r(ssh_ctx *ctx, const float *X, const float *Q, const flo
     return SSH_OK;
 }
 
+template <int R>
+static int launch_dtw32w(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
+                         const DtwWave &L, const float *thr, int nq, int wave, cudaStream_t st) {
+    const int m = ctx->p.m;
+    constexpr int NB = 2 * R + 1;
+    const int YP = ((m + 2 * R + 8) + 3) & ~3;
+    const size_t smem = (size_t)(4 * YP + 2 * m + (NB + 6) * DW_ITEMS) * sizeof(float) + 2 * DW_ITEMS * 4;
+    SSH_REQUIRE(smem <= 227 * 1024, SSH_ERR_UNSUPPORTED, "wave DTW: series too long (m=%d)", m);
+    SSH_CUDA(cudaFuncSetAttribute(dtw32w_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (wave <= 0) return SSH_OK;
+    dim3 grid((unsigned)ssh_div_up(wave, DW_ITEMS), (unsigned)nq);
+    dtw32w_kernel<R><<<grid, DW_ITEMS, smem, st>>>(X, m, Q, U, Lo, L, thr, ctx->profile ? ctx->d_cells : nullptr);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
+// wave fp32 DTW: compacting register-band kernel for the common radii, the
+// generic lane-per-candidate kernel otherwise
+static int launch_dtw32_wave(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
+                             const DtwWave &W, const DtwList &Lg, const float *thr, int nq, int wave,
+                             cudaStream_t st);
+
 // fp32 DTW of a candidate list (register band for the common radii, shared-memory band otherwise)
 static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const float *U,
                         const float *Lo, const DtwList &L, const float *thr, int nq,
@@ -1441,6 +1749,25 @@ static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const floa
                                                  ctx->profile ? ctx->d_cells : nullptr);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
+}
+
+static int launch_dtw32_wave(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
+                             const DtwWave &W, const DtwList &Lg, const float *thr, int nq, int wave,
+                             cudaStream_t st) {
+    const int m = ctx->p.m, r = ctx->p.radius;
+    const int YPmax = m + 2 * r + 12;
+    const bool fits = (m & 3) == 0 && (size_t)(4 * YPmax + 2 * m + (2 * r + 7) * DW_ITEMS + 2 * DW_ITEMS) * 4 <= 227 * 1024;
+#define DTWW(RR) \
+    case RR:     \
+        if (fits) return launch_dtw32w<RR>(ctx, X, Q, U, Lo, W, thr, nq, wave, st); \
+        break;
+    static const bool legacy = getenv("SSH_DEBUG_DTW_LEGACY") != nullptr;
+    if (!legacy) switch (r) {
+        DTWW(3) DTWW(6) DTWW(13) DTWW(26) DTWW(51)
+        default: break;
+    }
+#undef DTWW
+    return launch_dtw32(ctx, X, Q, U, Lo, Lg, thr, nq, st);
 }
 
 static int launch_dtw64_list(const float *X, int m, int r, const float *Q, const uint32_t *list,
@@ -1612,51 +1939,73 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         // K7/K8: waves in LB_PAA order: LB_Kim/LB_Keogh -> fp32 DTW -> threshold
         uint32_t *wrows = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)nc * WCAP, st);
         float *wd32 = (float *)ssh_slot(ctx, SLOT_Q_D32, sizeof(float) * (size_t)nc * WCAP, st);
+        float2 *wlb = (float2 *)ssh_slot(ctx, SLOT_Q_WLB, sizeof(float2) * (size_t)nc * WCAP, st);
         float *topk = (float *)ssh_slot(ctx, SLOT_Q_TOPK, sizeof(float) * (size_t)nc * k, st);
         uint32_t *keep_rows = (uint32_t *)ssh_slot(ctx, SLOT_Q_KEEP, sizeof(uint32_t) * (size_t)nc * KCAP, st);
         float *keep_d32 = (float *)ssh_slot(ctx, SLOT_Q_KEEP_D, sizeof(float) * (size_t)nc * KCAP, st);
         uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_HIST, sizeof(uint32_t) * (size_t)nc * KCAP, st);
         double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)nc * KCAP, st);
-        if (!wrows || !wd32 || !topk || !keep_rows || !keep_d32 || !resc || !d64) return SSH_ERR_OOM;
+        if (!wrows || !wd32 || !wlb || !topk || !keep_rows || !keep_d32 || !resc || !d64) return SSH_ERR_OOM;
         wave_init_kernel<<<ssh_div_up(std::max<int64_t>((int64_t)nc * k, nc), 256), 256, 0, st>>>(
             nc, k, B.mcnt, B.thr, topk, B.pos, B.done, B.wcnt, B.keep_cnt, B.computed, B.aband);
         SSH_CHECK_LAUNCH();
         std::vector<float> thr0h;
+        // waves over the active queries only: block row y = slot y = query act[y];
+        // the per-wave lists share one pool, so the per-slot capacity grows as
+        // queries finish
+        const int64_t pool = (int64_t)nc * WCAP;
+        compact_active_kernel<<<1, 1024, 0, st>>>(B.done, nc, B.act, B.nact);
+        SSH_CHECK_LAUNCH();
+        int nact = 0;
+        SSH_CUDA(cudaMemcpyAsync(&nact, B.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SSH_CUDA(cudaStreamSynchronize(st));
         WaveLbArgs wl{Qc, B.U, B.Lo, (const uint4 *)ix->rec, ix->codes, ix->cstride, rows_s, lb_s, B.roff,
-                      B.mcnt, B.pos, B.done, B.thr, wrows, B.wcnt, cnt5,
+                      B.mcnt, B.pos, B.done, B.thr, B.act, wrows, wlb, B.wcnt, cnt5,
                       ctx->profile ? ctx->d_cells : nullptr, m, ix->mp, W0, WCAP};
         const int wl_warps = 8;
         const size_t wl_smem = (size_t)3 * ix->mp * sizeof(float);
         SSH_CUDA(cudaFuncSetAttribute(wave_lb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wl_smem));
-        for (int wave = W0, it = 0;; wave = std::min(2 * wave, WCAP), it++) {
-            SSH_CUDA(cudaMemsetAsync(B.active, 0, sizeof(int), st));
+        for (int wave = W0, it = 0; nact > 0; wave *= 2, it++) {
+            const int wcap = (int)std::min<int64_t>((int64_t)1 << 20, (pool / nact) & ~(int64_t)255);
+            wave = std::min(wave, wcap);
             pf.begin();
             {
-                dim3 g((unsigned)std::min(ssh_div_up(wave, 32 * wl_warps), 512), (unsigned)nc);
+                dim3 g((unsigned)std::min(ssh_div_up(wave, 32 * wl_warps), 512), (unsigned)nact);
                 wl.wave = wave;
+                wl.wcap = wcap;
                 wave_lb_kernel<<<g, 32 * wl_warps, wl_smem, st>>>(wl);
                 SSH_CHECK_LAUNCH();
             }
             pf.end(3);
+            const float lb_ms = pf.last;
             pf.begin();
             {
-                DtwList dl{wrows, WCAP, B.wcnt, nullptr, wave, nullptr, wd32, B.aband, B.computed};
-                rc = launch_dtw32(ctx, X, Qc, B.U, B.Lo, dl, B.thr, nc, st);
+                DtwList dl{wrows, wcap, B.wcnt, nullptr, wave, nullptr, wd32, B.aband, B.computed, B.act};
+                DtwWave dw{wrows, wlb, wcap, B.wcnt, wd32, B.aband, B.computed, (const uint4 *)ix->rec,
+                           ix->codes, ix->cstride, ix->mp, B.act};
+                rc = launch_dtw32_wave(ctx, X, Qc, B.U, B.Lo, dw, dl, B.thr, nact, wave, st);
                 if (rc) return rc;
             }
             pf.end(4);
-            wave_update_kernel<<<nc, 256, 0, st>>>(wd32, wrows, B.wcnt, WCAP, lb_s, B.roff, B.mcnt, wave, k, eps,
-                                                   topk, B.thr, B.pos, B.done, B.active, keep_rows, keep_d32,
-                                                   B.keep_cnt, KCAP);
+            if (ctx->profile && getenv("SSH_DEBUG_WAVES"))
+                fprintf(stderr, "wave %d: active %d wave %d cap %d | LB %.3f ms DTW %.3f ms\n", it, nact, wave,
+                        wcap, lb_ms, pf.last);
+            wave_update_kernel<<<nact, 256, 0, st>>>(B.act, wd32, wrows, B.wcnt, wcap, lb_s, B.roff, B.mcnt, wave,
+                                                     k, eps, topk, B.thr, B.pos, B.done, B.active, keep_rows,
+                                                     keep_d32, B.keep_cnt, KCAP);
+            SSH_CHECK_LAUNCH();
+            compact_active_kernel<<<1, 1024, 0, st>>>(B.done, nc, B.act, B.nact);
             SSH_CHECK_LAUNCH();
             if (ctx->profile && it == 0) {
                 thr0h.resize(nc);
                 cudaMemcpyAsync(thr0h.data(), B.thr, sizeof(float) * nc, cudaMemcpyDeviceToHost, st);
             }
-            int act = 0;
-            SSH_CUDA(cudaMemcpyAsync(&act, B.active, sizeof(int), cudaMemcpyDeviceToHost, st));
+            SSH_CUDA(cudaMemcpyAsync(&nact, B.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
             SSH_CUDA(cudaStreamSynchronize(st));
-            if (!act) break;
+            if (ctx->profile) {
+                ctx->prof[16] += 1;
+                ctx->prof[17] += nact;
+            }
         }
         int maxkeep = 0;
         rc = max_of(B.keep_cnt, nc, st, &maxkeep);
