@@ -1588,6 +1588,8 @@ struct Carver {
     }
 };
 
+#define SSH_MEMBER_BUDGET ((int64_t)1 << 29)  // members per sub-range (8 GiB of lists)
+
 struct QueryBufs {
     uint64_t *qsig, *qbits, *bstart;
     uint32_t *blen;
@@ -1619,6 +1621,32 @@ struct QueryBufs {
         Lseg = c.take<float>((size_t)nc * nseg);
         thr = c.take<float>(nc);
         aband = c.take<unsigned long long>(nc);
+    }
+
+    // view of queries [qa, ...): per-query arrays advanced by qa (roff and the
+    // scalar flags stay shared; roff is rewritten per sub-range)
+    QueryBufs shifted(int qa, int L, int words, int m, int nseg) const {
+        QueryBufs o = *this;
+        o.qsig += (size_t)qa * L;
+        o.qbits += (size_t)qa * words;
+        o.bstart += (size_t)qa * L;
+        o.blen += (size_t)qa * L;
+        o.isfb += qa;
+        o.mcnt += qa;
+        o.pos += qa;
+        o.done += qa;
+        o.act += qa;
+        o.wcnt += qa;
+        o.keep_cnt += qa;
+        o.rcnt += qa;
+        o.computed += qa;
+        o.U += (size_t)qa * m;
+        o.Lo += (size_t)qa * m;
+        o.Useg += (size_t)qa * nseg;
+        o.Lseg += (size_t)qa * nseg;
+        o.thr += qa;
+        o.aband += qa;
+        return o;
     }
 };
 
@@ -1875,10 +1903,10 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     const int WCAP = std::max(W0, 16384);
     const int KCAP = 4096 + 4 * k;
     const int fallback = (flags & SSH_QUERY_FALLBACK_ON_EMPTY) ? 1 : 0;
-    // query chunk: membership bitmaps <= 1 GiB and worst-case member lists <= 8 GiB
+    // query chunk: membership bitmaps <= 1 GiB; within a chunk, sub-ranges of
+    // queries whose actual member lists (16 B per member) fit SSH_MEMBER_BUDGET
     int64_t qc64 = std::min<int64_t>(nq, 32768);
     qc64 = std::min<int64_t>(qc64, ((int64_t)1 << 28) / std::max<int64_t>(1, NW));
-    qc64 = std::min<int64_t>(qc64, ((int64_t)1 << 33) / std::max<int64_t>(1, N * 16));
     const int qc = (int)std::max<int64_t>(1, qc64);
     SSH_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 5 * (size_t)nq, st));
     SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1910,148 +1938,166 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         envelope_kernel<<<nc, 256, 2 * m * sizeof(float), st>>>(Qc, m, r, ix->seg, nseg, B.U, B.Lo, B.Useg, B.Lseg);
         SSH_CHECK_LAUNCH();
         std::vector<long long> hc(nc);
-        std::vector<int64_t> hoff(nc + 1);
         SSH_CUDA(cudaMemcpyAsync(hc.data(), ncand, sizeof(long long) * nc, cudaMemcpyDeviceToHost, st));
         SSH_CUDA(cudaStreamSynchronize(st));
-        hoff[0] = 0;
-        for (int q = 0; q < nc; q++) hoff[q + 1] = hoff[q] + hc[q];
-        const int64_t total = hoff[nc];
-        SSH_CUDA(cudaMemcpyAsync(B.roff, hoff.data(), sizeof(int64_t) * (nc + 1), cudaMemcpyHostToDevice, st));
         pf.end(1);
-        // LB_PAA of every member, then per-query counting sort by LB_PAA bin
-        pf.begin();
-        uint32_t *rows_u = (uint32_t *)ssh_slot(ctx, SLOT_Q_SURV, sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1), st);
-        float *lb_u = (float *)ssh_slot(ctx, SLOT_Q_SURV_LB, sizeof(float) * (size_t)std::max<int64_t>(total, 1), st);
-        uint32_t *rows_s = (uint32_t *)ssh_slot(ctx, SLOT_Q_W2, sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1), st);
-        float *lb_s = (float *)ssh_slot(ctx, SLOT_Q_D2, sizeof(float) * (size_t)std::max<int64_t>(total, 1), st);
-        if (!rows_u || !lb_u || !rows_s || !lb_s) return SSH_ERR_OOM;
-        SSH_CUDA(cudaMemsetAsync(B.mcnt, 0, sizeof(int) * nc, st));
-        {
-            PaaArgs pa{B.Useg, B.Lseg, Qc, (const uint4 *)ix->rec, bitmap, B.roff, rows_u, lb_u, B.mcnt, NW,
-                       m, ix->seg, nseg};
-            dim3 g((unsigned)ssh_div_up(NW, MB_SLICE_WORDS), (unsigned)nc);
-            paa_members_kernel<<<g, MB_THREADS, MB_WARPS * 1024 * 4, st>>>(pa);
-            SSH_CHECK_LAUNCH();
-        }
-        binsort_kernel<<<nc, 1024, 0, st>>>(rows_u, lb_u, B.roff, B.mcnt, rows_s, lb_s);
-        SSH_CHECK_LAUNCH();
-        pf.end(2);
-        // K7/K8: waves in LB_PAA order: LB_Kim/LB_Keogh -> fp32 DTW -> threshold
-        uint32_t *wrows = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)nc * WCAP, st);
-        float *wd32 = (float *)ssh_slot(ctx, SLOT_Q_D32, sizeof(float) * (size_t)nc * WCAP, st);
-        float2 *wlb = (float2 *)ssh_slot(ctx, SLOT_Q_WLB, sizeof(float2) * (size_t)nc * WCAP, st);
-        float *topk = (float *)ssh_slot(ctx, SLOT_Q_TOPK, sizeof(float) * (size_t)nc * k, st);
-        uint32_t *keep_rows = (uint32_t *)ssh_slot(ctx, SLOT_Q_KEEP, sizeof(uint32_t) * (size_t)nc * KCAP, st);
-        float *keep_d32 = (float *)ssh_slot(ctx, SLOT_Q_KEEP_D, sizeof(float) * (size_t)nc * KCAP, st);
-        uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_HIST, sizeof(uint32_t) * (size_t)nc * KCAP, st);
-        double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)nc * KCAP, st);
-        if (!wrows || !wd32 || !wlb || !topk || !keep_rows || !keep_d32 || !resc || !d64) return SSH_ERR_OOM;
-        wave_init_kernel<<<ssh_div_up(std::max<int64_t>((int64_t)nc * k, nc), 256), 256, 0, st>>>(
-            nc, k, B.mcnt, B.thr, topk, B.pos, B.done, B.wcnt, B.keep_cnt, B.computed, B.aband);
-        SSH_CHECK_LAUNCH();
-        std::vector<float> thr0h;
-        // waves over the active queries only: block row y = slot y = query act[y];
-        // the per-wave lists share one pool, so the per-slot capacity grows as
-        // queries finish
-        const int64_t pool = (int64_t)nc * WCAP;
-        compact_active_kernel<<<1, 1024, 0, st>>>(B.done, nc, B.act, B.nact);
-        SSH_CHECK_LAUNCH();
-        int nact = 0;
-        SSH_CUDA(cudaMemcpyAsync(&nact, B.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
-        SSH_CUDA(cudaStreamSynchronize(st));
-        WaveLbArgs wl{Qc, B.U, B.Lo, (const uint4 *)ix->rec, ix->codes, ix->cstride, rows_s, lb_s, B.roff,
-                      B.mcnt, B.pos, B.done, B.thr, B.act, wrows, wlb, B.wcnt, cnt5,
-                      ctx->profile ? ctx->d_cells : nullptr, m, ix->mp, W0, WCAP};
-        const int wl_warps = 8;
-        const size_t wl_smem = (size_t)3 * ix->mp * sizeof(float);
-        SSH_CUDA(cudaFuncSetAttribute(wave_lb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wl_smem));
-        for (int wave = W0, it = 0; nact > 0; wave *= 2, it++) {
-            const int wcap = (int)std::min<int64_t>((int64_t)1 << 20, (pool / nact) & ~(int64_t)255);
-            wave = std::min(wave, wcap);
-            pf.begin();
+        // sub-ranges of the chunk whose actual member lists fit the budget
+        // (SSH_DEBUG_MEMBER_BUDGET overrides it, for tests of the split path)
+        int64_t budget = SSH_MEMBER_BUDGET;
+        if (const char *ev = getenv("SSH_DEBUG_MEMBER_BUDGET")) budget = std::max<int64_t>(1, atoll(ev));
+        for (int sa = 0; sa < nc;) {
+            int sb = sa;
+            int64_t total = 0;
+            while (sb < nc && (sb == sa || total + hc[sb] <= budget)) total += hc[sb++];
+            const int ns = sb - sa;
+            QueryBufs S = B.shifted(sa, L, ctx->words, m, nseg);
+            const float *Qs = Qc + (int64_t)sa * m;
+            uint32_t *bms = bitmap + (int64_t)sa * NW;
+            long long *ncs = ncand + sa;
+            long long *c5s = cnt5 + (int64_t)sa * 5;
+            const int qs0 = q0 + sa;
             {
-                dim3 g((unsigned)std::min(ssh_div_up(wave, 32 * wl_warps), 512), (unsigned)nact);
-                wl.wave = wave;
-                wl.wcap = wcap;
-                wave_lb_kernel<<<g, 32 * wl_warps, wl_smem, st>>>(wl);
+                std::vector<int64_t> hoff(ns + 1);
+                hoff[0] = 0;
+                for (int q = 0; q < ns; q++) hoff[q + 1] = hoff[q] + hc[sa + q];
+                SSH_CUDA(cudaMemcpyAsync(S.roff, hoff.data(), sizeof(int64_t) * (ns + 1), cudaMemcpyHostToDevice, st));
+            }
+            // LB_PAA of every member, then per-query counting sort by LB_PAA bin
+            pf.begin();
+            uint32_t *rows_u = (uint32_t *)ssh_slot(ctx, SLOT_Q_SURV, sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1), st);
+            float *lb_u = (float *)ssh_slot(ctx, SLOT_Q_SURV_LB, sizeof(float) * (size_t)std::max<int64_t>(total, 1), st);
+            uint32_t *rows_s = (uint32_t *)ssh_slot(ctx, SLOT_Q_W2, sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1), st);
+            float *lb_s = (float *)ssh_slot(ctx, SLOT_Q_D2, sizeof(float) * (size_t)std::max<int64_t>(total, 1), st);
+            if (!rows_u || !lb_u || !rows_s || !lb_s) return SSH_ERR_OOM;
+            SSH_CUDA(cudaMemsetAsync(S.mcnt, 0, sizeof(int) * ns, st));
+            {
+                PaaArgs pa{S.Useg, S.Lseg, Qs, (const uint4 *)ix->rec, bms, S.roff, rows_u, lb_u, S.mcnt, NW,
+                           m, ix->seg, nseg};
+                dim3 g((unsigned)ssh_div_up(NW, MB_SLICE_WORDS), (unsigned)ns);
+                paa_members_kernel<<<g, MB_THREADS, MB_WARPS * 1024 * 4, st>>>(pa);
                 SSH_CHECK_LAUNCH();
             }
-            pf.end(3);
-            const float lb_ms = pf.last;
-            pf.begin();
-            {
-                DtwList dl{wrows, wcap, B.wcnt, nullptr, wave, nullptr, wd32, B.aband, B.computed, B.act};
-                DtwWave dw{wrows, wlb, wcap, B.wcnt, wd32, B.aband, B.computed, (const uint4 *)ix->rec,
-                           ix->codes, ix->cstride, ix->mp, B.act};
-                rc = launch_dtw32_wave(ctx, X, Qc, B.U, B.Lo, dw, dl, B.thr, nact, wave, st);
-                if (rc) return rc;
-            }
-            pf.end(4);
-            if (ctx->profile && getenv("SSH_DEBUG_WAVES"))
-                fprintf(stderr, "wave %d: active %d wave %d cap %d | LB %.3f ms DTW %.3f ms\n", it, nact, wave,
-                        wcap, lb_ms, pf.last);
-            wave_update_kernel<<<nact, 256, 0, st>>>(B.act, wd32, wrows, B.wcnt, wcap, lb_s, B.roff, B.mcnt, wave,
-                                                     k, eps, topk, B.thr, B.pos, B.done, B.active, keep_rows,
-                                                     keep_d32, B.keep_cnt, KCAP);
+            binsort_kernel<<<ns, 1024, 0, st>>>(rows_u, lb_u, S.roff, S.mcnt, rows_s, lb_s);
             SSH_CHECK_LAUNCH();
-            compact_active_kernel<<<1, 1024, 0, st>>>(B.done, nc, B.act, B.nact);
+            pf.end(2);
+            // K7/K8: waves in LB_PAA order: LB_Kim/LB_Keogh -> fp32 DTW -> threshold
+            uint32_t *wrows = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)ns * WCAP, st);
+            float *wd32 = (float *)ssh_slot(ctx, SLOT_Q_D32, sizeof(float) * (size_t)ns * WCAP, st);
+            float2 *wlb = (float2 *)ssh_slot(ctx, SLOT_Q_WLB, sizeof(float2) * (size_t)ns * WCAP, st);
+            float *topk = (float *)ssh_slot(ctx, SLOT_Q_TOPK, sizeof(float) * (size_t)ns * k, st);
+            uint32_t *keep_rows = (uint32_t *)ssh_slot(ctx, SLOT_Q_KEEP, sizeof(uint32_t) * (size_t)ns * KCAP, st);
+            float *keep_d32 = (float *)ssh_slot(ctx, SLOT_Q_KEEP_D, sizeof(float) * (size_t)ns * KCAP, st);
+            uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_HIST, sizeof(uint32_t) * (size_t)ns * KCAP, st);
+            double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)ns * KCAP, st);
+            if (!wrows || !wd32 || !wlb || !topk || !keep_rows || !keep_d32 || !resc || !d64) return SSH_ERR_OOM;
+            wave_init_kernel<<<ssh_div_up(std::max<int64_t>((int64_t)ns * k, ns), 256), 256, 0, st>>>(
+                ns, k, S.mcnt, S.thr, topk, S.pos, S.done, S.wcnt, S.keep_cnt, S.computed, S.aband);
             SSH_CHECK_LAUNCH();
-            if (ctx->profile && it == 0) {
-                thr0h.resize(nc);
-                cudaMemcpyAsync(thr0h.data(), B.thr, sizeof(float) * nc, cudaMemcpyDeviceToHost, st);
-            }
-            SSH_CUDA(cudaMemcpyAsync(&nact, B.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
+            std::vector<float> thr0h;
+            // waves over the active queries only: block row y = slot y = query act[y];
+            // the per-wave lists share one pool, so the per-slot capacity grows as
+            // queries finish
+            const int64_t pool = (int64_t)ns * WCAP;
+            compact_active_kernel<<<1, 1024, 0, st>>>(S.done, ns, S.act, S.nact);
+            SSH_CHECK_LAUNCH();
+            int nact = 0;
+            SSH_CUDA(cudaMemcpyAsync(&nact, S.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
             SSH_CUDA(cudaStreamSynchronize(st));
-            if (ctx->profile) {
-                ctx->prof[16] += 1;
-                ctx->prof[17] += nact;
-            }
-        }
-        int maxkeep = 0;
-        rc = max_of(B.keep_cnt, nc, st, &maxkeep);
-        if (rc) return rc;
-        SSH_REQUIRE(maxkeep <= KCAP, SSH_ERR_UNSUPPORTED,
-                    "ssh_query_batch: %d candidates within the rescoring margin of one query "
-                    "(limit %d; massively tied distances)", maxkeep, KCAP);
-        // K9/K10: rescoring set, exact f64 DTW, top-k by (d64, id)
-        pf.begin();
-        select_kernel<<<nc, 256, 0, st>>>(keep_rows, keep_d32, B.keep_cnt, KCAP, k, eps, resc, B.rcnt, cnt5,
-                                          B.mcnt, B.pos);
-        SSH_CHECK_LAUNCH();
-        int maxr = 0;
-        rc = max_of(B.rcnt, nc, st, &maxr);
-        if (rc) return rc;
-        rc = launch_dtw64_list(X, m, r, Qc, resc, KCAP, B.rcnt, maxr, d64, nc, st);
-        if (rc) return rc;
-        const int P2k = next_pow2(k);
-        size_t stk = (size_t)P2k * (sizeof(double) + sizeof(uint32_t));
-        SSH_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stk));
-        topk_kernel<<<nc, 256, stk, st>>>(resc, d64, B.rcnt, KCAP, P2k, k, ix->id_base, ncand,
-                                          (long long *)out_ids + (int64_t)q0 * k,
-                                          out_d2 + (int64_t)q0 * k, n_out + q0);
-        SSH_CHECK_LAUNCH();
-        finalize_counters<<<ssh_div_up(nc, 128), 128, 0, st>>>(B.computed, B.aband, nc, ncand, B.isfb, cnt5,
-                                                               status + q0);
-        SSH_CHECK_LAUNCH();
-        pf.end(5);
-        if (ctx->profile) {
-            std::vector<int> h(nc);
-            cudaMemcpy(h.data(), B.computed, sizeof(int) * nc, cudaMemcpyDeviceToHost);
-            for (int v : h) ctx->prof[8] += v;
-            cudaMemcpy(h.data(), B.rcnt, sizeof(int) * nc, cudaMemcpyDeviceToHost);
-            for (int v : h) ctx->prof[9] += v;
-            std::vector<float> thr1h(nc);
-            std::vector<double> dk((size_t)nc * k);
-            cudaMemcpy(thr1h.data(), B.thr, sizeof(float) * nc, cudaMemcpyDeviceToHost);
-            cudaMemcpy(dk.data(), out_d2 + (int64_t)q0 * k, sizeof(double) * nc * k, cudaMemcpyDeviceToHost);
-            for (int q = 0; q < nc; q++) {
-                double d = dk[(size_t)q * k + k - 1];
-                if (d > 0 && std::isfinite(d) && !thr0h.empty() && std::isfinite(thr0h[q])) {
-                    ctx->prof[13] += thr0h[q] / d;
-                    ctx->prof[14] += thr1h[q] / d;
-                    ctx->prof[15] += 1;
+            WaveLbArgs wl{Qs, S.U, S.Lo, (const uint4 *)ix->rec, ix->codes, ix->cstride, rows_s, lb_s, S.roff,
+                          S.mcnt, S.pos, S.done, S.thr, S.act, wrows, wlb, S.wcnt, c5s,
+                          ctx->profile ? ctx->d_cells : nullptr, m, ix->mp, W0, WCAP};
+            const int wl_warps = 8;
+            const size_t wl_smem = (size_t)3 * ix->mp * sizeof(float);
+            SSH_CUDA(cudaFuncSetAttribute(wave_lb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wl_smem));
+            for (int wave = W0, it = 0; nact > 0; wave *= 2, it++) {
+                const int wcap = (int)std::min<int64_t>((int64_t)1 << 20, (pool / nact) & ~(int64_t)255);
+                wave = std::min(wave, wcap);
+                pf.begin();
+                {
+                    dim3 g((unsigned)std::min(ssh_div_up(wave, 32 * wl_warps), 512), (unsigned)nact);
+                    wl.wave = wave;
+                    wl.wcap = wcap;
+                    wave_lb_kernel<<<g, 32 * wl_warps, wl_smem, st>>>(wl);
+                    SSH_CHECK_LAUNCH();
+                }
+                pf.end(3);
+                const float lb_ms = pf.last;
+                pf.begin();
+                {
+                    DtwList dl{wrows, wcap, S.wcnt, nullptr, wave, nullptr, wd32, S.aband, S.computed, S.act};
+                    DtwWave dw{wrows, wlb, wcap, S.wcnt, wd32, S.aband, S.computed, (const uint4 *)ix->rec,
+                               ix->codes, ix->cstride, ix->mp, S.act};
+                    rc = launch_dtw32_wave(ctx, X, Qs, S.U, S.Lo, dw, dl, S.thr, nact, wave, st);
+                    if (rc) return rc;
+                }
+                pf.end(4);
+                if (ctx->profile && getenv("SSH_DEBUG_WAVES"))
+                    fprintf(stderr, "wave %d: active %d wave %d cap %d | LB %.3f ms DTW %.3f ms\n", it, nact, wave,
+                            wcap, lb_ms, pf.last);
+                wave_update_kernel<<<nact, 256, 0, st>>>(S.act, wd32, wrows, S.wcnt, wcap, lb_s, S.roff, S.mcnt, wave,
+                                                         k, eps, topk, S.thr, S.pos, S.done, S.active, keep_rows,
+                                                         keep_d32, S.keep_cnt, KCAP);
+                SSH_CHECK_LAUNCH();
+                compact_active_kernel<<<1, 1024, 0, st>>>(S.done, ns, S.act, S.nact);
+                SSH_CHECK_LAUNCH();
+                if (ctx->profile && it == 0) {
+                    thr0h.resize(ns);
+                    cudaMemcpyAsync(thr0h.data(), S.thr, sizeof(float) * ns, cudaMemcpyDeviceToHost, st);
+                }
+                SSH_CUDA(cudaMemcpyAsync(&nact, S.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
+                SSH_CUDA(cudaStreamSynchronize(st));
+                if (ctx->profile) {
+                    ctx->prof[16] += 1;
+                    ctx->prof[17] += nact;
                 }
             }
+            int maxkeep = 0;
+            rc = max_of(S.keep_cnt, ns, st, &maxkeep);
+            if (rc) return rc;
+            SSH_REQUIRE(maxkeep <= KCAP, SSH_ERR_UNSUPPORTED,
+                        "ssh_query_batch: %d candidates within the rescoring margin of one query "
+                        "(limit %d; massively tied distances)", maxkeep, KCAP);
+            // K9/K10: rescoring set, exact f64 DTW, top-k by (d64, id)
+            pf.begin();
+            select_kernel<<<ns, 256, 0, st>>>(keep_rows, keep_d32, S.keep_cnt, KCAP, k, eps, resc, S.rcnt, c5s,
+                                              S.mcnt, S.pos);
+            SSH_CHECK_LAUNCH();
+            int maxr = 0;
+            rc = max_of(S.rcnt, ns, st, &maxr);
+            if (rc) return rc;
+            rc = launch_dtw64_list(X, m, r, Qs, resc, KCAP, S.rcnt, maxr, d64, ns, st);
+            if (rc) return rc;
+            const int P2k = next_pow2(k);
+            size_t stk = (size_t)P2k * (sizeof(double) + sizeof(uint32_t));
+            SSH_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stk));
+            topk_kernel<<<ns, 256, stk, st>>>(resc, d64, S.rcnt, KCAP, P2k, k, ix->id_base, ncs,
+                                              (long long *)out_ids + (int64_t)qs0 * k,
+                                              out_d2 + (int64_t)qs0 * k, n_out + qs0);
+            SSH_CHECK_LAUNCH();
+            finalize_counters<<<ssh_div_up(ns, 128), 128, 0, st>>>(S.computed, S.aband, ns, ncs, S.isfb, c5s,
+                                                                   status + qs0);
+            SSH_CHECK_LAUNCH();
+            pf.end(5);
+            if (ctx->profile) {
+                std::vector<int> h(ns);
+                cudaMemcpy(h.data(), S.computed, sizeof(int) * ns, cudaMemcpyDeviceToHost);
+                for (int v : h) ctx->prof[8] += v;
+                cudaMemcpy(h.data(), S.rcnt, sizeof(int) * ns, cudaMemcpyDeviceToHost);
+                for (int v : h) ctx->prof[9] += v;
+                std::vector<float> thr1h(ns);
+                std::vector<double> dk((size_t)ns * k);
+                cudaMemcpy(thr1h.data(), S.thr, sizeof(float) * ns, cudaMemcpyDeviceToHost);
+                cudaMemcpy(dk.data(), out_d2 + (int64_t)qs0 * k, sizeof(double) * ns * k, cudaMemcpyDeviceToHost);
+                for (int q = 0; q < ns; q++) {
+                    double d = dk[(size_t)q * k + k - 1];
+                    if (d > 0 && std::isfinite(d) && !thr0h.empty() && std::isfinite(thr0h[q])) {
+                        ctx->prof[13] += thr0h[q] / d;
+                        ctx->prof[14] += thr1h[q] / d;
+                        ctx->prof[15] += 1;
+                    }
+                }
+            }
+            sa = sb;
         }
     }
     return SSH_OK;

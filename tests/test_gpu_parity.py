@@ -400,3 +400,19 @@ def test_cascade_bounds_adversarial(cuda, kind):
             continue
         assert r.ids == ores["ids"][i][:n].tolist(), (kind, i)
         assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), (kind, i)
+
+
+def test_query_member_budget_split(cuda, golden, monkeypatch):
+    """A tiny member budget splits the batch into many sub-ranges (each with
+    its own member lists and wave loop); results stay identical."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw512")
+    c = golden["cases"]["rw512"]
+    idx = ssh.build_index(ssh.Dataset(X), params(band, K=1))
+    monkeypatch.setenv("SSH_DEBUG_MEMBER_BUDGET", "300")
+    res = ssh.query_index_batch(idx, Q, 10)
+    for qi, (r, g) in enumerate(zip(res, c["queries_k1"])):
+        assert r.stats.candidates == g["candidates"], qi
+        assert r.ids == g["ids"], qi
+        assert r.distances == g["distances"], qi
