@@ -245,14 +245,14 @@ __global__ void envelope_kernel(const float *__restrict__ Q, int m, int r, int s
 
 // ------------------------------------------------------ shard summaries
 // Rerank summaries of every row (layout in common.cuh): one warp per row.
-// The row is staged in the warp's shared-memory slice padded with -inf/+inf
-// outside [0, m); the per-row grid is lo = min x, sc ~ (max x - lo) / 254
-// with dec(255) >= max x verified; sample codes and PAA codes are chosen and
-// verified with the same fp32 dec() the query kernels use, so every stored
-// interval provably contains its value.  Then log-step doubling turns the
-// slice into running max/min and the envelope codes are written (upper code
-// rounded up, lower code rounded down: the fp32 LB_Keogh(q, env(x)) over
-// decoded codes never exceeds the exact one, dtw.py:124-151 envelope).
+// The row is staged in the warp's shared-memory slice; the per-row grid is
+// lo = min x, sc ~ (max x - lo) / 254 with dec(255) >= max x verified; sample
+// codes and PAA codes are chosen and verified with the same fp32 dec() the
+// query kernels use, so every stored interval provably contains its value.
+// The envelope codes come from the sample codes: over the window
+// [i - r, i + r] (dtw.py:124-151), U8 = max c + 1 and L8 = min c bracket the
+// exact running max / min (dec(c_j) <= x_j <= dec(c_j + 1)), computed by
+// byte-packed log-step doubling (__vmaxu4 on the codes and their complements).
 __device__ __forceinline__ float sdec(int c, float sc, float lo) { return fmaf((float)c, sc, lo); }
 
 // c in [0, 254] with dec(c) <= v <= dec(c + 1)
@@ -263,55 +263,41 @@ __device__ __forceinline__ int code_in(float v, float lo, float sc, float inv) {
     for (int it = 0; it < 256 && c < 254 && sdec(c + 1, sc, lo) < v; it++) c++;
     return c;
 }
-// smallest c in [0, 255] with dec(c) >= v (v <= dec(255))
-__device__ __forceinline__ int code_up(float v, float lo, float sc, float inv) {
-    int c = __float2int_ru((v - lo) * inv);
-    c = min(max(c, 0), 255);
-    for (int it = 0; it < 256 && c > 0 && sdec(c - 1, sc, lo) >= v; it++) c--;
-    for (int it = 0; it < 256 && c < 255 && sdec(c, sc, lo) < v; it++) c++;
-    return c;
-}
-// largest c in [0, 255] with dec(c) <= v (v >= lo)
-__device__ __forceinline__ int code_dn(float v, float lo, float sc, float inv) {
-    int c = __float2int_rd((v - lo) * inv);
-    c = min(max(c, 0), 255);
-    for (int it = 0; it < 256 && c < 255 && sdec(c + 1, sc, lo) <= v; it++) c++;
-    for (int it = 0; it < 256 && c > 0 && sdec(c, sc, lo) > v; it++) c--;
-    return c;
-}
-
 struct SumArgs {
     const float *X;
     int64_t N, ld, cstride;
-    int m, r, lev, pad, seg, nseg, mp;
+    int m, r, lev, pad, seg, nseg, mp, warp_bytes;
     uint4 *rec;
     uint8_t *codes;
 };
 
 __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
-    extern __shared__ float xsm[];
+    extern __shared__ __align__(16) unsigned char xsmb[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-    const int m = a.m, pad = a.pad;
-    float *mx = xsm + (size_t)w * (2 * pad + 16), *mn = mx + pad;
-    uint8_t *prec = reinterpret_cast<uint8_t *>(mn + pad);  // 64-byte record staging
+    const int m = a.m, pad = a.pad, padw = pad >> 2;
+    unsigned char *base = xsmb + (size_t)w * a.warp_bytes;
+    float *xs = reinterpret_cast<float *>(base);                      // m samples
+    uint32_t *cmx = reinterpret_cast<uint32_t *>(xs + ((m + 3) & ~3));  // pad bytes: codes, 0 outside
+    uint32_t *cmn = cmx + padw;                                       // pad bytes: 255 - codes, 0 outside
+    uint8_t *prec = reinterpret_cast<uint8_t *>(cmn + padw);          // 64-byte record staging
+    uint8_t *bmx = reinterpret_cast<uint8_t *>(cmx), *bmn = reinterpret_cast<uint8_t *>(cmn);
     const int win = 2 * a.r + 1;
-    const int sh = win - (1 << a.lev);
+    const int shw = win - (1 << a.lev);
     const int64_t nwarps = (int64_t)gridDim.x * nwb;
     for (int64_t row = (int64_t)blockIdx.x * nwb + w; row < a.N; row += nwarps) {
         const float *x = a.X + row * a.ld;
         float vmin = INFINITY, vmax = -INFINITY;
         bool fin = true;
-        for (int t = lane; t < pad; t += 32) {
-            const int j = t - a.r;
-            const bool in = j >= 0 && j < m;
-            const float v = in ? __ldg(x + j) : 0.f;
-            mx[t] = in ? v : -INFINITY;
-            mn[t] = in ? v : INFINITY;
-            if (in) {
-                fin = fin && isfinite(v);
-                vmin = fminf(vmin, v);
-                vmax = fmaxf(vmax, v);
-            }
+        for (int i = lane; i < m; i += 32) {
+            const float v = __ldg(x + i);
+            xs[i] = v;
+            fin = fin && isfinite(v);
+            vmin = fminf(vmin, v);
+            vmax = fmaxf(vmax, v);
+        }
+        for (int t = lane; t < padw; t += 32) {
+            cmx[t] = 0u;
+            cmn[t] = 0u;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -327,16 +313,19 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
         }
         if (!fin || !isfinite(sc) || sdec(255, sc, lo) < vmax) sc = __int_as_float(0x7FC00000);  // NaN
         const float inv = 1.0f / sc;
-        const float x0 = mx[a.r], xl = mx[a.r + m - 1];
-        // sample codes, 4 per lane per 128-sample chunk
+        // sample codes, 4 per lane per 128-sample chunk (global) + padded byte arrays (smem)
         uint8_t *cr = a.codes + row * a.cstride;
         for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
             uint32_t pk = 0;
 #pragma unroll
             for (int t = 0; t < 4; t++) {
                 const int i = i4 + t;
-                const int c = i < m ? code_in(mx[a.r + i], lo, sc, inv) : 0;
-                pk |= (uint32_t)c << (8 * t);
+                if (i < m) {
+                    const int c = code_in(xs[i], lo, sc, inv);
+                    pk |= (uint32_t)c << (8 * t);
+                    bmx[a.r + i] = (uint8_t)c;
+                    bmn[a.r + i] = (uint8_t)(255 - c);
+                }
             }
             *reinterpret_cast<uint32_t *>(cr + i4) = pk;
         }
@@ -349,7 +338,7 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
             if (s < a.nseg) {
                 const int b0 = s * a.seg, b1 = min(m, b0 + a.seg);
                 double sum = 0.0;
-                for (int i = b0; i < b1; i++) sum += (double)mx[a.r + i];
+                for (int i = b0; i < b1; i++) sum += (double)xs[i];
                 const double md = sum / (double)(b1 - b0);
                 c = __double2int_rd((md - (double)lo) * (double)inv);
                 c = min(max(c, 0), 254);
@@ -360,55 +349,57 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
             }
             prec[16 + s] = (uint8_t)c;
         }
-        if (lane == 0) {
-            float4 h = make_float4(lo, sc, x0, xl);
-            *reinterpret_cast<float4 *>(prec) = h;
-        }
+        if (lane == 0) *reinterpret_cast<float4 *>(prec) = make_float4(lo, sc, xs[0], xs[m - 1]);
         __syncwarp();
         if (lane < 4) a.rec[row * 4 + lane] = reinterpret_cast<const uint4 *>(prec)[lane];
-        // running max/min by log-step doubling
+        // running max of the codes and of their complements (= running min) over
+        // [t, t + 2^lev) by byte-packed log-step doubling
         for (int l = 0; l < a.lev; l++) {
-            const int d = 1 << l;
-            for (int t0 = 0; t0 < pad; t0 += 32 * 8) {
-                float va[8], vb[8];
+            const int d = 1 << l, dq = d >> 2;
+            const unsigned sel = d & 3 ? 0x3210u + 0x1111u * (unsigned)(d & 3) : 0x3210u;
+            for (int t0 = 0; t0 < padw; t0 += 32 * 8) {
+                uint32_t va[8], vb[8];
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
                     const int t = t0 + u * 32 + lane;
-                    if (t + d < pad) {
-                        va[u] = fmaxf(mx[t], mx[t + d]);
-                        vb[u] = fminf(mn[t], mn[t + d]);
-                    } else if (t < pad) {
-                        va[u] = mx[t];
-                        vb[u] = mn[t];
+                    if (t < padw) {
+                        const int q0 = t + dq;
+                        const uint32_t a0 = q0 < padw ? cmx[q0] : 0u, a1 = q0 + 1 < padw ? cmx[q0 + 1] : 0u;
+                        const uint32_t b0 = q0 < padw ? cmn[q0] : 0u, b1 = q0 + 1 < padw ? cmn[q0 + 1] : 0u;
+                        va[u] = __vmaxu4(cmx[t], __byte_perm(a0, a1, sel));
+                        vb[u] = __vmaxu4(cmn[t], __byte_perm(b0, b1, sel));
                     }
                 }
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
                     const int t = t0 + u * 32 + lane;
-                    if (t < pad) {
-                        mx[t] = va[u];
-                        mn[t] = vb[u];
+                    if (t < padw) {
+                        cmx[t] = va[u];
+                        cmn[t] = vb[u];
                     }
                 }
                 __syncwarp();
             }
         }
-        // envelope codes: (U8, L8) pairs, 4 samples per lane per chunk
-        for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
-            uint32_t p0 = 0, p1 = 0;
-#pragma unroll
-            for (int t = 0; t < 4; t++) {
-                const int i = i4 + t;
-                int cu = 255, cl = 0;
-                if (i < m) {
-                    cu = code_up(fmaxf(mx[i], mx[i + sh]), lo, sc, inv);
-                    cl = code_dn(fminf(mn[i], mn[i + sh]), lo, sc, inv);
+        // envelope codes of samples i4..i4+3: window [i - r, i + r] = padded
+        // [i, i + win) = max over [i, i + 2^lev) and [i + shw, i + shw + 2^lev);
+        // U8 = max code + 1 (dec(c + 1) >= x), L8 = min code (dec(c) <= x)
+        {
+            const int sq = shw >> 2;
+            const unsigned sel = shw & 3 ? 0x3210u + 0x1111u * (unsigned)(shw & 3) : 0x3210u;
+            for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
+                const int t = i4 >> 2;
+                uint32_t u = 0xFFFFFFFFu, lw = 0u;
+                if (i4 < m) {
+                    const uint32_t ma = __vmaxu4(cmx[t], __byte_perm(cmx[t + sq], cmx[t + sq + 1], sel));
+                    const uint32_t mb = __vmaxu4(cmn[t], __byte_perm(cmn[t + sq], cmn[t + sq + 1], sel));
+                    u = __vadd4(ma, 0x01010101u);
+                    lw = ~mb;  // 255 - max(255 - c) = min c
                 }
-                const uint32_t pr = (uint32_t)cu | ((uint32_t)cl << 8);
-                if (t < 2) p0 |= pr << (16 * t); else p1 |= pr << (16 * (t - 2));
+                const uint32_t p0 = __byte_perm(u, lw, 0x5140u), p1 = __byte_perm(u, lw, 0x7362u);
+                *reinterpret_cast<uint2 *>(cr + a.mp + 2 * i4) = make_uint2(p0, p1);
             }
-            *reinterpret_cast<uint2 *>(cr + a.mp + 2 * i4) = make_uint2(p0, p1);
         }
         __syncwarp();
     }
@@ -422,8 +413,11 @@ int ssh_launch_summaries(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t N,
     const int mp = ((m + 127) / 128) * 128;
     int lev = 0;
     while ((2 << lev) <= 2 * r + 1) lev++;
-    const int pad = ((m + 2 * r + (1 << lev)) + 3) & ~3;
-    const size_t per_warp = ((size_t)2 * pad + 16) * sizeof(float);
+    // padded code arrays: sample j at byte j + r; the last doubling read
+    // reaches byte (m - 1) + 2r + 2^lev + 3 -> round up to whole words + 1
+    const int pad = ((m + 2 * r + (1 << lev) + 12) + 7) & ~7;  // 2 pad % 16 == 0: the record stays 16-byte aligned
+    const int warp_bytes = (((m + 3) & ~3) * 4 + 2 * pad + 64 + 15) & ~15;
+    const size_t per_warp = (size_t)warp_bytes;
     const int nwb = (int)std::min<size_t>(8, (200 * 1024) / per_warp);
     SSH_REQUIRE(nwb >= 1, SSH_ERR_UNSUPPORTED, "series too long for the summaries kernel (m=%d, r=%d)", m, r);
     if (!ix->rec) {
@@ -439,7 +433,7 @@ int ssh_launch_summaries(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t N,
     ix->nseg = nseg;
     ix->mp = mp;
     ix->cstride = (int64_t)3 * mp;
-    SumArgs a{X, N, ld, ix->cstride, m, r, lev, pad, seg, nseg, mp, (uint4 *)ix->rec, ix->codes};
+    SumArgs a{X, N, ld, ix->cstride, m, r, lev, pad, seg, nseg, mp, warp_bytes, (uint4 *)ix->rec, ix->codes};
     const size_t smem = per_warp * nwb;
     SSH_CUDA(cudaFuncSetAttribute(summaries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
@@ -1059,8 +1053,6 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
 // with the totals from the wave LB kernel (code-based terms; the exact-x row
 // terms subtracted here are never smaller, so remK stays a lower bound) and
 // slack = total * (2m + 8) u for the fp32 running sums.
-#define DW_WARPS 8
-#define DW_ITEMS (32 * DW_WARPS)
 
 struct DtwWave {
     const uint32_t *rows;
@@ -1077,12 +1069,13 @@ struct DtwWave {
     const int *act;  // block row y -> query act[y]; rows/lbs/out/cnt per slot y
 };
 
-template <int R>
-__global__ void __launch_bounds__(DW_ITEMS, R <= 32 ? 2 : 1)
+template <int R, int DW_WARPS>
+__global__ void __launch_bounds__(32 * DW_WARPS)
 dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, const float *__restrict__ U,
               const float *__restrict__ Lo, DtwWave L, const float *__restrict__ thr,
               unsigned long long *__restrict__ cells) {
     constexpr int NB = 2 * R + 1;
+    constexpr int DW_ITEMS = 32 * DW_WARPS;
     extern __shared__ __align__(16) float wsm2[];
     __shared__ int n_live, n_next;
     const int slot = blockIdx.y;
@@ -1093,8 +1086,8 @@ dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
     if (base >= total) return;
     const int n0 = min(total - base, DW_ITEMS);
     const int YP = ((m + 2 * R + 8) + 3) & ~3;
-    float *yc = wsm2;           // 4 x YP
-    float *su = yc + 4 * YP;    // m
+    float *yc = wsm2;           // YP: y[j] at yc[j + R], +inf outside [0, m)
+    float *su = yc + YP;        // m
     float *sl = su + m;         // m
     float *sband = sl + m;      // NB x DW_ITEMS
     float *sremk = sband + NB * DW_ITEMS, *srem2 = sremk + DW_ITEMS;
@@ -1103,8 +1096,8 @@ dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
     uint32_t *srow = reinterpret_cast<uint32_t *>(ssc + DW_ITEMS);
     int *se = reinterpret_cast<int *>(srow + DW_ITEMS);
     const float *y = Q + (int64_t)q * m;
-    for (int t = threadIdx.x; t < 4 * YP; t += blockDim.x) {
-        int c = t / YP, jj = (t - c * YP) + c - R;
+    for (int t = threadIdx.x; t < YP; t += blockDim.x) {
+        const int jj = t - R;
         yc[t] = (jj >= 0 && jj < m) ? y[jj] : INFINITY;
     }
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -1733,20 +1726,33 @@ static int launch_dtw32r(ssh_ctx *ctx, const float *X, const float *Q, const flo
     return SSH_OK;
 }
 
+template <int R, int DW_WARPS>
+static int launch_dtw32w_w(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
+                           const DtwWave &L, const float *thr, int nq, int wave, cudaStream_t st) {
+    const int m = ctx->p.m;
+    constexpr int NB = 2 * R + 1;
+    constexpr int DW_ITEMS = 32 * DW_WARPS;
+    const int YP = ((m + 2 * R + 8) + 3) & ~3;
+    const size_t smem = (size_t)(YP + 2 * m + (NB + 6) * DW_ITEMS) * sizeof(float) + 2 * DW_ITEMS * 4;
+    SSH_REQUIRE(smem <= 227 * 1024, SSH_ERR_UNSUPPORTED, "wave DTW: series too long (m=%d)", m);
+    SSH_CUDA(cudaFuncSetAttribute(dtw32w_kernel<R, DW_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    dim3 grid((unsigned)ssh_div_up(wave, DW_ITEMS), (unsigned)nq);
+    dtw32w_kernel<R, DW_WARPS><<<grid, DW_ITEMS, smem, st>>>(X, m, Q, U, Lo, L, thr,
+                                                             ctx->profile ? ctx->d_cells : nullptr);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
+// block size by wave length: small early waves use 2-warp blocks (more
+// resident blocks per SM), long waves 8-warp blocks (more to compact)
 template <int R>
 static int launch_dtw32w(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
                          const DtwWave &L, const float *thr, int nq, int wave, cudaStream_t st) {
-    const int m = ctx->p.m;
-    constexpr int NB = 2 * R + 1;
-    const int YP = ((m + 2 * R + 8) + 3) & ~3;
-    const size_t smem = (size_t)(4 * YP + 2 * m + (NB + 6) * DW_ITEMS) * sizeof(float) + 2 * DW_ITEMS * 4;
-    SSH_REQUIRE(smem <= 227 * 1024, SSH_ERR_UNSUPPORTED, "wave DTW: series too long (m=%d)", m);
-    SSH_CUDA(cudaFuncSetAttribute(dtw32w_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (wave <= 0) return SSH_OK;
-    dim3 grid((unsigned)ssh_div_up(wave, DW_ITEMS), (unsigned)nq);
-    dtw32w_kernel<R><<<grid, DW_ITEMS, smem, st>>>(X, m, Q, U, Lo, L, thr, ctx->profile ? ctx->d_cells : nullptr);
-    SSH_CHECK_LAUNCH();
-    return SSH_OK;
+    if (wave <= 256) return launch_dtw32w_w<R, 2>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
+    if (wave <= 2048) return launch_dtw32w_w<R, 4>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
+    return launch_dtw32w_w<R, 8>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
 }
 
 // wave fp32 DTW: compacting register-band kernel for the common radii, the
@@ -1784,7 +1790,7 @@ static int launch_dtw32_wave(ssh_ctx *ctx, const float *X, const float *Q, const
                              cudaStream_t st) {
     const int m = ctx->p.m, r = ctx->p.radius;
     const int YPmax = m + 2 * r + 12;
-    const bool fits = (m & 3) == 0 && (size_t)(4 * YPmax + 2 * m + (2 * r + 7) * DW_ITEMS + 2 * DW_ITEMS) * 4 <= 227 * 1024;
+    const bool fits = (m & 3) == 0 && (size_t)(YPmax + 2 * m + (2 * r + 9) * 256) * 4 <= 227 * 1024;
 #define DTWW(RR) \
     case RR:     \
         if (fits) return launch_dtw32w<RR>(ctx, X, Q, U, Lo, W, thr, nq, wave, st); \
