@@ -456,7 +456,7 @@ __device__ void warp_cws(const SigArgs &a, int64_t row, const WarpSmem &w, int D
 }
 
 template <int MODE, int NS>
-__global__ void __launch_bounds__(32 * SG_WARPS, 3) shingle_cws_kernel(SigArgs a, int warps) {
+__global__ void __launch_bounds__(32 * SG_WARPS, 4) shingle_cws_kernel(SigArgs a, int warps) {
     extern __shared__ __align__(16) unsigned char sg_smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
