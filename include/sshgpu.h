@@ -122,9 +122,16 @@ int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int64_t id_bas
                     ssh_index **out, void *stream);
 /* K1 -> K4 fused — build_index (index.py:159-172): signatures (written to
  * sig_out u64[N][L] when non-NULL), bucket tables and the shard's rerank
- * summary (PAA means, emitted by the sketch kernel while it stages X). */
+ * summaries (64-byte series records + u8 sample/envelope codes, computed on a
+ * side stream).  X stays owned by the caller and is read by later queries. */
 int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, int64_t id_base,
                     uint64_t *sig_out, ssh_index **out, void *stream);
+/* Same from HOST series (pinned memory for copy/compute overlap): rows are
+ * copied in 65536-row chunks into the caller's device buffer X_dev (N x ld
+ * f32, kept for queries) while the previous chunk is sketched, signed and
+ * summarised; sig_out (u64[N][L], device) is required. */
+int ssh_build_index_host(ssh_ctx *ctx, const float *X_host, int64_t N, int64_t ld, int64_t id_base,
+                         float *X_dev, uint64_t *sig_out, ssh_index **out, void *stream);
 int ssh_index_destroy(ssh_index *idx);
 int ssh_index_num_buckets(const ssh_index *idx, int table, int64_t *n_buckets);
 int64_t ssh_index_size(const ssh_index *idx);

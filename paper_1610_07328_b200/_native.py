@@ -103,6 +103,7 @@ def lib():
             "ssh_signatures": ([P, P, i64, i64, P, P, P], ctypes.c_int),
             "ssh_index_build": ([P, P, i64, i64, PP, P], ctypes.c_int),
             "ssh_build_index": ([P, P, i64, i64, i64, P, PP, P], ctypes.c_int),
+            "ssh_build_index_host": ([P, P, i64, i64, i64, P, P, PP, P], ctypes.c_int),
             "ssh_index_destroy": ([P], ctypes.c_int),
             "ssh_index_num_buckets": ([P, ctypes.c_int, ctypes.POINTER(i64)], ctypes.c_int),
             "ssh_index_size": ([P], i64),
@@ -124,7 +125,7 @@ EXPORTED = [
     "ssh_last_error", "ssh_abi_version", "ssh_launch_count", "ssh_ctx_set_profiling",
     "ssh_ctx_profile", "ssh_ctx_create", "ssh_ctx_destroy", "ssh_ctx_set_params",
     "ssh_num_sketch_bits", "ssh_sketch_words", "ssh_tokens_per_series", "ssh_sketch", "ssh_shingle",
-    "ssh_cws", "ssh_signatures", "ssh_index_build", "ssh_build_index", "ssh_index_destroy", "ssh_index_num_buckets",
+    "ssh_cws", "ssh_signatures", "ssh_index_build", "ssh_build_index", "ssh_build_index_host", "ssh_index_destroy", "ssh_index_num_buckets",
     "ssh_index_size", "ssh_index_export", "ssh_index_summarize", "ssh_probe", "ssh_query_batch", "ssh_dtw_exact",
 ]
 

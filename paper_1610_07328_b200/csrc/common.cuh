@@ -64,7 +64,8 @@ struct ssh_ctx {
                                             // [3] members visited by the filter
     // side stream for independent build work (candidate envelopes), joined by events
     cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t copy = nullptr;  // host->device series chunks (ssh_build_index_host)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_copy = nullptr;
     // named grow-only scratch slots reused across calls (stream-ordered)
     void *slot_ptr[32] = {nullptr};
     size_t slot_bytes[32] = {0};
@@ -91,6 +92,7 @@ enum {
     SLOT_Q_KEEP,
     SLOT_Q_KEEP_D,
     SLOT_Q_WLB,
+    SLOT_Q_KHIST,
     SLOT_COUNT
 };
 
@@ -129,6 +131,10 @@ void *ssh_slot(ssh_ctx *ctx, int slot, size_t bytes, cudaStream_t st);
 
 // rerank summaries of N rows into ix (allocates rec/codes if needed)
 int ssh_launch_summaries(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t N, int64_t ld, cudaStream_t st);
+// allocate ix's summaries for N rows / summarise rows [r0, r0 + n) of X (row r0 at X)
+int ssh_alloc_summaries(ssh_ctx *ctx, ssh_index *ix, int64_t N, cudaStream_t st);
+int ssh_launch_summaries_rows(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t r0, int64_t n, int64_t ld,
+                              cudaStream_t st);
 
 // ----------------------------------------------------------- device math
 __host__ __device__ __forceinline__ uint64_t ssh_mix64(uint64_t x) {

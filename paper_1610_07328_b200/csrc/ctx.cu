@@ -97,8 +97,10 @@ extern "C" int ssh_ctx_create(int device, ssh_ctx **out) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return ssh_cuda_fail(cudaGetLastError(), "ssh_ctx_create streams", __FILE__, __LINE__);
     }
@@ -125,6 +127,8 @@ extern "C" int ssh_ctx_destroy(ssh_ctx *ctx) {
         if (ctx->slot_ptr[i]) cudaFree(ctx->slot_ptr[i]);
     if (ctx->d_cells) cudaFree(ctx->d_cells);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     delete ctx;

@@ -405,43 +405,70 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
     }
 }
 
-int ssh_launch_summaries(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t N, int64_t ld,
-                         cudaStream_t st) {
+struct SumGeom {
+    int seg, nseg, mp, lev, pad, warp_bytes, nwb;
+};
+
+static int summaries_geom(const ssh_ctx *ctx, SumGeom &g) {
     const int m = ctx->p.m, r = ctx->p.radius;
-    const int seg = (m + SSH_REC_CODES - 1) / SSH_REC_CODES;
-    const int nseg = (m + seg - 1) / seg;
-    const int mp = ((m + 127) / 128) * 128;
-    int lev = 0;
-    while ((2 << lev) <= 2 * r + 1) lev++;
+    g.seg = (m + SSH_REC_CODES - 1) / SSH_REC_CODES;
+    g.nseg = (m + g.seg - 1) / g.seg;
+    g.mp = ((m + 127) / 128) * 128;
+    g.lev = 0;
+    while ((2 << g.lev) <= 2 * r + 1) g.lev++;
     // padded code arrays: sample j at byte j + r; the last doubling read
-    // reaches byte (m - 1) + 2r + 2^lev + 3 -> round up to whole words + 1
-    const int pad = ((m + 2 * r + (1 << lev) + 12) + 7) & ~7;  // 2 pad % 16 == 0: the record stays 16-byte aligned
-    const int warp_bytes = (((m + 3) & ~3) * 4 + 2 * pad + 64 + 15) & ~15;
-    const size_t per_warp = (size_t)warp_bytes;
-    const int nwb = (int)std::min<size_t>(8, (200 * 1024) / per_warp);
-    SSH_REQUIRE(nwb >= 1, SSH_ERR_UNSUPPORTED, "series too long for the summaries kernel (m=%d, r=%d)", m, r);
+    // reaches byte (m - 1) + 2r + 2^lev + 3; 2 pad % 16 == 0 keeps the record aligned
+    g.pad = ((m + 2 * r + (1 << g.lev) + 12) + 7) & ~7;
+    g.warp_bytes = (((m + 3) & ~3) * 4 + 2 * g.pad + 64 + 15) & ~15;
+    g.nwb = (int)std::min<size_t>(8, (200 * 1024) / (size_t)g.warp_bytes);
+    SSH_REQUIRE(g.nwb >= 1, SSH_ERR_UNSUPPORTED, "series too long for the summaries kernel (m=%d, r=%d)", m, r);
+    return SSH_OK;
+}
+
+int ssh_alloc_summaries(ssh_ctx *ctx, ssh_index *ix, int64_t N, cudaStream_t st) {
+    SumGeom g;
+    int rc = summaries_geom(ctx, g);
+    if (rc) return rc;
     if (!ix->rec) {
         SSH_CUDA(cudaMallocAsync(&ix->rec, (size_t)64 * N, st));
-        cudaError_t e = cudaMallocAsync((void **)&ix->codes, (size_t)3 * mp * N, st);
+        cudaError_t e = cudaMallocAsync((void **)&ix->codes, (size_t)3 * g.mp * N, st);
         if (e != cudaSuccess) {
             cudaFreeAsync(ix->rec, st);
             ix->rec = nullptr;
             return ssh_cuda_fail(e, "rerank summaries (3 m bytes per series)", __FILE__, __LINE__);
         }
     }
-    ix->seg = seg;
-    ix->nseg = nseg;
-    ix->mp = mp;
-    ix->cstride = (int64_t)3 * mp;
-    SumArgs a{X, N, ld, ix->cstride, m, r, lev, pad, seg, nseg, mp, warp_bytes, (uint4 *)ix->rec, ix->codes};
-    const size_t smem = per_warp * nwb;
+    ix->seg = g.seg;
+    ix->nseg = g.nseg;
+    ix->mp = g.mp;
+    ix->cstride = (int64_t)3 * g.mp;
+    return SSH_OK;
+}
+
+int ssh_launch_summaries_rows(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t r0, int64_t n, int64_t ld,
+                              cudaStream_t st) {
+    if (n <= 0) return SSH_OK;
+    SumGeom g;
+    int rc = summaries_geom(ctx, g);
+    if (rc) return rc;
+    const int m = ctx->p.m, r = ctx->p.radius;
+    SumArgs a{X, n, ld, ix->cstride, m, r, g.lev, g.pad, g.seg, g.nseg, g.mp, g.warp_bytes,
+              (uint4 *)ix->rec + r0 * 4, ix->codes + r0 * ix->cstride};
+    const size_t smem = (size_t)g.warp_bytes * g.nwb;
     SSH_CUDA(cudaFuncSetAttribute(summaries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, summaries_kernel, 32 * nwb, smem);
-    const int grid = (int)std::min<int64_t>((N + nwb - 1) / nwb, (int64_t)ctx->num_sms * std::max(1, per_sm));
-    summaries_kernel<<<grid, 32 * nwb, smem, st>>>(a);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, summaries_kernel, 32 * g.nwb, smem);
+    const int grid = (int)std::min<int64_t>((n + g.nwb - 1) / g.nwb, (int64_t)ctx->num_sms * std::max(1, per_sm));
+    summaries_kernel<<<grid, 32 * g.nwb, smem, st>>>(a);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
+}
+
+int ssh_launch_summaries(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t N, int64_t ld,
+                         cudaStream_t st) {
+    int rc = ssh_alloc_summaries(ctx, ix, N, st);
+    if (rc) return rc;
+    return ssh_launch_summaries_rows(ctx, ix, X, 0, N, ld, st);
 }
 
 extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t ld,
@@ -455,14 +482,19 @@ extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, 
 
 // --------------------------------------------------- LB_PAA of every member
 // One CTA per (query, slice of MB_SLICE_WORDS bitmap words).  A warp turns 32
-// words into a member list in shared memory, reserves space in the query's
-// CSR segment with one atomic, and evaluates lane-per-member the summary key
-// from the member's 64-byte record (L2-resident for shards up to ~2M rows):
+// words into a member list in shared memory and evaluates lane-per-member the
+// summary key from the member's 64-byte record (L2-resident for shards up to
+// ~2M rows):
 //   LB_PAA = shrink * sum_seg len * max(dec(c) - Useg, Lseg - dec(c+1), 0)^2
 //   LB_Kim = (x_0 - q_0)^2 + (x_last - q_last)^2            (dtw.py:154-160)
 //   key    = max(LB_PAA, LB_Kim), bit 0 = "LB_Kim is the larger" (the key is
 //            first lowered by >= 1 ulp, so setting the bit keeps it a bound)
 // shrink = 1 - (3 nseg + 8) u absorbs the fp32 evaluation error.
+// SAMPLE: members of every 8th bitmap word only; their key bins go to a
+// per-query histogram (cutoff choice).  Otherwise members whose key bin lies
+// in [binlo_q, binhi_q] are appended to the query's list; the LB_PAA sum is
+// abandoned once a partial sum passes the upper bin (a partial sum is a lower
+// bound of the key).
 struct PaaArgs {
     const float *Useg, *Lseg, *Q;
     const uint4 *rec;
@@ -471,6 +503,8 @@ struct PaaArgs {
     uint32_t *rows;
     float *lb;
     int *cnt;
+    const int *binlo, *binhi;  // per query (full pass)
+    unsigned *hist;            // [q][NBINS] (sample pass)
     int64_t NW;
     int m, seg, nseg;
 };
@@ -480,6 +514,9 @@ __device__ __forceinline__ float code_f(uint32_t w, int t) {
     return __uint_as_float(__byte_perm(w, 0x4B000000u, (unsigned)t | 0x7440u)) - 8388608.f;
 }
 
+#define SAMPLE_SHIFT 3  // sample pass: bitmap words w with w % 8 == 0
+
+template <bool SAMPLE>
 __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
     extern __shared__ __align__(16) unsigned char msm[];
     __shared__ float sUs[SSH_REC_CODES], sLs[SSH_REC_CODES];
@@ -487,22 +524,37 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nseg = a.nseg;
     uint32_t *list = reinterpret_cast<uint32_t *>(msm) + w * 1024;
+    float *accb = reinterpret_cast<float *>(msm) + MB_WARPS * 1024 + w * 1024;
+    unsigned *shist = reinterpret_cast<unsigned *>(msm) + 2 * MB_WARPS * 1024;  // SAMPLE: NBINS
+    int blo = 0, bhi = NBINS - 1;
+    if (!SAMPLE) {
+        blo = a.binlo[q];
+        bhi = a.binhi[q];
+        if (blo > bhi) return;  // block-uniform: nothing to collect for this query
+    }
     for (int s = threadIdx.x; s < SSH_REC_CODES; s += MB_THREADS) {
         // unused segments contribute max(dec - inf, -inf - dec, 0) = 0
         sUs[s] = s < nseg ? a.Useg[(int64_t)q * nseg + s] : INFINITY;
         sLs[s] = s < nseg ? a.Lseg[(int64_t)q * nseg + s] : -INFINITY;
     }
+    if (SAMPLE)
+        for (int b = threadIdx.x; b < NBINS; b += MB_THREADS) shist[b] = 0u;
     __syncthreads();
     const float q0 = a.Q[(int64_t)q * a.m], ql = a.Q[(int64_t)q * a.m + a.m - 1];
     const float shrink = 1.f - (3.f * nseg + 8.f) * U32_EPS;
     const float segf = (float)a.seg;
     const float lastlen = (float)(a.m - (nseg - 1) * a.seg);
+    // smallest key value in bin bhi + 1: keys at or above it are dropped
+    const float edge = bhi >= NBINS - 1 ? INFINITY : __uint_as_float((uint32_t)(bhi + 1) << 20);
     const uint32_t *bm = a.bitmap + (int64_t)q * a.NW;
     const int64_t base_q = a.roff[q];
-    const int64_t s0 = (int64_t)blockIdx.x * MB_SLICE_WORDS;
-    const int64_t s1 = min(a.NW, s0 + MB_SLICE_WORDS);
-    for (int64_t wb = s0 + 32 * w; wb < s1; wb += 32 * MB_WARPS) {
-        const int64_t wd = wb + lane;
+    // a sample block covers 2^SAMPLE_SHIFT slices (same sampled words per block)
+    const int64_t slice = SAMPLE ? ((int64_t)MB_SLICE_WORDS << SAMPLE_SHIFT) : MB_SLICE_WORDS;
+    const int64_t s0 = (int64_t)blockIdx.x * slice;
+    const int64_t s1 = min(a.NW, s0 + slice);
+    const int wstep = SAMPLE ? (32 << SAMPLE_SHIFT) : 32;
+    for (int64_t wb = s0 + (int64_t)wstep * w; wb < s1; wb += (int64_t)wstep * MB_WARPS) {
+        const int64_t wd = wb + (SAMPLE ? ((int64_t)lane << SAMPLE_SHIFT) : lane);
         uint32_t word = wd < s1 ? bm[wd] : 0u;
         const int c = __popc(word);
         int incl = c;
@@ -519,37 +571,138 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
             word &= word - 1;
             list[pos++] = (uint32_t)(wd * 32 + b);
         }
-        int dst = 0;
-        if (lane == 0) dst = atomicAdd(&a.cnt[q], total);
-        dst = __shfl_sync(0xFFFFFFFFu, dst, 0);
         __syncwarp();
-        for (int e = lane; e < total; e += 32) {
-            const uint32_t row = list[e];
-            const uint4 *rp = a.rec + (int64_t)row * 4;
-            const uint4 h = __ldg(rp);
-            const uint4 c0 = __ldg(rp + 1), c1 = __ldg(rp + 2), c2 = __ldg(rp + 3);
-            const uint32_t cw[12] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w};
-            const float lo = __uint_as_float(h.x), sc = __uint_as_float(h.y);
-            float acc = 0.f;
+        // three passes over the list, one 16-segment group each; after each
+        // pass the members still below the edge are compacted in place (rows
+        // in list, partial sums in accb) so every pass runs on full warps
+        int n = total;
+        for (int g = 0; g < 3 && n > 0; g++) {
+            int nk = 0;
+            for (int e0 = 0; e0 < n; e0 += 32) {
+                const int e = e0 + lane;
+                bool keep = false;
+                float acc = 0.f, key = 0.f;
+                uint32_t row = 0;
+                if (e < n) {
+                    row = list[e];
+                    acc = g ? accb[e] : 0.f;
+                    const uint4 *rp = a.rec + (int64_t)row * 4;
+                    const float2 h = __ldg(reinterpret_cast<const float2 *>(rp));
+                    const float lo = h.x, sc = h.y;
+                    const uint4 cg = __ldg(rp + 1 + g);
+                    const uint32_t cw[4] = {cg.x, cg.y, cg.z, cg.w};
 #pragma unroll
-            for (int s = 0; s < SSH_REC_CODES; s++) {
-                const float cf = code_f(cw[s >> 2], s & 3);
-                const float xa = cf == 255.f ? lo : fmaf(cf, sc, lo);
-                const float xb = fmaf(cf + 1.f, sc, lo);
-                const float ev = fmaxf(fmaxf(xa - sUs[s], sLs[s] - xb), 0.f);
-                const float len = s == nseg - 1 ? lastlen : segf;
-                acc = fmaf(len * ev, ev, acc);
+                    for (int j = 0; j < 16; j++) {
+                        const int sgi = 16 * g + j;
+                        const float cf = code_f(cw[j >> 2], j & 3);
+                        const float xa = cf == 255.f ? lo : fmaf(cf, sc, lo);
+                        const float xb = fmaf(cf + 1.f, sc, lo);
+                        const float ev = fmaxf(fmaxf(xa - sUs[sgi], sLs[sgi] - xb), 0.f);
+                        const float len = sgi == nseg - 1 ? lastlen : segf;
+                        acc = fmaf(len * ev, ev, acc);
+                    }
+                    if (g < 2) {
+                        keep = SAMPLE || acc * shrink * (1.f - 4.f * U32_EPS) < edge;
+                    } else {
+                        const float2 kx = __ldg(reinterpret_cast<const float2 *>(rp) + 1);
+                        const float d0 = kx.x - q0, dl = kx.y - ql;
+                        const float kim = a.m >= 2 ? fmaf(dl, dl, d0 * d0) : d0 * d0;
+                        const float paa = acc * shrink;
+                        if (kim > paa) key = __uint_as_float(__float_as_uint(kim * (1.f - 2.f * U32_EPS)) | 1u);
+                        else key = __uint_as_float(__float_as_uint(paa) & ~1u);
+                        const int kb = (int)lb_bin(key);
+                        keep = kb >= blo && kb <= bhi;
+                    }
+                }
+                if (g < 2) {
+                    const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+                    __syncwarp();
+                    if (keep) {
+                        const int p = nk + __popc(km & ((1u << lane) - 1u));
+                        list[p] = row;
+                        accb[p] = acc;
+                    }
+                    nk += __popc(km);
+                    __syncwarp();
+                } else if (SAMPLE) {
+                    const unsigned bin = keep ? lb_bin(key) : 0xFFFFFFFFu;
+                    const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+                    if (keep && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&shist[bin], (unsigned)__popc(peers));
+                } else {
+                    const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+                    if (km) {
+                        int dst = 0;
+                        if (lane == 0) dst = atomicAdd(&a.cnt[q], __popc(km));
+                        dst = __shfl_sync(0xFFFFFFFFu, dst, 0) + __popc(km & ((1u << lane) - 1u));
+                        if (keep) {
+                            a.rows[base_q + dst] = row;
+                            a.lb[base_q + dst] = key;
+                        }
+                    }
+                }
             }
-            const float paa = acc * shrink;
-            const float d0 = __uint_as_float(h.z) - q0, dl = __uint_as_float(h.w) - ql;
-            const float kim = a.m >= 2 ? fmaf(dl, dl, d0 * d0) : d0 * d0;
-            float key;
-            if (kim > paa) key = __uint_as_float(__float_as_uint(kim * (1.f - 2.f * U32_EPS)) | 1u);
-            else key = __uint_as_float(__float_as_uint(paa) & ~1u);
-            a.rows[base_q + dst + e] = row;
-            a.lb[base_q + dst + e] = key;
+            n = nk;
         }
         __syncwarp();
+    }
+    if (SAMPLE) {
+        __syncthreads();
+        for (int b = threadIdx.x; b < NBINS; b += MB_THREADS)
+            if (shist[b]) atomicAdd(&a.hist[(int64_t)q * NBINS + b], shist[b]);
+    }
+}
+
+// Per-query member cutoff from the sampled key histogram: the smallest bin b
+// whose sampled cumulative count reaches target >> SAMPLE_SHIFT (all bins when
+// the sample is smaller).  Round 0 keeps bins [0, b]; overflow rounds [b+1, ...).
+__global__ void cutoff_kernel(const unsigned *__restrict__ hist, int target, int *__restrict__ binlo,
+                              int *__restrict__ binhi) {
+    __shared__ unsigned part[256];
+    const int q = blockIdx.x;
+    constexpr int PER = NBINS / 256;
+    const unsigned *hq = hist + (int64_t)q * NBINS;
+    unsigned loc = 0;
+    for (int i = 0; i < PER; i++) loc += hq[threadIdx.x * PER + i];
+    part[threadIdx.x] = loc;
+    __syncthreads();
+    for (int off = 1; off < 256; off <<= 1) {
+        const unsigned v = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    const unsigned need = (unsigned)(target >> SAMPLE_SHIFT);
+    const unsigned before = part[threadIdx.x] - loc;
+    if (threadIdx.x == 0) {
+        binlo[q] = 0;
+        if (part[255] < need) binhi[q] = NBINS - 1;
+    }
+    if (part[255] >= need && before < need && part[threadIdx.x] >= need) {
+        unsigned run = before;
+        int b = threadIdx.x * PER;
+        for (int i = 0; i < PER; i++) {
+            run += hq[threadIdx.x * PER + i];
+            if (run >= need) {
+                b = threadIdx.x * PER + i;
+                break;
+            }
+        }
+        binhi[q] = b;
+    }
+}
+
+// overflow round: queries whose round-0 list ran out below their threshold get
+// the bins above their cutoff; the others get an empty window
+__global__ void overflow_window_kernel(const int *__restrict__ overflow, int nq, int *__restrict__ binlo,
+                                       int *__restrict__ binhi) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    if (overflow[q]) {
+        binlo[q] = binhi[q] + 1;
+        binhi[q] = NBINS - 1;
+    } else {
+        binlo[q] = NBINS;
+        binhi[q] = NBINS - 1;
     }
 }
 
@@ -1353,9 +1506,10 @@ __global__ void wave_update_kernel(const int *__restrict__ act, const float *__r
                                    const uint32_t *__restrict__ wrows,
                                    int *__restrict__ wcnt, int wcap, const float *__restrict__ slbp,
                                    const int64_t *__restrict__ roff, const int *__restrict__ cnt,
+                                   const int *__restrict__ binhi,
                                    int wave, int k, float eps, float *__restrict__ topk,
                                    float *__restrict__ thr, int *__restrict__ pos,
-                                   int *__restrict__ done, int *__restrict__ active,
+                                   int *__restrict__ done, int *__restrict__ overflow,
                                    uint32_t *__restrict__ keep_rows, float *__restrict__ keep_d32,
                                    int *__restrict__ keep_cnt, int kcap) {
     __shared__ int red[32];
@@ -1410,7 +1564,9 @@ __global__ void wave_update_kernel(const int *__restrict__ act, const float *__r
         pos[q] = end;
         const bool fin = end >= total || lb_bin(slbp[roff[q] + end]) > lb_bin(T);
         done[q] = fin;
-        if (!fin) atomicOr(active, 1);
+        // list exhausted while thr still reaches past the cutoff: members in
+        // the dropped bins may still beat thr -> overflow round
+        if (end >= total && lb_bin(T) > (unsigned)binhi[q]) overflow[q] = 1;
     }
 }
 
@@ -1527,24 +1683,35 @@ __global__ void finalize_counters(const int *__restrict__ computed,
     if (q >= nq) return;
     counters[q * 5 + 3] = computed[q];
     counters[q * 5 + 4] = (long long)abandoned[q];
+    // every member not pruned by LB_Kim / LB_Keogh2 nor DTW-evaluated was
+    // pruned by a query-envelope bound (LB_PAA key, cutoff, LB_Keogh)
+    counters[q * 5 + 1] = n_cand[q] - counters[q * 5 + 0] - counters[q * 5 + 2] - computed[q];
     status[q] = n_cand[q] == 0 ? 1 : (is_fb[q] ? 2 : 0);
 }
 
-__global__ void wave_init_kernel(int nq, int k, const int *__restrict__ cnt, float *__restrict__ thr,
+__global__ void wave_init_kernel(int nq, int k, int round, const int *__restrict__ cnt,
+                                 int *__restrict__ overflow, float *__restrict__ thr,
                                  float *__restrict__ topk, int *__restrict__ pos, int *__restrict__ done,
                                  int *__restrict__ wcnt, int *__restrict__ keep_cnt,
                                  int *__restrict__ computed, unsigned long long *__restrict__ aband) {
     const int64_t n = (int64_t)nq * k;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-        reinterpret_cast<uint32_t *>(topk)[e] = 0xFFFFFFFFu;  // NaN bits: above every finite value
+    if (round == 0)
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+            reinterpret_cast<uint32_t *>(topk)[e] = 0xFFFFFFFFu;  // NaN bits: above every finite value
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
-        thr[q] = INFINITY;
         pos[q] = 0;
-        done[q] = cnt[q] == 0;
         wcnt[q] = 0;
-        keep_cnt[q] = 0;
-        computed[q] = 0;
-        aband[q] = 0ULL;
+        if (round == 0) {
+            thr[q] = INFINITY;
+            done[q] = cnt[q] == 0;
+            keep_cnt[q] = 0;
+            computed[q] = 0;
+            aband[q] = 0ULL;
+        } else {
+            // overflow round: only the flagged queries continue, with their state
+            done[q] = !overflow[q] || cnt[q] == 0;
+        }
+        overflow[q] = 0;
     }
 }
 
@@ -1582,12 +1749,14 @@ struct Carver {
 };
 
 #define SSH_MEMBER_BUDGET ((int64_t)1 << 29)  // members per sub-range (8 GiB of lists)
+#define SSH_MEMBER_TARGET 65536               // round-0 members per query (sampled cutoff)
 
 struct QueryBufs {
     uint64_t *qsig, *qbits, *bstart;
     uint32_t *blen;
     int64_t *roff;
     int *isfb, *mcnt, *pos, *done, *active, *wcnt, *keep_cnt, *rcnt, *computed, *act, *nact;
+    int *binlo, *binhi, *overflow;
     float *U, *Lo, *Useg, *Lseg, *thr;
     unsigned long long *aband;
 
@@ -1604,6 +1773,9 @@ struct QueryBufs {
         active = c.take<int>(1);
         nact = c.take<int>(1);
         act = c.take<int>(nc);
+        binlo = c.take<int>(nc);
+        binhi = c.take<int>(nc);
+        overflow = c.take<int>(nc);
         wcnt = c.take<int>(nc);
         keep_cnt = c.take<int>(nc);
         rcnt = c.take<int>(nc);
@@ -1629,6 +1801,9 @@ struct QueryBufs {
         o.pos += qa;
         o.done += qa;
         o.act += qa;
+        o.binlo += qa;
+        o.binhi += qa;
+        o.overflow += qa;
         o.wcnt += qa;
         o.keep_cnt += qa;
         o.rcnt += qa;
@@ -1915,8 +2090,10 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     qc64 = std::min<int64_t>(qc64, ((int64_t)1 << 28) / std::max<int64_t>(1, NW));
     const int qc = (int)std::max<int64_t>(1, qc64);
     SSH_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 5 * (size_t)nq, st));
-    SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(MB_WARPS * 1024 * 4)));
+    SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(MB_WARPS * 1024 * 8)));
+    SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(MB_WARPS * 1024 * 8 + NBINS * 4)));
     for (int q0 = 0; q0 < nq; q0 += qc) {
         const int nc = std::min(qc, nq - q0);
         const float *Qc = Q + (int64_t)q0 * m;
@@ -1951,6 +2128,9 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         // (SSH_DEBUG_MEMBER_BUDGET overrides it, for tests of the split path)
         int64_t budget = SSH_MEMBER_BUDGET;
         if (const char *ev = getenv("SSH_DEBUG_MEMBER_BUDGET")) budget = std::max<int64_t>(1, atoll(ev));
+        // (SSH_DEBUG_MEMBER_TARGET lowers the round-0 cutoff, for tests of the overflow round)
+        int member_target = SSH_MEMBER_TARGET;
+        if (const char *ev = getenv("SSH_DEBUG_MEMBER_TARGET")) member_target = std::max(8, atoi(ev));
         for (int sa = 0; sa < nc;) {
             int sb = sa;
             int64_t total = 0;
@@ -1968,25 +2148,30 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                 for (int q = 0; q < ns; q++) hoff[q + 1] = hoff[q] + hc[sa + q];
                 SSH_CUDA(cudaMemcpyAsync(S.roff, hoff.data(), sizeof(int64_t) * (ns + 1), cudaMemcpyHostToDevice, st));
             }
-            // LB_PAA of every member, then per-query counting sort by LB_PAA bin
+            // K7 lists: members with their summary key, sorted by key bin.  Round 0
+            // keeps the bins up to a per-query cutoff chosen from a 1/8 sample of
+            // the keys (about SSH_MEMBER_TARGET members); a query whose list runs
+            // out while its threshold is still above the cutoff takes an overflow
+            // round over the remaining bins, continuing the same top-k state.
             pf.begin();
             uint32_t *rows_u = (uint32_t *)ssh_slot(ctx, SLOT_Q_SURV, sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1), st);
             float *lb_u = (float *)ssh_slot(ctx, SLOT_Q_SURV_LB, sizeof(float) * (size_t)std::max<int64_t>(total, 1), st);
             uint32_t *rows_s = (uint32_t *)ssh_slot(ctx, SLOT_Q_W2, sizeof(uint32_t) * (size_t)std::max<int64_t>(total, 1), st);
             float *lb_s = (float *)ssh_slot(ctx, SLOT_Q_D2, sizeof(float) * (size_t)std::max<int64_t>(total, 1), st);
-            if (!rows_u || !lb_u || !rows_s || !lb_s) return SSH_ERR_OOM;
-            SSH_CUDA(cudaMemsetAsync(S.mcnt, 0, sizeof(int) * ns, st));
+            unsigned *khist = (unsigned *)ssh_slot(ctx, SLOT_Q_KHIST, sizeof(unsigned) * (size_t)ns * NBINS, st);
+            if (!rows_u || !lb_u || !rows_s || !lb_s || !khist) return SSH_ERR_OOM;
+            const dim3 gm((unsigned)ssh_div_up(NW, MB_SLICE_WORDS), (unsigned)ns);
+            PaaArgs pa{S.Useg, S.Lseg, Qs, (const uint4 *)ix->rec, bms, S.roff, rows_u, lb_u, S.mcnt,
+                       S.binlo, S.binhi, khist, NW, m, ix->seg, nseg};
             {
-                PaaArgs pa{S.Useg, S.Lseg, Qs, (const uint4 *)ix->rec, bms, S.roff, rows_u, lb_u, S.mcnt, NW,
-                           m, ix->seg, nseg};
-                dim3 g((unsigned)ssh_div_up(NW, MB_SLICE_WORDS), (unsigned)ns);
-                paa_members_kernel<<<g, MB_THREADS, MB_WARPS * 1024 * 4, st>>>(pa);
+                SSH_CUDA(cudaMemsetAsync(khist, 0, sizeof(unsigned) * (size_t)ns * NBINS, st));
+                const dim3 gs((unsigned)ssh_div_up(NW, (int64_t)MB_SLICE_WORDS << SAMPLE_SHIFT), (unsigned)ns);
+                paa_members_kernel<true><<<gs, MB_THREADS, MB_WARPS * 1024 * 8 + NBINS * 4, st>>>(pa);
+                SSH_CHECK_LAUNCH();
+                cutoff_kernel<<<ns, 256, 0, st>>>(khist, member_target, S.binlo, S.binhi);
                 SSH_CHECK_LAUNCH();
             }
-            binsort_kernel<<<ns, 1024, 0, st>>>(rows_u, lb_u, S.roff, S.mcnt, rows_s, lb_s);
-            SSH_CHECK_LAUNCH();
             pf.end(2);
-            // K7/K8: waves in LB_PAA order: LB_Kim/LB_Keogh -> fp32 DTW -> threshold
             uint32_t *wrows = (uint32_t *)ssh_slot(ctx, SLOT_Q_RESC, sizeof(uint32_t) * (size_t)ns * WCAP, st);
             float *wd32 = (float *)ssh_slot(ctx, SLOT_Q_D32, sizeof(float) * (size_t)ns * WCAP, st);
             float2 *wlb = (float2 *)ssh_slot(ctx, SLOT_Q_WLB, sizeof(float2) * (size_t)ns * WCAP, st);
@@ -1996,65 +2181,89 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             uint32_t *resc = (uint32_t *)ssh_slot(ctx, SLOT_Q_HIST, sizeof(uint32_t) * (size_t)ns * KCAP, st);
             double *d64 = (double *)ssh_slot(ctx, SLOT_Q_D64, sizeof(double) * (size_t)ns * KCAP, st);
             if (!wrows || !wd32 || !wlb || !topk || !keep_rows || !keep_d32 || !resc || !d64) return SSH_ERR_OOM;
-            wave_init_kernel<<<ssh_div_up(std::max<int64_t>((int64_t)ns * k, ns), 256), 256, 0, st>>>(
-                ns, k, S.mcnt, S.thr, topk, S.pos, S.done, S.wcnt, S.keep_cnt, S.computed, S.aband);
-            SSH_CHECK_LAUNCH();
             std::vector<float> thr0h;
-            // waves over the active queries only: block row y = slot y = query act[y];
-            // the per-wave lists share one pool, so the per-slot capacity grows as
-            // queries finish
             const int64_t pool = (int64_t)ns * WCAP;
-            compact_active_kernel<<<1, 1024, 0, st>>>(S.done, ns, S.act, S.nact);
-            SSH_CHECK_LAUNCH();
-            int nact = 0;
-            SSH_CUDA(cudaMemcpyAsync(&nact, S.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
-            SSH_CUDA(cudaStreamSynchronize(st));
-            WaveLbArgs wl{Qs, S.U, S.Lo, (const uint4 *)ix->rec, ix->codes, ix->cstride, rows_s, lb_s, S.roff,
-                          S.mcnt, S.pos, S.done, S.thr, S.act, wrows, wlb, S.wcnt, c5s,
-                          ctx->profile ? ctx->d_cells : nullptr, m, ix->mp, W0, WCAP};
             const int wl_warps = 8;
             const size_t wl_smem = (size_t)3 * ix->mp * sizeof(float);
             SSH_CUDA(cudaFuncSetAttribute(wave_lb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wl_smem));
-            for (int wave = W0, it = 0; nact > 0; wave *= 2, it++) {
-                const int wcap = (int)std::min<int64_t>((int64_t)1 << 20, (pool / nact) & ~(int64_t)255);
-                wave = std::min(wave, wcap);
+            for (int round = 0; round < 2; round++) {
                 pf.begin();
-                {
-                    dim3 g((unsigned)std::min(ssh_div_up(wave, 32 * wl_warps), 512), (unsigned)nact);
-                    wl.wave = wave;
-                    wl.wcap = wcap;
-                    wave_lb_kernel<<<g, 32 * wl_warps, wl_smem, st>>>(wl);
+                if (round == 1) {
+                    overflow_window_kernel<<<ssh_div_up(ns, 256), 256, 0, st>>>(S.overflow, ns, S.binlo, S.binhi);
                     SSH_CHECK_LAUNCH();
                 }
-                pf.end(3);
-                const float lb_ms = pf.last;
-                pf.begin();
-                {
-                    DtwList dl{wrows, wcap, S.wcnt, nullptr, wave, nullptr, wd32, S.aband, S.computed, S.act};
-                    DtwWave dw{wrows, wlb, wcap, S.wcnt, wd32, S.aband, S.computed, (const uint4 *)ix->rec,
-                               ix->codes, ix->cstride, ix->mp, S.act};
-                    rc = launch_dtw32_wave(ctx, X, Qs, S.U, S.Lo, dw, dl, S.thr, nact, wave, st);
-                    if (rc) return rc;
-                }
-                pf.end(4);
-                if (ctx->profile && getenv("SSH_DEBUG_WAVES"))
-                    fprintf(stderr, "wave %d: active %d wave %d cap %d | LB %.3f ms DTW %.3f ms\n", it, nact, wave,
-                            wcap, lb_ms, pf.last);
-                wave_update_kernel<<<nact, 256, 0, st>>>(S.act, wd32, wrows, S.wcnt, wcap, lb_s, S.roff, S.mcnt, wave,
-                                                         k, eps, topk, S.thr, S.pos, S.done, S.active, keep_rows,
-                                                         keep_d32, S.keep_cnt, KCAP);
+                SSH_CUDA(cudaMemsetAsync(S.mcnt, 0, sizeof(int) * ns, st));
+                paa_members_kernel<false><<<gm, MB_THREADS, MB_WARPS * 1024 * 8, st>>>(pa);
                 SSH_CHECK_LAUNCH();
+                binsort_kernel<<<ns, 1024, 0, st>>>(rows_u, lb_u, S.roff, S.mcnt, rows_s, lb_s);
+                SSH_CHECK_LAUNCH();
+                pf.end(2);
+                // K7/K8: waves in key order: LB_Keogh2/LB_Keogh -> fp32 DTW -> threshold
+                wave_init_kernel<<<ssh_div_up(std::max<int64_t>((int64_t)ns * k, ns), 256), 256, 0, st>>>(
+                    ns, k, round, S.mcnt, S.overflow, S.thr, topk, S.pos, S.done, S.wcnt, S.keep_cnt, S.computed,
+                    S.aband);
+                SSH_CHECK_LAUNCH();
+                // waves over the active queries only: block row y = slot y = query
+                // act[y]; the per-wave lists share one pool, so the per-slot
+                // capacity grows as queries finish
                 compact_active_kernel<<<1, 1024, 0, st>>>(S.done, ns, S.act, S.nact);
                 SSH_CHECK_LAUNCH();
-                if (ctx->profile && it == 0) {
-                    thr0h.resize(ns);
-                    cudaMemcpyAsync(thr0h.data(), S.thr, sizeof(float) * ns, cudaMemcpyDeviceToHost, st);
-                }
+                int nact = 0;
                 SSH_CUDA(cudaMemcpyAsync(&nact, S.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
                 SSH_CUDA(cudaStreamSynchronize(st));
-                if (ctx->profile) {
-                    ctx->prof[16] += 1;
-                    ctx->prof[17] += nact;
+                if (nact == 0) break;
+                WaveLbArgs wl{Qs, S.U, S.Lo, (const uint4 *)ix->rec, ix->codes, ix->cstride, rows_s, lb_s, S.roff,
+                              S.mcnt, S.pos, S.done, S.thr, S.act, wrows, wlb, S.wcnt, c5s,
+                              ctx->profile ? ctx->d_cells : nullptr, m, ix->mp, W0, WCAP};
+                for (int wave = W0, it = 0; nact > 0; wave *= 2, it++) {
+                    const int wcap = (int)std::min<int64_t>((int64_t)1 << 20, (pool / nact) & ~(int64_t)255);
+                    wave = std::min(wave, wcap);
+                    pf.begin();
+                    {
+                        dim3 g((unsigned)std::min(ssh_div_up(wave, 32 * wl_warps), 512), (unsigned)nact);
+                        wl.wave = wave;
+                        wl.wcap = wcap;
+                        wave_lb_kernel<<<g, 32 * wl_warps, wl_smem, st>>>(wl);
+                        SSH_CHECK_LAUNCH();
+                    }
+                    pf.end(3);
+                    const float lb_ms = pf.last;
+                    pf.begin();
+                    {
+                        DtwList dl{wrows, wcap, S.wcnt, nullptr, wave, nullptr, wd32, S.aband, S.computed, S.act};
+                        DtwWave dw{wrows, wlb, wcap, S.wcnt, wd32, S.aband, S.computed, (const uint4 *)ix->rec,
+                                   ix->codes, ix->cstride, ix->mp, S.act};
+                        rc = launch_dtw32_wave(ctx, X, Qs, S.U, S.Lo, dw, dl, S.thr, nact, wave, st);
+                        if (rc) return rc;
+                    }
+                    pf.end(4);
+                    if (ctx->profile && getenv("SSH_DEBUG_WAVES"))
+                        fprintf(stderr, "round %d wave %d: active %d wave %d cap %d | LB %.3f ms DTW %.3f ms\n", round,
+                                it, nact, wave, wcap, lb_ms, pf.last);
+                    wave_update_kernel<<<nact, 256, 0, st>>>(S.act, wd32, wrows, S.wcnt, wcap, lb_s, S.roff, S.mcnt,
+                                                             S.binhi, wave, k, eps, topk, S.thr, S.pos, S.done,
+                                                             S.overflow, keep_rows, keep_d32, S.keep_cnt, KCAP);
+                    SSH_CHECK_LAUNCH();
+                    compact_active_kernel<<<1, 1024, 0, st>>>(S.done, ns, S.act, S.nact);
+                    SSH_CHECK_LAUNCH();
+                    if (ctx->profile && it == 0 && round == 0) {
+                        thr0h.resize(ns);
+                        cudaMemcpyAsync(thr0h.data(), S.thr, sizeof(float) * ns, cudaMemcpyDeviceToHost, st);
+                    }
+                    SSH_CUDA(cudaMemcpyAsync(&nact, S.nact, sizeof(int), cudaMemcpyDeviceToHost, st));
+                    SSH_CUDA(cudaStreamSynchronize(st));
+                    if (ctx->profile) {
+                        ctx->prof[16] += 1;
+                        ctx->prof[17] += nact;
+                    }
+                }
+                if (round == 0) {
+                    int nover = 0;
+                    rc = max_of(S.overflow, ns, st, &nover);
+                    if (rc) return rc;
+                    if (ctx->profile) ctx->prof[18] += 1;
+                    if (!nover) break;
+                    if (ctx->profile) ctx->prof[19] += 1;
                 }
             }
             int maxkeep = 0;

@@ -483,3 +483,57 @@ extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t 
     (*out)->cstride = summ.cstride;
     return SSH_OK;
 }
+
+// build_index from HOST series (index.py:159-172 with the H2D copy inside):
+// rows are copied in chunks on the copy stream into X_dev (the caller's device
+// buffer, N x ld f32, which the index then uses for DTW) while the previous
+// chunk is sketched, signed and summarised on `stream`; bucket tables last.
+extern "C" int ssh_build_index_host(ssh_ctx *ctx, const float *X_host, int64_t N, int64_t ld, int64_t id_base,
+                                    float *X_dev, uint64_t *sig_out, ssh_index **out, void *stream) {
+    SSH_REQUIRE(ctx && X_host && X_dev && sig_out && out, SSH_ERR_INVALID, "ssh_build_index_host: NULL argument");
+    SSH_REQUIRE(ctx->have_params, SSH_ERR_STATE, "ssh_build_index_host: ssh_ctx_set_params not called");
+    SSH_REQUIRE(N >= 1 && ld >= ctx->p.m, SSH_ERR_INVALID, "ssh_build_index_host: bad shape N=%lld ld=%lld",
+                (long long)N, (long long)ld);
+    SSH_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t CH = 65536;
+    uint64_t *bits = (uint64_t *)ssh_slot(ctx, SLOT_BITS, sizeof(uint64_t) * (size_t)std::min(N, CH) * ctx->words, st);
+    if (!bits) return SSH_ERR_OOM;
+    ssh_index summ;
+    summ.N = N;
+    int rc = ssh_alloc_summaries(ctx, &summ, N, st);
+    if (rc) return rc;
+    // the copy stream may only write X_dev after the caller's prior work on it
+    SSH_CUDA(cudaEventRecord(ctx->ev_fork, st));
+    SSH_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->ev_fork, 0));
+    for (int64_t r0 = 0; r0 < N && rc == SSH_OK; r0 += CH) {
+        const int64_t n = std::min(CH, N - r0);
+        cudaError_t e = cudaMemcpyAsync(X_dev + r0 * ld, X_host + r0 * ld, sizeof(float) * (size_t)(n * ld),
+                                        cudaMemcpyHostToDevice, ctx->copy);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_copy, ctx->copy);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ctx->ev_copy, 0);
+        if (e != cudaSuccess) {
+            rc = ssh_cuda_fail(e, "ssh_build_index_host copy", __FILE__, __LINE__);
+            break;
+        }
+        const float *Xc = X_dev + r0 * ld;
+        rc = ssh_launch_sketch(ctx, Xc, n, ld, bits, nullptr, st);
+        if (rc == SSH_OK)
+            rc = ssh_launch_shingle_cws(ctx, bits, nullptr, nullptr, nullptr, n, nullptr, nullptr, nullptr,
+                                        nullptr, sig_out + r0 * ctx->p.L, SIG_MODE_FUSED, st);
+        if (rc == SSH_OK) rc = ssh_launch_summaries_rows(ctx, &summ, Xc, r0, n, ld, st);
+    }
+    if (rc == SSH_OK) rc = ssh_index_build(ctx, sig_out, N, id_base, out, stream);
+    if (rc != SSH_OK) {
+        if (summ.rec) cudaFreeAsync(summ.rec, st);
+        if (summ.codes) cudaFreeAsync(summ.codes, st);
+        return rc;
+    }
+    (*out)->rec = summ.rec;
+    (*out)->codes = summ.codes;
+    (*out)->seg = summ.seg;
+    (*out)->nseg = summ.nseg;
+    (*out)->mp = summ.mp;
+    (*out)->cstride = summ.cstride;
+    return SSH_OK;
+}

@@ -237,6 +237,18 @@ def _stream_ptr(device: int):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+def _host_f32(values):
+    """Contiguous f32 CPU tensor view of host series (None for device tensors)."""
+    torch = _torch()
+    if _is_torch(values):
+        if values.is_cuda:
+            return None
+        t = values.to(dtype=torch.float32)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32))
+    return t.contiguous()
+
+
 def _as_device_f32(values, device: int):
     torch = _torch()
     if _is_torch(values):
@@ -343,13 +355,23 @@ def build_index(dataset, params: SshParams, normalized: bool = True, threads: in
     params.validate_for_length(dataset.length)
     dev = _device_index(device)
     ctx = get_context(dev, params, dataset.length)
-    X = _as_device_f32(dataset.values, dev)
     torch = _torch()
-    sig = torch.empty((int(X.shape[0]), params.d), dtype=torch.int64, device=X.device)
+    host = _host_f32(dataset.values)
     handle = ctypes.c_void_p()
-    nat.check(nat.lib().ssh_build_index(ctx.handle, nat.ptr(X), int(X.shape[0]), int(X.stride(0)),
-                                        int(id_base), nat.ptr(sig), ctypes.byref(handle),
-                                        _stream_ptr(dev)), "ssh_build_index")
+    if host is not None:
+        # host series: chunked copy into X overlapped with the per-chunk kernels
+        N, m = host.shape
+        X = torch.empty((N, m), dtype=torch.float32, device=f"cuda:{dev}")
+        sig = torch.empty((N, params.d), dtype=torch.int64, device=X.device)
+        nat.check(nat.lib().ssh_build_index_host(ctx.handle, host.data_ptr(), N, m, int(id_base), nat.ptr(X),
+                                                 nat.ptr(sig), ctypes.byref(handle), _stream_ptr(dev)),
+                  "ssh_build_index_host")
+    else:
+        X = _as_device_f32(dataset.values, dev)
+        sig = torch.empty((int(X.shape[0]), params.d), dtype=torch.int64, device=X.device)
+        nat.check(nat.lib().ssh_build_index(ctx.handle, nat.ptr(X), int(X.shape[0]), int(X.stride(0)),
+                                            int(id_base), nat.ptr(sig), ctypes.byref(handle),
+                                            _stream_ptr(dev)), "ssh_build_index")
     tables = _TablesHandle(handle)
     return SshIndex(params=params, filter=ctx.filter, dataset=dataset, normalized=normalized,
                     device=dev, X=X, sig_dev=sig, id_base=id_base, _tables=tables)

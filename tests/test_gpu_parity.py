@@ -416,3 +416,21 @@ def test_query_member_budget_split(cuda, golden, monkeypatch):
         assert r.stats.candidates == g["candidates"], qi
         assert r.ids == g["ids"], qi
         assert r.distances == g["distances"], qi
+
+
+@pytest.mark.parametrize("target", ["8", "64"])
+def test_query_overflow_round(cuda, golden, monkeypatch, target):
+    """A tiny round-0 member target cuts every query's list far below its
+    threshold, so the overflow round must supply the rest; results stay
+    identical to the reference."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw1024")
+    c = golden["cases"]["rw1024"]
+    idx = ssh.build_index(ssh.Dataset(X), params(band, K=4))
+    monkeypatch.setenv("SSH_DEBUG_MEMBER_TARGET", target)
+    res = ssh.query_index_batch(idx, Q, 10)
+    for qi, (r, g) in enumerate(zip(res, c["queries_k4"])):
+        assert r.stats.candidates == g["candidates"], qi
+        assert r.ids == g["ids"], qi
+        assert r.distances == g["distances"], qi
