@@ -434,3 +434,54 @@ def test_query_overflow_round(cuda, golden, monkeypatch, target):
         assert r.stats.candidates == g["candidates"], qi
         assert r.ids == g["ids"], qi
         assert r.distances == g["distances"], qi
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_config_shapes_sampled(cuda, cfg):
+    """configs[2] (ECG windows, m=1024, band 5%) and configs[3] (random walks,
+    m=2048, band 10%: radius 205, the generic shared-memory DTW kernel) at their
+    series length and band on a 300k-series shard: 8 warped queries, top-10
+    ids and distances identical to the oracle cascade over the same signatures."""
+    import paper_1610_07328_b200 as ssh
+    from paper_1610_07328_b200 import datagen
+
+    X, Q, src, p = datagen.workload(cfg, device="cuda", nq=8, n_override=300_000)
+    params_ = ssh.SshParams(**p)
+    idx = ssh.build_index(ssh.Dataset(X), params_)
+    res = ssh.query_index_batch(idx, Q, 10)
+    Xh = X.cpu().numpy()
+    sig = idx.signatures
+    rows = np.random.default_rng(1).choice(Xh.shape[0], 2000, replace=False)
+    assert np.array_equal(sig[rows], O.signatures(Xh[rows], 80, 3, 15, 20, 4, 0, threads=16))
+    ocsr = O.tables_from_signatures(sig)
+    oidx = O.OracleIndex(Xh, 80, 3, 15, 20, 4, 0, p["band"], O.make_filter(80, 0), sig, ocsr)
+    ores = O.query_batch(oidx, Q, 10, threads=16)
+    for i, r in enumerate(res):
+        n = int(ores["n"][i])
+        assert r.stats.candidates == int(ores["n_cand"][i])
+        assert r.ids == ores["ids"][i][:n].tolist(), i
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
+
+
+@pytest.mark.slow
+def test_config3_full_size_properties(cuda):
+    """configs[3] at full size (N=4,000,000, m=2048): self-queries return their
+    own row first at distance 0, distances ascend, and every reported distance
+    equals the exact f64 DTW of that pair (ssh_dtw_exact)."""
+    import torch
+
+    import paper_1610_07328_b200 as ssh
+    from paper_1610_07328_b200 import datagen
+    from paper_1610_07328_b200.index import dtw_exact_pairs
+
+    X, _, _, p = datagen.workload(3, device="cuda", nq=0)
+    idx = ssh.build_index(ssh.Dataset(X), ssh.SshParams(**p))
+    rows = np.random.default_rng(5).choice(X.shape[0], 12, replace=False)
+    Q = X[torch.from_numpy(rows).cuda()].cpu().numpy()
+    res = ssh.query_index_batch(idx, Q, 10)
+    for i, r in enumerate(res):
+        assert r.ids[0] == int(rows[i]) and r.distances[0] == 0.0
+        assert r.distances == sorted(r.distances)
+        d2 = dtw_exact_pairs(idx, Q, np.full(len(r.ids), i), np.asarray(r.ids))
+        assert np.sqrt(d2).tolist() == r.distances
