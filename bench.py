@@ -348,6 +348,7 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     res["wave_lb_paa_skips"] = prof[10]
     res["wave_lb_keogh_prunes"] = prof[11]
     res["wave_members_visited"] = prof[12]
+    res["dtw_cells_executed"] = prof[20]
     res["waves"] = prof[16]
     res["active_query_waves"] = prof[17]
     if prof[15] > 0:

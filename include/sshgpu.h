@@ -82,7 +82,8 @@ int ssh_ctx_set_params(ssh_ctx *ctx, const ssh_params *p, const double *filter,
  * wave LB, [8] fp32 DTWs started, [9] rescored pairs, [10] key prunes
  * (LB_PAA / LB_Kim), [11] LB_Keogh prunes, [12] members visited,
  * [13]/[14]/[15] sum of first-wave / final thr over the exact k-th distance
- * and their count, [16] waves, [17] sum over waves of active queries. */
+ * and their count, [16] waves, [17] sum over waves of active queries,
+ * [18] query sub-ranges, [19] overflow rounds, [20] DTW lane-cells executed. */
 int ssh_ctx_set_profiling(ssh_ctx *ctx, int on);
 int ssh_ctx_profile(const ssh_ctx *ctx, double *out, int n);
 

@@ -19,7 +19,7 @@ from .core import ConfigError, SshError
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
-LIB_PATH = PKG / "libsshgpu.so"
+LIB_PATH = Path(os.environ["SSH_LIB_PATH"]).resolve() if os.environ.get("SSH_LIB_PATH") else PKG / "libsshgpu.so"
 SOURCES = ["ctx.cu", "sketch.cu", "signature.cu", "tables.cu", "query.cu"]
 
 NVCC_FLAGS = [

@@ -93,6 +93,10 @@ enum {
     SLOT_Q_KEEP_D,
     SLOT_Q_WLB,
     SLOT_Q_KHIST,
+    SLOT_Q_POOLA,
+    SLOT_Q_POOLB,
+    SLOT_Q_POOLCNT,
+    SLOT_Q_QPAD,
     SLOT_COUNT
 };
 

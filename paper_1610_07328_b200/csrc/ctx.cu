@@ -36,7 +36,8 @@ extern "C" int ssh_ctx_profile(const ssh_ctx *ctx, double *out, int n) {
             out[11] = (double)c[2];
             out[12] = (double)c[3];
         }
-        if (n > 7) out[7] = (double)(c[4] + c[5]);  // bytes of rows/envelopes read by the wave LB
+        if (n > 7) out[7] = (double)c[4];  // bytes of codes read by the wave LB
+        if (n > 20) out[20] = (double)c[5];  // DTW lane-cells executed (incl. idle lanes)
     }
     return SSH_OK;
 }

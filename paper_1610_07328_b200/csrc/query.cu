@@ -257,12 +257,25 @@ __device__ __forceinline__ float sdec(int c, float sc, float lo) { return fmaf((
 
 // c in [0, 254] with dec(c) <= v <= dec(c + 1)
 __device__ __forceinline__ int code_in(float v, float lo, float sc, float inv) {
-    int c = __float2int_rd((v - lo) * inv);
-    c = min(max(c, 0), 254);
+    // estimate, then verify both ends with the decoder's own arithmetic
+    const float cf = fminf(fmaxf(floorf((v - lo) * inv), 0.f), 254.f);
+    if (fmaf(cf, sc, lo) <= v && fmaf(cf + 1.f, sc, lo) >= v) return (int)cf;
+    int c = (int)cf;
     for (int it = 0; it < 256 && c > 0 && sdec(c, sc, lo) > v; it++) c--;
     for (int it = 0; it < 256 && c < 254 && sdec(c + 1, sc, lo) < v; it++) c++;
     return c;
 }
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 struct SumArgs {
     const float *X;
     int64_t N, ld, cstride;
@@ -276,21 +289,38 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     const int m = a.m, pad = a.pad, padw = pad >> 2;
     unsigned char *base = xsmb + (size_t)w * a.warp_bytes;
-    float *xs = reinterpret_cast<float *>(base);                      // m samples
-    uint32_t *cmx = reinterpret_cast<uint32_t *>(xs + ((m + 3) & ~3));  // pad bytes: codes, 0 outside
+    const int mq = (m + 3) & ~3;
+    float *xbuf = reinterpret_cast<float *>(base);                    // 2 x mq samples (double buffer)
+    uint32_t *cmx = reinterpret_cast<uint32_t *>(xbuf + 2 * mq);     // pad bytes: codes, 0 outside
     uint32_t *cmn = cmx + padw;                                       // pad bytes: 255 - codes, 0 outside
     uint8_t *prec = reinterpret_cast<uint8_t *>(cmn + padw);          // 64-byte record staging
     uint8_t *bmx = reinterpret_cast<uint8_t *>(cmx), *bmn = reinterpret_cast<uint8_t *>(cmn);
     const int win = 2 * a.r + 1;
     const int shw = win - (1 << a.lev);
     const int64_t nwarps = (int64_t)gridDim.x * nwb;
-    for (int64_t row = (int64_t)blockIdx.x * nwb + w; row < a.N; row += nwarps) {
-        const float *x = a.X + row * a.ld;
+    const bool v16 = ((m & 3) == 0) && ((a.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
+    // rows stream into the warp's double buffer with cp.async, one row ahead
+    auto prefetch = [&](int64_t rw, float *dst) {
+        if (rw < a.N) {
+            const float *src = a.X + rw * a.ld;
+            if (v16)
+                for (int i = 4 * lane; i < m; i += 128) cp_async16(dst + i, src + i);
+            else
+                for (int i = lane; i < m; i += 32) cp_async4(dst + i, src + i);
+        }
+        cp_async_commit();
+    };
+    int64_t row = (int64_t)blockIdx.x * nwb + w;
+    prefetch(row, xbuf);
+    for (int buf = 0; row < a.N; row += nwarps, buf ^= 1) {
+        float *xs = xbuf + buf * mq;
+        prefetch(row + nwarps, xbuf + (buf ^ 1) * mq);
+        cp_async_wait1();
+        __syncwarp();
         float vmin = INFINITY, vmax = -INFINITY;
         bool fin = true;
         for (int i = lane; i < m; i += 32) {
-            const float v = __ldg(x + i);
-            xs[i] = v;
+            const float v = xs[i];
             fin = fin && isfinite(v);
             vmin = fminf(vmin, v);
             vmax = fmaxf(vmax, v);
@@ -419,7 +449,7 @@ static int summaries_geom(const ssh_ctx *ctx, SumGeom &g) {
     // padded code arrays: sample j at byte j + r; the last doubling read
     // reaches byte (m - 1) + 2r + 2^lev + 3; 2 pad % 16 == 0 keeps the record aligned
     g.pad = ((m + 2 * r + (1 << g.lev) + 12) + 7) & ~7;
-    g.warp_bytes = (((m + 3) & ~3) * 4 + 2 * g.pad + 64 + 15) & ~15;
+    g.warp_bytes = (((m + 3) & ~3) * 8 + 2 * g.pad + 64 + 15) & ~15;
     g.nwb = (int)std::min<size_t>(8, (200 * 1024) / (size_t)g.warp_bytes);
     SSH_REQUIRE(g.nwb >= 1, SSH_ERR_UNSUPPORTED, "series too long for the summaries kernel (m=%d, r=%d)", m, r);
     return SSH_OK;
@@ -1190,14 +1220,15 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
     }
 }
 
-// Register-band fp32 DTW of one wave's candidate list with in-block
-// compaction.  A block owns up to DW_ITEMS candidates of one query and runs
-// them through row passes [0,32), [32,64), [64,128), ... ; after each pass
-// the survivors' state (band registers, remaining bounds) is compacted in
-// shared memory and redistributed over the leading warps, so lanes whose
-// candidate was abandoned early do not idle until the slowest lane of their
-// warp finishes.  Rows stay warp-uniform (query reads are LDS.128
-// broadcasts from 4 shifted copies, as in dtw32r_kernel).
+// Register-band fp32 DTW of one wave's candidate list with per-warp
+// compaction.  Each warp owns DW_IPW candidates of one query and runs them
+// through row passes [0,8), [8,16), [16,32), ... in batches of 32; after
+// a pass the survivors' state (band registers, remaining bounds) is parked
+// in the warp's shared-memory slots and their indices form the next pass's
+// list, so lanes whose candidate was abandoned early do not idle until the
+// slowest lane finishes, and warps never wait for each other (one block
+// barrier, after staging the query).  Rows stay warp-uniform (query reads
+// are shared-memory broadcasts).
 // Abandon test after row i (UCR-suite cumulative bounds, dtw.py:206-215):
 //   rmin_i + max(remK_i - slackK, rem2_i - slack2, 0) > thr
 //   remK_i = LBK total - sum_{i' <= i} LB_Keogh term of row i'     (rows left)
@@ -1206,6 +1237,7 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
 // with the totals from the wave LB kernel (code-based terms; the exact-x row
 // terms subtracted here are never smaller, so remK stays a lower bound) and
 // slack = total * (2m + 8) u for the fp32 running sums.
+#define DW_IPW 64  // candidates per warp in the wave DTW kernel
 
 struct DtwWave {
     const uint32_t *rows;
@@ -1228,26 +1260,24 @@ dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
               const float *__restrict__ Lo, DtwWave L, const float *__restrict__ thr,
               unsigned long long *__restrict__ cells) {
     constexpr int NB = 2 * R + 1;
-    constexpr int DW_ITEMS = 32 * DW_WARPS;
+    constexpr int IPW = DW_IPW;  // candidates per warp
     extern __shared__ __align__(16) float wsm2[];
-    __shared__ int n_live, n_next;
     const int slot = blockIdx.y;
     const int q = L.act[slot];
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int total = min(L.cnt[slot], (int)L.stride);
-    const int base = blockIdx.x * DW_ITEMS;
+    const int base = blockIdx.x * DW_WARPS * IPW;
     if (base >= total) return;
-    const int n0 = min(total - base, DW_ITEMS);
     const int YP = ((m + 2 * R + 8) + 3) & ~3;
     float *yc = wsm2;           // YP: y[j] at yc[j + R], +inf outside [0, m)
     float *su = yc + YP;        // m
     float *sl = su + m;         // m
-    float *sband = sl + m;      // NB x DW_ITEMS
-    float *sremk = sband + NB * DW_ITEMS, *srem2 = sremk + DW_ITEMS;
-    float *sslk = srem2 + DW_ITEMS, *ssl2 = sslk + DW_ITEMS;
-    float *slo = ssl2 + DW_ITEMS, *ssc = slo + DW_ITEMS;
-    uint32_t *srow = reinterpret_cast<uint32_t *>(ssc + DW_ITEMS);
-    int *se = reinterpret_cast<int *>(srow + DW_ITEMS);
+    // per-warp candidate state, [k][IPW] for the band
+    float *sband = sl + m + (size_t)w * (NB + 6) * IPW;
+    float *sremk = sband + NB * IPW, *srem2 = sremk + IPW;
+    float *sslk = srem2 + IPW, *ssl2 = sslk + IPW;
+    float *slo = ssl2 + IPW, *ssc = slo + IPW;
+    int *lists = reinterpret_cast<int *>(sl + m + (size_t)DW_WARPS * (NB + 6) * IPW) + w * 2 * IPW;
     const float *y = Q + (int64_t)q * m;
     for (int t = threadIdx.x; t < YP; t += blockDim.x) {
         const int jj = t - R;
@@ -1257,67 +1287,64 @@ dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
         su[i] = U[(int64_t)q * m + i];
         sl[i] = Lo[(int64_t)q * m + i];
     }
+    __syncthreads();  // the only block-wide barrier: warps run independently from here
+    const int wbase = base + w * IPW;
+    const int n0 = min(total - wbase, IPW);
+    if (n0 <= 0) return;
     const float T = thr[q];
     const float slf = (float)(2 * m + 8) * U32_EPS;
-    if (threadIdx.x < n0) {
-        const int t = threadIdx.x, e = base + t;
-        const uint32_t row = L.rows[(int64_t)slot * L.stride + e];
-        const float2 lb = L.lbs[(int64_t)slot * L.stride + e];
-        const float2 h = __ldg(reinterpret_cast<const float2 *>(L.rec + (int64_t)row * 4));
-        L.out[(int64_t)slot * L.stride + e] = INFINITY;
-        srow[t] = row;
-        se[t] = e;
-        sremk[t] = lb.x;
-        srem2[t] = lb.y;
-        sslk[t] = lb.x * slf;
-        ssl2[t] = lb.y * slf;
-        slo[t] = h.x;
-        ssc[t] = h.y;
-#pragma unroll
-        for (int k = 0; k < NB; k++) sband[k * DW_ITEMS + t] = k == R ? 0.f : INFINITY;
-    }
-    if (threadIdx.x == 0) {
-        n_live = n0;
-        if (L.computed) atomicAdd(&L.computed[q], n0);
-    }
-    __syncthreads();
+    if (lane == 0 && L.computed) atomicAdd(&L.computed[q], n0);
+    int *cur = lists, *nxt = lists + IPW;
+    for (int i = lane; i < n0; i += 32) cur[i] = i;
+    __syncwarp();
+    int ncur = n0;
     unsigned long long my_cells = 0;
     unsigned long long my_ab = 0;
-    for (int a = 0; a < m;) {
-        const int b = min(m, a < 32 ? 32 : 2 * a);
-        const int nl = n_live;
-        if (nl == 0) break;
-        const int t = threadIdx.x;
-        const bool have = t < nl;
-        float band[NB];
-        uint32_t row = 0;
-        int e = 0;
-        float remk = 0.f, rem2 = 0.f, slk = 0.f, sl2 = 0.f, lo = 0.f, sc = 0.f;
-        if (have) {
+    unsigned long long wrows = 0;  // rows the warp executed (all lanes), profiling
+    for (int a = 0; a < m && ncur > 0;) {
+        const int b = min(m, a < 8 ? 8 : 2 * a);  // passes [0,8), [8,16), [16,32), ...
+        int nn = 0;
+        for (int b0 = 0; b0 < ncur; b0 += 32) {
+            const bool have = b0 + lane < ncur;
+            const int it = have ? cur[b0 + lane] : 0;
+            const int e = wbase + it;
+            float band[NB];
+            uint32_t row = 0;
+            float remk = 0.f, rem2 = 0.f, slk = 0.f, sl2 = 0.f, lo = 0.f, sc = 0.f;
+            if (have) {
+                row = L.rows[(int64_t)slot * L.stride + e];
+                if (a == 0) {
+                    const float2 lb = L.lbs[(int64_t)slot * L.stride + e];
+                    const float2 h = __ldg(reinterpret_cast<const float2 *>(L.rec + (int64_t)row * 4));
+                    L.out[(int64_t)slot * L.stride + e] = INFINITY;
+                    remk = lb.x;
+                    rem2 = lb.y;
+                    slk = lb.x * slf;
+                    sl2 = lb.y * slf;
+                    lo = h.x;
+                    sc = h.y;
 #pragma unroll
-            for (int k = 0; k < NB; k++) band[k] = sband[k * DW_ITEMS + t];
-            row = srow[t];
-            e = se[t];
-            remk = sremk[t];
-            rem2 = srem2[t];
-            slk = sslk[t];
-            sl2 = ssl2[t];
-            lo = slo[t];
-            sc = ssc[t];
-        } else {
+                    for (int k = 0; k < NB; k++) band[k] = k == R ? 0.f : INFINITY;
+                } else {
 #pragma unroll
-            for (int k = 0; k < NB; k++) band[k] = INFINITY;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) n_next = 0;
-        __syncthreads();
-        if ((t & ~31) < nl) {
+                    for (int k = 0; k < NB; k++) band[k] = sband[k * IPW + it];
+                    remk = sremk[it];
+                    rem2 = srem2[it];
+                    slk = sslk[it];
+                    sl2 = ssl2[it];
+                    lo = slo[it];
+                    sc = ssc[it];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < NB; k++) band[k] = INFINITY;
+            }
             const float *x = X + (int64_t)row * m;
             const uint8_t *env = L.codes + (int64_t)row * L.cstride + L.mp;
             bool alive = have;
-            uint2 ev = make_uint2(0u, 0u);
             if (a == 0 && have) {
                 // columns j < R leave the LB_Keogh2 remainder before row 0
+                uint2 ev = make_uint2(0u, 0u);
                 for (int j = 0; j < min(R, m); j++) {
                     if ((j & 3) == 0) ev = __ldg(reinterpret_cast<const uint2 *>(env + 2 * j));
                     const uint32_t wv = (j & 2) ? ev.y : ev.x;
@@ -1328,17 +1355,13 @@ dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
                     rem2 = fmaf(-d, d, rem2);
                 }
             }
-            // 4 rows per step, interleaved with a one-cell lag (row i0+u works on
-            // band cell s-u at step s): all four need y[i0 + s - R], and the four
-            // dependency chains overlap.  Registers update in place: row u reads
-            // band[k] (row u-1's value from step s-1) and band[k+1] (written by
-            // row u-1 earlier in this step) before overwriting band[k].
             const float4 *xp = reinterpret_cast<const float4 *>(x);
             float4 xn = have ? __ldg(xp + (a >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
             int rows = 0;
             for (int i0 = a; i0 < b; i0 += 4) {
                 if (!__any_sync(0xFFFFFFFFu, alive)) break;
                 rows += alive ? 4 : 0;
+                wrows += 4;
                 const float4 xc = xn;
                 if (i0 + 4 < b) xn = __ldg(xp + (i0 >> 2) + 1);
                 // envelope codes of columns i0+R .. i0+R+3 (two aligned 4-column groups)
@@ -1397,32 +1420,30 @@ dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
                 }
             }
             my_cells += (unsigned long long)rows * NB;
+            // survivors keep their state slot and join the next pass's list
             const unsigned am = __ballot_sync(0xFFFFFFFFu, alive && b < m);
-            int dst = 0;
-            if (am) {
-                if (lane == 0) dst = atomicAdd(&n_next, __popc(am));
-                dst = __shfl_sync(0xFFFFFFFFu, dst, 0) + __popc(am & ((1u << lane) - 1u));
-            }
             if (alive) {
                 if (b >= m) {
                     L.out[(int64_t)slot * L.stride + e] = band[R];
                 } else {
+                    nxt[nn + __popc(am & ((1u << lane) - 1u))] = it;
 #pragma unroll
-                    for (int k = 0; k < NB; k++) sband[k * DW_ITEMS + dst] = band[k];
-                    srow[dst] = row;
-                    se[dst] = e;
-                    sremk[dst] = remk;
-                    srem2[dst] = rem2;
-                    sslk[dst] = slk;
-                    ssl2[dst] = sl2;
-                    slo[dst] = lo;
-                    ssc[dst] = sc;
+                    for (int k = 0; k < NB; k++) sband[k * IPW + it] = band[k];
+                    sremk[it] = remk;
+                    srem2[it] = rem2;
+                    sslk[it] = slk;
+                    ssl2[it] = sl2;
+                    slo[it] = lo;
+                    ssc[it] = sc;
                 }
             }
+            nn += __popc(am);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) n_live = n_next;
-        __syncthreads();
+        __syncwarp();
+        int *t = cur;
+        cur = nxt;
+        nxt = t;
+        ncur = nn;
         a = b;
     }
     if (cells || L.abandoned) {
@@ -1433,8 +1454,281 @@ dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
         }
         if (lane == 0) {
             if (cells && my_cells) atomicAdd(cells, my_cells);
+            if (cells && wrows) atomicAdd(cells + 5, wrows * 32 * NB);
             if (L.abandoned && my_ab) atomicAdd(&L.abandoned[q], my_ab);
         }
+    }
+}
+
+// ----------------------------------------------- pooled wave fp32 DTW
+// The wave's candidates of all queries run through row passes [0,8),
+// [8,16), [16,32), ... .  The first pass works per query slot straight from
+// the wave lists; every later pass takes the survivors of all queries from a
+// shared pool (state in global memory, SoA), so warps are always full and no
+// lane waits for a slower candidate beyond the end of a pass.  Lanes of one
+// warp may serve different queries: query samples, envelope and threshold are
+// per-lane loads (L1/L2-resident).  Per row block of 4 rows: the band lives
+// in registers, the 4 rows interleave with a one-cell lag (all four need the
+// same query sample at a step).  Abandon test after row i (UCR-suite
+// cumulative bounds, dtw.py:206-215):
+//   rmin_i + max(remK_i - slackK, rem2_i - slack2, 0) > thr
+//   remK_i = LBK total - sum_{i' <= i} LB_Keogh term of row i'     (rows left)
+//   rem2_i = LBK2 total - sum_{j <= i + R} LB_Keogh2 term of col j (columns
+//            no path through row i has reached)
+// with the totals from the wave LB kernel (code-based terms; the exact-x row
+// terms subtracted here are never smaller, so remK stays a lower bound) and
+// slack = total * (2m + 8) u for the fp32 running sums.
+struct DtwPool {
+    int *q;          // local query index
+    uint32_t *row;   // series row
+    int64_t *out;    // index into the wave's d32 array
+    float *st;       // [6][cap]: remK, rem2, slackK, slack2, lo, sc
+    float *band;     // [NB][cap]
+    int *count;
+    int64_t cap;
+};
+
+struct DtwCommon {
+    const float *X;
+    const float *qpad;  // [nq][YP]: y[j] at j + R, +inf outside [0, m)
+    const float *U, *Lo;
+    const float *thr;
+    const uint8_t *codes;
+    int64_t cstride;
+    int m, mp, YP;
+    float *out;  // the wave's d32 array
+    unsigned long long *abandoned;
+    int *computed;
+    unsigned long long *cells;  // profiling: [0] alive lane-cells, [5] executed lane-cells
+};
+
+#define DP_WARPS 4
+
+// rows [a, b) of one lane's candidate; returns whether it is still alive
+template <int R>
+__device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t row, float (&band)[2 * R + 1],
+                                          float &remk, float &rem2, float slk, float sl2, float lo, float sc,
+                                          float T, int a, int b, bool alive, unsigned long long &cal,
+                                          unsigned long long &cex, unsigned long long &nab) {
+    constexpr int NB = 2 * R + 1;
+    const int m = C.m;
+    const float *yq = C.qpad + (int64_t)q * C.YP;
+    const float *uq = C.U + (int64_t)q * m, *lq = C.Lo + (int64_t)q * m;
+    const float4 *xp = reinterpret_cast<const float4 *>(C.X + (int64_t)row * m);
+    const uint8_t *env = C.codes + (int64_t)row * C.cstride + C.mp;
+    float4 xn = alive ? __ldg(xp + (a >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i0 = a; i0 < b; i0 += 4) {
+        if (!__any_sync(0xFFFFFFFFu, alive)) break;
+        cal += alive ? 4 * NB : 0;
+        cex += 4 * NB;
+        const float4 xc = xn;
+        if (i0 + 4 < b && alive) xn = __ldg(xp + (i0 >> 2) + 1);
+        const int jb = (i0 + R) & ~3;
+        uint2 e0 = make_uint2(0u, 0u), e1 = make_uint2(0u, 0u);
+        if (alive && jb < m) e0 = __ldg(reinterpret_cast<const uint2 *>(env + 2 * jb));
+        if (alive && jb + 4 < m) e1 = __ldg(reinterpret_cast<const uint2 *>(env + 2 * jb + 8));
+        const float xr[4] = {xc.x, xc.y, xc.z, xc.w};
+        float lft[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        float rmn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        const float4 *yp = reinterpret_cast<const float4 *>(yq + i0);
+#pragma unroll
+        for (int s4 = 0; s4 < (NB + 3 + 3) / 4; s4++) {
+            const float4 yv4 = __ldg(yp + s4);
+            const float yv[4] = {yv4.x, yv4.y, yv4.z, yv4.w};
+#pragma unroll
+            for (int sv = 0; sv < 4; sv++) {
+                const int stp = 4 * s4 + sv;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int k = stp - u;
+                    if (k >= 0 && k < NB) {
+                        const float up = (k + 1 < NB) ? band[k + 1] : INFINITY;
+                        const float d = xr[u] - yv[sv];
+                        const float cv = fmaf(d, d, fminf(fminf(band[k], up), lft[u]));
+                        band[k] = cv;
+                        lft[u] = cv;
+                        rmn[u] = fminf(rmn[u], cv);
+                    }
+                }
+            }
+        }
+        const float4 u4 = __ldg(reinterpret_cast<const float4 *>(uq + i0));
+        const float4 l4 = __ldg(reinterpret_cast<const float4 *>(lq + i0));
+        const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+        bool cut = false;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const float v = fmaxf(fmaxf(xr[u] - uu[u], ll[u] - xr[u]), 0.f);
+            remk = fmaf(-v, v, remk);
+            const int jj = i0 + u + R;
+            if (jj < m) {
+                const int off = (R & 3) + u;  // column jj within the 8-column window
+                const uint32_t wv = off < 2 ? e0.x : off < 4 ? e0.y : off < 6 ? e1.x : e1.y;
+                const int bu = 2 * (off & 1);
+                const float qj = __ldg(yq + jj + R);
+                const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
+                const float dd = fmaxf(fmaxf(qj - ue, le - qj), 0.f);
+                rem2 = fmaf(-dd, dd, rem2);
+            }
+            cut = cut || (rmn[u] + fmaxf(fmaxf(remk - slk, rem2 - sl2), 0.f) > T);
+        }
+        if (alive && cut) {
+            alive = false;
+            nab++;
+        }
+    }
+    return alive;
+}
+
+// survivors of a pass -> pool (warp-aggregated append); finished -> d32
+template <int R>
+__device__ __forceinline__ void dtwp_emit(const DtwCommon &C, const DtwPool &P, bool alive, bool last, int q,
+                                          uint32_t row, int64_t oi, const float (&band)[2 * R + 1], float remk,
+                                          float rem2, float slk, float sl2, float lo, float sc) {
+    constexpr int NB = 2 * R + 1;
+    const int lane = threadIdx.x & 31;
+    const unsigned am = __ballot_sync(0xFFFFFFFFu, alive && !last);
+    int base = 0;
+    if (am) {
+        if (lane == 0) base = atomicAdd(P.count, __popc(am));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    }
+    if (!alive) return;
+    if (last) {
+        C.out[oi] = band[R];
+        return;
+    }
+    const int64_t d = base + __popc(am & ((1u << lane) - 1u));
+    if (d >= P.cap) return;  // cannot happen: the pool holds every wave candidate
+    P.q[d] = q;
+    P.row[d] = row;
+    P.out[d] = oi;
+    P.st[0 * P.cap + d] = remk;
+    P.st[1 * P.cap + d] = rem2;
+    P.st[2 * P.cap + d] = slk;
+    P.st[3 * P.cap + d] = sl2;
+    P.st[4 * P.cap + d] = lo;
+    P.st[5 * P.cap + d] = sc;
+#pragma unroll
+    for (int k = 0; k < NB; k++) P.band[(int64_t)k * P.cap + d] = band[k];
+}
+
+__device__ __forceinline__ void dtwp_flush(const DtwCommon &C, unsigned long long cal, unsigned long long cex) {
+    if (!C.cells) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cal += __shfl_xor_sync(0xFFFFFFFFu, cal, o);
+        cex += __shfl_xor_sync(0xFFFFFFFFu, cex, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (cal) atomicAdd(C.cells, cal);
+        if (cex) atomicAdd(C.cells + 5, cex);
+    }
+}
+
+// first pass, per query slot: wave list entries -> rows [0, b) -> pool
+template <int R>
+__global__ void __launch_bounds__(32 * DP_WARPS)
+dtwp_first_kernel(DtwCommon C, const int *__restrict__ act, const uint32_t *__restrict__ wrows,
+                  const float2 *__restrict__ wlb, const int *__restrict__ wcnt, int64_t wcap,
+                  const uint4 *__restrict__ rec, int b, DtwPool P) {
+    constexpr int NB = 2 * R + 1;
+    const int slot = blockIdx.y;
+    const int q = act[slot];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int total = min(wcnt[slot], (int)wcap);
+    const int e0 = (blockIdx.x * DP_WARPS + w) * 32;
+    if (e0 >= total) return;
+    const int e = e0 + lane;
+    const bool have = e < total;
+    if (lane == 0 && C.computed) atomicAdd(&C.computed[q], min(32, total - e0));
+    const int64_t oi = (int64_t)slot * wcap + e;
+    uint32_t row = 0;
+    float remk = 0.f, rem2 = 0.f, slk = 0.f, sl2 = 0.f, lo = 0.f, sc = 0.f;
+    const float slf = (float)(2 * C.m + 8) * U32_EPS;
+    if (have) {
+        row = wrows[oi];
+        const float2 lb = wlb[oi];
+        const float2 h = __ldg(reinterpret_cast<const float2 *>(rec + (int64_t)row * 4));
+        C.out[oi] = INFINITY;
+        remk = lb.x;
+        rem2 = lb.y;
+        slk = lb.x * slf;
+        sl2 = lb.y * slf;
+        lo = h.x;
+        sc = h.y;
+        // columns j < R leave the LB_Keogh2 remainder before row 0
+        const uint8_t *env = C.codes + (int64_t)row * C.cstride + C.mp;
+        const float *yq = C.qpad + (int64_t)q * C.YP;
+        uint2 ev = make_uint2(0u, 0u);
+        for (int j = 0; j < min(R, C.m); j++) {
+            if ((j & 3) == 0) ev = __ldg(reinterpret_cast<const uint2 *>(env + 2 * j));
+            const uint32_t wv = (j & 2) ? ev.y : ev.x;
+            const int bu = 2 * (j & 1);
+            const float qj = __ldg(yq + j + R);
+            const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
+            const float d = fmaxf(fmaxf(qj - ue, le - qj), 0.f);
+            rem2 = fmaf(-d, d, rem2);
+        }
+    }
+    float band[NB];
+#pragma unroll
+    for (int k = 0; k < NB; k++) band[k] = k == R ? 0.f : INFINITY;
+    unsigned long long cal = 0, cex = 0, nab = 0;
+    const bool alive = dtwp_rows<R>(C, q, row, band, remk, rem2, slk, sl2, lo, sc, C.thr[q], 0, b, have, cal,
+                                    cex, nab);
+    if (nab && C.abandoned) atomicAdd(&C.abandoned[q], nab);
+    dtwp_emit<R>(C, P, alive, b >= C.m, q, row, oi, band, remk, rem2, slk, sl2, lo, sc);
+    dtwp_flush(C, cal, cex);
+}
+
+// later passes over the pooled survivors of all queries (persistent grid)
+template <int R>
+__global__ void __launch_bounds__(32 * DP_WARPS)
+dtwp_pass_kernel(DtwCommon C, DtwPool in, DtwPool P, int a, int b) {
+    constexpr int NB = 2 * R + 1;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n = min(*in.count, (int)in.cap);
+    unsigned long long cal = 0, cex = 0;
+    for (int e0 = (blockIdx.x * DP_WARPS + w) * 32; e0 < n; e0 += gridDim.x * DP_WARPS * 32) {
+        const int e = e0 + lane;
+        const bool have = e < n;
+        int q = 0;
+        uint32_t row = 0;
+        int64_t oi = 0;
+        float remk = 0.f, rem2 = 0.f, slk = 0.f, sl2 = 0.f, lo = 0.f, sc = 0.f;
+        float band[NB];
+        if (have) {
+            q = in.q[e];
+            row = in.row[e];
+            oi = in.out[e];
+            remk = in.st[0 * in.cap + e];
+            rem2 = in.st[1 * in.cap + e];
+            slk = in.st[2 * in.cap + e];
+            sl2 = in.st[3 * in.cap + e];
+            lo = in.st[4 * in.cap + e];
+            sc = in.st[5 * in.cap + e];
+#pragma unroll
+            for (int k = 0; k < NB; k++) band[k] = in.band[(int64_t)k * in.cap + e];
+        } else {
+#pragma unroll
+            for (int k = 0; k < NB; k++) band[k] = INFINITY;
+        }
+        unsigned long long nab = 0;
+        const bool alive = dtwp_rows<R>(C, q, row, band, remk, rem2, slk, sl2, lo, sc, have ? C.thr[q] : 0.f,
+                                        a, b, have, cal, cex, nab);
+        if (nab && C.abandoned) atomicAdd(&C.abandoned[q], nab);
+        dtwp_emit<R>(C, P, alive, b >= C.m, q, row, oi, band, remk, rem2, slk, sl2, lo, sc);
+    }
+    dtwp_flush(C, cal, cex);
+}
+
+// padded query copies for the pooled DTW: qpad[q][t] = y[t - R] (+inf outside)
+__global__ void qpad_kernel(const float *__restrict__ Q, int m, int R, int YP, float *__restrict__ qpad) {
+    const int q = blockIdx.x;
+    for (int t = threadIdx.x; t < YP; t += blockDim.x) {
+        const int j = t - R;
+        qpad[(int64_t)q * YP + t] = (j >= 0 && j < m) ? Q[(int64_t)q * m + j] : INFINITY;
     }
 }
 
@@ -1906,15 +2200,15 @@ static int launch_dtw32w_w(ssh_ctx *ctx, const float *X, const float *Q, const f
                            const DtwWave &L, const float *thr, int nq, int wave, cudaStream_t st) {
     const int m = ctx->p.m;
     constexpr int NB = 2 * R + 1;
-    constexpr int DW_ITEMS = 32 * DW_WARPS;
+    constexpr int DW_ITEMS = DW_WARPS * DW_IPW;
     const int YP = ((m + 2 * R + 8) + 3) & ~3;
     const size_t smem = (size_t)(YP + 2 * m + (NB + 6) * DW_ITEMS) * sizeof(float) + 2 * DW_ITEMS * 4;
     SSH_REQUIRE(smem <= 227 * 1024, SSH_ERR_UNSUPPORTED, "wave DTW: series too long (m=%d)", m);
     SSH_CUDA(cudaFuncSetAttribute(dtw32w_kernel<R, DW_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     dim3 grid((unsigned)ssh_div_up(wave, DW_ITEMS), (unsigned)nq);
-    dtw32w_kernel<R, DW_WARPS><<<grid, DW_ITEMS, smem, st>>>(X, m, Q, U, Lo, L, thr,
-                                                             ctx->profile ? ctx->d_cells : nullptr);
+    dtw32w_kernel<R, DW_WARPS><<<grid, 32 * DW_WARPS, smem, st>>>(X, m, Q, U, Lo, L, thr,
+                                                                  ctx->profile ? ctx->d_cells : nullptr);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
@@ -1925,16 +2219,15 @@ template <int R>
 static int launch_dtw32w(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
                          const DtwWave &L, const float *thr, int nq, int wave, cudaStream_t st) {
     if (wave <= 0) return SSH_OK;
-    if (wave <= 256) return launch_dtw32w_w<R, 2>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
-    if (wave <= 2048) return launch_dtw32w_w<R, 4>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
-    return launch_dtw32w_w<R, 8>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
+    if (wave <= 2 * DW_IPW) return launch_dtw32w_w<R, 2>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
+    return launch_dtw32w_w<R, 4>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
 }
 
 // wave fp32 DTW: compacting register-band kernel for the common radii, the
 // generic lane-per-candidate kernel otherwise
 static int launch_dtw32_wave(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
-                             const DtwWave &W, const DtwList &Lg, const float *thr, int nq, int wave,
-                             cudaStream_t st);
+                             const DtwWave &W, const DtwList &Lg, const DtwCommon &C, const float *thr, int nq,
+                             int wave, cudaStream_t st);
 
 // fp32 DTW of a candidate list (register band for the common radii, shared-memory band otherwise)
 static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const float *U,
@@ -1960,23 +2253,76 @@ static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const floa
     return SSH_OK;
 }
 
+template <int R>
+static int launch_dtw_pooled(ssh_ctx *ctx, const DtwCommon &C, const int *act, const uint32_t *wrows,
+                             const float2 *wlb, const int *wcnt, int64_t wcap, const uint4 *rec, int nact,
+                             int wave, cudaStream_t st);
+
 static int launch_dtw32_wave(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
-                             const DtwWave &W, const DtwList &Lg, const float *thr, int nq, int wave,
-                             cudaStream_t st) {
+                             const DtwWave &W, const DtwList &Lg, const DtwCommon &C, const float *thr, int nq,
+                             int wave, cudaStream_t st) {
     const int m = ctx->p.m, r = ctx->p.radius;
-    const int YPmax = m + 2 * r + 12;
-    const bool fits = (m & 3) == 0 && (size_t)(YPmax + 2 * m + (2 * r + 9) * 256) * 4 <= 227 * 1024;
-#define DTWW(RR) \
-    case RR:     \
-        if (fits) return launch_dtw32w<RR>(ctx, X, Q, U, Lo, W, thr, nq, wave, st); \
-        break;
     static const bool legacy = getenv("SSH_DEBUG_DTW_LEGACY") != nullptr;
-    if (!legacy) switch (r) {
-        DTWW(3) DTWW(6) DTWW(13) DTWW(26) DTWW(51)
+#define DTWP(RR) \
+    case RR:     \
+        return launch_dtw_pooled<RR>(ctx, C, W.act, W.rows, W.lbs, W.cnt, W.stride, W.rec, nq, wave, st);
+    if (!legacy && (m & 3) == 0 && C.qpad) switch (r) {
+        DTWP(3) DTWP(6) DTWP(13) DTWP(26) DTWP(51)
         default: break;
     }
-#undef DTWW
+#undef DTWP
     return launch_dtw32(ctx, X, Q, U, Lo, Lg, thr, nq, st);
+}
+
+
+// pooled wave DTW (register band, radius R): first pass per slot, then
+// pooled passes over the survivors of all queries
+template <int R>
+static int launch_dtw_pooled(ssh_ctx *ctx, const DtwCommon &C, const int *act, const uint32_t *wrows,
+                             const float2 *wlb, const int *wcnt, int64_t wcap, const uint4 *rec, int nact,
+                             int wave, cudaStream_t st) {
+    constexpr int NB = 2 * R + 1;
+    if (wave <= 0 || nact <= 0) return SSH_OK;
+    const int64_t cap = (int64_t)nact * wave;
+    const size_t per = 4 + 4 + 8 + 6 * 4 + NB * 4;
+    DtwPool pool[2];
+    for (int i = 0; i < 2; i++) {
+        unsigned char *base = (unsigned char *)ssh_slot(ctx, i ? SLOT_Q_POOLB : SLOT_Q_POOLA, per * (size_t)cap + 64, st);
+        if (!base) return SSH_ERR_OOM;
+        pool[i].out = reinterpret_cast<int64_t *>(base);
+        pool[i].q = reinterpret_cast<int *>(pool[i].out + cap);
+        pool[i].row = reinterpret_cast<uint32_t *>(pool[i].q + cap);
+        pool[i].st = reinterpret_cast<float *>(pool[i].row + cap);
+        pool[i].band = pool[i].st + 6 * cap;
+        pool[i].cap = cap;
+    }
+    int *cnt = (int *)ssh_slot(ctx, SLOT_Q_POOLCNT, 64 * sizeof(int), st);
+    if (!cnt) return SSH_ERR_OOM;
+    const int m = C.m;
+    int nlev = 1;
+    for (int a = 8; a < m; a = std::min(m, 2 * a)) nlev++;
+    SSH_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * nlev, st));
+    pool[0].count = cnt;
+    const int b0 = std::min(m, 8);
+    dim3 g1((unsigned)ssh_div_up(wave, 32 * DP_WARPS), (unsigned)nact);
+    dtwp_first_kernel<R><<<g1, 32 * DP_WARPS, 0, st>>>(C, act, wrows, wlb, wcnt, wcap, rec, b0, pool[0]);
+    SSH_CHECK_LAUNCH();
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtwp_pass_kernel<R>, 32 * DP_WARPS, 0);
+        per_sm = std::max(1, per_sm);
+    }
+    int lev = 1;
+    for (int a = b0; a < m; lev++) {
+        const int b = std::min(m, 2 * a);
+        DtwPool in = pool[(lev - 1) & 1], out = pool[lev & 1];
+        in.count = cnt + lev - 1;
+        out.count = cnt + lev;
+        dtwp_pass_kernel<R><<<ctx->num_sms * per_sm, 32 * DP_WARPS, 0, st>>>(C, in, out, a, b);
+        SSH_CHECK_LAUNCH();
+        a = b;
+    }
+    return SSH_OK;
 }
 
 static int launch_dtw64_list(const float *X, int m, int r, const float *Q, const uint32_t *list,
@@ -2120,6 +2466,12 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         if (rc) return rc;
         envelope_kernel<<<nc, 256, 2 * m * sizeof(float), st>>>(Qc, m, r, ix->seg, nseg, B.U, B.Lo, B.Useg, B.Lseg);
         SSH_CHECK_LAUNCH();
+        // padded query copies for the pooled wave DTW
+        const int qYP = ((m + 2 * r + 8) + 3) & ~3;
+        float *qpad = (float *)ssh_slot(ctx, SLOT_Q_QPAD, sizeof(float) * (size_t)nc * qYP, st);
+        if (!qpad) return SSH_ERR_OOM;
+        qpad_kernel<<<nc, 256, 0, st>>>(Qc, m, r, qYP, qpad);
+        SSH_CHECK_LAUNCH();
         std::vector<long long> hc(nc);
         SSH_CUDA(cudaMemcpyAsync(hc.data(), ncand, sizeof(long long) * nc, cudaMemcpyDeviceToHost, st));
         SSH_CUDA(cudaStreamSynchronize(st));
@@ -2233,7 +2585,10 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                         DtwList dl{wrows, wcap, S.wcnt, nullptr, wave, nullptr, wd32, S.aband, S.computed, S.act};
                         DtwWave dw{wrows, wlb, wcap, S.wcnt, wd32, S.aband, S.computed, (const uint4 *)ix->rec,
                                    ix->codes, ix->cstride, ix->mp, S.act};
-                        rc = launch_dtw32_wave(ctx, X, Qs, S.U, S.Lo, dw, dl, S.thr, nact, wave, st);
+                        DtwCommon dc{X, qpad ? qpad + (int64_t)sa * qYP : nullptr, S.U, S.Lo, S.thr, ix->codes,
+                                     ix->cstride, m, ix->mp, qYP, wd32, S.aband, S.computed,
+                                     ctx->profile ? ctx->d_cells : nullptr};
+                        rc = launch_dtw32_wave(ctx, X, Qs, S.U, S.Lo, dw, dl, dc, S.thr, nact, wave, st);
                         if (rc) return rc;
                     }
                     pf.end(4);
