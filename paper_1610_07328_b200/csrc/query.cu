@@ -1503,6 +1503,7 @@ struct DtwCommon {
 };
 
 #define DP_WARPS 4
+#define DP_MAXPASS 64  // longest pooled row pass
 
 // rows [a, b) of one lane's candidate; returns whether it is still alive
 template <int R>
@@ -2299,8 +2300,10 @@ static int launch_dtw_pooled(ssh_ctx *ctx, const DtwCommon &C, const int *act, c
     int *cnt = (int *)ssh_slot(ctx, SLOT_Q_POOLCNT, 64 * sizeof(int), st);
     if (!cnt) return SSH_ERR_OOM;
     const int m = C.m;
+    // pass ends 8, 16, 32, 64, then every DP_MAXPASS rows
+    auto next_end = [&](int a) { return std::min(m, a < DP_MAXPASS ? 2 * a : a + DP_MAXPASS); };
     int nlev = 1;
-    for (int a = 8; a < m; a = std::min(m, 2 * a)) nlev++;
+    for (int a = std::min(m, 8); a < m; a = next_end(a)) nlev++;
     SSH_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * nlev, st));
     pool[0].count = cnt;
     const int b0 = std::min(m, 8);
@@ -2314,7 +2317,7 @@ static int launch_dtw_pooled(ssh_ctx *ctx, const DtwCommon &C, const int *act, c
     }
     int lev = 1;
     for (int a = b0; a < m; lev++) {
-        const int b = std::min(m, 2 * a);
+        const int b = next_end(a);
         DtwPool in = pool[(lev - 1) & 1], out = pool[lev & 1];
         in.count = cnt + lev - 1;
         out.count = cnt + lev;
