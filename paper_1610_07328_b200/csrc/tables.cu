@@ -8,6 +8,8 @@
 // memory so each digit run is written contiguously.  Then a run-length pass
 // emits CSR: sorted unique keys, u32 offsets, u32 rows.  Bytes per
 // (series, table): 8 B key read + 8 B key + 4 B row written per pass.
+#include <limits.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -41,15 +43,16 @@ __global__ void rs_transpose(const uint64_t *__restrict__ sig, int64_t N, int L,
     }
 }
 
+template <typename K>
 __global__ void __launch_bounds__(RS_THREADS)
-rs_hist(const uint64_t *__restrict__ keys, int64_t N, int shift, int ntiles,
+rs_hist(const K *__restrict__ keys, int64_t N, int shift, int ntiles,
         uint32_t *__restrict__ hist) {
     __shared__ uint32_t h[RS_BINS];
     const int j = blockIdx.y;
     const int tile = blockIdx.x;
     h[threadIdx.x] = 0;
     __syncthreads();
-    const uint64_t *k = keys + (int64_t)j * N;
+    const K *k = keys + (int64_t)j * N;
     int64_t base = (int64_t)tile * RS_TILE;
 #pragma unroll 4
     for (int it = 0; it < RS_ITEMS; it++) {
@@ -87,13 +90,14 @@ __global__ void __launch_bounds__(1024) rs_scan(uint32_t *__restrict__ hist, int
     }
 }
 
+template <typename K>
 __global__ void __launch_bounds__(RS_THREADS)
-rs_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ rin, int64_t N,
-           int shift, int ntiles, const uint32_t *__restrict__ gofs, uint64_t *__restrict__ kout,
+rs_scatter(const K *__restrict__ kin, const uint32_t *__restrict__ rin, int64_t N,
+           int shift, int ntiles, const uint32_t *__restrict__ gofs, K *__restrict__ kout,
            uint32_t *__restrict__ rout) {
     __shared__ uint32_t wcnt[RS_WARPS][RS_BINS];
     __shared__ uint32_t dstart[RS_BINS];
-    __shared__ uint64_t skey[RS_TILE];
+    __shared__ K skey[RS_TILE];
     __shared__ uint32_t srow[RS_TILE];
     const int j = blockIdx.y;
     const int tile = blockIdx.x;
@@ -101,18 +105,18 @@ rs_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ rin, i
     const unsigned lt = (1u << lane) - 1u;
     for (int e = threadIdx.x; e < RS_WARPS * RS_BINS; e += RS_THREADS) (&wcnt[0][0])[e] = 0;
     __syncthreads();
-    const uint64_t *k = kin + (int64_t)j * N;
+    const K *k = kin + (int64_t)j * N;
     const uint32_t *r = rin + (int64_t)j * N;
     // warp w owns the contiguous sub-tile [w*32*ITEMS, (w+1)*32*ITEMS) of the tile
     const int64_t wbase = (int64_t)tile * RS_TILE + (int64_t)w * 32 * RS_ITEMS;
-    uint64_t key[RS_ITEMS];
+    K key[RS_ITEMS];
     uint32_t row[RS_ITEMS];
     uint32_t rank[RS_ITEMS];
 #pragma unroll
     for (int it = 0; it < RS_ITEMS; it++) {
         int64_t i = wbase + it * 32 + lane;
         bool valid = i < N;
-        key[it] = valid ? k[i] : 0ULL;
+        key[it] = valid ? k[i] : (K)0;
         row[it] = valid ? r[i] : 0u;
         unsigned d = valid ? (unsigned)((key[it] >> shift) & 0xFF) : RS_BINS;
         unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
@@ -171,7 +175,7 @@ rs_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ rin, i
     const int nvalid = (int)min((int64_t)RS_TILE, N - tbase);
     const uint32_t *go = gofs + (int64_t)j * RS_BINS * ntiles;
     for (int e = threadIdx.x; e < nvalid; e += RS_THREADS) {
-        uint64_t kk = skey[e];
+        K kk = skey[e];
         unsigned d = (unsigned)((kk >> shift) & 0xFF);
         int64_t dst = (int64_t)go[(int64_t)d * ntiles + tile] + (e - dstart[d]);
         kout[(int64_t)j * N + dst] = kk;
@@ -276,14 +280,244 @@ int ssh_sort_columns(ssh_ctx *ctx, const uint64_t *rowmajor, int64_t N, int L, u
     dim3 grid((unsigned)ntiles, (unsigned)L);
     for (int pass = 0; pass < 8; pass++) {
         int shift = 8 * pass;
-        rs_hist<<<grid, RS_THREADS, 0, st>>>(kin, N, shift, ntiles, hist); ssh_count_launch();
+        rs_hist<uint64_t><<<grid, RS_THREADS, 0, st>>>(kin, N, shift, ntiles, hist); ssh_count_launch();
         rs_scan<<<L, 1024, 0, st>>>(hist, ntiles); ssh_count_launch();
-        rs_scatter<<<grid, RS_THREADS, 0, st>>>(kin, rin, N, shift, ntiles, hist, kout, rout); ssh_count_launch();
+        rs_scatter<uint64_t><<<grid, RS_THREADS, 0, st>>>(kin, rin, N, shift, ntiles, hist, kout, rout);
+        ssh_count_launch();
         uint64_t *tk = kin; kin = kout; kout = tk;
         uint32_t *tr = rin; rin = rout; rout = tr;
     }
     SSH_CUDA(cudaGetLastError());
     *keys_sorted = kin;
+    return SSH_OK;
+}
+
+
+// sig [N][L] -> full keys kT [L][N], high halves hi [L][N], rows [L][N] = 0..N-1
+__global__ void rs_transpose_hi(const uint64_t *__restrict__ sig, int64_t N, int L, uint64_t *__restrict__ keys,
+                                uint32_t *__restrict__ hi, uint32_t *__restrict__ rows) {
+    __shared__ uint64_t tile[32][33];
+    int64_t r0 = (int64_t)blockIdx.x * 32;
+    int j0 = blockIdx.y * 32;
+    int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int yy = ty; yy < 32; yy += 8) {
+        int64_t r = r0 + yy;
+        int j = j0 + tx;
+        if (r < N && j < L) tile[yy][tx] = sig[r * L + j];
+    }
+    __syncthreads();
+    for (int yy = ty; yy < 32; yy += 8) {
+        int j = j0 + yy;
+        int64_t r = r0 + tx;
+        if (r < N && j < L) {
+            const uint64_t k = tile[tx][yy];
+            keys[(int64_t)j * N + r] = k;
+            hi[(int64_t)j * N + r] = (uint32_t)(k >> 32);
+            rows[(int64_t)j * N + r] = (uint32_t)r;
+        }
+    }
+}
+
+// full keys in (hi-sorted) order; a position whose high half equals the
+// previous one's but whose key differs lies in a run of equal high halves that
+// needs a fix-up; its bounds come from binary searches on the sorted high
+// halves (duplicates are removed by rs_dedup_runs).
+__global__ void rs_gather_dirty(const uint64_t *__restrict__ kT, const uint32_t *__restrict__ rows,
+                                const uint32_t *__restrict__ hs, int64_t N, int L, uint64_t *__restrict__ ks,
+                                int4 *__restrict__ runs, int *__restrict__ nruns, int maxruns) {
+    const int j = blockIdx.y;
+    const uint64_t *kt = kT + (int64_t)j * N;
+    const uint32_t *rw = rows + (int64_t)j * N;
+    const uint32_t *h = hs + (int64_t)j * N;
+    uint64_t *ko = ks + (int64_t)j * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = kt[rw[i]];
+        ko[i] = k;
+        if (i == 0 || h[i - 1] != h[i]) continue;
+        if (kt[rw[i - 1]] == k) continue;
+        const uint32_t hv = h[i];
+        int64_t lo = 0, hi = i;  // first position with h == hv
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (h[mid] < hv) lo = mid + 1; else hi = mid;
+        }
+        const int64_t s = lo;
+        lo = i;
+        hi = N;  // first position with h > hv
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (h[mid] <= hv) lo = mid + 1; else hi = mid;
+        }
+        const int slot = atomicAdd(nruns, 1);
+        if (slot < maxruns) runs[slot] = make_int4(j, (int)s, (int)(lo - s), 0);
+    }
+}
+
+// one block: sort the reported runs by (table, start) and drop duplicates
+__global__ void __launch_bounds__(1024) rs_dedup_runs(int4 *__restrict__ runs, int *__restrict__ nruns, int maxruns) {
+    extern __shared__ int4 rsm[];
+    const int n = min(*nruns, maxruns);
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) rsm[i] = i < n ? runs[i] : make_int4(INT_MAX, INT_MAX, 0, 0);
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int idx = threadIdx.x; idx < (P >> 1); idx += blockDim.x) {
+                const int i = 2 * idx - (idx & (jj - 1)), l = i + jj;
+                const int4 x = rsm[i], y = rsm[l];
+                const bool gt = x.x > y.x || (x.x == y.x && x.y > y.y);
+                if (gt == ((i & k) == 0)) {
+                    rsm[i] = y;
+                    rsm[l] = x;
+                }
+            }
+            __syncthreads();
+        }
+    __shared__ int cnt;
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int i = 0; i < n; i++)
+            if (i == 0 || rsm[i].x != rsm[i - 1].x || rsm[i].y != rsm[i - 1].y) rsm[c++] = rsm[i];
+        cnt = c;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) runs[i] = rsm[i];
+    if (threadIdx.x == 0) *nruns = cnt;
+}
+
+// stable sort of each dirty run by the full key (rows ascending inside a
+// key): one block per run, 4 LSD passes over the low halves through scratch
+__global__ void __launch_bounds__(1024)
+rs_fix_runs(uint64_t *__restrict__ ks, uint32_t *__restrict__ rows, int64_t N, const int4 *__restrict__ runs,
+            const int *__restrict__ nruns, int maxruns, uint64_t *__restrict__ kscr, uint32_t *__restrict__ rscr) {
+    __shared__ uint32_t hist[256], wcnt[32][256];
+    __shared__ uint32_t carry[256];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nr = min(*nruns, maxruns);
+    for (int ri = blockIdx.x; ri < nr; ri += gridDim.x) {
+        const int4 rr = runs[ri];
+        const int64_t off = (int64_t)rr.x * N + rr.y;
+        const int len = rr.z;
+        uint64_t *ka = ks + off, *kb = kscr + off;
+        uint32_t *ra = rows + off, *rb = rscr + off;
+        for (int pass = 0; pass < 4; pass++) {
+            const int shift = 8 * pass;
+            for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+            __syncthreads();
+            for (int i = threadIdx.x; i < len; i += blockDim.x) atomicAdd(&hist[(ka[i] >> shift) & 0xFF], 1u);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t run = 0;
+                for (int b = 0; b < 256; b++) {
+                    carry[b] = run;
+                    run += hist[b];
+                }
+            }
+            __syncthreads();
+            // tiles of blockDim elements in order; inside a tile: warp order,
+            // then lane order (match_any peers) -> stable
+            for (int t0 = 0; t0 < len; t0 += blockDim.x) {
+                const int i = t0 + threadIdx.x;
+                const bool valid = i < len;
+                const uint64_t k = valid ? ka[i] : 0ULL;
+                const uint32_t rw = valid ? ra[i] : 0u;
+                const unsigned d = valid ? (unsigned)((k >> shift) & 0xFF) : 256u;
+                for (int b = lane; b < 256; b += 32) wcnt[w][b] = 0;
+                __syncthreads();
+                const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+                const unsigned lt = (1u << lane) - 1u;
+                if (valid && (peers & lt) == 0) wcnt[w][d] = __popc(peers);
+                __syncthreads();
+                uint32_t before = 0;
+                if (valid)
+                    for (int ww = 0; ww < w; ww++) before += wcnt[ww][d];
+                __syncthreads();
+                if (valid) {
+                    const uint32_t p = carry[d] + before + __popc(peers & lt);
+                    kb[p] = k;
+                    rb[p] = rw;
+                }
+                __syncthreads();
+                // advance carries by this tile's digit counts
+                for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+                    uint32_t c = 0;
+                    for (int ww = 0; ww < 32; ww++) c += wcnt[ww][b];
+                    carry[b] += c;
+                }
+                __syncthreads();
+            }
+            uint64_t *tk = ka; ka = kb; kb = tk;
+            uint32_t *tr = ra; ra = rb; rb = tr;
+            __syncthreads();
+        }
+        // 4 passes (even): the result is back in ks/rows
+    }
+}
+
+// Stable sort of every table column of sig by the full u64 key: 4 LSD passes
+// over the high 32 bits (16 B moved per element and pass instead of 24 for
+// 8 passes over the whole key), then runs whose keys share the high half but
+// differ are fixed up by a per-run stable sort.  rows_out [L][N] receives the
+// rows, *keys_sorted [L][N] the full keys (ctx slot).
+int ssh_sort_columns_hi(ssh_ctx *ctx, const uint64_t *rowmajor, int64_t N, int L, uint32_t *rows_out,
+                        uint64_t **keys_sorted, cudaStream_t st) {
+    const int ntiles = ssh_div_up(N, RS_TILE);
+    const size_t kbytes = sizeof(uint64_t) * (size_t)L * N;
+    const size_t hbytes32 = sizeof(uint32_t) * (size_t)L * N;
+    const size_t hbytes = sizeof(uint32_t) * (size_t)L * RS_BINS * ntiles;
+    const int MAXRUNS = 8192;  // reported high-half collision runs per build (expected ~10 per table)
+    uint64_t *kT = (uint64_t *)ssh_slot(ctx, SLOT_RS_KEYS_A, kbytes, st);
+    uint64_t *ks = (uint64_t *)ssh_slot(ctx, SLOT_RS_KEYS_B, kbytes + 2 * hbytes32 + 16 + sizeof(int4) * MAXRUNS, st);
+    uint32_t *rB = (uint32_t *)ssh_slot(ctx, SLOT_RS_ROWS_B, hbytes32, st);
+    uint32_t *hist = (uint32_t *)ssh_slot(ctx, SLOT_RS_HIST, hbytes, st);
+    if (!kT || !ks || !rB || !hist) return SSH_ERR_OOM;
+    uint32_t *hA = reinterpret_cast<uint32_t *>(ks + (size_t)L * N);
+    uint32_t *hB = hA + (size_t)L * N;
+    int *nruns = reinterpret_cast<int *>(hB + (size_t)L * N);
+    int4 *runs = reinterpret_cast<int4 *>(reinterpret_cast<unsigned char *>(nruns) + 16);
+    uint32_t *rA = rows_out;  // 4 passes (even): the sorted rows land back in rA
+    {
+        dim3 g((unsigned)ssh_div_up(N, 32), (unsigned)ssh_div_up(L, 32));
+        rs_transpose_hi<<<g, 256, 0, st>>>(rowmajor, N, L, kT, hA, rA);
+        ssh_count_launch();
+    }
+    uint32_t *kin = hA, *kout = hB;
+    uint32_t *rin = rA, *rout = rB;
+    dim3 grid((unsigned)ntiles, (unsigned)L);
+    for (int pass = 0; pass < 4; pass++) {
+        const int shift = 8 * pass;
+        rs_hist<uint32_t><<<grid, RS_THREADS, 0, st>>>(kin, N, shift, ntiles, hist); ssh_count_launch();
+        rs_scan<<<L, 1024, 0, st>>>(hist, ntiles); ssh_count_launch();
+        rs_scatter<uint32_t><<<grid, RS_THREADS, 0, st>>>(kin, rin, N, shift, ntiles, hist, kout, rout);
+        ssh_count_launch();
+        uint32_t *tk = kin; kin = kout; kout = tk;
+        uint32_t *tr = rin; rin = rout; rout = tr;
+    }
+    SSH_CUDA(cudaMemsetAsync(nruns, 0, sizeof(int), st));
+    {
+        dim3 g((unsigned)std::min<int64_t>(ssh_div_up(N, 256), 1024), (unsigned)L);
+        rs_gather_dirty<<<g, 256, 0, st>>>(kT, rA, kin, N, L, ks, runs, nruns, MAXRUNS);
+        ssh_count_launch();
+    }
+    int hn = 0;
+    SSH_CUDA(cudaMemcpyAsync(&hn, nruns, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SSH_CUDA(cudaStreamSynchronize(st));
+    if (hn > MAXRUNS)  // more high-half collisions than the fix-up list holds: full-key sort
+        return ssh_sort_columns(ctx, rowmajor, N, L, rows_out, keys_sorted, st);
+    if (hn == 0) {
+        *keys_sorted = ks;
+        return SSH_OK;
+    }
+    SSH_CUDA(cudaFuncSetAttribute(rs_dedup_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(int4) * MAXRUNS)));
+    rs_dedup_runs<<<1, 1024, sizeof(int4) * MAXRUNS, st>>>(runs, nruns, MAXRUNS);
+    ssh_count_launch();
+    // scratch for the fix-ups: the transposed keys and the spare row buffer
+    rs_fix_runs<<<256, 1024, 0, st>>>(ks, rA, N, runs, nruns, MAXRUNS, kT, rB);
+    ssh_count_launch();
+    SSH_CUDA(cudaGetLastError());
+    *keys_sorted = ks;
     return SSH_OK;
 }
 
@@ -351,7 +585,7 @@ extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int
     size_t rbytes = sizeof(uint32_t) * (size_t)L * N;
     e = cudaMallocAsync((void **)&ix->ids, rbytes, st);
     if (e != cudaSuccess) { delete ix; return ssh_cuda_fail(e, "cudaMallocAsync(ids)", __FILE__, __LINE__); }
-    rc = ssh_sort_columns(ctx, sig, N, L, ix->ids, &kin, st);
+    rc = ssh_sort_columns_hi(ctx, sig, N, L, ix->ids, &kin, st);
     if (rc) goto fail;
     {
     uint32_t *hist = (uint32_t *)ctx->slot_ptr[SLOT_RS_HIST];

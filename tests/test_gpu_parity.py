@@ -485,3 +485,56 @@ def test_config3_full_size_properties(cuda):
         assert r.distances == sorted(r.distances)
         d2 = dtw_exact_pairs(idx, Q, np.full(len(r.ids), i), np.asarray(r.ids))
         assert np.sqrt(d2).tolist() == r.distances
+
+
+def _device_tables(sig_u64):
+    """ssh_index_build over a given signature matrix -> host CSR per table."""
+    import torch
+
+    from paper_1610_07328_b200 import _native as nat
+    from paper_1610_07328_b200.index import _stream_ptr
+
+    N, L = sig_u64.shape
+    ctx = _stage_ctx(params(), 512)
+    lib = nat.lib()
+    sig = torch.from_numpy(np.ascontiguousarray(sig_u64).view(np.int64)).cuda()
+    h = ctypes.c_void_p()
+    nat.check(lib.ssh_index_build(ctx.handle, nat.ptr(sig), N, 0, ctypes.byref(h), _stream_ptr(0)))
+    out = []
+    try:
+        for j in range(L):
+            nb = ctypes.c_int64()
+            nat.check(lib.ssh_index_num_buckets(h, j, ctypes.byref(nb)))
+            keys = np.empty(nb.value, dtype=np.uint64)
+            offsets = np.empty(nb.value + 1, dtype=np.int64)
+            ids = np.empty(N, dtype=np.int64)
+            nat.check(lib.ssh_index_export(h, j, nat.ptr(keys), nat.ptr(offsets), nat.ptr(ids), _stream_ptr(0)))
+            out.append((keys, offsets, ids))
+    finally:
+        lib.ssh_index_destroy(h)
+    return out
+
+
+@pytest.mark.parametrize("kind", ["few_hi_long_runs", "pair_runs_over_capacity", "random"])
+def test_tables_high_half_collisions(cuda, kind):
+    """The bucket tables sort on the high 32 key bits and fix up runs whose keys
+    share a high half: crafted signatures with long colliding runs, more
+    colliding runs than the fix-up list holds (full-key fallback), and random
+    keys all give the reference's tables (stable argsort, index.py:141-156)."""
+    rng = np.random.default_rng(21)
+    N, L = 40_000, 20
+    if kind == "few_hi_long_runs":
+        hi = rng.integers(0, 3, size=(N, L)).astype(np.uint64)
+        lo = rng.integers(0, 5, size=(N, L)).astype(np.uint64) * np.uint64(0x9E3779B1)
+    elif kind == "pair_runs_over_capacity":
+        hi = (np.arange(N, dtype=np.uint64) // np.uint64(2))[:, None].repeat(L, 1)
+        lo = rng.integers(0, 2, size=(N, L)).astype(np.uint64)
+    else:
+        hi = rng.integers(0, 2**32, size=(N, L), dtype=np.uint64)
+        lo = rng.integers(0, 2**32, size=(N, L), dtype=np.uint64)
+    sig = (hi << np.uint64(32)) | lo
+    got = _device_tables(sig)
+    want = O.tables_from_signatures(sig)
+    for j in range(L):
+        for a, b in zip(got[j], want[j]):
+            assert np.array_equal(a, b), (kind, j)
