@@ -276,6 +276,46 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// byte-packed running max doubling of one padded code array held in
+// registers: lane owns words [lane * WPL, lane * WPL + WPL); a word shifted
+// by 2^l bytes comes from the lane's own registers or, via shuffles, from
+// the next lanes (compile-time offsets).  Words at or past padw are 0
+// (neutral).  Reads the array from shared memory and writes it back.
+template <int WPL>
+__device__ __forceinline__ void env_doubling_regs(uint32_t *arr, int padw, int lev, int lane) {
+    uint32_t v[WPL];
+    const int w0 = lane * WPL;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) v[j] = w0 + j < padw ? arr[w0 + j] : 0u;
+    __syncwarp();
+#pragma unroll
+    for (int l = 0; l < 9; l++) {
+        if (l < lev) {
+            const int d = 1 << l;
+            const int dq = d >> 2;
+            const unsigned sel = (d & 3) ? 0x3210u + 0x1111u * (unsigned)(d & 3) : 0x3210u;
+            uint32_t nv[WPL];
+#pragma unroll
+            for (int j = 0; j < WPL; j++) {
+                // words j + dq and j + dq + 1 of this lane's block (may lie in later lanes)
+                const int k0 = j + dq, k1 = j + dq + 1;
+                const uint32_t s0 = k0 < WPL ? v[k0] : __shfl_down_sync(0xFFFFFFFFu, v[k0 % WPL], k0 / WPL);
+                const uint32_t s1 = k1 < WPL ? v[k1] : __shfl_down_sync(0xFFFFFFFFu, v[k1 % WPL], k1 / WPL);
+                const uint32_t a0 = (w0 + k0 < padw && lane + k0 / WPL < 32) ? s0 : 0u;
+                const uint32_t a1 = (w0 + k1 < padw && lane + k1 / WPL < 32) ? s1 : 0u;
+                nv[j] = __vmaxu4(v[j], __byte_perm(a0, a1, sel));
+            }
+#pragma unroll
+            for (int j = 0; j < WPL; j++) v[j] = nv[j];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < WPL; j++)
+        if (w0 + j < padw) arr[w0 + j] = v[j];
+    __syncwarp();
+}
+
 struct SumArgs {
     const float *X;
     int64_t N, ld, cstride;
@@ -284,6 +324,7 @@ struct SumArgs {
     uint8_t *codes;
 };
 
+template <int WPL>
 __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
     extern __shared__ __align__(16) unsigned char xsmb[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
@@ -384,32 +425,37 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
         if (lane < 4) a.rec[row * 4 + lane] = reinterpret_cast<const uint4 *>(prec)[lane];
         // running max of the codes and of their complements (= running min) over
         // [t, t + 2^lev) by byte-packed log-step doubling
-        for (int l = 0; l < a.lev; l++) {
-            const int d = 1 << l, dq = d >> 2;
-            const unsigned sel = d & 3 ? 0x3210u + 0x1111u * (unsigned)(d & 3) : 0x3210u;
-            for (int t0 = 0; t0 < padw; t0 += 32 * 8) {
-                uint32_t va[8], vb[8];
+        if (WPL > 0) {
+            env_doubling_regs<(WPL > 0 ? WPL : 1)>(cmx, padw, a.lev, lane);
+            env_doubling_regs<(WPL > 0 ? WPL : 1)>(cmn, padw, a.lev, lane);
+        } else {
+            for (int l = 0; l < a.lev; l++) {
+                const int d = 1 << l, dq = d >> 2;
+                const unsigned sel = d & 3 ? 0x3210u + 0x1111u * (unsigned)(d & 3) : 0x3210u;
+                for (int t0 = 0; t0 < padw; t0 += 32 * 8) {
+                    uint32_t va[8], vb[8];
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int t = t0 + u * 32 + lane;
-                    if (t < padw) {
-                        const int q0 = t + dq;
-                        const uint32_t a0 = q0 < padw ? cmx[q0] : 0u, a1 = q0 + 1 < padw ? cmx[q0 + 1] : 0u;
-                        const uint32_t b0 = q0 < padw ? cmn[q0] : 0u, b1 = q0 + 1 < padw ? cmn[q0 + 1] : 0u;
-                        va[u] = __vmaxu4(cmx[t], __byte_perm(a0, a1, sel));
-                        vb[u] = __vmaxu4(cmn[t], __byte_perm(b0, b1, sel));
+                    for (int u = 0; u < 8; u++) {
+                        const int t = t0 + u * 32 + lane;
+                        if (t < padw) {
+                            const int q0 = t + dq;
+                            const uint32_t a0 = q0 < padw ? cmx[q0] : 0u, a1 = q0 + 1 < padw ? cmx[q0 + 1] : 0u;
+                            const uint32_t b0 = q0 < padw ? cmn[q0] : 0u, b1 = q0 + 1 < padw ? cmn[q0 + 1] : 0u;
+                            va[u] = __vmaxu4(cmx[t], __byte_perm(a0, a1, sel));
+                            vb[u] = __vmaxu4(cmn[t], __byte_perm(b0, b1, sel));
+                        }
                     }
-                }
-                __syncwarp();
+                    __syncwarp();
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int t = t0 + u * 32 + lane;
-                    if (t < padw) {
-                        cmx[t] = va[u];
-                        cmn[t] = vb[u];
+                    for (int u = 0; u < 8; u++) {
+                        const int t = t0 + u * 32 + lane;
+                        if (t < padw) {
+                            cmx[t] = va[u];
+                            cmn[t] = vb[u];
+                        }
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
         // envelope codes of samples i4..i4+3: window [i - r, i + r] = padded
@@ -485,11 +531,16 @@ int ssh_launch_summaries_rows(ssh_ctx *ctx, ssh_index *ix, const float *X, int64
     SumArgs a{X, n, ld, ix->cstride, m, r, g.lev, g.pad, g.seg, g.nseg, g.mp, g.warp_bytes,
               (uint4 *)ix->rec + r0 * 4, ix->codes + r0 * ix->cstride};
     const size_t smem = (size_t)g.warp_bytes * g.nwb;
-    SSH_CUDA(cudaFuncSetAttribute(summaries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // envelope doubling in registers when the padded array fits 32 x WPL words
+    const int padw = g.pad / 4;
+    auto kern = padw <= 32 * 6 ? summaries_kernel<6>
+                : padw <= 32 * 12 ? summaries_kernel<12>
+                : padw <= 32 * 24 ? summaries_kernel<24> : summaries_kernel<0>;
+    SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, summaries_kernel, 32 * g.nwb, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * g.nwb, smem);
     const int grid = (int)std::min<int64_t>((n + g.nwb - 1) / g.nwb, (int64_t)ctx->num_sms * std::max(1, per_sm));
-    summaries_kernel<<<grid, 32 * g.nwb, smem, st>>>(a);
+    kern<<<grid, 32 * g.nwb, smem, st>>>(a);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
