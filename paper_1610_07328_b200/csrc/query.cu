@@ -158,6 +158,55 @@ __global__ void bitmap_kernel(const uint32_t *__restrict__ ids, const uint64_t *
     }
 }
 
+
+// membership bitmap, one CTA per (query, slice of <= BM_SLICE_WORDS words):
+// the slice is built with shared-memory atomics from the sub-range of each
+// probed bucket that falls into it (bucket ids are ascending, so two binary
+// searches per bucket bound it), then stored with coalesced writes
+#define BM_SLICE_WORDS 32768  // 1M rows, 128 KB of shared memory
+__global__ void __launch_bounds__(1024)
+bitmap_smem_kernel(const uint32_t *__restrict__ ids, const uint64_t *__restrict__ bstart,
+                   const uint32_t *__restrict__ blen, int L, int64_t N, int64_t NW, uint32_t *__restrict__ bitmap) {
+    extern __shared__ uint32_t bmsm[];
+    __shared__ uint32_t slo[64], shi[64];
+    const int q = blockIdx.y;
+    const int64_t w0 = (int64_t)blockIdx.x * BM_SLICE_WORDS;
+    const int nw = (int)min((int64_t)BM_SLICE_WORDS, NW - w0);
+    const uint32_t r0 = (uint32_t)(w0 * 32), r1 = (uint32_t)min(N, (w0 + nw) * 32);
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) bmsm[w] = 0u;
+    if (threadIdx.x < L) {
+        const int j = threadIdx.x;
+        const uint32_t len = blen[(int64_t)q * L + j];
+        const uint32_t *b = ids + bstart[(int64_t)q * L + j];
+        uint32_t lo = 0, hi = len;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (b[mid] < r0) lo = mid + 1; else hi = mid;
+        }
+        slo[j] = lo;
+        hi = len;
+        uint32_t l2 = lo;
+        while (l2 < hi) {
+            const uint32_t mid = (l2 + hi) >> 1;
+            if (b[mid] < r1) l2 = mid + 1; else hi = mid;
+        }
+        shi[j] = l2;
+    }
+    __syncthreads();
+    for (int j = 0; j < L; j++) {
+        const uint32_t a = slo[j], e = shi[j];
+        if (a >= e) continue;
+        const uint32_t *b = ids + bstart[(int64_t)q * L + j];
+        for (uint32_t i = a + threadIdx.x; i < e; i += blockDim.x) {
+            const uint32_t id = b[i] - r0;
+            atomicOr(&bmsm[id >> 5], 1u << (id & 31));
+        }
+    }
+    __syncthreads();
+    uint32_t *out = bitmap + (int64_t)q * NW + w0;
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) out[w] = bmsm[w];
+}
+
 // |R| per query; with fallback, an empty R becomes the whole shard
 __global__ void count_kernel(uint32_t *__restrict__ bitmap, int64_t NW, int64_t N,
                              const uint32_t *__restrict__ blen, int L, int fallback,
@@ -2424,9 +2473,17 @@ static int probe_and_bitmap(const ssh_index *ix, const uint64_t *qsig, int nq, i
     probe_kernel<<<ssh_div_up((int64_t)nq * L, 128), 128, 0, st>>>(
         qsig, nq, L, ix->keys, ix->offsets, ix->d_nb, ix->d_kbase, N, bstart, blen);
     SSH_CHECK_LAUNCH();
-    SSH_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)nq * NW, st));
-    dim3 g((unsigned)(nq * L), 8);
-    bitmap_kernel<<<g, 256, 0, st>>>(ix->ids, bstart, blen, L, NW, bitmap);
+    if (L <= 64) {
+        const int sw = (int)std::min<int64_t>(NW, BM_SLICE_WORDS);
+        SSH_CUDA(cudaFuncSetAttribute(bitmap_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(uint32_t) * sw)));
+        dim3 g((unsigned)ssh_div_up(NW, BM_SLICE_WORDS), (unsigned)nq);
+        bitmap_smem_kernel<<<g, 1024, sizeof(uint32_t) * sw, st>>>(ix->ids, bstart, blen, L, N, NW, bitmap);
+    } else {
+        SSH_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)nq * NW, st));
+        dim3 g((unsigned)(nq * L), 8);
+        bitmap_kernel<<<g, 256, 0, st>>>(ix->ids, bstart, blen, L, NW, bitmap);
+    }
     SSH_CHECK_LAUNCH();
     count_kernel<<<nq, 256, 0, st>>>(bitmap, NW, N, blen, L, fallback, n_cand, is_fb);
     SSH_CHECK_LAUNCH();
