@@ -1833,6 +1833,58 @@ __global__ void qpad_kernel(const float *__restrict__ Q, int m, int R, int YP, f
     }
 }
 
+
+// Exact f64 rescoring, register band (radius R) with 4 rows interleaved per
+// lane (one-cell lag, as in the fp32 kernels): the reference recurrence
+// d = x - y; d = d * d; c = d + min(diag, up, left) (dtw.py:100-113) with
+// _rn intrinsics, out-of-band / out-of-range cells +inf (the query is padded
+// with +inf, so such cells evaluate to +inf exactly).  One query per block row.
+template <int R>
+__global__ void __launch_bounds__(128)
+dtw64r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, const uint32_t *__restrict__ list,
+              int64_t list_stride, const int *__restrict__ list_cnt, double *__restrict__ out) {
+    constexpr int NB = 2 * R + 1;
+    extern __shared__ __align__(16) double ysm[];
+    const int q = blockIdx.y;
+    const int cnt = list_cnt[q];
+    if ((int)(blockIdx.x * blockDim.x) >= cnt) return;
+    const int YP = m + 2 * R + 8;
+    for (int t = threadIdx.x; t < YP; t += blockDim.x) {
+        const int j = t - R;
+        ysm[t] = (j >= 0 && j < m) ? (double)Q[(int64_t)q * m + j] : (double)INFINITY;
+    }
+    __syncthreads();
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= cnt) return;
+    const float4 *xp = reinterpret_cast<const float4 *>(X + (int64_t)list[(int64_t)q * list_stride + e] * m);
+    double band[NB];
+#pragma unroll
+    for (int k = 0; k < NB; k++) band[k] = k == R ? 0.0 : (double)INFINITY;
+    for (int i0 = 0; i0 < m; i0 += 4) {
+        const float4 xv = __ldg(xp + (i0 >> 2));
+        const double xr[4] = {(double)xv.x, (double)xv.y, (double)xv.z, (double)xv.w};
+        double lft[4] = {(double)INFINITY, (double)INFINITY, (double)INFINITY, (double)INFINITY};
+        const double *yp = ysm + i0;
+#pragma unroll
+        for (int st = 0; st < NB + 3; st++) {
+            const double yv = yp[st];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int k = st - u;
+                if (k >= 0 && k < NB) {
+                    const double up = (k + 1 < NB) ? band[k + 1] : (double)INFINITY;
+                    double d = __dsub_rn(xr[u], yv);
+                    d = __dmul_rn(d, d);
+                    const double c = __dadd_rn(d, fmin(fmin(up, lft[u]), band[k]));
+                    band[k] = c;
+                    lft[u] = c;
+                }
+            }
+        }
+    }
+    out[(int64_t)q * list_stride + e] = band[R];
+}
+
 // ------------------------------------------------------------ fp64 DTW
 // exact reference arithmetic (dtw.py:100-113): d = x - y; d = d*d; c = d + min(...)
 __global__ void dtw64_kernel(const float *__restrict__ X, int m, int r, const float *__restrict__ Q,
@@ -2428,13 +2480,34 @@ static int launch_dtw_pooled(ssh_ctx *ctx, const DtwCommon &C, const int *act, c
     return SSH_OK;
 }
 
+template <int R>
+static int launch_dtw64r(const float *X, int m, const float *Q, const uint32_t *list, int64_t stride,
+                         const int *cnt, int maxcnt, double *out, int nq, cudaStream_t st) {
+    const size_t smem = sizeof(double) * (size_t)(m + 2 * R + 8);
+    SSH_CUDA(cudaFuncSetAttribute(dtw64r_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((unsigned)ssh_div_up(maxcnt, 128), (unsigned)nq);
+    dtw64r_kernel<R><<<grid, 128, smem, st>>>(X, m, Q, list, stride, cnt, out);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
 static int launch_dtw64_list(const float *X, int m, int r, const float *Q, const uint32_t *list,
                              int64_t stride, const int *cnt, int maxcnt, double *out, int nq,
                              cudaStream_t st) {
+    if (maxcnt <= 0) return SSH_OK;
+    if ((m & 3) == 0 && (size_t)(m + 2 * r + 8) * 8 <= 160 * 1024) {
+        switch (r) {
+            case 3: return launch_dtw64r<3>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
+            case 6: return launch_dtw64r<6>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
+            case 13: return launch_dtw64r<13>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
+            case 26: return launch_dtw64r<26>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
+            case 51: return launch_dtw64r<51>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
+            default: break;
+        }
+    }
     size_t smem;
     int t = dtw64_threads(r, &smem);
     SSH_CUDA(cudaFuncSetAttribute(dtw64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (maxcnt <= 0) return SSH_OK;
     dim3 grid((unsigned)ssh_div_up(maxcnt, t), (unsigned)nq);
     dtw64_kernel<<<grid, t, smem, st>>>(X, m, r, Q, nullptr, list, stride, cnt, nullptr, 0, out);
     SSH_CHECK_LAUNCH();
