@@ -17,6 +17,7 @@ host threads) on bounded samples of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import ctypes
 import json
 import os
@@ -173,10 +174,15 @@ def run_ours(args):
     sampler.start()
     launches0 = lib.ssh_launch_count()
     evs = []
+    # the build synchronises with the host twice (bucket counts); a cyclic-GC
+    # pause landing between those points would show up as device idle time
+    gc.collect()
+    gc.disable()
     for _ in range(args.steps):
         ev, last = step()
         evs.append(ev)
     torch.cuda.synchronize()
+    gc.enable()
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()

@@ -693,9 +693,13 @@ extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t 
     if (!bits || !sig) return SSH_ERR_OOM;
     ssh_index summ;
     summ.N = N;
+    // allocate on the caller's stream (where earlier indexes were freed, so the
+    // pool reuses their memory), then summarise on the side stream
+    int rc = ssh_alloc_summaries(ctx, &summ, N, st);
+    if (rc) return rc;
     SSH_CUDA(cudaEventRecord(ctx->ev_fork, st));
     SSH_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    int rc = ssh_launch_summaries(ctx, &summ, X, N, ld, ctx->side);
+    rc = ssh_launch_summaries_rows(ctx, &summ, X, 0, N, ld, ctx->side);
     if (rc == SSH_OK) rc = cudaEventRecord(ctx->ev_join, ctx->side) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
     if (rc == SSH_OK) rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st);
     if (rc == SSH_OK)
