@@ -275,6 +275,16 @@ def _time(fn, reps=5):
     return statistics.median(ts)
 
 
+def _ncu_traffic(kernel):
+    """DRAM bytes (read + write) of all launches of `kernel` in one configs[1]
+    build + 1000-query batch, from the committed ncu capture (profiles/), or None."""
+    try:
+        d = json.loads((Path(__file__).resolve().parent / "profiles" / "r01" / "traffic_cfg1.json").read_text())
+        return d["kernels"][kernel]["dram_bytes"]
+    except Exception:
+        return None
+
+
 def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     import torch
 
@@ -347,9 +357,10 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     if lb_ms > 0:
         res["q3"]["roofline"] = dict(
             bound="hbm", achieved=lb_bytes / lb_ms / 1e6, peak=hbm, unit="GB/s",
-            frac=lb_bytes / lb_ms / 1e6 / hbm, traffic=None, kernel="wave_lb_kernel",
-            note="algorithmic bytes = candidate row (f32) and envelope (fp16x2) chunks the "
-                 "LB_Kim/LB_Keogh/LB_Keogh2 cascade actually reads before abandoning (device counter)")
+            frac=lb_bytes / lb_ms / 1e6 / hbm, traffic=_ncu_traffic("wave_lb_kernel"), kernel="wave_lb_kernel",
+            note="algorithmic bytes = u8 envelope-code and sample-code blocks the LB_Keogh2/LB_Keogh "
+                 "cascade reads before abandoning (device counter, per 1000-query batch); traffic = "
+                 "ncu dram bytes of the same launches (profiles/r01/traffic_cfg1.json)")
     res["wave_lb_bytes"] = lb_bytes
     res["wave_lb_paa_skips"] = prof[10]
     res["wave_lb_keogh_prunes"] = prof[11]
