@@ -134,6 +134,17 @@ int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, int64_t
 int ssh_build_index_host(ssh_ctx *ctx, const float *X_host, int64_t N, int64_t ld, int64_t id_base,
                          float *X_dev, uint64_t *sig_out, ssh_index **out, void *stream);
 int ssh_index_destroy(ssh_index *idx);
+/* An index without bucket tables over N series (summaries only): queries on
+ * it search the whole shard exactly — exact_search (dtw.py:293-326). */
+int ssh_index_create_bare(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, int64_t id_base,
+                          ssh_index **out, void *stream);
+/* Host-only: parse the per-table section of an SSHI index file
+ * (index.py:279-396, load_index) starting at byte `off` into the signature
+ * matrix sig u64[N][L] (signatures[ids, j] = key), checking ids in [0, N) and
+ * every id exactly once per table.  Returns 0, 1 (truncated) or 2 (invalid)
+ * with a message in msg; *end_off = offset after the last table. */
+int ssh_sshi_parse_tables(const uint8_t *buf, int64_t len, int64_t off, int32_t L, int64_t N, uint64_t *sig,
+                          int64_t *end_off, char *msg, int32_t msg_len);
 int ssh_index_num_buckets(const ssh_index *idx, int table, int64_t *n_buckets);
 int64_t ssh_index_size(const ssh_index *idx);
 /* Copy table `table` to HOST arrays: keys u64[nb], offsets i64[nb+1],
@@ -166,6 +177,8 @@ int ssh_probe(ssh_ctx *ctx, const ssh_index *idx, const uint64_t *qsig, int32_t 
 #define SSH_QUERY_FALLBACK_ON_EMPTY 1 /* empty R -> exact search over the shard
                                          (query_index(fallback_on_empty=True),
                                          index.py:239-243) */
+#define SSH_QUERY_EXACT 2             /* R = the whole shard, no probe (exact_search,
+                                         dtw.py:293-326); implied for bare indexes */
 int ssh_query_batch(ssh_ctx *ctx, const ssh_index *idx, const float *X, const float *Q,
                     int32_t nq, int32_t k, int32_t flags, int64_t *ids, double *d2,
                     int32_t *n_out, int64_t *n_cand, int64_t *counters, int32_t *status,

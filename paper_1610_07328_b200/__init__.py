@@ -27,13 +27,19 @@ from .index import (
     SshIndex,
     SshParams,
     WarpingParams,
+    SearchResult,
     build_index,
     compute_signatures,
+    exact_search,
+    exact_search_batch,
+    index_from_signatures,
     num_sketch_bits,
     probe_candidates,
     query_index,
     query_index_batch,
     query_signature,
 )
+
+from .persist import file_checksum, load_dataset, load_index, read_index_file, save_dataset, save_index
 
 __version__ = "0.1.0"

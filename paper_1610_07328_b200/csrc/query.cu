@@ -2540,9 +2540,17 @@ static int qsig_batch(ssh_ctx *ctx, const float *Q, int nq, uint64_t *qsig, uint
 
 static int probe_and_bitmap(const ssh_index *ix, const uint64_t *qsig, int nq, int fallback,
                             uint64_t *bstart, uint32_t *blen, uint32_t *bitmap, long long *n_cand,
-                            int *is_fb, cudaStream_t st) {
+                            int *is_fb, cudaStream_t st, bool exact = false) {
     const int L = ix->L;
     const int64_t N = ix->N, NW = (N + 31) / 32;
+    if (exact || !ix->keys) {
+        // exact search: no probe; every query's R is the whole shard (count_kernel fills it)
+        SSH_CUDA(cudaMemsetAsync(blen, 0, sizeof(uint32_t) * (size_t)nq * L, st));
+        SSH_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)nq * NW, st));
+        count_kernel<<<nq, 256, 0, st>>>(bitmap, NW, N, blen, L, 1, n_cand, is_fb);
+        SSH_CHECK_LAUNCH();
+        return SSH_OK;
+    }
     probe_kernel<<<ssh_div_up((int64_t)nq * L, 128), 128, 0, st>>>(
         qsig, nq, L, ix->keys, ix->offsets, ix->d_nb, ix->d_kbase, N, bstart, blen);
     SSH_CHECK_LAUNCH();
@@ -2566,6 +2574,7 @@ static int probe_and_bitmap(const ssh_index *ix, const uint64_t *qsig, int nq, i
 extern "C" int ssh_probe(ssh_ctx *ctx, const ssh_index *ix, const uint64_t *qsig, int32_t nq,
                          uint32_t *bitmap, int64_t *n_cand, void *stream) {
     SSH_REQUIRE(ctx && ix && qsig && bitmap && n_cand, SSH_ERR_INVALID, "ssh_probe: NULL argument");
+    SSH_REQUIRE(ix->keys != nullptr, SSH_ERR_STATE, "ssh_probe: index has no bucket tables");
     SSH_REQUIRE(nq >= 0 && ix->L == ctx->p.L, SSH_ERR_INVALID, "ssh_probe: bad arguments");
     if (nq == 0) return SSH_OK;
     SSH_CUDA(cudaSetDevice(ctx->device));
@@ -2614,6 +2623,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     const int WCAP = std::max(W0, 16384);
     const int KCAP = 4096 + 4 * k;
     const int fallback = (flags & SSH_QUERY_FALLBACK_ON_EMPTY) ? 1 : 0;
+    const bool exact = (flags & SSH_QUERY_EXACT) != 0 || !ix->keys;
     // query chunk: membership bitmaps <= 1 GiB; within a chunk, sub-ranges of
     // queries whose actual member lists (16 B per member) fit SSH_MEMBER_BUDGET
     int64_t qc64 = std::min<int64_t>(nq, 32768);
@@ -2646,7 +2656,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         pf.end(0);
         // K6: probe + candidate bitmap; member counts -> CSR offsets
         pf.begin();
-        rc = probe_and_bitmap(ix, B.qsig, nc, fallback, B.bstart, B.blen, bitmap, ncand, B.isfb, st);
+        rc = probe_and_bitmap(ix, B.qsig, nc, fallback, B.bstart, B.blen, bitmap, ncand, B.isfb, st, exact);
         if (rc) return rc;
         envelope_kernel<<<nc, 256, 2 * m * sizeof(float), st>>>(Qc, m, r, ix->seg, nseg, B.U, B.Lo, B.Useg, B.Lseg);
         SSH_CHECK_LAUNCH();

@@ -631,10 +631,10 @@ extern "C" int ssh_index_destroy(ssh_index *ix) {
     // stream-ordered frees on the legacy stream: memory returns to the pool
     // without a device-wide synchronisation
     cudaStream_t st = 0;
-    cudaFreeAsync(ix->keys, st);
-    cudaFreeAsync(ix->offsets, st);
-    cudaFreeAsync(ix->ids, st);
-    cudaFreeAsync(ix->d_nb, st);
+    if (ix->keys) cudaFreeAsync(ix->keys, st);
+    if (ix->offsets) cudaFreeAsync(ix->offsets, st);
+    if (ix->ids) cudaFreeAsync(ix->ids, st);
+    if (ix->d_nb) cudaFreeAsync(ix->d_nb, st);
     if (ix->rec) cudaFreeAsync(ix->rec, st);
     if (ix->codes) cudaFreeAsync(ix->codes, st);
     delete[] ix->h_nb;
@@ -773,5 +773,28 @@ extern "C" int ssh_build_index_host(ssh_ctx *ctx, const float *X_host, int64_t N
     (*out)->nseg = summ.nseg;
     (*out)->mp = summ.mp;
     (*out)->cstride = summ.cstride;
+    return SSH_OK;
+}
+
+// An index without bucket tables (exact search over the whole shard): the
+// series summaries only.  ssh_query_batch treats every query's R as the shard.
+extern "C" int ssh_index_create_bare(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, int64_t id_base,
+                                     ssh_index **out, void *stream) {
+    SSH_REQUIRE(ctx && X && out, SSH_ERR_INVALID, "ssh_index_create_bare: NULL argument");
+    SSH_REQUIRE(ctx->have_params, SSH_ERR_STATE, "ssh_index_create_bare: params not set");
+    SSH_REQUIRE(N >= 1 && N < (int64_t)0xFFFFFFFF && ld >= ctx->p.m, SSH_ERR_INVALID,
+                "ssh_index_create_bare: bad shape N=%lld ld=%lld", (long long)N, (long long)ld);
+    SSH_CUDA(cudaSetDevice(ctx->device));
+    ssh_index *ix = new ssh_index();
+    ix->L = ctx->p.L;
+    ix->N = N;
+    ix->id_base = id_base;
+    ix->device = ctx->device;
+    int rc = ssh_launch_summaries(ctx, ix, X, N, ld, (cudaStream_t)stream);
+    if (rc != SSH_OK) {
+        ssh_index_destroy(ix);
+        return rc;
+    }
+    *out = ix;
     return SSH_OK;
 }

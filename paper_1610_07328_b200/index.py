@@ -377,6 +377,105 @@ def build_index(dataset, params: SshParams, normalized: bool = True, threads: in
                     device=dev, X=X, sig_dev=sig, id_base=id_base, _tables=tables)
 
 
+def index_from_signatures(dataset, params: SshParams, sig, normalized: bool = True, device=None,
+                          id_base: int = 0, filter_weights=None, filter_seed=None) -> SshIndex:
+    """An index over `dataset` whose (N, d) uint64 signatures are already known
+    (load_index): device tables from the signatures (ssh_index_build) and the
+    rerank summaries of the series (ssh_index_summarize)."""
+    if not isinstance(dataset, Dataset):
+        dataset = Dataset(values=dataset)
+    params.validate_for_length(dataset.length)
+    dev = _device_index(device)
+    ctx = get_context(dev, params, dataset.length)
+    if filter_weights is not None and not np.array_equal(np.asarray(filter_weights, dtype=np.float64),
+                                                         ctx.filter.weights):
+        raise ConfigError("index filter weights differ from make_filter(W, seed)")
+    if filter_seed is not None and int(filter_seed) != ctx.filter.seed:
+        raise ConfigError(f"index filter seed {filter_seed} differs from params.seed {ctx.filter.seed}")
+    torch = _torch()
+    X = _as_device_f32(dataset.values, dev)
+    sig_h = np.ascontiguousarray(np.asarray(sig, dtype=np.uint64))
+    if sig_h.shape != (X.shape[0], params.d):
+        raise ConfigError(f"signatures shape {sig_h.shape} != ({X.shape[0]}, {params.d})")
+    sig_d = torch.from_numpy(sig_h.view(np.int64)).to(X.device)
+    handle = ctypes.c_void_p()
+    L = nat.lib()
+    nat.check(L.ssh_index_build(ctx.handle, nat.ptr(sig_d), int(X.shape[0]), int(id_base),
+                                ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_build")
+    tables = _TablesHandle(handle)
+    nat.check(L.ssh_index_summarize(ctx.handle, handle, nat.ptr(X), int(X.stride(0)), _stream_ptr(dev)),
+              "ssh_index_summarize")
+    return SshIndex(params=params, filter=ctx.filter, dataset=dataset, normalized=normalized,
+                    device=dev, X=X, sig_dev=sig_d, id_base=id_base, _tables=tables)
+
+
+@dataclass
+class SearchResult:
+    """exact_search result (dtw.py:75-81)."""
+
+    ids: list
+    distances: list
+    stats: SearchStats
+    warning: str | None = None
+
+
+def exact_search_batch(dataset, Q, k: int, params: WarpingParams = WarpingParams(), device=None) -> list:
+    """exact_search (dtw.py:293-326) for every row of Q: the exact top-k by
+    (DTW^2, id) over the whole dataset, on the device (an index without bucket
+    tables; every query's candidate set is the full shard)."""
+    if not isinstance(dataset, Dataset):
+        dataset = Dataset(values=dataset)
+    Qh = Q.detach().double().cpu().numpy() if _is_torch(Q) else np.asarray(Q, dtype=np.float64)
+    if Qh.ndim == 1:
+        Qh = Qh.reshape(1, -1)
+    if dataset.length != Qh.shape[1]:
+        raise ValueError(f"query length {Qh.shape[1]} does not match dataset length {dataset.length}")
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    warning = None
+    if k > dataset.n_series:
+        warning = f"k={k} exceeds dataset size {dataset.n_series}; returning all series"
+        k = dataset.n_series
+    sp = SshParams(W=min(30, dataset.length), delta=5, n=1, band=params.band)
+    dev = _device_index(device)
+    ctx = get_context(dev, sp, dataset.length)
+    torch = _torch()
+    X = _as_device_f32(dataset.values, dev)
+    handle = ctypes.c_void_p()
+    L = nat.lib()
+    nat.check(L.ssh_index_create_bare(ctx.handle, nat.ptr(X), int(X.shape[0]), int(X.stride(0)), 0,
+                                      ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_create_bare")
+    bare = _TablesHandle(handle)
+    Qd = _as_device_f32(Qh, dev)
+    nq = int(Qd.shape[0])
+    ids = torch.empty((nq, k), dtype=torch.int64, device=X.device)
+    d2 = torch.empty((nq, k), dtype=torch.float64, device=X.device)
+    n_out = torch.empty(nq, dtype=torch.int32, device=X.device)
+    n_cand = torch.empty(nq, dtype=torch.int64, device=X.device)
+    counters = torch.empty((nq, 5), dtype=torch.int64, device=X.device)
+    status = torch.empty(nq, dtype=torch.int32, device=X.device)
+    nat.check(L.ssh_query_batch(ctx.handle, bare.handle, nat.ptr(X), nat.ptr(Qd), nq, k, nat.SSH_QUERY_EXACT,
+                                nat.ptr(ids), nat.ptr(d2), nat.ptr(n_out), nat.ptr(n_cand), nat.ptr(counters),
+                                nat.ptr(status), _stream_ptr(dev)), "ssh_query_batch")
+    ids, d2, n_out, counters = ids.cpu().numpy(), d2.cpu().numpy(), n_out.cpu().numpy(), counters.cpu().numpy()
+    del bare
+    out = []
+    for i in range(nq):
+        n = int(n_out[i])
+        c = counters[i]
+        stats = SearchStats(candidates=dataset.n_series, kim_pruned=int(c[0]), keogh_pruned=int(c[1]),
+                            keogh2_pruned=int(c[2]), dtw_computed=int(c[3]), dtw_abandoned=int(c[4]))
+        out.append(SearchResult(ids=[int(v) for v in ids[i, :n]],
+                                distances=[float(v) for v in np.sqrt(d2[i, :n])], stats=stats, warning=warning))
+    return out
+
+
+def exact_search(dataset, q, k: int, params: WarpingParams = WarpingParams(), device=None) -> SearchResult:
+    """dtw.py:293-326 on the device."""
+    qv = q.values if isinstance(q, TimeSeries) else q
+    return exact_search_batch(dataset, qv, k, params, device)[0]
+
+
 def compute_signatures(values, params: SshParams, weights=None, threads: int = 1, device=None):
     """(N, d) uint64 signature matrix (index.py:123-138, with the K fold)."""
     ds = values if isinstance(values, Dataset) else Dataset(values=values)

@@ -204,6 +204,30 @@ def empty_candidates_fixture():
                 fallback_status=r1.status, fallback_ids=r1.ids, fallback_distances=r1.distances)
 
 
+def persist_fixture():
+    """save_index / save_dataset bytes of the reference (index.py:287-310,
+    core.py:181-194): SHA-256 of the SSHI file and its f64le sidecar for a K=1
+    index over rw512[:200] saved as 'idx.sshi', and of the CSV of 5 rows."""
+    import tempfile
+
+    from sshts.core import save_dataset
+
+    X, Q, _, band = case_data("rw512")
+    params = sidx.SshParams(band=band, **SSH)
+    ds = Dataset(values=X[:200].astype(np.float64))
+    index = sidx.build_index(ds, params)
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "idx.sshi"
+        sidx.save_index(index, p)
+        idx_sha = hashlib.sha256(p.read_bytes()).hexdigest()
+        side_sha = hashlib.sha256((Path(td) / "idx.sshi.sshd").read_bytes()).hexdigest()
+        idx_len = len(p.read_bytes())
+        c = Path(td) / "five.csv"
+        save_dataset(Dataset(values=X[:5].astype(np.float64)), c, fmt="csv")
+        csv_sha = hashlib.sha256(c.read_bytes()).hexdigest()
+    return dict(n=200, index_sha256=idx_sha, index_bytes=idx_len, sidecar_sha256=side_sha, csv5_sha256=csv_sha)
+
+
 def main():
     out = dict(ssh=SSH, numpy=np.__version__, cases={})
     for name in CASES:
@@ -213,6 +237,7 @@ def main():
     out["dtw"] = dtw_fixture()
     out["spec"] = spec_fixture()
     out["empty"] = empty_candidates_fixture()
+    out["persist"] = persist_fixture()
     (HERE / "golden.json").write_text(json.dumps(out, indent=None, separators=(",", ":")))
     print("wrote", HERE / "golden.json")
 

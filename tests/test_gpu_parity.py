@@ -538,3 +538,50 @@ def test_tables_high_half_collisions(cuda, kind):
     for j in range(L):
         for a, b in zip(got[j], want[j]):
             assert np.array_equal(a, b), (kind, j)
+
+
+def test_save_index_bytes_and_round_trip(cuda, golden, tmp_path):
+    """save_index from the device CSR is byte-identical to the reference's file
+    (K=1); load_index rebuilds an index with the same signatures, tables and
+    query results; K=4 round-trips through version 2."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw512")
+    X200 = X[:200].astype(np.float64)
+    idx = ssh.build_index(ssh.Dataset(X200), params(band, K=1))
+    ssh.save_index(idx, tmp_path / "idx.sshi")
+    data = (tmp_path / "idx.sshi").read_bytes()
+    assert hashlib.sha256(data).hexdigest() == golden["persist"]["index_sha256"]
+    back = ssh.load_index(tmp_path / "idx.sshi")
+    assert np.array_equal(back.signatures, idx.signatures)
+    for j in (0, 7, 19):
+        for a, b in zip(back.table_csr(j), idx.table_csr(j)):
+            assert np.array_equal(a, b)
+    r1 = ssh.query_index_batch(idx, Q, 10)
+    r2 = ssh.query_index_batch(back, Q, 10)
+    assert [r.ids for r in r1] == [r.ids for r in r2]
+    assert [r.distances for r in r1] == [r.distances for r in r2]
+    idx4 = ssh.build_index(ssh.Dataset(X200), params(band, K=4))
+    ssh.save_index(idx4, tmp_path / "k4.sshi")
+    back4 = ssh.load_index(tmp_path / "k4.sshi")
+    assert back4.params.K == 4 and np.array_equal(back4.signatures, idx4.signatures)
+    assert [r.ids for r in ssh.query_index_batch(back4, Q, 10)] == [r.ids for r in ssh.query_index_batch(idx4, Q, 10)]
+
+
+@pytest.mark.parametrize("name", ["rw512", "rw1024"])
+def test_exact_search_vs_oracle(cuda, name):
+    """exact_search (dtw.py:293-326) on the device == the oracle's brute-force
+    (d2, id) top-k over every series (bench.py:45-60)."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data(name)
+    X = X[:600]
+    res = ssh.exact_search_batch(ssh.Dataset(X), Q[:6], 10, ssh.WarpingParams(band))
+    r = O.radius(band, X.shape[1])
+    for i, rr in enumerate(res):
+        ids, d2 = O.brute_force_topk_over(X, np.arange(X.shape[0]), Q[i], r, 10)
+        assert rr.ids == ids.tolist(), i
+        assert rr.distances == np.sqrt(d2).tolist(), i
+        assert rr.stats.candidates == X.shape[0]
+    one = ssh.exact_search(ssh.Dataset(X[:5]), Q[0], 9, ssh.WarpingParams(band))
+    assert one.warning and len(one.ids) == 5
