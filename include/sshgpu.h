@@ -138,6 +138,14 @@ int ssh_index_destroy(ssh_index *idx);
  * it search the whole shard exactly — exact_search (dtw.py:293-326). */
 int ssh_index_create_bare(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, int64_t id_base,
                           ssh_index **out, void *stream);
+/* make_dataset (core.py:162-169) on the device: windows of length t every
+ * `stride` samples of the f64 recording rec[len] (stride 1 = the reference's
+ * extract_subsequences, core.py:138-146), z-normalised per window exactly as
+ * numpy's float64 mean/std (z_normalize_dataset, core.py:127-135) when
+ * normalize != 0; written as f32 (out32) and/or f64 (out64) [count][t] with
+ * count = (len - t) / stride + 1. */
+int ssh_windows(const double *rec, int64_t len, int32_t t, int64_t stride, int32_t normalize, float *out32,
+                double *out64, int64_t *count, void *stream);
 /* Host-only: parse the per-table section of an SSHI index file
  * (index.py:279-396, load_index) starting at byte `off` into the signature
  * matrix sig u64[N][L] (signatures[ids, j] = key), checking ids in [0, N) and

@@ -40,6 +40,7 @@ from .index import (
     query_signature,
 )
 
+from .pipeline import extract_subsequences, make_dataset
 from .persist import file_checksum, load_dataset, load_index, read_index_file, save_dataset, save_index
 
 __version__ = "0.1.0"

@@ -228,6 +228,21 @@ def persist_fixture():
     return dict(n=200, index_sha256=idx_sha, index_bytes=idx_len, sidecar_sha256=side_sha, csv5_sha256=csv_sha)
 
 
+def windows_fixture():
+    """make_dataset (core.py:162-169) of two seeded random-walk recordings:
+    SHA-256 of the float64 window matrices (t=128 and t=1000; the latter
+    exercises numpy's recursive pairwise split)."""
+    from sshts.core import generate_random_walk, make_dataset
+
+    out = {}
+    for length, t, seed in ((20_000, 128, 7), (6_000, 1000, 8)):
+        rec = generate_random_walk(length, seed)
+        ds = make_dataset(rec, t, normalize=True)
+        out[f"rw{length}_t{t}"] = dict(length=length, t=t, seed=seed, count=ds.n_series,
+                                       sha256=sha(np.ascontiguousarray(ds.values, dtype=np.float64)))
+    return out
+
+
 def main():
     out = dict(ssh=SSH, numpy=np.__version__, cases={})
     for name in CASES:
@@ -238,6 +253,7 @@ def main():
     out["spec"] = spec_fixture()
     out["empty"] = empty_candidates_fixture()
     out["persist"] = persist_fixture()
+    out["windows"] = windows_fixture()
     (HERE / "golden.json").write_text(json.dumps(out, indent=None, separators=(",", ":")))
     print("wrote", HERE / "golden.json")
 

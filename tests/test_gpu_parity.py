@@ -585,3 +585,22 @@ def test_exact_search_vs_oracle(cuda, name):
         assert rr.stats.candidates == X.shape[0]
     one = ssh.exact_search(ssh.Dataset(X[:5]), Q[0], 9, ssh.WarpingParams(band))
     assert one.warning and len(one.ids) == 5
+
+
+@pytest.mark.parametrize("key", ["rw20000_t128", "rw6000_t1000"])
+def test_make_dataset_device_matches_reference(cuda, golden, key):
+    """Windowing + per-window z-normalisation on the device (ssh_windows) is
+    bit-identical to the reference's make_dataset (core.py:162-169), float64;
+    the float32 output is its rounding."""
+    import paper_1610_07328_b200 as ssh
+
+    g = golden["windows"][key]
+    rec = np.cumsum(np.random.default_rng(g["seed"]).standard_normal(g["length"]))  # generate_random_walk
+    d64 = ssh.make_dataset(ssh.TimeSeries(values=rec), g["t"], dtype="float64")
+    v = d64.values.cpu().numpy()
+    assert v.shape == (g["count"], g["t"])
+    assert sha(v) == g["sha256"]
+    d32 = ssh.make_dataset(ssh.TimeSeries(values=rec), g["t"])
+    assert np.array_equal(d32.values.cpu().numpy(), v.astype(np.float32))
+    raw = ssh.make_dataset(ssh.TimeSeries(values=rec), g["t"], normalize=False, stride=7, dtype="float64")
+    assert np.array_equal(raw.values.cpu().numpy(), np.lib.stride_tricks.sliding_window_view(rec, g["t"])[::7])
