@@ -146,6 +146,12 @@ int ssh_index_create_bare(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, i
  * count = (len - t) / stride + 1. */
 int ssh_windows(const double *rec, int64_t len, int32_t t, int64_t stride, int32_t normalize, float *out32,
                 double *out64, int64_t *count, void *stream);
+/* srp_matrix (index.py:420-423): out i8[N][bits] = +1 if X[i] . V[j] >= 0
+ * else -1; V64 f64[bits][m] (default_rng([seed, j]) rows, host-drawn) and
+ * V32 its f32 rounding.  fp32 tiled product with an error bound, fp64
+ * sequential recheck of the undecided signs (counted in *nrecheck). */
+int ssh_srp(const float *X, int64_t N, int32_t m, const float *V32, const double *V64, int32_t bits,
+            int8_t *out, unsigned long long *nrecheck, void *stream);
 /* Host-only: parse the per-table section of an SSHI index file
  * (index.py:279-396, load_index) starting at byte `off` into the signature
  * matrix sig u64[N][L] (signatures[ids, j] = key), checking ids in [0, N) and

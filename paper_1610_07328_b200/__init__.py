@@ -40,6 +40,7 @@ from .index import (
     query_signature,
 )
 
+from .srp import ndcg_at_k, precision_at_k, srp_matrix, srp_signature, srp_vectors
 from .pipeline import extract_subsequences, make_dataset
 from .persist import file_checksum, load_dataset, load_index, read_index_file, save_dataset, save_index
 

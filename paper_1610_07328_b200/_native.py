@@ -20,7 +20,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB_PATH = Path(os.environ["SSH_LIB_PATH"]).resolve() if os.environ.get("SSH_LIB_PATH") else PKG / "libsshgpu.so"
-SOURCES = ["ctx.cu", "sketch.cu", "signature.cu", "tables.cu", "query.cu", "persist.cu", "windows.cu"]
+SOURCES = ["ctx.cu", "sketch.cu", "signature.cu", "tables.cu", "query.cu", "persist.cu", "windows.cu", "srp.cu"]
 
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
@@ -115,6 +115,7 @@ def lib():
             "ssh_dtw_exact": ([P, P, P, P, P, i64, P, P], ctypes.c_int),
             "ssh_index_create_bare": ([P, P, i64, i64, i64, PP, P], ctypes.c_int),
             "ssh_windows": ([P, i64, i32, i64, i32, P, P, ctypes.POINTER(i64), P], ctypes.c_int),
+            "ssh_srp": ([P, i64, i32, P, P, i32, P, P, P], ctypes.c_int),
             "ssh_sshi_parse_tables": ([P, i64, i64, i32, i64, P, ctypes.POINTER(i64), ctypes.c_char_p, i32],
                                       ctypes.c_int),
         }
@@ -132,7 +133,7 @@ EXPORTED = [
     "ssh_num_sketch_bits", "ssh_sketch_words", "ssh_tokens_per_series", "ssh_sketch", "ssh_shingle",
     "ssh_cws", "ssh_signatures", "ssh_index_build", "ssh_build_index", "ssh_build_index_host", "ssh_index_destroy", "ssh_index_num_buckets",
     "ssh_index_size", "ssh_index_export", "ssh_index_summarize", "ssh_probe", "ssh_query_batch", "ssh_dtw_exact",
-    "ssh_index_create_bare", "ssh_sshi_parse_tables", "ssh_windows",
+    "ssh_index_create_bare", "ssh_sshi_parse_tables", "ssh_windows", "ssh_srp",
 ]
 
 

@@ -243,6 +243,23 @@ def windows_fixture():
     return out
 
 
+def srp_fixture():
+    """srp_matrix (index.py:420-423) over rw512[:300] (f64 of the f32 data),
+    64 and 100 bits; precision_at_k / ndcg_at_k on fixed rankings."""
+    from sshts import bench as sbench
+
+    X, _, _, _ = case_data("rw512")
+    V = X[:300].astype(np.float64)
+    out = {}
+    for bits, seed in ((64, 3), (100, 11)):
+        out[f"b{bits}_s{seed}"] = sha(sidx.srp_matrix(V, bits, seed))
+    retrieved = [5, 3, 9, 1, 7, 2, 8]
+    gold = [3, 5, 1, 4, 9, 6, 0]
+    out["metrics"] = {str(k): [sbench.precision_at_k(retrieved, gold, k), sbench.ndcg_at_k(retrieved, gold, k)]
+                      for k in (1, 3, 5, 7)}
+    return out
+
+
 def main():
     out = dict(ssh=SSH, numpy=np.__version__, cases={})
     for name in CASES:
@@ -254,6 +271,7 @@ def main():
     out["empty"] = empty_candidates_fixture()
     out["persist"] = persist_fixture()
     out["windows"] = windows_fixture()
+    out["srp"] = srp_fixture()
     (HERE / "golden.json").write_text(json.dumps(out, indent=None, separators=(",", ":")))
     print("wrote", HERE / "golden.json")
 

@@ -604,3 +604,15 @@ def test_make_dataset_device_matches_reference(cuda, golden, key):
     assert np.array_equal(d32.values.cpu().numpy(), v.astype(np.float32))
     raw = ssh.make_dataset(ssh.TimeSeries(values=rec), g["t"], normalize=False, stride=7, dtype="float64")
     assert np.array_equal(raw.values.cpu().numpy(), np.lib.stride_tricks.sliding_window_view(rec, g["t"])[::7])
+
+
+@pytest.mark.parametrize("bits,seed", [(64, 3), (100, 11)])
+def test_srp_matrix_matches_reference(cuda, golden, bits, seed):
+    """srp_matrix (index.py:420-423) on the device == the reference's int8 signs."""
+    import paper_1610_07328_b200 as ssh
+
+    X, _, _, _ = case_data("rw512")
+    got = ssh.srp_matrix(X[:300], bits, seed)
+    assert got.dtype == np.int8 and got.shape == (300, bits)
+    assert sha(got) == golden["srp"][f"b{bits}_s{seed}"]
+    assert np.array_equal(ssh.srp_signature(X[7], bits, seed), got[7])

@@ -143,3 +143,16 @@ def test_read_index_file_errors(tmp_path):
         ssh.read_index_file(p)
     with pytest.raises(ssh.IndexLoadError, match="no such file"):
         ssh.read_index_file(tmp_path / "absent.sshi")
+
+
+def test_ranking_metrics_match_reference(golden):
+    """precision_at_k / ndcg_at_k (bench.py:63-90) on the golden rankings."""
+    import paper_1610_07328_b200 as ssh
+
+    retrieved = [5, 3, 9, 1, 7, 2, 8]
+    gold = [3, 5, 1, 4, 9, 6, 0]
+    for k, (p, n) in golden["srp"]["metrics"].items():
+        assert ssh.precision_at_k(retrieved, gold, int(k)) == p
+        assert ssh.ndcg_at_k(retrieved, gold, int(k)) == n
+    with pytest.raises(ValueError, match="k must be >= 1"):
+        ssh.ndcg_at_k(retrieved, gold, 0)
