@@ -97,6 +97,7 @@ enum {
     SLOT_Q_POOLB,
     SLOT_Q_POOLCNT,
     SLOT_Q_QPAD,
+    SLOT_Q_BSHIST,
     SLOT_COUNT
 };
 

@@ -895,6 +895,89 @@ binsort_kernel(const uint32_t *__restrict__ rows_in, const float *__restrict__ l
     }
 }
 
+
+// Multi-block version of the per-query bin sort (large lists): chunks of
+// BS_CHUNK members per block; per-(query, bin, chunk) counts -> per-query
+// exclusive scan (bin-major) -> scatter.  Order inside a bin is arbitrary.
+#define BS_CHUNK 32768
+__global__ void __launch_bounds__(1024)
+bs_hist_kernel(const float *__restrict__ lb_in, const int64_t *__restrict__ roff, const int *__restrict__ cnt,
+               int nch, uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[NBINS];
+    const int q = blockIdx.y, ch = blockIdx.x;
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) h[b] = 0u;
+    __syncthreads();
+    const int n = cnt[q];
+    const int64_t o = roff[q];
+    const int e0 = ch * BS_CHUNK, e1 = min(n, e0 + BS_CHUNK);
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int b0 = e0; b0 < e1; b0 += blockDim.x) {
+        const int e = b0 + threadIdx.x;
+        const unsigned bin = e < e1 ? lb_bin(lb_in[o + e]) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+        if (e < e1 && (peers & lt) == 0) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[((int64_t)q * NBINS + b) * nch + ch] = h[b];
+}
+
+__global__ void __launch_bounds__(1024) bs_scan_kernel(uint32_t *__restrict__ hist, int nch) {
+    __shared__ uint32_t part[1024];
+    const int q = blockIdx.x;
+    uint32_t *h = hist + (int64_t)q * NBINS * nch;
+    const int64_t n = (int64_t)NBINS * nch;
+    const int64_t chunk = (n + 1023) / 1024;
+    const int64_t b = threadIdx.x * chunk, e = min(n, b + chunk);
+    uint32_t s = 0;
+    for (int64_t i = b; i < e; i++) s += h[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const uint32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+    for (int64_t i = b; i < e; i++) {
+        const uint32_t v = h[i];
+        h[i] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+bs_scatter_kernel(const uint32_t *__restrict__ rows_in, const float *__restrict__ lb_in,
+                  const int64_t *__restrict__ roff, const int *__restrict__ cnt, int nch,
+                  const uint32_t *__restrict__ hist, uint32_t *__restrict__ rows_out, float *__restrict__ lb_out) {
+    __shared__ uint32_t h[NBINS];
+    const int q = blockIdx.y, ch = blockIdx.x;
+    const int n = cnt[q];
+    const int e0 = ch * BS_CHUNK, e1 = min(n, e0 + BS_CHUNK);
+    if (e0 >= e1) return;
+    for (int b = threadIdx.x; b < NBINS; b += blockDim.x) h[b] = hist[((int64_t)q * NBINS + b) * nch + ch];
+    __syncthreads();
+    const int64_t o = roff[q];
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int b0 = e0; b0 < e1; b0 += blockDim.x) {
+        const int e = b0 + threadIdx.x;
+        const float v = e < e1 ? lb_in[o + e] : 0.f;
+        const unsigned bin = e < e1 ? lb_bin(v) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+        const int leader = __ffs(peers) - 1;
+        uint32_t basep = 0;
+        if (e < e1 && lane == leader) basep = atomicAdd(&h[bin], (uint32_t)__popc(peers));
+        basep = __shfl_sync(0xFFFFFFFFu, basep, leader);
+        if (e < e1) {
+            const uint32_t p = basep + __popc(peers & lt);
+            rows_out[o + p] = rows_in[o + e];
+            lb_out[o + p] = v;
+        }
+    }
+}
+
 // One wave, part 1: members [pos_q, pos_q + wave) of the key-sorted list.
 // A warp takes 32 consecutive members (coalesced key/row loads, ballot of
 // key <= thr) and walks the live ones with the next member's first
@@ -2682,6 +2765,8 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             int64_t total = 0;
             while (sb < nc && (sb == sa || total + hc[sb] <= budget)) total += hc[sb++];
             const int ns = sb - sa;
+            int64_t maxcand = 0;
+            for (int q = sa; q < sb; q++) maxcand = std::max<int64_t>(maxcand, hc[q]);
             QueryBufs S = B.shifted(sa, L, ctx->words, m, nseg);
             const float *Qs = Qc + (int64_t)sa * m;
             uint32_t *bms = bitmap + (int64_t)sa * NW;
@@ -2741,7 +2826,20 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                 SSH_CUDA(cudaMemsetAsync(S.mcnt, 0, sizeof(int) * ns, st));
                 paa_members_kernel<false><<<gm, MB_THREADS, MB_WARPS * 1024 * 8, st>>>(pa);
                 SSH_CHECK_LAUNCH();
-                binsort_kernel<<<ns, 1024, 0, st>>>(rows_u, lb_u, S.roff, S.mcnt, rows_s, lb_s);
+                if (round == 0) {
+                    binsort_kernel<<<ns, 1024, 0, st>>>(rows_u, lb_u, S.roff, S.mcnt, rows_s, lb_s);
+                } else {
+                    // overflow lists are long: chunked multi-block sort
+                    const int nch = (int)std::max<int64_t>(1, (maxcand + BS_CHUNK - 1) / BS_CHUNK);
+                    uint32_t *bsh = (uint32_t *)ssh_slot(ctx, SLOT_Q_BSHIST, sizeof(uint32_t) * (size_t)ns * NBINS * nch, st);
+                    if (!bsh) return SSH_ERR_OOM;
+                    dim3 gb((unsigned)nch, (unsigned)ns);
+                    bs_hist_kernel<<<gb, 1024, 0, st>>>(lb_u, S.roff, S.mcnt, nch, bsh);
+                    SSH_CHECK_LAUNCH();
+                    bs_scan_kernel<<<ns, 1024, 0, st>>>(bsh, nch);
+                    SSH_CHECK_LAUNCH();
+                    bs_scatter_kernel<<<gb, 1024, 0, st>>>(rows_u, lb_u, S.roff, S.mcnt, nch, bsh, rows_s, lb_s);
+                }
                 SSH_CHECK_LAUNCH();
                 pf.end(2);
                 // K7/K8: waves in key order: LB_Keogh2/LB_Keogh -> fp32 DTW -> threshold
