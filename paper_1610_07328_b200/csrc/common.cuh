@@ -111,7 +111,9 @@ struct ssh_index {
     // Decoding is dec(c) = fmaf(c, sc, lo) (fp32); every code brackets its
     // value exactly: dec(x8) <= x <= dec(x8 + 1), dec(U8) >= U, dec(L8) <= L,
     // and dec(pc) <= segment mean <= dec(pc + 1).  Rows with non-finite
-    // values have sc = NaN, which turns every bound on them into 0.
+    // values have sc = NaN, which turns every bound on them into 0; a row
+    // where some segment mean lies within the f64 error margin of a grid
+    // point stores -sc (decoders use |sc|; the PAA key then ignores its codes).
     void *rec = nullptr;
     uint8_t *codes = nullptr;
     int seg = 0, nseg = 0, mp = 0;

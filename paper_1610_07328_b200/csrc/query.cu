@@ -449,10 +449,11 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
             }
             *reinterpret_cast<uint32_t *>(cr + i4) = pk;
         }
-        // PAA codes of the segment means (f64 sums); an ambiguous mean (a grid
-        // point within the f64 error margin) gets the sentinel 255 = [lo, dec(256)]
+        // PAA codes of the segment means (f64 sums); a mean with a grid point
+        // within its f64 error margin makes the row's PAA codes unusable (flag)
         const double amax = fmax(fabs((double)lo), fabs((double)vmax));
         const double mg = amax * 0x1p-36;
+        bool ambiguous = false;
         for (int s = lane; s < SSH_REC_CODES; s += 32) {
             int c = 0;
             if (s < a.nseg) {
@@ -464,12 +465,16 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
                 c = min(max(c, 0), 254);
                 for (int it = 0; it < 256 && c > 0 && (double)sdec(c, sc, lo) > md - mg; it++) c--;
                 for (int it = 0; it < 256 && c < 254 && (double)sdec(c + 1, sc, lo) < md - mg; it++) c++;
-                if (c > 0 && (double)sdec(c, sc, lo) > md - mg) c = 255;
-                else if (c < 254 && (double)sdec(c + 1, sc, lo) < md + mg) c = 255;
+                if ((c > 0 && (double)sdec(c, sc, lo) > md - mg) ||
+                    (c < 254 && (double)sdec(c + 1, sc, lo) < md + mg))
+                    ambiguous = true;  // a grid point within the f64 error of the mean
             }
             prec[16 + s] = (uint8_t)c;
         }
-        if (lane == 0) *reinterpret_cast<float4 *>(prec) = make_float4(lo, sc, xs[0], xs[m - 1]);
+        // a row with an ambiguous segment mean carries -sc: its PAA codes are
+        // not used (the key falls back to LB_Kim); decoders take |sc|
+        ambiguous = __any_sync(0xFFFFFFFFu, ambiguous);
+        if (lane == 0) *reinterpret_cast<float4 *>(prec) = make_float4(lo, ambiguous ? -sc : sc, xs[0], xs[m - 1]);
         __syncwarp();
         if (lane < 4) a.rec[row * 4 + lane] = reinterpret_cast<const uint4 *>(prec)[lane];
         // running max of the codes and of their complements (= running min) over
@@ -671,9 +676,12 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
         for (int b = threadIdx.x; b < NBINS; b += MB_THREADS) shist[b] = 0u;
     __syncthreads();
     const float q0 = a.Q[(int64_t)q * a.m], ql = a.Q[(int64_t)q * a.m + a.m - 1];
-    const float shrink = 1.f - (3.f * nseg + 8.f) * U32_EPS;
     const float segf = (float)a.seg;
     const float lastlen = (float)(a.m - (nseg - 1) * a.seg);
+    // fp32 evaluation error of the weighted sum, including the last-segment
+    // correction (cancellation relative to seg / lastlen)
+    const float shrink = 1.f - (3.f * nseg + 12.f + 4.f * segf / lastlen) * U32_EPS;
+    const float wseg = segf;
     // smallest key value in bin bhi + 1: keys at or above it are dropped
     const float edge = bhi >= NBINS - 1 ? INFINITY : __uint_as_float((uint32_t)(bhi + 1) << 20);
     const uint32_t *bm = a.bitmap + (int64_t)q * a.NW;
@@ -718,26 +726,31 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                     acc = g ? accb[e] : 0.f;
                     const uint4 *rp = a.rec + (int64_t)row * 4;
                     const float2 h = __ldg(reinterpret_cast<const float2 *>(rp));
-                    const float lo = h.x, sc = h.y;
+                    // flagged rows (-sc): NaN scale -> every PAA term max(NaN, ..., 0) = 0
+                    const float lo = h.x, sc = h.y >= 0.f ? h.y : __int_as_float(0x7FC00000);
                     const uint4 cg = __ldg(rp + 1 + g);
                     const uint32_t cw[4] = {cg.x, cg.y, cg.z, cg.w};
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
                         const int sgi = 16 * g + j;
                         const float cf = code_f(cw[j >> 2], j & 3);
-                        const float xa = cf == 255.f ? lo : fmaf(cf, sc, lo);
+                        const float xa = fmaf(cf, sc, lo);
                         const float xb = fmaf(cf + 1.f, sc, lo);
                         const float ev = fmaxf(fmaxf(xa - sUs[sgi], sLs[sgi] - xb), 0.f);
-                        const float len = sgi == nseg - 1 ? lastlen : segf;
-                        acc = fmaf(len * ev, ev, acc);
+                        acc = fmaf(ev, ev, acc);  // weight seg for every segment; the last is fixed below
                     }
                     if (g < 2) {
-                        keep = SAMPLE || acc * shrink * (1.f - 4.f * U32_EPS) < edge;
+                        keep = SAMPLE || acc * wseg * shrink * (1.f - 4.f * U32_EPS) < edge;
                     } else {
+                        // the last segment has lastlen <= seg samples: remove its excess weight
+                        const int sl = nseg - 1;
+                        const uint32_t lw = __ldg(reinterpret_cast<const uint32_t *>(rp) + 4 + (sl >> 2));
+                        const float cf = code_f(lw, sl & 3);
+                        const float ev = fmaxf(fmaxf(fmaf(cf, sc, lo) - sUs[sl], sLs[sl] - fmaf(cf + 1.f, sc, lo)), 0.f);
+                        const float paa = fmaxf(fmaf(-(segf - lastlen) * ev, ev, acc * segf), 0.f) * shrink;
                         const float2 kx = __ldg(reinterpret_cast<const float2 *>(rp) + 1);
                         const float d0 = kx.x - q0, dl = kx.y - ql;
                         const float kim = a.m >= 2 ? fmaf(dl, dl, d0 * d0) : d0 * d0;
-                        const float paa = acc * shrink;
                         if (kim > paa) key = __uint_as_float(__float_as_uint(kim * (1.f - 2.f * U32_EPS)) | 1u);
                         else key = __uint_as_float(__float_as_uint(paa) & ~1u);
                         const int kb = (int)lb_bin(key);
@@ -1078,6 +1091,7 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
         live &= live - 1;
         uint32_t rc = __shfl_sync(0xFFFFFFFFu, row, j);
         float2 hc = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rc * 4));
+        hc.y = fabsf(hc.y);  // sign = PAA-codes flag, not part of the scale
         uint2 vc[4];
         wl_load_env(a.codes + (int64_t)rc * a.cstride, mp, 0, vc);
         for (;;) {
@@ -1091,6 +1105,7 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
                 live &= live - 1;
                 rn = __shfl_sync(0xFFFFFFFFu, row, j);
                 hn = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rn * 4));
+                hn.y = fabsf(hn.y);
                 wl_load_env(a.codes + (int64_t)rn * a.cstride, mp, 0, vn);
             }
             const uint8_t *cr = a.codes + (int64_t)rc * a.cstride;
@@ -1498,7 +1513,8 @@ dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
                 row = L.rows[(int64_t)slot * L.stride + e];
                 if (a == 0) {
                     const float2 lb = L.lbs[(int64_t)slot * L.stride + e];
-                    const float2 h = __ldg(reinterpret_cast<const float2 *>(L.rec + (int64_t)row * 4));
+                    float2 h = __ldg(reinterpret_cast<const float2 *>(L.rec + (int64_t)row * 4));
+                    h.y = fabsf(h.y);
                     L.out[(int64_t)slot * L.stride + e] = INFINITY;
                     remk = lb.x;
                     rem2 = lb.y;
@@ -1833,7 +1849,8 @@ dtwp_first_kernel(DtwCommon C, const int *__restrict__ act, const uint32_t *__re
     if (have) {
         row = wrows[oi];
         const float2 lb = wlb[oi];
-        const float2 h = __ldg(reinterpret_cast<const float2 *>(rec + (int64_t)row * 4));
+        float2 h = __ldg(reinterpret_cast<const float2 *>(rec + (int64_t)row * 4));
+        h.y = fabsf(h.y);
         C.out[oi] = INFINITY;
         remk = lb.x;
         rem2 = lb.y;
