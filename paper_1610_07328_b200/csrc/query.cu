@@ -1418,25 +1418,7 @@ dtw32r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q,
     }
 }
 
-// Register-band fp32 DTW of one wave's candidate list with per-warp
-// compaction.  Each warp owns DW_IPW candidates of one query and runs them
-// through row passes [0,8), [8,16), [16,32), ... in batches of 32; after
-// a pass the survivors' state (band registers, remaining bounds) is parked
-// in the warp's shared-memory slots and their indices form the next pass's
-// list, so lanes whose candidate was abandoned early do not idle until the
-// slowest lane finishes, and warps never wait for each other (one block
-// barrier, after staging the query).  Rows stay warp-uniform (query reads
-// are shared-memory broadcasts).
-// Abandon test after row i (UCR-suite cumulative bounds, dtw.py:206-215):
-//   rmin_i + max(remK_i - slackK, rem2_i - slack2, 0) > thr
-//   remK_i = LBK total - sum_{i' <= i} LB_Keogh term of row i'     (rows left)
-//   rem2_i = LBK2 total - sum_{j <= i + R} LB_Keogh2 term of col j (columns
-//            no path through row i has reached)
-// with the totals from the wave LB kernel (code-based terms; the exact-x row
-// terms subtracted here are never smaller, so remK stays a lower bound) and
-// slack = total * (2m + 8) u for the fp32 running sums.
-#define DW_IPW 64  // candidates per warp in the wave DTW kernel
-
+// Wave DTW list (per active-query slot) handed to the pooled DTW launcher.
 struct DtwWave {
     const uint32_t *rows;
     const float2 *lbs;  // (LB_Keogh, LB_Keogh2) totals per entry
@@ -1451,213 +1433,6 @@ struct DtwWave {
     int mp;
     const int *act;  // block row y -> query act[y]; rows/lbs/out/cnt per slot y
 };
-
-template <int R, int DW_WARPS>
-__global__ void __launch_bounds__(32 * DW_WARPS)
-dtw32w_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, const float *__restrict__ U,
-              const float *__restrict__ Lo, DtwWave L, const float *__restrict__ thr,
-              unsigned long long *__restrict__ cells) {
-    constexpr int NB = 2 * R + 1;
-    constexpr int IPW = DW_IPW;  // candidates per warp
-    extern __shared__ __align__(16) float wsm2[];
-    const int slot = blockIdx.y;
-    const int q = L.act[slot];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int total = min(L.cnt[slot], (int)L.stride);
-    const int base = blockIdx.x * DW_WARPS * IPW;
-    if (base >= total) return;
-    const int YP = ((m + 2 * R + 8) + 3) & ~3;
-    float *yc = wsm2;           // YP: y[j] at yc[j + R], +inf outside [0, m)
-    float *su = yc + YP;        // m
-    float *sl = su + m;         // m
-    // per-warp candidate state, [k][IPW] for the band
-    float *sband = sl + m + (size_t)w * (NB + 6) * IPW;
-    float *sremk = sband + NB * IPW, *srem2 = sremk + IPW;
-    float *sslk = srem2 + IPW, *ssl2 = sslk + IPW;
-    float *slo = ssl2 + IPW, *ssc = slo + IPW;
-    int *lists = reinterpret_cast<int *>(sl + m + (size_t)DW_WARPS * (NB + 6) * IPW) + w * 2 * IPW;
-    const float *y = Q + (int64_t)q * m;
-    for (int t = threadIdx.x; t < YP; t += blockDim.x) {
-        const int jj = t - R;
-        yc[t] = (jj >= 0 && jj < m) ? y[jj] : INFINITY;
-    }
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        su[i] = U[(int64_t)q * m + i];
-        sl[i] = Lo[(int64_t)q * m + i];
-    }
-    __syncthreads();  // the only block-wide barrier: warps run independently from here
-    const int wbase = base + w * IPW;
-    const int n0 = min(total - wbase, IPW);
-    if (n0 <= 0) return;
-    const float T = thr[q];
-    const float slf = (float)(2 * m + 8) * U32_EPS;
-    if (lane == 0 && L.computed) atomicAdd(&L.computed[q], n0);
-    int *cur = lists, *nxt = lists + IPW;
-    for (int i = lane; i < n0; i += 32) cur[i] = i;
-    __syncwarp();
-    int ncur = n0;
-    unsigned long long my_cells = 0;
-    unsigned long long my_ab = 0;
-    unsigned long long wrows = 0;  // rows the warp executed (all lanes), profiling
-    for (int a = 0; a < m && ncur > 0;) {
-        const int b = min(m, a < 8 ? 8 : 2 * a);  // passes [0,8), [8,16), [16,32), ...
-        int nn = 0;
-        for (int b0 = 0; b0 < ncur; b0 += 32) {
-            const bool have = b0 + lane < ncur;
-            const int it = have ? cur[b0 + lane] : 0;
-            const int e = wbase + it;
-            float band[NB];
-            uint32_t row = 0;
-            float remk = 0.f, rem2 = 0.f, slk = 0.f, sl2 = 0.f, lo = 0.f, sc = 0.f;
-            if (have) {
-                row = L.rows[(int64_t)slot * L.stride + e];
-                if (a == 0) {
-                    const float2 lb = L.lbs[(int64_t)slot * L.stride + e];
-                    float2 h = __ldg(reinterpret_cast<const float2 *>(L.rec + (int64_t)row * 4));
-                    h.y = fabsf(h.y);
-                    L.out[(int64_t)slot * L.stride + e] = INFINITY;
-                    remk = lb.x;
-                    rem2 = lb.y;
-                    slk = lb.x * slf;
-                    sl2 = lb.y * slf;
-                    lo = h.x;
-                    sc = h.y;
-#pragma unroll
-                    for (int k = 0; k < NB; k++) band[k] = k == R ? 0.f : INFINITY;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < NB; k++) band[k] = sband[k * IPW + it];
-                    remk = sremk[it];
-                    rem2 = srem2[it];
-                    slk = sslk[it];
-                    sl2 = ssl2[it];
-                    lo = slo[it];
-                    sc = ssc[it];
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < NB; k++) band[k] = INFINITY;
-            }
-            const float *x = X + (int64_t)row * m;
-            const uint8_t *env = L.codes + (int64_t)row * L.cstride + L.mp;
-            bool alive = have;
-            if (a == 0 && have) {
-                // columns j < R leave the LB_Keogh2 remainder before row 0
-                uint2 ev = make_uint2(0u, 0u);
-                for (int j = 0; j < min(R, m); j++) {
-                    if ((j & 3) == 0) ev = __ldg(reinterpret_cast<const uint2 *>(env + 2 * j));
-                    const uint32_t wv = (j & 2) ? ev.y : ev.x;
-                    const int bu = 2 * (j & 1);
-                    const float qj = yc[j + R];
-                    const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
-                    const float d = fmaxf(fmaxf(qj - ue, le - qj), 0.f);
-                    rem2 = fmaf(-d, d, rem2);
-                }
-            }
-            const float4 *xp = reinterpret_cast<const float4 *>(x);
-            float4 xn = have ? __ldg(xp + (a >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            int rows = 0;
-            for (int i0 = a; i0 < b; i0 += 4) {
-                if (!__any_sync(0xFFFFFFFFu, alive)) break;
-                rows += alive ? 4 : 0;
-                wrows += 4;
-                const float4 xc = xn;
-                if (i0 + 4 < b) xn = __ldg(xp + (i0 >> 2) + 1);
-                // envelope codes of columns i0+R .. i0+R+3 (two aligned 4-column groups)
-                const int jb = (i0 + R) & ~3;
-                uint2 e0 = make_uint2(0u, 0u), e1 = make_uint2(0u, 0u);
-                if (jb < m) e0 = __ldg(reinterpret_cast<const uint2 *>(env + 2 * jb));
-                if (jb + 4 < m) e1 = __ldg(reinterpret_cast<const uint2 *>(env + 2 * jb + 8));
-                const float xr[4] = {xc.x, xc.y, xc.z, xc.w};
-                float lft[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-                float rmn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-                const float4 *yp = reinterpret_cast<const float4 *>(yc + i0);
-#pragma unroll
-                for (int s4 = 0; s4 < (NB + 3 + 3) / 4; s4++) {
-                    const float4 yv4 = yp[s4];
-                    const float yv[4] = {yv4.x, yv4.y, yv4.z, yv4.w};
-#pragma unroll
-                    for (int sv = 0; sv < 4; sv++) {
-                        const int st = 4 * s4 + sv;
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const int k = st - u;
-                            if (k >= 0 && k < NB) {
-                                const float up = (k + 1 < NB) ? band[k + 1] : INFINITY;
-                                const float d = xr[u] - yv[sv];
-                                const float cv = fmaf(d, d, fminf(fminf(band[k], up), lft[u]));
-                                band[k] = cv;
-                                lft[u] = cv;
-                                rmn[u] = fminf(rmn[u], cv);
-                            }
-                        }
-                    }
-                }
-                const float4 u4 = *reinterpret_cast<const float4 *>(su + i0);
-                const float4 l4 = *reinterpret_cast<const float4 *>(sl + i0);
-                const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
-                bool cut = false;
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const float v = fmaxf(fmaxf(xr[u] - uu[u], ll[u] - xr[u]), 0.f);
-                    remk = fmaf(-v, v, remk);
-                    const int jj = i0 + u + R;
-                    if (jj < m) {
-                        const int off = (R & 3) + u;  // column jj within the 8-column window
-                        const uint32_t wv = off < 2 ? e0.x : off < 4 ? e0.y : off < 6 ? e1.x : e1.y;
-                        const int bu = 2 * (off & 1);
-                        const float qj = yc[jj + R];
-                        const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
-                        const float dd = fmaxf(fmaxf(qj - ue, le - qj), 0.f);
-                        rem2 = fmaf(-dd, dd, rem2);
-                    }
-                    cut = cut || (rmn[u] + fmaxf(fmaxf(remk - slk, rem2 - sl2), 0.f) > T);
-                }
-                if (alive && cut) {
-                    alive = false;
-                    my_ab++;
-                }
-            }
-            my_cells += (unsigned long long)rows * NB;
-            // survivors keep their state slot and join the next pass's list
-            const unsigned am = __ballot_sync(0xFFFFFFFFu, alive && b < m);
-            if (alive) {
-                if (b >= m) {
-                    L.out[(int64_t)slot * L.stride + e] = band[R];
-                } else {
-                    nxt[nn + __popc(am & ((1u << lane) - 1u))] = it;
-#pragma unroll
-                    for (int k = 0; k < NB; k++) sband[k * IPW + it] = band[k];
-                    sremk[it] = remk;
-                    srem2[it] = rem2;
-                    sslk[it] = slk;
-                    ssl2[it] = sl2;
-                    slo[it] = lo;
-                    ssc[it] = sc;
-                }
-            }
-            nn += __popc(am);
-        }
-        __syncwarp();
-        int *t = cur;
-        cur = nxt;
-        nxt = t;
-        ncur = nn;
-        a = b;
-    }
-    if (cells || L.abandoned) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            my_cells += __shfl_xor_sync(0xFFFFFFFFu, my_cells, o);
-            my_ab += __shfl_xor_sync(0xFFFFFFFFu, my_ab, o);
-        }
-        if (lane == 0) {
-            if (cells && my_cells) atomicAdd(cells, my_cells);
-            if (cells && wrows) atomicAdd(cells + 5, wrows * 32 * NB);
-            if (L.abandoned && my_ab) atomicAdd(&L.abandoned[q], my_ab);
-        }
-    }
-}
 
 // ----------------------------------------------- pooled wave fp32 DTW
 // The wave's candidates of all queries run through row passes [0,8),
@@ -2446,34 +2221,6 @@ static int launch_dtw32r(ssh_ctx *ctx, const float *X, const float *Q, const flo
                                                      ctx->profile ? ctx->d_cells : nullptr);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
-}
-
-template <int R, int DW_WARPS>
-static int launch_dtw32w_w(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
-                           const DtwWave &L, const float *thr, int nq, int wave, cudaStream_t st) {
-    const int m = ctx->p.m;
-    constexpr int NB = 2 * R + 1;
-    constexpr int DW_ITEMS = DW_WARPS * DW_IPW;
-    const int YP = ((m + 2 * R + 8) + 3) & ~3;
-    const size_t smem = (size_t)(YP + 2 * m + (NB + 6) * DW_ITEMS) * sizeof(float) + 2 * DW_ITEMS * 4;
-    SSH_REQUIRE(smem <= 227 * 1024, SSH_ERR_UNSUPPORTED, "wave DTW: series too long (m=%d)", m);
-    SSH_CUDA(cudaFuncSetAttribute(dtw32w_kernel<R, DW_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    dim3 grid((unsigned)ssh_div_up(wave, DW_ITEMS), (unsigned)nq);
-    dtw32w_kernel<R, DW_WARPS><<<grid, 32 * DW_WARPS, smem, st>>>(X, m, Q, U, Lo, L, thr,
-                                                                  ctx->profile ? ctx->d_cells : nullptr);
-    SSH_CHECK_LAUNCH();
-    return SSH_OK;
-}
-
-// block size by wave length: small early waves use 2-warp blocks (more
-// resident blocks per SM), long waves 8-warp blocks (more to compact)
-template <int R>
-static int launch_dtw32w(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
-                         const DtwWave &L, const float *thr, int nq, int wave, cudaStream_t st) {
-    if (wave <= 0) return SSH_OK;
-    if (wave <= 2 * DW_IPW) return launch_dtw32w_w<R, 2>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
-    return launch_dtw32w_w<R, 4>(ctx, X, Q, U, Lo, L, thr, nq, wave, st);
 }
 
 // wave fp32 DTW: compacting register-band kernel for the common radii, the
