@@ -195,6 +195,69 @@ __device__ void sort_keys(uint32_t *keys, int D, uint32_t *buf, int P2, int lane
     __syncwarp();
 }
 
+
+// Distinct tokens + counts by a register sort (T <= 32 V): the row's bit
+// words are staged in shared memory, each lane builds V tokens (element
+// e = lane * V + v), a warp bitonic sort orders them, and run starts give the
+// np.unique order directly: w.ukey[d] = token << 12 | count.  Returns D.
+template <int V>
+__device__ int warp_dedup_sort(const SigArgs &a, int64_t row, const WarpSmem &w, int lane) {
+    uint64_t *wsm = reinterpret_cast<uint64_t *>(w.hkey);  // >= 8 words of scratch (8 H bytes)
+    for (int i = lane; i < a.words; i += 32) wsm[i] = a.bits[row * a.words + i];
+    __syncwarp();
+    const uint32_t nmask = (a.n == 32) ? 0xFFFFFFFFu : ((1u << a.n) - 1u);
+    uint32_t x[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        const int e = lane * V + v;
+        uint32_t tok = 0xFFFFFFFFu;
+        if (e < a.T) {
+            const int wi = e >> 6, sh = e & 63;
+            const uint64_t w0 = wsm[wi], w1 = wi + 1 < a.words ? wsm[wi + 1] : 0ULL;
+            const uint64_t bitsv = sh ? ((w0 >> sh) | (w1 << (64 - sh))) : w0;
+            tok = __brev((uint32_t)bitsv & nmask) >> (32 - a.n);
+        }
+        x[v] = tok;
+    }
+    __syncwarp();
+    warp_sort_regs<V>(x, lane);
+    // run starts
+    const uint32_t pv = __shfl_up_sync(0xFFFFFFFFu, x[V - 1], 1);
+    unsigned smask = 0;
+    int c = 0;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        const uint32_t prev = v ? x[v - 1] : pv;
+        const bool st = x[v] != 0xFFFFFFFFu && (lane * V + v == 0 || x[v] != prev);
+        smask |= (unsigned)st << v;
+        c += st;
+    }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int D = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    int d = incl - c;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        if ((smask >> v) & 1u) {
+            w.utok[d] = x[v];
+            w.ustart[d] = (uint16_t)(lane * V + v);
+            d++;
+        }
+    }
+    if (lane == 0) w.ustart[D] = (uint16_t)a.T;
+    __syncwarp();
+    for (int k = lane; k < D; k += 32) {
+        const uint32_t cnt = (uint32_t)w.ustart[k + 1] - (uint32_t)w.ustart[k];
+        w.ukey[k] = (w.utok[k] << 12) | cnt;
+    }
+    __syncwarp();
+    return D;
+}
+
 // Distinct tokens + counts via the per-warp hash set, as packed keys
 // (token << 12 | count) sorted ascending (= np.unique order); returns D.
 // The hash table is left empty again for the next series.
@@ -476,6 +539,12 @@ __global__ void __launch_bounds__(32 * SG_WARPS, 4) shingle_cws_kernel(SigArgs a
             __syncwarp();
         } else if (MODE == SIG_MODE_SHINGLE) {
             D = warp_shingle_sorted(a, row, w, lane);
+        } else if (a.T <= 128) {
+            D = warp_dedup_sort<4>(a, row, w, lane);
+        } else if (a.T <= 256) {
+            D = warp_dedup_sort<8>(a, row, w, lane);
+        } else if (a.T <= 512) {
+            D = warp_dedup_sort<16>(a, row, w, lane);
         } else {
             D = warp_dedup(a, row, w, lane);
         }
