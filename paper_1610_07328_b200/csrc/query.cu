@@ -1760,6 +1760,102 @@ dtw64r_kernel(const float *__restrict__ X, int m, const float *__restrict__ Q, c
     out[(int64_t)q * list_stride + e] = band[R];
 }
 
+
+// Exact f64 DTW, one warp per pair, anti-diagonal wavefront over rows: lane l
+// owns rows l, l + 32, ...; within a round it walks its row's band left to
+// right, two steps behind lane l - 1, so the cell above arrives by a shuffle
+// from lane l - 1 one step earlier (its diagonal one step before that) and
+// lane 0 continues after lane 31 (period 64 steps, 2 r + 1 busy).  Every
+// cell is the reference recurrence d = x - y; d = d * d; c = d + min(up,
+// left, diag) (dtw.py:100-113) with _rn intrinsics, so the result is the
+// same bits as a sequential evaluation; cells outside the band or the series
+// are +inf.  Needs 2 r + 1 <= 64 (a lane's row must end before its next
+// round starts).  The query (as f64, padded with +inf) is staged per warp.
+// Pairs: list mode (blockIdx.y = query, list[q][e]) or explicit (qrow, xrow).
+#define D64W_WARPS 4
+__global__ void __launch_bounds__(32 * D64W_WARPS)
+dtw64w_kernel(const float *__restrict__ X, int m, int r, const float *__restrict__ Q,
+              const int32_t *__restrict__ qrow, const uint32_t *__restrict__ list, int64_t list_stride,
+              const int *__restrict__ list_cnt, const int64_t *__restrict__ xrow64, int64_t npair,
+              double *__restrict__ out) {
+    extern __shared__ double ysm64[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int YP = m + 2 * r + 2;
+    double *yq = ysm64 + (size_t)w * YP;  // yq[j + r] = y[j]
+    int64_t e, row;
+    int q;
+    if (list) {
+        q = blockIdx.y;
+        e = (int64_t)blockIdx.x * D64W_WARPS + w;
+        if (e >= list_cnt[q]) return;  // warp-uniform
+        row = list[(int64_t)q * list_stride + e];
+    } else {
+        e = (int64_t)blockIdx.x * D64W_WARPS + w;
+        if (e >= npair) return;
+        q = qrow[e];
+        row = xrow64[e];
+    }
+    const double inf = (double)INFINITY;
+    const float *y = Q + (int64_t)q * m;
+    for (int t = lane; t < YP; t += 32) {
+        const int j = t - r;
+        yq[t] = (j >= 0 && j < m) ? (double)y[j] : inf;
+    }
+    __syncwarp();
+    const float *x = X + row * m;
+    const int NB = 2 * r + 1;
+    const int rounds = (m + 31) / 32;
+    const int last_t = 64 * (rounds - 1) + 2 * 31 + NB;  // last active step of lane 31
+    double cur = inf;     // value this lane produced in the previous step (shared to lane + 1)
+    double diag_in = inf; // value received one step ago (= diag for this step)
+    double left = inf;
+    double xi = 0.0;
+    double res = inf;
+    for (int t = 0; t <= last_t; t++) {
+        // value from lane - 1 (lane 0: lane 31, previous round) produced at step t - 1
+        const double up_in = __shfl_sync(0xFFFFFFFFu, cur, (lane + 31) & 31);
+        const int tl = t - 2 * lane;
+        double c = inf;
+        if (tl >= 0) {
+            const int k = tl >> 6, sstep = tl & 63;
+            const int i = 32 * k + lane;
+            if (sstep < NB && i < m) {
+                if (sstep == 0) {
+                    xi = (double)x[i];
+                    left = inf;
+                }
+                const int j = i - r + sstep;
+                double up = up_in, dg = diag_in;
+                if (i == 0) {
+                    up = inf;
+                    dg = (j == 0) ? 0.0 : inf;
+                } else if (sstep == NB - 1) {
+                    up = inf;  // D(i - 1, i + r) lies outside row i - 1's band
+                }
+                if (j >= 0 && j < m) {
+                    double d = __dsub_rn(xi, yq[j + r]);
+                    d = __dmul_rn(d, d);
+                    double best = up;
+                    if (left < best) best = left;
+                    if (dg < best) best = dg;
+                    c = __dadd_rn(d, best);
+                }
+                left = c;
+                if (i == m - 1 && j == m - 1) res = c;
+            }
+        }
+        diag_in = up_in;
+        cur = c;
+    }
+    // the lane owning row m - 1 holds the result
+    const int owner = (m - 1) & 31;
+    res = __shfl_sync(0xFFFFFFFFu, res, owner);
+    if (lane == 0) {
+        if (list) out[(int64_t)q * list_stride + e] = res;
+        else out[e] = res;
+    }
+}
+
 // ------------------------------------------------------------ fp64 DTW
 // exact reference arithmetic (dtw.py:100-113): d = x - y; d = d*d; c = d + min(...)
 __global__ void dtw64_kernel(const float *__restrict__ X, int m, int r, const float *__restrict__ Q,
@@ -2342,21 +2438,25 @@ static int launch_dtw64_list(const float *X, int m, int r, const float *Q, const
                              int64_t stride, const int *cnt, int maxcnt, double *out, int nq,
                              cudaStream_t st) {
     if (maxcnt <= 0) return SSH_OK;
+    const size_t smem = sizeof(double) * (size_t)(m + 2 * r + 2) * D64W_WARPS;
+    if (2 * r + 1 <= 64 && smem <= 200 * 1024) {  // wavefront period 64 >= band width
+        SSH_CUDA(cudaFuncSetAttribute(dtw64w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid((unsigned)ssh_div_up(maxcnt, D64W_WARPS), (unsigned)nq);
+        dtw64w_kernel<<<grid, 32 * D64W_WARPS, smem, st>>>(X, m, r, Q, nullptr, list, stride, cnt, nullptr, 0, out);
+        SSH_CHECK_LAUNCH();
+        return SSH_OK;
+    }
     if ((m & 3) == 0 && (size_t)(m + 2 * r + 8) * 8 <= 160 * 1024) {
         switch (r) {
-            case 3: return launch_dtw64r<3>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
-            case 6: return launch_dtw64r<6>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
-            case 13: return launch_dtw64r<13>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
-            case 26: return launch_dtw64r<26>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
             case 51: return launch_dtw64r<51>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
             default: break;
         }
     }
-    size_t smem;
-    int t = dtw64_threads(r, &smem);
-    SSH_CUDA(cudaFuncSetAttribute(dtw64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    size_t smem2;
+    int t = dtw64_threads(r, &smem2);
+    SSH_CUDA(cudaFuncSetAttribute(dtw64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     dim3 grid((unsigned)ssh_div_up(maxcnt, t), (unsigned)nq);
-    dtw64_kernel<<<grid, t, smem, st>>>(X, m, r, Q, nullptr, list, stride, cnt, nullptr, 0, out);
+    dtw64_kernel<<<grid, t, smem2, st>>>(X, m, r, Q, nullptr, list, stride, cnt, nullptr, 0, out);
     SSH_CHECK_LAUNCH();
     return SSH_OK;
 }
@@ -2368,10 +2468,18 @@ extern "C" int ssh_dtw_exact(ssh_ctx *ctx, const float *X, const float *Q, const
     SSH_REQUIRE(X && Q && qrow && xrow && d2, SSH_ERR_INVALID, "ssh_dtw_exact: NULL pointer");
     SSH_CUDA(cudaSetDevice(ctx->device));
     int m = ctx->p.m, r = ctx->p.radius;
-    size_t smem;
-    int t = dtw64_threads(r, &smem);
-    SSH_CUDA(cudaFuncSetAttribute(dtw64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dtw64_kernel<<<(unsigned)ssh_div_up(npair, t), t, smem, (cudaStream_t)stream>>>(
+    const size_t smem = sizeof(double) * (size_t)(m + 2 * r + 2) * D64W_WARPS;
+    if (2 * r + 1 <= 64 && smem <= 200 * 1024) {  // wavefront period 64 >= band width
+        SSH_CUDA(cudaFuncSetAttribute(dtw64w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dtw64w_kernel<<<(unsigned)ssh_div_up(npair, D64W_WARPS), 32 * D64W_WARPS, smem, (cudaStream_t)stream>>>(
+            X, m, r, Q, qrow, nullptr, 0, nullptr, xrow, npair, d2);
+        SSH_CHECK_LAUNCH();
+        return SSH_OK;
+    }
+    size_t smem2;
+    int t = dtw64_threads(r, &smem2);
+    SSH_CUDA(cudaFuncSetAttribute(dtw64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    dtw64_kernel<<<(unsigned)ssh_div_up(npair, t), t, smem2, (cudaStream_t)stream>>>(
         X, m, r, Q, qrow, nullptr, 0, nullptr, xrow, npair, d2);
     SSH_CHECK_LAUNCH();
     return SSH_OK;

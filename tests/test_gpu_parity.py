@@ -616,3 +616,22 @@ def test_srp_matrix_matches_reference(cuda, golden, bits, seed):
     assert got.dtype == np.int8 and got.shape == (300, bits)
     assert sha(got) == golden["srp"][f"b{bits}_s{seed}"]
     assert np.array_equal(ssh.srp_signature(X[7], bits, seed), got[7])
+
+
+@pytest.mark.parametrize("band", [0.0605, 0.0625, 0.0])
+def test_dtw_exact_band_edges(cuda, band):
+    """The exact f64 DTW (warp wavefront for 2r+1 <= 64, other kernels above):
+    radii 31 / 32 / 0 around the wavefront limit, bit-identical to the oracle's
+    reference recurrence."""
+    import paper_1610_07328_b200 as ssh
+    from paper_1610_07328_b200.index import dtw_exact_pairs
+
+    X, Q, _, _ = case_data("rw512")
+    idx = ssh.build_index(ssh.Dataset(X[:300]), params(band, K=1))
+    rng = np.random.default_rng(4)
+    qrow = rng.integers(0, Q.shape[0], 40)
+    xrow = rng.integers(0, 300, 40)
+    got = dtw_exact_pairs(idx, Q, qrow, xrow)
+    r = O.radius(band, X.shape[1])
+    want = np.array([O.dtw_sq(X[b], Q[a], r) for a, b in zip(qrow, xrow)])
+    assert np.array_equal(got, want)
