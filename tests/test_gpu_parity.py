@@ -635,3 +635,19 @@ def test_dtw_exact_band_edges(cuda, band):
     r = O.radius(band, X.shape[1])
     want = np.array([O.dtw_sq(X[b], Q[a], r) for a, b in zip(qrow, xrow)])
     assert np.array_equal(got, want)
+
+
+def test_large_k_vs_oracle(cuda):
+    """k = 700 (top-k sort and rescoring sets far beyond the usual 10) against
+    the oracle cascade; results sorted by (distance, id)."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw512")
+    p = ssh.SshParams(W=16, delta=2, n=4, d=3, band=band, K=1)  # short shingles: R is most of the shard
+    idx = ssh.build_index(ssh.Dataset(X), p)
+    oidx = O.build_index(X, 16, 2, 4, 3, 1, 0, band)
+    ores = O.query_batch(oidx, Q[:4], 700)
+    for i, r in enumerate(ssh.query_index_batch(idx, Q[:4], 700)):
+        n = int(ores["n"][i])
+        assert r.ids == ores["ids"][i][:n].tolist(), i
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
