@@ -1021,6 +1021,9 @@ struct WaveLbArgs {
 };
 
 #define WL_BLK 512  // samples per block of loads (4 chunks of 128, one per lane each)
+#ifndef SSH_WL_KEOGH_FIRST
+#define SSH_WL_KEOGH_FIRST 0  // 1: LB_Keogh over sample codes before LB_Keogh2 over envelope codes
+#endif
 
 __device__ __forceinline__ void wl_load_env(const uint8_t *cr, int mp, int base, uint2 (&v)[4]) {
     const uint2 *p = reinterpret_cast<const uint2 *>(cr + mp + 2 * base) + (threadIdx.x & 31);
@@ -1045,6 +1048,36 @@ __device__ __forceinline__ float wl_env_block(const uint2 (&v)[4], const float *
                 const int bu = 2 * (t & 1);
                 const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
                 const float d = fmaxf(fmaxf(qq[t] - ue, le - qq[t]), 0.f);
+                acc = fmaf(d, d, acc);
+            }
+        }
+    }
+    return acc;
+}
+
+__device__ __forceinline__ void wl_load_smp(const uint8_t *cr, int mp, int base, uint32_t (&v)[4]) {
+    const uint32_t *p = reinterpret_cast<const uint32_t *>(cr + base) + (threadIdx.x & 31);
+#pragma unroll
+    for (int c = 0; c < 4; c++) v[c] = base + 128 * c < mp ? __ldg(p + 32 * c) : 0u;
+}
+
+// partial LB_Keogh of one 512-sample block over sample codes (tails: U = inf, L = -inf -> 0)
+__device__ __forceinline__ float wl_smp_block(const uint32_t (&cw)[4], const float *su, const float *sl, int base,
+                                              int mp, float sc, float lo) {
+    const int lane = threadIdx.x & 31;
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        const int i0 = base + 128 * c + 4 * lane;
+        if (base + 128 * c < mp) {
+            const float4 u4 = *reinterpret_cast<const float4 *>(su + i0);
+            const float4 l4 = *reinterpret_cast<const float4 *>(sl + i0);
+            const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const float cf = code_f(cw[c], t);
+                const float xa = fmaf(cf, sc, lo), xb = fmaf(cf + 1.f, sc, lo);
+                const float d = fmaxf(fmaxf(xa - uu[t], ll[t] - xb), 0.f);
                 acc = fmaf(d, d, acc);
             }
         }
@@ -1092,26 +1125,63 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
         uint32_t rc = __shfl_sync(0xFFFFFFFFu, row, j);
         float2 hc = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rc * 4));
         hc.y = fabsf(hc.y);  // sign = PAA-codes flag, not part of the scale
+#if SSH_WL_KEOGH_FIRST
+        uint32_t vc[4];
+        wl_load_smp(a.codes + (int64_t)rc * a.cstride, mp, 0, vc);
+#else
         uint2 vc[4];
         wl_load_env(a.codes + (int64_t)rc * a.cstride, mp, 0, vc);
+#endif
         for (;;) {
             // prefetch the next live member's header and first block
             const bool more = live != 0;
             uint32_t rn = 0;
             float2 hn = make_float2(0.f, 0.f);
+#if SSH_WL_KEOGH_FIRST
+            uint32_t vn[4];
+#else
             uint2 vn[4];
+#endif
             if (more) {
                 j = __ffs(live) - 1;
                 live &= live - 1;
                 rn = __shfl_sync(0xFFFFFFFFu, row, j);
                 hn = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rn * 4));
                 hn.y = fabsf(hn.y);
+#if SSH_WL_KEOGH_FIRST
+                wl_load_smp(a.codes + (int64_t)rn * a.cstride, mp, 0, vn);
+#else
                 wl_load_env(a.codes + (int64_t)rn * a.cstride, mp, 0, vn);
+#endif
             }
             const uint8_t *cr = a.codes + (int64_t)rc * a.cstride;
             const float lo = hc.x, sc = hc.y;
             bool pruned = false;
             float acc = 0.f, tot2 = 0.f, tot1 = 0.f;
+#if SSH_WL_KEOGH_FIRST
+            for (int base = 0; base < mp; base += WL_BLK) {
+                if (base) wl_load_smp(cr, mp, base, vc);
+                nbytes += min(WL_BLK, mp - base);
+                acc += wl_smp_block(vc, su, sl, base, mp, sc, lo);
+                tot1 = warp_sum(acc);
+                if (tot1 > T) { pruned = true; break; }
+            }
+            if (pruned) {
+                keo++;
+            } else {
+                acc = 0.f;
+                for (int base = 0; base < mp; base += WL_BLK) {
+                    uint2 ve[4];
+                    wl_load_env(cr, mp, base, ve);
+                    nbytes += 2 * min(WL_BLK, mp - base);
+                    acc += wl_env_block(ve, sq, base, mp, sc, lo);
+                    tot2 = warp_sum(acc);
+                    if (tot2 > T) { pruned = true; break; }
+                }
+                if (pruned) {
+                    keo2++;
+                } else if (lane == 0) {
+#else
             for (int base = 0; base < mp; base += WL_BLK) {
                 if (base) wl_load_env(cr, mp, base, vc);
                 nbytes += 2 * min(WL_BLK, mp - base);
@@ -1123,34 +1193,18 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
                 keo2++;
             } else {
                 acc = 0.f;
-                for (int base = 0; base < mp && !pruned; base += WL_BLK) {
+                for (int base = 0; base < mp; base += WL_BLK) {
                     uint32_t cw[4];
-                    const uint32_t *p = reinterpret_cast<const uint32_t *>(cr + base) + lane;
-#pragma unroll
-                    for (int c = 0; c < 4; c++) cw[c] = base + 128 * c < mp ? __ldg(p + 32 * c) : 0u;
+                    wl_load_smp(cr, mp, base, cw);
                     nbytes += min(WL_BLK, mp - base);
-#pragma unroll
-                    for (int c = 0; c < 4; c++) {
-                        const int i0 = base + 128 * c + 4 * lane;
-                        if (base + 128 * c < mp) {
-                            const float4 u4 = *reinterpret_cast<const float4 *>(su + i0);
-                            const float4 l4 = *reinterpret_cast<const float4 *>(sl + i0);
-                            const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-                            for (int t = 0; t < 4; t++) {
-                                const float cf = code_f(cw[c], t);
-                                const float xa = fmaf(cf, sc, lo), xb = fmaf(cf + 1.f, sc, lo);
-                                const float d = fmaxf(fmaxf(xa - uu[t], ll[t] - xb), 0.f);
-                                acc = fmaf(d, d, acc);
-                            }
-                        }
-                    }
+                    acc += wl_smp_block(cw, su, sl, base, mp, sc, lo);
                     tot1 = warp_sum(acc);
-                    if (tot1 > T) pruned = true;
+                    if (tot1 > T) { pruned = true; break; }
                 }
                 if (pruned) {
                     keo++;
                 } else if (lane == 0) {
+#endif
                     const int p = atomicAdd(&a.wcnt[slot], 1);
                     if (p < a.wcap) {
                         a.wrows[(int64_t)slot * a.wcap + p] = rc;
@@ -1478,6 +1532,9 @@ struct DtwCommon {
 
 #define DP_WARPS 4
 #define DP_MAXPASS 64  // longest pooled row pass
+#ifndef SSH_DTW_PASS_DOUBLING
+#define SSH_DTW_PASS_DOUBLING 0
+#endif
 
 // rows [a, b) of one lane's candidate; returns whether it is still alive
 template <int R>
@@ -1660,11 +1717,10 @@ dtwp_first_kernel(DtwCommon C, const int *__restrict__ act, const uint32_t *__re
 
 // later passes over the pooled survivors of all queries (persistent grid)
 template <int R>
-__global__ void __launch_bounds__(32 * DP_WARPS)
-dtwp_pass_kernel(DtwCommon C, DtwPool in, DtwPool P, int a, int b) {
+__device__ __forceinline__ void dtwp_pass_body(const DtwCommon &C, const DtwPool &in, const DtwPool &P, int a, int b,
+                                               int n) {
     constexpr int NB = 2 * R + 1;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int n = min(*in.count, (int)in.cap);
     unsigned long long cal = 0, cex = 0;
     for (int e0 = (blockIdx.x * DP_WARPS + w) * 32; e0 < n; e0 += gridDim.x * DP_WARPS * 32) {
         const int e = e0 + lane;
@@ -1697,6 +1753,169 @@ dtwp_pass_kernel(DtwCommon C, DtwPool in, DtwPool P, int a, int b) {
         dtwp_emit<R>(C, P, alive, b >= C.m, q, row, oi, band, remk, rem2, slk, sl2, lo, sc);
     }
     dtwp_flush(C, cal, cex);
+}
+
+// Tail of a pooled wave: once fewer than `lim` candidates are left, the
+// remaining rows [a, m) of each run in one launch, one warp per candidate,
+// as an anti-diagonal wavefront (lane l owns rows a + l, a + l + 32, ...,
+// starting two steps behind lane l - 1 and computing two band cells per step,
+// so a row of NB = 2R + 1 cells takes R + 1 steps and a round of 32 rows 64).
+// The cell above arrives by shuffle from lane l - 1 (lane 0: lane 31 of the
+// previous round, or the pooled band of row a - 1 in the first round).  Cells
+// are the pooled kernel's fmaf(d, d, min(diag, up, left)), so the distance is
+// the same fp32 value; a lane checks the cumulative bound of dtwp_rows when
+// its row ends, with the LB_Keogh / LB_Keogh2 remainders of its row taken from
+// warp prefix sums of the row / column terms at the start of each round.
+#define DT_WARPS 4
+#ifndef SSH_DTW_TAIL
+#define SSH_DTW_TAIL 2048  // pooled candidates below which the tail kernel takes over
+#endif
+
+__device__ __forceinline__ float warp_incl_scan(float v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float u = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+template <int R>
+__device__ __forceinline__ void dtwt_body(const DtwCommon &C, const DtwPool &in, int a, int n, float *dtsm) {
+    constexpr int NB = 2 * R + 1, NP = R + 1;  // pairs per row; the last pair's second cell is out of band
+    static_assert(NP <= 63, "a row must end before its lane's next round");
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int m = C.m, YP = C.YP;
+    const int stride = YP + 2 * 64 + 4;
+    float *ys = dtsm + (size_t)w * stride;
+    float *bs = ys + YP;
+    const int rows = m - a, rounds = (rows + 31) >> 5;
+    const int last_t = 64 * (rounds - 1) + 62 + NP - 1;
+    const int owner = (m - 1 - a) & 31;
+    unsigned long long cal = 0, cex = 0;
+    for (int e = blockIdx.x * DT_WARPS + w; e < n; e += gridDim.x * DT_WARPS) {
+        const int q = in.q[e];
+        const uint32_t row = in.row[e];
+        const int64_t oi = in.out[e];
+        float remk = in.st[0 * in.cap + e], rem2 = in.st[1 * in.cap + e];
+        const float slk = in.st[2 * in.cap + e], sl2 = in.st[3 * in.cap + e];
+        const float lo = in.st[4 * in.cap + e], sc = in.st[5 * in.cap + e];
+        const float T = C.thr[q];
+        const float *yq = C.qpad + (int64_t)q * YP;
+        __syncwarp();
+        for (int t = lane; t < YP; t += 32) ys[t] = __ldg(yq + t);
+        for (int k = lane; k < 2 * 64 + 4; k += 32) bs[k] = k < NB ? in.band[(int64_t)k * in.cap + e] : INFINITY;
+        __syncwarp();
+        const float *xp = C.X + (int64_t)row * m;
+        const uint8_t *env = C.codes + (int64_t)row * C.cstride + C.mp;
+        const float *uq = C.U + (int64_t)q * m, *lq = C.Lo + (int64_t)q * m;
+        // row / column inputs of this lane's row in the next round (prefetched a round ahead)
+        float xn = 0.f, un = 0.f, ln = 0.f;
+        uint32_t en = 0;
+        auto fetch = [&](int i) {
+            xn = 0.f;
+            un = 0.f;
+            ln = 0.f;
+            en = 0;
+            if (i < m) {
+                xn = __ldg(xp + i);
+                un = __ldg(uq + i);
+                ln = __ldg(lq + i);
+                if (i + R < m) en = *reinterpret_cast<const unsigned short *>(env + 2 * (i + R));
+            }
+        };
+        fetch(a + lane);
+        float xr = 0.f, rk = 0.f, r2 = 0.f;
+        float2 rp = lane == 0 ? make_float2(bs[0], bs[1]) : make_float2(INFINITY, INFINITY);
+        float c0 = INFINITY, c1 = INFINITY, left = INFINITY, rmn = INFINITY, res = INFINITY;
+        bool cut = false, ab = false;
+        const int kend = (last_t + 64) >> 6;  // rows of the last round drain into one more
+        for (int k = 0; k < kend; k++) {
+            // round k: LB_Keogh / LB_Keogh2 remainders after rows a + 32 k + lane
+            const int ik = a + 32 * k + lane;
+            const float xrn = xn;
+            float kt = 0.f, ct = 0.f;
+            if (ik < m) {
+                const float g = fmaxf(fmaxf(xn - un, ln - xn), 0.f);
+                kt = g * g;
+                if (ik + R < m) {
+                    const float qj = ys[ik + 2 * R];
+                    const float ue = fmaf((float)(en & 0xFFu), sc, lo), le = fmaf((float)(en >> 8), sc, lo);
+                    const float dd = fmaxf(fmaxf(qj - ue, le - qj), 0.f);
+                    ct = dd * dd;
+                }
+            }
+            fetch(ik + 32);
+            kt = warp_incl_scan(kt);
+            ct = warp_incl_scan(ct);
+            const float rkn = remk - kt, r2n = rem2 - ct;
+            remk -= __shfl_sync(0xFFFFFFFFu, kt, 31);
+            rem2 -= __shfl_sync(0xFFFFFFFFu, ct, 31);
+            const int send = min(64, last_t + 1 - 64 * k);
+            for (int s0 = 0; s0 < send; s0 += 8) {
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int s = s0 + u;
+                    // the pair lane - 1 produced last step (lane 0, first round: the pooled band)
+                    const float2 bb = reinterpret_cast<const float2 *>(bs)[min(s + 1, 63)];
+                    const bool fromb = (k == 0) & (lane == 0);
+                    float rx = __shfl_sync(0xFFFFFFFFu, c0, (lane + 31) & 31);
+                    float ry = __shfl_sync(0xFFFFFFFFu, c1, (lane + 31) & 31);
+                    rx = fromb ? bb.x : rx;
+                    ry = fromb ? bb.y : ry;
+                    const int d = s - 2 * lane;  // >= 0: this round's row, else the previous round's
+                    const int sp = d & 63;
+                    const int i = ik - (d < 0 ? 32 : 0);
+                    const bool act = (s < send) & (sp < NP) & (i < m) & (i >= a);
+                    const bool st0 = d == 0;
+                    xr = st0 ? xrn : xr;
+                    rk = st0 ? rkn : rk;
+                    r2 = st0 ? r2n : r2;
+                    left = st0 ? INFINITY : left;
+                    rmn = st0 ? INFINITY : rmn;
+                    const int yi = act ? i + 2 * sp : 0;
+                    const float d0 = xr - ys[yi], d1 = xr - ys[yi + 1];
+                    const float n0 = fmaf(d0, d0, fminf(fminf(rp.x, rp.y), left));
+                    const float n1 = fmaf(d1, d1, fminf(fminf(rp.y, rx), n0));
+                    c0 = act ? n0 : INFINITY;
+                    c1 = (act && sp < NP - 1) ? n1 : INFINITY;
+                    left = c1;
+                    rmn = fminf(rmn, fminf(c0, c1));
+                    res = (act & (i == m - 1) & (sp == (R >> 1))) ? ((R & 1) ? c1 : c0) : res;
+                    cut |= act & (sp == NP - 1) & (rmn + fmaxf(fmaxf(rk - slk, r2 - sl2), 0.f) > T);
+                    cal += act ? ((sp < NP - 1) ? 2 : 1) : 0;
+                    rp = make_float2(rx, ry);
+                }
+                if (__any_sync(0xFFFFFFFFu, cut)) {
+                    ab = true;
+                    cex += 2 * (64 * k + s0 + 8);
+                    break;
+                }
+            }
+            if (ab) break;
+        }
+        if (ab) {
+            if (lane == 0 && C.abandoned) atomicAdd(&C.abandoned[q], 1ull);
+        } else {
+            cex += 2 * (last_t + 1);
+            res = __shfl_sync(0xFFFFFFFFu, res, owner);
+            if (lane == 0) C.out[oi] = res;
+        }
+    }
+    dtwp_flush(C, cal, cex);
+}
+
+// one pooled level: rows [a, b) of every pooled candidate, or, once fewer
+// than lim are left, all remaining rows [a, m) in the wavefront tail
+template <int R>
+__global__ void __launch_bounds__(32 * DP_WARPS)
+dtwp_level_kernel(DtwCommon C, DtwPool in, DtwPool P, int a, int b, int lim) {
+    extern __shared__ __align__(16) float dtsm[];
+    const int n = min(*in.count, (int)in.cap);
+    if (n == 0) return;
+    if (n < lim) dtwt_body<R>(C, in, a, n, dtsm);
+    else dtwp_pass_body<R>(C, in, P, a, b, n);
 }
 
 // padded query copies for the pooled DTW: qpad[q][t] = y[t - R] (+inf outside)
@@ -2168,6 +2387,9 @@ struct Carver {
 
 #define SSH_MEMBER_BUDGET ((int64_t)1 << 29)  // members per sub-range (8 GiB of lists)
 #define SSH_MEMBER_TARGET 65536               // round-0 members per query (sampled cutoff)
+#ifndef SSH_WAVE_GROWTH
+#define SSH_WAVE_GROWTH 8                     // wave size multiplier
+#endif
 
 struct QueryBufs {
     uint64_t *qsig, *qbits, *bstart;
@@ -2395,8 +2617,10 @@ static int launch_dtw_pooled(ssh_ctx *ctx, const DtwCommon &C, const int *act, c
     int *cnt = (int *)ssh_slot(ctx, SLOT_Q_POOLCNT, 64 * sizeof(int), st);
     if (!cnt) return SSH_ERR_OOM;
     const int m = C.m;
-    // pass ends 8, 16, 32, 64, then every DP_MAXPASS rows
-    auto next_end = [&](int a) { return std::min(m, a < DP_MAXPASS ? 2 * a : a + DP_MAXPASS); };
+    // pass ends 8, 16, 32, 64, then every DP_MAXPASS rows (or doubling)
+    auto next_end = [&](int a) {
+        return std::min(m, (a < DP_MAXPASS || SSH_DTW_PASS_DOUBLING) ? 2 * a : a + DP_MAXPASS);
+    };
     int nlev = 1;
     for (int a = std::min(m, 8); a < m; a = next_end(a)) nlev++;
     SSH_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * nlev, st));
@@ -2405,10 +2629,27 @@ static int launch_dtw_pooled(ssh_ctx *ctx, const DtwCommon &C, const int *act, c
     dim3 g1((unsigned)ssh_div_up(wave, 32 * DP_WARPS), (unsigned)nact);
     dtwp_first_kernel<R><<<g1, 32 * DP_WARPS, 0, st>>>(C, act, wrows, wlb, wcnt, wcap, rec, b0, pool[0]);
     SSH_CHECK_LAUNCH();
+    // the wavefront tail (per-warp staged query + band) once fewer than lim are left
+    const size_t tail_smem = sizeof(float) * (size_t)DT_WARPS * (C.YP + 2 * 64 + 4);
+    const int lim = tail_smem <= 160 * 1024 ? SSH_DTW_TAIL : 0;
+    const size_t lsmem = lim ? tail_smem : 0;
+    static size_t attr_smem = 0;
     static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtwp_pass_kernel<R>, 32 * DP_WARPS, 0);
+    static size_t per_sm_smem = ~(size_t)0;
+    if (lsmem > attr_smem) {
+        SSH_CUDA(cudaFuncSetAttribute(dtwp_level_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
+        attr_smem = lsmem;
+    }
+    if (per_sm_smem != lsmem) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtwp_level_kernel<R>, 32 * DP_WARPS, lsmem);
         per_sm = std::max(1, per_sm);
+        per_sm_smem = lsmem;
+    }
+    static const bool dbg = getenv("SSH_DEBUG_DTW_PASSES") != nullptr;
+    cudaEvent_t ev[66];
+    if (dbg) {
+        for (int i = 0; i <= nlev; i++) cudaEventCreate(&ev[i]);
+        cudaEventRecord(ev[0], st);
     }
     int lev = 1;
     for (int a = b0; a < m; lev++) {
@@ -2416,9 +2657,26 @@ static int launch_dtw_pooled(ssh_ctx *ctx, const DtwCommon &C, const int *act, c
         DtwPool in = pool[(lev - 1) & 1], out = pool[lev & 1];
         in.count = cnt + lev - 1;
         out.count = cnt + lev;
-        dtwp_pass_kernel<R><<<ctx->num_sms * per_sm, 32 * DP_WARPS, 0, st>>>(C, in, out, a, b);
+        if (dbg) cudaEventRecord(ev[lev], st);
+        dtwp_level_kernel<R><<<ctx->num_sms * per_sm, 32 * DP_WARPS, lsmem, st>>>(C, in, out, a, b, lim);
         SSH_CHECK_LAUNCH();
         a = b;
+    }
+    if (dbg) {
+        cudaEventRecord(ev[lev], st);
+        cudaEventSynchronize(ev[lev]);
+        std::vector<int> hc(nlev);
+        cudaMemcpy(hc.data(), cnt, sizeof(int) * nlev, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "dtw pooled: nact %d wave %d |", nact, wave);
+        for (int i = 1; i < lev; i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            fprintf(stderr, " [%d items %.3f ms]", hc[i - 1], ms);
+        }
+        float f0 = 0.f;
+        cudaEventElapsedTime(&f0, ev[0], ev[1]);
+        fprintf(stderr, " first %.3f ms\n", f0);
+        for (int i = 0; i <= nlev; i++) cudaEventDestroy(ev[i]);
     }
     return SSH_OK;
 }
@@ -2574,7 +2832,10 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     const int m = ctx->p.m, r = ctx->p.radius, L = ix->L, nseg = ix->nseg;
     const int64_t N = ix->N, NW = (N + 31) / 32;
     const float eps = rescore_eps(m);
-    const int W0 = ((std::max(64, 2 * k) + 31) / 32) * 32;
+#ifndef SSH_W0
+#define SSH_W0 64
+#endif
+    const int W0 = ((std::max(SSH_W0, 2 * k) + 31) / 32) * 32;
     const int WCAP = std::max(W0, 16384);
     const int KCAP = 4096 + 4 * k;
     const int fallback = (flags & SSH_QUERY_FALLBACK_ON_EMPTY) ? 1 : 0;
@@ -2731,7 +2992,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                 WaveLbArgs wl{Qs, S.U, S.Lo, (const uint4 *)ix->rec, ix->codes, ix->cstride, rows_s, lb_s, S.roff,
                               S.mcnt, S.pos, S.done, S.thr, S.act, wrows, wlb, S.wcnt, c5s,
                               ctx->profile ? ctx->d_cells : nullptr, m, ix->mp, W0, WCAP};
-                for (int wave = W0, it = 0; nact > 0; wave *= 2, it++) {
+                for (int wave = W0, it = 0; nact > 0; wave *= SSH_WAVE_GROWTH, it++) {
                     const int wcap = (int)std::min<int64_t>((int64_t)1 << 20, (pool / nact) & ~(int64_t)255);
                     wave = std::min(wave, wcap);
                     pf.begin();
