@@ -27,6 +27,7 @@
 #include <float.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -45,6 +46,8 @@ struct SigArgs {
     uint64_t *sig_out;
     const double *lna1, *tr, *tlnc, *tbeta, *lnw;
     const void *rank;  // per-slot rank of ln_a1: u16 (n <= 16) or u32
+    const uint16_t *rankp;  // order-free path: u16 ranks, 16*QL slots per token row
+    const uint16_t *inv;    // order-free path: (slot << n | rank) -> token
     int64_t N;
     int words, nb, n, T, P2, H, S, L, K;
     int warp_smem;  // bytes per warp
@@ -518,6 +521,340 @@ __device__ void warp_cws(const SigArgs &a, int64_t row, const WarpSmem &w, int D
     __syncwarp();
 }
 
+// ---------------------------------------------------------------- order-free CWS
+// The argmin of every slot only needs the distinct tokens and their counts,
+// not np.unique's order: ties are broken by comparing tokens (lowest wins =
+// np.argmin's first occurrence over sorted tokens), and the count-1 argmin is
+// an integer min over ln_a1 ranks, which are a total order by (value, token).
+// This path (n <= 15, S = K*L <= 16*QL, T <= 1024) therefore
+//   * dedups without a global sort: the first 32V tokens are sorted in
+//     registers (run starts give their counts), the remaining tokens are
+//     merged 32 at a time (match_any inside the chunk, binary search in the
+//     sorted part, linear search among tokens appended earlier);
+//   * takes the count-1 minimum with two lanes per token row (lane half h
+//     loads 8*QL u16 ranks as QL 16-byte vectors) and packed u16x2 minima,
+//     then a reduce-scatter across the 16 token lanes; the winning rank maps
+//     back to its token through the inverse table, and its ln_a1 seeds the
+//     per-slot best;
+//   * evaluates count > 1 tokens with the full formula (wmh.py:74-76) with
+//     lanes owning slots, as before.
+
+template <int V>
+__device__ int warp_dedup_split(const SigArgs &a, int64_t row, const WarpSmem &w, int lane) {
+    uint64_t *wsm = reinterpret_cast<uint64_t *>(w.hkey);
+    for (int i = lane; i < a.words; i += 32) wsm[i] = a.bits[row * a.words + i];
+    __syncwarp();
+    const uint32_t nmask = (1u << a.n) - 1u;  // n <= 15 on this path
+    const int TM = min(a.T, 32 * V);
+    const unsigned lt0 = (1u << lane) - 1u;
+    uint32_t x[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        const int e = lane * V + v;
+        uint32_t tok = 0xFFFFFFFFu;
+        if (e < TM) {
+            const int wi = e >> 6, sh = e & 63;
+            const uint64_t w0 = wsm[wi], w1 = wi + 1 < a.words ? wsm[wi + 1] : 0ULL;
+            const uint64_t bitsv = sh ? ((w0 >> sh) | (w1 << (64 - sh))) : w0;
+            tok = __brev((uint32_t)bitsv & nmask) >> (32 - a.n);
+        }
+        x[v] = tok;
+    }
+    warp_sort_regs<V>(x, lane);
+    const uint32_t pv = __shfl_up_sync(0xFFFFFFFFu, x[V - 1], 1);
+    unsigned smask = 0;
+    int c = 0;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        const uint32_t prev = v ? x[v - 1] : pv;
+        const bool st = x[v] != 0xFFFFFFFFu && (lane * V + v == 0 || x[v] != prev);
+        smask |= (unsigned)st << v;
+        c += st;
+    }
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    int D = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    int d = incl - c;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        if ((smask >> v) & 1u) {
+            w.utok[d] = x[v];
+            w.ustart[d] = (uint16_t)(lane * V + v);
+            d++;
+        }
+    }
+    if (lane == 0) w.ustart[D] = (uint16_t)TM;
+    __syncwarp();
+    for (int k = lane; k < D; k += 32) {
+        const uint32_t cnt = (uint32_t)w.ustart[k + 1] - (uint32_t)w.ustart[k];
+        w.ukey[k] = (w.utok[k] << 12) | cnt;
+    }
+    __syncwarp();
+    const int Dm = D;
+    for (int c0 = 32 * V; c0 < a.T; c0 += 32) {
+        const int e = c0 + lane;
+        uint32_t tok = 0xFFFFFFFFu;
+        if (e < a.T) {
+            const int wi = e >> 6, sh = e & 63;
+            const uint64_t w0 = wsm[wi], w1 = wi + 1 < a.words ? wsm[wi + 1] : 0ULL;
+            const uint64_t bitsv = sh ? ((w0 >> sh) | (w1 << (64 - sh))) : w0;
+            tok = __brev((uint32_t)bitsv & nmask) >> (32 - a.n);
+        }
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, tok);
+        bool need = false;
+        if (tok != 0xFFFFFFFFu && (peers & lt0) == 0) {
+            const uint32_t add = __popc(peers);
+            int lo = 0, hi = Dm;  // first entry with token >= tok
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((w.ukey[mid] >> 12) < tok) lo = mid + 1;
+                else hi = mid;
+            }
+            int pos = -1;
+            if (lo < Dm && (w.ukey[lo] >> 12) == tok) pos = lo;
+            for (int q = Dm; pos < 0 && q < D; q++)
+                if ((w.ukey[q] >> 12) == tok) pos = q;
+            if (pos >= 0) w.ukey[pos] += add;  // leaders hold distinct tokens
+            else need = true;
+        }
+        const unsigned nm = __ballot_sync(0xFFFFFFFFu, need);
+        if (need) w.ukey[D + __popc(nm & lt0)] = (tok << 12) | __popc(peers);
+        D += __popc(nm);
+        __syncwarp();
+    }
+    return D;
+}
+
+// reduce-scatter of A packed u16x2 minima over the lane bits M, M/2, .., 1:
+// halve while A is even (a lane keeps the half selected by its bit), then a
+// full butterfly on the rest.  base = original index of x[0].
+__host__ __device__ constexpr int rs_final(int A, int M) {
+    return (M == 0 || (A & 1)) ? A : rs_final(A / 2, M / 2);
+}
+__host__ __device__ constexpr int rs_group(int A, int M) {  // lanes sharing a result
+    return M == 0 ? 1 : ((A & 1) ? 2 * M : rs_group(A / 2, M / 2));
+}
+
+template <int A, int M>
+__device__ __forceinline__ void rs_reduce(uint32_t (&x)[A], int lane, int &base) {
+    if constexpr (M == 0) {
+        return;
+    } else if constexpr ((A & 1) == 0) {
+        constexpr int H = A / 2;
+        const bool hi = (lane & M) != 0;
+        uint32_t y[H];
+#pragma unroll
+        for (int i = 0; i < H; i++) {
+            const uint32_t send = hi ? x[i] : x[i + H];
+            const uint32_t keep = hi ? x[i + H] : x[i];
+            y[i] = __vminu2(keep, __shfl_xor_sync(0xFFFFFFFFu, send, M));
+        }
+        if (hi) base += H;
+        rs_reduce<H, M / 2>(y, lane, base);
+#pragma unroll
+        for (int i = 0; i < H; i++) x[i] = y[i];
+    } else {
+#pragma unroll
+        for (int mm = M; mm >= 1; mm >>= 1)
+#pragma unroll
+            for (int i = 0; i < A; i++) x[i] = __vminu2(x[i], __shfl_xor_sync(0xFFFFFFFFu, x[i], mm));
+    }
+}
+
+template <int QL>
+__device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, int D, int lane) {
+    constexpr int NS = (16 * QL + 31) / 32;
+    constexpr int A = 4 * QL;
+    const int S = a.S;
+    uint16_t *list1 = w.ustart;
+    uint16_t *listm = w.ucnt;
+    int n1 = 0, nm = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = 0; base < D; base += 32) {
+        const int d = base + lane;
+        const uint32_t key = d < D ? w.ukey[d] : 0u;
+        const bool one = d < D && (key & 0xFFFu) == 1u;
+        const bool many = d < D && (key & 0xFFFu) > 1u;
+        const unsigned m1 = __ballot_sync(0xFFFFFFFFu, one);
+        const unsigned mm = __ballot_sync(0xFFFFFFFFu, many);
+        if (one) list1[n1 + __popc(m1 & lt)] = (uint16_t)d;
+        if (many) listm[nm + __popc(mm & lt)] = (uint16_t)d;
+        n1 += __popc(m1);
+        nm += __popc(mm);
+    }
+    __syncwarp();
+    // count-1 tokens: packed u16x2 rank minima, lane = (row half h, token j)
+    const int h = lane >> 4, j = lane & 15;
+    uint32_t acc[A];
+#pragma unroll
+    for (int i = 0; i < A; i++) acc[i] = 0xFFFFFFFFu;
+    const uint4 *rp = reinterpret_cast<const uint4 *>(a.rankp);
+    for (int e0 = 0; e0 < n1; e0 += 32) {
+        const int ea = e0 + j, eb = e0 + 16 + j;
+        uint4 va[QL], vb[QL];
+        const uint4 ff = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        const size_t ba = ea < n1 ? (size_t)(w.ukey[list1[ea]] >> 12) * (2 * QL) + h * QL : 0;
+        const size_t bb = eb < n1 ? (size_t)(w.ukey[list1[eb]] >> 12) * (2 * QL) + h * QL : 0;
+#pragma unroll
+        for (int q = 0; q < QL; q++) va[q] = ea < n1 ? __ldg(rp + ba + q) : ff;
+#pragma unroll
+        for (int q = 0; q < QL; q++) vb[q] = eb < n1 ? __ldg(rp + bb + q) : ff;
+#pragma unroll
+        for (int q = 0; q < QL; q++) {
+            acc[4 * q + 0] = __vminu2(acc[4 * q + 0], __vminu2(va[q].x, vb[q].x));
+            acc[4 * q + 1] = __vminu2(acc[4 * q + 1], __vminu2(va[q].y, vb[q].y));
+            acc[4 * q + 2] = __vminu2(acc[4 * q + 2], __vminu2(va[q].z, vb[q].z));
+            acc[4 * q + 3] = __vminu2(acc[4 * q + 3], __vminu2(va[q].w, vb[q].w));
+        }
+    }
+    int rbase = 0;
+    rs_reduce<A, 8>(acc, lane, rbase);
+    constexpr int AF = rs_final(A, 8);
+    constexpr int G = rs_group(A, 8);
+    double *bv = reinterpret_cast<double *>(w.keys);  // S entries, rewritten as keys below
+    uint32_t *bt = w.hkey;                              // S entries
+#pragma unroll
+    for (int l = 0; l < 2 * AF; l++) {
+        if (l % G == (j & (G - 1))) {
+            const int r = rbase + (l >> 1), hw = l & 1;
+            const int s = 8 * QL * h + 2 * r + hw;
+            if (s < S) {
+                const uint32_t rk = (acc[l >> 1] >> (16 * hw)) & 0xFFFFu;
+                double v = (double)INFINITY;
+                uint32_t tok = 0xFFFFFFFFu;
+                if (rk != 0xFFFFu) {
+                    tok = __ldg(a.inv + (((size_t)s << a.n) | rk));
+                    v = __ldg(a.lna1 + (size_t)tok * S + s);
+                }
+                bv[s] = v;
+                bt[s] = tok;
+            }
+        }
+    }
+    __syncwarp();
+    double best[NS];
+    uint32_t btok[NS], bcnt[NS];
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+        const int s = lane + 32 * i;
+        best[i] = s < S ? bv[s] : (double)INFINITY;
+        btok[i] = s < S ? bt[s] : 0xFFFFFFFFu;
+        bcnt[i] = 1u;
+    }
+    // count > 1 tokens: full formula, ties toward the lower token
+    for (int f = 0; f < nm; f++) {
+        const uint32_t key = w.ukey[listm[f]];
+        const uint32_t tok = key >> 12, cnt = key & 0xFFFu;
+        const size_t base = (size_t)tok * S;
+        const double lw = __ldg(a.lnw + cnt);
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+            const int s = lane + 32 * i;
+            if (s < S) {
+                const double r = __ldg(a.tr + base + s);
+                const double lnc = __ldg(a.tlnc + base + s), b = __ldg(a.tbeta + base + s);
+                const double v = cws_lna(cws_t(lw, r, b), r, lnc, b);
+                const bool l = v < best[i] || (v == best[i] && tok < btok[i]);
+                best[i] = l ? v : best[i];
+                btok[i] = l ? tok : btok[i];
+                bcnt[i] = l ? cnt : bcnt[i];
+            }
+        }
+    }
+    // winners -> keys (wmh.py:79-81); bv is dead from here on
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+        const int s = lane + 32 * i;
+        if (s < S) {
+            const uint32_t tok = btok[i], cnt = bcnt[i];
+            const size_t ent = (size_t)tok * S + s;
+            const double b = __ldg(a.tbeta + ent);
+            double t;
+            if (cnt == 1u) t = floor(b);  // fl(0/r + b) = b
+            else t = cws_t(__ldg(a.lnw + cnt), __ldg(a.tr + ent), b);
+            const uint64_t tt = (uint64_t)(int64_t)t;
+            const uint64_t k64 = ssh_mix64((uint64_t)tok ^ ssh_mix64(tt ^ SSH_SALT_KEY));
+            w.keys[s] = k64;
+            if (a.keys_out) a.keys_out[row * S + s] = k64;
+        }
+    }
+    __syncwarp();
+    for (int jj = lane; jj < a.L; jj += 32) {
+        uint64_t acc64 = w.keys[jj * a.K];
+        for (int i = 1; i < a.K; i++) acc64 = ssh_mix64(acc64 ^ w.keys[jj * a.K + i]);
+        a.sig_out[row * a.L + jj] = acc64;
+    }
+    __syncwarp();
+}
+
+template <int MODE, int QL, int V>
+__global__ void __launch_bounds__(32 * SG_WARPS, 3) cws_fast_kernel(SigArgs a, int warps) {
+    extern __shared__ __align__(16) unsigned char sg_smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    WarpSmem w = carve(sg_smem + (size_t)wid * a.warp_smem, a);
+    const int64_t nwarps = (int64_t)gridDim.x * warps;
+    for (int64_t row = (int64_t)blockIdx.x * warps + wid; row < a.N; row += nwarps) {
+        int D;
+        if (MODE == SIG_MODE_CWS_FROM_SETS) {
+            D = a.len_in[row];
+            for (int d = lane; d < D; d += 32)
+                w.ukey[d] = (a.tok_in[row * a.T + d] << 12) | (uint32_t)a.cnt_in[row * a.T + d];
+            __syncwarp();
+        } else {
+            D = warp_dedup_split<V>(a, row, w, lane);
+        }
+        warp_cws_fast<QL>(a, row, w, D, lane);
+    }
+}
+
+template <int MODE, int QL, int V>
+static int launch_fast(ssh_ctx *ctx, const SigArgs &a, int64_t N, cudaStream_t st) {
+    auto kern = cws_fast_kernel<MODE, QL, V>;
+    int warps = SG_WARPS;
+    while (warps > 1 && (size_t)a.warp_smem * warps > 200 * 1024) warps--;
+    size_t smem = (size_t)a.warp_smem * warps;
+    SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t nblk = (N + warps - 1) / warps;
+    const int grid = (int)std::min<int64_t>(nblk, (int64_t)ctx->num_sms * per_sm);
+    kern<<<grid, 32 * warps, smem, st>>>(a, warps);
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
+template <int MODE, int QL>
+static int launch_fast_v(ssh_ctx *ctx, const SigArgs &a, int64_t N, cudaStream_t st) {
+    if (MODE == SIG_MODE_CWS_FROM_SETS) return launch_fast<MODE, QL, 1>(ctx, a, N, st);
+    const int v = a.T / 32;
+    if (v >= 16) return launch_fast<MODE, QL, 16>(ctx, a, N, st);
+    if (v >= 8) return launch_fast<MODE, QL, 8>(ctx, a, N, st);
+    if (v >= 4) return launch_fast<MODE, QL, 4>(ctx, a, N, st);
+    if (v >= 2) return launch_fast<MODE, QL, 2>(ctx, a, N, st);
+    return launch_fast<MODE, QL, 1>(ctx, a, N, st);
+}
+
+// 1: launched on the order-free path, 0: not applicable, <0: error
+template <int MODE>
+static int try_fast(ssh_ctx *ctx, const SigArgs &a, int64_t N, cudaStream_t st) {
+    if (ctx->rank_ql == 0 || a.T > 1024 || ctx->p.n > 15) return 0;
+    const int region = 8 * a.H > 4 * a.P2 ? 8 * a.H : 4 * a.P2;
+    if (4 * a.S > region) return 0;
+    int rc;
+    switch (ctx->rank_ql) {
+        case 2: rc = launch_fast_v<MODE, 2>(ctx, a, N, st); break;
+        case 5: rc = launch_fast_v<MODE, 5>(ctx, a, N, st); break;
+        default: return 0;
+    }
+    return rc == SSH_OK ? 1 : rc;
+}
+
 template <int MODE, int NS>
 __global__ void __launch_bounds__(32 * SG_WARPS, 4) shingle_cws_kernel(SigArgs a, int warps) {
     extern __shared__ __align__(16) unsigned char sg_smem[];
@@ -597,6 +934,15 @@ static int launch_sig_ns(ssh_ctx *ctx, const SigArgs &a, int64_t N, cudaStream_t
     }
 }
 
+// SSH_CWS_FAST=0 selects the sorted-set kernel (A/B comparisons, tests)
+static bool ssh_cws_fast_disabled() {
+    static const int off = [] {
+        const char *e = getenv("SSH_CWS_FAST");
+        return (e && e[0] == '0') ? 1 : 0;
+    }();
+    return off != 0;
+}
+
 int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *tok_in,
                            const uint16_t *cnt_in, const int32_t *len_in, int64_t N,
                            uint32_t *tok_out, uint16_t *cnt_out, int32_t *len_out,
@@ -608,6 +954,8 @@ int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *t
     a.lna1 = ctx->d_lna1; a.tr = ctx->d_r; a.tlnc = ctx->d_lnc; a.tbeta = ctx->d_beta;
     a.lnw = ctx->d_lnw;
     a.rank = ctx->d_rank;
+    a.rankp = ctx->d_rankp;
+    a.inv = ctx->d_inv;
     a.N = N; a.words = ctx->words; a.nb = ctx->nb; a.n = ctx->p.n; a.T = ctx->T;
     int P2 = 32;
     while (P2 < ctx->T) P2 <<= 1;
@@ -616,6 +964,11 @@ int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *t
     a.S = ctx->S; a.L = ctx->p.L; a.K = ctx->p.K;
     a.warp_smem = warp_smem_bytes(a.S, a.P2, a.H, a.T);
     if (mode == SIG_MODE_SHINGLE) return launch_sig<SIG_MODE_SHINGLE, 1>(ctx, a, N, st);
+    if (!ssh_cws_fast_disabled()) {
+        const int f = mode == SIG_MODE_CWS_FROM_SETS ? try_fast<SIG_MODE_CWS_FROM_SETS>(ctx, a, N, st)
+                                                     : try_fast<SIG_MODE_FUSED>(ctx, a, N, st);
+        if (f != 0) return f > 0 ? SSH_OK : f;
+    }
     if (mode == SIG_MODE_CWS_FROM_SETS) return launch_sig_ns<SIG_MODE_CWS_FROM_SETS>(ctx, a, N, st);
     return launch_sig_ns<SIG_MODE_FUSED>(ctx, a, N, st);
 }

@@ -538,6 +538,26 @@ __global__ void rank_scatter_kernel(const uint32_t *__restrict__ rows, int64_t T
     }
 }
 
+// Order-free CWS tables (signature.cu, cws_fast): padded u16 ranks per token
+// row and the inverse map (slot, rank) -> token.
+__global__ void rank_fast_kernel(const uint32_t *__restrict__ rows, int64_t T, int S, int SP,
+                                 uint16_t *__restrict__ rankp, uint16_t *__restrict__ inv) {
+    const int64_t n = T * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / T, p = e - j * T;
+        const uint32_t tok = rows[e];
+        rankp[(int64_t)tok * SP + j] = (uint16_t)p;
+        inv[e] = (uint16_t)tok;
+    }
+}
+
+static int pick_rank_ql(int S) {
+    const int q = (S + 15) / 16;
+    if (q <= 6) return q;
+    if (q <= 8) return 8;
+    return 0;
+}
+
 int ssh_build_ranks(ssh_ctx *ctx, cudaStream_t st) {
     const int64_t T = (int64_t)1 << ctx->p.n;
     const int S = ctx->S;
@@ -558,8 +578,22 @@ int ssh_build_ranks(ssh_ctx *ctx, cudaStream_t st) {
             rank_scatter_kernel<uint32_t><<<grid, 256, 0, st>>>(rows, T, S, (uint32_t *)ctx->d_rank);
         }
         ssh_count_launch();
+        const int ql = ctx->p.n <= 15 ? pick_rank_ql(S) : 0;
+        if (ql > 0) {
+            const int SP = 16 * ql;
+            cudaError_t e = cudaMalloc(&ctx->d_rankp, sizeof(uint16_t) * (size_t)T * SP);
+            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_inv, sizeof(uint16_t) * n);
+            if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_rankp, 0xFF, sizeof(uint16_t) * (size_t)T * SP, st);
+            if (e == cudaSuccess) {
+                rank_fast_kernel<<<grid, 256, 0, st>>>(rows, T, S, SP, ctx->d_rankp, ctx->d_inv);
+                ssh_count_launch();
+                e = cudaGetLastError();
+            }
+            if (e != cudaSuccess) rc = ssh_cuda_fail(e, "ssh_build_ranks(fast tables)", __FILE__, __LINE__);
+            else ctx->rank_ql = ql;
+        }
         cudaError_t e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) rc = ssh_cuda_fail(e, "ssh_build_ranks", __FILE__, __LINE__);
+        if (e != cudaSuccess && rc == SSH_OK) rc = ssh_cuda_fail(e, "ssh_build_ranks", __FILE__, __LINE__);
     }
     cudaFree(keys);
     cudaFree(rows);
