@@ -55,10 +55,13 @@ struct ssh_ctx {
     double *d_r = nullptr, *d_lnc = nullptr, *d_beta = nullptr, *d_lna1 = nullptr;
     double *d_lnw = nullptr;  // ln(count)
     void *d_rank = nullptr;   // per-slot rank of ln_a1 by (value, token): u16 (n <= 16) or u32
-    // order-free CWS path (n <= 15, S <= 128; signature.cu): u16 ranks padded to
-    // 16*rank_ql slots per token (pad = 0xFFFF) and the inverse map (slot, rank) -> token
+    // order-free CWS path (n <= 15, S <= 128; signature.cu):
+    //  rankp  u16 ranks padded to 16*rank_ql slots per token row (pad = 0xFFFF)
+    //  byrank per (slot, rank): {f64 ln_a1, u32 token | floor(beta) << 16, pad}
+    //  rlcb   per (token, slot): f64 {r, 1/r, ln c, beta}
     uint16_t *d_rankp = nullptr;
-    uint16_t *d_inv = nullptr;
+    uint4 *d_byrank = nullptr;
+    double *d_rlcb = nullptr;
     int rank_ql = 0;  // 0: path unavailable
     size_t tab_entries = 0;
     // profiling (ssh_ctx_set_profiling)

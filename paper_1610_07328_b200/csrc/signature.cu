@@ -32,6 +32,15 @@
 #include "common.cuh"
 
 #define SG_WARPS 8
+#ifndef SG_FAST_MINB
+#define SG_FAST_MINB 4
+#endif
+#ifndef SG_CWS_U2
+#define SG_CWS_U2 0
+#endif
+#ifndef SG_RANK_U2
+#define SG_RANK_U2 0
+#endif
 #define SG_EMPTY 0xFFFFFFFFu
 
 struct SigArgs {
@@ -47,7 +56,8 @@ struct SigArgs {
     const double *lna1, *tr, *tlnc, *tbeta, *lnw;
     const void *rank;  // per-slot rank of ln_a1: u16 (n <= 16) or u32
     const uint16_t *rankp;  // order-free path: u16 ranks, 16*QL slots per token row
-    const uint16_t *inv;    // order-free path: (slot << n | rank) -> token
+    const uint4 *byrank;    // order-free path: (slot << n | rank) -> {ln_a1, token | t1 << 16}
+    const double2 *rlcb;    // order-free path: (token, slot) -> {r, 1/r}, {ln c, beta}
     int64_t N;
     int words, nb, n, T, P2, H, S, L, K;
     int warp_smem;  // bytes per warp
@@ -380,6 +390,16 @@ __device__ __forceinline__ double cws_t(double lw, double r, double b) {
     return floor(__dadd_rn(__ddiv_rn(lw, r), b));
 }
 
+// cws_t with a tabulated reciprocal 1/r = fl(1/r): fma(lw, 1/r, b) is within
+// 4u(lw/r + b) of fl(fl(lw/r) + b), far inside the 1e-12 relative guard.
+__device__ __forceinline__ double cws_t_inv(double lw, double r, double rinv, double b) {
+    const double s1 = fma(lw, rinv, b);
+    const double fl = floor(s1);
+    const double tol = s1 * 1e-12;
+    if (s1 - fl > tol && (fl + 1.0) - s1 > tol) return fl;
+    return floor(__dadd_rn(__ddiv_rn(lw, r), b));
+}
+
 __device__ __forceinline__ double cws_lna(double t, double r, double lnc, double b) {
     const double lny = __dmul_rn(r, __dsub_rn(t, b));
     return __dsub_rn(__dsub_rn(lnc, lny), r);
@@ -693,6 +713,7 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
 #pragma unroll
     for (int i = 0; i < A; i++) acc[i] = 0xFFFFFFFFu;
     const uint4 *rp = reinterpret_cast<const uint4 *>(a.rankp);
+#if SG_RANK_U2
     for (int e0 = 0; e0 < n1; e0 += 32) {
         const int ea = e0 + j, eb = e0 + 16 + j;
         uint4 va[QL], vb[QL];
@@ -711,12 +732,28 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
             acc[4 * q + 3] = __vminu2(acc[4 * q + 3], __vminu2(va[q].w, vb[q].w));
         }
     }
+#else
+    for (int e0 = 0; e0 < n1; e0 += 16) {
+        const int ea = e0 + j;
+        if (ea < n1) {
+            const size_t ba = (size_t)(w.ukey[list1[ea]] >> 12) * (2 * QL) + h * QL;
+#pragma unroll
+            for (int q = 0; q < QL; q++) {
+                const uint4 va = __ldg(rp + ba + q);
+                acc[4 * q + 0] = __vminu2(acc[4 * q + 0], va.x);
+                acc[4 * q + 1] = __vminu2(acc[4 * q + 1], va.y);
+                acc[4 * q + 2] = __vminu2(acc[4 * q + 2], va.z);
+                acc[4 * q + 3] = __vminu2(acc[4 * q + 3], va.w);
+            }
+        }
+    }
+#endif
     int rbase = 0;
     rs_reduce<A, 8>(acc, lane, rbase);
     constexpr int AF = rs_final(A, 8);
     constexpr int G = rs_group(A, 8);
     double *bv = reinterpret_cast<double *>(w.keys);  // S entries, rewritten as keys below
-    uint32_t *bt = w.hkey;                              // S entries
+    uint32_t *bt = w.hkey;                              // S entries: token | t1 << 16
 #pragma unroll
     for (int l = 0; l < 2 * AF; l++) {
         if (l % G == (j & (G - 1))) {
@@ -725,43 +762,70 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
             if (s < S) {
                 const uint32_t rk = (acc[l >> 1] >> (16 * hw)) & 0xFFFFu;
                 double v = (double)INFINITY;
-                uint32_t tok = 0xFFFFFFFFu;
+                uint32_t tt = 0xFFFFu;
                 if (rk != 0xFFFFu) {
-                    tok = __ldg(a.inv + (((size_t)s << a.n) | rk));
-                    v = __ldg(a.lna1 + (size_t)tok * S + s);
+                    const uint4 br = __ldg(a.byrank + (((size_t)s << a.n) | rk));
+                    v = __hiloint2double((int)br.y, (int)br.x);
+                    tt = br.z;
                 }
                 bv[s] = v;
-                bt[s] = tok;
+                bt[s] = tt;
             }
         }
     }
     __syncwarp();
-    double best[NS];
-    uint32_t btok[NS], bcnt[NS];
+    double best[NS], bestt[NS];
+    uint32_t btok[NS];
 #pragma unroll
     for (int i = 0; i < NS; i++) {
         const int s = lane + 32 * i;
+        const uint32_t tt = s < S ? bt[s] : 0xFFFFu;
         best[i] = s < S ? bv[s] : (double)INFINITY;
-        btok[i] = s < S ? bt[s] : 0xFFFFFFFFu;
-        bcnt[i] = 1u;
+        btok[i] = tt & 0xFFFFu;
+        bestt[i] = (double)(tt >> 16);
     }
-    // count > 1 tokens: full formula, ties toward the lower token
-    for (int f = 0; f < nm; f++) {
-        const uint32_t key = w.ukey[listm[f]];
-        const uint32_t tok = key >> 12, cnt = key & 0xFFFu;
-        const size_t base = (size_t)tok * S;
-        const double lw = __ldg(a.lnw + cnt);
+    // count > 1 tokens: full formula, ties toward the lower token; two tokens
+    // per step keep their twelve variate loads in flight together
+    auto eval = [&](uint32_t tok, double lw, int i, double2 p0, double2 p1) {
+        const double r = p0.x, rinv = p0.y, lnc = p1.x, b = p1.y;
+        const double t = cws_t_inv(lw, r, rinv, b);
+        const double v = cws_lna(t, r, lnc, b);
+        const bool l = v < best[i] || (v == best[i] && tok < btok[i]);
+        best[i] = l ? v : best[i];
+        btok[i] = l ? tok : btok[i];
+        bestt[i] = l ? t : bestt[i];
+    };
+    int f = 0;
+    for (; SG_CWS_U2 && f + 1 < nm; f += 2) {
+        const uint32_t ka = w.ukey[listm[f]], kb = w.ukey[listm[f + 1]];
+        const uint32_t ta = ka >> 12, tb = kb >> 12;
+        const double lwa = __ldg(a.lnw + (ka & 0xFFFu)), lwb = __ldg(a.lnw + (kb & 0xFFFu));
+        double2 pa0[NS], pa1[NS], pb0[NS], pb1[NS];
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+            const int s = min(lane + 32 * i, S - 1);
+            const size_t ea = 2 * ((size_t)ta * S + s), eb = 2 * ((size_t)tb * S + s);
+            pa0[i] = __ldg(a.rlcb + ea); pa1[i] = __ldg(a.rlcb + ea + 1);
+            pb0[i] = __ldg(a.rlcb + eb); pb1[i] = __ldg(a.rlcb + eb + 1);
+        }
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+            if (lane + 32 * i < S) {
+                eval(ta, lwa, i, pa0[i], pa1[i]);
+                eval(tb, lwb, i, pb0[i], pb1[i]);
+            }
+        }
+    }
+    for (; f < nm; f++) {
+        const uint32_t ka = w.ukey[listm[f]];
+        const uint32_t ta = ka >> 12;
+        const double lwa = __ldg(a.lnw + (ka & 0xFFFu));
 #pragma unroll
         for (int i = 0; i < NS; i++) {
             const int s = lane + 32 * i;
             if (s < S) {
-                const double r = __ldg(a.tr + base + s);
-                const double lnc = __ldg(a.tlnc + base + s), b = __ldg(a.tbeta + base + s);
-                const double v = cws_lna(cws_t(lw, r, b), r, lnc, b);
-                const bool l = v < best[i] || (v == best[i] && tok < btok[i]);
-                best[i] = l ? v : best[i];
-                btok[i] = l ? tok : btok[i];
-                bcnt[i] = l ? cnt : bcnt[i];
+                const size_t ea = 2 * ((size_t)ta * S + s);
+                eval(ta, lwa, i, __ldg(a.rlcb + ea), __ldg(a.rlcb + ea + 1));
             }
         }
     }
@@ -770,14 +834,8 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
     for (int i = 0; i < NS; i++) {
         const int s = lane + 32 * i;
         if (s < S) {
-            const uint32_t tok = btok[i], cnt = bcnt[i];
-            const size_t ent = (size_t)tok * S + s;
-            const double b = __ldg(a.tbeta + ent);
-            double t;
-            if (cnt == 1u) t = floor(b);  // fl(0/r + b) = b
-            else t = cws_t(__ldg(a.lnw + cnt), __ldg(a.tr + ent), b);
-            const uint64_t tt = (uint64_t)(int64_t)t;
-            const uint64_t k64 = ssh_mix64((uint64_t)tok ^ ssh_mix64(tt ^ SSH_SALT_KEY));
+            const uint64_t tt = (uint64_t)(int64_t)bestt[i];
+            const uint64_t k64 = ssh_mix64((uint64_t)btok[i] ^ ssh_mix64(tt ^ SSH_SALT_KEY));
             w.keys[s] = k64;
             if (a.keys_out) a.keys_out[row * S + s] = k64;
         }
@@ -792,7 +850,7 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
 }
 
 template <int MODE, int QL, int V>
-__global__ void __launch_bounds__(32 * SG_WARPS, 3) cws_fast_kernel(SigArgs a, int warps) {
+__global__ void __launch_bounds__(32 * SG_WARPS, SG_FAST_MINB) cws_fast_kernel(SigArgs a, int warps) {
     extern __shared__ __align__(16) unsigned char sg_smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
@@ -955,7 +1013,8 @@ int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *t
     a.lnw = ctx->d_lnw;
     a.rank = ctx->d_rank;
     a.rankp = ctx->d_rankp;
-    a.inv = ctx->d_inv;
+    a.byrank = ctx->d_byrank;
+    a.rlcb = reinterpret_cast<const double2 *>(ctx->d_rlcb);
     a.N = N; a.words = ctx->words; a.nb = ctx->nb; a.n = ctx->p.n; a.T = ctx->T;
     int P2 = 32;
     while (P2 < ctx->T) P2 <<= 1;

@@ -539,15 +539,30 @@ __global__ void rank_scatter_kernel(const uint32_t *__restrict__ rows, int64_t T
 }
 
 // Order-free CWS tables (signature.cu, cws_fast): padded u16 ranks per token
-// row and the inverse map (slot, rank) -> token.
+// row, the count-1 winner record per (slot, rank) and the packed variates.
 __global__ void rank_fast_kernel(const uint32_t *__restrict__ rows, int64_t T, int S, int SP,
-                                 uint16_t *__restrict__ rankp, uint16_t *__restrict__ inv) {
+                                 const double *__restrict__ r, const double *__restrict__ lnc,
+                                 const double *__restrict__ beta, const double *__restrict__ lna1,
+                                 uint16_t *__restrict__ rankp, uint4 *__restrict__ byrank,
+                                 double *__restrict__ rlcb) {
     const int64_t n = T * S;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = e / T, p = e - j * T;
         const uint32_t tok = rows[e];
         rankp[(int64_t)tok * SP + j] = (uint16_t)p;
-        inv[e] = (uint16_t)tok;
+        const int64_t te = (int64_t)tok * S + j;
+        const double v = lna1[te];
+        const uint32_t t1 = (uint32_t)floor(beta[te]);  // beta in (0, 1]: 0 or 1
+        byrank[e] = make_uint4((uint32_t)__double2loint(v), (uint32_t)__double2hiint(v),
+                               tok | (t1 << 16), 0u);
+    }
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const double rr = r[e];
+        double *q = rlcb + 4 * e;
+        q[0] = rr;
+        q[1] = __drcp_rn(rr);
+        q[2] = lnc[e];
+        q[3] = beta[e];
     }
 }
 
@@ -582,10 +597,13 @@ int ssh_build_ranks(ssh_ctx *ctx, cudaStream_t st) {
         if (ql > 0) {
             const int SP = 16 * ql;
             cudaError_t e = cudaMalloc(&ctx->d_rankp, sizeof(uint16_t) * (size_t)T * SP);
-            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_inv, sizeof(uint16_t) * n);
+            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_byrank, sizeof(uint4) * n);
+            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rlcb, 4 * sizeof(double) * n);
             if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_rankp, 0xFF, sizeof(uint16_t) * (size_t)T * SP, st);
             if (e == cudaSuccess) {
-                rank_fast_kernel<<<grid, 256, 0, st>>>(rows, T, S, SP, ctx->d_rankp, ctx->d_inv);
+                rank_fast_kernel<<<grid, 256, 0, st>>>(rows, T, S, SP, ctx->d_r, ctx->d_lnc, ctx->d_beta,
+                                                       ctx->d_lna1, ctx->d_rankp, ctx->d_byrank,
+                                                       ctx->d_rlcb);
                 ssh_count_launch();
                 e = cudaGetLastError();
             }
