@@ -173,6 +173,13 @@ int ssh_index_export(const ssh_index *idx, int table, uint64_t *keys, int64_t *o
  * shard the index was built over, f32[N][ld] device. */
 int ssh_index_summarize(ssh_ctx *ctx, ssh_index *idx, const float *X, int64_t ld, void *stream);
 
+/* Copy the rerank summaries of rows [r0, r0 + n) out of the index (inspection
+ * and tests): rec_out receives 64 B per row, codes_out *cstride B per row
+ * (u8 sample codes x8[mp], then (U8, L8) pairs).  Either buffer may be NULL;
+ * both may be host or device memory.  *mp, *cstride report the layout. */
+int ssh_index_copy_summaries(const ssh_index *idx, int64_t r0, int64_t n, void *rec_out,
+                             void *codes_out, int32_t *mp, int64_t *cstride, void *stream);
+
 /* K6 — probe_candidates (index.py:184-190) for a batch: membership bitmap
  * u32[nq][ceil(N/32)] of the deduplicated bucket union (bit = local row),
  * and n_cand[nq] = |R|.  qsig: u64[nq][L] device. */

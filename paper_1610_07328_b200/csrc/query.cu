@@ -326,34 +326,39 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-// byte-packed running max doubling of one padded code array held in
-// registers: lane owns words [lane * WPL, lane * WPL + WPL); a word shifted
-// by 2^l bytes comes from the lane's own registers or, via shuffles, from
-// the next lanes (compile-time offsets).  Words at or past padw are 0
-// (neutral).  Reads the array from shared memory and writes it back.
+// running max doubling of one padded u16 code array held in registers
+// (two codes per word, native VIMNMX.U16x2): lane owns words
+// [lane * WPL, lane * WPL + WPL); a word shifted by 2^l elements comes from
+// the lane's own registers or, via shuffles, from the next lanes
+// (compile-time offsets).  Words at or past padw are 0 (neutral).  A shuffle
+// past lane 31 returns the caller's own word; after the levels that garbage
+// reaches down to word 32 WPL - 2^(lev-1) at most, so the caller guarantees
+// 32 WPL >= padw + 2^(lev-1) and every word written back or read later is exact.  Reads the array from shared memory and
+// writes it back.
 template <int WPL>
-__device__ __forceinline__ void env_doubling_regs(uint32_t *arr, int padw, int lev, int lane) {
+__device__ __forceinline__ void env_doubling16(uint32_t *arr, int padw, int lev, int lane) {
     uint32_t v[WPL];
     const int w0 = lane * WPL;
 #pragma unroll
     for (int j = 0; j < WPL; j++) v[j] = w0 + j < padw ? arr[w0 + j] : 0u;
     __syncwarp();
 #pragma unroll
-    for (int l = 0; l < 9; l++) {
+    for (int l = 0; l < 12; l++) {
         if (l < lev) {
             const int d = 1 << l;
-            const int dq = d >> 2;
-            const unsigned sel = (d & 3) ? 0x3210u + 0x1111u * (unsigned)(d & 3) : 0x3210u;
+            const int dq = d >> 1;
             uint32_t nv[WPL];
 #pragma unroll
             for (int j = 0; j < WPL; j++) {
-                // words j + dq and j + dq + 1 of this lane's block (may lie in later lanes)
-                const int k0 = j + dq, k1 = j + dq + 1;
-                const uint32_t s0 = k0 < WPL ? v[k0] : __shfl_down_sync(0xFFFFFFFFu, v[k0 % WPL], k0 / WPL);
-                const uint32_t s1 = k1 < WPL ? v[k1] : __shfl_down_sync(0xFFFFFFFFu, v[k1 % WPL], k1 / WPL);
-                const uint32_t a0 = (w0 + k0 < padw && lane + k0 / WPL < 32) ? s0 : 0u;
-                const uint32_t a1 = (w0 + k1 < padw && lane + k1 / WPL < 32) ? s1 : 0u;
-                nv[j] = __vmaxu4(v[j], __byte_perm(a0, a1, sel));
+                const int k0 = j + dq;
+                const uint32_t a0 = k0 < WPL ? v[k0] : __shfl_down_sync(0xFFFFFFFFu, v[k0 % WPL], k0 / WPL);
+                uint32_t sh = a0;
+                if (d == 1) {  // odd shift: halves of words j and j + 1
+                    const int k1 = j + 1;
+                    const uint32_t a1 = k1 < WPL ? v[k1] : __shfl_down_sync(0xFFFFFFFFu, v[k1 % WPL], k1 / WPL);
+                    sh = __byte_perm(a0, a1, 0x5432u);
+                }
+                nv[j] = __vmaxu2(v[j], sh);
             }
 #pragma unroll
             for (int j = 0; j < WPL; j++) v[j] = nv[j];
@@ -365,6 +370,12 @@ __device__ __forceinline__ void env_doubling_regs(uint32_t *arr, int padw, int l
     __syncwarp();
 }
 
+// element e of a u16 array held as words: the word starting at element e
+__device__ __forceinline__ uint32_t u16_word_at(const uint32_t *arr, int e) {
+    const int q = e >> 1;
+    return (e & 1) ? __byte_perm(arr[q], arr[q + 1], 0x5432u) : arr[q];
+}
+
 struct SumArgs {
     const float *X;
     int64_t N, ld, cstride;
@@ -374,17 +385,17 @@ struct SumArgs {
 };
 
 template <int WPL>
-__global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
+__global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 12) ? 4 : 1) summaries_kernel(SumArgs a) {
     extern __shared__ __align__(16) unsigned char xsmb[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-    const int m = a.m, pad = a.pad, padw = pad >> 2;
+    const int m = a.m, pad = a.pad, padw = pad >> 1;
     unsigned char *base = xsmb + (size_t)w * a.warp_bytes;
     const int mq = (m + 3) & ~3;
     float *xbuf = reinterpret_cast<float *>(base);                    // 2 x mq samples (double buffer)
-    uint32_t *cmx = reinterpret_cast<uint32_t *>(xbuf + 2 * mq);     // pad bytes: codes, 0 outside
-    uint32_t *cmn = cmx + padw;                                       // pad bytes: 255 - codes, 0 outside
+    uint32_t *cmx = reinterpret_cast<uint32_t *>(xbuf + 2 * mq);     // pad u16: codes, 0 outside
+    uint32_t *cmn = cmx + padw;                                       // pad u16: 255 - codes, 0 outside
     uint8_t *prec = reinterpret_cast<uint8_t *>(cmn + padw);          // 64-byte record staging
-    uint8_t *bmx = reinterpret_cast<uint8_t *>(cmx), *bmn = reinterpret_cast<uint8_t *>(cmn);
+    uint16_t *bmx = reinterpret_cast<uint16_t *>(cmx), *bmn = reinterpret_cast<uint16_t *>(cmn);
     const int win = 2 * a.r + 1;
     const int shw = win - (1 << a.lev);
     const int64_t nwarps = (int64_t)gridDim.x * nwb;
@@ -443,8 +454,8 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
                 if (i < m) {
                     const int c = code_in(xs[i], lo, sc, inv);
                     pk |= (uint32_t)c << (8 * t);
-                    bmx[a.r + i] = (uint8_t)c;
-                    bmn[a.r + i] = (uint8_t)(255 - c);
+                    bmx[a.r + i] = (uint16_t)c;
+                    bmn[a.r + i] = (uint16_t)(255 - c);
                 }
             }
             *reinterpret_cast<uint32_t *>(cr + i4) = pk;
@@ -480,12 +491,12 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
         // running max of the codes and of their complements (= running min) over
         // [t, t + 2^lev) by byte-packed log-step doubling
         if (WPL > 0) {
-            env_doubling_regs<(WPL > 0 ? WPL : 1)>(cmx, padw, a.lev, lane);
-            env_doubling_regs<(WPL > 0 ? WPL : 1)>(cmn, padw, a.lev, lane);
+            env_doubling16<(WPL > 0 ? WPL : 1)>(cmx, padw, a.lev, lane);
+            env_doubling16<(WPL > 0 ? WPL : 1)>(cmn, padw, a.lev, lane);
         } else {
             for (int l = 0; l < a.lev; l++) {
-                const int d = 1 << l, dq = d >> 2;
-                const unsigned sel = d & 3 ? 0x3210u + 0x1111u * (unsigned)(d & 3) : 0x3210u;
+                const int d = 1 << l, dq = d >> 1;
+                const unsigned sel = d & 1 ? 0x5432u : 0x3210u;
                 for (int t0 = 0; t0 < padw; t0 += 32 * 8) {
                     uint32_t va[8], vb[8];
 #pragma unroll
@@ -495,8 +506,8 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
                             const int q0 = t + dq;
                             const uint32_t a0 = q0 < padw ? cmx[q0] : 0u, a1 = q0 + 1 < padw ? cmx[q0 + 1] : 0u;
                             const uint32_t b0 = q0 < padw ? cmn[q0] : 0u, b1 = q0 + 1 < padw ? cmn[q0 + 1] : 0u;
-                            va[u] = __vmaxu4(cmx[t], __byte_perm(a0, a1, sel));
-                            vb[u] = __vmaxu4(cmn[t], __byte_perm(b0, b1, sel));
+                            va[u] = __vmaxu2(cmx[t], __byte_perm(a0, a1, sel));
+                            vb[u] = __vmaxu2(cmn[t], __byte_perm(b0, b1, sel));
                         }
                     }
                     __syncwarp();
@@ -516,19 +527,17 @@ __global__ void __launch_bounds__(256) summaries_kernel(SumArgs a) {
         // [i, i + win) = max over [i, i + 2^lev) and [i + shw, i + shw + 2^lev);
         // U8 = max code + 1 (dec(c + 1) >= x), L8 = min code (dec(c) <= x)
         {
-            const int sq = shw >> 2;
-            const unsigned sel = shw & 3 ? 0x3210u + 0x1111u * (unsigned)(shw & 3) : 0x3210u;
             for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
-                const int t = i4 >> 2;
-                uint32_t u = 0xFFFFFFFFu, lw = 0u;
+                uint2 out = make_uint2(0x00FF00FFu, 0x00FF00FFu);  // U8 = 255, L8 = 0
                 if (i4 < m) {
-                    const uint32_t ma = __vmaxu4(cmx[t], __byte_perm(cmx[t + sq], cmx[t + sq + 1], sel));
-                    const uint32_t mb = __vmaxu4(cmn[t], __byte_perm(cmn[t + sq], cmn[t + sq + 1], sel));
-                    u = __vadd4(ma, 0x01010101u);
-                    lw = ~mb;  // 255 - max(255 - c) = min c
+                    // padded element i of sample i (window [i - r, i + r] -> [i, i + win))
+                    const uint32_t u01 = __vmaxu2(cmx[i4 >> 1], u16_word_at(cmx, i4 + shw)) + 0x00010001u;
+                    const uint32_t u23 = __vmaxu2(cmx[(i4 >> 1) + 1], u16_word_at(cmx, i4 + 2 + shw)) + 0x00010001u;
+                    const uint32_t l01 = __vmaxu2(cmn[i4 >> 1], u16_word_at(cmn, i4 + shw)) ^ 0x00FF00FFu;
+                    const uint32_t l23 = __vmaxu2(cmn[(i4 >> 1) + 1], u16_word_at(cmn, i4 + 2 + shw)) ^ 0x00FF00FFu;
+                    out = make_uint2(__byte_perm(u01, l01, 0x6240u), __byte_perm(u23, l23, 0x6240u));
                 }
-                const uint32_t p0 = __byte_perm(u, lw, 0x5140u), p1 = __byte_perm(u, lw, 0x7362u);
-                *reinterpret_cast<uint2 *>(cr + a.mp + 2 * i4) = make_uint2(p0, p1);
+                *reinterpret_cast<uint2 *>(cr + a.mp + 2 * i4) = out;
             }
         }
         __syncwarp();
@@ -546,10 +555,10 @@ static int summaries_geom(const ssh_ctx *ctx, SumGeom &g) {
     g.mp = ((m + 127) / 128) * 128;
     g.lev = 0;
     while ((2 << g.lev) <= 2 * r + 1) g.lev++;
-    // padded code arrays: sample j at byte j + r; the last doubling read
-    // reaches byte (m - 1) + 2r + 2^lev + 3; 2 pad % 16 == 0 keeps the record aligned
+    // padded u16 code arrays: sample j at element j + r; the last doubling read
+    // reaches element (m - 1) + 2r + 2^lev + 3; 4 pad % 16 == 0 keeps the record aligned
     g.pad = ((m + 2 * r + (1 << g.lev) + 12) + 7) & ~7;
-    g.warp_bytes = (((m + 3) & ~3) * 8 + 2 * g.pad + 64 + 15) & ~15;
+    g.warp_bytes = (((m + 3) & ~3) * 8 + 4 * g.pad + 64 + 15) & ~15;
     g.nwb = (int)std::min<size_t>(8, (200 * 1024) / (size_t)g.warp_bytes);
     SSH_REQUIRE(g.nwb >= 1, SSH_ERR_UNSUPPORTED, "series too long for the summaries kernel (m=%d, r=%d)", m, r);
     return SSH_OK;
@@ -586,10 +595,12 @@ int ssh_launch_summaries_rows(ssh_ctx *ctx, ssh_index *ix, const float *X, int64
               (uint4 *)ix->rec + r0 * 4, ix->codes + r0 * ix->cstride};
     const size_t smem = (size_t)g.warp_bytes * g.nwb;
     // envelope doubling in registers when the padded array fits 32 x WPL words
-    const int padw = g.pad / 4;
-    auto kern = padw <= 32 * 6 ? summaries_kernel<6>
-                : padw <= 32 * 12 ? summaries_kernel<12>
-                : padw <= 32 * 24 ? summaries_kernel<24> : summaries_kernel<0>;
+    // (zero margin of 2^(lev-1) words past padw: see env_doubling16)
+    const int need = g.pad / 2 + (1 << g.lev) / 2;
+    auto kern = need <= 32 * 10 ? summaries_kernel<10>
+                : need <= 32 * 12 ? summaries_kernel<12>
+                : need <= 32 * 24 ? summaries_kernel<24>
+                : need <= 32 * 48 ? summaries_kernel<48> : summaries_kernel<0>;
     SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * g.nwb, smem);
@@ -604,6 +615,27 @@ int ssh_launch_summaries(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t N,
     int rc = ssh_alloc_summaries(ctx, ix, N, st);
     if (rc) return rc;
     return ssh_launch_summaries_rows(ctx, ix, X, 0, N, ld, st);
+}
+
+extern "C" int ssh_index_copy_summaries(const ssh_index *ix, int64_t r0, int64_t n, void *rec_out,
+                                        void *codes_out, int32_t *mp, int64_t *cstride, void *stream) {
+    SSH_REQUIRE(ix, SSH_ERR_INVALID, "ssh_index_copy_summaries: NULL index");
+    SSH_REQUIRE(ix->rec && ix->codes, SSH_ERR_STATE, "ssh_index_copy_summaries: index has no summaries");
+    SSH_REQUIRE(r0 >= 0 && n >= 0 && r0 + n <= ix->N, SSH_ERR_INVALID,
+                "ssh_index_copy_summaries: rows [%lld, %lld) outside [0, %lld)", (long long)r0,
+                (long long)(r0 + n), (long long)ix->N);
+    SSH_CUDA(cudaSetDevice(ix->device));
+    if (mp) *mp = ix->mp;
+    if (cstride) *cstride = ix->cstride;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (rec_out && n)
+        SSH_CUDA(cudaMemcpyAsync(rec_out, (const uint8_t *)ix->rec + 64 * r0, (size_t)64 * n,
+                                 cudaMemcpyDefault, st));
+    if (codes_out && n)
+        SSH_CUDA(cudaMemcpyAsync(codes_out, ix->codes + ix->cstride * r0, (size_t)ix->cstride * n,
+                                 cudaMemcpyDefault, st));
+    SSH_CUDA(cudaStreamSynchronize(st));
+    return SSH_OK;
 }
 
 extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, int64_t ld,

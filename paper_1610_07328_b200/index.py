@@ -304,6 +304,23 @@ class SshIndex:
             self._sig_host = self.sig_dev.cpu().numpy().view(np.uint64)
         return self._sig_host
 
+    def summaries(self, r0: int = 0, n: int | None = None):
+        """Rerank summaries of rows [r0, r0 + n) copied to the host (inspection,
+        tests): (rec u8[n][64], codes u8[n][cstride], mp) — rec = f32 {lo, sc,
+        x0, x_last} + u8 PAA codes; codes = u8 sample codes x8[mp] followed by
+        interleaved (U8, L8) envelope codes (layout in csrc/common.cuh)."""
+        n = self.n_series - r0 if n is None else n
+        L = nat.lib()
+        mp = ctypes.c_int32()
+        cs = ctypes.c_int64()
+        nat.check(L.ssh_index_copy_summaries(self._tables.handle, 0, 0, None, None, ctypes.byref(mp),
+                                             ctypes.byref(cs), _stream_ptr(self.device)))
+        rec = np.empty((n, 64), dtype=np.uint8)
+        codes = np.empty((n, cs.value), dtype=np.uint8)
+        nat.check(L.ssh_index_copy_summaries(self._tables.handle, int(r0), int(n), nat.ptr(rec), nat.ptr(codes),
+                                             None, None, _stream_ptr(self.device)), "ssh_index_copy_summaries")
+        return rec, codes, mp.value
+
     def table_csr(self, j: int):
         """Table j as host CSR: (keys uint64[nb], offsets int64[nb+1], ids int64[N])."""
         L = nat.lib()

@@ -651,3 +651,54 @@ def test_large_k_vs_oracle(cuda):
         n = int(ores["n"][i])
         assert r.ids == ores["ids"][i][:n].tolist(), i
         assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
+
+
+def _dec32(c, sc, lo):
+    """fmaf(c, sc, lo) in f32 (c * sc is exact in long double; one rounding)."""
+    return (c.astype(np.longdouble) * np.longdouble(sc) + np.longdouble(lo)).astype(np.float32)
+
+
+@pytest.mark.parametrize("m,band", [(512, 0.05), (1024, 0.05), (2048, 0.10), (301, 0.1), (5000, 0.01)])
+def test_summaries_codes_exact(cuda, m, band):
+    """Rerank summaries read back from the device: every sample code brackets
+    its value with the decoder's own fp32 arithmetic, PAA codes bracket the
+    f64 segment means (rows not flagged ambiguous), and the envelope codes are
+    exactly max/min of the sample codes over the Sakoe-Chiba window
+    [i - r, i + r] (dtw.py:124-151), U8 = max + 1 and L8 = min (the
+    byte/u16-packed doubling must reproduce the plain running max/min)."""
+    import paper_1610_07328_b200 as ssh
+
+    rng = np.random.default_rng(m)
+    n = 300
+    X = np.cumsum(rng.standard_normal((n, m)), axis=1).astype(np.float32)
+    X[7] = 0.0
+    X[11, : m // 3] = 3.5
+    X[13] = np.round(X[13])
+    p = ssh.SshParams(W=16, delta=2, n=4, d=3, band=band, K=1)
+    idx = ssh.build_index(ssh.Dataset(X), p)
+    rec, codes, mp = idx.summaries()
+    r = p.warping().radius(m)
+    assert codes.shape == (n, 3 * mp)
+    f = rec[:, :16].copy().view(np.float32)
+    lo, sc = f[:, 0], f[:, 1]
+    x8 = codes[:, :m].astype(np.int64)
+    ul = codes[:, mp:mp + 2 * m].reshape(n, m, 2).astype(np.int64)
+    seg = (m + 47) // 48
+    nseg = (m + seg - 1) // seg
+    for i in range(n):
+        scale = abs(sc[i])
+        if not np.isfinite(scale):
+            continue
+        assert f[i, 2] == X[i, 0] and f[i, 3] == X[i, -1], i
+        assert (_dec32(x8[i], scale, lo[i]) <= X[i]).all(), i
+        assert (_dec32(x8[i] + 1, scale, lo[i]) >= X[i]).all(), i
+        pad_hi = np.concatenate([np.full(r, -1), x8[i], np.full(r, -1)])
+        pad_lo = np.concatenate([np.full(r, 1 << 20), x8[i], np.full(r, 1 << 20)])
+        win = np.lib.stride_tricks.sliding_window_view
+        assert np.array_equal(ul[i, :, 0], win(pad_hi, 2 * r + 1).max(1) + 1), i
+        assert np.array_equal(ul[i, :, 1], win(pad_lo, 2 * r + 1).min(1)), i
+        if sc[i] > 0:
+            pc = rec[i, 16:16 + nseg].astype(np.int64)
+            means = np.array([X[i, s * seg:min(m, s * seg + seg)].astype(np.float64).mean() for s in range(nseg)])
+            assert (_dec32(pc, scale, lo[i]).astype(np.float64) <= means).all(), i
+            assert (_dec32(pc + 1, scale, lo[i]).astype(np.float64) >= means).all(), i
