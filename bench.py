@@ -299,15 +299,17 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     b = N * (4 * m + 8 * words)
     res["sketch"] = dict(name="sketch (K1)", ms=ms, bytes=b, roofline=dict(
         bound="hbm", achieved=b / ms / 1e6, peak=hbm, unit="GB/s", frac=b / ms / 1e6 / hbm,
-        traffic=None, kernel="sketch_poly_kernel<80,3>",
-        note="algorithmic bytes = N*(4m + 8*ceil(N_B/64)); peak = %s HBM copy" % peaks["source"]))
+        traffic=_ncu_traffic("sketch_pair_kernel<80, 3>"), kernel="sketch_pair_kernel<80,3>",
+        note="algorithmic bytes = N*(4m + 8*ceil(N_B/64)); peak = %s HBM copy; traffic = ncu dram bytes of "
+             "the build launch + the 1000-query hash launch (0.1%%) (profiles/r01/traffic_cfg1.json)"
+             % peaks["source"]))
     ms_sig = _time(lambda: nat.check(lib.ssh_signatures(ctx.handle, nat.ptr(X), N, m, nat.ptr(sig), None, st)))
     cws_ms = max(ms_sig - ms, 1e-6)
     b2 = N * (4 * m + 8 * params.d)
     res["shingle_cws"] = dict(name="shingle+CWS (K2+K3)", ms=cws_ms, evaluations=None, roofline=dict(
         bound="hbm", achieved=N * (8 * words + 8 * params.d) / cws_ms / 1e6, peak=hbm, unit="GB/s",
-        frac=N * (8 * words + 8 * params.d) / cws_ms / 1e6 / hbm, traffic=None,
-        kernel="shingle_cws_kernel<FUSED>",
+        frac=N * (8 * words + 8 * params.d) / cws_ms / 1e6 / hbm, traffic=_ncu_traffic("cws_fast_kernel<3, 5, 4>"),
+        kernel="cws_fast_kernel<FUSED,5,4>",
         note="HBM bytes in/out only; the kernel is bound by L2 gathers of the CWS tables + FP64"))
     res["signatures_fused"] = dict(name="K1-K3", ms_total=ms_sig)
 
@@ -332,7 +334,7 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     nat.check(lib.ssh_ctx_set_profiling(ctx.handle, 0))
     names = ["hash (K5)", "probe+bitmap (K6)", "member keys (sample, cutoff pass, overflow) + bin sort (K7)",
              "wave LB_Keogh2/LB_Keogh over u8 codes (K8a wave_lb_kernel)",
-             "wave fp32 DTW (K8b dtw32w_kernel)", "rescore+top-k (K9/K10)"]
+             "wave fp32 DTW (K8b dtwp_first/dtwp_level pooled passes)", "rescore+top-k (K9/K10)"]
     r = params.warping().radius(m)
     for i, n in enumerate(names):
         res[f"q{i}"] = dict(name=n, ms=prof[i])
@@ -347,7 +349,8 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     res["q4"]["roofline"] = dict(bound="fp32", achieved=(cells / (dtw_ms / 1e3)) / 1e12 if dtw_ms else 0,
                                  peak=peak_cells / 1e12, unit="Tcells/s",
                                  frac=(cells / (dtw_ms / 1e3)) / peak_cells if dtw_ms else 0,
-                                 traffic=None, kernel="dtw32w_kernel",
+                                 traffic=_ncu_traffic("dtwp_level_kernel<26>"),
+                                 kernel="dtwp_first_kernel + dtwp_level_kernel<26>",
                                  note="cells = alive lane-rows x (2r+1); 2 fma-pipe + 2 alu-pipe instr per cell; "
                                       "peak 148 x 64 x f_max / 2")
     res["dtw_evaluated"] = prof[8]
