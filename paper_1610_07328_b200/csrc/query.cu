@@ -686,7 +686,7 @@ __device__ __forceinline__ float code_f(uint32_t w, int t) {
 template <bool SAMPLE>
 __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
     extern __shared__ __align__(16) unsigned char msm[];
-    __shared__ float sUs[SSH_REC_CODES], sLs[SSH_REC_CODES];
+    __shared__ float2 sUL[SSH_REC_CODES];  // {-Useg, Lseg}
     const int q = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nseg = a.nseg;
@@ -701,8 +701,8 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
     }
     for (int s = threadIdx.x; s < SSH_REC_CODES; s += MB_THREADS) {
         // unused segments contribute max(dec - inf, -inf - dec, 0) = 0
-        sUs[s] = s < nseg ? a.Useg[(int64_t)q * nseg + s] : INFINITY;
-        sLs[s] = s < nseg ? a.Lseg[(int64_t)q * nseg + s] : -INFINITY;
+        sUL[s] = s < nseg ? make_float2(-a.Useg[(int64_t)q * nseg + s], a.Lseg[(int64_t)q * nseg + s])
+                          : make_float2(-INFINITY, -INFINITY);
     }
     if (SAMPLE)
         for (int b = threadIdx.x; b < NBINS; b += MB_THREADS) shist[b] = 0u;
@@ -748,29 +748,58 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
         int n = total;
         for (int g = 0; g < 3 && n > 0; g++) {
             int nk = 0;
+            // the next 32 members' records are loaded one iteration ahead (L2
+            // latency overlaps this iteration's arithmetic); compaction only
+            // writes list/accb below e0 + 32, ahead of the prefetched entries
+            uint32_t rowN = 0;
+            float accN = 0.f;
+            float2 hN = make_float2(0.f, 0.f);
+            uint4 cgN = make_uint4(0u, 0u, 0u, 0u);
+            auto fetch = [&](int e) {
+                if (e < n) {
+                    rowN = list[e];
+                    accN = g ? accb[e] : 0.f;
+                    const uint4 *rp = a.rec + (int64_t)rowN * 4;
+                    hN = __ldg(reinterpret_cast<const float2 *>(rp));
+                    cgN = __ldg(rp + 1 + g);
+                }
+            };
+            fetch(lane);
             for (int e0 = 0; e0 < n; e0 += 32) {
                 const int e = e0 + lane;
                 bool keep = false;
-                float acc = 0.f, key = 0.f;
-                uint32_t row = 0;
+                float acc = accN, key = 0.f;
+                const uint32_t row = rowN;
+                const float2 h = hN;
+                const uint4 cg = cgN;
+                fetch(e + 32);
                 if (e < n) {
-                    row = list[e];
-                    acc = g ? accb[e] : 0.f;
                     const uint4 *rp = a.rec + (int64_t)row * 4;
-                    const float2 h = __ldg(reinterpret_cast<const float2 *>(rp));
                     // flagged rows (-sc): NaN scale -> every PAA term max(NaN, ..., 0) = 0
                     const float lo = h.x, sc = h.y >= 0.f ? h.y : __int_as_float(0x7FC00000);
-                    const uint4 cg = __ldg(rp + 1 + g);
                     const uint32_t cw[4] = {cg.x, cg.y, cg.z, cg.w};
+                    // packed f32x2, the same IEEE operations as the scalar
+                    // forms: {xa, xb} = fma({c, c + 1}, sc, lo) and
+                    // {xa - U, L - xb} = fma({xa, xb}, {1, -1}, {-U, L})
+                    const float2 sc2 = make_float2(sc, sc), lo2 = make_float2(lo, lo);
+                    const float2 off = make_float2(-8388608.f, -8388607.f), pm = make_float2(1.f, -1.f);
+                    float2 acc2 = make_float2(acc, 0.f);
 #pragma unroll
-                    for (int j = 0; j < 16; j++) {
-                        const int sgi = 16 * g + j;
-                        const float cf = code_f(cw[j >> 2], j & 3);
-                        const float xa = fmaf(cf, sc, lo);
-                        const float xb = fmaf(cf + 1.f, sc, lo);
-                        const float ev = fmaxf(fmaxf(xa - sUs[sgi], sLs[sgi] - xb), 0.f);
-                        acc = fmaf(ev, ev, acc);  // weight seg for every segment; the last is fixed below
+                    for (int j = 0; j < 16; j += 2) {
+                        float ev[2];
+#pragma unroll
+                        for (int u = 0; u < 2; u++) {
+                            const int jj = j + u;
+                            const float r = __uint_as_float(__byte_perm(cw[jj >> 2], 0x4B000000u,
+                                                                        (unsigned)(jj & 3) | 0x7440u));
+                            const float2 x = __ffma2_rn(__fadd2_rn(make_float2(r, r), off), sc2, lo2);
+                            const float2 df = __ffma2_rn(x, pm, sUL[16 * g + jj]);
+                            ev[u] = fmaxf(fmaxf(df.x, df.y), 0.f);
+                        }
+                        // weight seg for every segment; the last is fixed below
+                        acc2 = __ffma2_rn(make_float2(ev[0], ev[1]), make_float2(ev[0], ev[1]), acc2);
                     }
+                    acc = acc2.x + acc2.y;
                     if (g < 2) {
                         keep = SAMPLE || acc * wseg * shrink * (1.f - 4.f * U32_EPS) < edge;
                     } else {
@@ -778,7 +807,7 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                         const int sl = nseg - 1;
                         const uint32_t lw = __ldg(reinterpret_cast<const uint32_t *>(rp) + 4 + (sl >> 2));
                         const float cf = code_f(lw, sl & 3);
-                        const float ev = fmaxf(fmaxf(fmaf(cf, sc, lo) - sUs[sl], sLs[sl] - fmaf(cf + 1.f, sc, lo)), 0.f);
+                        const float ev = fmaxf(fmaxf(fmaf(cf, sc, lo) + sUL[sl].x, sUL[sl].y - fmaf(cf + 1.f, sc, lo)), 0.f);
                         const float paa = fmaxf(fmaf(-(segf - lastlen) * ev, ev, acc * segf), 0.f) * shrink;
                         const float2 kx = __ldg(reinterpret_cast<const float2 *>(rp) + 1);
                         const float d0 = kx.x - q0, dl = kx.y - ql;
@@ -1053,9 +1082,13 @@ struct WaveLbArgs {
 };
 
 #define WL_BLK 512  // samples per block of loads (4 chunks of 128, one per lane each)
-#ifndef SSH_WL_KEOGH_FIRST
-#define SSH_WL_KEOGH_FIRST 0  // 1: LB_Keogh over sample codes before LB_Keogh2 over envelope codes
-#endif
+
+// bytes t0, t1 of w as exact floats {c0, c1} (0x4B0000cc = 2^23 + cc)
+__device__ __forceinline__ float2 code_f2(uint32_t w, int t0, int t1) {
+    const float a = __uint_as_float(__byte_perm(w, 0x4B000000u, (unsigned)t0 | 0x7440u));
+    const float b = __uint_as_float(__byte_perm(w, 0x4B000000u, (unsigned)t1 | 0x7440u));
+    return __fadd2_rn(make_float2(a, b), make_float2(-8388608.f, -8388608.f));
+}
 
 __device__ __forceinline__ void wl_load_env(const uint8_t *cr, int mp, int base, uint2 (&v)[4]) {
     const uint2 *p = reinterpret_cast<const uint2 *>(cr + mp + 2 * base) + (threadIdx.x & 31);
@@ -1063,28 +1096,38 @@ __device__ __forceinline__ void wl_load_env(const uint8_t *cr, int mp, int base,
     for (int c = 0; c < 4; c++) v[c] = base + 128 * c < mp ? __ldg(p + 32 * c) : make_uint2(0u, 0u);
 }
 
-// partial LB_Keogh2 of one 512-sample block (tails: sq = NaN -> term 0)
-__device__ __forceinline__ float wl_env_block(const uint2 (&v)[4], const float *sq, int base, int mp, float sc,
-                                              float lo) {
+// partial LB_Keogh2 over chunks [C0, C1) of one 512-sample block (tails: sq =
+// NaN -> term 0).  Packed f32x2: {ue, le} = fma({cU, cL}, sc, lo) and
+// {q - ue, le - q} = fma({ue, le}, {-1, 1}, {q, -q}) are the same IEEE
+// operations as the scalar forms (dtw.py:154-168 terms, fp32 screen).
+template <int C0, int C1>
+__device__ __forceinline__ float wl_env_chunks(const uint2 (&v)[4], const float2 *sq2, int base, int mp, float sc,
+                                               float lo) {
     const int lane = threadIdx.x & 31;
-    float acc = 0.f;
+    float2 acc = make_float2(0.f, 0.f);
+    const float2 sc2 = make_float2(sc, sc), lo2 = make_float2(lo, lo), pm = make_float2(-1.f, 1.f);
 #pragma unroll
-    for (int c = 0; c < 4; c++) {
+    for (int c = C0; c < C1; c++) {
         const int i0 = base + 128 * c + 4 * lane;
         if (base + 128 * c < mp) {
-            const float4 q4 = *reinterpret_cast<const float4 *>(sq + i0);
-            const float qq[4] = {q4.x, q4.y, q4.z, q4.w};
+            const float4 q01 = *reinterpret_cast<const float4 *>(sq2 + i0);
+            const float4 q23 = *reinterpret_cast<const float4 *>(sq2 + i0 + 2);
+            const float2 qq[4] = {make_float2(q01.x, q01.y), make_float2(q01.z, q01.w),
+                                  make_float2(q23.x, q23.y), make_float2(q23.z, q23.w)};  // {q, -q}
+            float dd[4];
 #pragma unroll
             for (int t = 0; t < 4; t++) {
                 const uint32_t wv = t < 2 ? v[c].x : v[c].y;
                 const int bu = 2 * (t & 1);
-                const float ue = fmaf(code_f(wv, bu), sc, lo), le = fmaf(code_f(wv, bu + 1), sc, lo);
-                const float d = fmaxf(fmaxf(qq[t] - ue, le - qq[t]), 0.f);
-                acc = fmaf(d, d, acc);
+                const float2 ul = __ffma2_rn(code_f2(wv, bu, bu + 1), sc2, lo2);
+                const float2 df = __ffma2_rn(ul, pm, qq[t]);
+                dd[t] = fmaxf(fmaxf(df.x, df.y), 0.f);
             }
+            acc = __ffma2_rn(make_float2(dd[0], dd[1]), make_float2(dd[0], dd[1]), acc);
+            acc = __ffma2_rn(make_float2(dd[2], dd[3]), make_float2(dd[2], dd[3]), acc);
         }
     }
-    return acc;
+    return acc.x + acc.y;
 }
 
 __device__ __forceinline__ void wl_load_smp(const uint8_t *cr, int mp, int base, uint32_t (&v)[4]) {
@@ -1093,28 +1136,36 @@ __device__ __forceinline__ void wl_load_smp(const uint8_t *cr, int mp, int base,
     for (int c = 0; c < 4; c++) v[c] = base + 128 * c < mp ? __ldg(p + 32 * c) : 0u;
 }
 
-// partial LB_Keogh of one 512-sample block over sample codes (tails: U = inf, L = -inf -> 0)
-__device__ __forceinline__ float wl_smp_block(const uint32_t (&cw)[4], const float *su, const float *sl, int base,
+// partial LB_Keogh of one 512-sample block over sample codes (tails: U = inf,
+// L = -inf -> 0); sul[i] = {-U_i, L_i}.  {xa, xb} = fma({c, c + 1}, sc, lo)
+// and {xa - U, L - xb} = fma({xa, xb}, {1, -1}, {-U, L}) (same IEEE ops).
+__device__ __forceinline__ float wl_smp_block(const uint32_t (&cw)[4], const float2 *sul, int base,
                                               int mp, float sc, float lo) {
     const int lane = threadIdx.x & 31;
-    float acc = 0.f;
+    float2 acc = make_float2(0.f, 0.f);
+    const float2 sc2 = make_float2(sc, sc), lo2 = make_float2(lo, lo), pm = make_float2(1.f, -1.f);
+    const float2 off = make_float2(-8388608.f, -8388607.f);  // {c, c + 1}
 #pragma unroll
     for (int c = 0; c < 4; c++) {
         const int i0 = base + 128 * c + 4 * lane;
         if (base + 128 * c < mp) {
-            const float4 u4 = *reinterpret_cast<const float4 *>(su + i0);
-            const float4 l4 = *reinterpret_cast<const float4 *>(sl + i0);
-            const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
+            const float4 p01 = *reinterpret_cast<const float4 *>(sul + i0);
+            const float4 p23 = *reinterpret_cast<const float4 *>(sul + i0 + 2);
+            const float2 ul[4] = {make_float2(p01.x, p01.y), make_float2(p01.z, p01.w),
+                                  make_float2(p23.x, p23.y), make_float2(p23.z, p23.w)};
+            float dd[4];
 #pragma unroll
             for (int t = 0; t < 4; t++) {
-                const float cf = code_f(cw[c], t);
-                const float xa = fmaf(cf, sc, lo), xb = fmaf(cf + 1.f, sc, lo);
-                const float d = fmaxf(fmaxf(xa - uu[t], ll[t] - xb), 0.f);
-                acc = fmaf(d, d, acc);
+                const float r = __uint_as_float(__byte_perm(cw[c], 0x4B000000u, (unsigned)t | 0x7440u));
+                const float2 x = __ffma2_rn(__fadd2_rn(make_float2(r, r), off), sc2, lo2);
+                const float2 df = __ffma2_rn(x, pm, ul[t]);
+                dd[t] = fmaxf(fmaxf(df.x, df.y), 0.f);
             }
+            acc = __ffma2_rn(make_float2(dd[0], dd[1]), make_float2(dd[0], dd[1]), acc);
+            acc = __ffma2_rn(make_float2(dd[2], dd[3]), make_float2(dd[2], dd[3]), acc);
         }
     }
-    return acc;
+    return acc.x + acc.y;
 }
 
 __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
@@ -1126,12 +1177,14 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
     const int start = a.pos[q];
     const int end = min(a.cnt[q], start + a.wave);
     if (start + (int)blockIdx.x * nw * 32 >= end) return;
-    float *su = wsm, *sl = wsm + mp, *sq = wsm + 2 * mp;
+    float2 *sul = reinterpret_cast<float2 *>(wsm);       // {-U_i, L_i}
+    float2 *sq2 = reinterpret_cast<float2 *>(wsm) + mp;  // {q_i, -q_i}
     for (int i = threadIdx.x; i < mp; i += blockDim.x) {
         const bool in = i < m;
-        su[i] = in ? a.U[(int64_t)q * m + i] : INFINITY;
-        sl[i] = in ? a.Lo[(int64_t)q * m + i] : -INFINITY;
-        sq[i] = in ? a.Q[(int64_t)q * m + i] : __int_as_float(0x7FC00000);
+        sul[i] = in ? make_float2(-a.U[(int64_t)q * m + i], a.Lo[(int64_t)q * m + i])
+                    : make_float2(-INFINITY, -INFINITY);
+        const float qv = in ? a.Q[(int64_t)q * m + i] : __int_as_float(0x7FC00000);
+        sq2[i] = make_float2(qv, -qv);
     }
     __syncthreads();
     const float T = a.thr[q];
@@ -1157,69 +1210,38 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
         uint32_t rc = __shfl_sync(0xFFFFFFFFu, row, j);
         float2 hc = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rc * 4));
         hc.y = fabsf(hc.y);  // sign = PAA-codes flag, not part of the scale
-#if SSH_WL_KEOGH_FIRST
-        uint32_t vc[4];
-        wl_load_smp(a.codes + (int64_t)rc * a.cstride, mp, 0, vc);
-#else
         uint2 vc[4];
         wl_load_env(a.codes + (int64_t)rc * a.cstride, mp, 0, vc);
-#endif
         for (;;) {
             // prefetch the next live member's header and first block
             const bool more = live != 0;
             uint32_t rn = 0;
             float2 hn = make_float2(0.f, 0.f);
-#if SSH_WL_KEOGH_FIRST
-            uint32_t vn[4];
-#else
             uint2 vn[4];
-#endif
             if (more) {
                 j = __ffs(live) - 1;
                 live &= live - 1;
                 rn = __shfl_sync(0xFFFFFFFFu, row, j);
                 hn = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rn * 4));
                 hn.y = fabsf(hn.y);
-#if SSH_WL_KEOGH_FIRST
-                wl_load_smp(a.codes + (int64_t)rn * a.cstride, mp, 0, vn);
-#else
                 wl_load_env(a.codes + (int64_t)rn * a.cstride, mp, 0, vn);
-#endif
             }
             const uint8_t *cr = a.codes + (int64_t)rc * a.cstride;
             const float lo = hc.x, sc = hc.y;
             bool pruned = false;
             float acc = 0.f, tot2 = 0.f, tot1 = 0.f;
-#if SSH_WL_KEOGH_FIRST
-            for (int base = 0; base < mp; base += WL_BLK) {
-                if (base) wl_load_smp(cr, mp, base, vc);
-                nbytes += min(WL_BLK, mp - base);
-                acc += wl_smp_block(vc, su, sl, base, mp, sc, lo);
-                tot1 = warp_sum(acc);
-                if (tot1 > T) { pruned = true; break; }
-            }
-            if (pruned) {
-                keo++;
-            } else {
-                acc = 0.f;
-                for (int base = 0; base < mp; base += WL_BLK) {
-                    uint2 ve[4];
-                    wl_load_env(cr, mp, base, ve);
-                    nbytes += 2 * min(WL_BLK, mp - base);
-                    acc += wl_env_block(ve, sq, base, mp, sc, lo);
-                    tot2 = warp_sum(acc);
-                    if (tot2 > T) { pruned = true; break; }
-                }
-                if (pruned) {
-                    keo2++;
-                } else if (lane == 0) {
-#else
+            // abandon checks after every 256 samples (partial sums are lower bounds)
             for (int base = 0; base < mp; base += WL_BLK) {
                 if (base) wl_load_env(cr, mp, base, vc);
                 nbytes += 2 * min(WL_BLK, mp - base);
-                acc += wl_env_block(vc, sq, base, mp, sc, lo);
+                acc += wl_env_chunks<0, 2>(vc, sq2, base, mp, sc, lo);
                 tot2 = warp_sum(acc);
                 if (tot2 > T) { pruned = true; break; }
+                if (base + 256 < mp) {
+                    acc += wl_env_chunks<2, 4>(vc, sq2, base, mp, sc, lo);
+                    tot2 = warp_sum(acc);
+                    if (tot2 > T) { pruned = true; break; }
+                }
             }
             if (pruned) {
                 keo2++;
@@ -1229,14 +1251,13 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
                     uint32_t cw[4];
                     wl_load_smp(cr, mp, base, cw);
                     nbytes += min(WL_BLK, mp - base);
-                    acc += wl_smp_block(cw, su, sl, base, mp, sc, lo);
+                    acc += wl_smp_block(cw, sul, base, mp, sc, lo);
                     tot1 = warp_sum(acc);
                     if (tot1 > T) { pruned = true; break; }
                 }
                 if (pruned) {
                     keo++;
                 } else if (lane == 0) {
-#endif
                     const int p = atomicAdd(&a.wcnt[slot], 1);
                     if (p < a.wcap) {
                         a.wrows[(int64_t)slot * a.wcap + p] = rc;
@@ -2980,7 +3001,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             std::vector<float> thr0h;
             const int64_t pool = (int64_t)ns * WCAP;
             const int wl_warps = 8;
-            const size_t wl_smem = (size_t)3 * ix->mp * sizeof(float);
+            const size_t wl_smem = (size_t)4 * ix->mp * sizeof(float);
             SSH_CUDA(cudaFuncSetAttribute(wave_lb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wl_smem));
             for (int round = 0; round < 2; round++) {
                 pf.begin();
