@@ -9,13 +9,16 @@
 //                                    <= screen_c * max|x|      (ctx.cu)
 // so every emitted bit equals the reference bit.
 //
-// Layout/roofline: one CTA stages a tile of ST series from HBM with
-// coalesced float4 loads into a polyphase shared-memory layout
-// x_b[j] = x[j*delta + b] (b < delta), padded by one float per 8 so that
-// threads owning 8 consecutive windows read with a bank-conflict-free stride
-// of 9.  With W, delta compile-time, each thread keeps a sliding register
-// window and the taps come from the constant bank: 8 FFMA per LDS.  The
-// kernel is HBM-bound: 4m bytes in + 8*words bytes out per series.
+// Kernels (dispatch in ssh_launch_sketch):
+//  * sketch_stream_kernel<80,3,20> (float4-aligned rows, m <= ~1500): rows
+//    staged by the bulk-copy engine into a ring of shared-memory stages
+//    (warp-specialised producer, mbarriers), FFMA2 window pairs with
+//    broadcast samples; 4.2 TB/s (64% of HBM) at configs[1].
+//  * sketch_pair_kernel / sketch_poly_kernel: polyphase shared-memory layout
+//    x_b[j] = x[j*delta + b] (padded by one float per 8, conflict-free stride
+//    9) staged by LDG + scatter; used for longer rows (configs[3]).
+//  * sketch_generic_kernel: any W, delta.
+// All are HBM-bound by design: 4m bytes in + 8*words bytes out per series.
 #include <algorithm>
 #include <cstdlib>
 
@@ -319,6 +322,263 @@ sketch_pair_kernel(const float *__restrict__ X, SketchGeom g, const SketchW2 wp,
     }
 }
 
+// ---------------------------------------------------------------------------
+// sketch_stream_kernel<W, D, J>: TMA-staged rows, no polyphase scatter.
+//
+// A tile of ST series is copied row by row into shared memory by the bulk
+// copy engine (cp.async.bulk, one mbarrier per stage, two stages per CTA), so
+// the SMs spend no instructions on staging.  Rows keep the HBM layout with a
+// stride of an odd number of 16-byte units, so the 8 lanes of each LDS.128
+// phase (8 consecutive series, same offset) hit 8 distinct bank quads.
+// Thread (s, t) owns windows [J t, J t + J) of series s: J/2 accumulator
+// pairs {acc_2q, acc_2q+1}.  Window 2q uses x[6q + d] with tap d and window
+// 2q+1 the same sample with tap d - D, so one FFMA2 with the sample broadcast
+// and the tap pair WP[d] = {w_d, w_{d-D}} (zero outside [0, W)) advances both
+// windows.  Loops run weight-block stationary (blocks of 2D taps, uniform
+// registers) over a sliding register window of samples.  Every product/sum is
+// an IEEE f32 fma of exact products of f32 inputs and f32 taps, so the same
+// (W+2) u sum|x||w| screen bound as sketch_poly_kernel holds (summation order
+// does not enter it); the per-thread max|x| over its own sample range bounds
+// every window it decides, and the zero tail beyond m only meets zero taps of
+// real windows or windows >= nb that are never emitted.
+// ---------------------------------------------------------------------------
+#ifndef SKS_ST
+#define SKS_ST 16
+#endif
+
+template <int W, int D>
+struct SketchWP {
+    float2 w[((W + D) + 2 * D - 1) / (2 * D) * (2 * D)];  // {w_d, w_{d-D}}
+};
+
+struct StreamGeom {
+    int m, nb, words, stride, tps, nstages, ngroups, gthreads;
+    int64_t N, ld;
+    float screen_c;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+        "[%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+// Exact reference-order f64 dot over a contiguous row window (sketch.py:60).
+__device__ __noinline__ double exact_row_dot(const float *x, const double *w64, int W) {
+    double d = 0.0;
+    for (int k = 0; k < W; k++) d = __dadd_rn(d, __dmul_rn((double)x[k], w64[k]));
+    return d;
+}
+
+#define SKS_MAXSTAGES 8
+#define SKS_MAXG 4
+
+// Warp-specialised pipeline: warp 0 produces (bulk row copies into a ring of
+// ns_stages tiles, one full/empty mbarrier pair per stage); consumer groups of
+// gthreads threads (ST series x tps window slots) take tiles round-robin, so
+// up to ns_stages - ngroups tiles are in flight from HBM while the others are
+// computed.
+template <int W, int D, int J>
+__global__ void __launch_bounds__(544)
+sketch_stream_kernel(const float *__restrict__ X, StreamGeom g, const SketchWP<W, D> wp,
+                     const double *__restrict__ w64g, uint64_t *__restrict__ bits, long long *stats) {
+    constexpr int S2 = 2 * D;                        // sample shift between window pairs
+    constexpr int NWB = (W + D + S2 - 1) / S2;       // weight blocks of S2 tap pairs
+    constexpr int NQ = J / 2;                        // accumulator pairs
+    constexpr int NXB = NWB + NQ - 1;                // sample blocks a thread reads
+    static_assert(J % 2 == 0, "J even");
+    static_assert((J * D) % 4 == 0, "thread sample bases must be 16-byte aligned");
+    extern __shared__ __align__(128) unsigned char sks_smem[];
+    __shared__ uint64_t full[SKS_MAXSTAGES], empty[SKS_MAXSTAGES];
+    __shared__ double w64[W];
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const int NS = g.nstages, NG = g.ngroups;
+    const int stage_floats = SKS_ST * g.stride;
+    float *xs = reinterpret_cast<float *>(sks_smem);
+    // after the stages: per group, two packed-bit buffers of ST x words
+    unsigned long long *wbits_all = reinterpret_cast<unsigned long long *>(xs + (size_t)NS * stage_floats);
+    for (int k = tid; k < W; k += nthr) w64[k] = w64g[k];
+    // zero tails of every stage (never written by the bulk copies)
+    const int tail = g.stride - g.m;
+    for (int e = tid; e < NS * SKS_ST * tail; e += nthr) {
+        const int r = e / tail;
+        xs[r * g.stride + g.m + (e - r * tail)] = 0.f;
+    }
+    if (tid == 0) {
+        for (int i = 0; i < NS; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t ntiles = (g.N + SKS_ST - 1) / SKS_ST;
+    // this CTA's tiles: blockIdx.x + k gridDim.x, k = 0, 1, ...
+    const int64_t nmine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (tid < 32) {
+        // producer warp
+        uint64_t policy;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+        const unsigned row_bytes = (unsigned)g.m * 4u;
+        const int lane = tid;
+        for (int64_t k = 0; k < nmine; k++) {
+            const int stg = (int)(k % NS);
+            if (k >= NS) mbar_wait(&empty[stg], (unsigned)((k / NS) - 1) & 1u);
+            const int64_t s0 = (blockIdx.x + k * gridDim.x) * SKS_ST;
+            const int ns = (int)min((int64_t)SKS_ST, g.N - s0);
+            if (lane == 0) mbar_expect_tx(&full[stg], row_bytes * (unsigned)ns);
+            __syncwarp();
+            if (lane < ns)
+                bulk_g2s(xs + stg * stage_floats + lane * g.stride, X + (s0 + lane) * g.ld, row_bytes,
+                         &full[stg], policy);
+        }
+        return;
+    }
+    const int ctid = tid - 32;
+    const int grp = ctid / g.gthreads;
+    if (grp >= NG) return;
+    const int gtid = ctid - grp * g.gthreads;
+    const int s = gtid % SKS_ST;
+    const int t = gtid / SKS_ST;
+    const int wpr = g.words;
+    int par = 0;
+    for (int64_t k = grp; k < nmine; k += NG, par ^= 1) {
+        const int stg = (int)(k % NS);
+        const int64_t s0 = (blockIdx.x + k * gridDim.x) * SKS_ST;
+        const int ns = (int)min((int64_t)SKS_ST, g.N - s0);
+        unsigned long long *wbits = wbits_all + (size_t)(2 * grp + par) * SKS_ST * wpr;
+        for (int e = gtid; e < SKS_ST * wpr; e += g.gthreads) wbits[e] = 0ULL;
+        mbar_wait(&full[stg], (unsigned)(k / NS) & 1u);
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(g.gthreads) : "memory");
+        if (s < ns && t < g.tps) {
+            const float *xr = xs + stg * stage_floats + s * g.stride;
+            const float *xt = xr + t * (J * D);
+            float2 acc[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; q++) acc[q] = make_float2(0.f, 0.f);
+            float xv[NXB * S2 + 4];  // fully unrolled: registers hold a sliding subset
+            float mx = 0.f;
+#pragma unroll
+            for (int e = 0; e < NQ * S2; e += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(xt + e);
+                xv[e] = v.x; xv[e + 1] = v.y; xv[e + 2] = v.z; xv[e + 3] = v.w;
+            }
+#pragma unroll
+            for (int b = 0; b < NWB; b++) {
+                // samples of block b + NQ - 1 (the newest block this step needs)
+                const int lo = (b + NQ - 1) * S2;
+                if (b > 0) {
+#pragma unroll
+                    for (int e = 0; e < S2; e++) {
+                        const int p = lo + e;
+                        if ((p & 3) == 0) {
+                            const float4 v = *reinterpret_cast<const float4 *>(xt + p);
+                            xv[p] = v.x; xv[p + 1] = v.y; xv[p + 2] = v.z; xv[p + 3] = v.w;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < S2; e++) {
+                    const float2 wk = wp.w[b * S2 + e];
+#pragma unroll
+                    for (int q = 0; q < NQ; q++) {
+                        const float xq = xv[(b + q) * S2 + e];
+                        acc[q] = __ffma2_rn(make_float2(xq, xq), wk, acc[q]);
+                    }
+                }
+                // max|x| over the block that leaves the window
+#pragma unroll
+                for (int e = 0; e < S2; e++) mx = fmaxf(mx, fabsf(xv[b * S2 + e]));
+            }
+#pragma unroll
+            for (int e = NWB * S2; e < NXB * S2; e++) mx = fmaxf(mx, fabsf(xv[e]));
+            const float thr = g.screen_c * mx + 2e-9f;
+            // branch-free common case: sign bits of the screen values and the NaN-propagating
+            // minimum |value| over the thread's valid windows; the exact path runs only when
+            // some window is within the screen bound (or NaN)
+            const int nval = min(J, g.nb - t * J);
+            unsigned neg = 0;
+            float amin = __int_as_float(0x7f800000);
+            if (nval == J) {
+#pragma unroll
+                for (int c = 0; c < J; c++) {
+                    const float a = (c & 1) ? acc[c >> 1].y : acc[c >> 1].x;
+                    neg |= (__float_as_uint(a) >> 31) << c;
+                    amin = fmin_nan(amin, fabsf(a));
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < J; c++) {
+                    const float a = (c & 1) ? acc[c >> 1].y : acc[c >> 1].x;
+                    if (c < nval) {
+                        neg |= (__float_as_uint(a) >> 31) << c;
+                        amin = fmin_nan(amin, fabsf(a));
+                    }
+                }
+            }
+            unsigned msk = ~neg & (nval >= 32 ? 0xffffffffu : ((1u << nval) - 1u));
+            if (!(amin > thr)) {
+#pragma unroll
+                for (int c = 0; c < J; c++) {
+                    const float a = (c & 1) ? acc[c >> 1].y : acc[c >> 1].x;
+                    if (c < nval && !(fabsf(a) > thr)) {
+                        const int i = t * J + c;
+                        const double d = exact_row_dot(xr + i * D, w64, W);
+                        msk = d >= 0.0 ? (msk | (1u << c)) : (msk & ~(1u << c));
+                        if (stats) {
+                            atomicAdd(reinterpret_cast<unsigned long long *>(&stats[0]), 1ULL);
+                            if (fabs(d) < 1e-9)
+                                atomicAdd(reinterpret_cast<unsigned long long *>(&stats[1]), 1ULL);
+                        }
+                    }
+                }
+            }
+            const int i0 = t * J;
+            const unsigned long long lo = (unsigned long long)msk << (i0 & 63);
+            if (lo) atomicOr(&wbits[s * wpr + (i0 >> 6)], lo);
+            if ((i0 & 63) + J > 64) {
+                const unsigned long long hi = (unsigned long long)msk >> (64 - (i0 & 63));
+                if (hi) atomicOr(&wbits[s * wpr + (i0 >> 6) + 1], hi);
+            }
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(g.gthreads) : "memory");
+        // every thread of the group is done with the stage: release it
+        if (gtid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[stg])) : "memory");
+        for (int e = gtid; e < ns * wpr; e += g.gthreads) bits[s0 * wpr + e] = wbits[e];
+    }
+}
+
 // Generic W, delta: one thread per window, taps from shared memory.
 __global__ void __launch_bounds__(SK_THREADS)
 sketch_generic_kernel(const float *__restrict__ X, SketchGeom g, const SketchW wp,
@@ -431,8 +691,77 @@ static bool try_pair(ssh_ctx *ctx, const float *X, const SketchGeom &g0, uint64_
     return true;
 }
 
+template <int W, int D, int J>
+static bool try_stream(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *bits,
+                       int64_t *stats, cudaStream_t st, int *rc) {
+    const ssh_params &p = ctx->p;
+    if (p.W != W || p.delta != D) return false;
+    static const bool off = [] {
+        const char *e = getenv("SSH_SKETCH_STREAM");
+        return e && e[0] == '0';
+    }();
+    const bool vec = ((ld & 3) == 0) && ((p.m & 3) == 0) && ((((uintptr_t)X) & 15) == 0);
+    if (off || !vec || N <= 0) return false;
+    constexpr int S2 = 2 * D;
+    constexpr int NWB = (W + D + S2 - 1) / S2;
+    constexpr int NXB = NWB + J / 2 - 1;
+    StreamGeom g;
+    g.m = p.m; g.nb = ctx->nb; g.words = ctx->words; g.N = N; g.ld = ld; g.screen_c = ctx->screen_c;
+    g.tps = (g.nb + J - 1) / J;
+    if (g.words > 16) return false;
+    g.gthreads = (SKS_ST * g.tps + 31) / 32 * 32;
+    if (g.gthreads > 512) return false;
+    int need = (g.tps - 1) * J * D + NXB * S2 + 4;
+    int stride = std::max(need, g.m);
+    stride = (stride + 3) & ~3;
+    if (((stride >> 2) & 1) == 0) stride += 4;  // odd number of 16-byte units
+    g.stride = stride;
+    const size_t stage_bytes = (size_t)SKS_ST * stride * 4;
+    static const int env_groups = [] {
+        const char *e = getenv("SSH_SKETCH_GROUPS");
+        return e ? atoi(e) : 0;
+    }();
+    g.ngroups = env_groups > 0 ? env_groups : std::max(1, 512 / g.gthreads);
+    g.ngroups = std::min(g.ngroups, std::min(SKS_MAXG, 512 / g.gthreads));
+    if (g.ngroups < 1) return false;
+    const size_t wbits_bytes = (size_t)g.ngroups * 2 * SKS_ST * g.words * 8;
+    const size_t smem_cap = 232448 - 4096 - wbits_bytes;
+    g.nstages = (int)std::min<size_t>(SKS_MAXSTAGES, smem_cap / stage_bytes);
+    if (g.nstages < g.ngroups + 1) return false;
+    const int threads = 32 + g.ngroups * g.gthreads;
+    const size_t smem = (size_t)g.nstages * stage_bytes + wbits_bytes;
+    SketchWP<W, D> wp;
+    constexpr int NWP = sizeof(wp.w) / sizeof(wp.w[0]);
+    for (int d = 0; d < NWP; d++) {
+        const float a = d < W ? ctx->h_w32[d] : 0.f;
+        const float b = (d >= D && d - D < W) ? ctx->h_w32[d - D] : 0.f;
+        wp.w[d] = make_float2(a, b);
+    }
+    auto kern = sketch_stream_kernel<W, D, J>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) { *rc = ssh_cuda_fail(e, "cudaFuncSetAttribute(sketch_stream)", __FILE__, __LINE__); return true; }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t ntiles = (N + SKS_ST - 1) / SKS_ST;
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * per_sm);
+    (void)threads;
+    kern<<<grid, threads, smem, st>>>(X, g, wp, ctx->d_w64, bits, (long long *)stats);
+    ssh_count_launch();
+    e = cudaGetLastError();
+    *rc = e == cudaSuccess ? SSH_OK : ssh_cuda_fail(e, "sketch_stream_kernel", __FILE__, __LINE__);
+    return true;
+}
+
 int ssh_launch_sketch(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *bits,
                       int64_t *stats, cudaStream_t st) {
+    {
+        int rc = SSH_OK;
+        if (ctx->p.m >= 64) {
+            // J = 20 windows per thread measured best against J = 12 and 16 (configs[1]/[2])
+            if (try_stream<80, 3, 20>(ctx, X, N, ld, bits, stats, st, &rc)) return rc;
+        }
+    }
     const ssh_params &p = ctx->p;
     SketchGeom g;
     g.m = p.m; g.nb = ctx->nb; g.words = ctx->words; g.W = p.W; g.delta = p.delta;

@@ -97,6 +97,37 @@ def test_sketch_recheck_near_zero(cuda):
     assert int(stats[1]) == int((np.abs(dots) < 1e-9).sum())
 
 
+@pytest.mark.parametrize("m", [512, 1024])
+def test_sketch_stream_ring_partial_tile(cuda, m):
+    """TMA-staged sketch kernel: enough series that every CTA wraps its stage
+    ring several times, a partial last tile, and rows with NaN / inf / huge
+    values (the screen must defer to the exact f64 sequence there)."""
+    import torch
+
+    from paper_1610_07328_b200 import _native as nat
+    from paper_1610_07328_b200.index import _stream_ptr
+
+    p = params(0.05)
+    ctx = _stage_ctx(p, m)
+    N = 16 * 148 * 9 + 5
+    rng = np.random.default_rng(11 + m)
+    X = np.cumsum(rng.standard_normal((N, m)), axis=1).astype(np.float32)
+    X[7, 100] = np.nan
+    X[N - 2, 3] = np.inf
+    X[N - 1, m - 1] = -np.inf
+    X[N // 2] *= np.float32(1e30)
+    Xd = torch.from_numpy(X).cuda()
+    bits = torch.zeros((N, ctx.words), dtype=torch.int64, device="cuda")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    nat.check(nat.lib().ssh_sketch(ctx.handle, nat.ptr(Xd), N, m, nat.ptr(bits), nat.ptr(stats), _stream_ptr(0)))
+    got = unpack_bits(bits.cpu().numpy().view(np.uint64), ctx.nb)
+    rows = np.unique(np.concatenate([np.arange(16), np.arange(N - 40, N), [N // 2],
+                                     rng.choice(N, 400, replace=False)]))
+    with np.errstate(invalid="ignore", over="ignore"):
+        want = O.sketch_matrix(X[rows], O.make_filter(80, 0), 3)
+    assert np.array_equal(got[rows], want)
+
+
 @pytest.mark.parametrize("name", ["rw512", "rw2048"])
 def test_shingle_and_cws_stages(cuda, name):
     import torch
