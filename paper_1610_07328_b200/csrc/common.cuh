@@ -48,6 +48,7 @@ struct ssh_ctx {
     int T = 0;       // tokens per series
     int S = 0;       // K*L slots
     int max_count = 0;
+    double h_ln2 = 0.0;  // host ln(2) from the uploaded ln(count) table
     float screen_c = 0.f;  // |dot32 - dot64| <= screen_c * max|x|  (sketch.cu)
     float h_w32[SSH_MAX_W];  // filter rounded to f32 (host copy, passed as kernel params)
     double *d_w64 = nullptr;  // filter f64[W]
@@ -62,6 +63,7 @@ struct ssh_ctx {
     uint16_t *d_rankp = nullptr;
     uint4 *d_byrank = nullptr;
     double *d_rlcb = nullptr;
+    double *d_lna2 = nullptr;  // per (token, slot): ln_a for count 2 (order-free CWS)
     int rank_ql = 0;  // 0: path unavailable
     size_t tab_entries = 0;
     // profiling (ssh_ctx_set_profiling)

@@ -116,7 +116,8 @@ static void free_tables(ssh_ctx *c) {
     cudaFree(c->d_rank);
     c->d_rank = nullptr;
     cudaFree(c->d_rankp); cudaFree(c->d_byrank); cudaFree(c->d_rlcb);
-    c->d_rankp = nullptr; c->d_byrank = nullptr; c->d_rlcb = nullptr;
+    cudaFree(c->d_lna2);
+    c->d_rankp = nullptr; c->d_byrank = nullptr; c->d_rlcb = nullptr; c->d_lna2 = nullptr;
     c->rank_ql = 0;
     c->d_w64 = nullptr; c->d_w32 = nullptr; c->d_r = c->d_lnc = c->d_beta = c->d_lna1 = nullptr;
     c->d_lnw = nullptr;
@@ -175,6 +176,7 @@ extern "C" int ssh_ctx_set_params(ssh_ctx *ctx, const ssh_params *p, const doubl
     ctx->T = T;
     ctx->S = p->K * p->L;
     ctx->max_count = max_count;
+    ctx->h_ln2 = max_count >= 2 ? ln_w[2] : 0.0;
     double l1 = 0.0;
     float w32[SSH_MAX_W];
     for (int k = 0; k < p->W; k++) {

@@ -58,6 +58,7 @@ struct SigArgs {
     const uint16_t *rankp;  // order-free path: u16 ranks, 16*QL slots per token row
     const uint4 *byrank;    // order-free path: (slot << n | rank) -> {ln_a1, token | t1 << 16}
     const double2 *rlcb;    // order-free path: (token, slot) -> {r, 1/r}, {ln c, beta}
+    const double *lna2;     // order-free path: (token, slot) -> ln_a for count 2 (or null)
     int64_t N;
     int words, nb, n, T, P2, H, S, L, K;
     int warp_smem;  // bytes per warp
@@ -691,19 +692,26 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
     constexpr int A = 4 * QL;
     const int S = a.S;
     uint16_t *list1 = w.ustart;
-    uint16_t *listm = w.ucnt;
-    int n1 = 0, nm = 0;
+    uint16_t *list2 = w.ucnt;                  // count-2 tokens from the front
+    uint16_t *listm = w.ucnt + (a.T - 1);      // count > 2 tokens from the back (listm[-f])
+    int n1 = 0, n2 = 0, nm = 0;
     const unsigned lt = (1u << lane) - 1u;
+    const bool have2 = a.lna2 != nullptr;
     for (int base = 0; base < D; base += 32) {
         const int d = base + lane;
         const uint32_t key = d < D ? w.ukey[d] : 0u;
-        const bool one = d < D && (key & 0xFFFu) == 1u;
-        const bool many = d < D && (key & 0xFFFu) > 1u;
+        const uint32_t c = key & 0xFFFu;
+        const bool one = d < D && c == 1u;
+        const bool two = d < D && c == 2u && have2;
+        const bool many = d < D && c > 1u && !two;
         const unsigned m1 = __ballot_sync(0xFFFFFFFFu, one);
+        const unsigned m2 = __ballot_sync(0xFFFFFFFFu, two);
         const unsigned mm = __ballot_sync(0xFFFFFFFFu, many);
         if (one) list1[n1 + __popc(m1 & lt)] = (uint16_t)d;
-        if (many) listm[nm + __popc(mm & lt)] = (uint16_t)d;
+        if (two) list2[n2 + __popc(m2 & lt)] = (uint16_t)d;
+        if (many) listm[-(nm + __popc(mm & lt))] = (uint16_t)d;
         n1 += __popc(m1);
+        n2 += __popc(m2);
         nm += __popc(mm);
     }
     __syncwarp();
@@ -795,29 +803,44 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
         btok[i] = l ? tok : btok[i];
         bestt[i] = l ? t : bestt[i];
     };
-    int f = 0;
-    for (; SG_CWS_U2 && f + 1 < nm; f += 2) {
-        const uint32_t ka = w.ukey[listm[f]], kb = w.ukey[listm[f + 1]];
-        const uint32_t ta = ka >> 12, tb = kb >> 12;
-        const double lwa = __ldg(a.lnw + (ka & 0xFFFu)), lwb = __ldg(a.lnw + (kb & 0xFFFu));
-        double2 pa0[NS], pa1[NS], pb0[NS], pb1[NS];
+    // count-2 tokens: tabulated ln_a2 (exact reference formula, rank_fast_kernel);
+    // t is recomputed for the slots they win (bestt = -1 marks them)
+    {
+        int f = 0;
+        for (; f + 1 < n2; f += 2) {
+            const uint32_t ta = w.ukey[list2[f]] >> 12, tb = w.ukey[list2[f + 1]] >> 12;
+            double va[NS], vb[NS];
 #pragma unroll
-        for (int i = 0; i < NS; i++) {
-            const int s = min(lane + 32 * i, S - 1);
-            const size_t ea = 2 * ((size_t)ta * S + s), eb = 2 * ((size_t)tb * S + s);
-            pa0[i] = __ldg(a.rlcb + ea); pa1[i] = __ldg(a.rlcb + ea + 1);
-            pb0[i] = __ldg(a.rlcb + eb); pb1[i] = __ldg(a.rlcb + eb + 1);
+            for (int i = 0; i < NS; i++) {
+                const int s = min(lane + 32 * i, S - 1);
+                va[i] = __ldg(a.lna2 + (size_t)ta * S + s);
+                vb[i] = __ldg(a.lna2 + (size_t)tb * S + s);
+            }
+#pragma unroll
+            for (int i = 0; i < NS; i++) {
+                if (lane + 32 * i < S) {
+                    bool l = va[i] < best[i] || (va[i] == best[i] && ta < btok[i]);
+                    best[i] = l ? va[i] : best[i]; btok[i] = l ? ta : btok[i]; bestt[i] = l ? -1.0 : bestt[i];
+                    l = vb[i] < best[i] || (vb[i] == best[i] && tb < btok[i]);
+                    best[i] = l ? vb[i] : best[i]; btok[i] = l ? tb : btok[i]; bestt[i] = l ? -1.0 : bestt[i];
+                }
+            }
         }
+        if (f < n2) {
+            const uint32_t ta = w.ukey[list2[f]] >> 12;
 #pragma unroll
-        for (int i = 0; i < NS; i++) {
-            if (lane + 32 * i < S) {
-                eval(ta, lwa, i, pa0[i], pa1[i]);
-                eval(tb, lwb, i, pb0[i], pb1[i]);
+            for (int i = 0; i < NS; i++) {
+                const int s = lane + 32 * i;
+                if (s < S) {
+                    const double v = __ldg(a.lna2 + (size_t)ta * S + s);
+                    const bool l = v < best[i] || (v == best[i] && ta < btok[i]);
+                    best[i] = l ? v : best[i]; btok[i] = l ? ta : btok[i]; bestt[i] = l ? -1.0 : bestt[i];
+                }
             }
         }
     }
-    for (; f < nm; f++) {
-        const uint32_t ka = w.ukey[listm[f]];
+    for (int f = 0; f < nm; f++) {
+        const uint32_t ka = w.ukey[listm[-f]];
         const uint32_t ta = ka >> 12;
         const double lwa = __ldg(a.lnw + (ka & 0xFFFu));
 #pragma unroll
@@ -826,6 +849,18 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
             if (s < S) {
                 const size_t ea = 2 * ((size_t)ta * S + s);
                 eval(ta, lwa, i, __ldg(a.rlcb + ea), __ldg(a.rlcb + ea + 1));
+            }
+        }
+    }
+    if (n2 > 0) {
+        const double ln2 = __ldg(a.lnw + 2);
+#pragma unroll
+        for (int i = 0; i < NS; i++) {
+            const int s = lane + 32 * i;
+            if (s < S && bestt[i] < 0.0) {
+                const size_t ea = 2 * ((size_t)btok[i] * S + s);
+                const double2 p0 = __ldg(a.rlcb + ea), p1 = __ldg(a.rlcb + ea + 1);
+                bestt[i] = cws_t_inv(ln2, p0.x, p0.y, p1.y);
             }
         }
     }
@@ -1015,6 +1050,7 @@ int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *t
     a.rankp = ctx->d_rankp;
     a.byrank = ctx->d_byrank;
     a.rlcb = reinterpret_cast<const double2 *>(ctx->d_rlcb);
+    a.lna2 = ctx->d_lna2;
     a.N = N; a.words = ctx->words; a.nb = ctx->nb; a.n = ctx->p.n; a.T = ctx->T;
     int P2 = 32;
     while (P2 < ctx->T) P2 <<= 1;

@@ -544,7 +544,7 @@ __global__ void rank_fast_kernel(const uint32_t *__restrict__ rows, int64_t T, i
                                  const double *__restrict__ r, const double *__restrict__ lnc,
                                  const double *__restrict__ beta, const double *__restrict__ lna1,
                                  uint16_t *__restrict__ rankp, uint4 *__restrict__ byrank,
-                                 double *__restrict__ rlcb) {
+                                 double *__restrict__ rlcb, double *__restrict__ lna2, double ln2) {
     const int64_t n = T * S;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = e / T, p = e - j * T;
@@ -563,6 +563,14 @@ __global__ void rank_fast_kernel(const uint32_t *__restrict__ rows, int64_t T, i
         q[1] = __drcp_rn(rr);
         q[2] = lnc[e];
         q[3] = beta[e];
+        if (lna2) {
+            // count 2 (wmh.py:74-76, reference op order): t = floor(fl(fl(ln 2 / r) + beta)),
+            // ln_a = (ln_c - r (t - beta)) - r
+            const double b = beta[e];
+            const double t = floor(__dadd_rn(__ddiv_rn(ln2, rr), b));
+            const double lny = __dmul_rn(rr, __dsub_rn(t, b));
+            lna2[e] = __dsub_rn(__dsub_rn(lnc[e], lny), rr);
+        }
     }
 }
 
@@ -599,11 +607,15 @@ int ssh_build_ranks(ssh_ctx *ctx, cudaStream_t st) {
             cudaError_t e = cudaMalloc(&ctx->d_rankp, sizeof(uint16_t) * (size_t)T * SP);
             if (e == cudaSuccess) e = cudaMalloc(&ctx->d_byrank, sizeof(uint4) * n);
             if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rlcb, 4 * sizeof(double) * n);
+            // count-2 table when ln(2) is in the uploaded ln(count) table (SSH_CWS_LNA2=0 disables)
+            const char *ev = getenv("SSH_CWS_LNA2");
+            const bool want2 = ctx->max_count >= 2 && !(ev && ev[0] == '0');
+            if (e == cudaSuccess && want2) e = cudaMalloc(&ctx->d_lna2, sizeof(double) * n);
             if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_rankp, 0xFF, sizeof(uint16_t) * (size_t)T * SP, st);
             if (e == cudaSuccess) {
                 rank_fast_kernel<<<grid, 256, 0, st>>>(rows, T, S, SP, ctx->d_r, ctx->d_lnc, ctx->d_beta,
                                                        ctx->d_lna1, ctx->d_rankp, ctx->d_byrank,
-                                                       ctx->d_rlcb);
+                                                       ctx->d_rlcb, ctx->d_lna2, ctx->h_ln2);
                 ssh_count_launch();
                 e = cudaGetLastError();
             }
