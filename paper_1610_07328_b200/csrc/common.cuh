@@ -63,7 +63,7 @@ struct ssh_ctx {
     uint16_t *d_rankp = nullptr;
     uint4 *d_byrank = nullptr;
     double *d_rlcb = nullptr;
-    double *d_lna2 = nullptr;  // per (token, slot): ln_a for count 2 (order-free CWS)
+    double *d_edge = nullptr;  // per (token 0 | 2^n-1, count, slot): {ln_a, t} (order-free CWS)  // per (token, slot): ln_a for count 2 (order-free CWS)
     int rank_ql = 0;  // 0: path unavailable
     size_t tab_entries = 0;
     // profiling (ssh_ctx_set_profiling)

@@ -116,8 +116,9 @@ static void free_tables(ssh_ctx *c) {
     cudaFree(c->d_rank);
     c->d_rank = nullptr;
     cudaFree(c->d_rankp); cudaFree(c->d_byrank); cudaFree(c->d_rlcb);
-    cudaFree(c->d_lna2);
-    c->d_rankp = nullptr; c->d_byrank = nullptr; c->d_rlcb = nullptr; c->d_lna2 = nullptr;
+    cudaFree(c->d_edge);
+    c->d_edge = nullptr;
+    c->d_rankp = nullptr; c->d_byrank = nullptr; c->d_rlcb = nullptr;
     c->rank_ql = 0;
     c->d_w64 = nullptr; c->d_w32 = nullptr; c->d_r = c->d_lnc = c->d_beta = c->d_lna1 = nullptr;
     c->d_lnw = nullptr;

@@ -38,9 +38,6 @@
 #ifndef SG_CWS_U2
 #define SG_CWS_U2 0
 #endif
-#ifndef SG_RANK_U2
-#define SG_RANK_U2 0
-#endif
 #define SG_EMPTY 0xFFFFFFFFu
 
 struct SigArgs {
@@ -55,10 +52,11 @@ struct SigArgs {
     uint64_t *sig_out;
     const double *lna1, *tr, *tlnc, *tbeta, *lnw;
     const void *rank;  // per-slot rank of ln_a1: u16 (n <= 16) or u32
-    const uint16_t *rankp;  // order-free path: u16 ranks, 16*QL slots per token row
-    const uint4 *byrank;    // order-free path: (slot << n | rank) -> {ln_a1, token | t1 << 16}
+    const uint16_t *rankp;  // order-free path: u16 ranks, 16*QL slots per (2 token + count - 1) row
+    const uint4 *byrank;    // order-free path: (slot << (n+1) | rank) -> {ln_a, token | t << 16}, counts 1-2
     const double2 *rlcb;    // order-free path: (token, slot) -> {r, 1/r}, {ln c, beta}
-    const double *lna2;     // order-free path: (token, slot) -> ln_a for count 2 (or null)
+    const double2 *edge;    // order-free path: (token 0 | 2^n-1, count, slot) -> {ln_a, t} (or null)
+    int maxc;
     int64_t N;
     int words, nb, n, T, P2, H, S, L, K;
     int warp_smem;  // bytes per warp
@@ -691,27 +689,21 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
     constexpr int NS = (16 * QL + 31) / 32;
     constexpr int A = 4 * QL;
     const int S = a.S;
-    uint16_t *list1 = w.ustart;
-    uint16_t *list2 = w.ucnt;                  // count-2 tokens from the front
-    uint16_t *listm = w.ucnt + (a.T - 1);      // count > 2 tokens from the back (listm[-f])
-    int n1 = 0, n2 = 0, nm = 0;
+    uint16_t *list1 = w.ustart;                // count-1 and count-2 tokens (combined ranks)
+    uint16_t *listm = w.ucnt;                  // count > 2 tokens
+    int n1 = 0, nm = 0;
     const unsigned lt = (1u << lane) - 1u;
-    const bool have2 = a.lna2 != nullptr;
     for (int base = 0; base < D; base += 32) {
         const int d = base + lane;
         const uint32_t key = d < D ? w.ukey[d] : 0u;
         const uint32_t c = key & 0xFFFu;
-        const bool one = d < D && c == 1u;
-        const bool two = d < D && c == 2u && have2;
-        const bool many = d < D && c > 1u && !two;
+        const bool one = d < D && c <= 2u;
+        const bool many = d < D && c > 2u;
         const unsigned m1 = __ballot_sync(0xFFFFFFFFu, one);
-        const unsigned m2 = __ballot_sync(0xFFFFFFFFu, two);
         const unsigned mm = __ballot_sync(0xFFFFFFFFu, many);
         if (one) list1[n1 + __popc(m1 & lt)] = (uint16_t)d;
-        if (two) list2[n2 + __popc(m2 & lt)] = (uint16_t)d;
-        if (many) listm[-(nm + __popc(mm & lt))] = (uint16_t)d;
+        if (many) listm[nm + __popc(mm & lt)] = (uint16_t)d;
         n1 += __popc(m1);
-        n2 += __popc(m2);
         nm += __popc(mm);
     }
     __syncwarp();
@@ -721,30 +713,11 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
 #pragma unroll
     for (int i = 0; i < A; i++) acc[i] = 0xFFFFFFFFu;
     const uint4 *rp = reinterpret_cast<const uint4 *>(a.rankp);
-#if SG_RANK_U2
-    for (int e0 = 0; e0 < n1; e0 += 32) {
-        const int ea = e0 + j, eb = e0 + 16 + j;
-        uint4 va[QL], vb[QL];
-        const uint4 ff = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        const size_t ba = ea < n1 ? (size_t)(w.ukey[list1[ea]] >> 12) * (2 * QL) + h * QL : 0;
-        const size_t bb = eb < n1 ? (size_t)(w.ukey[list1[eb]] >> 12) * (2 * QL) + h * QL : 0;
-#pragma unroll
-        for (int q = 0; q < QL; q++) va[q] = ea < n1 ? __ldg(rp + ba + q) : ff;
-#pragma unroll
-        for (int q = 0; q < QL; q++) vb[q] = eb < n1 ? __ldg(rp + bb + q) : ff;
-#pragma unroll
-        for (int q = 0; q < QL; q++) {
-            acc[4 * q + 0] = __vminu2(acc[4 * q + 0], __vminu2(va[q].x, vb[q].x));
-            acc[4 * q + 1] = __vminu2(acc[4 * q + 1], __vminu2(va[q].y, vb[q].y));
-            acc[4 * q + 2] = __vminu2(acc[4 * q + 2], __vminu2(va[q].z, vb[q].z));
-            acc[4 * q + 3] = __vminu2(acc[4 * q + 3], __vminu2(va[q].w, vb[q].w));
-        }
-    }
-#else
     for (int e0 = 0; e0 < n1; e0 += 16) {
         const int ea = e0 + j;
         if (ea < n1) {
-            const size_t ba = (size_t)(w.ukey[list1[ea]] >> 12) * (2 * QL) + h * QL;
+            const uint32_t kk = w.ukey[list1[ea]];
+            const size_t ba = (size_t)(((kk >> 12) << 1) | ((kk & 0xFFFu) - 1u)) * (2 * QL) + h * QL;
 #pragma unroll
             for (int q = 0; q < QL; q++) {
                 const uint4 va = __ldg(rp + ba + q);
@@ -755,7 +728,6 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
             }
         }
     }
-#endif
     int rbase = 0;
     rs_reduce<A, 8>(acc, lane, rbase);
     constexpr int AF = rs_final(A, 8);
@@ -771,8 +743,8 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
                 const uint32_t rk = (acc[l >> 1] >> (16 * hw)) & 0xFFFFu;
                 double v = (double)INFINITY;
                 uint32_t tt = 0xFFFFu;
-                if (rk != 0xFFFFu) {
-                    const uint4 br = __ldg(a.byrank + (((size_t)s << a.n) | rk));
+                if (n1 > 0) {  // every slot then has a real minimum (0xFFFF is a valid rank)
+                    const uint4 br = __ldg(a.byrank + (((size_t)s << (a.n + 1)) | rk));
                     v = __hiloint2double((int)br.y, (int)br.x);
                     tt = br.z;
                 }
@@ -803,45 +775,25 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
         btok[i] = l ? tok : btok[i];
         bestt[i] = l ? t : bestt[i];
     };
-    // count-2 tokens: tabulated ln_a2 (exact reference formula, rank_fast_kernel);
-    // t is recomputed for the slots they win (bestt = -1 marks them)
-    {
-        int f = 0;
-        for (; f + 1 < n2; f += 2) {
-            const uint32_t ta = w.ukey[list2[f]] >> 12, tb = w.ukey[list2[f + 1]] >> 12;
-            double va[NS], vb[NS];
-#pragma unroll
-            for (int i = 0; i < NS; i++) {
-                const int s = min(lane + 32 * i, S - 1);
-                va[i] = __ldg(a.lna2 + (size_t)ta * S + s);
-                vb[i] = __ldg(a.lna2 + (size_t)tb * S + s);
-            }
-#pragma unroll
-            for (int i = 0; i < NS; i++) {
-                if (lane + 32 * i < S) {
-                    bool l = va[i] < best[i] || (va[i] == best[i] && ta < btok[i]);
-                    best[i] = l ? va[i] : best[i]; btok[i] = l ? ta : btok[i]; bestt[i] = l ? -1.0 : bestt[i];
-                    l = vb[i] < best[i] || (vb[i] == best[i] && tb < btok[i]);
-                    best[i] = l ? vb[i] : best[i]; btok[i] = l ? tb : btok[i]; bestt[i] = l ? -1.0 : bestt[i];
-                }
-            }
-        }
-        if (f < n2) {
-            const uint32_t ta = w.ukey[list2[f]] >> 12;
+    const uint32_t tmax = (1u << a.n) - 1u;
+    for (int f = 0; f < nm; f++) {
+        const uint32_t ka = w.ukey[listm[f]];
+        const uint32_t ta = ka >> 12;
+        if (a.edge && (ta == 0u || ta == tmax)) {
+            // all-zero / all-one tokens (sign runs; most counts > 2): tabulated
+            // {ln_a, t} per (count, slot), same exact formula
+            const double2 *er = a.edge + ((size_t)(ta ? 1 : 0) * (a.maxc + 1) + (ka & 0xFFFu)) * S;
 #pragma unroll
             for (int i = 0; i < NS; i++) {
                 const int s = lane + 32 * i;
                 if (s < S) {
-                    const double v = __ldg(a.lna2 + (size_t)ta * S + s);
-                    const bool l = v < best[i] || (v == best[i] && ta < btok[i]);
-                    best[i] = l ? v : best[i]; btok[i] = l ? ta : btok[i]; bestt[i] = l ? -1.0 : bestt[i];
+                    const double2 v = __ldg(er + s);
+                    const bool l = v.x < best[i] || (v.x == best[i] && ta < btok[i]);
+                    best[i] = l ? v.x : best[i]; btok[i] = l ? ta : btok[i]; bestt[i] = l ? v.y : bestt[i];
                 }
             }
+            continue;
         }
-    }
-    for (int f = 0; f < nm; f++) {
-        const uint32_t ka = w.ukey[listm[-f]];
-        const uint32_t ta = ka >> 12;
         const double lwa = __ldg(a.lnw + (ka & 0xFFFu));
 #pragma unroll
         for (int i = 0; i < NS; i++) {
@@ -849,18 +801,6 @@ __device__ void warp_cws_fast(const SigArgs &a, int64_t row, const WarpSmem &w, 
             if (s < S) {
                 const size_t ea = 2 * ((size_t)ta * S + s);
                 eval(ta, lwa, i, __ldg(a.rlcb + ea), __ldg(a.rlcb + ea + 1));
-            }
-        }
-    }
-    if (n2 > 0) {
-        const double ln2 = __ldg(a.lnw + 2);
-#pragma unroll
-        for (int i = 0; i < NS; i++) {
-            const int s = lane + 32 * i;
-            if (s < S && bestt[i] < 0.0) {
-                const size_t ea = 2 * ((size_t)btok[i] * S + s);
-                const double2 p0 = __ldg(a.rlcb + ea), p1 = __ldg(a.rlcb + ea + 1);
-                bestt[i] = cws_t_inv(ln2, p0.x, p0.y, p1.y);
             }
         }
     }
@@ -1050,7 +990,8 @@ int ssh_launch_shingle_cws(ssh_ctx *ctx, const uint64_t *bits, const uint32_t *t
     a.rankp = ctx->d_rankp;
     a.byrank = ctx->d_byrank;
     a.rlcb = reinterpret_cast<const double2 *>(ctx->d_rlcb);
-    a.lna2 = ctx->d_lna2;
+    a.edge = reinterpret_cast<const double2 *>(ctx->d_edge);
+    a.maxc = ctx->max_count;
     a.N = N; a.words = ctx->words; a.nb = ctx->nb; a.n = ctx->p.n; a.T = ctx->T;
     int P2 = 32;
     while (P2 < ctx->T) P2 <<= 1;

@@ -538,24 +538,58 @@ __global__ void rank_scatter_kernel(const uint32_t *__restrict__ rows, int64_t T
     }
 }
 
-// Order-free CWS tables (signature.cu, cws_fast): padded u16 ranks per token
-// row, the count-1 winner record per (slot, rank) and the packed variates.
-__global__ void rank_fast_kernel(const uint32_t *__restrict__ rows, int64_t T, int S, int SP,
+// ln_a and t of a count-2 token (wmh.py:74-76, reference op order):
+// t = floor(fl(fl(ln 2 / r) + beta)), ln_a = (ln_c - r (t - beta)) - r.
+__device__ __forceinline__ double lna_count2(double rr, double lnc, double b, double ln2, double &t) {
+    t = floor(__dadd_rn(__ddiv_rn(ln2, rr), b));
+    const double lny = __dmul_rn(rr, __dsub_rn(t, b));
+    return __dsub_rn(__dsub_rn(lnc, lny), rr);
+}
+
+// Orderable keys of the combined (token, count in {1, 2}) rows: row 2 tok + (count - 1).
+__global__ void comb_orderable_kernel(const double *__restrict__ r, const double *__restrict__ lnc,
+                                      const double *__restrict__ beta, const double *__restrict__ lna1,
+                                      double ln2, size_t n, int S, uint64_t *__restrict__ keys) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        const size_t tok = e / S, s = e - tok * S;
+        double t2;
+        const double v2 = lna_count2(r[e], lnc[e], beta[e], ln2, t2);
+        const double v[2] = {lna1[e], v2};
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            const uint64_t bb = (uint64_t)__double_as_longlong(v[c]);
+            keys[(2 * tok + c) * S + s] = (bb >> 63) ? ~bb : (bb | 0x8000000000000000ULL);
+        }
+    }
+}
+
+// Order-free CWS tables (signature.cu, cws_fast): padded u16 ranks per
+// combined row (count-1 and count-2 tokens share one per-slot order by
+// (ln_a, row) = (ln_a, token): a token has one count per series), the winner
+// record per (slot, rank), and the packed variates.
+__global__ void rank_fast_kernel(const uint32_t *__restrict__ rows, int64_t T2, int S, int SP,
                                  const double *__restrict__ r, const double *__restrict__ lnc,
                                  const double *__restrict__ beta, const double *__restrict__ lna1,
-                                 uint16_t *__restrict__ rankp, uint4 *__restrict__ byrank,
-                                 double *__restrict__ rlcb, double *__restrict__ lna2, double ln2) {
-    const int64_t n = T * S;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = e / T, p = e - j * T;
-        const uint32_t tok = rows[e];
-        rankp[(int64_t)tok * SP + j] = (uint16_t)p;
+                                 double ln2, uint16_t *__restrict__ rankp, uint4 *__restrict__ byrank,
+                                 double *__restrict__ rlcb) {
+    const int64_t n2 = T2 * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / T2, p = e - j * T2;
+        const uint32_t row = rows[e];
+        const uint32_t tok = row >> 1;
+        rankp[(int64_t)row * SP + j] = (uint16_t)p;
         const int64_t te = (int64_t)tok * S + j;
-        const double v = lna1[te];
-        const uint32_t t1 = (uint32_t)floor(beta[te]);  // beta in (0, 1]: 0 or 1
+        double v, t;
+        if (row & 1u) {
+            v = lna_count2(r[te], lnc[te], beta[te], ln2, t);
+        } else {
+            v = lna1[te];
+            t = floor(beta[te]);  // beta in (0, 1]: 0 or 1
+        }
         byrank[e] = make_uint4((uint32_t)__double2loint(v), (uint32_t)__double2hiint(v),
-                               tok | (t1 << 16), 0u);
+                               tok | ((uint32_t)t << 16), 0u);
     }
+    const int64_t n = (T2 / 2) * S;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         const double rr = r[e];
         double *q = rlcb + 4 * e;
@@ -563,14 +597,26 @@ __global__ void rank_fast_kernel(const uint32_t *__restrict__ rows, int64_t T, i
         q[1] = __drcp_rn(rr);
         q[2] = lnc[e];
         q[3] = beta[e];
-        if (lna2) {
-            // count 2 (wmh.py:74-76, reference op order): t = floor(fl(fl(ln 2 / r) + beta)),
-            // ln_a = (ln_c - r (t - beta)) - r
-            const double b = beta[e];
-            const double t = floor(__dadd_rn(__ddiv_rn(ln2, rr), b));
-            const double lny = __dmul_rn(rr, __dsub_rn(t, b));
-            lna2[e] = __dsub_rn(__dsub_rn(lnc[e], lny), rr);
-        }
+    }
+}
+
+// {ln_a, t} for the all-zero and all-one tokens at every count (wmh.py:74-76,
+// reference op order): e = (which * (maxc + 1) + count) * S + slot.
+__global__ void edge_table_kernel(const double *__restrict__ r, const double *__restrict__ lnc,
+                                  const double *__restrict__ beta, const double *__restrict__ lnw,
+                                  int n, int S, int maxc, double2 *__restrict__ out) {
+    const int64_t total = 2LL * (maxc + 1) * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(e % S);
+        const int64_t wc = e / S;
+        const int c = (int)(wc % (maxc + 1));
+        const int which = (int)(wc / (maxc + 1));
+        if (c < 1) { out[e] = make_double2(INFINITY, 0.0); continue; }
+        const int64_t te = (int64_t)(which ? ((1 << n) - 1) : 0) * S + s;
+        const double rr = r[te], b = beta[te];
+        const double t = floor(__dadd_rn(__ddiv_rn(lnw[c], rr), b));
+        const double lny = __dmul_rn(rr, __dsub_rn(t, b));
+        out[e] = make_double2(__dsub_rn(__dsub_rn(lnc[te], lny), rr), t);
     }
 }
 
@@ -604,21 +650,49 @@ int ssh_build_ranks(ssh_ctx *ctx, cudaStream_t st) {
         const int ql = ctx->p.n <= 15 ? pick_rank_ql(S) : 0;
         if (ql > 0) {
             const int SP = 16 * ql;
-            cudaError_t e = cudaMalloc(&ctx->d_rankp, sizeof(uint16_t) * (size_t)T * SP);
-            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_byrank, sizeof(uint4) * n);
-            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rlcb, 4 * sizeof(double) * n);
-            // count-2 table when ln(2) is in the uploaded ln(count) table (SSH_CWS_LNA2=0 disables)
-            const char *ev = getenv("SSH_CWS_LNA2");
-            const bool want2 = ctx->max_count >= 2 && !(ev && ev[0] == '0');
-            if (e == cudaSuccess && want2) e = cudaMalloc(&ctx->d_lna2, sizeof(double) * n);
-            if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_rankp, 0xFF, sizeof(uint16_t) * (size_t)T * SP, st);
+            const int64_t T2 = 2 * T;
+            const size_t n2 = (size_t)T2 * S;
+            uint64_t *keys2 = nullptr;
+            uint32_t *rows2 = nullptr;
+            cudaError_t e = cudaMalloc(&keys2, sizeof(uint64_t) * n2);
+            if (e == cudaSuccess) e = cudaMalloc(&rows2, sizeof(uint32_t) * n2);
             if (e == cudaSuccess) {
-                rank_fast_kernel<<<grid, 256, 0, st>>>(rows, T, S, SP, ctx->d_r, ctx->d_lnc, ctx->d_beta,
-                                                       ctx->d_lna1, ctx->d_rankp, ctx->d_byrank,
-                                                       ctx->d_rlcb, ctx->d_lna2, ctx->h_ln2);
+                comb_orderable_kernel<<<grid, 256, 0, st>>>(ctx->d_r, ctx->d_lnc, ctx->d_beta, ctx->d_lna1,
+                                                            ctx->h_ln2, n, S, keys2);
                 ssh_count_launch();
                 e = cudaGetLastError();
             }
+            if (e == cudaSuccess) {
+                uint64_t *sorted2 = nullptr;
+                const int rc2 = ssh_sort_columns(ctx, keys2, T2, S, rows2, &sorted2, st);
+                if (rc2 != SSH_OK) e = cudaErrorUnknown;
+            }
+            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rankp, sizeof(uint16_t) * (size_t)T2 * SP);
+            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_byrank, sizeof(uint4) * n2);
+            if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rlcb, 4 * sizeof(double) * n);
+            const char *ee = getenv("SSH_CWS_EDGE");
+            const bool wante = !(ee && ee[0] == '0');
+            const size_t nedge = 2 * (size_t)(ctx->max_count + 1) * S;
+            if (e == cudaSuccess && wante) e = cudaMalloc(&ctx->d_edge, 2 * sizeof(double) * nedge);
+            if (e == cudaSuccess && wante) {
+                const int g2 = (int)std::min<size_t>((nedge + 255) / 256, (size_t)ctx->num_sms * 8);
+                edge_table_kernel<<<g2, 256, 0, st>>>(ctx->d_r, ctx->d_lnc, ctx->d_beta, ctx->d_lnw, ctx->p.n, S,
+                                                      ctx->max_count, reinterpret_cast<double2 *>(ctx->d_edge));
+                ssh_count_launch();
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_rankp, 0xFF, sizeof(uint16_t) * (size_t)T2 * SP, st);
+            if (e == cudaSuccess) {
+                const int g3 = (int)std::min<size_t>((n2 + 255) / 256, (size_t)ctx->num_sms * 16);
+                rank_fast_kernel<<<g3, 256, 0, st>>>(rows2, T2, S, SP, ctx->d_r, ctx->d_lnc, ctx->d_beta,
+                                                     ctx->d_lna1, ctx->h_ln2, ctx->d_rankp, ctx->d_byrank,
+                                                     ctx->d_rlcb);
+                ssh_count_launch();
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            cudaFree(keys2);
+            cudaFree(rows2);
             if (e != cudaSuccess) rc = ssh_cuda_fail(e, "ssh_build_ranks(fast tables)", __FILE__, __LINE__);
             else ctx->rank_ql = ql;
         }
