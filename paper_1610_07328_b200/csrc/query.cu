@@ -681,7 +681,9 @@ __device__ __forceinline__ float code_f(uint32_t w, int t) {
     return __uint_as_float(__byte_perm(w, 0x4B000000u, (unsigned)t | 0x7440u)) - 8388608.f;
 }
 
-#define SAMPLE_SHIFT 3  // sample pass: bitmap words w with w % 8 == 0
+#ifndef SAMPLE_SHIFT
+#define SAMPLE_SHIFT 5  // sample pass: bitmap words w with w % 32 == 0 (3: 27.9 ms, 4: 27.3, 5: 27.0 per 1000-query batch)
+#endif
 
 template <bool SAMPLE>
 __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
@@ -875,7 +877,8 @@ __global__ void cutoff_kernel(const unsigned *__restrict__ hist, int target, int
         part[threadIdx.x] += v;
         __syncthreads();
     }
-    const unsigned need = (unsigned)(target >> SAMPLE_SHIFT);
+    // at least one sampled member: need = 0 would leave binhi unset
+    const unsigned need = max(1u, (unsigned)(target >> SAMPLE_SHIFT));
     const unsigned before = part[threadIdx.x] - loc;
     if (threadIdx.x == 0) {
         binlo[q] = 0;
