@@ -859,16 +859,19 @@ extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t 
     // pool reuses their memory), then summarise on the side stream
     int rc = ssh_alloc_summaries(ctx, &summ, N, st);
     if (rc) return rc;
-    SSH_CUDA(cudaEventRecord(ctx->ev_fork, st));
-    SSH_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    rc = ssh_launch_summaries_rows(ctx, &summ, X, 0, N, ld, ctx->side);
-    if (rc == SSH_OK) rc = cudaEventRecord(ctx->ev_join, ctx->side) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
-    if (rc == SSH_OK) rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st);
+    // sketch + CWS first (CWS fills every SM), then the summaries on the side
+    // stream run alongside the bucket-table sorts (memory-bound kernels with
+    // host syncs for the bucket counts between them); joined at the end
+    rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st);
     if (rc == SSH_OK)
         rc = ssh_launch_shingle_cws(ctx, bits, nullptr, nullptr, nullptr, N, nullptr, nullptr, nullptr,
                                     nullptr, sig, SIG_MODE_FUSED, st);
-    if (rc == SSH_OK) rc = cudaStreamWaitEvent(st, ctx->ev_join, 0) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
+    if (rc == SSH_OK) rc = cudaEventRecord(ctx->ev_fork, st) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
+    if (rc == SSH_OK) rc = cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
+    if (rc == SSH_OK) rc = ssh_launch_summaries_rows(ctx, &summ, X, 0, N, ld, ctx->side);
+    if (rc == SSH_OK) rc = cudaEventRecord(ctx->ev_join, ctx->side) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
     if (rc == SSH_OK) rc = ssh_index_build(ctx, sig, N, id_base, out, stream);
+    if (rc == SSH_OK) rc = cudaStreamWaitEvent(st, ctx->ev_join, 0) == cudaSuccess ? SSH_OK : SSH_ERR_CUDA;
     if (rc != SSH_OK) {
         cudaStreamWaitEvent(st, ctx->ev_join, 0);
         if (summ.rec) cudaFreeAsync(summ.rec, st);
