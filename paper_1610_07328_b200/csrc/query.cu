@@ -446,16 +446,31 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 12) ? 4 : 1) summaries
         const float inv = 1.0f / sc;
         // sample codes, 4 per lane per 128-sample chunk (global) + padded byte arrays (smem)
         uint8_t *cr = a.codes + row * a.cstride;
+        const bool r_even = (a.r & 1) == 0;
         for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
             uint32_t pk = 0;
+            if (i4 + 4 <= m && r_even) {
+                // whole quad: one LDS.128, codes packed as u16 pairs (4-byte aligned: r even)
+                const float4 x4 = *reinterpret_cast<const float4 *>(xs + i4);
+                const int c0 = code_in(x4.x, lo, sc, inv), c1 = code_in(x4.y, lo, sc, inv);
+                const int c2 = code_in(x4.z, lo, sc, inv), c3 = code_in(x4.w, lo, sc, inv);
+                pk = (uint32_t)c0 | ((uint32_t)c1 << 8) | ((uint32_t)c2 << 16) | ((uint32_t)c3 << 24);
+                const uint32_t w01 = (uint32_t)c0 | ((uint32_t)c1 << 16), w23 = (uint32_t)c2 | ((uint32_t)c3 << 16);
+                const int wi = (a.r + i4) >> 1;
+                cmx[wi] = w01;
+                cmx[wi + 1] = w23;
+                cmn[wi] = 0x00FF00FFu - w01;
+                cmn[wi + 1] = 0x00FF00FFu - w23;
+            } else {
 #pragma unroll
-            for (int t = 0; t < 4; t++) {
-                const int i = i4 + t;
-                if (i < m) {
-                    const int c = code_in(xs[i], lo, sc, inv);
-                    pk |= (uint32_t)c << (8 * t);
-                    bmx[a.r + i] = (uint16_t)c;
-                    bmn[a.r + i] = (uint16_t)(255 - c);
+                for (int t = 0; t < 4; t++) {
+                    const int i = i4 + t;
+                    if (i < m) {
+                        const int c = code_in(xs[i], lo, sc, inv);
+                        pk |= (uint32_t)c << (8 * t);
+                        bmx[a.r + i] = (uint16_t)c;
+                        bmn[a.r + i] = (uint16_t)(255 - c);
+                    }
                 }
             }
             *reinterpret_cast<uint32_t *>(cr + i4) = pk;
