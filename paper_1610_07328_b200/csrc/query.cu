@@ -1602,6 +1602,12 @@ struct DtwCommon {
 };
 
 #define DP_WARPS 4
+#ifndef DTWP_PAIRED
+#define DTWP_PAIRED 1
+#endif
+#ifndef DTWP_MINB
+#define DTWP_MINB 1
+#endif
 #define DP_MAXPASS 64  // longest pooled row pass
 #ifndef SSH_DTW_PASS_DOUBLING
 #define SSH_DTW_PASS_DOUBLING 0
@@ -1633,6 +1639,69 @@ __device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t ro
         const float xr[4] = {xc.x, xc.y, xc.z, xc.w};
         float lft[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
         float rmn[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+#if DTWP_PAIRED
+        // Row u runs two steps behind row u - 1 (step t: band offset k = t - 2u,
+        // query sample i0 + t - u), so rows (u + 1, u) never touch each other's
+        // fresh cells within a step and advance together as one f32x2 pair:
+        // d = fma(y, -1, x) = x - y and cv = fma(d, d, min3) are the same IEEE
+        // operations as the scalar recurrence (in-place band: row u + 1 reads
+        // offsets k - 2, k - 1 that row u wrote one and two steps earlier).
+        // Row minima fold two cells per FMNMX3.
+        constexpr int NSTEP = NB + 6;
+        const float2 xp01 = make_float2(xr[1], xr[0]), xp23 = make_float2(xr[3], xr[2]);
+        const float2 neg1 = make_float2(-1.f, -1.f);
+        float yw[NSTEP + 4];
+        float cvp[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        const float4 *yp = reinterpret_cast<const float4 *>(yq + i0);
+#pragma unroll
+        for (int t = 0; t < NSTEP; t++) {
+            if ((t & 3) == 0 && t < NB + 3) {
+                const float4 v = __ldg(yp + (t >> 2));
+                yw[t] = v.x; yw[t + 1] = v.y; yw[t + 2] = v.z; yw[t + 3] = v.w;
+            }
+            float cvs[4];
+            bool val[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) val[u] = t - 2 * u >= 0 && t - 2 * u < NB;
+#pragma unroll
+            for (int pr = 0; pr < 2; pr++) {
+                const int ua = 2 * pr, ub = 2 * pr + 1;  // rows (ub, ua) -> pair {.x = ub, .y = ua}
+                const int ka = t - 2 * ua, kb = t - 2 * ub;
+                if (val[ua] && val[ub]) {
+                    const float upa = (ka + 1 < NB) ? band[ka + 1] : INFINITY;
+                    const float ma = fminf(fminf(band[ka], upa), lft[ua]);
+                    const float mb = fminf(fminf(band[kb], band[kb + 1]), lft[ub]);
+                    const float2 d = __ffma2_rn(make_float2(yw[t - ub], yw[t - ua]), neg1, pr ? xp23 : xp01);
+                    const float2 cv = __ffma2_rn(d, d, make_float2(mb, ma));
+                    cvs[ua] = cv.y;
+                    cvs[ub] = cv.x;
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int u = h ? ub : ua;
+                        const int k = t - 2 * u;
+                        if (val[u]) {
+                            const float up = (k + 1 < NB) ? band[k + 1] : INFINITY;
+                            const float d = xr[u] - yw[t - u];
+                            cvs[u] = fmaf(d, d, fminf(fminf(band[k], up), lft[u]));
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int k = t - 2 * u;
+                if (val[u]) {
+                    band[k] = cvs[u];
+                    lft[u] = cvs[u];
+                    if (k & 1) rmn[u] = fminf(fminf(rmn[u], cvp[u]), cvs[u]);
+                    else cvp[u] = cvs[u];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) rmn[u] = fminf(rmn[u], cvp[u]);  // NB odd: the last cell
+#else
         const float4 *yp = reinterpret_cast<const float4 *>(yq + i0);
 #pragma unroll
         for (int s4 = 0; s4 < (NB + 3 + 3) / 4; s4++) {
@@ -1655,6 +1724,7 @@ __device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t ro
                 }
             }
         }
+#endif
         const float4 u4 = __ldg(reinterpret_cast<const float4 *>(uq + i0));
         const float4 l4 = __ldg(reinterpret_cast<const float4 *>(lq + i0));
         const float uu[4] = {u4.x, u4.y, u4.z, u4.w}, ll[4] = {l4.x, l4.y, l4.z, l4.w};
@@ -1731,7 +1801,7 @@ __device__ __forceinline__ void dtwp_flush(const DtwCommon &C, unsigned long lon
 
 // first pass, per query slot: wave list entries -> rows [0, b) -> pool
 template <int R>
-__global__ void __launch_bounds__(32 * DP_WARPS)
+__global__ void __launch_bounds__(32 * DP_WARPS, DTWP_MINB)
 dtwp_first_kernel(DtwCommon C, const int *__restrict__ act, const uint32_t *__restrict__ wrows,
                   const float2 *__restrict__ wlb, const int *__restrict__ wcnt, int64_t wcap,
                   const uint4 *__restrict__ rec, int b, DtwPool P) {
@@ -1980,7 +2050,7 @@ __device__ __forceinline__ void dtwt_body(const DtwCommon &C, const DtwPool &in,
 // one pooled level: rows [a, b) of every pooled candidate, or, once fewer
 // than lim are left, all remaining rows [a, m) in the wavefront tail
 template <int R>
-__global__ void __launch_bounds__(32 * DP_WARPS)
+__global__ void __launch_bounds__(32 * DP_WARPS, DTWP_MINB)
 dtwp_level_kernel(DtwCommon C, DtwPool in, DtwPool P, int a, int b, int lim) {
     extern __shared__ __align__(16) float dtsm[];
     const int n = min(*in.count, (int)in.cap);
