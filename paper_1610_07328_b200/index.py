@@ -609,22 +609,32 @@ def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = Fals
     dt = time.perf_counter() - t0
     nq = Qd.shape[0]
     N = index.n_series
+    # whole-batch conversions to Python scalars (tolist is exact: int64 -> int,
+    # float64 -> float); the per-query loop only slices lists
+    ids_l = ids.tolist()
+    with np.errstate(invalid="ignore"):  # entries past n_out are unused
+        dist_l = np.sqrt(d2).tolist()
+    n_out_l = n_out.tolist()
+    n_cand_l = n_cand.tolist()
+    cnt_l = counters.tolist()
+    status_l = status.tolist()
+    per_q = dt / max(1, nq)
     out = []
     for i in range(nq):
-        n = int(n_out[i])
-        c = counters[i]
-        cascade = SearchStats(candidates=int(n_cand[i]), kim_pruned=int(c[0]), keogh_pruned=int(c[1]),
-                              keogh2_pruned=int(c[2]), dtw_computed=int(c[3]), dtw_abandoned=int(c[4]))
-        timings = {"batch": dt, "per_query": dt / max(1, nq)}
-        if status[i] == 1:
+        timings = {"batch": dt, "per_query": per_q}
+        st = status_l[i]
+        if st == 1:
             stats = QueryStats(n_indexed=N, candidates=0, cascade=SearchStats(0, 0, 0, 0, 0, 0))
             out.append(QueryResult([], [], stats, timings, status="no-candidates", warning=warning))
             continue
-        stats = QueryStats(n_indexed=N, candidates=int(n_cand[i]), cascade=cascade)
-        out.append(QueryResult(ids=[int(v) for v in ids[i, :n]],
-                               distances=[float(v) for v in np.sqrt(d2[i, :n])],
-                               stats=stats, timings=timings,
-                               status="fallback" if status[i] == 2 else "ok", warning=warning))
+        n = n_out_l[i]
+        c = cnt_l[i]
+        nc = n_cand_l[i]
+        cascade = SearchStats(candidates=nc, kim_pruned=c[0], keogh_pruned=c[1], keogh2_pruned=c[2],
+                              dtw_computed=c[3], dtw_abandoned=c[4])
+        stats = QueryStats(n_indexed=N, candidates=nc, cascade=cascade)
+        out.append(QueryResult(ids=ids_l[i][:n], distances=dist_l[i][:n], stats=stats, timings=timings,
+                               status="fallback" if st == 2 else "ok", warning=warning))
     return out
 
 
