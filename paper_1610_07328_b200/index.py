@@ -589,23 +589,25 @@ def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = Fals
         if Qd.ndim == 1:
             Qd = Qd.reshape(1, -1)
     else:
-        Qh = np.asarray(Q, dtype=np.float64)
+        # float32 input goes straight to the device (the f64 round trip is the identity)
+        Qh = Q if isinstance(Q, np.ndarray) and Q.dtype == np.float32 else np.asarray(Q, dtype=np.float64)
         if Qh.ndim == 1:
             Qh = Qh.reshape(1, -1)
-        if not np.all(np.isfinite(Qh)):
+        if not np.isfinite(Qh).all():
             raise ValueError("series values contains non-finite values")
         Qd = _as_device_f32(Qh, index.device)
     if Qd.shape[1] != index.length:
         raise ValueError(f"query length {Qd.shape[1]} does not match indexed length {index.length}")
     k, warning = _validate_k(index, k)
     t0 = time.perf_counter()
-    ids, d2, n_out, n_cand, counters, status = query_batch_device(index, Qd, k, fallback_on_empty)
-    status = status.cpu().numpy()
-    ids = ids.cpu().numpy()
-    d2 = d2.cpu().numpy()
-    n_out = n_out.cpu().numpy()
-    n_cand = n_cand.cpu().numpy()
-    counters = counters.cpu().numpy()
+    dev = query_batch_device(index, Qd, k, fallback_on_empty)
+    # one synchronisation for the six result arrays (pinned, non-blocking copies)
+    torch = _torch()
+    host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev]
+    for h, t in zip(host, dev):
+        h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(index.device).synchronize()
+    ids, d2, n_out, n_cand, counters, status = (h.numpy() for h in host)
     dt = time.perf_counter() - t0
     nq = Qd.shape[0]
     N = index.n_series
