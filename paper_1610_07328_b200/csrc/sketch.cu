@@ -342,8 +342,8 @@ sketch_pair_kernel(const float *__restrict__ X, SketchGeom g, const SketchW2 wp,
 // every window it decides, and the zero tail beyond m only meets zero taps of
 // real windows or windows >= nb that are never emitted.
 // ---------------------------------------------------------------------------
-#ifndef SKS_ST
-#define SKS_ST 16
+#ifndef SKS_ST_DEFAULT
+#define SKS_ST_DEFAULT 16
 #endif
 
 template <int W, int D>
@@ -408,7 +408,7 @@ __device__ __noinline__ double exact_row_dot(const float *x, const double *w64, 
 // gthreads threads (ST series x tps window slots) take tiles round-robin, so
 // up to ns_stages - ngroups tiles are in flight from HBM while the others are
 // computed.
-template <int W, int D, int J>
+template <int W, int D, int J, int SKS_ST>
 __global__ void __launch_bounds__(544)
 sketch_stream_kernel(const float *__restrict__ X, StreamGeom g, const SketchWP<W, D> wp,
                      const double *__restrict__ w64g, uint64_t *__restrict__ bits, long long *stats) {
@@ -691,7 +691,7 @@ static bool try_pair(ssh_ctx *ctx, const float *X, const SketchGeom &g0, uint64_
     return true;
 }
 
-template <int W, int D, int J>
+template <int W, int D, int J, int SKS_ST>
 static bool try_stream(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint64_t *bits,
                        int64_t *stats, cudaStream_t st, int *rc) {
     const ssh_params &p = ctx->p;
@@ -737,7 +737,7 @@ static bool try_stream(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint
         const float b = (d >= D && d - D < W) ? ctx->h_w32[d - D] : 0.f;
         wp.w[d] = make_float2(a, b);
     }
-    auto kern = sketch_stream_kernel<W, D, J>;
+    auto kern = sketch_stream_kernel<W, D, J, SKS_ST>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) { *rc = ssh_cuda_fail(e, "cudaFuncSetAttribute(sketch_stream)", __FILE__, __LINE__); return true; }
     int per_sm = 0;
@@ -759,7 +759,9 @@ int ssh_launch_sketch(ssh_ctx *ctx, const float *X, int64_t N, int64_t ld, uint6
         int rc = SSH_OK;
         if (ctx->p.m >= 64) {
             // J = 20 windows per thread measured best against J = 12 and 16 (configs[1]/[2])
-            if (try_stream<80, 3, 20>(ctx, X, N, ld, bits, stats, st, &rc)) return rc;
+            if (try_stream<80, 3, 20, SKS_ST_DEFAULT>(ctx, X, N, ld, bits, stats, st, &rc)) return rc;
+            // long rows (configs[3], m = 2048): 8-series tiles keep a 3-stage ring
+            if (try_stream<80, 3, 20, 8>(ctx, X, N, ld, bits, stats, st, &rc)) return rc;
         }
     }
     const ssh_params &p = ctx->p;

@@ -97,7 +97,7 @@ def test_sketch_recheck_near_zero(cuda):
     assert int(stats[1]) == int((np.abs(dots) < 1e-9).sum())
 
 
-@pytest.mark.parametrize("m", [512, 1024])
+@pytest.mark.parametrize("m", [512, 1024, 2048])
 def test_sketch_stream_ring_partial_tile(cuda, m):
     """TMA-staged sketch kernel: enough series that every CTA wraps its stage
     ring several times, a partial last tile, and rows with NaN / inf / huge
