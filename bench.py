@@ -299,7 +299,7 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     b = N * (4 * m + 8 * words)
     res["sketch"] = dict(name="sketch (K1)", ms=ms, bytes=b, roofline=dict(
         bound="hbm", achieved=b / ms / 1e6, peak=hbm, unit="GB/s", frac=b / ms / 1e6 / hbm,
-        traffic=_ncu_traffic("sketch_stream_kernel<80, 3, 20>"), kernel="sketch_stream_kernel<80,3,20>",
+        traffic=_ncu_traffic("sketch_stream_kernel<80, 3, 20, 16>"), kernel="sketch_stream_kernel<80,3,20,16>",
         note="algorithmic bytes = N*(4m + 8*ceil(N_B/64)); peak = %s HBM copy; traffic = ncu dram bytes of "
              "the build launch + the 1000-query hash launch (0.1%%) (profiles/r01/traffic_cfg1.json)"
              % peaks["source"]))
