@@ -1014,28 +1014,52 @@ bs_hist_kernel(const float *__restrict__ lb_in, const int64_t *__restrict__ roff
     for (int b = threadIdx.x; b < NBINS; b += blockDim.x) hist[((int64_t)q * NBINS + b) * nch + ch] = h[b];
 }
 
+// exclusive scan of hist[q][*] (NBINS * nch entries, a multiple of 4), one
+// block per query: coalesced 16-byte loads over per-warp segments, a warp
+// scan of the segment totals, then in-lane prefix of 4 + shuffle scans
 __global__ void __launch_bounds__(1024) bs_scan_kernel(uint32_t *__restrict__ hist, int nch) {
-    __shared__ uint32_t part[1024];
+    static_assert(NBINS % 4 == 0, "");
+    __shared__ uint32_t wtot[32];
     const int q = blockIdx.x;
-    uint32_t *h = hist + (int64_t)q * NBINS * nch;
-    const int64_t n = (int64_t)NBINS * nch;
-    const int64_t chunk = (n + 1023) / 1024;
-    const int64_t b = threadIdx.x * chunk, e = min(n, b + chunk);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint4 *h = reinterpret_cast<uint4 *>(hist + (int64_t)q * NBINS * nch);
+    const int64_t n4 = (int64_t)NBINS * nch / 4;
+    const int64_t seg = ((n4 + 31) / 32 + 31) / 32 * 32;
+    const int64_t b = (int64_t)w * seg, e = min(n4, b + seg);
     uint32_t s = 0;
-    for (int64_t i = b; i < e; i++) s += h[i];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        const uint32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
+#pragma unroll 4
+    for (int64_t i = b + lane; i < e; i += 32) {
+        const uint4 v = h[i];
+        s += v.x + v.y + v.z + v.w;
     }
-    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
-    for (int64_t i = b; i < e; i++) {
-        const uint32_t v = h[i];
-        h[i] = run;
-        run += v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if (lane == 0) wtot[w] = s;
+    __syncthreads();
+    uint32_t run;
+    {
+        const uint32_t t = wtot[lane];
+        uint32_t x = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        run = __shfl_sync(0xFFFFFFFFu, x - t, w);
+    }
+    for (int64_t c = b; c < e; c += 32) {
+        const int64_t i = c + lane;
+        const uint4 v = i < e ? h[i] : make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t p1 = v.x, p2 = p1 + v.y, p3 = p2 + v.z, tot = p3 + v.w;
+        uint32_t x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        const uint32_t base = run + x - tot;
+        if (i < e) h[i] = make_uint4(base, base + p1, base + p2, base + p3);
+        run += __shfl_sync(0xFFFFFFFFu, x, 31);
     }
 }
 
