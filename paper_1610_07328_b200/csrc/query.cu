@@ -1138,32 +1138,32 @@ __device__ __forceinline__ void wl_load_env(const uint8_t *cr, int mp, int base,
     for (int c = 0; c < 4; c++) v[c] = base + 128 * c < mp ? __ldg(p + 32 * c) : make_uint2(0u, 0u);
 }
 
-// partial LB_Keogh2 over chunks [C0, C1) of one 512-sample block (tails: sq =
+// partial LB_Keogh2 over chunks [C0, C1) of one 512-sample block (tails: sqn =
 // NaN -> term 0).  Packed f32x2: {ue, le} = fma({cU, cL}, sc, lo) and
-// {q - ue, le - q} = fma({ue, le}, {-1, 1}, {q, -q}) are the same IEEE
-// operations as the scalar forms (dtw.py:154-168 terms, fp32 screen).
+// {ue - q, le - q} = {ue, le} + (-q) (broadcast addend), so the terms
+// max(q - ue, le - q, 0) = max(-(ue - q), le - q, 0) are the same IEEE values
+// as the scalar forms (round-to-nearest is sign-symmetric; dtw.py:154-168
+// terms, fp32 screen).  sqn holds -q_i: one 16-byte LDS per 4 samples.
 template <int C0, int C1>
-__device__ __forceinline__ float wl_env_chunks(const uint2 (&v)[4], const float2 *sq2, int base, int mp, float sc,
+__device__ __forceinline__ float wl_env_chunks(const uint2 (&v)[4], const float *sqn, int base, int mp, float sc,
                                                float lo) {
     const int lane = threadIdx.x & 31;
     float2 acc = make_float2(0.f, 0.f);
-    const float2 sc2 = make_float2(sc, sc), lo2 = make_float2(lo, lo), pm = make_float2(-1.f, 1.f);
+    const float2 sc2 = make_float2(sc, sc), lo2 = make_float2(lo, lo);
 #pragma unroll
     for (int c = C0; c < C1; c++) {
         const int i0 = base + 128 * c + 4 * lane;
         if (base + 128 * c < mp) {
-            const float4 q01 = *reinterpret_cast<const float4 *>(sq2 + i0);
-            const float4 q23 = *reinterpret_cast<const float4 *>(sq2 + i0 + 2);
-            const float2 qq[4] = {make_float2(q01.x, q01.y), make_float2(q01.z, q01.w),
-                                  make_float2(q23.x, q23.y), make_float2(q23.z, q23.w)};  // {q, -q}
+            const float4 qn = *reinterpret_cast<const float4 *>(sqn + i0);
+            const float nq[4] = {qn.x, qn.y, qn.z, qn.w};
             float dd[4];
 #pragma unroll
             for (int t = 0; t < 4; t++) {
                 const uint32_t wv = t < 2 ? v[c].x : v[c].y;
                 const int bu = 2 * (t & 1);
                 const float2 ul = __ffma2_rn(code_f2(wv, bu, bu + 1), sc2, lo2);
-                const float2 df = __ffma2_rn(ul, pm, qq[t]);
-                dd[t] = fmaxf(fmaxf(df.x, df.y), 0.f);
+                const float2 df = __fadd2_rn(ul, make_float2(nq[t], nq[t]));
+                dd[t] = fmaxf(fmaxf(-df.x, df.y), 0.f);
             }
             acc = __ffma2_rn(make_float2(dd[0], dd[1]), make_float2(dd[0], dd[1]), acc);
             acc = __ffma2_rn(make_float2(dd[2], dd[3]), make_float2(dd[2], dd[3]), acc);
@@ -1220,13 +1220,13 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
     const int end = min(a.cnt[q], start + a.wave);
     if (start + (int)blockIdx.x * nw * 32 >= end) return;
     float2 *sul = reinterpret_cast<float2 *>(wsm);       // {-U_i, L_i}
-    float2 *sq2 = reinterpret_cast<float2 *>(wsm) + mp;  // {q_i, -q_i}
+    float *sqn = reinterpret_cast<float *>(reinterpret_cast<float2 *>(wsm) + mp);  // -q_i
     for (int i = threadIdx.x; i < mp; i += blockDim.x) {
         const bool in = i < m;
         sul[i] = in ? make_float2(-a.U[(int64_t)q * m + i], a.Lo[(int64_t)q * m + i])
                     : make_float2(-INFINITY, -INFINITY);
         const float qv = in ? a.Q[(int64_t)q * m + i] : __int_as_float(0x7FC00000);
-        sq2[i] = make_float2(qv, -qv);
+        sqn[i] = -qv;
     }
     __syncthreads();
     const float T = a.thr[q];
@@ -1276,11 +1276,11 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
             for (int base = 0; base < mp; base += WL_BLK) {
                 if (base) wl_load_env(cr, mp, base, vc);
                 nbytes += 2 * min(WL_BLK, mp - base);
-                acc += wl_env_chunks<0, 2>(vc, sq2, base, mp, sc, lo);
+                acc += wl_env_chunks<0, 2>(vc, sqn, base, mp, sc, lo);
                 tot2 = warp_sum(acc);
                 if (tot2 > T) { pruned = true; break; }
                 if (base + 256 < mp) {
-                    acc += wl_env_chunks<2, 4>(vc, sq2, base, mp, sc, lo);
+                    acc += wl_env_chunks<2, 4>(vc, sqn, base, mp, sc, lo);
                     tot2 = warp_sum(acc);
                     if (tot2 > T) { pruned = true; break; }
                 }
