@@ -582,35 +582,11 @@ def _validate_k(index: SshIndex, k: int):
     return k, warning
 
 
-def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = False) -> list:
-    """query_index for every row of Q (nq, m) in one device batch."""
-    if _is_torch(Q):
-        Qd = Q.to(device=f"cuda:{index.device}", dtype=_torch().float32).contiguous()
-        if Qd.ndim == 1:
-            Qd = Qd.reshape(1, -1)
-    else:
-        # float32 input goes straight to the device (the f64 round trip is the identity)
-        Qh = Q if isinstance(Q, np.ndarray) and Q.dtype == np.float32 else np.asarray(Q, dtype=np.float64)
-        if Qh.ndim == 1:
-            Qh = Qh.reshape(1, -1)
-        if not np.isfinite(Qh).all():
-            raise ValueError("series values contains non-finite values")
-        Qd = _as_device_f32(Qh, index.device)
-    if Qd.shape[1] != index.length:
-        raise ValueError(f"query length {Qd.shape[1]} does not match indexed length {index.length}")
-    k, warning = _validate_k(index, k)
-    t0 = time.perf_counter()
-    dev = query_batch_device(index, Qd, k, fallback_on_empty)
-    # one synchronisation for the six result arrays (pinned, non-blocking copies)
-    torch = _torch()
-    host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev]
-    for h, t in zip(host, dev):
-        h.copy_(t, non_blocking=True)
-    torch.cuda.current_stream(index.device).synchronize()
-    ids, d2, n_out, n_cand, counters, status = (h.numpy() for h in host)
-    dt = time.perf_counter() - t0
-    nq = Qd.shape[0]
-    N = index.n_series
+def _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N: int, dt: float, warning) -> list:
+    """QueryResult per query from the host copies of ssh_query_batch's outputs
+    (ids/d2 (nq, k), n_out, n_cand, counters (nq, 5), status: 0 ok, 1 no-candidates,
+    2 fallback); distances = sqrt(d2) (index.py:268)."""
+    nq = int(status.shape[0])
     # whole-batch conversions to Python scalars (tolist is exact: int64 -> int,
     # float64 -> float); the per-query loop only slices lists
     ids_l = ids.tolist()
@@ -645,6 +621,36 @@ def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = Fals
                           status="fallback" if st == 2 else "ok", warning=warning)
         out.append(r)
     return out
+
+
+def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = False) -> list:
+    """query_index for every row of Q (nq, m) in one device batch."""
+    if _is_torch(Q):
+        Qd = Q.to(device=f"cuda:{index.device}", dtype=_torch().float32).contiguous()
+        if Qd.ndim == 1:
+            Qd = Qd.reshape(1, -1)
+    else:
+        # float32 input goes straight to the device (the f64 round trip is the identity)
+        Qh = Q if isinstance(Q, np.ndarray) and Q.dtype == np.float32 else np.asarray(Q, dtype=np.float64)
+        if Qh.ndim == 1:
+            Qh = Qh.reshape(1, -1)
+        if not np.isfinite(Qh).all():
+            raise ValueError("series values contains non-finite values")
+        Qd = _as_device_f32(Qh, index.device)
+    if Qd.shape[1] != index.length:
+        raise ValueError(f"query length {Qd.shape[1]} does not match indexed length {index.length}")
+    k, warning = _validate_k(index, k)
+    t0 = time.perf_counter()
+    dev = query_batch_device(index, Qd, k, fallback_on_empty)
+    # one synchronisation for the six result arrays (pinned, non-blocking copies)
+    torch = _torch()
+    host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev]
+    for h, t in zip(host, dev):
+        h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(index.device).synchronize()
+    ids, d2, n_out, n_cand, counters, status = (h.numpy() for h in host)
+    dt = time.perf_counter() - t0
+    return _results_from_arrays(ids, d2, n_out, n_cand, counters, status, index.n_series, dt, warning)
 
 
 def query_index(index: SshIndex, q, k: int, fallback_on_empty: bool = False) -> QueryResult:

@@ -159,3 +159,39 @@ def test_product_never_imports_oracle():
         src = p.read_text()
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\S+)", src, flags=re.M), p
         assert "import oracle" not in src and "from oracle" not in src, p
+
+
+def test_results_from_arrays_match_dataclass_construction():
+    """query_index_batch's fast result construction (field dicts, whole-batch
+    tolist) yields objects equal to the normally constructed dataclasses, with
+    the reference's statuses and sqrt distances (index.py:233-273)."""
+    import dataclasses
+
+    from paper_1610_07328_b200.index import QueryResult, QueryStats, SearchStats, _results_from_arrays
+
+    rng = np.random.default_rng(3)
+    nq, k, N = 5, 4, 1000
+    ids = rng.integers(0, N, size=(nq, k)).astype(np.int64)
+    d2 = rng.random((nq, k)) * 10.0
+    d2[2, 1:] = -1.0  # entries past n_out are garbage and must not be used
+    n_out = np.array([4, 4, 1, 0, 3], dtype=np.int32)
+    n_cand = np.array([9, 7, 1, 0, 1000], dtype=np.int64)
+    counters = rng.integers(0, 50, size=(nq, 5)).astype(np.int64)
+    status = np.array([0, 0, 0, 1, 2], dtype=np.int32)
+    got = _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N, 0.5, "w")
+    for i, r in enumerate(got):
+        t = {"batch": 0.5, "per_query": 0.5 / nq}
+        if status[i] == 1:
+            want = QueryResult([], [], QueryStats(N, 0, SearchStats(0, 0, 0, 0, 0, 0)), t,
+                               status="no-candidates", warning="w")
+        else:
+            c = [int(v) for v in counters[i]]
+            st = QueryStats(N, int(n_cand[i]), SearchStats(int(n_cand[i]), *c))
+            n = int(n_out[i])
+            want = QueryResult([int(v) for v in ids[i, :n]], [float(v) for v in np.sqrt(d2[i, :n])], st, t,
+                               status="fallback" if status[i] == 2 else "ok", warning="w")
+        assert r == want
+        assert type(r.ids[0] if r.ids else 0) is int and all(type(v) is float for v in r.distances)
+        with pytest.raises(dataclasses.FrozenInstanceError):
+            r.status = "x"
+        assert r.stats.cascade.pruned == want.stats.cascade.pruned
