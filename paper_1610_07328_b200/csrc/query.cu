@@ -178,14 +178,16 @@ bitmap_smem_kernel(const uint32_t *__restrict__ ids, const uint64_t *__restrict_
         const int j = threadIdx.x;
         const uint32_t len = blen[(int64_t)q * L + j];
         const uint32_t *b = ids + bstart[(int64_t)q * L + j];
+        // (a slice starting at row 0 / ending at N needs no search on that side:
+        // at configs[1] one slice covers the whole shard)
         uint32_t lo = 0, hi = len;
-        while (lo < hi) {
+        while (r0 > 0 && lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
             if (b[mid] < r0) lo = mid + 1; else hi = mid;
         }
         slo[j] = lo;
         hi = len;
-        uint32_t l2 = lo;
+        uint32_t l2 = (int64_t)r1 >= N ? len : lo;
         while (l2 < hi) {
             const uint32_t mid = (l2 + hi) >> 1;
             if (b[mid] < r1) l2 = mid + 1; else hi = mid;
