@@ -1,5 +1,6 @@
-"""Dev: time ssh_sketch at a config size; prints ms and a SHA-256 of the bits
-(A/B the pipelined FFMA2 kernel with SSH_SKETCH_PIPE=0)."""
+"""Dev: time ssh_sketch at a config size; prints ms, GB/s and a SHA-256 of the bits
+(A/B the TMA-staged stream kernel against the polyphase pair kernel with
+SSH_SKETCH_STREAM=0)."""
 import hashlib, os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -25,4 +26,4 @@ for _ in range(8):
     torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
 h = hashlib.sha256(bits.cpu().numpy().tobytes()).hexdigest()[:16]
 gbs = N * (4 * m + 8 * words) / (sorted(ts)[0] * 1e-3) / 1e9
-print(f"cfg{cfg} N={N} PIPE={os.environ.get('SSH_SKETCH_PIPE', '1')} sketch ms {sorted(ts)[:3]} {gbs:.0f} GB/s sha {h} rechecks {stats.tolist()}")
+print(f"cfg{cfg} N={N} STREAM={os.environ.get('SSH_SKETCH_STREAM', '1')} sketch ms {sorted(ts)[:3]} {gbs:.0f} GB/s sha {h} rechecks {stats.tolist()}")
