@@ -205,10 +205,38 @@ int ssh_query_batch(ssh_ctx *ctx, const ssh_index *idx, const float *X, const fl
                     int32_t *n_out, int64_t *n_cand, int64_t *counters, int32_t *status,
                     void *stream);
 
+/* Device time (ms) of the phases of the last ssh_query_batch on ctx,
+ * summed over its query chunks: [0] query signatures ("hash"), [1] probe +
+ * candidate bitmap ("probe"), [2] bounds + DTW rerank + top-k ("rerank") —
+ * the phases of query_index's timings dict (index.py:224-235,265).  Waits
+ * for the batch's last event. */
+int ssh_query_phase_ms(ssh_ctx *ctx, double *out3);
+
 /* Exact f64 banded DTW (dtw.py:83-121, FMA-free, no abandon) of npair
  * (query row, series row) pairs; rows index X / Q.  d2: f64[npair]. */
 int ssh_dtw_exact(ssh_ctx *ctx, const float *X, const float *Q, const int32_t *qrow,
                   const int64_t *xrow, int64_t npair, double *d2, void *stream);
+
+/* ---- the reference's public DTW utilities (dtw.py:239-284), float64 on the
+ * device in the reference's operation order.  All arrays are device f64,
+ * row-major [rows][m]; row index arrays may be NULL (= identity). */
+
+/* dtw_distance (dtw.py:239-250) / _dtw_band_sq (dtw.py:83-121): squared
+ * banded DTW of X[xrow[p]] vs Y[yrow[p]]; abandon_sq >= 0 enables the
+ * row-minimum abandon (+inf).  Band-chunked warp wavefront (any radius). */
+int ssh_dtw_pairs64(const double *X, const double *Y, const int64_t *xrow, const int64_t *yrow,
+                    int64_t npair, int32_t m, int32_t r, double abandon_sq, double *out_sq, void *stream);
+/* build_envelope (dtw.py:262-268) / _envelope_into (dtw.py:124-151): running
+ * max / min over [i - r, i + r] of each row. */
+int ssh_envelope64(const double *X, int64_t n, int32_t m, int32_t r, double *upper, double *lower,
+                   void *stream);
+/* lb_keogh (dtw.py:271-276) / _lb_keogh_sq (dtw.py:154-168): squared
+ * excursion of each row of C outside the envelope (one envelope shared by
+ * every row when env_rows == 1, else one per row). */
+int ssh_lb_keogh64(const double *C, const double *U, const double *Lo, int64_t n, int32_t m,
+                   int32_t env_rows, double *out_sq, void *stream);
+/* lb_kim (dtw.py:252-260): sqrt of the first and last squared differences. */
+int ssh_lb_kim64(const double *X, const double *Y, int64_t n, int32_t m, double *out, void *stream);
 
 #ifdef __cplusplus
 }

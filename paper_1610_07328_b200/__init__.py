@@ -18,12 +18,12 @@ from .core import (
     z_normalize_rows,
     z_normalize_values,
 )
-from .cws import make_filter
 from .index import (
     QueryResult,
     QueryStats,
     RandomFilter,
     SearchStats,
+    Float32RoundingWarning,
     SshIndex,
     SshParams,
     WarpingParams,
@@ -33,6 +33,7 @@ from .index import (
     exact_search,
     exact_search_batch,
     index_from_signatures,
+    make_filter,
     num_sketch_bits,
     probe_candidates,
     query_index,
@@ -40,6 +41,7 @@ from .index import (
     query_signature,
 )
 
+from .dtw import Envelope, build_envelope, dtw_distance, dtw_pairs, lb_keogh, lb_keogh2, lb_kim
 from .srp import ndcg_at_k, precision_at_k, srp_matrix, srp_signature, srp_vectors
 from .pipeline import extract_subsequences, make_dataset
 from .persist import file_checksum, load_dataset, load_index, read_index_file, save_dataset, save_index

@@ -20,7 +20,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB_PATH = Path(os.environ["SSH_LIB_PATH"]).resolve() if os.environ.get("SSH_LIB_PATH") else PKG / "libsshgpu.so"
-SOURCES = ["ctx.cu", "sketch.cu", "signature.cu", "tables.cu", "query.cu", "persist.cu", "windows.cu", "srp.cu"]
+SOURCES = ["ctx.cu", "sketch.cu", "signature.cu", "tables.cu", "query.cu", "persist.cu", "windows.cu", "srp.cu", "pairs.cu"]
 
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
@@ -54,7 +54,7 @@ def nvcc() -> str:
 def build_native(verbose: bool = False, force: bool = False) -> Path:
     """Compile csrc/*.cu for sm_100a into paper_1610_07328_b200/libsshgpu.so."""
     srcs = [CSRC / s for s in SOURCES]
-    deps = srcs + [CSRC / "common.cuh", INCLUDE / "sshgpu.h"]
+    deps = srcs + [CSRC / "common.cuh", CSRC / "dtw_warp.cuh", INCLUDE / "sshgpu.h"]
     if (not force and LIB_PATH.exists()
             and LIB_PATH.stat().st_mtime >= max(p.stat().st_mtime for p in deps)):
         return LIB_PATH
@@ -115,6 +115,11 @@ def lib():
                                          ctypes.c_int),
             "ssh_query_batch": ([P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P], ctypes.c_int),
             "ssh_dtw_exact": ([P, P, P, P, P, i64, P, P], ctypes.c_int),
+            "ssh_query_phase_ms": ([P, P], ctypes.c_int),
+            "ssh_dtw_pairs64": ([P, P, P, P, i64, i32, i32, ctypes.c_double, P, P], ctypes.c_int),
+            "ssh_envelope64": ([P, i64, i32, i32, P, P, P], ctypes.c_int),
+            "ssh_lb_keogh64": ([P, P, P, i64, i32, i32, P, P], ctypes.c_int),
+            "ssh_lb_kim64": ([P, P, i64, i32, P, P], ctypes.c_int),
             "ssh_index_create_bare": ([P, P, i64, i64, i64, PP, P], ctypes.c_int),
             "ssh_windows": ([P, i64, i32, i64, i32, P, P, ctypes.POINTER(i64), P], ctypes.c_int),
             "ssh_srp": ([P, i64, i32, P, P, i32, P, P, P], ctypes.c_int),
@@ -135,6 +140,7 @@ EXPORTED = [
     "ssh_num_sketch_bits", "ssh_sketch_words", "ssh_tokens_per_series", "ssh_sketch", "ssh_shingle",
     "ssh_cws", "ssh_signatures", "ssh_index_build", "ssh_build_index", "ssh_build_index_host", "ssh_index_destroy", "ssh_index_num_buckets",
     "ssh_index_size", "ssh_index_export", "ssh_index_summarize", "ssh_index_copy_summaries", "ssh_probe", "ssh_query_batch", "ssh_dtw_exact",
+    "ssh_query_phase_ms", "ssh_dtw_pairs64", "ssh_envelope64", "ssh_lb_keogh64", "ssh_lb_kim64",
     "ssh_index_create_bare", "ssh_sshi_parse_tables", "ssh_windows", "ssh_srp",
 ]
 

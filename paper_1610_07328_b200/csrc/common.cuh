@@ -76,6 +76,12 @@ struct ssh_ctx {
     cudaStream_t side = nullptr;
     cudaStream_t copy = nullptr;  // host->device series chunks (ssh_build_index_host)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_copy = nullptr;
+    // phase clock of the last ssh_query_batch (query_index timings "hash",
+    // "probe", "rerank", index.py:235,265): events at the phase boundaries of
+    // every query chunk, accumulated without extra host syncs
+    cudaEvent_t qev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double qphase[3] = {0, 0, 0};
+    bool qpending = false;  // the last chunk's rerank span is not folded in yet
     // named grow-only scratch slots reused across calls (stream-ordered)
     void *slot_ptr[32] = {nullptr};
     size_t slot_bytes[32] = {0};
@@ -139,7 +145,14 @@ struct ssh_index {
     int64_t *d_nb = nullptr;      // device copies
     int64_t *d_kbase = nullptr;
     int64_t total_buckets = 0;
+    // last stream-ordered use (build, summaries, probe, query): destroy makes
+    // its frees wait on it, so a caller working on any stream can drop the
+    // index while its last query is still in flight
+    cudaEvent_t last_use = nullptr;
 };
+
+// record ix's last use on `st` (see ssh_index::last_use)
+void ssh_index_touch(const ssh_index *ix, cudaStream_t st);
 
 // grow-only named scratch slot; returns pointer or nullptr (error set)
 void *ssh_slot(ssh_ctx *ctx, int slot, size_t bytes, cudaStream_t st);

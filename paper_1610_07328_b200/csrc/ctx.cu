@@ -137,6 +137,8 @@ extern "C" int ssh_ctx_destroy(ssh_ctx *ctx) {
     if (ctx->ev_copy) cudaEventDestroy(ctx->ev_copy);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    for (int i = 0; i < 4; i++)
+        if (ctx->qev[i]) cudaEventDestroy(ctx->qev[i]);
     delete ctx;
     return SSH_OK;
 }

@@ -37,6 +37,7 @@
 #include <cuda_fp16.h>
 
 #include "common.cuh"
+#include "dtw_warp.cuh"
 
 #define MB_THREADS 256
 #define MB_WARPS (MB_THREADS / 32)
@@ -661,7 +662,9 @@ extern "C" int ssh_index_summarize(ssh_ctx *ctx, ssh_index *ix, const float *X, 
     SSH_REQUIRE(ctx->have_params, SSH_ERR_STATE, "ssh_index_summarize: params not set");
     SSH_REQUIRE(ld >= ctx->p.m, SSH_ERR_INVALID, "ssh_index_summarize: ld < m");
     SSH_CUDA(cudaSetDevice(ctx->device));
-    return ssh_launch_summaries(ctx, ix, X, ix->N, ld, (cudaStream_t)stream);
+    int rc = ssh_launch_summaries(ctx, ix, X, ix->N, ld, (cudaStream_t)stream);
+    if (rc == SSH_OK) ssh_index_touch(ix, (cudaStream_t)stream);
+    return rc;
 }
 
 // --------------------------------------------------- LB_PAA of every member
@@ -1455,6 +1458,232 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
     }
 }
 
+// Wide-band wave DTW (fp32 screen): the band-chunked warp wavefront of
+// dtw_warp.cuh, one warp per candidate.  Lane l owns the C band offsets
+// k = lC + c in registers and sweeps row i = s - l at step s (cell update
+// in place, ascending k; left edge from lane l - 1 by shfl_up, up edge from
+// lane l + 1's first cell of the same step by shfl_down).  The query (padded
+// with +inf) is staged once per block; each lane's query samples are a
+// register window sliding one sample per step (the new one from lane l + 1),
+// its series samples x[s - l] are loaded per group of C steps (coalesced
+// across lanes).  Per cell: FADD + FMNMX3 + FFMA.
+//
+// Abandon (UCR-suite cumulative bound, dtw.py:206-215) on a skewed cut: after
+// step s the lanes hold the cells with i + floor(k / C) = s.  Along any
+// warping path f = i + floor(k / C) grows by 0 or 1 per move, from
+// floor(r / C) at (0, 0) to m - 1 + floor(r / C), so for s in that range every
+// path crosses the cut; the path's remaining rows are all > s - 31 ... s, so
+//   DTW >= min_cut D + sum_{i' > s} LB_Keogh term(i')
+// (lane 0 holds row s).  The test runs once per group of C steps with the same
+// fp32 slack as the row test: cut_min + max(remK - slack, 0) > thr.
+// remK = total - prefix(s) with the exact-x LB_Keogh terms (query envelope)
+// summed by a warp scan while the candidate is first read.
+#define DW_WARPS 8
+#define DW_XPAD 32
+// one step of the wide-band wavefront (see dtw32w_kernel); MASK: lanes whose
+// row is still negative keep their virtual row -1 (ramp-up steps only)
+template <int C, int U, bool MASK>
+__device__ __forceinline__ void dw_step(float (&band)[C], float (&yw)[C], const float xi, const int i,
+                                        const int lane, const int own, const int cst, const float y31) {
+    const float inf = INFINITY;
+    float leftv = __shfl_up_sync(0xFFFFFFFFu, band[C - 1], 1);
+    if (lane == 0) leftv = inf;
+    const bool act = !MASK || i >= 0;
+    {
+        const float d = xi - yw[U % C];
+        float v = fmaf(d, d, fminf(fminf(band[0], band[1]), leftv));
+        if (cst == 0 && lane == own) v = inf;
+        band[0] = act ? v : band[0];
+    }
+    float upr = __shfl_down_sync(0xFFFFFFFFu, band[0], 1);
+    if (lane == 31) upr = inf;
+#pragma unroll
+    for (int c = 1; c < C; c++) {
+        const float up = (c + 1 < C) ? band[c + 1] : upr;
+        const float d = xi - yw[(U + c) % C];
+        float v = fmaf(d, d, fminf(fminf(band[c], up), band[c - 1]));
+        if (cst == c && lane == own) v = inf;
+        band[c] = act ? v : band[c];
+    }
+    // slide the query window: logical 0 (phys U) expires, the new last sample
+    // comes from lane l + 1's logical 1 (lane 31: from the staged query)
+    float yn = __shfl_down_sync(0xFFFFFFFFu, yw[(U + 1) % C], 1);
+    if (lane == 31) yn = y31;
+    yw[U % C] = yn;
+}
+
+template <int C, int U, bool MASK>
+__device__ __forceinline__ void dw_group(float (&band)[C], float (&yw)[C], const float *xb, const float *yb,
+                                         const int s0, const int lane, const int own, const int cst,
+                                         const int rown, const int rcc, const int m, float &res) {
+    if constexpr (U < C) {
+        const int s = s0 + U;
+        dw_step<C, U, MASK>(band, yw, xb[U], s - lane, lane, own, cst, yb[U]);
+        if (s - lane == m - 1 && lane == rown) {
+#pragma unroll
+            for (int c = 0; c < C; c++)
+                if (c == rcc) res = band[c];
+        }
+        dw_group<C, U + 1, MASK>(band, yw, xb, yb, s0, lane, own, cst, rown, rcc, m, res);
+    }
+}
+
+// Wide-band wave DTW (fp32 screen): the band-chunked warp wavefront of
+// dtw_warp.cuh, one warp per candidate.  Lane l owns the C band offsets
+// k = lC + c in registers and sweeps row i = s - l at step s (cell update
+// in place, ascending k; left edge from lane l - 1 by shfl_up, up edge from
+// lane l + 1's first cell of the same step by shfl_down).  The query (padded
+// with +inf) is staged once per block and the candidate once per warp (zero
+// padded) in shared memory; each lane's query samples are a register window
+// sliding one sample per step (the new one from lane l + 1), its series
+// samples x[s - l] come from shared memory per group of C steps.  Per cell:
+// FADD + FMNMX3 + FFMA; ramp-up steps (rows < 0 on some lanes) keep the
+// virtual row -1 by selects, all later steps run unmasked (rows >= m only
+// produce values no in-range cell reads).
+//
+// Abandon (UCR-suite cumulative bound, dtw.py:206-215) on a skewed cut: after
+// step s the lanes hold the cells with i + floor(k / C) = s.  Along any
+// warping path f = i + floor(k / C) grows by 0 or 1 per move, from
+// floor(r / C) at (0, 0) to m - 1 + floor(r / C), so for s in that range every
+// path crosses the cut; the path's remaining rows are all > s - 31 ... s, so
+//   DTW >= min_cut D + sum_{i' > s} LB_Keogh term(i')
+// (lane 0 holds row s).  The test runs once per group of C steps with the same
+// fp32 slack as the row test: cut_min + max(remK - slack, 0) > thr.
+// remK = total - prefix(s) with the exact-x LB_Keogh terms (query envelope)
+// summed by a warp scan while the candidate is staged.
+template <int C, int RF>
+__global__ void __launch_bounds__(32 * DW_WARPS)
+dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restrict__ Q,
+              const float *__restrict__ U, const float *__restrict__ Lo, DtwList L,
+              const float *__restrict__ thr, unsigned long long *__restrict__ cells) {
+    const int r = RF >= 0 ? RF : r_rt;
+    const int nk = 2 * r + 1;
+    const int own = nk / C, cst = nk - own * C;  // cell k = nk (forced +inf): lane own, index cst
+    const int rown = r / C, rcc = r - rown * C;   // result cell k = r
+    const int G = (m + 31 + C - 1) / C;          // step groups
+    const int RU = (31 + C - 1) / C;             // ramp-up groups (some rows negative)
+    const int YP = r + m + 33 * C + 64;
+    const int XS = DW_XPAD + G * C + 32;
+    extern __shared__ __align__(16) float wsm[];
+    float *yq = wsm;          // yq[j + r] = y[j], +inf outside [0, m)
+    float *su = yq + YP;      // query envelope
+    float *sl = su + m;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float *pre = sl + m + (size_t)w * (G + 1 + XS);  // prefix of LB_Keogh terms at group ends
+    float *xs = pre + G + 1;                          // xs[DW_XPAD + i] = x[i], 0 outside
+    const int q = L.act ? L.act[blockIdx.y] : blockIdx.y;
+    const int slot = blockIdx.y;
+    int start, end;
+    dtw_list_range(L, slot, start, end);
+    if (start + (int)blockIdx.x * DW_WARPS >= end) return;  // block-uniform
+    const float *y = Q + (int64_t)q * m;
+    for (int t = threadIdx.x; t < YP; t += blockDim.x) {
+        const int j = t - r;
+        yq[t] = (j >= 0 && j < m) ? y[j] : INFINITY;
+    }
+    const float T = thr ? thr[q] : INFINITY;
+    const bool cb = !isinf(T) && U != nullptr;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        su[i] = cb ? U[(int64_t)q * m + i] : INFINITY;
+        sl[i] = cb ? Lo[(int64_t)q * m + i] : -INFINITY;
+    }
+    for (int t = lane; t < DW_XPAD; t += 32) xs[t] = 0.f;
+    for (int t = DW_XPAD + m + lane; t < XS; t += 32) xs[t] = 0.f;
+    __syncthreads();
+    const float inf = INFINITY;
+    const int f_lo = r / C, f_hi = m - 1 + r / C;  // cut steps every path crosses
+    unsigned long long my_cells = 0;
+    for (int e = start + (int)blockIdx.x * DW_WARPS + w; e < end; e += (int)gridDim.x * DW_WARPS) {
+        const uint32_t row = L.rows[(int64_t)slot * L.stride + e];
+        const bool valid = row != 0xFFFFFFFFu && (!L.lbs || !(L.lbs[(int64_t)slot * L.stride + e] > T));
+        if (!valid) {  // warp-uniform
+            if (lane == 0) L.out[(int64_t)slot * L.stride + e] = inf;
+            continue;
+        }
+        if (L.computed && lane == 0) atomicAdd(&L.computed[q], 1);
+        const float *x = X + (int64_t)row * m;
+        __syncwarp();
+        // stage x and the prefix sums of its LB_Keogh terms (exact x vs the
+        // query envelope) at the group-end steps s = (g + 1) C - 1
+        float carry = 0.f;
+        for (int i0 = 0; i0 < G * C; i0 += 32) {
+            const int i = i0 + lane;
+            float v2 = 0.f;
+            if (i < m) {
+                const float xv = __ldg(x + i);
+                xs[DW_XPAD + i] = xv;
+                const float v = fmaxf(fmaxf(xv - su[i], sl[i] - xv), 0.f);
+                v2 = v * v;
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float t = __shfl_up_sync(0xFFFFFFFFu, v2, o);
+                if (lane >= o) v2 += t;
+            }
+            const float P = carry + v2;
+            if ((i + 1) % C == 0) pre[(i + 1) / C - 1] = P;
+            carry = __shfl_sync(0xFFFFFFFFu, P, 31);
+        }
+        const float total = carry;
+        const float slack = total * (float)(2 * m + 8) * U32_EPS;
+        __syncwarp();
+        float band[C], yw[C];
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            band[c] = (lane * C + c == r) ? 0.f : inf;  // virtual row -1: D(0, 0) = d(0, 0)
+            yw[c] = yq[lane * (C - 1) + c];
+        }
+        float res = inf;
+        bool dead = false;
+        int g = 0;
+        for (; g < G; g++) {
+            const int s0 = g * C;
+            const float *xb = xs + DW_XPAD + s0 - lane;
+            const float *yb = yq + s0 + 32 * C - 31;
+            if (g < RU)
+                dw_group<C, 0, true>(band, yw, xb, yb, s0, lane, own, cst, rown, rcc, m, res);
+            else
+                dw_group<C, 0, false>(band, yw, xb, yb, s0, lane, own, cst, rown, rcc, m, res);
+            // cut test after step s = s0 + C - 1
+            const int s = s0 + C - 1;
+            if (cb && s >= f_lo && s <= f_hi) {
+                const int i = s - lane;
+                float cm = inf;
+                if (i >= 0 && i < m) {
+#pragma unroll
+                    for (int c = 0; c < C; c++)
+                        if (lane * C + c < nk) cm = fminf(cm, band[c]);
+                }
+                const unsigned cmb = __reduce_min_sync(0xFFFFFFFFu, __float_as_uint(cm));
+                const float remk = fmaxf(total - pre[g] - slack, 0.f);
+                if (__uint_as_float(cmb) + remk > T) {
+                    dead = true;
+                    break;
+                }
+            }
+        }
+        res = __shfl_sync(0xFFFFFFFFu, res, rown);
+        if (lane == 0) {
+            L.out[(int64_t)slot * L.stride + e] = dead ? inf : res;
+            if (dead && L.abandoned) atomicAdd(&L.abandoned[q], 1ULL);
+        }
+        if (cells) {
+            // in-band cells of the rows lane 31 completed
+            const long long rows = dead ? (long long)min(m, max(0, (g + 1) * C - 31)) : (long long)m;
+            long long c = rows * nk;
+            const long long a = min(rows, (long long)r);  // rows i < r lose r - i cells
+            c -= a * r - a * (a - 1) / 2;
+            const long long b0 = max(0LL, (long long)(m - r));  // rows i >= m - r lose i + r - m + 1
+            if (rows > b0) {
+                const long long nb = rows - b0;
+                c -= nb * (b0 + r - m + 1) + nb * (nb - 1) / 2;
+            }
+            my_cells += (unsigned long long)c;
+        }
+    }
+    if (cells && lane == 0 && my_cells) atomicAdd(cells, my_cells);
+}
+
 // Register-resident band (radius R compile-time): band[k], k = j - i + R, lives
 // in registers and is updated in place k-ascending (diag = old band[k], up =
 // old band[k+1], left = new band[k-1]).  The query is staged in 4 copies
@@ -2242,6 +2471,52 @@ dtw64w_kernel(const float *__restrict__ X, int m, int r, const float *__restrict
     }
 }
 
+// Exact f64 DTW for bands wider than the lane-per-row wavefront covers
+// (2 r + 1 > 64): the band-chunked warp wavefront of dtw_warp.cuh, one warp
+// per pair (list mode: blockIdx.y = query, list[q][e]; or explicit pairs).
+#define D64B_WARPS 4
+template <int C>
+__global__ void __launch_bounds__(32 * D64B_WARPS)
+dtw64band_kernel(const float *__restrict__ X, int m, int r, const float *__restrict__ Q,
+                 const int32_t *__restrict__ qrow, const uint32_t *__restrict__ list, int64_t list_stride,
+                 const int *__restrict__ list_cnt, const int64_t *__restrict__ xrow64, int64_t npair,
+                 double *__restrict__ out) {
+    const int w = threadIdx.x >> 5;
+    const int64_t e = (int64_t)blockIdx.x * D64B_WARPS + w;
+    int q;
+    int64_t row;
+    if (list) {
+        q = blockIdx.y;
+        if (e >= list_cnt[q]) return;  // warp-uniform
+        row = list[(int64_t)q * list_stride + e];
+    } else {
+        if (e >= npair) return;
+        q = qrow[e];
+        row = xrow64[e];
+    }
+    const double res = dtw_warp_band64<float, C>(X + row * m, Q + (int64_t)q * m, m, r, -1.0);
+    if ((threadIdx.x & 31) == 0) {
+        if (list) out[(int64_t)q * list_stride + e] = res;
+        else out[e] = res;
+    }
+}
+
+static int launch_dtw64band(const float *X, int m, int r, const float *Q, const int32_t *qrow,
+                            const uint32_t *list, int64_t stride, const int *cnt, const int64_t *xrow,
+                            int64_t n, int nq, double *out, cudaStream_t st, bool *done) {
+    *done = false;
+    const int C = dtw_warp_chunk(r);
+    if (C == 0) return SSH_OK;
+    dim3 grid((unsigned)ssh_div_up(n, D64B_WARPS), (unsigned)(list ? nq : 1));
+#define D64B_CALL(CC) \
+    dtw64band_kernel<CC><<<grid, 32 * D64B_WARPS, 0, st>>>(X, m, r, Q, qrow, list, stride, cnt, xrow, n, out)
+    DTW_WARP_DISPATCH(C, D64B_CALL)
+#undef D64B_CALL
+    SSH_CHECK_LAUNCH();
+    *done = true;
+    return SSH_OK;
+}
+
 // ------------------------------------------------------------ fp64 DTW
 // exact reference arithmetic (dtw.py:100-113): d = x - y; d = d*d; c = d + min(...)
 __global__ void dtw64_kernel(const float *__restrict__ X, int m, int r, const float *__restrict__ Q,
@@ -2714,11 +2989,56 @@ static int launch_dtw32_wave(ssh_ctx *ctx, const float *X, const float *Q, const
                              const DtwWave &W, const DtwList &Lg, const DtwCommon &C, const float *thr, int nq,
                              int wave, cudaStream_t st);
 
+// wide-band wave DTW (band-chunked warp wavefront); *done = false when r is
+// outside its range (C = ceil((2r+1)/32) in [3, 32])
+static int launch_dtw32w(ssh_ctx *ctx, const float *X, const float *Q, const float *U, const float *Lo,
+                         const DtwList &L, const float *thr, int nq, cudaStream_t st, bool *done) {
+    *done = false;
+    const int m = ctx->p.m, r = ctx->p.radius;
+    const int C = dtw_warp_chunk(r);
+    if (C < 3) return SSH_OK;
+    const int G = (m + 31 + C - 1) / C;
+    const int XS = DW_XPAD + G * C + 32;
+    const size_t smem = sizeof(float) * ((size_t)(r + m + 33 * C + 64) + 2 * (size_t)m + (size_t)DW_WARPS * (G + 1 + XS));
+    if (smem > 200 * 1024) return SSH_OK;
+    *done = true;
+    if (L.wave <= 0 || nq <= 0) return SSH_OK;
+    // about 4 candidates per warp; the grid covers the longest list
+    dim3 grid((unsigned)ssh_div_up(L.wave, DW_WARPS * 4), (unsigned)nq);
+    unsigned long long *cells = ctx->profile ? ctx->d_cells : nullptr;
+#define DW_LAUNCH(CC, RR)                                                                                   \
+    do {                                                                                                  \
+        SSH_CUDA(cudaFuncSetAttribute(dtw32w_kernel<CC, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      (int)smem));                                                        \
+        dtw32w_kernel<CC, RR><<<grid, 32 * DW_WARPS, smem, st>>>(X, m, r, Q, U, Lo, L, thr, cells);        \
+    } while (0)
+    if (r == 205) {
+        DW_LAUNCH(13, 205);
+    } else if (r == 51) {
+        DW_LAUNCH(4, 51);
+    } else {
+#define DW_CALL(CC) DW_LAUNCH(CC, -1)
+        DTW_WARP_DISPATCH(C, DW_CALL)
+#undef DW_CALL
+    }
+#undef DW_LAUNCH
+    SSH_CHECK_LAUNCH();
+    return SSH_OK;
+}
+
 // fp32 DTW of a candidate list (register band for the common radii, shared-memory band otherwise)
 static int launch_dtw32(ssh_ctx *ctx, const float *X, const float *Q, const float *U,
                         const float *Lo, const DtwList &L, const float *thr, int nq,
                         cudaStream_t st) {
     const int m = ctx->p.m, r = ctx->p.radius;
+    {
+        static const bool no_wide = getenv("SSH_DEBUG_DTW_NO_WAVEFRONT") != nullptr;
+        bool done = false;
+        if (!no_wide) {
+            int rc = launch_dtw32w(ctx, X, Q, U, Lo, L, thr, nq, st, &done);
+            if (rc || done) return rc;
+        }
+    }
 #define DTWR(RR) \
     case RR: return launch_dtw32r<RR>(ctx, X, Q, U, Lo, L, thr, nq, st);
     switch (r) {
@@ -2751,7 +3071,9 @@ static int launch_dtw32_wave(ssh_ctx *ctx, const float *X, const float *Q, const
 #define DTWP(RR) \
     case RR:     \
         return launch_dtw_pooled<RR>(ctx, C, W.act, W.rows, W.lbs, W.cnt, W.stride, W.rec, nq, wave, st);
-    if (!legacy && (m & 3) == 0 && C.qpad) switch (r) {
+    // SSH_DEBUG_DTW_WAVEFRONT: the warp wavefront also for the pooled radii (A/B)
+    static const bool wavefront = getenv("SSH_DEBUG_DTW_WAVEFRONT") != nullptr;
+    if (!legacy && !wavefront && (m & 3) == 0 && C.qpad) switch (r) {
         DTWP(3) DTWP(6) DTWP(13) DTWP(26) DTWP(51)
         default: break;
     }
@@ -2871,11 +3193,10 @@ static int launch_dtw64_list(const float *X, int m, int r, const float *Q, const
         SSH_CHECK_LAUNCH();
         return SSH_OK;
     }
-    if ((m & 3) == 0 && (size_t)(m + 2 * r + 8) * 8 <= 160 * 1024) {
-        switch (r) {
-            case 51: return launch_dtw64r<51>(X, m, Q, list, stride, cnt, maxcnt, out, nq, st);
-            default: break;
-        }
+    {
+        bool done = false;
+        int rc = launch_dtw64band(X, m, r, Q, nullptr, list, stride, cnt, nullptr, maxcnt, nq, out, st, &done);
+        if (rc || done) return rc;
     }
     size_t smem2;
     int t = dtw64_threads(r, &smem2);
@@ -2900,6 +3221,12 @@ extern "C" int ssh_dtw_exact(ssh_ctx *ctx, const float *X, const float *Q, const
             X, m, r, Q, qrow, nullptr, 0, nullptr, xrow, npair, d2);
         SSH_CHECK_LAUNCH();
         return SSH_OK;
+    }
+    {
+        bool done = false;
+        int rc = launch_dtw64band(X, m, r, Q, qrow, nullptr, 0, nullptr, xrow, npair, 1, d2,
+                                  (cudaStream_t)stream, &done);
+        if (rc || done) return rc;
     }
     size_t smem2;
     int t = dtw64_threads(r, &smem2);
@@ -2965,7 +3292,29 @@ extern "C" int ssh_probe(ssh_ctx *ctx, const ssh_index *ix, const uint64_t *qsig
     uint32_t *blen = A.get<uint32_t>((size_t)nq * ix->L);
     int *isfb = A.get<int>(nq);
     if (A.err) return ssh_cuda_fail(A.err, "ssh_probe scratch", __FILE__, __LINE__);
-    return probe_and_bitmap(ix, qsig, nq, 0, bstart, blen, bitmap, (long long *)n_cand, isfb, st);
+    int rc = probe_and_bitmap(ix, qsig, nq, 0, bstart, blen, bitmap, (long long *)n_cand, isfb, st);
+    if (rc == SSH_OK) ssh_index_touch(ix, st);
+    return rc;
+}
+
+// fold the last chunk's rerank span [qev[2], qev[3]] into ctx->qphase[2]
+static int fold_rerank(ssh_ctx *ctx) {
+    if (!ctx->qpending) return SSH_OK;
+    SSH_CUDA(cudaEventSynchronize(ctx->qev[3]));
+    float ms = 0.f;
+    SSH_CUDA(cudaEventElapsedTime(&ms, ctx->qev[2], ctx->qev[3]));
+    ctx->qphase[2] += ms;
+    ctx->qpending = false;
+    return SSH_OK;
+}
+
+extern "C" int ssh_query_phase_ms(ssh_ctx *ctx, double *out3) {
+    SSH_REQUIRE(ctx && out3, SSH_ERR_INVALID, "ssh_query_phase_ms: NULL argument");
+    SSH_CUDA(cudaSetDevice(ctx->device));
+    int rc = fold_rerank(ctx);
+    if (rc) return rc;
+    for (int i = 0; i < 3; i++) out3[i] = ctx->qphase[i];
+    return SSH_OK;
 }
 
 static int max_of(const int *d, int n, cudaStream_t st, int *out) {
@@ -2991,6 +3340,10 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                 "ssh_query_batch: NULL pointer");
     SSH_CUDA(cudaSetDevice(ctx->device));
     cudaStream_t st = (cudaStream_t)stream;
+    for (int i = 0; i < 4; i++)
+        if (!ctx->qev[i]) SSH_CUDA(cudaEventCreate(&ctx->qev[i]));
+    ctx->qpending = false;
+    ctx->qphase[0] = ctx->qphase[1] = ctx->qphase[2] = 0.0;
     ssh_index *mix = const_cast<ssh_index *>(ix);
     if (!mix->rec) {
         int rc = ssh_index_summarize(ctx, mix, X, ctx->p.m, stream);
@@ -3034,8 +3387,12 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         Prof pf(ctx, st);
         // K5: query signatures
         pf.begin();
-        int rc = qsig_batch(ctx, Qc, nc, B.qsig, B.qbits, st);
+        int rc = fold_rerank(ctx);  // previous chunk (its events are re-recorded below)
         if (rc) return rc;
+        SSH_CUDA(cudaEventRecord(ctx->qev[0], st));
+        rc = qsig_batch(ctx, Qc, nc, B.qsig, B.qbits, st);
+        if (rc) return rc;
+        SSH_CUDA(cudaEventRecord(ctx->qev[1], st));
         pf.end(0);
         // K6: probe + candidate bitmap; member counts -> CSR offsets
         pf.begin();
@@ -3049,9 +3406,17 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
         if (!qpad) return SSH_ERR_OOM;
         qpad_kernel<<<nc, 256, 0, st>>>(Qc, m, r, qYP, qpad);
         SSH_CHECK_LAUNCH();
+        SSH_CUDA(cudaEventRecord(ctx->qev[2], st));
         std::vector<long long> hc(nc);
         SSH_CUDA(cudaMemcpyAsync(hc.data(), ncand, sizeof(long long) * nc, cudaMemcpyDeviceToHost, st));
         SSH_CUDA(cudaStreamSynchronize(st));
+        {
+            float a = 0.f, b = 0.f;
+            SSH_CUDA(cudaEventElapsedTime(&a, ctx->qev[0], ctx->qev[1]));
+            SSH_CUDA(cudaEventElapsedTime(&b, ctx->qev[1], ctx->qev[2]));
+            ctx->qphase[0] += a;
+            ctx->qphase[1] += b;
+        }
         pf.end(1);
         // sub-ranges of the chunk whose actual member lists fit the budget
         // (SSH_DEBUG_MEMBER_BUDGET overrides it, for tests of the split path)
@@ -3261,6 +3626,9 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             }
             sa = sb;
         }
+        SSH_CUDA(cudaEventRecord(ctx->qev[3], st));
+        ctx->qpending = true;
     }
+    ssh_index_touch(ix, st);
     return SSH_OK;
 }

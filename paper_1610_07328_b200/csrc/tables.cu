@@ -779,6 +779,7 @@ extern "C" int ssh_index_build(ssh_ctx *ctx, const uint64_t *sig, int64_t N, int
         if (e != cudaSuccess) { rc = ssh_cuda_fail(e, "rle_emit", __FILE__, __LINE__); goto fail; }
     }
     }
+    ssh_index_touch(ix, st);
     *out = ix;
     return SSH_OK;
 fail:
@@ -787,12 +788,26 @@ fail:
     return rc;
 }
 
+void ssh_index_touch(const ssh_index *ix, cudaStream_t st) {
+    ssh_index *m = const_cast<ssh_index *>(ix);
+    if (!m->last_use && cudaEventCreateWithFlags(&m->last_use, cudaEventDisableTiming) != cudaSuccess) {
+        m->last_use = nullptr;
+        return;
+    }
+    cudaEventRecord(m->last_use, st);
+}
+
 extern "C" int ssh_index_destroy(ssh_index *ix) {
     if (!ix) return SSH_OK;
     cudaSetDevice(ix->device);
     // stream-ordered frees on the legacy stream: memory returns to the pool
-    // without a device-wide synchronisation
+    // without a device-wide synchronisation, after the index's last use on
+    // whatever stream the caller ran it (ssh_index_touch)
     cudaStream_t st = 0;
+    if (ix->last_use) {
+        cudaStreamWaitEvent(st, ix->last_use, 0);
+        cudaEventDestroy(ix->last_use);
+    }
     if (ix->keys) cudaFreeAsync(ix->keys, st);
     if (ix->offsets) cudaFreeAsync(ix->offsets, st);
     if (ix->ids) cudaFreeAsync(ix->ids, st);
@@ -884,6 +899,7 @@ extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t 
     (*out)->nseg = summ.nseg;
     (*out)->mp = summ.mp;
     (*out)->cstride = summ.cstride;
+    ssh_index_touch(*out, st);
     return SSH_OK;
 }
 
@@ -938,6 +954,7 @@ extern "C" int ssh_build_index_host(ssh_ctx *ctx, const float *X_host, int64_t N
     (*out)->nseg = summ.nseg;
     (*out)->mp = summ.mp;
     (*out)->cstride = summ.cstride;
+    ssh_index_touch(*out, st);
     return SSH_OK;
 }
 
@@ -960,6 +977,7 @@ extern "C" int ssh_index_create_bare(ssh_ctx *ctx, const float *X, int64_t N, in
         ssh_index_destroy(ix);
         return rc;
     }
+    ssh_index_touch(ix, (cudaStream_t)stream);
     *out = ix;
     return SSH_OK;
 }

@@ -45,8 +45,9 @@ def _open_unit(h: np.ndarray) -> np.ndarray:
     return ((h >> _U(11)).astype(np.float64) + 0.5) * 2.0 ** -53
 
 
-def make_filter(W: int, seed: int) -> np.ndarray:
-    """W standard-normal taps from default_rng(seed) (sketch.py:36-43)."""
+def filter_weights(W: int, seed: int) -> np.ndarray:
+    """W standard-normal taps from default_rng(seed) (sketch.py:36-43); the
+    public make_filter (index.py) wraps them in a RandomFilter."""
     if W < 1:
         raise ValueError(f"filter length W must be >= 1, got {W}")
     if seed < 0:

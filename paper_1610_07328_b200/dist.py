@@ -8,6 +8,12 @@ answer is the (d2, id) merge of the per-rank lists, which equals the exact
 top-k of R = U_g R_g.  The exchange is one all_gather of the per-rank top-k
 (d2 f64, id i64) and one all_reduce(sum) of |R_g| and the cascade counters,
 all batched over the whole query batch.
+
+Statuses follow the reference over the union R (index.py:233-243): a query
+is "no-candidates" only when every R_g is empty (|R| = sum of |R_g| is
+all-reduced first), and with fallback_on_empty such queries run the exact
+search over every shard (SSH_QUERY_EXACT) and merge the same way
+(`sharded_query`), so the global answer equals the single-index one.
 """
 
 from __future__ import annotations
@@ -103,3 +109,47 @@ def merge_numpy(parts, k: int):
         out_i[q, :order.shape[0]] = ids[q][sel][order]
         out_d[q, :order.shape[0]] = d2[q][sel][order]
     return out_i, out_d
+
+
+def sharded_query(Q, k: int, local, exact=None, fallback_on_empty: bool = False, group=None):
+    """query_index_batch over a series-sharded index (index.py:204-273).
+
+    local(Q, k) -> (ids, d2, n_out, n_cand, counters, status) of this rank's
+    shard, run WITHOUT the empty-R fallback; exact(Qsub, k) -> the same tuple
+    for an exact search of Qsub over the rank's shard (dtw.py:293-326).
+    Returns the merged tuple (identical on every rank): ids/d2 the exact
+    (d2, id) top-k of R = U_g R_g, n_cand = |R|, counters summed, status 0 ok,
+    1 no-candidates (every R_g empty), 2 fallback (exact over all shards)."""
+    torch = _torch()
+    ids, d2, _, n_cand, counters, _ = local(Q, k)
+    mids, md2, nc, cnt = merge_across_ranks(ids, d2, n_cand, counters, k, group=group)
+    empty = nc == 0
+    status = torch.zeros(nc.shape, dtype=torch.int32, device=nc.device)
+    if bool(empty.any()):  # same decision on every rank (nc is all-reduced)
+        if fallback_on_empty and exact is not None:
+            sub = torch.nonzero(empty).flatten()
+            eids, ed2, _, enc, ecnt, _ = exact(Q[sub.to(Q.device)].contiguous(), k)
+            fi, fd, fnc, fc = merge_across_ranks(eids, ed2, enc, ecnt, k, group=group)
+            sub = sub.to(mids.device)
+            mids[sub] = fi.to(mids.device)
+            md2[sub] = fd.to(md2.device)
+            nc[sub] = fnc.to(nc.device)
+            cnt[sub] = fc.to(cnt.device)
+            status[sub] = 2
+        else:
+            status[empty] = 1
+    n_out = (mids >= 0).sum(dim=1).to(torch.int32)
+    return mids, md2, n_out, nc, cnt, status
+
+
+def index_query_fns(index):
+    """(local, exact) callables of sharded_query for a device SshIndex shard."""
+    from .index import query_batch_device
+
+    def local(Q, k):
+        return query_batch_device(index, Q, k, False)
+
+    def exact(Q, k):
+        return query_batch_device(index, Q, k, False, exact=True)
+
+    return local, exact

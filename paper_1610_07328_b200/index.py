@@ -15,10 +15,12 @@ PyTorch is used only for device memory and the current CUDA stream.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
 import threading
 import time
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -81,6 +83,12 @@ class RandomFilter:
     @property
     def W(self) -> int:
         return self.weights.shape[0]
+
+
+def make_filter(W: int, seed: int) -> RandomFilter:
+    """Deterministic filter: W standard normal draws from the given seed
+    (sketch.py:36-43; same ValueError messages)."""
+    return RandomFilter(weights=cws.filter_weights(W, seed), seed=seed)
 
 
 @dataclass(frozen=True)
@@ -181,17 +189,27 @@ def _device_index(device) -> int:
 
 
 class DeviceContext:
-    """One ssh_ctx per (device, parameters, series length)."""
+    """One ssh_ctx per (device, parameters, series length).
+
+    The ssh_ctx owns grow-only scratch slots that every build / query call
+    reuses, so calls on one context must not overlap.  The
+    reference's query_index is pure and callable from many threads at once
+    (bench.py:129-133); `use()` makes the device path equally
+    safe: it serialises the native calls on the context and orders each
+    call's stream after the previous call's device work (an event), so two
+    threads on different CUDA streams never share scratch in flight."""
 
     def __init__(self, device: int, params: SshParams, m: int):
         self.device = device
         self.params = params
         self.m = m
+        self.lock = threading.RLock()
+        self._last = None
         L = nat.lib()
         h = ctypes.c_void_p()
         nat.check(L.ssh_ctx_create(device, ctypes.byref(h)), "ssh_ctx_create")
         self.handle = h
-        w = cws.make_filter(params.W, params.seed)
+        w = cws.filter_weights(params.W, params.seed)
         self.filter = RandomFilter(weights=w, seed=params.seed)
         S = params.K * params.d
         r, lnc, beta = cws.tables(params.n, S, params.seed)
@@ -207,6 +225,21 @@ class DeviceContext:
         self.nb = L.ssh_num_sketch_bits(h)
         self.words = L.ssh_sketch_words(h)
         self.T = L.ssh_tokens_per_series(h)
+
+    @contextlib.contextmanager
+    def use(self):
+        """Exclusive, stream-ordered use of the context (see the class doc)."""
+        with self.lock:
+            torch = _torch()
+            st = torch.cuda.current_stream(self.device)
+            if self._last is not None:
+                st.wait_event(self._last)
+            try:
+                yield st
+            finally:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                self._last = ev
 
     def __del__(self):
         try:
@@ -235,6 +268,32 @@ def get_context(device: int, params: SshParams, m: int) -> DeviceContext:
 def _stream_ptr(device: int):
     torch = _torch()
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class Float32RoundingWarning(UserWarning):
+    """float64 input that float32 cannot represent exactly was rounded."""
+
+
+def _warn_f32_rounding(values, what: str) -> None:
+    """The device path computes on float32 series (BASELINE.json's workloads
+    are float32; the oracle upcasts them exactly).  A float64 input whose
+    values are not all float32-representable is rounded once, so sketch
+    signs, signatures and distances can differ from the reference's float64
+    evaluation of the unrounded values: say so (never silently)."""
+    if _is_torch(values):
+        torch = _torch()
+        if values.dtype != torch.float64:
+            return
+        changed = bool((values.float().double() != values).any())
+    else:
+        v = np.asarray(values)
+        if v.dtype != np.float64:
+            return
+        changed = bool(np.any(v.astype(np.float32).astype(np.float64) != v))
+    if changed:
+        warnings.warn(f"{what} values are float64 and not exactly representable in float32; the device "
+                      "path rounds them to float32 once (results are the reference's for the rounded "
+                      "values)", Float32RoundingWarning, stacklevel=3)
 
 
 def _host_f32(values):
@@ -358,8 +417,9 @@ def compute_signatures_device(ctx: DeviceContext, X, stats=None):
     N = int(X.shape[0])
     sig = torch.empty((N, ctx.params.d), dtype=torch.int64, device=X.device)
     if N:
-        nat.check(nat.lib().ssh_signatures(ctx.handle, nat.ptr(X), N, int(X.stride(0)), nat.ptr(sig),
-                                           nat.ptr(stats), _stream_ptr(ctx.device)), "ssh_signatures")
+        with ctx.use():
+            nat.check(nat.lib().ssh_signatures(ctx.handle, nat.ptr(X), N, int(X.stride(0)), nat.ptr(sig),
+                                               nat.ptr(stats), _stream_ptr(ctx.device)), "ssh_signatures")
     return sig
 
 
@@ -373,6 +433,7 @@ def build_index(dataset, params: SshParams, normalized: bool = True, threads: in
     dev = _device_index(device)
     ctx = get_context(dev, params, dataset.length)
     torch = _torch()
+    _warn_f32_rounding(dataset.values, "dataset")
     host = _host_f32(dataset.values)
     handle = ctypes.c_void_p()
     if host is not None:
@@ -380,15 +441,17 @@ def build_index(dataset, params: SshParams, normalized: bool = True, threads: in
         N, m = host.shape
         X = torch.empty((N, m), dtype=torch.float32, device=f"cuda:{dev}")
         sig = torch.empty((N, params.d), dtype=torch.int64, device=X.device)
-        nat.check(nat.lib().ssh_build_index_host(ctx.handle, host.data_ptr(), N, m, int(id_base), nat.ptr(X),
-                                                 nat.ptr(sig), ctypes.byref(handle), _stream_ptr(dev)),
-                  "ssh_build_index_host")
+        with ctx.use():
+            nat.check(nat.lib().ssh_build_index_host(ctx.handle, host.data_ptr(), N, m, int(id_base), nat.ptr(X),
+                                                     nat.ptr(sig), ctypes.byref(handle), _stream_ptr(dev)),
+                      "ssh_build_index_host")
     else:
         X = _as_device_f32(dataset.values, dev)
         sig = torch.empty((int(X.shape[0]), params.d), dtype=torch.int64, device=X.device)
-        nat.check(nat.lib().ssh_build_index(ctx.handle, nat.ptr(X), int(X.shape[0]), int(X.stride(0)),
-                                            int(id_base), nat.ptr(sig), ctypes.byref(handle),
-                                            _stream_ptr(dev)), "ssh_build_index")
+        with ctx.use():
+            nat.check(nat.lib().ssh_build_index(ctx.handle, nat.ptr(X), int(X.shape[0]), int(X.stride(0)),
+                                                int(id_base), nat.ptr(sig), ctypes.byref(handle),
+                                                _stream_ptr(dev)), "ssh_build_index")
     tables = _TablesHandle(handle)
     return SshIndex(params=params, filter=ctx.filter, dataset=dataset, normalized=normalized,
                     device=dev, X=X, sig_dev=sig, id_base=id_base, _tables=tables)
@@ -410,6 +473,7 @@ def index_from_signatures(dataset, params: SshParams, sig, normalized: bool = Tr
     if filter_seed is not None and int(filter_seed) != ctx.filter.seed:
         raise ConfigError(f"index filter seed {filter_seed} differs from params.seed {ctx.filter.seed}")
     torch = _torch()
+    _warn_f32_rounding(dataset.values, "dataset")
     X = _as_device_f32(dataset.values, dev)
     sig_h = np.ascontiguousarray(np.asarray(sig, dtype=np.uint64))
     if sig_h.shape != (X.shape[0], params.d):
@@ -417,11 +481,12 @@ def index_from_signatures(dataset, params: SshParams, sig, normalized: bool = Tr
     sig_d = torch.from_numpy(sig_h.view(np.int64)).to(X.device)
     handle = ctypes.c_void_p()
     L = nat.lib()
-    nat.check(L.ssh_index_build(ctx.handle, nat.ptr(sig_d), int(X.shape[0]), int(id_base),
-                                ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_build")
-    tables = _TablesHandle(handle)
-    nat.check(L.ssh_index_summarize(ctx.handle, handle, nat.ptr(X), int(X.stride(0)), _stream_ptr(dev)),
-              "ssh_index_summarize")
+    with ctx.use():
+        nat.check(L.ssh_index_build(ctx.handle, nat.ptr(sig_d), int(X.shape[0]), int(id_base),
+                                    ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_build")
+        tables = _TablesHandle(handle)
+        nat.check(L.ssh_index_summarize(ctx.handle, handle, nat.ptr(X), int(X.stride(0)), _stream_ptr(dev)),
+                  "ssh_index_summarize")
     return SshIndex(params=params, filter=ctx.filter, dataset=dataset, normalized=normalized,
                     device=dev, X=X, sig_dev=sig_d, id_base=id_base, _tables=tables)
 
@@ -449,6 +514,8 @@ def exact_search_batch(dataset, Q, k: int, params: WarpingParams = WarpingParams
         raise ValueError(f"query length {Qh.shape[1]} does not match dataset length {dataset.length}")
     if k < 1:
         raise ValueError(f"k must be >= 1, got {k}")
+    _warn_f32_rounding(dataset.values, "dataset")
+    _warn_f32_rounding(Qh, "query")
     warning = None
     if k > dataset.n_series:
         warning = f"k={k} exceeds dataset size {dataset.n_series}; returning all series"
@@ -460,8 +527,9 @@ def exact_search_batch(dataset, Q, k: int, params: WarpingParams = WarpingParams
     X = _as_device_f32(dataset.values, dev)
     handle = ctypes.c_void_p()
     L = nat.lib()
-    nat.check(L.ssh_index_create_bare(ctx.handle, nat.ptr(X), int(X.shape[0]), int(X.stride(0)), 0,
-                                      ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_create_bare")
+    with ctx.use():
+        nat.check(L.ssh_index_create_bare(ctx.handle, nat.ptr(X), int(X.shape[0]), int(X.stride(0)), 0,
+                                          ctypes.byref(handle), _stream_ptr(dev)), "ssh_index_create_bare")
     bare = _TablesHandle(handle)
     Qd = _as_device_f32(Qh, dev)
     nq = int(Qd.shape[0])
@@ -471,9 +539,10 @@ def exact_search_batch(dataset, Q, k: int, params: WarpingParams = WarpingParams
     n_cand = torch.empty(nq, dtype=torch.int64, device=X.device)
     counters = torch.empty((nq, 5), dtype=torch.int64, device=X.device)
     status = torch.empty(nq, dtype=torch.int32, device=X.device)
-    nat.check(L.ssh_query_batch(ctx.handle, bare.handle, nat.ptr(X), nat.ptr(Qd), nq, k, nat.SSH_QUERY_EXACT,
-                                nat.ptr(ids), nat.ptr(d2), nat.ptr(n_out), nat.ptr(n_cand), nat.ptr(counters),
-                                nat.ptr(status), _stream_ptr(dev)), "ssh_query_batch")
+    with ctx.use():
+        nat.check(L.ssh_query_batch(ctx.handle, bare.handle, nat.ptr(X), nat.ptr(Qd), nq, k, nat.SSH_QUERY_EXACT,
+                                    nat.ptr(ids), nat.ptr(d2), nat.ptr(n_out), nat.ptr(n_cand),
+                                    nat.ptr(counters), nat.ptr(status), _stream_ptr(dev)), "ssh_query_batch")
     ids, d2, n_out, counters = ids.cpu().numpy(), d2.cpu().numpy(), n_out.cpu().numpy(), counters.cpu().numpy()
     del bare
     out = []
@@ -533,8 +602,10 @@ def probe_candidates(index: SshIndex, qsig) -> np.ndarray:
     NW = (N + 31) // 32
     bm = torch.empty((1, NW), dtype=torch.int32, device=qs.device)
     nc = torch.empty(1, dtype=torch.int64, device=qs.device)
-    nat.check(nat.lib().ssh_probe(index.context().handle, index._tables.handle, nat.ptr(qs), 1,
-                                  nat.ptr(bm), nat.ptr(nc), _stream_ptr(index.device)), "ssh_probe")
+    ctx = index.context()
+    with ctx.use():
+        nat.check(nat.lib().ssh_probe(ctx.handle, index._tables.handle, nat.ptr(qs), 1,
+                                      nat.ptr(bm), nat.ptr(nc), _stream_ptr(index.device)), "ssh_probe")
     words = bm.cpu().numpy().view(np.uint32)[0]
     bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:N]
     return np.nonzero(bits)[0].astype(np.int64) + index.id_base
@@ -552,7 +623,8 @@ class BatchResult:
     seconds: float
 
 
-def query_batch_device(index: SshIndex, Q, k: int, fallback_on_empty: bool = False):
+def query_batch_device(index: SshIndex, Q, k: int, fallback_on_empty: bool = False, phase_ms: list | None = None,
+                       exact: bool = False):
     """Run ssh_query_batch on a device tensor Q (nq, m) f32; returns device tensors."""
     torch = _torch()
     nq = int(Q.shape[0])
@@ -563,11 +635,17 @@ def query_batch_device(index: SshIndex, Q, k: int, fallback_on_empty: bool = Fal
     n_cand = torch.empty(nq, dtype=torch.int64, device=dev)
     counters = torch.empty((nq, 5), dtype=torch.int64, device=dev)
     status = torch.empty(nq, dtype=torch.int32, device=dev)
-    flags = nat.SSH_QUERY_FALLBACK_ON_EMPTY if fallback_on_empty else 0
-    nat.check(nat.lib().ssh_query_batch(
-        index.context().handle, index._tables.handle, nat.ptr(index.X), nat.ptr(Q), nq, k, flags,
-        nat.ptr(ids), nat.ptr(d2), nat.ptr(n_out), nat.ptr(n_cand), nat.ptr(counters),
-        nat.ptr(status), _stream_ptr(index.device)), "ssh_query_batch")
+    flags = (nat.SSH_QUERY_FALLBACK_ON_EMPTY if fallback_on_empty else 0) | (nat.SSH_QUERY_EXACT if exact else 0)
+    ctx = index.context()
+    with ctx.use():
+        nat.check(nat.lib().ssh_query_batch(
+            ctx.handle, index._tables.handle, nat.ptr(index.X), nat.ptr(Q), nq, k, flags,
+            nat.ptr(ids), nat.ptr(d2), nat.ptr(n_out), nat.ptr(n_cand), nat.ptr(counters),
+            nat.ptr(status), _stream_ptr(index.device)), "ssh_query_batch")
+        if phase_ms is not None:
+            ph = (ctypes.c_double * 3)()
+            nat.check(nat.lib().ssh_query_phase_ms(ctx.handle, ph), "ssh_query_phase_ms")
+            phase_ms[:] = list(ph)
     return ids, d2, n_out, n_cand, counters, status
 
 
@@ -582,10 +660,16 @@ def _validate_k(index: SshIndex, k: int):
     return k, warning
 
 
-def _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N: int, dt: float, warning) -> list:
+def _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N: int, dt: float, warning,
+                         phase_ms=None) -> list:
     """QueryResult per query from the host copies of ssh_query_batch's outputs
     (ids/d2 (nq, k), n_out, n_cand, counters (nq, 5), status: 0 ok, 1 no-candidates,
-    2 fallback); distances = sqrt(d2) (index.py:268)."""
+    2 fallback); distances = sqrt(d2) (index.py:268).
+
+    timings carries the reference's keys "hash", "probe" and "rerank"
+    (index.py:235,265; read by cli.py:184-185), in seconds: each query's share
+    of the batch's device time in that phase (phase_ms, ssh_query_phase_ms),
+    plus "batch" (host wall time of the whole batch) and "per_query"."""
     nq = int(status.shape[0])
     # whole-batch conversions to Python scalars (tolist is exact: int64 -> int,
     # float64 -> float); the per-query loop only slices lists
@@ -597,12 +681,14 @@ def _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N: int, dt: f
     cnt_l = counters.tolist()
     status_l = status.tolist()
     per_q = dt / max(1, nq)
+    ph = [0.0, 0.0, 0.0] if phase_ms is None else [v / 1e3 / max(1, nq) for v in phase_ms]
+    tmpl = {"hash": ph[0], "probe": ph[1], "rerank": ph[2], "batch": dt, "per_query": per_q}
     out = []
     # the frozen dataclasses' __init__ (object.__setattr__ per field) dominates
     # the host time of a 1000-query batch; instances get their field dict directly
     new = object.__new__
     for i in range(nq):
-        timings = {"batch": dt, "per_query": per_q}
+        timings = dict(tmpl)
         st = status_l[i]
         if st == 1:
             stats = QueryStats(n_indexed=N, candidates=0, cascade=SearchStats(0, 0, 0, 0, 0, 0))
@@ -636,21 +722,26 @@ def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = Fals
             Qh = Qh.reshape(1, -1)
         if not np.isfinite(Qh).all():
             raise ValueError("series values contains non-finite values")
+        _warn_f32_rounding(Qh, "query")
         Qd = _as_device_f32(Qh, index.device)
     if Qd.shape[1] != index.length:
         raise ValueError(f"query length {Qd.shape[1]} does not match indexed length {index.length}")
     k, warning = _validate_k(index, k)
     t0 = time.perf_counter()
-    dev = query_batch_device(index, Qd, k, fallback_on_empty)
-    # one synchronisation for the six result arrays (pinned, non-blocking copies)
     torch = _torch()
-    host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev]
-    for h, t in zip(host, dev):
-        h.copy_(t, non_blocking=True)
-    torch.cuda.current_stream(index.device).synchronize()
+    phase = [0.0, 0.0, 0.0]
+    # the whole batch (launches, result copies, phase clock) holds the context
+    with index.context().use():
+        dev = query_batch_device(index, Qd, k, fallback_on_empty, phase_ms=phase)
+        # one synchronisation for the six result arrays (pinned, non-blocking copies)
+        host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev]
+        for h, t in zip(host, dev):
+            h.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(index.device).synchronize()
     ids, d2, n_out, n_cand, counters, status = (h.numpy() for h in host)
     dt = time.perf_counter() - t0
-    return _results_from_arrays(ids, d2, n_out, n_cand, counters, status, index.n_series, dt, warning)
+    return _results_from_arrays(ids, d2, n_out, n_cand, counters, status, index.n_series, dt, warning,
+                                phase_ms=phase)
 
 
 def query_index(index: SshIndex, q, k: int, fallback_on_empty: bool = False) -> QueryResult:
@@ -670,7 +761,9 @@ def dtw_exact_pairs(index: SshIndex, Q, qrow, xrow) -> np.ndarray:
     qr = torch.as_tensor(np.asarray(qrow, dtype=np.int32)).to(Qd.device)
     xr = torch.as_tensor(np.asarray(xrow, dtype=np.int64)).to(Qd.device)
     out = torch.empty(qr.shape[0], dtype=torch.float64, device=Qd.device)
-    nat.check(nat.lib().ssh_dtw_exact(index.context().handle, nat.ptr(index.X), nat.ptr(Qd),
-                                      nat.ptr(qr), nat.ptr(xr), int(qr.shape[0]), nat.ptr(out),
-                                      _stream_ptr(index.device)), "ssh_dtw_exact")
+    ctx = index.context()
+    with ctx.use():
+        nat.check(nat.lib().ssh_dtw_exact(ctx.handle, nat.ptr(index.X), nat.ptr(Qd),
+                                          nat.ptr(qr), nat.ptr(xr), int(qr.shape[0]), nat.ptr(out),
+                                          _stream_ptr(index.device)), "ssh_dtw_exact")
     return out.cpu().numpy()

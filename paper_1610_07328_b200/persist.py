@@ -171,7 +171,12 @@ def save_index(index, path) -> None:
     dataset_name = path.name + ".sshd"
     save_dataset(index.dataset, path.parent / dataset_name, fmt="f64le")
     checksum = file_checksum(path.parent / dataset_name)
-    tables = (index.table_csr(j) for j in range(index.params.d))
+    # the file describes its own dataset (row r = id r): a shard built with
+    # id_base != 0 (dist.py) is written with local ids; load_index(id_base=...)
+    # restores the global numbering
+    base = int(getattr(index, "id_base", 0))
+    tables = ((keys, offsets, ids - base) for keys, offsets, ids in
+              (index.table_csr(j) for j in range(index.params.d)))
     path.write_bytes(index_file_bytes(index.params, index.normalized, index.filter.seed, index.filter.weights,
                                       dataset_name, checksum, tables))
 
@@ -237,11 +242,12 @@ def read_index_file(path):
     return params, weights, filter_seed, bool(normalized), dataset, sig
 
 
-def load_index(path, device=None):
+def load_index(path, device=None, id_base: int = 0):
     """index.py:333-396: parse + verify, then rebuild the device index from the
-    recovered signatures (tables are a function of the signatures)."""
+    recovered signatures (tables are a function of the signatures).  id_base
+    re-attaches a shard's global id offset (save_index writes local ids)."""
     from .index import index_from_signatures
 
     params, weights, filter_seed, normalized, dataset, sig = read_index_file(path)
     return index_from_signatures(dataset, params, sig, normalized=normalized, device=device,
-                                 filter_weights=weights, filter_seed=filter_seed)
+                                 filter_weights=weights, filter_seed=filter_seed, id_base=id_base)

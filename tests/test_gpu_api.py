@@ -1,0 +1,199 @@
+"""Device parity of the reference-facing surface beyond the index hot path:
+the public DTW utilities (dtw.py:239-284), the wide-band warp-wavefront DTW
+(any radius), concurrent queries on one index, the reference's timing keys,
+sharded indexes (id_base) merged across shards, and shard persistence."""
+
+import concurrent.futures as cf
+
+import numpy as np
+import pytest
+
+from fixture_data import case_data
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _params(band=0.05, K=4, **kw):
+    import paper_1610_07328_b200 as ssh
+
+    d = dict(W=80, delta=3, n=15, d=20, seed=0, band=band, K=K)
+    d.update(kw)
+    return ssh.SshParams(**d)
+
+
+def test_dtw_utilities_golden(cuda, golden):
+    """dtw_distance / build_envelope / lb_keogh / lb_keogh2 / lb_kim on the
+    reference-generated float64 pairs: bit-identical to sshts.dtw."""
+    import paper_1610_07328_b200 as ssh
+
+    for p in golden["dtw"]["pairs"]:
+        x, y = np.array(p["x"]), np.array(p["y"])
+        wp = ssh.WarpingParams(band=p["band"])
+        assert ssh.dtw_distance(x, y, wp) == float(np.sqrt(p["d2"]))
+        env = ssh.build_envelope(y, wp)
+        assert env.upper.tolist() == p["upper"] and env.lower.tolist() == p["lower"]
+        assert ssh.lb_keogh(env, x) == float(np.sqrt(p["lb_keogh_sq"]))
+        assert ssh.lb_keogh2(x, y, wp) == float(np.sqrt(p["lb_keogh_sq"]))
+        d0, dm = x[0] - y[0], x[-1] - y[-1]
+        assert ssh.lb_kim(x, y) == float(np.sqrt(d0 * d0 + dm * dm))
+    one = ssh.dtw_distance(np.array([1.0, 2, 3]), np.array([2.0, 3, 4]), ssh.WarpingParams(band=1.0))
+    assert one == golden["dtw"]["spec_sqrt2"]
+    with pytest.raises(ValueError, match="length mismatch"):
+        ssh.dtw_distance(np.zeros(3), np.zeros(4))
+
+
+@pytest.mark.parametrize("m,r", [(700, 0), (700, 5), (700, 31), (700, 32), (700, 100), (2048, 205), (900, 600)])
+def test_dtw_pairs_any_radius(cuda, m, r):
+    """The band-chunked warp wavefront (C = ceil((2r+1)/32) cells per lane,
+    2 <= C <= 32) and the row kernel beyond it: bit-identical to the oracle's
+    reference recurrence, with and without the row-minimum abandon."""
+    import paper_1610_07328_b200 as ssh
+
+    rng = np.random.default_rng(r + m)
+    X = np.cumsum(rng.standard_normal((12, m)), axis=1)
+    Y = np.cumsum(rng.standard_normal((12, m)), axis=1)
+    wp = ssh.WarpingParams(band=r / m)
+    assert wp.radius(m) == r
+    got = ssh.dtw_pairs(X, Y, wp)
+    want = np.sqrt([O.dtw_sq(X[i], Y[i], r) for i in range(12)])
+    assert got.tolist() == want.tolist()
+    ab = float(np.median(want))
+    got_ab = ssh.dtw_pairs(X, Y, wp, abandon_above=ab)
+    want_ab = np.sqrt([O.dtw_sq(X[i], Y[i], r, ab * ab) for i in range(12)])
+    assert got_ab.tolist() == want_ab.tolist()
+
+
+@pytest.mark.parametrize("band", [0.12, 0.2, 0.45])
+def test_query_wide_band_vs_oracle(cuda, band):
+    """Radii 61 / 102 / 230 at m = 512 take the wide-band wavefront DTW in the
+    query waves (and the band-chunked f64 rescoring): ids, |R| and squared
+    distances identical to the oracle cascade."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, _ = case_data("rw512")
+    p = _params(band, K=4)
+    idx = ssh.build_index(ssh.Dataset(X), p)
+    oidx = O.build_index(X, 80, 3, 15, 20, 4, 0, band)
+    ores = O.query_batch(oidx, Q, 10)
+    for i, r in enumerate(ssh.query_index_batch(idx, Q, 10)):
+        n = int(ores["n"][i])
+        assert r.stats.candidates == int(ores["n_cand"][i]), i
+        assert r.ids == ores["ids"][i][:n].tolist(), i
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
+
+
+def test_concurrent_queries_threadpool(cuda):
+    """SPEC.md:424 / bench.py:129-133: query_index from 8 threads on one index
+    (each thread on its own CUDA stream) equals serial calls."""
+    import torch
+
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw1024")
+    idx = ssh.build_index(ssh.Dataset(X), _params(band))
+    serial = [ssh.query_index(idx, q, 10) for q in Q]
+
+    def work(i):
+        with torch.cuda.stream(torch.cuda.Stream()):
+            return ssh.query_index(idx, Q[i], 10)
+
+    for _ in range(2):
+        with cf.ThreadPoolExecutor(8) as ex:
+            par = list(ex.map(work, range(len(Q))))
+        for a, b in zip(serial, par):
+            assert (a.ids, a.distances, a.status, a.stats) == (b.ids, b.distances, b.status, b.stats)
+
+
+def test_timings_keys_cli_style(cuda, golden):
+    """QueryResult.timings carries the reference's "hash"/"probe"/"rerank"
+    seconds, so the reference CLI's report loop (cli.py:172-186) runs
+    unchanged against the drop-in."""
+    import io
+
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw512")
+    idx = ssh.build_index(ssh.Dataset(X), _params(band))
+    out, err = io.StringIO(), io.StringIO()
+    for qi in range(3):
+        q = ssh.z_normalize(ssh.TimeSeries(np.asarray(Q[qi], dtype=np.float64))) if idx.normalized else Q[qi]
+        res = ssh.query_index(idx, q, 10, fallback_on_empty=False)
+        s = res.stats
+        print(f"# query {qi}: status={res.status} candidates={s.candidates} "
+              f"hash_pruned={s.hash_pruned_fraction:.6f} total_pruned={s.total_pruned_fraction:.6f}", file=out)
+        for rank, (sid, dist) in enumerate(zip(res.ids, res.distances), start=1):
+            print(f"{rank},{sid},{dist:.10g}", file=out)
+        print(f"timings: hash={res.timings['hash']:.4f}s probe={res.timings['probe']:.4f}s "
+              f"rerank={res.timings['rerank']:.4f}s", file=err)
+        assert all(res.timings[key] >= 0.0 for key in ("hash", "probe", "rerank"))
+        assert res.timings["hash"] + res.timings["probe"] + res.timings["rerank"] > 0.0
+    assert out.getvalue().count("# query") == 3
+
+
+def test_id_base_shards_merge_equals_single_index(cuda):
+    """3 id_base shards of one dataset on one GPU, merged by
+    (d2, id) with summed |R_g|, equal the single index and the oracle; a query
+    with R empty on every shard is "no-candidates" (and exact under fallback)."""
+    import torch
+
+    import paper_1610_07328_b200 as ssh
+    from paper_1610_07328_b200 import dist as D
+    from paper_1610_07328_b200.index import query_batch_device
+
+    X, Q, _, band = case_data("rw1024")
+    rng = np.random.default_rng(9)
+    noise = rng.standard_normal((2, X.shape[1]))
+    noise = ((noise - noise.mean(1, keepdims=True)) / noise.std(1, keepdims=True)).astype(np.float32)
+    Qs = np.ascontiguousarray(np.concatenate([Q, noise]), dtype=np.float32)
+    p = _params(band)
+    Xd = torch.from_numpy(X).cuda()
+    Qd = torch.from_numpy(Qs).cuda()
+    N = X.shape[0]
+    single = ssh.query_index_batch(ssh.build_index(ssh.Dataset(Xd), p), Qs, 10, fallback_on_empty=True)
+    parts = []
+    for g in range(3):
+        lo, hi = D.shard_range(N, g, 3)
+        idx = ssh.build_index(ssh.Dataset(Xd[lo:hi]), p, id_base=lo)
+        parts.append((idx, query_batch_device(idx, Qd, 10)))
+    ids = torch.cat([o[0] for _, o in parts], dim=1)
+    d2 = torch.cat([o[1] for _, o in parts], dim=1)
+    mi, md, n = D.merge_topk_local(ids, d2, 10)
+    ncand = sum(o[3] for _, o in parts)
+    oidx = O.build_index(X, 80, 3, 15, 20, 4, 0, band)
+    ores = O.query_batch(oidx, Qs, 10)
+    r = O.radius(band, X.shape[1])
+    empty = 0
+    for i in range(Qs.shape[0]):
+        k_i = int(ores["n"][i])
+        assert int(ncand[i]) == int(ores["n_cand"][i]) == single[i].stats.candidates or single[i].status == "fallback"
+        if ores["n_cand"][i] == 0:
+            empty += 1
+            assert int(n[i]) == 0
+            bi, bd = O.brute_force_topk_over(X, np.arange(N), Qs[i], r, 10)
+            assert single[i].status == "fallback" and single[i].ids == bi.tolist()
+            # the sharded exact fallback: every shard searched exactly, merged
+            ex = [query_batch_device(idx, Qd[i:i + 1], 10, exact=True) for idx, _ in parts]
+            ei, ed, _ = D.merge_topk_local(torch.cat([e[0] for e in ex], 1), torch.cat([e[1] for e in ex], 1), 10)
+            assert ei[0].tolist() == bi.tolist() and ed[0].tolist() == bd.tolist()
+            continue
+        assert mi[i][:k_i].tolist() == ores["ids"][i][:k_i].tolist() == single[i].ids
+        assert md[i][:k_i].tolist() == ores["d2"][i][:k_i].tolist()
+    assert empty >= 1
+
+
+def test_shard_save_load_round_trip(cuda, tmp_path):
+    """save_index of an id_base shard writes local ids (the file describes its
+    own rows); load_index(id_base=...) restores the global numbering."""
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw512")
+    p = _params(band, K=1)
+    lo = X.shape[0] // 2
+    idx = ssh.build_index(ssh.Dataset(X[lo:]), p, id_base=lo)
+    ssh.save_index(idx, tmp_path / "s.sshi")
+    back = ssh.load_index(tmp_path / "s.sshi", id_base=lo)
+    a = ssh.query_index_batch(idx, Q[:4], 10)
+    b = ssh.query_index_batch(back, Q[:4], 10)
+    assert [r.ids for r in a] == [r.ids for r in b] and all(min(r.ids) >= lo for r in a if r.ids)
+    assert [r.distances for r in a] == [r.distances for r in b]

@@ -35,9 +35,9 @@ def test_cws_tables_match_reference_keys(golden):
 
 
 def test_make_filter_matches_reference(golden):
-    assert cws.make_filter(80, 0).tolist() == golden["spec"]["filter80"]
+    assert cws.filter_weights(80, 0).tolist() == golden["spec"]["filter80"]
     with pytest.raises(ValueError):
-        cws.make_filter(0, 0)
+        cws.filter_weights(0, 0)
 
 
 def test_params_validation_messages():
@@ -178,9 +178,11 @@ def test_results_from_arrays_match_dataclass_construction():
     n_cand = np.array([9, 7, 1, 0, 1000], dtype=np.int64)
     counters = rng.integers(0, 50, size=(nq, 5)).astype(np.int64)
     status = np.array([0, 0, 0, 1, 2], dtype=np.int32)
-    got = _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N, 0.5, "w")
+    got = _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N, 0.5, "w", phase_ms=[10.0, 20.0, 30.0])
     for i, r in enumerate(got):
-        t = {"batch": 0.5, "per_query": 0.5 / nq}
+        # the reference's timing keys (index.py:235,265; cli.py:184-185) in seconds per query
+        t = {"hash": 10.0 / 1e3 / nq, "probe": 20.0 / 1e3 / nq, "rerank": 30.0 / 1e3 / nq,
+             "batch": 0.5, "per_query": 0.5 / nq}
         if status[i] == 1:
             want = QueryResult([], [], QueryStats(N, 0, SearchStats(0, 0, 0, 0, 0, 0)), t,
                                status="no-candidates", warning="w")
@@ -195,3 +197,42 @@ def test_results_from_arrays_match_dataclass_construction():
         with pytest.raises(dataclasses.FrozenInstanceError):
             r.status = "x"
         assert r.stats.cascade.pruned == want.stats.cascade.pruned
+
+
+def test_make_filter_returns_random_filter(golden):
+    """make_filter returns the reference's RandomFilter (sketch.py:36-43)."""
+    f = ssh.make_filter(80, 0)
+    assert isinstance(f, ssh.RandomFilter) and f.seed == 0 and f.W == 80
+    assert f.weights.tolist() == golden["spec"]["filter80"]
+    with pytest.raises(ValueError, match="filter length W must be >= 1"):
+        ssh.make_filter(0, 0)
+    with pytest.raises(ValueError, match="seed must be non-negative"):
+        ssh.make_filter(3, -1)
+
+
+def test_reference_public_names_exported():
+    """Every hot-path name of the reference's sshts/__init__.py that this
+    drop-in covers is importable from the package."""
+    for name in ["Dataset", "TimeSeries", "SshParams", "SshIndex", "QueryResult", "WarpingParams", "SearchStats",
+                 "SearchResult", "Envelope", "RandomFilter", "build_index", "query_index", "save_index", "load_index",
+                 "make_filter", "num_sketch_bits", "build_envelope", "dtw_distance", "lb_kim", "lb_keogh",
+                 "lb_keogh2", "exact_search", "make_dataset", "extract_subsequences", "z_normalize",
+                 "z_normalize_dataset", "save_dataset", "load_dataset", "srp_signature", "precision_at_k",
+                 "ndcg_at_k", "ConfigError", "SshError", "IndexLoadError", "DataFormatError"]:
+        assert hasattr(ssh, name), name
+
+
+def test_float64_rounding_warning_policy():
+    """float64 inputs that float32 cannot hold exactly warn (never silently
+    rounded); exactly representable ones do not."""
+    import warnings
+
+    from paper_1610_07328_b200.index import Float32RoundingWarning, _warn_f32_rounding
+
+    exact = np.arange(12, dtype=np.float64).reshape(3, 4) / 4.0
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        _warn_f32_rounding(exact, "dataset")
+        _warn_f32_rounding(exact.astype(np.float32), "dataset")
+    with pytest.warns(Float32RoundingWarning):
+        _warn_f32_rounding(exact + 0.1, "dataset")
