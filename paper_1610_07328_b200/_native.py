@@ -58,11 +58,24 @@ def build_native(verbose: bool = False, force: bool = False) -> Path:
     if (not force and LIB_PATH.exists()
             and LIB_PATH.stat().st_mtime >= max(p.stat().st_mtime for p in deps)):
         return LIB_PATH
+    import concurrent.futures as cf
+    import tempfile
+
     tmp = LIB_PATH.with_suffix(".so.tmp%d" % os.getpid())
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(INCLUDE), "-o", str(tmp), *map(str, srcs)]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.check_call(cmd, cwd=str(CSRC))
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "--cudart", "static")]
+    with tempfile.TemporaryDirectory() as td:
+        objs = [str(Path(td) / (p.stem + ".o")) for p in srcs]
+        cmds = [[nvcc(), *compile_flags, "-c", "-I", str(INCLUDE), "-o", o, str(p)] for p, o in zip(srcs, objs)]
+        if verbose:
+            for c in cmds:
+                print(" ".join(c), flush=True)
+        # one nvcc per translation unit, in parallel (query.cu dominates)
+        with cf.ThreadPoolExecutor(len(cmds)) as ex:
+            for f in [ex.submit(subprocess.check_call, c, cwd=str(CSRC)) for c in cmds]:
+                f.result()
+        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "--cudart", "static",
+                "-o", str(tmp), *objs]
+        subprocess.check_call(link, cwd=str(CSRC))
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

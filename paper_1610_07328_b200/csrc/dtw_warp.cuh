@@ -133,6 +133,17 @@ static inline int dtw_warp_chunk(int r) {
     return c <= 32 ? c : 0;
 }
 
+// chunk sizes 2..16 only (radius <= 255): the query-path kernels
+#define DTW_WARP_DISPATCH16(C_, CALL)                                              \
+    switch (C_) {                                                                  \
+        case 2: CALL(2); break;   case 3: CALL(3); break;   case 4: CALL(4); break;    \
+        case 5: CALL(5); break;   case 6: CALL(6); break;   case 7: CALL(7); break;    \
+        case 8: CALL(8); break;   case 9: CALL(9); break;   case 10: CALL(10); break;  \
+        case 11: CALL(11); break; case 12: CALL(12); break; case 13: CALL(13); break;  \
+        case 14: CALL(14); break; case 15: CALL(15); break; case 16: CALL(16); break;  \
+        default: break;                                                            \
+    }
+
 // switch over the instantiated chunk sizes: FN<C>(args...) for C = chunk
 #define DTW_WARP_DISPATCH(C_, CALL)                                                \
     switch (C_) {                                                                  \

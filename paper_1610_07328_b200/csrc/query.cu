@@ -1464,9 +1464,13 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
 // in place, ascending k; left edge from lane l - 1 by shfl_up, up edge from
 // lane l + 1's first cell of the same step by shfl_down).  The query (padded
 // with +inf) is staged once per block; each lane's query samples are a
-// register window sliding one sample per step (the new one from lane l + 1),
-// its series samples x[s - l] are loaded per group of C steps (coalesced
-// across lanes).  Per cell: FADD + FMNMX3 + FFMA.
+// register window sliding one sample per step (the new one from lane l + 1);
+// its series sample x[s - l] is a coalesced load per step from L1 (the row
+// was just read by the vectorised LB-prefix pass).  Per cell: FADD + FMNMX3 +
+// FFMA.  Groups of C steps come in three variants: ramp-up (lanes whose row is
+// still negative keep the virtual row -1 by selects), main (no checks), and
+// ramp-down (sample indices checked; rows >= m produce values no in-range
+// cell reads).
 //
 // Abandon (UCR-suite cumulative bound, dtw.py:206-215) on a skewed cut: after
 // step s the lanes hold the cells with i + floor(k / C) = s.  Along any
@@ -1479,7 +1483,9 @@ __global__ void dtw32_kernel(const float *__restrict__ X, int m, int r, const fl
 // remK = total - prefix(s) with the exact-x LB_Keogh terms (query envelope)
 // summed by a warp scan while the candidate is first read.
 #define DW_WARPS 8
-#define DW_XPAD 32
+#ifndef DW_MINB
+#define DW_MINB 3
+#endif
 // one step of the wide-band wavefront (see dtw32w_kernel); MASK: lanes whose
 // row is still negative keep their virtual row -1 (ramp-up steps only)
 template <int C, int U, bool MASK>
@@ -1512,47 +1518,29 @@ __device__ __forceinline__ void dw_step(float (&band)[C], float (&yw)[C], const 
     yw[U % C] = yn;
 }
 
-template <int C, int U, bool MASK>
-__device__ __forceinline__ void dw_group(float (&band)[C], float (&yw)[C], const float *xb, const float *yb,
-                                         const int s0, const int lane, const int own, const int cst,
-                                         const int rown, const int rcc, const int m, float &res) {
+// C steps from s0 (a multiple of C): MASK during ramp-up; CHECK: some lane's
+// sample index s - lane lies outside [0, m) (ramp-up / ramp-down groups)
+template <int C, int U, bool MASK, bool CHECK>
+__device__ __forceinline__ void dw_group(float (&band)[C], float (&yw)[C], const float *__restrict__ x,
+                                         const float *yb, const int s0, const int lane, const int own,
+                                         const int cst, const int rown, const int rcc, const int m, float &res) {
     if constexpr (U < C) {
         const int s = s0 + U;
-        dw_step<C, U, MASK>(band, yw, xb[U], s - lane, lane, own, cst, yb[U]);
-        if (s - lane == m - 1 && lane == rown) {
+        const int ix = s - lane;
+        float xi;
+        if (CHECK) xi = (unsigned)ix < (unsigned)m ? __ldg(x + ix) : 0.f;
+        else xi = __ldg(x + ix);
+        dw_step<C, U, MASK>(band, yw, xi, ix, lane, own, cst, yb[U]);
+        if (CHECK && ix == m - 1 && lane == rown) {
 #pragma unroll
             for (int c = 0; c < C; c++)
                 if (c == rcc) res = band[c];
         }
-        dw_group<C, U + 1, MASK>(band, yw, xb, yb, s0, lane, own, cst, rown, rcc, m, res);
+        dw_group<C, U + 1, MASK, CHECK>(band, yw, x, yb, s0, lane, own, cst, rown, rcc, m, res);
     }
 }
-
-// Wide-band wave DTW (fp32 screen): the band-chunked warp wavefront of
-// dtw_warp.cuh, one warp per candidate.  Lane l owns the C band offsets
-// k = lC + c in registers and sweeps row i = s - l at step s (cell update
-// in place, ascending k; left edge from lane l - 1 by shfl_up, up edge from
-// lane l + 1's first cell of the same step by shfl_down).  The query (padded
-// with +inf) is staged once per block and the candidate once per warp (zero
-// padded) in shared memory; each lane's query samples are a register window
-// sliding one sample per step (the new one from lane l + 1), its series
-// samples x[s - l] come from shared memory per group of C steps.  Per cell:
-// FADD + FMNMX3 + FFMA; ramp-up steps (rows < 0 on some lanes) keep the
-// virtual row -1 by selects, all later steps run unmasked (rows >= m only
-// produce values no in-range cell reads).
-//
-// Abandon (UCR-suite cumulative bound, dtw.py:206-215) on a skewed cut: after
-// step s the lanes hold the cells with i + floor(k / C) = s.  Along any
-// warping path f = i + floor(k / C) grows by 0 or 1 per move, from
-// floor(r / C) at (0, 0) to m - 1 + floor(r / C), so for s in that range every
-// path crosses the cut; the path's remaining rows are all > s - 31 ... s, so
-//   DTW >= min_cut D + sum_{i' > s} LB_Keogh term(i')
-// (lane 0 holds row s).  The test runs once per group of C steps with the same
-// fp32 slack as the row test: cut_min + max(remK - slack, 0) > thr.
-// remK = total - prefix(s) with the exact-x LB_Keogh terms (query envelope)
-// summed by a warp scan while the candidate is staged.
 template <int C, int RF>
-__global__ void __launch_bounds__(32 * DW_WARPS)
+__global__ void __launch_bounds__(32 * DW_WARPS, DW_MINB)
 dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restrict__ Q,
               const float *__restrict__ U, const float *__restrict__ Lo, DtwList L,
               const float *__restrict__ thr, unsigned long long *__restrict__ cells) {
@@ -1561,16 +1549,13 @@ dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restr
     const int own = nk / C, cst = nk - own * C;  // cell k = nk (forced +inf): lane own, index cst
     const int rown = r / C, rcc = r - rown * C;   // result cell k = r
     const int G = (m + 31 + C - 1) / C;          // step groups
-    const int RU = (31 + C - 1) / C;             // ramp-up groups (some rows negative)
-    const int YP = r + m + 33 * C + 64;
-    const int XS = DW_XPAD + G * C + 32;
+    const int YP = (r + m + 33 * C + 64 + 3) & ~3;  // keeps su / sl 16-byte aligned
     extern __shared__ __align__(16) float wsm[];
     float *yq = wsm;          // yq[j + r] = y[j], +inf outside [0, m)
     float *su = yq + YP;      // query envelope
     float *sl = su + m;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float *pre = sl + m + (size_t)w * (G + 1 + XS);  // prefix of LB_Keogh terms at group ends
-    float *xs = pre + G + 1;                          // xs[DW_XPAD + i] = x[i], 0 outside
+    float *pre = sl + m + (size_t)w * (G + 1);  // prefix of LB_Keogh terms at group ends
     const int q = L.act ? L.act[blockIdx.y] : blockIdx.y;
     const int slot = blockIdx.y;
     int start, end;
@@ -1587,11 +1572,13 @@ dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restr
         su[i] = cb ? U[(int64_t)q * m + i] : INFINITY;
         sl[i] = cb ? Lo[(int64_t)q * m + i] : -INFINITY;
     }
-    for (int t = lane; t < DW_XPAD; t += 32) xs[t] = 0.f;
-    for (int t = DW_XPAD + m + lane; t < XS; t += 32) xs[t] = 0.f;
     __syncthreads();
     const float inf = INFINITY;
     const int f_lo = r / C, f_hi = m - 1 + r / C;  // cut steps every path crosses
+    // groups [g_main0, g_main1) need no index checks (0 <= s - lane < m - 1 for
+    // every lane; the result row m - 1 is always reached in a checked group)
+    const int g_main0 = (31 + C - 1) / C, g_main1 = max(g_main0, (m - 1) / C);
+    const bool vec = (m & 3) == 0;
     unsigned long long my_cells = 0;
     for (int e = start + (int)blockIdx.x * DW_WARPS + w; e < end; e += (int)gridDim.x * DW_WARPS) {
         const uint32_t row = L.rows[(int64_t)slot * L.stride + e];
@@ -1603,26 +1590,62 @@ dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restr
         if (L.computed && lane == 0) atomicAdd(&L.computed[q], 1);
         const float *x = X + (int64_t)row * m;
         __syncwarp();
-        // stage x and the prefix sums of its LB_Keogh terms (exact x vs the
-        // query envelope) at the group-end steps s = (g + 1) C - 1
+        // prefix sums of the LB_Keogh terms (exact x vs the query envelope) at
+        // the group-end steps s = (g + 1) C - 1: 4 consecutive samples per
+        // lane per 128 (independent vector loads; the row then sits in L1 for
+        // the sweep)
         float carry = 0.f;
-        for (int i0 = 0; i0 < G * C; i0 += 32) {
-            const int i = i0 + lane;
-            float v2 = 0.f;
-            if (i < m) {
-                const float xv = __ldg(x + i);
-                xs[DW_XPAD + i] = xv;
-                const float v = fmaxf(fmaxf(xv - su[i], sl[i] - xv), 0.f);
-                v2 = v * v;
-            }
+        if (vec) {
+#pragma unroll 4
+            for (int i0 = 0; i0 < G * C; i0 += 128) {
+                const int i = i0 + 4 * lane;
+                float v2[4] = {0.f, 0.f, 0.f, 0.f};
+                if (i < m) {
+                    const float4 xv = __ldg(reinterpret_cast<const float4 *>(x + i));
+                    const float4 uv = *reinterpret_cast<const float4 *>(su + i);
+                    const float4 lv = *reinterpret_cast<const float4 *>(sl + i);
+                    const float xa[4] = {xv.x, xv.y, xv.z, xv.w};
+                    const float ua[4] = {uv.x, uv.y, uv.z, uv.w};
+                    const float la[4] = {lv.x, lv.y, lv.z, lv.w};
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const float t = __shfl_up_sync(0xFFFFFFFFu, v2, o);
-                if (lane >= o) v2 += t;
+                    for (int t = 0; t < 4; t++) {
+                        const float v = fmaxf(fmaxf(xa[t] - ua[t], la[t] - xa[t]), 0.f);
+                        v2[t] = v * v;
+                    }
+                }
+                v2[1] += v2[0];
+                v2[2] += v2[1];
+                v2[3] += v2[2];
+                float sc = v2[3];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float t = __shfl_up_sync(0xFFFFFFFFu, sc, o);
+                    if (lane >= o) sc += t;
+                }
+                const float base = carry + sc - v2[3];
+#pragma unroll
+                for (int t = 0; t < 4; t++)
+                    if ((i + t + 1) % C == 0 && i + t < G * C) pre[(i + t + 1) / C - 1] = base + v2[t];
+                carry = __shfl_sync(0xFFFFFFFFu, carry + sc, 31);
             }
-            const float P = carry + v2;
-            if ((i + 1) % C == 0) pre[(i + 1) / C - 1] = P;
-            carry = __shfl_sync(0xFFFFFFFFu, P, 31);
+        } else {
+            for (int i0 = 0; i0 < G * C; i0 += 32) {
+                const int i = i0 + lane;
+                float v2 = 0.f;
+                if (i < m) {
+                    const float xv = __ldg(x + i);
+                    const float v = fmaxf(fmaxf(xv - su[i], sl[i] - xv), 0.f);
+                    v2 = v * v;
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float t = __shfl_up_sync(0xFFFFFFFFu, v2, o);
+                    if (lane >= o) v2 += t;
+                }
+                const float P = carry + v2;
+                if ((i + 1) % C == 0) pre[(i + 1) / C - 1] = P;
+                carry = __shfl_sync(0xFFFFFFFFu, P, 31);
+            }
         }
         const float total = carry;
         const float slack = total * (float)(2 * m + 8) * U32_EPS;
@@ -1638,12 +1661,13 @@ dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restr
         int g = 0;
         for (; g < G; g++) {
             const int s0 = g * C;
-            const float *xb = xs + DW_XPAD + s0 - lane;
             const float *yb = yq + s0 + 32 * C - 31;
-            if (g < RU)
-                dw_group<C, 0, true>(band, yw, xb, yb, s0, lane, own, cst, rown, rcc, m, res);
+            if (g < g_main0)
+                dw_group<C, 0, true, true>(band, yw, x, yb, s0, lane, own, cst, rown, rcc, m, res);
+            else if (g < g_main1)
+                dw_group<C, 0, false, false>(band, yw, x, yb, s0, lane, own, cst, rown, rcc, m, res);
             else
-                dw_group<C, 0, false>(band, yw, xb, yb, s0, lane, own, cst, rown, rcc, m, res);
+                dw_group<C, 0, false, true>(band, yw, x, yb, s0, lane, own, cst, rown, rcc, m, res);
             // cut test after step s = s0 + C - 1
             const int s = s0 + C - 1;
             if (cb && s >= f_lo && s <= f_hi) {
@@ -2506,11 +2530,11 @@ static int launch_dtw64band(const float *X, int m, int r, const float *Q, const 
                             int64_t n, int nq, double *out, cudaStream_t st, bool *done) {
     *done = false;
     const int C = dtw_warp_chunk(r);
-    if (C == 0) return SSH_OK;
+    if (C == 0 || C > 16) return SSH_OK;
     dim3 grid((unsigned)ssh_div_up(n, D64B_WARPS), (unsigned)(list ? nq : 1));
 #define D64B_CALL(CC) \
     dtw64band_kernel<CC><<<grid, 32 * D64B_WARPS, 0, st>>>(X, m, r, Q, qrow, list, stride, cnt, xrow, n, out)
-    DTW_WARP_DISPATCH(C, D64B_CALL)
+    DTW_WARP_DISPATCH16(C, D64B_CALL)
 #undef D64B_CALL
     SSH_CHECK_LAUNCH();
     *done = true;
@@ -2996,10 +3020,10 @@ static int launch_dtw32w(ssh_ctx *ctx, const float *X, const float *Q, const flo
     *done = false;
     const int m = ctx->p.m, r = ctx->p.radius;
     const int C = dtw_warp_chunk(r);
-    if (C < 3) return SSH_OK;
+    if (C < 3 || C > 16) return SSH_OK;
     const int G = (m + 31 + C - 1) / C;
-    const int XS = DW_XPAD + G * C + 32;
-    const size_t smem = sizeof(float) * ((size_t)(r + m + 33 * C + 64) + 2 * (size_t)m + (size_t)DW_WARPS * (G + 1 + XS));
+    const size_t smem = sizeof(float) * ((size_t)((r + m + 33 * C + 64 + 3) & ~3) + 2 * (size_t)m +
+                                         (size_t)DW_WARPS * (G + 1));
     if (smem > 200 * 1024) return SSH_OK;
     *done = true;
     if (L.wave <= 0 || nq <= 0) return SSH_OK;
@@ -3018,7 +3042,7 @@ static int launch_dtw32w(ssh_ctx *ctx, const float *X, const float *Q, const flo
         DW_LAUNCH(4, 51);
     } else {
 #define DW_CALL(CC) DW_LAUNCH(CC, -1)
-        DTW_WARP_DISPATCH(C, DW_CALL)
+        DTW_WARP_DISPATCH16(C, DW_CALL)
 #undef DW_CALL
     }
 #undef DW_LAUNCH
