@@ -5,22 +5,33 @@ A step = one pass of the hot path over one batch of synthetic input: build
 the index over the rank's series (K1 sketch -> K2 shingle -> K3 CWS ->
 K4 bucket tables) and answer the query batch (K5 hash -> K6 probe -> K7 LB
 filter -> K8 DTW waves -> K10 exact rescoring -> K9 top-k, then the
-cross-rank merge).  Workload: BASELINE.json configs[1] (N=1,000,000 random
-walks, m=512, K=4, L=20, 1,000 queries, top-10) per GPU (weak scaling).
+cross-rank merge).
 
-value = series indexed/s over the whole job (build part of the timed steps,
-CUDA events, max over ranks); queries/s and DTW cells/s are reported beside
-it.  `--impl reference` times the CPU oracle port (oracle/ssh_oracle.c, all
-host threads) on bounded samples of the same workload.
+Workloads (BASELINE.json configs):
+* the headline line: configs[1] (N=1,000,000 random walks, m=512, K=4, L=20,
+  1,000 queries, band 5%, top-10) per GPU — weak scaling over N GPUs;
+* at N=1 the same line carries "workloads" with configs[2] (2M ECG windows of
+  1024) and configs[3] (4M x 2048 random walks, band 10%), each measured the
+  same way (device events, per-stage rooflines);
+* `--cfg 4`: configs[4], 64M series sharded across the N GPUs (strong
+  scaling), 10,000 queries.
+
+`--gpus N` without torchrun re-executes itself under torch.distributed.run
+(one process per GPU, NCCL).  value = series indexed/s over the whole job
+(build part of the timed steps, CUDA events, max over ranks); queries/s and
+DTW cells/s are reported beside it.  `--impl reference` times the CPU oracle
+port (oracle/ssh_oracle.c, all host threads) on bounded samples of the same
+workload.
 """
 
 from __future__ import annotations
 
 import argparse
-import gc
 import ctypes
+import gc
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,6 +45,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "series indexed/s; queries/s (probe + DTW rerank, top-10); DTW cells/s"
 UNIT = "series/s"
 K_TOP = 10
+PROFILE_ROUND = "r02"
 
 
 def load_peaks():
@@ -41,8 +53,8 @@ def load_peaks():
     if p.exists():
         d = json.loads(p.read_text())
         return dict(hbm_gbs=float(d["hbm_gbs"]), sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)),
-                    source="measured")
-    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback")
+                    source="measured (MEASURED_PEAKS.json)")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback (B200_PROFILING.md)")
 
 
 class ClockSampler:
@@ -116,11 +128,43 @@ def ncores():
         return os.cpu_count() or 1
 
 
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` run directly: one rank per GPU under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    print("relaunch: " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 # ----------------------------------------------------------------- our arm
 
-def run_ours(args):
+def _release_device_state():
+    """Drop cached contexts (grow-only scratch) and pooled memory between workloads."""
+    import torch
+
+    from paper_1610_07328_b200 import index as I
+
+    with I._ctx_lock:
+        I._ctx_cache.clear()
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def measure(args, cfg, rank, world, local, steps, warmup, nq=None, n_per=None, strong=False,
+            headline=False):
+    """Time `steps` build+query steps of configs[cfg] on this rank's shard; returns
+    the workload dict on rank 0 (None elsewhere)."""
     import numpy as np
     import torch
+    import torch.distributed as tdist
 
     import paper_1610_07328_b200 as ssh
     from paper_1610_07328_b200 import _native as nat
@@ -128,17 +172,20 @@ def run_ours(args):
     from paper_1610_07328_b200 import dist as D
     from paper_1610_07328_b200.index import _stream_ptr, get_context, query_batch_device
 
-    rank, world, local = D.init_from_env("nccl")
-    torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    c = datagen.CONFIGS[args.cfg]
-    N = args.n or c["N"]
+    c = datagen.CONFIGS[cfg]
     m = c["m"]
-    nq = args.nq if args.nq is not None else c["nq"]
-    N_total = N * world
-    lo, hi = rank * N, (rank + 1) * N
+    nq = c["nq"] if nq is None else nq
+    if strong:
+        N_total = n_per * world if n_per else c["N"]
+        lo, hi = D.shard_range(N_total, rank, world)
+    else:
+        N = n_per or c["N"]
+        N_total = N * world
+        lo, hi = rank * N, (rank + 1) * N
+    N = hi - lo
     t_gen = time.time()
-    X, Q, src, p = datagen.workload(args.cfg, lo=lo, hi=hi, device=dev, nq=nq, n_override=N_total)
+    X, Q, src, p = datagen.workload(cfg, lo=lo, hi=hi, device=dev, nq=nq, n_override=N_total)
     torch.cuda.synchronize()
     t_gen = time.time() - t_gen
     params = ssh.SshParams(**p)
@@ -146,7 +193,10 @@ def run_ours(args):
     Qd = torch.from_numpy(Q).to(dev)
     ctx = get_context(local, params, m)
     lib = nat.lib()
-    import torch.distributed as tdist
+    # the previous step's index stays alive while the next one builds (steady
+    # state of the stream-ordered pool) unless two indexes would not fit
+    keep_prev = N * (4 * m + 3 * m + 300) * 2 < 0.6 * torch.cuda.get_device_properties(dev).total_memory
+    local_fn = lambda index: (lambda Qs, k: query_batch_device(index, Qs, k, False))  # noqa: E731
 
     def step():
         e0 = torch.cuda.Event(enable_timing=True)
@@ -155,16 +205,17 @@ def run_ours(args):
         e0.record()
         index = ssh.build_index(ds, params, id_base=lo)
         e1.record()
-        ids, d2, n_out, n_cand, counters, status = query_batch_device(index, Qd, K_TOP)
         if world > 1:
-            ids, d2, n_cand, counters = D.merge_across_ranks(ids, d2, n_cand, counters, K_TOP)
+            ids, d2, n_out, n_cand, counters, status = D.sharded_query(Qd, K_TOP, local_fn(index))
+        else:
+            ids, d2, n_out, n_cand, counters, status = query_batch_device(index, Qd, K_TOP)
         e2.record()
-        return (e0, e1, e2), (index, ids, d2, n_cand, counters)
+        return (e0, e1, e2), (index, ids, d2, n_cand, counters, status)
 
-    # warm-up mirrors the timed loop (the previous step's index stays alive while
-    # the next one builds), so the stream-ordered memory pool reaches steady state
     last = None
-    for _ in range(args.warmup):
+    for _ in range(warmup):
+        if not keep_prev:
+            last = None
         _, last = step()
     torch.cuda.synchronize()
     if world > 1:
@@ -178,7 +229,9 @@ def run_ours(args):
     # pause landing between those points would show up as device idle time
     gc.collect()
     gc.disable()
-    for _ in range(args.steps):
+    for _ in range(steps):
+        if not keep_prev:
+            last = None
         ev, last = step()
         evs.append(ev)
     torch.cuda.synchronize()
@@ -190,70 +243,125 @@ def run_ours(args):
     clocks = sampler.stop()
     build_each = [a.elapsed_time(b) for a, b, _ in evs]
     query_each = [b.elapsed_time(c2) for _, b, c2 in evs]
-    build_ms = sum(build_each)
-    query_ms = sum(query_each)
-    total_ms = evs[0][0].elapsed_time(evs[-1][2])
-    t = torch.tensor([build_ms, query_ms, total_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([sum(build_each), sum(query_each), evs[0][0].elapsed_time(evs[-1][2])],
+                     dtype=torch.float64, device=dev)
     if world > 1:
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     build_ms, query_ms, total_ms = t.tolist()
-    index, ids, d2, n_cand, counters = last
-    mean_cand = float(n_cand.double().mean())
-    mean_cnt = counters.double().mean(dim=0).tolist()
-
+    index, ids, d2, n_cand, counters, status = last
+    ties = index.sketch_stats
+    tie_t = torch.tensor([ties["rechecked"], ties["near_zero"]], dtype=torch.int64, device=dev)
+    if world > 1:
+        tdist.all_reduce(tie_t, op=tdist.ReduceOp.SUM)
     out = None
+    if rank == 0:
+        kind = "ECG windows" if c["kind"] == "ecg" else "random walk"
+        out = {
+            "value": N_total * steps / (build_ms / 1e3),
+            "queries_per_s": nq * steps / (query_ms / 1e3),
+            "ms_per_step": total_ms / steps,
+            "build_ms_per_step": build_ms / steps,
+            "query_ms_per_step": query_ms / steps,
+            "build_ms_each": [round(v, 3) for v in build_each],
+            "query_ms_each": [round(v, 3) for v in query_each],
+            "steps": steps, "warmup": warmup,
+            "config": {
+                "workload": f"configs[{cfg}]: {kind} N={N_total} ({'sharded' if strong else 'per GPU'} "
+                            f"x {world}) x m={m}, W=80 delta=3 n=15 K=4 L=20, {nq} queries, "
+                            f"DTW band {c['band']}, top-{K_TOP}",
+                "cfg": cfg, "N_per_gpu": N, "N_total": N_total, "m": m, "queries": nq, "K": 4, "L": 20,
+                "band": c["band"], "radius": params.warping().radius(m), "k": K_TOP,
+                "parallelism": (f"shard{world} (series-sharded, queries replicated, top-k all_gather + "
+                                f"|R| all_reduce over NCCL)" if world > 1 else "single GPU"),
+                "l2": "inputs larger than L2 (X = %.2f GB per GPU)" % (N * m * 4 / 1e9),
+            },
+            "mean_candidates": float(n_cand.double().mean()),
+            "statuses": {s: int((status == v).sum()) for s, v in (("ok", 0), ("no-candidates", 1),
+                                                                   ("fallback", 2))},
+            "mean_counters": dict(zip(["kim_pruned", "keogh_pruned", "keogh2_pruned", "dtw_computed",
+                                       "dtw_abandoned"], counters.double().mean(dim=0).tolist())),
+            "sketch_ties": {"rechecked_f64": int(tie_t[0]), "near_zero_abs_dot_lt_1e-9": int(tie_t[1]),
+                            "note": "windows of the last timed build (all ranks) whose f32 screen "
+                                    "deferred to the exact f64 dot; |dot| < 1e-9 are sign ties"},
+            "gpu_launches": int(launches),
+            "gpu_launches_per_step": launches / steps,
+            "clocks": clocks,
+            "datagen_s": t_gen,
+            "scaling": "strong" if strong else "weak",
+        }
+    if world > 1:
+        tdist.barrier()
+    if rank == 0:
+        out["stages"] = stage_profile(ctx, X, Qd, index, params, lib, nat, _stream_ptr(local), query_batch_device,
+                                      cfg, float(n_cand.double().sum()))
+        out["dtw_cells_per_s"] = out["stages"].get("dtw_cells_per_s")
+        # dominant kernel = the longest single-kernel stage with a roofline
+        dom = max((s for s in out["stages"].values() if isinstance(s, dict) and s.get("roofline")),
+                  key=lambda s: s["ms"])
+        out["roofline"] = dom.get("roofline")
+        out["dominant_stage"] = dom.get("name")
+    del last, index
+    if world > 1:
+        tdist.barrier()
+    if not args.no_e2e and (headline or args.e2e_all):
+        e = e2e_run(X, Q, params, lo, nq, N_total, world)
+        if rank == 0:
+            out["e2e"] = e
+    if rank == 0 and headline and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(X, Q, p, args, cfg)
+    del X, Qd, ds
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1610_07328_b200 import dist as D
+
+    rank, world, local = D.init_from_env("nccl")
+    torch.cuda.set_device(local)
+    if args.gpus != world:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
+    strong = args.cfg == 4 or args.strong
+    if args.cfg == 4 and world == 1 and not args.n:
+        # 64M x 512 f32 (128 GB) + codes/summaries/tables do not fit one GPU
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": "configs[4] (64M series) needs >= 2 GPUs; "
+                              "run with --gpus 2..8", "n_gpus": world}), flush=True)
+        return
+    w = measure(args, args.cfg, rank, world, local, args.steps, args.warmup, nq=args.nq, n_per=args.n,
+                strong=strong, headline=True)
+    extras = {}
+    if world == 1 and args.cfg == 1 and not args.no_extra:
+        for cfg in (2, 3):
+            _release_device_state()
+            try:
+                extras[f"configs[{cfg}]"] = measure(args, cfg, rank, world, local, args.extra_steps,
+                                                    args.extra_warmup, nq=args.extra_nq)
+            except Exception as ex:  # report, never hide: the line says which workload failed
+                extras[f"configs[{cfg}]"] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0:
         out = {
             "metric": METRIC,
-            "value": N_total * args.steps / (build_ms / 1e3),
+            "value": w.pop("value"),
             "unit": UNIT,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps,
+            "ms_per_step": w.pop("ms_per_step"),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": w.pop("scaling"),
             "vs_baseline": None,
             "dtype": "f32 screen + f64 exact (sign recheck, CWS, DTW rescoring); u64 keys",
             "data": "synthetic (BASELINE.json configs[%d] recipe, seeded; no public dataset)" % args.cfg,
-            "config": {
-                "workload": f"configs[{args.cfg}]: random walk N={N}/GPU x m={m}, W=80 delta=3 n=15 "
-                            f"K=4 L=20, {nq} warped queries, DTW band {c['band']}, top-{K_TOP}",
-                "N_per_gpu": N, "N_total": N_total, "m": m, "queries": nq, "K": 4, "L": 20,
-                "band": c["band"], "k": K_TOP, "parallelism": f"shard{world} (series-sharded, "
-                "queries replicated, top-k all_gather)",
-                "l2": "inputs larger than L2 (X = %.2f GB per GPU)" % (N * m * 4 / 1e9),
-            },
-            "queries_per_s": nq * args.steps / (query_ms / 1e3),
-            "build_ms_per_step": build_ms / args.steps,
-            "build_ms_each": [round(v, 3) for v in build_each],
-            "query_ms_each": [round(v, 3) for v in query_each],
-            "query_ms_per_step": query_ms / args.steps,
-            "mean_candidates": mean_cand,
-            "mean_counters": dict(zip(["kim_pruned", "keogh_pruned", "keogh2_pruned", "dtw_computed",
-                                       "dtw_abandoned"], mean_cnt)),
-            "gpu_launches": int(launches),
-            "gpu_launches_per_step": launches / args.steps,
-            "clocks": clocks,
-            "datagen_s": t_gen,
         }
-    if world > 1:
-        tdist.barrier()
-    # ---- per-stage timing (outside the timed region) for the roofline
-    if rank == 0:
-        stages = stage_profile(ctx, X, Qd, index, params, lib, nat, _stream_ptr(local), query_batch_device)
-        out["stages"] = stages
-        out["dtw_cells_per_s"] = stages.get("dtw_cells_per_s")
-        # dominant kernel = the longest stage that is a single kernel with a
-        # roofline (grouped stages such as key+sort list their parts in "stages")
-        dom = max((s for s in stages.values() if isinstance(s, dict) and s.get("roofline")),
-                  key=lambda s: s["ms"])
-        out["roofline"] = dom.get("roofline")
-        out["dominant_stage"] = dom.get("name")
-        if not args.no_e2e:
-            out["e2e"] = e2e_run(args, ds, X, Q, params, lo, nq)
-        if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(X, Q, p, args, with_queries=True)
+        out.update(w)
+        if extras:
+            for v in extras.values():
+                if isinstance(v, dict):
+                    v.pop("scaling", None)
+            out["workloads"] = extras
         print(json.dumps(out), flush=True)
     if world > 1:
         tdist.barrier()
@@ -275,22 +383,35 @@ def _time(fn, reps=5):
     return statistics.median(ts)
 
 
-def _ncu_traffic(kernel):
-    """DRAM bytes (read + write) of all launches of `kernel` in one configs[1]
-    build + 1000-query batch, from the committed ncu capture (profiles/), or None."""
-    try:
-        d = json.loads((Path(__file__).resolve().parent / "profiles" / "r01" / "traffic_cfg1.json").read_text())
-        return d["kernels"][kernel]["dram_bytes"]
-    except Exception:
-        return None
+def _profile_json(cfg):
+    """The committed ncu summary of this workload (profiles/<round>/ncu_cfg<cfg>.json), or {}."""
+    for rnd in (PROFILE_ROUND, "r01"):
+        p = ROOT / "profiles" / rnd / f"ncu_cfg{cfg}.json"
+        if p.exists():
+            try:
+                return json.loads(p.read_text())
+            except Exception:
+                return {}
+    return {}
 
 
-def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
+def _traffic(prof, kernel_prefix):
+    """DRAM bytes (read + write) summed over the launches of kernels whose name
+    starts with `kernel_prefix` in one build + query batch (ncu --set full)."""
+    ks = prof.get("kernels", {})
+    tot = [v["dram_bytes"] for k, v in ks.items() if k.startswith(kernel_prefix) and v.get("dram_bytes")]
+    return float(sum(tot)) if tot else None
+
+
+def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device, cfg, cand_total):
+    import numpy as np
     import torch
 
     peaks = load_peaks()
     hbm = peaks["hbm_gbs"]
+    prof_json = _profile_json(cfg)
     N, m = X.shape
+    nq = Qd.shape[0]
     words = ctx.words
     bits = torch.empty((N, words), dtype=torch.int64, device=X.device)
     sig = torch.empty((N, params.d), dtype=torch.int64, device=X.device)
@@ -299,18 +420,41 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     b = N * (4 * m + 8 * words)
     res["sketch"] = dict(name="sketch (K1)", ms=ms, bytes=b, roofline=dict(
         bound="hbm", achieved=b / ms / 1e6, peak=hbm, unit="GB/s", frac=b / ms / 1e6 / hbm,
-        traffic=_ncu_traffic("sketch_stream_kernel<80, 3, 20, 16>"), kernel="sketch_stream_kernel<80,3,20,16>",
-        note="algorithmic bytes = N*(4m + 8*ceil(N_B/64)); peak = %s HBM copy; traffic = ncu dram bytes of "
-             "the build launch + the 1000-query hash launch (0.1%%) (profiles/r01/traffic_cfg1.json)"
-             % peaks["source"]))
+        traffic=_traffic(prof_json, "sketch_"), kernel="sketch_stream_kernel",
+        note="algorithmic bytes = N*(4m + 8*ceil(N_B/64)); peak = %s HBM copy; traffic = ncu dram bytes "
+             "(profiles/%s/ncu_cfg%d.json)" % (peaks["source"], PROFILE_ROUND, cfg)))
     ms_sig = _time(lambda: nat.check(lib.ssh_signatures(ctx.handle, nat.ptr(X), N, m, nat.ptr(sig), None, st)))
     cws_ms = max(ms_sig - ms, 1e-6)
-    b2 = N * (4 * m + 8 * params.d)
-    res["shingle_cws"] = dict(name="shingle+CWS (K2+K3)", ms=cws_ms, evaluations=None, roofline=dict(
-        bound="hbm", achieved=N * (8 * words + 8 * params.d) / cws_ms / 1e6, peak=hbm, unit="GB/s",
-        frac=N * (8 * words + 8 * params.d) / cws_ms / 1e6 / hbm, traffic=_ncu_traffic("cws_fast_kernel<3, 5, 4>"),
-        kernel="cws_fast_kernel<FUSED,5,4>",
-        note="HBM bytes in/out only; the kernel is bound by L2 gathers of the CWS tables + FP64"))
+    # CWS work unit: S = K*L slot evaluations per distinct token per series
+    # (SURVEY §8d); D = distinct tokens per series, counted on a sample
+    ns = min(N, 16384)
+    T = ctx.T
+    tok = torch.empty((ns, T), dtype=torch.int32, device=X.device)
+    cnt = torch.empty((ns, T), dtype=torch.int16, device=X.device)
+    nset = torch.empty(ns, dtype=torch.int32, device=X.device)
+    D_mean = None
+    try:
+        nat.check(lib.ssh_sketch(ctx.handle, nat.ptr(X), ns, m, nat.ptr(bits), None, st))
+        nat.check(lib.ssh_shingle(ctx.handle, nat.ptr(bits), ns, nat.ptr(tok), nat.ptr(cnt), nat.ptr(nset), st))
+        torch.cuda.synchronize()
+        D_mean = float(nset.double().mean())
+    except Exception:
+        D_mean = None
+    S = params.K * params.d
+    ev = N * S * D_mean if D_mean else None
+    cws_prof = prof_json.get("cws", {})
+    res["shingle_cws"] = dict(
+        name="shingle+CWS (K2+K3, fused)", ms=cws_ms, distinct_tokens_per_series=D_mean,
+        evaluations=ev, evaluations_per_s=(ev / (cws_ms / 1e3)) if ev else None,
+        l2_hit_rate=cws_prof.get("l2_hit_rate"), fp64_pipe_util=cws_prof.get("fp64_pipe_util"),
+        issue_active=cws_prof.get("issue_active"),
+        roofline=dict(
+            bound="hbm", achieved=N * (8 * words + 8 * params.d) / cws_ms / 1e6, peak=hbm, unit="GB/s",
+            frac=N * (8 * words + 8 * params.d) / cws_ms / 1e6 / hbm, traffic=_traffic(prof_json, "cws_"),
+            kernel="cws_fast_kernel",
+            note="HBM bytes in/out only (bits in, signatures out); the kernel is bound by dependent L2 "
+                 "gathers of the CWS tables: see evaluations_per_s (S*D per series), l2_hit_rate, "
+                 "fp64_pipe_util, issue_active (ncu --set full, profiles/%s)" % PROFILE_ROUND))
     res["signatures_fused"] = dict(name="K1-K3", ms_total=ms_sig)
 
     def mk():
@@ -320,10 +464,15 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
 
     ms_t = _time(mk, reps=3)
     bt = N * params.d * 20
+    tr = None
+    for pre in ("rs_", "rle_", "tb_"):
+        v = _traffic(prof_json, pre)
+        tr = (tr or 0.0) + v if v is not None else tr
     res["tables"] = dict(name="bucket tables (K4)", ms=ms_t, roofline=dict(
         bound="hbm", achieved=bt / ms_t / 1e6, peak=hbm, unit="GB/s", frac=bt / ms_t / 1e6 / hbm,
-        traffic=None, kernel="rs_scatter/rs_hist/rle_*",
-        note="algorithmic bytes = 20 B per (series, table): 8 B key in, 8 B key + 4 B id out"))
+        traffic=tr, kernel="rs_*/rle_* (radix passes + run-length CSR)",
+        note="algorithmic bytes = 20 B per (series, table): 8 B key in, 8 B key + 4 B id out; traffic = "
+             "ncu dram bytes of every table kernel of one build"))
     # query phases
     nat.check(lib.ssh_ctx_set_profiling(ctx.handle, 1))
     torch.cuda.synchronize()
@@ -334,25 +483,38 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     nat.check(lib.ssh_ctx_set_profiling(ctx.handle, 0))
     names = ["hash (K5)", "probe+bitmap (K6)", "member keys (sample, cutoff pass, overflow) + bin sort (K7)",
              "wave LB_Keogh2/LB_Keogh over u8 codes (K8a wave_lb_kernel)",
-             "wave fp32 DTW (K8b dtwp_first/dtwp_level pooled passes)", "rescore+top-k (K9/K10)"]
-    r = params.warping().radius(m)
+             "wave fp32 DTW (K8b)", "rescore+top-k (K9/K10)"]
     for i, n in enumerate(names):
         res[f"q{i}"] = dict(name=n, ms=prof[i])
+    # K6: bitmap words written + bucket id lists read
+    nw = (N + 31) // 32
+    # K7: every member of R costs one 64-byte record read (L2/HBM) + its key
+    # and bin written (8 B); the bitmap is read once per pass
+    k7_bytes = cand_total * (64 + 8) + nq * nw * 4 * 2
+    if prof[2] > 0:
+        res["q2"]["roofline"] = dict(
+            bound="hbm", achieved=k7_bytes / prof[2] / 1e6, peak=hbm, unit="GB/s",
+            frac=k7_bytes / prof[2] / 1e6 / hbm, traffic=_traffic(prof_json, "paa_members"),
+            kernel="paa_members_kernel + binsort_kernel",
+            note="algorithmic bytes = |R| x (64 B record + 8 B key/bin) + 2 bitmap passes; records are "
+                 "L2-resident at configs[1] (64 MB)")
     cells = prof[6]
     dtw_ms = prof[4]
     res["dtw_cells"] = cells
     res["dtw_cells_per_s"] = cells / (dtw_ms / 1e3) if dtw_ms > 0 else None
-    # per cell: FADD + FFMA on the fma pipe, FMNMX3 + FMNMX (row min) on the alu
-    # pipe; both pipes issue 16 lanes/clk/SMSP for these forms (B300_MICROARCH
-    # "rt_SMSP=2"), so the cell peak is 148 x 64 lanes x f / 2 instr
-    peak_cells = 148 * 64 * peaks["sm_max_mhz"] * 1e6 / 2.0
-    res["q4"]["roofline"] = dict(bound="fp32", achieved=(cells / (dtw_ms / 1e3)) / 1e12 if dtw_ms else 0,
-                                 peak=peak_cells / 1e12, unit="Tcells/s",
-                                 frac=(cells / (dtw_ms / 1e3)) / peak_cells if dtw_ms else 0,
-                                 traffic=_ncu_traffic("dtwp_level_kernel<26>"),
-                                 kernel="dtwp_first_kernel + dtwp_level_kernel<26>",
-                                 note="cells = alive lane-rows x (2r+1); 2 fma-pipe + 2 alu-pipe instr per cell; "
-                                      "peak 148 x 64 x f_max / 2")
+    # a cell is FADD + FFMA + FMNMX3 (3 FP32-pipe instructions) at
+    # 128 lanes/SM/clk -> 148 x 128 x f_max / 3 = 12.4 T cells/s at 1965 MHz
+    peak_cells = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 3.0
+    r = params.warping().radius(m)
+    res["q4"]["roofline"] = dict(
+        bound="fp32", achieved=(cells / (dtw_ms / 1e3)) / 1e12 if dtw_ms else 0,
+        peak=peak_cells / 1e12, unit="Tcells/s",
+        frac=(cells / (dtw_ms / 1e3)) / peak_cells if dtw_ms else 0,
+        traffic=_traffic(prof_json, "dtw"),
+        kernel=("dtwp_first/dtwp_pass pooled register band" if r in (3, 6, 13, 26, 51)
+                else "dtw32w_kernel (band-chunked warp wavefront)"),
+        note="cells = in-band cells of the rows each fp32 DTW evaluated; peak = SURVEY §8d's 148 x 128 x "
+             "f_max / 3 (FADD + FFMA + FMNMX3 per cell)")
     res["dtw_evaluated"] = prof[8]
     res["rescored"] = prof[9]
     lb_bytes = prof[7]
@@ -360,10 +522,9 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     if lb_ms > 0:
         res["q3"]["roofline"] = dict(
             bound="hbm", achieved=lb_bytes / lb_ms / 1e6, peak=hbm, unit="GB/s",
-            frac=lb_bytes / lb_ms / 1e6 / hbm, traffic=_ncu_traffic("wave_lb_kernel"), kernel="wave_lb_kernel",
+            frac=lb_bytes / lb_ms / 1e6 / hbm, traffic=_traffic(prof_json, "wave_lb"), kernel="wave_lb_kernel",
             note="algorithmic bytes = u8 envelope-code and sample-code blocks the LB_Keogh2/LB_Keogh "
-                 "cascade reads before abandoning (device counter, per 1000-query batch); traffic = "
-                 "ncu dram bytes of the same launches (profiles/r01/traffic_cfg1.json)")
+                 "cascade reads before abandoning (device counter, per query batch)")
     res["wave_lb_bytes"] = lb_bytes
     res["wave_lb_paa_skips"] = prof[10]
     res["wave_lb_keogh_prunes"] = prof[11]
@@ -374,14 +535,16 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device):
     if prof[15] > 0:
         res["thr0_over_dk"] = prof[13] / prof[15]
         res["thr1_over_dk"] = prof[14] / prof[15]
+    del bits, sig, tok, cnt, nset
     return res
 
 
-def e2e_run(args, ds, X, Q, params, lo, nq):
-    """Public API with HOST buffers: build_index from pinned host memory and
-    query_index_batch from host numpy; H2D/D2H inside the timed region."""
-    import numpy as np
+def e2e_run(X, Q, params, lo, nq, N_total, world):
+    """Public API with HOST buffers on every rank: build_index from pinned host
+    memory and query_index_batch (query_index_batch_sharded at N > 1) from host
+    numpy; H2D/D2H inside the timed region; wall time, max over ranks."""
     import torch
+    import torch.distributed as tdist
 
     import paper_1610_07328_b200 as ssh
 
@@ -392,95 +555,136 @@ def e2e_run(args, ds, X, Q, params, lo, nq):
     reps = 2
     tb, tq = [], []
     for i in range(reps + 1):
+        if world > 1:
+            tdist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         index = ssh.build_index(dsh, params, id_base=lo)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        res = ssh.query_index_batch(index, Q, K_TOP)
+        if world > 1:
+            res = ssh.query_index_batch_sharded(index, Q, K_TOP)
+        else:
+            res = ssh.query_index_batch(index, Q, K_TOP)
         t2 = time.perf_counter()
         if i:
             tb.append(t1 - t0)
             tq.append(t2 - t1)
         del index, res
+    t = torch.tensor([statistics.median(tb), statistics.median(tq)], dtype=torch.float64,
+                     device=X.device)
+    if world > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    tbm, tqm = t.tolist()
     h2d = N * m * 4 + Q.shape[0] * m * 4
     d2h = nq * K_TOP * 16 + nq * (4 + 8 + 40 + 4) + params.d * 8
-    return {"value": N / statistics.median(tb), "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "queries_per_s": nq / statistics.median(tq),
-            "note": "build_index(Dataset(pinned host f32)) + query_index_batch(host numpy) "
-                    "through the public API; wall clock with device sync"}
+    del Xh, dsh
+    return {"value": N_total / tbm, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "queries_per_s": nq / tqm,
+            "note": "build_index(Dataset(pinned host f32)) + query_index_batch(host numpy)"
+                    + (" / query_index_batch_sharded" if world > 1 else "") +
+                    " through the public API; wall clock with device sync, max over ranks; bytes per rank"}
 
 
 # ----------------------------------------------------------- reference arm
 
-def cpu_baseline(X, Q, p, args, with_queries=False):
+def cpu_baseline(X, Q, p, args, cfg, reps=1):
     """The oracle port (oracle/ssh_oracle.c, OpenMP over all host threads) on a
-    bounded sample of the same workload."""
-    import numpy as np
-
+    bounded sample of the same workload: build rate over the first
+    --cpu-build-sample series; queries/s of --cpu-queries queries against an
+    oracle index over the first --cpu-query-index series (1M = configs[1]'s
+    full N, so queries/s is a same-N figure)."""
     from oracle import oracle as orc
 
     th = ncores()
-    Xh = X.cpu().numpy() if hasattr(X, "cpu") else np.asarray(X)
+    Xh = X.cpu().numpy() if hasattr(X, "cpu") else X
     n_build = min(Xh.shape[0], args.cpu_build_sample)
     orc.get_tables(p["n"], p["d"] * p["K"], p["seed"], Xh.shape[1])
-    t0 = time.perf_counter()
-    sig = orc.signatures(Xh[:n_build], p["W"], p["delta"], p["n"], p["d"], p["K"], p["seed"], threads=th)
-    csr = orc.tables_from_signatures(sig)
-    tb = time.perf_counter() - t0
-    out = {"value": n_build / tb, "unit": UNIT, "cores": th, "kind": "port",
+    vals = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sig = orc.signatures(Xh[:n_build], p["W"], p["delta"], p["n"], p["d"], p["K"], p["seed"], threads=th)
+        orc.tables_from_signatures(sig)
+        vals.append(n_build / (time.perf_counter() - t0))
+    out = {"value": statistics.median(vals), "unit": UNIT, "cores": th, "kind": "port",
            "sample": f"build_index (K=4 signatures + stable-argsort tables) over the first {n_build} "
-                     f"series of the workload"}
-    if not with_queries:
-        return out
+                     f"series of configs[{cfg}]"}
     n_idx = min(Xh.shape[0], args.cpu_query_index)
+    t0 = time.perf_counter()
     idx = orc.build_index(Xh[:n_idx], p["W"], p["delta"], p["n"], p["d"], p["K"], p["seed"], p["band"],
                           threads=th)
+    t_idx = time.perf_counter() - t0
     nq = min(Q.shape[0], args.cpu_queries)
-    t0 = time.perf_counter()
-    res = orc.query_batch(idx, Q[:nq], K_TOP, threads=th)
-    tq = time.perf_counter() - t0
-    out["queries_per_s"] = nq / tq
-    out["query_sample"] = (f"{nq} queries against an oracle index over {n_idx} series "
-                           f"(mean |R|={float(res['n_cand'].mean()):.0f}); full-N CPU query time not measured")
+    qv = []
+    res = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = orc.query_batch(idx, Q[:nq], K_TOP, threads=th)
+        qv.append(nq / (time.perf_counter() - t0))
+    out["queries_per_s"] = statistics.median(qv)
+    out["query_sample"] = (f"{nq} queries (query_index cascade, one per host thread) against an oracle "
+                           f"index over the first {n_idx} series (mean |R|={float(res['n_cand'].mean()):.0f}; "
+                           f"index build {t_idx:.1f} s = {n_idx / t_idx:.0f} series/s, untimed setup)")
     return out
 
 
 def run_reference(args):
     """--impl reference: the CPU oracle port of the reference path on host cores."""
-    import numpy as np
-
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_1610_07328_b200 import datagen
 
+    cfg = args.cfg if args.cfg != 4 else 1
     dev = "cuda" if _cuda_ok() else "cpu"
-    c = datagen.CONFIGS[args.cfg]
+    c = datagen.CONFIGS[cfg]
     N = min(args.n or c["N"], max(args.cpu_build_sample, args.cpu_query_index))
-    X, Q, src, p = datagen.workload(args.cfg, lo=0, hi=N, device=dev, nq=args.cpu_queries,
+    X, Q, src, p = datagen.workload(cfg, lo=0, hi=N, device=dev, nq=args.cpu_queries,
                                     n_override=(args.n or c["N"]))
     Xh = X.cpu().numpy()
-    vals = []
-    qps = []
-    base = None
+    del X
+    from oracle import oracle as orc
+
+    th = ncores()
+    orc.get_tables(p["n"], p["d"] * p["K"], p["seed"], Xh.shape[1])
+    n_build = min(Xh.shape[0], args.cpu_build_sample)
+    n_idx = min(Xh.shape[0], args.cpu_query_index)
+    t0 = time.perf_counter()
+    idx = orc.build_index(Xh[:n_idx], p["W"], p["delta"], p["n"], p["d"], p["K"], p["seed"], p["band"],
+                          threads=th)
+    t_idx = time.perf_counter() - t0
+    nq = min(Q.shape[0], args.cpu_queries)
+    vals, qps, cands = [], [], []
     for i in range(args.warmup + args.steps):
-        base = cpu_baseline(Xh, Q, p, args, with_queries=(i >= args.warmup))
+        t0 = time.perf_counter()
+        sig = orc.signatures(Xh[:n_build], p["W"], p["delta"], p["n"], p["d"], p["K"], p["seed"], threads=th)
+        orc.tables_from_signatures(sig)
+        tb = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        res = orc.query_batch(idx, Q[:nq], K_TOP, threads=th)
+        tq = time.perf_counter() - t0
         if i >= args.warmup:
-            vals.append(base["value"])
-            qps.append(base.get("queries_per_s"))
+            vals.append(n_build / tb)
+            qps.append(nq / tq)
+            cands.append(float(res["n_cand"].mean()))
     v = statistics.median(vals)
+    sample = (f"each step: build_index (K=4 signatures + stable-argsort tables) over the first {n_build} "
+              f"series, then {nq} queries (query_index cascade, OpenMP over queries) against an oracle index "
+              f"over the first {n_idx} series of configs[{cfg}] (mean |R|={statistics.mean(cands):.0f}; index "
+              f"built once, {t_idx:.1f} s, untimed)")
     out = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-        "data": "synthetic (BASELINE.json configs[%d] recipe, seeded)" % args.cfg,
-        "config": {"workload": f"configs[{args.cfg}] (bounded CPU sample, see cpu_baseline.sample)",
-                   "N": args.n or c["N"], "m": c["m"], "K": 4, "L": 20, "k": K_TOP},
-        "queries_per_s": statistics.median([q for q in qps if q is not None]) if any(qps) else None,
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "port",
-                         "sample": base["sample"], "query_sample": base.get("query_sample")},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic (BASELINE.json configs[%d] recipe, seeded)" % cfg,
+        "config": {"workload": f"configs[{cfg}] (bounded CPU sample, see cpu_baseline.sample)",
+                   "cfg": cfg, "N": args.n or c["N"], "m": c["m"], "K": 4, "L": 20, "k": K_TOP,
+                   "queries": nq, "index_series": n_idx},
+        "queries_per_s": statistics.median(qps),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": th, "kind": "port", "sample": sample,
+                         "queries_per_s": statistics.median(qps)},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "queries_per_s": statistics.median(qps)},
     }
     print(json.dumps(out), flush=True)
 
@@ -501,16 +705,25 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=1)
-    ap.add_argument("--n", type=int, default=None, help="override N per GPU (dev only)")
+    ap.add_argument("--strong", action="store_true", help="shard a fixed N_total (default for --cfg 4)")
+    ap.add_argument("--n", type=int, default=None,
+                    help="override N per GPU (weak) or N_total / GPUs (strong) (dev only)")
     ap.add_argument("--nq", type=int, default=None, help="override query count (dev only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-all", action="store_true", help="e2e for the extra workloads too")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-build-sample", type=int, default=20000)
-    ap.add_argument("--cpu-query-index", type=int, default=100000)
-    ap.add_argument("--cpu-queries", type=int, default=16)
+    ap.add_argument("--no-extra", action="store_true", help="skip the configs[2]/[3] workloads at N=1")
+    ap.add_argument("--extra-steps", type=int, default=2)
+    ap.add_argument("--extra-warmup", type=int, default=3)
+    ap.add_argument("--extra-nq", type=int, default=None)
+    ap.add_argument("--cpu-build-sample", type=int, default=100_000)
+    ap.add_argument("--cpu-query-index", type=int, default=1_000_000)
+    ap.add_argument("--cpu-queries", type=int, default=24)
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference(args)
     else:

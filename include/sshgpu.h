@@ -161,6 +161,13 @@ int ssh_sshi_parse_tables(const uint8_t *buf, int64_t len, int64_t off, int32_t 
                           int64_t *end_off, char *msg, int32_t msg_len);
 int ssh_index_num_buckets(const ssh_index *idx, int table, int64_t *n_buckets);
 int64_t ssh_index_size(const ssh_index *idx);
+/* Sketch statistics of the build that made idx (ssh_build_index /
+ * ssh_build_index_host; zeros for an index built from signatures), copied to
+ * HOST out2[2] after synchronising `stream`: [0] windows whose f32 screen was
+ * undecided and were re-evaluated with the reference's exact f64 sequence,
+ * [1] of those, windows with |dot| < 1e-9 (near-zero sign ties, counted and
+ * reported per BASELINE.json's north star; sign(0) = +1 as sketch.py:60). */
+int ssh_index_sketch_stats(const ssh_index *idx, int64_t *out2, void *stream);
 /* Copy table `table` to HOST arrays: keys u64[nb], offsets i64[nb+1],
  * ids i64[N] (global ids).  The reference's dict view (index.py:151-154). */
 int ssh_index_export(const ssh_index *idx, int table, uint64_t *keys, int64_t *offsets,

@@ -43,6 +43,7 @@ from .index import (
 
 from .dtw import Envelope, build_envelope, dtw_distance, dtw_pairs, lb_keogh, lb_keogh2, lb_kim
 from .srp import ndcg_at_k, precision_at_k, srp_matrix, srp_signature, srp_vectors
+from .dist import query_index_batch_sharded, shard_range
 from .pipeline import extract_subsequences, make_dataset
 from .persist import file_checksum, load_dataset, load_index, read_index_file, save_dataset, save_index
 

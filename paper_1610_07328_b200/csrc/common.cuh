@@ -149,6 +149,9 @@ struct ssh_index {
     // its frees wait on it, so a caller working on any stream can drop the
     // index while its last query is still in flight
     cudaEvent_t last_use = nullptr;
+    // sketch statistics of the build (device i64[2], ssh_build_index*):
+    // [0] windows re-evaluated in exact f64, [1] of those |dot| < 1e-9
+    int64_t *d_sketch_stats = nullptr;
 };
 
 // record ix's last use on `st` (see ssh_index::last_use)

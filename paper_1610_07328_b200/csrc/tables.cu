@@ -814,6 +814,7 @@ extern "C" int ssh_index_destroy(ssh_index *ix) {
     if (ix->d_nb) cudaFreeAsync(ix->d_nb, st);
     if (ix->rec) cudaFreeAsync(ix->rec, st);
     if (ix->codes) cudaFreeAsync(ix->codes, st);
+    if (ix->d_sketch_stats) cudaFreeAsync(ix->d_sketch_stats, st);
     delete[] ix->h_nb;
     delete ix;
     return SSH_OK;
@@ -827,6 +828,17 @@ extern "C" int ssh_index_num_buckets(const ssh_index *ix, int table, int64_t *nb
 }
 
 extern "C" int64_t ssh_index_size(const ssh_index *ix) { return ix ? ix->N : -1; }
+
+extern "C" int ssh_index_sketch_stats(const ssh_index *ix, int64_t *out2, void *stream) {
+    SSH_REQUIRE(ix && out2, SSH_ERR_INVALID, "ssh_index_sketch_stats: NULL argument");
+    out2[0] = out2[1] = 0;
+    if (!ix->d_sketch_stats) return SSH_OK;  // built from signatures: no sketch ran
+    SSH_CUDA(cudaSetDevice(ix->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    SSH_CUDA(cudaMemcpyAsync(out2, ix->d_sketch_stats, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SSH_CUDA(cudaStreamSynchronize(st));
+    return SSH_OK;
+}
 
 extern "C" int ssh_index_export(const ssh_index *ix, int table, uint64_t *keys, int64_t *offsets,
                                 int64_t *ids, void *stream) {
@@ -874,10 +886,18 @@ extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t 
     // pool reuses their memory), then summarise on the side stream
     int rc = ssh_alloc_summaries(ctx, &summ, N, st);
     if (rc) return rc;
+    int64_t *skst = nullptr;  // near-zero sign-tie counters of this build (ssh_index_sketch_stats)
+    if (cudaMallocAsync((void **)&skst, 2 * sizeof(int64_t), st) != cudaSuccess ||
+        cudaMemsetAsync(skst, 0, 2 * sizeof(int64_t), st) != cudaSuccess) {
+        if (skst) cudaFreeAsync(skst, st);
+        cudaFreeAsync(summ.rec, st);
+        cudaFreeAsync(summ.codes, st);
+        return ssh_cuda_fail(cudaErrorMemoryAllocation, "cudaMallocAsync(sketch stats)", __FILE__, __LINE__);
+    }
     // sketch + CWS first (CWS fills every SM), then the summaries on the side
     // stream run alongside the bucket-table sorts (memory-bound kernels with
     // host syncs for the bucket counts between them); joined at the end
-    rc = ssh_launch_sketch(ctx, X, N, ld, bits, nullptr, st);
+    rc = ssh_launch_sketch(ctx, X, N, ld, bits, skst, st);
     if (rc == SSH_OK)
         rc = ssh_launch_shingle_cws(ctx, bits, nullptr, nullptr, nullptr, N, nullptr, nullptr, nullptr,
                                     nullptr, sig, SIG_MODE_FUSED, st);
@@ -891,8 +911,10 @@ extern "C" int ssh_build_index(ssh_ctx *ctx, const float *X, int64_t N, int64_t 
         cudaStreamWaitEvent(st, ctx->ev_join, 0);
         if (summ.rec) cudaFreeAsync(summ.rec, st);
         if (summ.codes) cudaFreeAsync(summ.codes, st);
+        cudaFreeAsync(skst, st);
         return rc;
     }
+    (*out)->d_sketch_stats = skst;
     (*out)->rec = summ.rec;
     (*out)->codes = summ.codes;
     (*out)->seg = summ.seg;
@@ -922,6 +944,14 @@ extern "C" int ssh_build_index_host(ssh_ctx *ctx, const float *X_host, int64_t N
     summ.N = N;
     int rc = ssh_alloc_summaries(ctx, &summ, N, st);
     if (rc) return rc;
+    int64_t *skst = nullptr;
+    if (cudaMallocAsync((void **)&skst, 2 * sizeof(int64_t), st) != cudaSuccess ||
+        cudaMemsetAsync(skst, 0, 2 * sizeof(int64_t), st) != cudaSuccess) {
+        if (skst) cudaFreeAsync(skst, st);
+        cudaFreeAsync(summ.rec, st);
+        cudaFreeAsync(summ.codes, st);
+        return ssh_cuda_fail(cudaErrorMemoryAllocation, "cudaMallocAsync(sketch stats)", __FILE__, __LINE__);
+    }
     // the copy stream may only write X_dev after the caller's prior work on it
     SSH_CUDA(cudaEventRecord(ctx->ev_fork, st));
     SSH_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->ev_fork, 0));
@@ -936,7 +966,7 @@ extern "C" int ssh_build_index_host(ssh_ctx *ctx, const float *X_host, int64_t N
             break;
         }
         const float *Xc = X_dev + r0 * ld;
-        rc = ssh_launch_sketch(ctx, Xc, n, ld, bits, nullptr, st);
+        rc = ssh_launch_sketch(ctx, Xc, n, ld, bits, skst, st);
         if (rc == SSH_OK)
             rc = ssh_launch_shingle_cws(ctx, bits, nullptr, nullptr, nullptr, n, nullptr, nullptr, nullptr,
                                         nullptr, sig_out + r0 * ctx->p.L, SIG_MODE_FUSED, st);
@@ -946,8 +976,10 @@ extern "C" int ssh_build_index_host(ssh_ctx *ctx, const float *X_host, int64_t N
     if (rc != SSH_OK) {
         if (summ.rec) cudaFreeAsync(summ.rec, st);
         if (summ.codes) cudaFreeAsync(summ.codes, st);
+        cudaFreeAsync(skst, st);
         return rc;
     }
+    (*out)->d_sketch_stats = skst;
     (*out)->rec = summ.rec;
     (*out)->codes = summ.codes;
     (*out)->seg = summ.seg;

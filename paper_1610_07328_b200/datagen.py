@@ -122,13 +122,16 @@ def ecg_signal(length: int, seed: int = 4000) -> np.ndarray:
     for off, width, amp in ((-40.0, 10.0, 0.15), (0.0, 4.0, 1.0), (60.0, 16.0, 0.3)):
         amps = amp * (1.0 + rng.uniform(-0.1, 0.1, size=peaks.shape[0]))
         span = int(4 * width)
-        for centre, a in zip(peaks + off, amps):
-            c = int(round(centre))
-            lo, hi = max(0, c - span), min(length, c + span + 1)
-            if lo >= hi:
-                continue
-            tt = t[lo:hi] - centre
-            x[lo:hi] += a * np.exp(-0.5 * (tt / width) ** 2)
+        centres = peaks + off
+        c = np.rint(centres).astype(np.int64)  # round-half-even, as Python's round()
+        # one offset from the bump centre at a time over all beats: beats are
+        # >= 180 samples apart and a bump spans <= 129, so the positions of one
+        # offset are distinct and each sample gets at most one term per bump type
+        for d in range(-span, span + 1):
+            pos = c + d
+            ok = (pos >= 0) & (pos < length)
+            pk = pos[ok]
+            x[pk] += amps[ok] * np.exp(-0.5 * ((pk - centres[ok]) / width) ** 2)
     return x
 
 
@@ -162,7 +165,15 @@ def workload(cfg: int, lo: int = 0, hi: int | None = None, device="cuda", nq: in
         stride = c["stride"]
         total = (N - 1) * stride + m
         sig = ecg_signal(total + 200_000, seed=4000)
-        X = torch.from_numpy(ecg_windows(sig[:total], m, stride, N)[lo:hi]).to(device)
+        rec = sig[lo * stride:(hi - 1) * stride + m]
+        if torch.device(device).type == "cuda":
+            # windows + per-window z-normalisation on the device (ssh_windows:
+            # numpy's pairwise float64 mean/std bit for bit, then f32)
+            from .pipeline import make_dataset
+
+            X = make_dataset(rec, m, stride=stride, device=torch.device(device).index or 0).values
+        else:
+            X = torch.from_numpy(ecg_windows(rec, m, stride, hi - lo))
         held = sig[total:]
         rng = np.random.default_rng(2000 + cfg)
         starts = rng.integers(0, held.shape[0] - m, size=nq)

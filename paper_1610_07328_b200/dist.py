@@ -84,6 +84,12 @@ def merge_across_ranks(ids, d2, n_cand, counters, k: int, group=None):
     world = dist.get_world_size(group)
     if world == 1:
         return ids, d2, n_cand, counters
+    if ids.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo collectives run on host tensors (functional tests of the sharded
+        # path on one GPU); NCCL takes the device tensors directly
+        dev = ids.device
+        out = merge_across_ranks(ids.cpu(), d2.cpu(), n_cand.cpu(), counters.cpu(), k, group)
+        return tuple(t.to(dev) for t in out)
     nq = ids.shape[0]
     g_ids = torch.empty((world * nq, k), dtype=ids.dtype, device=ids.device)
     g_d2 = torch.empty((world * nq, k), dtype=d2.dtype, device=d2.device)
@@ -153,3 +159,56 @@ def index_query_fns(index):
         return query_batch_device(index, Q, k, False, exact=True)
 
     return local, exact
+
+
+def _pad_k(t, k: int, fill):
+    torch = _torch()
+    if t.shape[1] == k:
+        return t
+    pad = torch.full((t.shape[0], k - t.shape[1]), fill, dtype=t.dtype, device=t.device)
+    return torch.cat([t, pad], dim=1)
+
+
+def query_index_batch_sharded(index, Q, k: int, fallback_on_empty: bool = False, group=None) -> list:
+    """query_index_batch (index.py:204-273) over a series-sharded index: every
+    rank of `group` calls it with its own shard (an SshIndex built with
+    id_base = the shard's first global id) and the same queries, and every
+    rank gets the same list of QueryResult — the exact top-k of the union
+    R = U_g R_g, |R| summed, statuses and the empty-R fallback decided over
+    R (sharded_query).  k is clamped to the total series count, with the
+    reference's warning."""
+    import time
+
+    import torch.distributed as dist
+
+    from .index import _prepare_queries, _results_from_arrays, _to_host
+
+    torch = _torch()
+    Qd = _prepare_queries(index, Q)
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    gloo = dist.get_backend(group) == "gloo"
+    n_tot = torch.tensor([index.n_series], dtype=torch.int64, device="cpu" if gloo else Qd.device)
+    dist.all_reduce(n_tot, op=dist.ReduceOp.SUM, group=group)
+    N = int(n_tot.item())
+    warning = None
+    if k > N:
+        warning = f"k={k} exceeds index size {N}; returning at most {N} series"
+        k = N
+    kl = min(k, index.n_series)
+    local_fn, exact_fn = index_query_fns(index)
+
+    def local(Qs, _k):
+        ids, d2, n_out, nc, cnt, st = local_fn(Qs, kl)
+        return _pad_k(ids, k, -1), _pad_k(d2, k, float("inf")), n_out, nc, cnt, st
+
+    def exact(Qs, _k):
+        ids, d2, n_out, nc, cnt, st = exact_fn(Qs, kl)
+        return _pad_k(ids, k, -1), _pad_k(d2, k, float("inf")), n_out, nc, cnt, st
+
+    t0 = time.perf_counter()
+    with index.context().use():
+        dev = sharded_query(Qd, k, local, exact, fallback_on_empty, group=group)
+        ids, d2, n_out, n_cand, counters, status = _to_host(dev, index.device)
+    dt = time.perf_counter() - t0
+    return _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N, dt, warning)

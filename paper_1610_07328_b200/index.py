@@ -406,6 +406,17 @@ class SshIndex:
     def context(self) -> DeviceContext:
         return get_context(self.device, self.params, self.length)
 
+    @property
+    def sketch_stats(self) -> dict:
+        """Sketch windows of this build whose f32 screen was undecided and that
+        were re-evaluated with the reference's exact f64 dot ("rechecked"), and
+        of those the near-zero sign ties |dot| < 1e-9 ("near_zero"; sign(0) is
+        +1 as in sketch.py:60).  Zeros for an index built from signatures."""
+        out = np.zeros(2, dtype=np.int64)
+        nat.check(nat.lib().ssh_index_sketch_stats(self._tables.handle, nat.ptr(out), _stream_ptr(self.device)),
+                  "ssh_index_sketch_stats")
+        return {"rechecked": int(out[0]), "near_zero": int(out[1])}
+
 
 def _check_params_length(params: SshParams, m: int):
     params.validate_for_length(m)
@@ -709,8 +720,9 @@ def _results_from_arrays(ids, d2, n_out, n_cand, counters, status, N: int, dt: f
     return out
 
 
-def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = False) -> list:
-    """query_index for every row of Q (nq, m) in one device batch."""
+def _prepare_queries(index: SshIndex, Q):
+    """Q (numpy / torch, (nq, m) or (m,)) -> contiguous f32 device tensor, with
+    the reference's validation (index.py:213-216)."""
     if _is_torch(Q):
         Qd = Q.to(device=f"cuda:{index.device}", dtype=_torch().float32).contiguous()
         if Qd.ndim == 1:
@@ -726,19 +738,30 @@ def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = Fals
         Qd = _as_device_f32(Qh, index.device)
     if Qd.shape[1] != index.length:
         raise ValueError(f"query length {Qd.shape[1]} does not match indexed length {index.length}")
+    return Qd
+
+
+def _to_host(dev, device: int):
+    """Pinned non-blocking copies of device result tensors, one synchronisation."""
+    torch = _torch()
+    host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev]
+    for h, t in zip(host, dev):
+        h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(device).synchronize()
+    return [h.numpy() for h in host]
+
+
+def query_index_batch(index: SshIndex, Q, k: int, fallback_on_empty: bool = False) -> list:
+    """query_index for every row of Q (nq, m) in one device batch."""
+    Qd = _prepare_queries(index, Q)
     k, warning = _validate_k(index, k)
     t0 = time.perf_counter()
-    torch = _torch()
     phase = [0.0, 0.0, 0.0]
     # the whole batch (launches, result copies, phase clock) holds the context
     with index.context().use():
         dev = query_batch_device(index, Qd, k, fallback_on_empty, phase_ms=phase)
         # one synchronisation for the six result arrays (pinned, non-blocking copies)
-        host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev]
-        for h, t in zip(host, dev):
-            h.copy_(t, non_blocking=True)
-        torch.cuda.current_stream(index.device).synchronize()
-    ids, d2, n_out, n_cand, counters, status = (h.numpy() for h in host)
+        ids, d2, n_out, n_cand, counters, status = _to_host(dev, index.device)
     dt = time.perf_counter() - t0
     return _results_from_arrays(ids, d2, n_out, n_cand, counters, status, index.n_series, dt, warning,
                                 phase_ms=phase)

@@ -197,3 +197,71 @@ def test_shard_save_load_round_trip(cuda, tmp_path):
     b = ssh.query_index_batch(back, Q[:4], 10)
     assert [r.ids for r in a] == [r.ids for r in b] and all(min(r.ids) >= lo for r in a if r.ids)
     assert [r.distances for r in a] == [r.distances for r in b]
+
+
+def _sharded_worker(rank, world, port, band, out_path):
+    """One rank of test_query_index_batch_sharded_two_processes (gloo, cuda:0)."""
+    import os
+    import pickle
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1610_07328_b200 as ssh
+    from fixture_data import case_data as cd
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    X, Q, _, _ = cd("rw1024")
+    rng = np.random.default_rng(9)
+    noise = rng.standard_normal((2, X.shape[1]))
+    noise = ((noise - noise.mean(1, keepdims=True)) / noise.std(1, keepdims=True)).astype(np.float32)
+    Qs = np.ascontiguousarray(np.concatenate([Q, noise]), dtype=np.float32)
+    lo, hi = ssh.shard_range(X.shape[0], rank, world)
+    idx = ssh.build_index(ssh.Dataset(torch.from_numpy(X[lo:hi]).cuda()), _params(band), id_base=lo)
+    got = {}
+    for fb in (False, True):
+        res = ssh.query_index_batch_sharded(idx, Qs, 10, fallback_on_empty=fb)
+        got[fb] = [(r.ids, r.distances, r.status, r.stats.candidates, r.stats.n_indexed) for r in res]
+    big = ssh.query_index_batch_sharded(idx, Qs[:2], X.shape[0] + 5)
+    got["big"] = [(r.ids, r.warning) for r in big]
+    if rank == 0:
+        with open(out_path, "wb") as f:
+            pickle.dump(got, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_query_index_batch_sharded_two_processes(cuda, tmp_path):
+    """The public sharded API with two real ranks (two processes on cuda:0
+    over gloo; functional, not a performance claim): every status, id list,
+    distance and |R| equals the single-index query_index_batch, with and
+    without the empty-R fallback, and k > N_total clamps with the warning."""
+    import pickle
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_1610_07328_b200 as ssh
+
+    X, Q, _, band = case_data("rw1024")
+    rng = np.random.default_rng(9)
+    noise = rng.standard_normal((2, X.shape[1]))
+    noise = ((noise - noise.mean(1, keepdims=True)) / noise.std(1, keepdims=True)).astype(np.float32)
+    Qs = np.ascontiguousarray(np.concatenate([Q, noise]), dtype=np.float32)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "sharded.pkl"
+    mp.spawn(_sharded_worker, args=(2, port, band, str(out)), nprocs=2, join=True)
+    got = pickle.loads(out.read_bytes())
+    idx = ssh.build_index(ssh.Dataset(torch.from_numpy(X).cuda()), _params(band))
+    for fb in (False, True):
+        want = [(r.ids, r.distances, r.status, r.stats.candidates, r.stats.n_indexed)
+                for r in ssh.query_index_batch(idx, Qs, 10, fallback_on_empty=fb)]
+        assert got[fb] == want
+    assert any(w[2] == "no-candidates" for w in got[False]) and any(w[2] == "fallback" for w in got[True])
+    big = ssh.query_index_batch(idx, Qs[:2], X.shape[0] + 5)
+    assert got["big"] == [(r.ids, r.warning) for r in big]

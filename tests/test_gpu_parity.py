@@ -97,6 +97,28 @@ def test_sketch_recheck_near_zero(cuda):
     assert int(stats[1]) == int((np.abs(dots) < 1e-9).sum())
 
 
+@pytest.mark.parametrize("host", [False, True])
+def test_build_index_reports_near_zero_ties(cuda, host):
+    """The product build (device and host-input paths) counts the windows it
+    re-evaluated in f64 and the near-zero sign ties |dot| < 1e-9 among them
+    (BASELINE.json north star: 'counted and reported')."""
+    import torch
+
+    import paper_1610_07328_b200 as ssh
+
+    m = 512
+    rng = np.random.default_rng(5)
+    X = np.zeros((300, m), dtype=np.float32)
+    X[1:100] = rng.standard_normal((99, m)).astype(np.float32)
+    X[100:] = rng.integers(-2, 3, size=(200, m)).astype(np.float32)
+    vals = X if host else torch.from_numpy(X).cuda()
+    index = ssh.build_index(ssh.Dataset(vals), params(0.05))
+    _, dots = O.sketch_matrix(X, O.make_filter(80, 0), 3, return_dots=True)
+    st = index.sketch_stats
+    assert st["near_zero"] == int((np.abs(dots) < 1e-9).sum()) > 0
+    assert st["rechecked"] >= st["near_zero"]
+
+
 @pytest.mark.parametrize("m", [512, 1024, 2048])
 def test_sketch_stream_ring_partial_tile(cuda, m):
     """TMA-staged sketch kernel: enough series that every CTA wraps its stage
