@@ -168,6 +168,15 @@ int64_t ssh_index_size(const ssh_index *idx);
  * [1] of those, windows with |dot| < 1e-9 (near-zero sign ties, counted and
  * reported per BASELINE.json's north star; sign(0) = +1 as sketch.py:60). */
 int ssh_index_sketch_stats(const ssh_index *idx, int64_t *out2, void *stream);
+/* Cross-shard top-k merge (multi-GPU query): the exact
+ * global top-k_out of a series-sharded index from the per-shard lists.
+ * ids i64 / d2 f64 [lists][nq][k_in] (device; the all_gather layout), each
+ * list sorted by (d2, id) and padded with id -1 / d2 +inf; out_ids /
+ * out_d2 [nq][k_out] and n_out[nq] (may be NULL) on the device.  Order:
+ * (d2, id) lexicographic, as the reference's final lexsort (index.py:249).
+ * lists <= 32.  Replaces the per-query sort of the merged lists. */
+int ssh_merge_topk(const int64_t *ids, const double *d2, int32_t nq, int32_t lists, int32_t k_in,
+                   int32_t k_out, int64_t *out_ids, double *out_d2, int32_t *n_out, void *stream);
 /* Copy table `table` to HOST arrays: keys u64[nb], offsets i64[nb+1],
  * ids i64[N] (global ids).  The reference's dict view (index.py:151-154). */
 int ssh_index_export(const ssh_index *idx, int table, uint64_t *keys, int64_t *offsets,

@@ -20,7 +20,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB_PATH = Path(os.environ["SSH_LIB_PATH"]).resolve() if os.environ.get("SSH_LIB_PATH") else PKG / "libsshgpu.so"
-SOURCES = ["ctx.cu", "sketch.cu", "signature.cu", "tables.cu", "query.cu", "persist.cu", "windows.cu", "srp.cu", "pairs.cu"]
+SOURCES = ["ctx.cu", "sketch.cu", "signature.cu", "tables.cu", "query.cu", "persist.cu", "windows.cu", "srp.cu", "pairs.cu",
+           "merge.cu"]
 
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
@@ -122,6 +123,7 @@ def lib():
             "ssh_index_num_buckets": ([P, ctypes.c_int, ctypes.POINTER(i64)], ctypes.c_int),
             "ssh_index_size": ([P], i64),
             "ssh_index_sketch_stats": ([P, P, P], ctypes.c_int),
+            "ssh_merge_topk": ([P, P, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
             "ssh_index_export": ([P, ctypes.c_int, P, P, P, P], ctypes.c_int),
             "ssh_probe": ([P, P, P, i32, P, P, P], ctypes.c_int),
             "ssh_index_summarize": ([P, P, P, i64, P], ctypes.c_int),
@@ -153,7 +155,7 @@ EXPORTED = [
     "ssh_ctx_profile", "ssh_ctx_create", "ssh_ctx_destroy", "ssh_ctx_set_params",
     "ssh_num_sketch_bits", "ssh_sketch_words", "ssh_tokens_per_series", "ssh_sketch", "ssh_shingle",
     "ssh_cws", "ssh_signatures", "ssh_index_build", "ssh_build_index", "ssh_build_index_host", "ssh_index_destroy", "ssh_index_num_buckets",
-    "ssh_index_size", "ssh_index_sketch_stats", "ssh_index_export", "ssh_index_summarize", "ssh_index_copy_summaries", "ssh_probe", "ssh_query_batch", "ssh_dtw_exact",
+    "ssh_index_size", "ssh_index_sketch_stats", "ssh_merge_topk", "ssh_index_export", "ssh_index_summarize", "ssh_index_copy_summaries", "ssh_probe", "ssh_query_batch", "ssh_dtw_exact",
     "ssh_query_phase_ms", "ssh_dtw_pairs64", "ssh_envelope64", "ssh_lb_keogh64", "ssh_lb_kim64",
     "ssh_index_create_bare", "ssh_sshi_parse_tables", "ssh_windows", "ssh_srp",
 ]

@@ -1708,6 +1708,305 @@ dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restr
     if (cells && lane == 0 && my_cells) atomicAdd(cells, my_cells);
 }
 
+// Wide-band wave DTW, paired form: the warp wavefront above with 64 VIRTUAL
+// lanes, two per physical lane, so every cell update is half of an f32x2 pair.
+// Virtual lane v owns the C2 band offsets k = v C2 + c and sweeps row s - v at
+// step s; physical lane l hosts A = virtual 2l (row s - 2l) and B = virtual
+// 2l + 1 (row s - 2l - 1, offsets right after A's), pair c = {A_c, B_c}.  In
+// one step, ascending c, A_c and B_c update together:
+//   A_c = d_A^2 + min(A_c, A_{c+1} | B_0 (new), A_{c-1} (new) | lane l-1's
+//         B_{C2-1} from the previous step (shfl_up; +inf on lane 0))
+//   B_c = d_B^2 + min(B_c, B_{c+1} | lane l+1's new A_0 (shfl_down after pair
+//         0; +inf on lane 31), B_{c-1} (new) | A_{C2-1} from the previous step)
+// d = {x_A, x_B} + {-y_A, -y_B} is one FADD2 and the cells one FFMA2 per pair
+// (the same IEEE operations as the scalar fmaf(d, d, min3) recurrence), so a
+// cell costs half an FADD2, half an FFMA2 and one FMNMX3.  Query samples are a
+// sliding register window of 2 C2 - 1 negated samples held as pairs
+// {Y[c], Y[c + C2 - 1]} (pair c serves A_c and B_c); one new sample per step
+// comes from lane l + 1 (lane 31: the staged query).  x_B is the previous
+// step's x_A.  Abandon: the skewed-cut cumulative bound of dtw32w_kernel with
+// 64 virtual lanes (virtual lane 0 holds row s).
+#ifndef DV_WARPS
+#define DV_WARPS 8
+#endif
+#ifndef DV_MINB
+#define DV_MINB 2
+#endif
+// f32x2 helpers on packed 64-bit registers (the PTX f32x2 operand type), so
+// the query-window pairs stay register pairs across the window rotation
+__device__ __forceinline__ unsigned long long dv_pack(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float dv_hi(unsigned long long v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return hi;
+}
+__device__ __forceinline__ float dv_lo(unsigned long long v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return lo;
+}
+__device__ __forceinline__ unsigned long long dv_add2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float2 dv_sqadd2(unsigned long long d, float mA, float mB) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(d), "l"(dv_pack(mA, mB)));
+    float2 o;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+    return o;
+}
+
+// window: NY[(U + c) % C2] = {-Y[c], -Y[c + C2 - 1]} (pair c serves A_c and B_c)
+template <int C2, int U, bool MASK>
+__device__ __forceinline__ void dv_step(float2 (&P)[C2], unsigned long long (&NY)[C2], float &xb, const float xa,
+                                        const int iA, const int lane, const int olane, const int ocomp,
+                                        const int cst, const float y31) {
+    const float inf = INFINITY;
+    float lA = __shfl_up_sync(0xFFFFFFFFu, P[C2 - 1].y, 1);  // lane l-1's B_{C2-1}, previous step
+    if (lane == 0) lA = inf;
+    const float lB = P[C2 - 1].x;                           // own A_{C2-1}, previous step
+    const unsigned long long XP = dv_pack(xa, xb);
+    const bool actA = !MASK || iA >= 0, actB = !MASK || iA >= 1;
+    float upr = inf;
+#pragma unroll
+    for (int c = 0; c < C2; c++) {
+        const float2 old = P[c];
+        const float upA = (c + 1 < C2) ? P[c + 1].x : P[0].y;
+        const float upB = (c + 1 < C2) ? P[c + 1].y : upr;
+        const float leftA = c == 0 ? lA : P[c - 1].x;
+        const float leftB = c == 0 ? lB : P[c - 1].y;
+        const float mA = fminf(fminf(old.x, upA), leftA);
+        const float mB = fminf(fminf(old.y, upB), leftB);
+        float2 v = dv_sqadd2(dv_add2(XP, NY[(U + c) % C2]), mA, mB);
+        if (c == cst && lane == olane) {  // first out-of-band offset k = 2r + 1 stays +inf
+            if (ocomp) v.y = inf;
+            else v.x = inf;
+        }
+        if (MASK) {
+            v.x = actA ? v.x : old.x;
+            v.y = actB ? v.y : old.y;
+        }
+        P[c] = v;
+        if (c == 0) {
+            upr = __shfl_down_sync(0xFFFFFFFFu, v.x, 1);
+            if (lane == 31) upr = inf;
+        }
+    }
+    xb = xa;
+    // slide: pair 0 expires; the new last pair is {Y[C2] (own pair 1's high
+    // half), Y[2 C2 - 1] (lane l + 1's Y[1] = its pair 1's low half)}
+    float yn = __shfl_down_sync(0xFFFFFFFFu, dv_lo(NY[(U + 1) % C2]), 1);
+    if (lane == 31) yn = y31;
+    NY[U % C2] = dv_pack(dv_hi(NY[(U + 1) % C2]), yn);
+}
+
+// C2 steps from s0 (window phase 0): MASK during ramp-up; CHECK: some lane's
+// row index lies outside [0, m)
+template <int C2, int U, bool MASK, bool CHECK>
+__device__ __forceinline__ void dv_group(float2 (&P)[C2], unsigned long long (&NY)[C2], float &xb,
+                                         const float *__restrict__ xg, const float *nyb, const int s0,
+                                         const int lane, const int olane, const int ocomp, const int cst,
+                                         const int rlane, const int rcomp, const int rcc, const int m, float &res) {
+    if constexpr (U < C2) {
+        const int iA = s0 + U - 2 * lane;
+        float xa;
+        if (CHECK) xa = (unsigned)iA < (unsigned)m ? __ldg(xg + U) : 0.f;
+        else xa = __ldg(xg + U);
+        dv_step<C2, U, MASK>(P, NY, xb, xa, iA, lane, olane, ocomp, cst, nyb[U]);
+        if (CHECK && lane == rlane && iA - rcomp == m - 1) {
+#pragma unroll
+            for (int c = 0; c < C2; c++)
+                if (c == rcc) res = rcomp ? P[c].y : P[c].x;
+        }
+        dv_group<C2, U + 1, MASK, CHECK>(P, NY, xb, xg, nyb, s0, lane, olane, ocomp, cst, rlane, rcomp, rcc, m,
+                                         res);
+    }
+}
+
+template <int C2, int RF>
+__global__ void __launch_bounds__(32 * DV_WARPS, DV_MINB)
+dtw32v_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restrict__ Q,
+              const float *__restrict__ U, const float *__restrict__ Lo, DtwList L,
+              const float *__restrict__ thr, unsigned long long *__restrict__ cells) {
+    const int r = RF >= 0 ? RF : r_rt;
+    const int nk = 2 * r + 1;
+    const int ov = nk / C2, cst = nk - ov * C2;  // cell k = nk (forced +inf): virtual lane ov, pair cst
+    const int olane = ov < 64 ? ov >> 1 : -1, ocomp = ov & 1;
+    const int rv = r / C2, rcc = r - rv * C2;    // result cell k = r
+    const int rlane = rv >> 1, rcomp = rv & 1;
+    constexpr int GS = C2;                       // steps per group (one window rotation)
+    const int NS = m + 63;                       // steps: virtual lane 63 finishes row m - 1 at m + 62
+    const int G = (NS + GS - 1) / GS;            // step groups
+    const int YP = (r + m + 64 * C2 + 2 * GS + 64 + 3) & ~3;
+    extern __shared__ __align__(16) float vsm[];
+    float *nyq = vsm;         // nyq[j + r] = -y[j], -inf outside [0, m)
+    float *su = nyq + YP;     // query envelope
+    float *sl = su + m;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float *pre = sl + m + (size_t)w * (G + 1);  // prefix of LB_Keogh terms at group ends
+    const int q = L.act ? L.act[blockIdx.y] : blockIdx.y;
+    const int slot = blockIdx.y;
+    int start, end;
+    dtw_list_range(L, slot, start, end);
+    if (start + (int)blockIdx.x * DV_WARPS >= end) return;  // block-uniform
+    const float *y = Q + (int64_t)q * m;
+    for (int t = threadIdx.x; t < YP; t += blockDim.x) {
+        const int j = t - r;
+        nyq[t] = (j >= 0 && j < m) ? -y[j] : -INFINITY;
+    }
+    const float T = thr ? thr[q] : INFINITY;
+    const bool cb = !isinf(T) && U != nullptr;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        su[i] = cb ? U[(int64_t)q * m + i] : INFINITY;
+        sl[i] = cb ? Lo[(int64_t)q * m + i] : -INFINITY;
+    }
+    __syncthreads();
+    const float inf = INFINITY;
+    const int f_lo = r / C2, f_hi = m - 1 + r / C2;  // cut steps every path crosses
+    // groups [g_main0, g_main1): every virtual lane's row in [0, m - 1)
+    const int g_main0 = (63 + GS - 1) / GS, g_main1 = max(g_main0, (m - 1) / GS);
+    const bool vec = (m & 3) == 0;
+    unsigned long long my_cells = 0;
+    for (int e = start + (int)blockIdx.x * DV_WARPS + w; e < end; e += (int)gridDim.x * DV_WARPS) {
+        const uint32_t row = L.rows[(int64_t)slot * L.stride + e];
+        const bool valid = row != 0xFFFFFFFFu && (!L.lbs || !(L.lbs[(int64_t)slot * L.stride + e] > T));
+        if (!valid) {  // warp-uniform
+            if (lane == 0) L.out[(int64_t)slot * L.stride + e] = inf;
+            continue;
+        }
+        if (L.computed && lane == 0) atomicAdd(&L.computed[q], 1);
+        const float *x = X + (int64_t)row * m;
+        __syncwarp();
+        // prefix sums of the LB_Keogh terms (exact x vs the query envelope) at
+        // the group-end steps s = (g + 1) C2 - 1 (rows >= m add nothing)
+        float carry = 0.f;
+        if (vec) {
+#pragma unroll 4
+            for (int i0 = 0; i0 < G * GS; i0 += 128) {
+                const int i = i0 + 4 * lane;
+                float v2[4] = {0.f, 0.f, 0.f, 0.f};
+                if (i < m) {
+                    const float4 xv = __ldg(reinterpret_cast<const float4 *>(x + i));
+                    const float4 uv = *reinterpret_cast<const float4 *>(su + i);
+                    const float4 lv = *reinterpret_cast<const float4 *>(sl + i);
+                    const float xa[4] = {xv.x, xv.y, xv.z, xv.w};
+                    const float ua[4] = {uv.x, uv.y, uv.z, uv.w};
+                    const float la[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        const float v = fmaxf(fmaxf(xa[t] - ua[t], la[t] - xa[t]), 0.f);
+                        v2[t] = v * v;
+                    }
+                }
+                v2[1] += v2[0];
+                v2[2] += v2[1];
+                v2[3] += v2[2];
+                float sc = v2[3];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float t = __shfl_up_sync(0xFFFFFFFFu, sc, o);
+                    if (lane >= o) sc += t;
+                }
+                const float base = carry + sc - v2[3];
+#pragma unroll
+                for (int t = 0; t < 4; t++)
+                    if ((i + t + 1) % GS == 0 && i + t < G * GS) pre[(i + t + 1) / GS - 1] = base + v2[t];
+                carry = __shfl_sync(0xFFFFFFFFu, carry + sc, 31);
+            }
+        } else {
+            for (int i0 = 0; i0 < G * GS; i0 += 32) {
+                const int i = i0 + lane;
+                float v2 = 0.f;
+                if (i < m) {
+                    const float xv = __ldg(x + i);
+                    const float v = fmaxf(fmaxf(xv - su[i], sl[i] - xv), 0.f);
+                    v2 = v * v;
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float t = __shfl_up_sync(0xFFFFFFFFu, v2, o);
+                    if (lane >= o) v2 += t;
+                }
+                const float P0 = carry + v2;
+                if ((i + 1) % GS == 0) pre[(i + 1) / GS - 1] = P0;
+                carry = __shfl_sync(0xFFFFFFFFu, P0, 31);
+            }
+        }
+        const float total = carry;
+        const float slack = total * (float)(2 * m + 8) * U32_EPS;
+        __syncwarp();
+        float2 P[C2];
+        unsigned long long NY[C2];
+        float xb = 0.f;
+        const int wy = 2 * lane * (C2 - 1);  // nyq index of Y[0] at step 0
+#pragma unroll
+        for (int c = 0; c < C2; c++) {
+            // virtual row -1: 0 at k = r (D(0, 0) = d(0, 0)), +inf elsewhere
+            P[c] = make_float2((2 * lane * C2 + c == r) ? 0.f : inf, ((2 * lane + 1) * C2 + c == r) ? 0.f : inf);
+            NY[c] = dv_pack(nyq[wy + c], nyq[wy + c + C2 - 1]);
+        }
+        const float *xl = x - 2 * lane;
+        float res = inf;
+        bool dead = false;
+        int g = 0;
+        for (; g < G; g++) {
+            const int s0 = g * GS;
+            // lane 31's new sample when sliding after step s: Y_31[2 C2 - 1] = nyq[s + 64 C2 - 63]
+            const float *nyb = nyq + s0 + 64 * C2 - 63;
+            const float *xg = xl + s0;
+            if (g < g_main0)
+                dv_group<C2, 0, true, true>(P, NY, xb, xg, nyb, s0, lane, olane, ocomp, cst, rlane, rcomp, rcc, m,
+                                            res);
+            else if (g < g_main1)
+                dv_group<C2, 0, false, false>(P, NY, xb, xg, nyb, s0, lane, olane, ocomp, cst, rlane, rcomp, rcc,
+                                              m, res);
+            else
+                dv_group<C2, 0, false, true>(P, NY, xb, xg, nyb, s0, lane, olane, ocomp, cst, rlane, rcomp, rcc, m,
+                                             res);
+            // cut test after step s = s0 + GS - 1
+            const int s = s0 + GS - 1;
+            if (cb && s >= f_lo && s <= f_hi) {
+                const int iA = s - 2 * lane;
+                const bool okA = iA >= 0 && iA < m, okB = iA >= 1 && iA <= m;
+                float cm = inf;
+#pragma unroll
+                for (int c = 0; c < C2; c++) cm = fminf(fminf(cm, okA ? P[c].x : inf), okB ? P[c].y : inf);
+                const unsigned cmb = __reduce_min_sync(0xFFFFFFFFu, __float_as_uint(cm));
+                const float remk = fmaxf(total - pre[g] - slack, 0.f);
+                if (__uint_as_float(cmb) + remk > T) {
+                    dead = true;
+                    break;
+                }
+            }
+        }
+        res = __shfl_sync(0xFFFFFFFFu, res, rlane);
+        if (lane == 0) {
+            L.out[(int64_t)slot * L.stride + e] = dead ? inf : res;
+            if (dead && L.abandoned) atomicAdd(&L.abandoned[q], 1ULL);
+        }
+        if (cells) {
+            // in-band cells of the rows virtual lane 63 completed
+            const long long rows = dead ? (long long)min(m, max(0, (g + 1) * GS - 63)) : (long long)m;
+            long long c = rows * nk;
+            const long long a = min(rows, (long long)r);  // rows i < r lose r - i cells
+            c -= a * r - a * (a - 1) / 2;
+            const long long b0 = max(0LL, (long long)(m - r));  // rows i >= m - r lose i + r - m + 1
+            if (rows > b0) {
+                const long long nb = rows - b0;
+                c -= nb * (b0 + r - m + 1) + nb * (nb - 1) / 2;
+            }
+            my_cells += (unsigned long long)c;
+        }
+    }
+    if (cells && lane == 0 && my_cells) atomicAdd(cells, my_cells);
+}
+
 // Register-resident band (radius R compile-time): band[k], k = j - i + R, lives
 // in registers and is updated in place k-ascending (diag = old band[k], up =
 // old band[k+1], left = new band[k-1]).  The query is staged in 4 copies
@@ -1887,10 +2186,20 @@ struct DtwCommon {
 #ifndef DTWP_MINB
 #define DTWP_MINB 1
 #endif
+#ifndef DTWP_BLOCKCUT
+#define DTWP_BLOCKCUT 1  // one cut test per 4-row block on the band minimum (else per row)
+#endif
 #define DP_MAXPASS 64  // longest pooled row pass
 #ifndef SSH_DTW_PASS_DOUBLING
 #define SSH_DTW_PASS_DOUBLING 0
 #endif
+
+// in-band cells (0 <= j < m, |i - j| <= R) of rows [i0, i0 + n) (profiling counters)
+__device__ __forceinline__ unsigned long long dtw_band_cells(int i0, int n, int R, int m) {
+    unsigned long long c = 0;
+    for (int i = i0; i < i0 + n && i < m; i++) c += (unsigned long long)(min(m - 1, i + R) - max(0, i - R) + 1);
+    return c;
+}
 
 // rows [a, b) of one lane's candidate; returns whether it is still alive
 template <int R>
@@ -1907,7 +2216,7 @@ __device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t ro
     float4 xn = alive ? __ldg(xp + (a >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i0 = a; i0 < b; i0 += 4) {
         if (!__any_sync(0xFFFFFFFFu, alive)) break;
-        cal += alive ? 4 * NB : 0;
+        if (alive && C.cells) cal += dtw_band_cells(i0, 4, R, m);  // in-band cells of rows i0 .. i0 + 3
         cex += 4 * NB;
         const float4 xc = xn;
         if (i0 + 4 < b && alive) xn = __ldg(xp + (i0 >> 2) + 1);
@@ -1925,19 +2234,27 @@ __device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t ro
         // d = fma(y, -1, x) = x - y and cv = fma(d, d, min3) are the same IEEE
         // operations as the scalar recurrence (in-place band: row u + 1 reads
         // offsets k - 2, k - 1 that row u wrote one and two steps earlier).
-        // Row minima fold two cells per FMNMX3.
+        // Rows (1, 0) take the query pair {y_(t-1), y_t}, rows (3, 2) {y_(t-3), y_(t-2)}.
+        // No per-cell row minimum: after the block the band IS row i0 + 3, and
+        // its minimum feeds one cut test per block (below).
         constexpr int NSTEP = NB + 6;
         const float2 xp01 = make_float2(xr[1], xr[0]), xp23 = make_float2(xr[3], xr[2]);
         const float2 neg1 = make_float2(-1.f, -1.f);
         float yw[NSTEP + 4];
+        const float4 *yp4 = reinterpret_cast<const float4 *>(yq + i0);
+#if !DTWP_BLOCKCUT
         float cvp[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-        const float4 *yp = reinterpret_cast<const float4 *>(yq + i0);
+#endif
 #pragma unroll
         for (int t = 0; t < NSTEP; t++) {
+            // query samples: one 16-byte load per 4 steps (per-sample 8-byte pair
+            // loads from a pre-paired copy measured 1.2-1.8x slower: L1-bound)
             if ((t & 3) == 0 && t < NB + 3) {
-                const float4 v = __ldg(yp + (t >> 2));
+                const float4 v = __ldg(yp4 + (t >> 2));
                 yw[t] = v.x; yw[t + 1] = v.y; yw[t + 2] = v.z; yw[t + 3] = v.w;
             }
+            const float2 ypr[2] = {make_float2(t >= 1 ? yw[t - 1] : 0.f, yw[t]),
+                                   make_float2(t >= 3 ? yw[t - 3] : 0.f, t >= 2 ? yw[t - 2] : 0.f)};
             float cvs[4];
             bool val[4];
 #pragma unroll
@@ -1950,7 +2267,7 @@ __device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t ro
                     const float upa = (ka + 1 < NB) ? band[ka + 1] : INFINITY;
                     const float ma = fminf(fminf(band[ka], upa), lft[ua]);
                     const float mb = fminf(fminf(band[kb], band[kb + 1]), lft[ub]);
-                    const float2 d = __ffma2_rn(make_float2(yw[t - ub], yw[t - ua]), neg1, pr ? xp23 : xp01);
+                    const float2 d = __ffma2_rn(ypr[pr], neg1, pr ? xp23 : xp01);
                     const float2 cv = __ffma2_rn(d, d, make_float2(mb, ma));
                     cvs[ua] = cv.y;
                     cvs[ub] = cv.x;
@@ -1961,7 +2278,7 @@ __device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t ro
                         const int k = t - 2 * u;
                         if (val[u]) {
                             const float up = (k + 1 < NB) ? band[k + 1] : INFINITY;
-                            const float d = xr[u] - yw[t - u];
+                            const float d = xr[u] - (h ? ypr[pr].x : ypr[pr].y);
                             cvs[u] = fmaf(d, d, fminf(fminf(band[k], up), lft[u]));
                         }
                     }
@@ -1973,13 +2290,25 @@ __device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t ro
                 if (val[u]) {
                     band[k] = cvs[u];
                     lft[u] = cvs[u];
+#if !DTWP_BLOCKCUT
                     if (k & 1) rmn[u] = fminf(fminf(rmn[u], cvp[u]), cvs[u]);
                     else cvp[u] = cvs[u];
+#endif
                 }
             }
         }
+#if DTWP_BLOCKCUT
+        {
+            float bm = band[0];
+#pragma unroll
+            for (int k = 1; k + 1 < NB; k += 2) bm = fminf(fminf(bm, band[k]), band[k + 1]);
+            if (!(NB & 1)) bm = fminf(bm, band[NB - 1]);
+            rmn[3] = bm;
+        }
+#else
 #pragma unroll
         for (int u = 0; u < 4; u++) rmn[u] = fminf(rmn[u], cvp[u]);  // NB odd: the last cell
+#endif
 #else
         const float4 *yp = reinterpret_cast<const float4 *>(yq + i0);
 #pragma unroll
@@ -2022,8 +2351,13 @@ __device__ __forceinline__ bool dtwp_rows(const DtwCommon &C, int q, uint32_t ro
                 const float dd = fmaxf(fmaxf(qj - ue, le - qj), 0.f);
                 rem2 = fmaf(-dd, dd, rem2);
             }
+#if !(DTWP_PAIRED && DTWP_BLOCKCUT)
             cut = cut || (rmn[u] + fmaxf(fmaxf(remk - slk, rem2 - sl2), 0.f) > T);
+#endif
         }
+#if DTWP_PAIRED && DTWP_BLOCKCUT
+        cut = rmn[3] + fmaxf(fmaxf(remk - slk, rem2 - sl2), 0.f) > T;
+#endif
         if (alive && cut) {
             alive = false;
             nab++;
@@ -2304,7 +2638,7 @@ __device__ __forceinline__ void dtwt_body(const DtwCommon &C, const DtwPool &in,
                     rmn = fminf(rmn, fminf(c0, c1));
                     res = (act & (i == m - 1) & (sp == (R >> 1))) ? ((R & 1) ? c1 : c0) : res;
                     cut |= act & (sp == NP - 1) & (rmn + fmaxf(fmaxf(rk - slk, r2 - sl2), 0.f) > T);
-                    cal += act ? ((sp < NP - 1) ? 2 : 1) : 0;
+                    if (C.cells && act && sp == NP - 1) cal += dtw_band_cells(i, 1, R, m);  // row i complete
                     rp = make_float2(rx, ry);
                 }
                 if (__any_sync(0xFFFFFFFFu, cut)) {
@@ -3019,6 +3353,45 @@ static int launch_dtw32w(ssh_ctx *ctx, const float *X, const float *Q, const flo
                          const DtwList &L, const float *thr, int nq, cudaStream_t st, bool *done) {
     *done = false;
     const int m = ctx->p.m, r = ctx->p.radius;
+    {
+        // paired 64-virtual-lane form (dtw32v_kernel) for C2 = ceil((2r+1)/64) in [3, 8]
+        // A/B only (measured slower than dtw32w at r = 205: 3.4 vs 4.4 T cells/s,
+        // fewer resident warps): SSH_DTW_PAIRED_WIDE=1
+        static const bool paired = getenv("SSH_DTW_PAIRED_WIDE") != nullptr;
+        const int C2 = (2 * r + 1 + 63) / 64;
+        if (paired && C2 >= 2 && C2 <= 8) {
+            // must match dtw32v_kernel's layout: YP + 2m + DV_WARPS (G + 1), groups of C2 steps
+            const int NS = m + 63, G = (NS + C2 - 1) / C2;
+            const size_t smem = sizeof(float) * ((size_t)((r + m + 64 * C2 + 2 * C2 + 64 + 3) & ~3) +
+                                                 2 * (size_t)m + (size_t)DV_WARPS * (G + 1));
+            if (smem <= 200 * 1024) {
+                *done = true;
+                if (L.wave <= 0 || nq <= 0) return SSH_OK;
+                dim3 grid((unsigned)ssh_div_up(L.wave, DV_WARPS * 4), (unsigned)nq);
+                unsigned long long *cells = ctx->profile ? ctx->d_cells : nullptr;
+#define DV_LAUNCH(CC, RR)                                                                                   \
+    do {                                                                                                  \
+        SSH_CUDA(cudaFuncSetAttribute(dtw32v_kernel<CC, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      (int)smem));                                                        \
+        dtw32v_kernel<CC, RR><<<grid, 32 * DV_WARPS, smem, st>>>(X, m, r, Q, U, Lo, L, thr, cells);        \
+    } while (0)
+                switch (r == 205 ? -1 : C2) {
+                    case -1: DV_LAUNCH(7, 205); break;
+                    case 2: DV_LAUNCH(2, -1); break;
+                    case 3: DV_LAUNCH(3, -1); break;
+                    case 4: DV_LAUNCH(4, -1); break;
+                    case 5: DV_LAUNCH(5, -1); break;
+                    case 6: DV_LAUNCH(6, -1); break;
+                    case 7: DV_LAUNCH(7, -1); break;
+                    case 8: DV_LAUNCH(8, -1); break;
+                    default: break;
+                }
+#undef DV_LAUNCH
+                SSH_CHECK_LAUNCH();
+                return SSH_OK;
+            }
+        }
+    }
     const int C = dtw_warp_chunk(r);
     if (C < 3 || C > 16) return SSH_OK;
     const int G = (m + 31 + C - 1) / C;
@@ -3097,7 +3470,9 @@ static int launch_dtw32_wave(ssh_ctx *ctx, const float *X, const float *Q, const
         return launch_dtw_pooled<RR>(ctx, C, W.act, W.rows, W.lbs, W.cnt, W.stride, W.rec, nq, wave, st);
     // SSH_DEBUG_DTW_WAVEFRONT: the warp wavefront also for the pooled radii (A/B)
     static const bool wavefront = getenv("SSH_DEBUG_DTW_WAVEFRONT") != nullptr;
-    if (!legacy && !wavefront && (m & 3) == 0 && C.qpad) switch (r) {
+    // SSH_DTW_POOLED_MAXR: largest radius served by the pooled kernels (A/B)
+    static const int pooled_maxr = getenv("SSH_DTW_POOLED_MAXR") ? atoi(getenv("SSH_DTW_POOLED_MAXR")) : 51;
+    if (!legacy && !wavefront && (m & 3) == 0 && C.qpad && r <= pooled_maxr) switch (r) {
         DTWP(3) DTWP(6) DTWP(13) DTWP(26) DTWP(51)
         default: break;
     }

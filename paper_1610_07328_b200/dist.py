@@ -72,6 +72,24 @@ def merge_topk_local(ids, d2, k: int):
     return ido, d2o, n
 
 
+def merge_topk_device(g_ids, g_d2, lists: int, nq: int, k: int):
+    """ssh_merge_topk on the device: g_ids / g_d2 (lists * nq, k_in) in the
+    all_gather layout (rank-major) -> (ids (nq, k), d2 (nq, k), n (nq,))."""
+    torch = _torch()
+    from . import _native as nat
+
+    k_in = int(g_ids.shape[1])
+    dev = g_ids.device
+    ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    d2 = torch.empty((nq, k), dtype=torch.float64, device=dev)
+    n = torch.empty(nq, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    nat.check(nat.lib().ssh_merge_topk(nat.ptr(g_ids.contiguous()), nat.ptr(g_d2.contiguous()), nq, lists, k_in, k,
+                                       nat.ptr(ids), nat.ptr(d2), nat.ptr(n), __import__("ctypes").c_void_p(stream)),
+              "ssh_merge_topk")
+    return ids, d2, n
+
+
 def merge_across_ranks(ids, d2, n_cand, counters, k: int, group=None):
     """All-gather per-rank top-k and merge; all-reduce |R_g| and counters.
 
@@ -84,22 +102,32 @@ def merge_across_ranks(ids, d2, n_cand, counters, k: int, group=None):
     world = dist.get_world_size(group)
     if world == 1:
         return ids, d2, n_cand, counters
+    nq = ids.shape[0]
     if ids.is_cuda and dist.get_backend(group) == "gloo":
         # gloo collectives run on host tensors (functional tests of the sharded
-        # path on one GPU); NCCL takes the device tensors directly
+        # path on one GPU); the merge itself still runs on the device
         dev = ids.device
-        out = merge_across_ranks(ids.cpu(), d2.cpu(), n_cand.cpu(), counters.cpu(), k, group)
-        return tuple(t.to(dev) for t in out)
-    nq = ids.shape[0]
+        g_ids = torch.empty((world * nq, k), dtype=ids.dtype)
+        g_d2 = torch.empty((world * nq, k), dtype=d2.dtype)
+        dist.all_gather_into_tensor(g_ids, ids.cpu().contiguous(), group=group)
+        dist.all_gather_into_tensor(g_d2, d2.cpu().contiguous(), group=group)
+        red = torch.cat([n_cand.view(nq, 1), counters], dim=1).cpu().contiguous()
+        dist.all_reduce(red, op=dist.ReduceOp.SUM, group=group)
+        mids, md2, _ = merge_topk_device(g_ids.to(dev), g_d2.to(dev), world, nq, k)
+        red = red.to(dev)
+        return mids, md2, red[:, 0].contiguous(), red[:, 1:].contiguous()
     g_ids = torch.empty((world * nq, k), dtype=ids.dtype, device=ids.device)
     g_d2 = torch.empty((world * nq, k), dtype=d2.dtype, device=d2.device)
     dist.all_gather_into_tensor(g_ids, ids.contiguous(), group=group)
     dist.all_gather_into_tensor(g_d2, d2.contiguous(), group=group)
-    cat_ids = g_ids.view(world, nq, k).permute(1, 0, 2).reshape(nq, world * k)
-    cat_d2 = g_d2.view(world, nq, k).permute(1, 0, 2).reshape(nq, world * k)
     red = torch.cat([n_cand.view(nq, 1), counters], dim=1).contiguous()
     dist.all_reduce(red, op=dist.ReduceOp.SUM, group=group)
-    mids, md2, _ = merge_topk_local(cat_ids, cat_d2, k)
+    if g_ids.is_cuda:
+        mids, md2, _ = merge_topk_device(g_ids, g_d2, world, nq, k)
+    else:  # host tensors (gloo tests of the merge logic without a GPU)
+        cat_ids = g_ids.view(world, nq, k).permute(1, 0, 2).reshape(nq, world * k)
+        cat_d2 = g_d2.view(world, nq, k).permute(1, 0, 2).reshape(nq, world * k)
+        mids, md2, _ = merge_topk_local(cat_ids, cat_d2, k)
     return mids, md2, red[:, 0].contiguous(), red[:, 1:].contiguous()
 
 

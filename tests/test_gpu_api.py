@@ -265,3 +265,36 @@ def test_query_index_batch_sharded_two_processes(cuda, tmp_path):
     assert any(w[2] == "no-candidates" for w in got[False]) and any(w[2] == "fallback" for w in got[True])
     big = ssh.query_index_batch(idx, Qs[:2], X.shape[0] + 5)
     assert got["big"] == [(r.ids, r.warning) for r in big]
+
+
+@pytest.mark.parametrize("lists,k_in,k_out", [(2, 10, 10), (8, 10, 10), (3, 64, 20), (8, 2048, 2048), (5, 7, 40)])
+def test_merge_topk_kernel_matches_lexsort(cuda, lists, k_in, k_out):
+    """ssh_merge_topk (the cross-shard merge) against a numpy lexsort of the
+    concatenated per-shard lists: exact d2 ties broken by id, inf distances
+    before padding, short lists padded with id -1 / +inf."""
+    import torch
+
+    from paper_1610_07328_b200 import dist as D
+
+    rng = np.random.default_rng(lists * 1000 + k_in)
+    nq = 37
+    parts = []
+    for g in range(lists):
+        ids = np.full((nq, k_in), -1, dtype=np.int64)
+        d2 = np.full((nq, k_in), np.inf)
+        for q in range(nq):
+            n = int(rng.integers(0, k_in + 1))
+            cand_ids = rng.choice(10 * k_in + 10, size=n, replace=False) * lists + g  # disjoint across shards
+            vals = np.round(rng.random(n) * 4) / 4  # many exact ties
+            vals[rng.random(n) < 0.05] = np.inf
+            o = np.lexsort((cand_ids, vals))
+            ids[q, :n] = cand_ids[o]
+            d2[q, :n] = vals[o]
+        parts.append((ids, d2))
+    g_ids = torch.from_numpy(np.concatenate([p[0] for p in parts])).cuda()
+    g_d2 = torch.from_numpy(np.concatenate([p[1] for p in parts])).cuda()
+    mi, md, n = D.merge_topk_device(g_ids, g_d2, lists, nq, k_out)
+    want_i, want_d = D.merge_numpy(parts, k_out)
+    assert np.array_equal(mi.cpu().numpy(), want_i)
+    assert np.array_equal(md.cpu().numpy(), want_d)
+    assert np.array_equal(n.cpu().numpy(), (want_i >= 0).sum(1))

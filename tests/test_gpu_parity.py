@@ -382,37 +382,72 @@ def test_dtw_exact_pairs(cuda, golden):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.slow
-def test_full_scale_cfg1_sampled(cuda):
-    """configs[1] shape (N=1,000,000): sampled signature parity, the tables of
-    the device signatures, and 16 queries' top-10 against the oracle cascade."""
-    import torch
-
+def test_config0_full_parity(cuda):
+    """SURVEY §8c scale plan, configs[0] in full: every signature, all 20
+    bucket tables and all 100 warped queries (ids, distances, |R|, statuses)
+    against an oracle index built independently from the same f32 series."""
     import paper_1610_07328_b200 as ssh
     from paper_1610_07328_b200 import datagen
 
-    X, Q, src, p = datagen.workload(1, device="cuda", nq=16)
+    X, Q, src, p = datagen.workload(0, device="cuda")
+    assert X.shape == (10_000, 512) and Q.shape == (100, 512)
     params_ = ssh.SshParams(**p)
     idx = ssh.build_index(ssh.Dataset(X), params_)
     res = ssh.query_index_batch(idx, Q, 10)
     Xh = X.cpu().numpy()
-    sig = idx.signatures
-    rng = np.random.default_rng(0)
-    rows = rng.choice(Xh.shape[0], 10000, replace=False)
-    osig = O.signatures(Xh[rows], 80, 3, 15, 20, 4, 0, threads=16)
-    assert np.array_equal(sig[rows], osig)
-    # tables built on the device == reference table construction over the same signatures
-    ocsr = O.tables_from_signatures(sig)
-    for j in (0, 9, 19):
+    oidx = O.build_index(Xh, 80, 3, 15, 20, 4, 0, p["band"], threads=16)
+    assert np.array_equal(idx.signatures, oidx.sig)
+    for j in range(20):
         k, o, i = idx.table_csr(j)
-        assert np.array_equal(k, ocsr[j][0]) and np.array_equal(o, ocsr[j][1]) and np.array_equal(i, ocsr[j][2])
+        assert np.array_equal(k, oidx.csr[j][0]) and np.array_equal(o, oidx.csr[j][1]) \
+            and np.array_equal(i, oidx.csr[j][2]), j
+    ores = O.query_batch(oidx, Q, 10, threads=16)
+    for i, r in enumerate(res):
+        n = int(ores["n"][i])
+        assert r.status == "ok" and r.stats.candidates == int(ores["n_cand"][i]) > 0, i
+        assert r.ids == ores["ids"][i][:n].tolist(), i
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
+    assert idx.sketch_stats["near_zero"] == 0
+
+
+def _full_size_vs_oracle(cfg, nq, sig_rows):
+    """Full-size configs[cfg]: signatures of `sig_rows` sampled rows against the
+    oracle's, all 20 device tables against the reference table construction
+    over the device signatures, and `nq` queries' |R|, top-10 ids and
+    distances against the oracle cascade (index.py:204-273) over the same
+    tables (A2-A6 sampled, tables exact, >= 20 queries)."""
+    import paper_1610_07328_b200 as ssh
+    from paper_1610_07328_b200 import datagen
+
+    X, Q, src, p = datagen.workload(cfg, device="cuda", nq=nq)
+    assert X.shape[0] == datagen.CONFIGS[cfg]["N"]
+    params_ = ssh.SshParams(**p)
+    idx = ssh.build_index(ssh.Dataset(X), params_)
+    res = ssh.query_index_batch(idx, Q, 10)
+    Xh = X.cpu().numpy()
+    del X
+    sig = idx.signatures
+    rows = np.random.default_rng(cfg).choice(Xh.shape[0], sig_rows, replace=False)
+    assert np.array_equal(sig[rows], O.signatures(Xh[rows], 80, 3, 15, 20, 4, 0, threads=16))
+    ocsr = O.tables_from_signatures(sig)
+    for j in range(20):
+        k, o, i = idx.table_csr(j)
+        assert np.array_equal(k, ocsr[j][0]) and np.array_equal(o, ocsr[j][1]) \
+            and np.array_equal(i, ocsr[j][2]), j
     oidx = O.OracleIndex(Xh, 80, 3, 15, 20, 4, 0, p["band"], O.make_filter(80, 0), sig, ocsr)
     ores = O.query_batch(oidx, Q, 10, threads=16)
     for i, r in enumerate(res):
         n = int(ores["n"][i])
-        assert r.stats.candidates == int(ores["n_cand"][i])
-        assert r.ids == ores["ids"][i][:n].tolist()
-        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist()
+        assert r.stats.candidates == int(ores["n_cand"][i]), i
+        assert r.ids == ores["ids"][i][:n].tolist(), i
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
+
+
+@pytest.mark.slow
+def test_full_scale_cfg1_vs_oracle(cuda):
+    """configs[1] (N=1,000,000, m=512, band 5%): 10k sampled signatures, all
+    tables, 24 queries against the oracle."""
+    _full_size_vs_oracle(1, 24, 10_000)
 
 
 def _adversarial_sets():
@@ -491,30 +526,12 @@ def test_query_overflow_round(cuda, golden, monkeypatch, target):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", [2, 3])
-def test_config_shapes_sampled(cuda, cfg):
-    """configs[2] (ECG windows, m=1024, band 5%) and configs[3] (random walks,
-    m=2048, band 10%: radius 205, the generic shared-memory DTW kernel) at their
-    series length and band on a 300k-series shard: 8 warped queries, top-10
-    ids and distances identical to the oracle cascade over the same signatures."""
-    import paper_1610_07328_b200 as ssh
-    from paper_1610_07328_b200 import datagen
-
-    X, Q, src, p = datagen.workload(cfg, device="cuda", nq=8, n_override=300_000)
-    params_ = ssh.SshParams(**p)
-    idx = ssh.build_index(ssh.Dataset(X), params_)
-    res = ssh.query_index_batch(idx, Q, 10)
-    Xh = X.cpu().numpy()
-    sig = idx.signatures
-    rows = np.random.default_rng(1).choice(Xh.shape[0], 2000, replace=False)
-    assert np.array_equal(sig[rows], O.signatures(Xh[rows], 80, 3, 15, 20, 4, 0, threads=16))
-    ocsr = O.tables_from_signatures(sig)
-    oidx = O.OracleIndex(Xh, 80, 3, 15, 20, 4, 0, p["band"], O.make_filter(80, 0), sig, ocsr)
-    ores = O.query_batch(oidx, Q, 10, threads=16)
-    for i, r in enumerate(res):
-        n = int(ores["n"][i])
-        assert r.stats.candidates == int(ores["n_cand"][i])
-        assert r.ids == ores["ids"][i][:n].tolist(), i
-        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
+def test_full_scale_cfg2_cfg3_vs_oracle(cuda, cfg):
+    """configs[2] (2M ECG windows, m=1024, band 5%: radius 51, pooled register
+    band) and configs[3] (4M random walks, m=2048, band 10%: radius 205, warp
+    wavefront) at FULL size: 4k sampled signatures, all tables, 20 queries'
+    top-10 ids and distances identical to the oracle cascade."""
+    _full_size_vs_oracle(cfg, 20, 4000)
 
 
 @pytest.mark.slow
