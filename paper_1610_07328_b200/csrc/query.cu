@@ -1215,6 +1215,49 @@ __device__ __forceinline__ float wl_smp_block(const uint32_t (&cw)[4], const flo
     return acc.x + acc.y;
 }
 
+// First-chunk screen, 8 lanes per member (4 members per warp instruction):
+// the partial LB_Keogh2 over samples [0, WL_F) of the member whose codes row is
+// cr; lane l8 of the group reads 16 contiguous code bytes (8 samples) per
+// 64-sample chunk, so a group reads 128 contiguous bytes per load.  Same
+// per-sample IEEE operations as wl_env_chunks; returns the group's sum on
+// every lane of the group (xor-shuffle over the 8 lanes).
+#define WL_F 256
+__device__ __forceinline__ float wl_env_first8(const uint8_t *cr, const float *sqn, int mp, float sc, float lo) {
+    const int l8 = threadIdx.x & 7;
+    float2 acc = make_float2(0.f, 0.f);
+    const float2 sc2 = make_float2(sc, sc), lo2 = make_float2(lo, lo);
+    const uint4 *p = reinterpret_cast<const uint4 *>(cr + mp) + l8;
+    uint4 v[WL_F / 64];
+#pragma unroll
+    for (int c = 0; c < WL_F / 64; c++) v[c] = 64 * c < mp ? __ldg(p + 8 * c) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int c = 0; c < WL_F / 64; c++) {
+        if (64 * c < mp) {
+            const int i0 = 64 * c + 8 * l8;
+            const float4 qa = *reinterpret_cast<const float4 *>(sqn + i0);
+            const float4 qb = *reinterpret_cast<const float4 *>(sqn + i0 + 4);
+            const float nq[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+            const uint32_t wv[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+            float dd[8];
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                const int bu = 2 * (t & 1);
+                const float2 ul = __ffma2_rn(code_f2(wv[t >> 1], bu, bu + 1), sc2, lo2);
+                const float2 df = __fadd2_rn(ul, make_float2(nq[t], nq[t]));
+                dd[t] = fmaxf(fmaxf(-df.x, df.y), 0.f);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; t += 2)
+                acc = __ffma2_rn(make_float2(dd[t], dd[t + 1]), make_float2(dd[t], dd[t + 1]), acc);
+        }
+    }
+    float s = acc.x + acc.y;
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 1);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 2);
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, 4);
+    return s;
+}
+
 __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
     extern __shared__ __align__(16) float wsm[];
     const int slot = blockIdx.y;
@@ -1252,8 +1295,46 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
         }
         unsigned live = __ballot_sync(0xFFFFFFFFu, e < end && key <= T);
         if (!live) continue;
+        // stage 1: LB_Keogh2 over the first WL_F samples, 4 members at a time
+        // (8 lanes each); most members are pruned here.  Survivors keep their
+        // partial sum (p1 on the member's own lane) for the warp-wide pass.
+        float p1 = 0.f;
+        {
+            unsigned todo = live, surv = 0u;
+            while (todo) {
+                int js[4];
+#pragma unroll
+                for (int g = 0; g < 4; g++) {
+                    js[g] = todo ? __ffs(todo) - 1 : -1;
+                    if (todo) todo &= todo - 1;
+                }
+                const int gi = lane >> 3;
+                const int jm = gi == 0 ? js[0] : gi == 1 ? js[1] : gi == 2 ? js[2] : js[3];
+                const uint32_t rm = __shfl_sync(0xFFFFFFFFu, row, jm < 0 ? 0 : jm);
+                float part = 0.f;
+                if (jm >= 0) {
+                    float2 h = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rm * 4));
+                    part = wl_env_first8(a.codes + (int64_t)rm * a.cstride, sqn, mp, fabsf(h.y), h.x);
+                } else {
+                    part = wl_env_first8(a.codes, sqn, 0, 0.f, 0.f);  // idle group: no loads (mp = 0)
+                }
+#pragma unroll
+                for (int g = 0; g < 4; g++) {
+                    const float pg = __shfl_sync(0xFFFFFFFFu, part, 8 * g);
+                    if (js[g] >= 0) {
+                        if (lane == js[g]) p1 = pg;
+                        if (pg > T) keo2++;
+                        else surv |= 1u << js[g];
+                        nbytes += 2 * min(WL_F, mp);
+                    }
+                }
+            }
+            live = surv;
+        }
+        if (!live) continue;
         int j = __ffs(live) - 1;
         live &= live - 1;
+        int jc = j;
         uint32_t rc = __shfl_sync(0xFFFFFFFFu, row, j);
         float2 hc = __ldg(reinterpret_cast<const float2 *>(a.rec + (int64_t)rc * 4));
         hc.y = fabsf(hc.y);  // sign = PAA-codes flag, not part of the scale
@@ -1276,14 +1357,20 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
             const uint8_t *cr = a.codes + (int64_t)rc * a.cstride;
             const float lo = hc.x, sc = hc.y;
             bool pruned = false;
-            float acc = 0.f, tot2 = 0.f, tot1 = 0.f;
+            // samples [0, WL_F) were summed by the stage-1 screen (p1 of lane jc)
+            const float pre = __shfl_sync(0xFFFFFFFFu, p1, jc);
+            float acc = lane == 0 ? pre : 0.f, tot2 = pre, tot1 = 0.f;
             // abandon checks after every 256 samples (partial sums are lower bounds)
             for (int base = 0; base < mp; base += WL_BLK) {
-                if (base) wl_load_env(cr, mp, base, vc);
-                nbytes += 2 * min(WL_BLK, mp - base);
-                acc += wl_env_chunks<0, 2>(vc, sqn, base, mp, sc, lo);
-                tot2 = warp_sum(acc);
-                if (tot2 > T) { pruned = true; break; }
+                if (base) {
+                    wl_load_env(cr, mp, base, vc);
+                    nbytes += 2 * min(WL_BLK, mp - base);
+                    acc += wl_env_chunks<0, 2>(vc, sqn, base, mp, sc, lo);
+                    tot2 = warp_sum(acc);
+                    if (tot2 > T) { pruned = true; break; }
+                } else {
+                    nbytes += 2 * max(0, min(WL_BLK, mp) - WL_F);
+                }
                 if (base + 256 < mp) {
                     acc += wl_env_chunks<2, 4>(vc, sqn, base, mp, sc, lo);
                     tot2 = warp_sum(acc);
@@ -1314,6 +1401,7 @@ __global__ void __launch_bounds__(256) wave_lb_kernel(WaveLbArgs a) {
             }
             if (!more) break;
             rc = rn;
+            jc = j;
             hc = hn;
 #pragma unroll
             for (int c = 0; c < 4; c++) vc[c] = vn[c];
@@ -2611,9 +2699,11 @@ __device__ __forceinline__ void dtwt_body(const DtwCommon &C, const DtwPool &in,
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
                     const int s = s0 + u;
-                    // the pair lane - 1 produced last step (lane 0, first round: the pooled band)
+                    // the pair lane - 1 produced last step (lane 0, first round: the pooled
+                    // band of row a - 1 while its row a needs it, s < NP; from step NP on it
+                    // carries lane 31's row a + 31 into round 1 like every later round)
                     const float2 bb = reinterpret_cast<const float2 *>(bs)[min(s + 1, 63)];
-                    const bool fromb = (k == 0) & (lane == 0);
+                    const bool fromb = (k == 0) & (lane == 0) & (s < NP);
                     float rx = __shfl_sync(0xFFFFFFFFu, c0, (lane + 31) & 31);
                     float ry = __shfl_sync(0xFFFFFFFFu, c1, (lane + 31) & 31);
                     rx = fromb ? bb.x : rx;
