@@ -397,9 +397,11 @@ def _profile_json(cfg):
 
 def _traffic(prof, kernel_prefix):
     """DRAM bytes (read + write) summed over the launches of kernels whose name
-    starts with `kernel_prefix` in one build + query batch (ncu --set full)."""
+    starts with `kernel_prefix` (a string or a tuple of them) in one build +
+    query batch (the committed ncu metrics capture)."""
     ks = prof.get("kernels", {})
-    tot = [v["dram_bytes"] for k, v in ks.items() if k.startswith(kernel_prefix) and v.get("dram_bytes")]
+    pre = kernel_prefix if isinstance(kernel_prefix, tuple) else (kernel_prefix,)
+    tot = [v["dram_bytes"] for k, v in ks.items() if k.startswith(pre) and v.get("dram_bytes")]
     return float(sum(tot)) if tot else None
 
 
@@ -464,15 +466,25 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device, c
 
     ms_t = _time(mk, reps=3)
     bt = N * params.d * 20
-    tr = None
-    for pre in ("rs_", "rle_", "tb_"):
-        v = _traffic(prof_json, pre)
-        tr = (tr or 0.0) + v if v is not None else tr
+    tr = _traffic(prof_json, ("rs_", "rle_"))
     res["tables"] = dict(name="bucket tables (K4)", ms=ms_t, roofline=dict(
         bound="hbm", achieved=bt / ms_t / 1e6, peak=hbm, unit="GB/s", frac=bt / ms_t / 1e6 / hbm,
         traffic=tr, kernel="rs_*/rle_* (radix passes + run-length CSR)",
         note="algorithmic bytes = 20 B per (series, table): 8 B key in, 8 B key + 4 B id out; traffic = "
              "ncu dram bytes of every table kernel of one build"))
+    # rerank summaries (part of every build, on the side stream beside K4):
+    # standalone over the same rows
+    def summ():
+        nat.check(lib.ssh_index_summarize(ctx.handle, index._tables.handle, nat.ptr(X), m, st))
+
+    ms_s = _time(summ, reps=3)
+    mp = (m + 127) // 128 * 128
+    bsum = N * (4 * m + 64 + 3 * mp)
+    res["summaries"] = dict(name="rerank summaries (records + u8 sample/envelope codes)", ms=ms_s, roofline=dict(
+        bound="hbm", achieved=bsum / ms_s / 1e6, peak=hbm, unit="GB/s", frac=bsum / ms_s / 1e6 / hbm,
+        traffic=_traffic(prof_json, "summaries"), kernel="summaries_kernel",
+        note="algorithmic bytes = N * (4m read + 64 B record + 3 m_p B codes written); runs on the build's side "
+             "stream concurrently with K4; issue-bound on the envelope-code running max/min"))
     # query phases
     nat.check(lib.ssh_ctx_set_profiling(ctx.handle, 1))
     torch.cuda.synchronize()
@@ -486,15 +498,29 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device, c
              "wave fp32 DTW (K8b)", "rescore+top-k (K9/K10)"]
     for i, n in enumerate(names):
         res[f"q{i}"] = dict(name=n, ms=prof[i])
+    # K5: query sketch + CWS (K1-K3 on the batch): 4m B in + 8L B out per query
+    bq = nq * (4 * m + 8 * params.d)
+    if prof[0] > 0:
+        res["q0"]["roofline"] = dict(
+            bound="hbm", achieved=bq / prof[0] / 1e6, peak=hbm, unit="GB/s", frac=bq / prof[0] / 1e6 / hbm,
+            traffic=None, kernel="sketch + cws_fast (query batch)",
+            note="algorithmic bytes = nq (4m + 8L); a few launches over a small batch: launch/latency-bound")
     # K6: bitmap words written + bucket id lists read
     nw = (N + 31) // 32
+    b6 = cand_total * 4 + nq * nw * 4 * 2
+    if prof[1] > 0:
+        res["q1"]["roofline"] = dict(
+            bound="hbm", achieved=b6 / prof[1] / 1e6, peak=hbm, unit="GB/s", frac=b6 / prof[1] / 1e6 / hbm,
+            traffic=_traffic(prof_json, ("probe", "bitmap", "count_kernel")), kernel="probe_kernel + bitmap_smem_kernel + count_kernel",
+            note="algorithmic bytes = |R| x 4 B (member ids of the probed buckets, a lower bound: buckets of "
+                 "different tables overlap) + the membership bitmap written and counted (2 x nq x N/8)")
     # K7: every member of R costs one 64-byte record read (L2/HBM) + its key
     # and bin written (8 B); the bitmap is read once per pass
     k7_bytes = cand_total * (64 + 8) + nq * nw * 4 * 2
     if prof[2] > 0:
         res["q2"]["roofline"] = dict(
             bound="hbm", achieved=k7_bytes / prof[2] / 1e6, peak=hbm, unit="GB/s",
-            frac=k7_bytes / prof[2] / 1e6 / hbm, traffic=_traffic(prof_json, "paa_members"),
+            frac=k7_bytes / prof[2] / 1e6 / hbm, traffic=_traffic(prof_json, ("paa_members", "binsort", "bs_")),
             kernel="paa_members_kernel + binsort_kernel",
             note="algorithmic bytes = |R| x (64 B record + 8 B key/bin) + 2 bitmap passes; records are "
                  "L2-resident at configs[1] (64 MB)")
@@ -510,13 +536,24 @@ def stage_profile(ctx, X, Qd, index, params, lib, nat, st, query_batch_device, c
         bound="fp32", achieved=(cells / (dtw_ms / 1e3)) / 1e12 if dtw_ms else 0,
         peak=peak_cells / 1e12, unit="Tcells/s",
         frac=(cells / (dtw_ms / 1e3)) / peak_cells if dtw_ms else 0,
-        traffic=_traffic(prof_json, "dtw"),
+        traffic=_traffic(prof_json, ("dtwp_", "dtw32")),
         kernel=("dtwp_first/dtwp_pass pooled register band" if r in (3, 6, 13, 26, 51)
                 else "dtw32w_kernel (band-chunked warp wavefront)"),
         note="cells = in-band cells of the rows each fp32 DTW evaluated; peak = SURVEY §8d's 148 x 128 x "
              "f_max / 3 (FADD + FFMA + FMNMX3 per cell)")
     res["dtw_evaluated"] = prof[8]
     res["rescored"] = prof[9]
+    # K10: exact f64 DTW of the rescoring set (the reference recurrence: DSUB, DMUL, DADD + 2 DMNMX per
+    # cell on the FP64 pipe, 64 lanes/SM/clk) + the final (d64, id) top-k
+    cells64 = prof[9] * m * (2 * r + 1)
+    peak64 = 148 * 64 * peaks["sm_max_mhz"] * 1e6 / 5.0
+    if prof[5] > 0:
+        res["q5"]["roofline"] = dict(
+            bound="fp64", achieved=cells64 / (prof[5] / 1e3) / 1e12, peak=peak64 / 1e12, unit="Tcells/s",
+            frac=cells64 / (prof[5] / 1e3) / peak64, traffic=_traffic(prof_json, "dtw64"),
+            kernel="dtw64r/dtw64band (exact rescoring) + select/topk",
+            note="cells = rescored pairs x m x (2r+1) (upper bound); about k + a few pairs per query, so the "
+                 "stage is latency-bound, not FP64-bound")
     lb_bytes = prof[7]
     lb_ms = prof[3]
     if lb_ms > 0:

@@ -152,6 +152,14 @@ int ssh_windows(const double *rec, int64_t len, int32_t t, int64_t stride, int32
  * sequential recheck of the undecided signs (counted in *nrecheck). */
 int ssh_srp(const float *X, int64_t N, int32_t m, const float *V32, const double *V64, int32_t bits,
             int8_t *out, unsigned long long *nrecheck, void *stream);
+/* srp_matrix (index.py:420-423) with the f32 product on the tensor cores
+ * (tcgen05.mma kind::tf32, accumulator in TMEM) when tensor_cores != 0 and
+ * bits <= 256, else SIMT fp32; signs within the rigorous product error bound
+ * are re-evaluated as a sequential f64 dot of the original values: X64
+ * (device f64 [N][m], may be NULL) when the input was float64, else X.
+ * nrecheck (device u64, may be NULL) counts the re-evaluated signs. */
+int ssh_srp2(const float *X, const double *X64, int64_t N, int32_t m, const float *V32, const double *V64,
+             int32_t bits, int8_t *out, unsigned long long *nrecheck, int32_t tensor_cores, void *stream);
 /* Host-only: parse the per-table section of an SSHI index file
  * (index.py:279-396, load_index) starting at byte `off` into the signature
  * matrix sig u64[N][L] (signatures[ids, j] = key), checking ids in [0, N) and

@@ -139,6 +139,7 @@ def lib():
             "ssh_index_create_bare": ([P, P, i64, i64, i64, PP, P], ctypes.c_int),
             "ssh_windows": ([P, i64, i32, i64, i32, P, P, ctypes.POINTER(i64), P], ctypes.c_int),
             "ssh_srp": ([P, i64, i32, P, P, i32, P, P, P], ctypes.c_int),
+            "ssh_srp2": ([P, P, i64, i32, P, P, i32, P, P, i32, P], ctypes.c_int),
             "ssh_sshi_parse_tables": ([P, i64, i64, i32, i64, P, ctypes.POINTER(i64), ctypes.c_char_p, i32],
                                       ctypes.c_int),
         }
@@ -157,7 +158,7 @@ EXPORTED = [
     "ssh_cws", "ssh_signatures", "ssh_index_build", "ssh_build_index", "ssh_build_index_host", "ssh_index_destroy", "ssh_index_num_buckets",
     "ssh_index_size", "ssh_index_sketch_stats", "ssh_merge_topk", "ssh_index_export", "ssh_index_summarize", "ssh_index_copy_summaries", "ssh_probe", "ssh_query_batch", "ssh_dtw_exact",
     "ssh_query_phase_ms", "ssh_dtw_pairs64", "ssh_envelope64", "ssh_lb_keogh64", "ssh_lb_kim64",
-    "ssh_index_create_bare", "ssh_sshi_parse_tables", "ssh_windows", "ssh_srp",
+    "ssh_index_create_bare", "ssh_sshi_parse_tables", "ssh_windows", "ssh_srp", "ssh_srp2",
 ]
 
 

@@ -23,6 +23,24 @@ int ssh_cuda_fail(cudaError_t e, const char *what, const char *file, int line);
     } while (0)
 
 void ssh_count_launch();
+// Device-side bounds assertions of the checked build (-DSSH_CHECKED; the
+// sanitizers are not available on the GPU pool): a failed check traps the
+// kernel, which surfaces as a CUDA error at the next call.  No code otherwise.
+#ifdef SSH_CHECKED
+#define SSH_DASSERT(cond)                                                                       \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("SSH_DASSERT failed: %s at %s:%d (block %d, thread %d)\n", #cond, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define SSH_DASSERT(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 #define SSH_CHECK_LAUNCH()          \
     do {                            \
         ssh_count_launch();         \

@@ -761,6 +761,7 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
         while (word) {
             int b = __ffs(word) - 1;
             word &= word - 1;
+            SSH_DASSERT(pos < 1024);
             list[pos++] = (uint32_t)(wd * 32 + b);
         }
         __syncwarp();
@@ -861,6 +862,7 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                         if (lane == 0) dst = atomicAdd(&a.cnt[q], __popc(km));
                         dst = __shfl_sync(0xFFFFFFFFu, dst, 0) + __popc(km & ((1u << lane) - 1u));
                         if (keep) {
+                            SSH_DASSERT(base_q + dst < a.roff[q + 1]);
                             a.rows[base_q + dst] = row;
                             a.lb[base_q + dst] = key;
                         }
@@ -986,6 +988,7 @@ binsort_kernel(const uint32_t *__restrict__ rows_in, const float *__restrict__ l
         basep = __shfl_sync(0xFFFFFFFFu, basep, leader);
         if (e < n) {
             const uint32_t p = basep + __popc(peers & lt);
+            SSH_DASSERT(p < (uint32_t)n);
             rows_out[o + p] = rows_in[o + e];
             lb_out[o + p] = v;
         }
@@ -1750,6 +1753,7 @@ dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restr
         for (; g < G; g++) {
             const int s0 = g * C;
             const float *yb = yq + s0 + 32 * C - 31;
+            SSH_DASSERT(s0 + 32 * C - 31 + C <= YP);
             if (g < g_main0)
                 dw_group<C, 0, true, true>(band, yw, x, yb, s0, lane, own, cst, rown, rcc, m, res);
             else if (g < g_main1)
@@ -1767,6 +1771,7 @@ dtw32w_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restr
                         if (lane * C + c < nk) cm = fminf(cm, band[c]);
                 }
                 const unsigned cmb = __reduce_min_sync(0xFFFFFFFFu, __float_as_uint(cm));
+                SSH_DASSERT(g < G);
                 const float remk = fmaxf(total - pre[g] - slack, 0.f);
                 if (__uint_as_float(cmb) + remk > T) {
                     dead = true;
@@ -2274,6 +2279,9 @@ struct DtwCommon {
 #ifndef DTWP_MINB
 #define DTWP_MINB 1
 #endif
+#ifndef DTWP_MINB_NARROW
+#define DTWP_MINB_NARROW 1  // radii <= 26 (A/B: 3 blocks/SM at 168 registers)
+#endif
 #ifndef DTWP_BLOCKCUT
 #define DTWP_BLOCKCUT 1  // one cut test per 4-row block on the band minimum (else per row)
 #endif
@@ -2473,6 +2481,7 @@ __device__ __forceinline__ void dtwp_emit(const DtwCommon &C, const DtwPool &P, 
         return;
     }
     const int64_t d = base + __popc(am & ((1u << lane) - 1u));
+    SSH_DASSERT(d < P.cap);
     if (d >= P.cap) return;  // cannot happen: the pool holds every wave candidate
     P.q[d] = q;
     P.row[d] = row;
@@ -2502,7 +2511,7 @@ __device__ __forceinline__ void dtwp_flush(const DtwCommon &C, unsigned long lon
 
 // first pass, per query slot: wave list entries -> rows [0, b) -> pool
 template <int R>
-__global__ void __launch_bounds__(32 * DP_WARPS, DTWP_MINB)
+__global__ void __launch_bounds__(32 * DP_WARPS, (R <= 26 ? DTWP_MINB_NARROW : DTWP_MINB))
 dtwp_first_kernel(DtwCommon C, const int *__restrict__ act, const uint32_t *__restrict__ wrows,
                   const float2 *__restrict__ wlb, const int *__restrict__ wcnt, int64_t wcap,
                   const uint4 *__restrict__ rec, int b, DtwPool P) {
@@ -2719,6 +2728,7 @@ __device__ __forceinline__ void dtwt_body(const DtwCommon &C, const DtwPool &in,
                     left = st0 ? INFINITY : left;
                     rmn = st0 ? INFINITY : rmn;
                     const int yi = act ? i + 2 * sp : 0;
+                    SSH_DASSERT(yi + 1 < YP);
                     const float d0 = xr - ys[yi], d1 = xr - ys[yi + 1];
                     const float n0 = fmaf(d0, d0, fminf(fminf(rp.x, rp.y), left));
                     const float n1 = fmaf(d1, d1, fminf(fminf(rp.y, rx), n0));
@@ -2753,7 +2763,7 @@ __device__ __forceinline__ void dtwt_body(const DtwCommon &C, const DtwPool &in,
 // one pooled level: rows [a, b) of every pooled candidate, or, once fewer
 // than lim are left, all remaining rows [a, m) in the wavefront tail
 template <int R>
-__global__ void __launch_bounds__(32 * DP_WARPS, DTWP_MINB)
+__global__ void __launch_bounds__(32 * DP_WARPS, (R <= 26 ? DTWP_MINB_NARROW : DTWP_MINB))
 dtwp_level_kernel(DtwCommon C, DtwPool in, DtwPool P, int a, int b, int lim) {
     extern __shared__ __align__(16) float dtsm[];
     const int n = min(*in.count, (int)in.cap);

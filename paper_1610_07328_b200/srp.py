@@ -22,15 +22,27 @@ def srp_vectors(m: int, bits: int, seed: int) -> np.ndarray:
     return out
 
 
-def srp_matrix(values, bits: int, seed: int, device=None) -> np.ndarray:
-    """(N, bits) int8 +1/-1 signs of values @ srp_vectors(m, bits, seed).T on the device."""
+def srp_matrix(values, bits: int, seed: int, device=None, tensor_cores: bool = True, stats: dict | None = None
+               ) -> np.ndarray:
+    """(N, bits) int8 +1/-1 signs of values @ srp_vectors(m, bits, seed).T on the
+    device (index.py:420-423): the product on the tensor cores (tcgen05, TF32
+    with a rigorous error bound; bits <= 256), undecided signs re-evaluated in
+    f64 from the original values (float64 inputs are kept in float64 for that).
+    `stats`, if given, receives {"rechecked": signs re-evaluated in f64}."""
     import torch
 
     dev = torch.device("cuda", 0 if device is None else int(device))
+    X64 = None
     if hasattr(values, "detach"):
-        X = values.detach().to(device=dev, dtype=torch.float32).contiguous()
+        v = values.detach().to(device=dev)
+        if v.dtype == torch.float64:
+            X64 = v.contiguous()
+        X = v.to(dtype=torch.float32).contiguous()
     else:
-        X = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).to(dev)
+        a = np.asarray(values)
+        if a.dtype == np.float64:
+            X64 = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        X = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
     if X.ndim != 2:
         raise ValueError(f"values must be 2-D, got shape {tuple(X.shape)}")
     N, m = X.shape
@@ -38,9 +50,12 @@ def srp_matrix(values, bits: int, seed: int, device=None) -> np.ndarray:
     V64 = torch.from_numpy(V).to(dev)
     V32 = V64.float()
     out = torch.empty((N, bits), dtype=torch.int8, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
     stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
-    nat.check(nat.lib().ssh_srp(nat.ptr(X), N, m, nat.ptr(V32), nat.ptr(V64), bits, nat.ptr(out), None, stream),
-              "ssh_srp")
+    nat.check(nat.lib().ssh_srp2(nat.ptr(X), nat.ptr(X64), N, m, nat.ptr(V32), nat.ptr(V64), bits, nat.ptr(out),
+                                 nat.ptr(cnt), 1 if tensor_cores else 0, stream), "ssh_srp2")
+    if stats is not None:
+        stats["rechecked"] = int(cnt.item())
     return out.cpu().numpy()
 
 

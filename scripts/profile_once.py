@@ -1,4 +1,6 @@
-"""One index build + one query batch at configs[1] shape (for ncu captures).
+"""One index build + one query batch at a config's shape (for ncu captures).
+The build + query are bracketed by cudaProfilerStart/Stop, so
+`ncu --profile-from-start off` skips the data generation.
 
 python scripts/profile_once.py [--cfg 1] [--nq 200] [--n N]
 """
@@ -23,8 +25,12 @@ X, Q, src, p = datagen.workload(a.cfg, device="cuda", nq=a.nq, n_override=a.n)
 params = ssh.SshParams(**p)
 ds = ssh.Dataset(X)
 Qd = torch.from_numpy(Q).cuda()
+ssh.index.get_context(0, params, X.shape[1])  # context setup (CWS tables) outside the range
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
 for _ in range(a.reps):
     idx = ssh.build_index(ds, params)
     out = query_batch_device(idx, Qd, 10)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok", float(out[3].double().mean()), out[4].double().mean(0).tolist())

@@ -1,7 +1,9 @@
 #!/bin/bash
-# ncu captures of this round (run under gpurun; outputs in gpurun_out/):
-# per-kernel metrics of one build + one 1000-query batch for configs[1..3],
-# and --set full of the DTW kernels.  bash scripts/profile_r02.sh [what...]
+# ncu captures of this round (run under gpurun; outputs in gpurun_out/prof/):
+# per-kernel metrics of one build + one query batch for configs[1..3]
+# (profile_once.py brackets them with cudaProfilerStart/Stop), the launch list
+# of the bench command, and --set full of single kernels.
+#   bash scripts/profile_r02.sh met1 met2 met3 launches full_<kernel-regex>[@skip] ...
 set -u
 O=gpurun_out/prof
 mkdir -p $O
@@ -10,22 +12,24 @@ python -c "import sys; sys.path.insert(0,'.'); from paper_1610_07328_b200 import
 for w in "$@"; do
   case $w in
     met1|met2|met3)
-      c=${w#met}
-      timeout 1200 ncu --metrics $M --clock-control none --csv --log-file $O/met_cfg$c.csv \
-        python scripts/profile_once.py --cfg $c --nq 1000 > $O/met_cfg$c.log 2>&1
+      c=${w#met}; nq=1000; [ $c = 3 ] && nq=200
+      timeout 1500 ncu --profile-from-start off --metrics $M --clock-control none --csv --log-file $O/met_cfg$c.csv \
+        python scripts/profile_once.py --cfg $c --nq $nq > $O/met_cfg$c.log 2>&1
       echo "met cfg$c rc=$?" ;;
-    full_dtw3)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:dtw32w --launch-skip 1 -c 1 \
-        -o $O/dtw32w_cfg3 python scripts/profile_once.py --cfg 3 --n 1000000 --nq 100 > $O/full_dtw3.log 2>&1
-      echo "full dtw3 rc=$?" ;;
-    full_dtw1)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:dtwp_level --launch-skip 3 -c 1 \
-        -o $O/dtwp_cfg1 python scripts/profile_once.py --cfg 1 --nq 1000 > $O/full_dtw1.log 2>&1
-      echo "full dtw1 rc=$?" ;;
+    launches)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-file $O/launches_cfg1.csv \
+        python bench.py --steps 2 --warmup 1 --no-extra --no-e2e --no-cpu-baseline > $O/launches.log 2>&1
+      echo "launches rc=$?" ;;
     full_*)
-      k=${w#full_}
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
-        -o $O/$k python scripts/profile_once.py --cfg 1 --nq 1000 > $O/full_$k.log 2>&1
-      echo "full $k rc=$?" ;;
+      spec=${w#full_}; k=${spec%@*}; skip=0; [ "$spec" != "$k" ] && skip=${spec#*@}
+      cfg=1; case $k in dtw32w*) cfg=3;; esac
+      timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:$k \
+        --launch-skip $skip -c 1 -o $O/full_$k python scripts/profile_once.py --cfg $cfg --nq 1000 > $O/full_$k.log 2>&1
+      echo "full $k rc=$?"
+      # reports are large (gpurun copies back <= 64 MiB): keep the details page
+      # and the per-line source summary, drop the report
+      ncu -i $O/full_$k.ncu-rep --page details --csv > $O/full_${k}_details.csv 2>/dev/null
+      python scripts/ncu_lines.py $O/full_$k.ncu-rep "$k" --top 40 > $O/full_${k}_lines.txt 2>/dev/null
+      rm -f $O/full_$k.ncu-rep ;;
   esac
 done

@@ -298,3 +298,29 @@ def test_merge_topk_kernel_matches_lexsort(cuda, lists, k_in, k_out):
     assert np.array_equal(mi.cpu().numpy(), want_i)
     assert np.array_equal(md.cpu().numpy(), want_d)
     assert np.array_equal(n.cpu().numpy(), (want_i >= 0).sum(1))
+
+
+@pytest.mark.parametrize("m,bits,f64", [(512, 64, False), (512, 100, True), (301, 16, False), (1024, 256, True),
+                                         (96, 300, False)])
+def test_srp_tensor_cores_vs_f64(cuda, m, bits, f64):
+    """srp_matrix on the tensor cores (tcgen05 TF32 screen + f64 recheck; bits
+    > 256 take the SIMT fp32 path) equals the SIMT kernel and numpy's f64
+    product signs (index.py:420-423) wherever the f64 value is not within a
+    few ulps of zero; float64 inputs are rechecked in float64."""
+    import paper_1610_07328_b200 as ssh
+
+    rng = np.random.default_rng(m + bits)
+    X = np.cumsum(rng.standard_normal((3000, m)), axis=1)
+    X = (X - X.mean(1, keepdims=True)) / X.std(1, keepdims=True)
+    X[5] = 0.0  # all-zero row: every projection is 0 -> +1
+    Xin = X if f64 else X.astype(np.float32)
+    st = {}
+    got = ssh.srp_matrix(Xin, bits, 7, stats=st)
+    simt = ssh.srp_matrix(Xin, bits, 7, tensor_cores=False)
+    proj = np.asarray(Xin, dtype=np.float64) @ ssh.srp_vectors(m, bits, 7).T
+    want = np.where(proj >= 0.0, 1, -1).astype(np.int8)
+    safe = np.abs(proj) > 1e-9 * np.sqrt(m) * 10
+    assert np.array_equal(got[safe], want[safe]) and np.array_equal(simt[safe], want[safe])
+    assert np.array_equal(got, simt)
+    assert (got[5] == 1).all()
+    assert st["rechecked"] < 0.2 * got.size
