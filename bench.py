@@ -136,11 +136,13 @@ def _free_port() -> int:
 
 def relaunch_under_torchrun(args) -> int:
     """`bench.py --gpus N` run directly: one rank per GPU under torch.distributed.run."""
+    # the ranks get this command line through the environment: torchrun's own
+    # parser would take abbreviations of its options (e.g. --n) after the script
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
-           *sys.argv[1:]]
-    print("relaunch: " + " ".join(cmd), file=sys.stderr, flush=True)
-    return subprocess.call(cmd)
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve())]
+    env = dict(os.environ, SSH_BENCH_ARGV=json.dumps(sys.argv[1:]))
+    print("relaunch: " + " ".join(cmd) + " (args " + " ".join(sys.argv[1:]) + ")", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 # ----------------------------------------------------------------- our arm
@@ -756,7 +758,8 @@ def main():
     ap.add_argument("--cpu-build-sample", type=int, default=100_000)
     ap.add_argument("--cpu-query-index", type=int, default=1_000_000)
     ap.add_argument("--cpu-queries", type=int, default=24)
-    args = ap.parse_args()
+    argv = json.loads(os.environ["SSH_BENCH_ARGV"]) if os.environ.get("SSH_BENCH_ARGV") else None
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
