@@ -1911,7 +1911,8 @@ __device__ __forceinline__ void dv_group(float2 (&P)[C2], unsigned long long (&N
         float xa;
         if (CHECK) xa = (unsigned)iA < (unsigned)m ? __ldg(xg + U) : 0.f;
         else xa = __ldg(xg + U);
-        dv_step<C2, U, MASK>(P, NY, xb, xa, iA, lane, olane, ocomp, cst, nyb[U]);
+        const float y31 = nyb[U];
+        dv_step<C2, U, MASK>(P, NY, xb, xa, iA, lane, olane, ocomp, cst, y31);
         if (CHECK && lane == rlane && iA - rcomp == m - 1) {
 #pragma unroll
             for (int c = 0; c < C2; c++)
@@ -1980,7 +1981,7 @@ dtw32v_kernel(const float *__restrict__ X, int m, int r_rt, const float *__restr
         // the group-end steps s = (g + 1) C2 - 1 (rows >= m add nothing)
         float carry = 0.f;
         if (vec) {
-#pragma unroll 4
+#pragma unroll 1
             for (int i0 = 0; i0 < G * GS; i0 += 128) {
                 const int i = i0 + 4 * lane;
                 float v2[4] = {0.f, 0.f, 0.f, 0.f};
@@ -2280,7 +2281,7 @@ struct DtwCommon {
 #define DTWP_MINB 1
 #endif
 #ifndef DTWP_MINB_NARROW
-#define DTWP_MINB_NARROW 1  // radii <= 26 (A/B: 3 blocks/SM at 168 registers)
+#define DTWP_MINB_NARROW 3  // radii <= 26: 3 blocks/SM at 168 registers (6.44 vs 6.77 ms per configs[1] batch at 1)
 #endif
 #ifndef DTWP_BLOCKCUT
 #define DTWP_BLOCKCUT 1  // one cut test per 4-row block on the band minimum (else per row)
