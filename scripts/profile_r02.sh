@@ -20,11 +20,12 @@ for w in "$@"; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-file $O/launches_cfg1.csv \
         python bench.py --steps 2 --warmup 1 --no-extra --no-e2e --no-cpu-baseline > $O/launches.log 2>&1
       echo "launches rc=$?" ;;
-    full_*)
-      spec=${w#full_}; k=${spec%@*}; skip=0; [ "$spec" != "$k" ] && skip=${spec#*@}
-      cfg=1; case $k in dtw32w*) cfg=3;; esac
+    full_*|full3_*)
+      spec=${w#full_}; spec=${spec#full3_}; spec=${spec#3_}; k=${spec%@*}; skip=0; [ "$spec" != "$k" ] && skip=${spec#*@}
+      cfg=1; n=""; case $k in dtw32w*) cfg=3;; esac
+      case $w in full3_*) cfg=3; n="--n 1000000";; esac
       timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:$k \
-        --launch-skip $skip -c 1 -o $O/full_$k python scripts/profile_once.py --cfg $cfg --nq 1000 > $O/full_$k.log 2>&1
+        --launch-skip $skip -c 1 -o $O/full_$k python scripts/profile_once.py --cfg $cfg $n --nq 1000 > $O/full_$k.log 2>&1
       echo "full $k rc=$?"
       # reports are large (gpurun copies back <= 64 MiB): keep the details page
       # and the per-line source summary, drop the report
