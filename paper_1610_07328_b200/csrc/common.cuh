@@ -10,6 +10,7 @@
 #define SSH_MAX_W 256
 #define SSH_MAX_N 20          // table-based CWS: 2^n x S variates resident in HBM
 #define SSH_MAX_SLOTS 256     // K*L
+#define SSH_MAX_K 16384       // top-k per query (shared-memory top-k state: 12 B per next_pow2(k))
 #define SSH_SALT_KEY 0xEB44ACCAB455D165ULL
 
 // --------------------------------------------------------------- errors

@@ -622,6 +622,7 @@ int ssh_launch_summaries_rows(ssh_ctx *ctx, ssh_index *ix, const float *X, int64
     SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * g.nwb, smem);
+    if (const char *ev = getenv("SSH_SUM_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(ev)));
     const int grid = (int)std::min<int64_t>((n + g.nwb - 1) / g.nwb, (int64_t)ctx->num_sms * std::max(1, per_sm));
     kern<<<grid, 32 * g.nwb, smem, st>>>(a);
     SSH_CHECK_LAUNCH();
@@ -3051,7 +3052,7 @@ __global__ void wave_update_kernel(const int *__restrict__ act, const float *__r
                                    uint32_t *__restrict__ keep_rows, float *__restrict__ keep_d32,
                                    int *__restrict__ keep_cnt, int kcap) {
     __shared__ int red[32];
-    __shared__ uint32_t tmp[2048];
+    extern __shared__ uint32_t tmp[];  // k entries
     __shared__ int npos;
     const int slot = blockIdx.x;
     const int q = act[slot];
@@ -3833,7 +3834,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     SSH_REQUIRE(ctx->have_params, SSH_ERR_STATE, "ssh_query_batch: params not set");
     SSH_REQUIRE(ix->L == ctx->p.L, SSH_ERR_INVALID, "ssh_query_batch: index/ctx table count mismatch");
     SSH_REQUIRE(k >= 1, SSH_ERR_INVALID, "k must be >= 1, got %d", k);
-    SSH_REQUIRE(k <= 2048, SSH_ERR_UNSUPPORTED, "k=%d exceeds the device limit 2048", k);
+    SSH_REQUIRE(k <= SSH_MAX_K, SSH_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, SSH_MAX_K);
     SSH_REQUIRE(nq >= 0, SSH_ERR_INVALID, "nq must be >= 0");
     if (nq == 0) return SSH_OK;
     SSH_REQUIRE(X && Q && out_ids && out_d2 && n_out && n_cand && counters && status, SSH_ERR_INVALID,
@@ -3857,7 +3858,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
 #endif
     const int W0 = ((std::max(SSH_W0, 2 * k) + 31) / 32) * 32;
     const int WCAP = std::max(W0, 16384);
-    const int KCAP = 4096 + 4 * k;
+    int KCAP = 4096 + 4 * k;  // per-query rescoring-list capacity; grows (and the slice reruns) when ties overflow it
     const int fallback = (flags & SSH_QUERY_FALLBACK_ON_EMPTY) ? 1 : 0;
     const bool exact = (flags & SSH_QUERY_EXACT) != 0 || !ix->keys;
     // query chunk: membership bitmaps <= 1 GiB; within a chunk, sub-ranges of
@@ -3866,6 +3867,8 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     qc64 = std::min<int64_t>(qc64, ((int64_t)1 << 28) / std::max<int64_t>(1, NW));
     const int qc = (int)std::max<int64_t>(1, qc64);
     SSH_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 5 * (size_t)nq, st));
+    SSH_CUDA(cudaFuncSetAttribute(wave_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(uint32_t) * SSH_MAX_K)));
     SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(MB_WARPS * 1024 * 8)));
     SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -4052,7 +4055,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                     if (ctx->profile && getenv("SSH_DEBUG_WAVES"))
                         fprintf(stderr, "round %d wave %d: active %d wave %d cap %d | LB %.3f ms DTW %.3f ms\n", round,
                                 it, nact, wave, wcap, lb_ms, pf.last);
-                    wave_update_kernel<<<nact, 256, 0, st>>>(S.act, wd32, wrows, S.wcnt, wcap, lb_s, S.roff, S.mcnt,
+                    wave_update_kernel<<<nact, 256, sizeof(uint32_t) * (size_t)k, st>>>(S.act, wd32, wrows, S.wcnt, wcap, lb_s, S.roff, S.mcnt,
                                                              S.binhi, wave, k, eps, topk, S.thr, S.pos, S.done,
                                                              S.overflow, keep_rows, keep_d32, S.keep_cnt, KCAP);
                     SSH_CHECK_LAUNCH();
@@ -4081,9 +4084,19 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             int maxkeep = 0;
             rc = max_of(S.keep_cnt, ns, st, &maxkeep);
             if (rc) return rc;
-            SSH_REQUIRE(maxkeep <= KCAP, SSH_ERR_UNSUPPORTED,
-                        "ssh_query_batch: %d candidates within the rescoring margin of one query "
-                        "(limit %d; massively tied distances)", maxkeep, KCAP);
+            if (maxkeep > KCAP) {
+                // massively tied distances (e.g. thousands of duplicate series): more
+                // candidates within the rescoring margin than the keep lists hold.  The
+                // reference cascade always answers (dtw.py:171-236), so the slice is
+                // searched again with lists that hold every such candidate
+                // (keep_cnt counted all of them, an upper bound of the rerun's need).
+                SSH_REQUIRE((int64_t)maxkeep <= N + 1, SSH_ERR_STATE,
+                            "ssh_query_batch: keep count %d exceeds the shard size", maxkeep);
+                KCAP = (maxkeep + 1023) & ~1023;
+                SSH_CUDA(cudaMemsetAsync(c5s, 0, sizeof(long long) * 5 * (size_t)ns, st));
+                if (ctx->profile) ctx->prof[20] += 1;
+                continue;  // sa unchanged: same slice, larger lists
+            }
             // K9/K10: rescoring set, exact f64 DTW, top-k by (d64, id)
             pf.begin();
             select_kernel<<<ns, 256, 0, st>>>(keep_rows, keep_d32, S.keep_cnt, KCAP, k, eps, resc, S.rcnt, c5s,

@@ -7,6 +7,7 @@ bit-identical to the reference's f64 DTW (the device rescoring is exact)."""
 
 import ctypes
 import hashlib
+import warnings
 
 import numpy as np
 import pytest
@@ -318,6 +319,33 @@ def test_duplicates_tie_break_by_id(cuda):
         assert r.ids == ores["ids"][i][:n].tolist()
         assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist()
     assert res[0].ids[:3] == [7, 57, 107]
+
+
+def test_massive_ties_beyond_rescoring_lists(cuda):
+    """6,000 copies of one series: every copy ties at distance 0 with the query,
+    far more than the rescoring lists (4096 + 4k) hold.  The reference cascade
+    (dtw.py:171-236) always answers; the device path grows the lists and
+    searches the slice again instead of failing: ids 0..k-1 (ties by id),
+    distances 0, |R| equal to the oracle's, also next to an ordinary query."""
+    import paper_1610_07328_b200 as ssh
+
+    X, _, _, band = case_data("rw512")
+    Xd = np.concatenate([np.repeat(X[3:4], 6000, axis=0), X[:200]]).astype(np.float32)
+    idx = ssh.build_index(ssh.Dataset(Xd), params(band, K=4))
+    oidx = O.build_index(Xd, 80, 3, 15, 20, 4, 0, band)
+    Q = np.stack([X[3], X[150] + 0.01, X[3] + 1e-4])
+    for k in (10, 50):
+        res = ssh.query_index_batch(idx, Q, k)
+        ores = O.query_batch(oidx, Q, k)
+        for i, r in enumerate(res):
+            n = int(ores["n"][i])
+            assert r.stats.candidates == int(ores["n_cand"][i]), (k, i)
+            assert r.ids == ores["ids"][i][:n].tolist(), (k, i)
+            assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), (k, i)
+        assert res[0].ids == list(range(k)) and set(res[0].distances) == {0.0}
+    # the per-query counters still add up to |R| after the rerun
+    st = res[0].stats.cascade
+    assert (st.kim_pruned + st.keogh_pruned + st.keogh2_pruned + st.dtw_computed) == res[0].stats.candidates
 
 
 def test_constant_and_edge_shapes(cuda):
@@ -721,6 +749,30 @@ def test_large_k_vs_oracle(cuda):
         n = int(ores["n"][i])
         assert r.ids == ores["ids"][i][:n].tolist(), i
         assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
+
+
+def test_k_beyond_2048_vs_oracle(cuda):
+    """k = 3000 of a 4,000-series shard (the round-1 device limit was 2048; the
+    reference accepts any k, index.py:204-232) and k = 16384 clamped to N."""
+    import paper_1610_07328_b200 as ssh
+    from fixture_data import perturbed_queries, random_walks
+
+    X = random_walks(4000, 256, 99)
+    Q, _ = perturbed_queries(X, 3, 17)
+    p = ssh.SshParams(W=16, delta=2, n=4, d=3, band=0.05, K=1)  # short shingles: R is most of the shard
+    idx = ssh.build_index(ssh.Dataset(X), p)
+    oidx = O.build_index(X, 16, 2, 4, 3, 1, 0, 0.05)
+    for k in (3000, 16384):
+        kk = min(k, 4000)
+        ores = O.query_batch(oidx, Q, kk)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            res = ssh.query_index_batch(idx, Q, k)
+        for i, r in enumerate(res):
+            n = int(ores["n"][i])
+            assert n > 2048 and len(r.ids) == n, (k, i, n)
+            assert r.ids == ores["ids"][i][:n].tolist(), (k, i)
+            assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), (k, i)
 
 
 def _dec32(c, sc, lo):
