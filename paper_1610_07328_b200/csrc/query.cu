@@ -42,6 +42,7 @@
 #define MB_THREADS 256
 #define MB_WARPS (MB_THREADS / 32)
 #define MB_SLICE_WORDS 256
+#define MB_WARP_BYTES (1024 * 6)  // per warp: 1024 u16 member slots + 1024 f32 partial sums
 #define NBINS 2048
 #define U32_EPS (1.0f / 16777216.0f)
 
@@ -713,9 +714,11 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
     const int q = blockIdx.y;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nseg = a.nseg;
-    uint32_t *list = reinterpret_cast<uint32_t *>(msm) + w * 1024;
-    float *accb = reinterpret_cast<float *>(msm) + MB_WARPS * 1024 + w * 1024;
-    unsigned *shist = reinterpret_cast<unsigned *>(msm) + 2 * MB_WARPS * 1024;  // SAMPLE: NBINS
+    // member slots hold the bit position within the warp's 32-word chunk
+    // (lane of the word * 32 + bit), 2 bytes each: 6 KB per warp, 4 blocks/SM
+    uint16_t *list = reinterpret_cast<uint16_t *>(msm) + w * 1024;
+    float *accb = reinterpret_cast<float *>(msm + MB_WARPS * 2048) + w * 1024;
+    unsigned *shist = reinterpret_cast<unsigned *>(msm + MB_WARPS * MB_WARP_BYTES);  // SAMPLE: NBINS
     int blo = 0, bhi = NBINS - 1;
     if (!SAMPLE) {
         blo = a.binlo[q];
@@ -763,9 +766,14 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
             int b = __ffs(word) - 1;
             word &= word - 1;
             SSH_DASSERT(pos < 1024);
-            list[pos++] = (uint32_t)(wd * 32 + b);
+            list[pos++] = (uint16_t)(lane * 32 + b);
         }
         __syncwarp();
+        // slot -> series row (the sample pass strides its words by 2^SAMPLE_SHIFT)
+        const int64_t row0 = wb * 32;
+        auto slot_row = [&](uint32_t sl) -> uint32_t {
+            return (uint32_t)(row0 + (SAMPLE ? ((int64_t)(sl >> 5) << (5 + SAMPLE_SHIFT)) + (sl & 31u) : (int64_t)sl));
+        };
         // three passes over the list, one 16-segment group each; after each
         // pass the members still below the edge are compacted in place (rows
         // in list, partial sums in accb) so every pass runs on full warps
@@ -775,13 +783,14 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
             // the next 32 members' records are loaded one iteration ahead (L2
             // latency overlaps this iteration's arithmetic); compaction only
             // writes list/accb below e0 + 32, ahead of the prefetched entries
-            uint32_t rowN = 0;
+            uint32_t rowN = 0, slN = 0;
             float accN = 0.f;
             float2 hN = make_float2(0.f, 0.f);
             uint4 cgN = make_uint4(0u, 0u, 0u, 0u);
             auto fetch = [&](int e) {
                 if (e < n) {
-                    rowN = list[e];
+                    slN = list[e];
+                    rowN = slot_row(slN);
                     accN = g ? accb[e] : 0.f;
                     const uint4 *rp = a.rec + (int64_t)rowN * 4;
                     hN = __ldg(reinterpret_cast<const float2 *>(rp));
@@ -793,7 +802,7 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                 const int e = e0 + lane;
                 bool keep = false;
                 float acc = accN, key = 0.f;
-                const uint32_t row = rowN;
+                const uint32_t row = rowN, sl = slN;
                 const float2 h = hN;
                 const uint4 cg = cgN;
                 fetch(e + 32);
@@ -828,10 +837,10 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                         keep = SAMPLE || acc * wseg * shrink * (1.f - 4.f * U32_EPS) < edge;
                     } else {
                         // the last segment has lastlen <= seg samples: remove its excess weight
-                        const int sl = nseg - 1;
-                        const uint32_t lw = __ldg(reinterpret_cast<const uint32_t *>(rp) + 4 + (sl >> 2));
-                        const float cf = code_f(lw, sl & 3);
-                        const float ev = fmaxf(fmaxf(fmaf(cf, sc, lo) + sUL[sl].x, sUL[sl].y - fmaf(cf + 1.f, sc, lo)), 0.f);
+                        const int sg = nseg - 1;
+                        const uint32_t lw = __ldg(reinterpret_cast<const uint32_t *>(rp) + 4 + (sg >> 2));
+                        const float cf = code_f(lw, sg & 3);
+                        const float ev = fmaxf(fmaxf(fmaf(cf, sc, lo) + sUL[sg].x, sUL[sg].y - fmaf(cf + 1.f, sc, lo)), 0.f);
                         const float paa = fmaxf(fmaf(-(segf - lastlen) * ev, ev, acc * segf), 0.f) * shrink;
                         const float2 kx = __ldg(reinterpret_cast<const float2 *>(rp) + 1);
                         const float d0 = kx.x - q0, dl = kx.y - ql;
@@ -847,7 +856,7 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                     __syncwarp();
                     if (keep) {
                         const int p = nk + __popc(km & ((1u << lane) - 1u));
-                        list[p] = row;
+                        list[p] = (uint16_t)sl;
                         accb[p] = acc;
                     }
                     nk += __popc(km);
@@ -857,17 +866,28 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                     const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
                     if (keep && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&shist[bin], (unsigned)__popc(peers));
                 } else {
+                    // kept members compact in place like the earlier passes (rows in
+                    // list, keys in accb); the chunk's kept run is reserved with one
+                    // atomic and copied out after the pass
                     const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
-                    if (km) {
-                        int dst = 0;
-                        if (lane == 0) dst = atomicAdd(&a.cnt[q], __popc(km));
-                        dst = __shfl_sync(0xFFFFFFFFu, dst, 0) + __popc(km & ((1u << lane) - 1u));
-                        if (keep) {
-                            SSH_DASSERT(base_q + dst < a.roff[q + 1]);
-                            a.rows[base_q + dst] = row;
-                            a.lb[base_q + dst] = key;
-                        }
+                    __syncwarp();
+                    if (keep) {
+                        const int p = nk + __popc(km & ((1u << lane) - 1u));
+                        list[p] = (uint16_t)sl;
+                        accb[p] = key;
                     }
+                    nk += __popc(km);
+                    __syncwarp();
+                }
+            }
+            if (!SAMPLE && g == 2 && nk > 0) {
+                int dst = 0;
+                if (lane == 0) dst = atomicAdd(&a.cnt[q], nk);
+                dst = __shfl_sync(0xFFFFFFFFu, dst, 0);
+                SSH_DASSERT(base_q + dst + nk <= a.roff[q + 1]);
+                for (int e = lane; e < nk; e += 32) {
+                    a.rows[base_q + dst + e] = slot_row(list[e]);
+                    a.lb[base_q + dst + e] = accb[e];
                 }
             }
             n = nk;
@@ -3874,9 +3894,9 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
     SSH_CUDA(cudaFuncSetAttribute(wave_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(uint32_t) * SSH_MAX_K)));
     SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(MB_WARPS * 1024 * 8)));
+                                  (int)(MB_WARPS * MB_WARP_BYTES)));
     SSH_CUDA(cudaFuncSetAttribute(paa_members_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(MB_WARPS * 1024 * 8 + NBINS * 4)));
+                                  (int)(MB_WARPS * MB_WARP_BYTES + NBINS * 4)));
     for (int q0 = 0; q0 < nq; q0 += qc) {
         const int nc = std::min(qc, nq - q0);
         const float *Qc = Q + (int64_t)q0 * m;
@@ -3969,7 +3989,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
             {
                 SSH_CUDA(cudaMemsetAsync(khist, 0, sizeof(unsigned) * (size_t)ns * NBINS, st));
                 const dim3 gs((unsigned)ssh_div_up(NW, (int64_t)MB_SLICE_WORDS << SAMPLE_SHIFT), (unsigned)ns);
-                paa_members_kernel<true><<<gs, MB_THREADS, MB_WARPS * 1024 * 8 + NBINS * 4, st>>>(pa);
+                paa_members_kernel<true><<<gs, MB_THREADS, MB_WARPS * MB_WARP_BYTES + NBINS * 4, st>>>(pa);
                 SSH_CHECK_LAUNCH();
                 cutoff_kernel<<<ns, 256, 0, st>>>(khist, member_target, S.binlo, S.binhi);
                 SSH_CHECK_LAUNCH();
@@ -3996,7 +4016,7 @@ extern "C" int ssh_query_batch(ssh_ctx *ctx, const ssh_index *ix, const float *X
                     SSH_CHECK_LAUNCH();
                 }
                 SSH_CUDA(cudaMemsetAsync(S.mcnt, 0, sizeof(int) * ns, st));
-                paa_members_kernel<false><<<gm, MB_THREADS, MB_WARPS * 1024 * 8, st>>>(pa);
+                paa_members_kernel<false><<<gm, MB_THREADS, MB_WARPS * MB_WARP_BYTES, st>>>(pa);
                 SSH_CHECK_LAUNCH();
                 if (round == 0) {
                     binsort_kernel<<<ns, 1024, 0, st>>>(rows_u, lb_u, S.roff, S.mcnt, rows_s, lb_s);
