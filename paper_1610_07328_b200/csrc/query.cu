@@ -698,6 +698,19 @@ struct PaaArgs {
     int m, seg, nseg;
 };
 
+// 256-bit read-only global load (sm_100 LDG.E.ENL2.256): p 32-byte aligned
+struct __align__(32) U32x8 {
+    uint32_t v[8];
+};
+__device__ __forceinline__ U32x8 ldg256(const void *p) {
+    U32x8 r;
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+                   "=r"(r.v[6]), "=r"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+
 __device__ __forceinline__ float code_f(uint32_t w, int t) {
     // byte t of w as an exact float (0x4B0000cc = 2^23 + cc)
     return __uint_as_float(__byte_perm(w, 0x4B000000u, (unsigned)t | 0x7440u)) - 8388608.f;
@@ -785,7 +798,7 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
             // writes list/accb below e0 + 32, ahead of the prefetched entries
             uint32_t rowN = 0, slN = 0;
             float accN = 0.f;
-            float2 hN = make_float2(0.f, 0.f);
+            float4 hN = make_float4(0.f, 0.f, 0.f, 0.f);  // lo, sc, x_0, x_last
             uint4 cgN = make_uint4(0u, 0u, 0u, 0u);
             auto fetch = [&](int e) {
                 if (e < n) {
@@ -793,8 +806,22 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                     rowN = slot_row(slN);
                     accN = g ? accb[e] : 0.f;
                     const uint4 *rp = a.rec + (int64_t)rowN * 4;
-                    hN = __ldg(reinterpret_cast<const float2 *>(rp));
-                    cgN = __ldg(rp + 1 + g);
+                    if (g == 0) {
+                        // header and the first code group share the record's first 32-byte
+                        // sector: one 256-bit gather instead of two (the kernel is bound by
+                        // the L1 tag stage of these scattered loads)
+                        const U32x8 v = ldg256(rp);
+                        hN = make_float4(__uint_as_float(v.v[0]), __uint_as_float(v.v[1]), 0.f, 0.f);
+                        cgN = make_uint4(v.v[4], v.v[5], v.v[6], v.v[7]);
+                    } else if (g == 1) {
+                        const float2 h2 = __ldg(reinterpret_cast<const float2 *>(rp));
+                        hN = make_float4(h2.x, h2.y, 0.f, 0.f);
+                        cgN = __ldg(rp + 2);
+                    } else {
+                        // the last pass also needs x_0 / x_last (LB_Kim): the whole header in one gather
+                        hN = __ldg(reinterpret_cast<const float4 *>(rp));
+                        cgN = __ldg(rp + 3);
+                    }
                 }
             };
             fetch(lane);
@@ -803,7 +830,7 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                 bool keep = false;
                 float acc = accN, key = 0.f;
                 const uint32_t row = rowN, sl = slN;
-                const float2 h = hN;
+                const float4 h = hN;
                 const uint4 cg = cgN;
                 fetch(e + 32);
                 if (e < n) {
@@ -814,8 +841,12 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                     // packed f32x2, the same IEEE operations as the scalar
                     // forms: {xa, xb} = fma({c, c + 1}, sc, lo) and
                     // {xa - U, L - xb} = fma({xa, xb}, {1, -1}, {-U, L})
-                    const float2 sc2 = make_float2(sc, sc), lo2 = make_float2(lo, lo);
-                    const float2 off = make_float2(-8388608.f, -8388607.f), pm = make_float2(1.f, -1.f);
+                    // upper end: fma(c, sc, lo_hi) with lo_hi = RU(lo + sc) is never below
+                    // dec(c + 1) = fma(c + 1, sc, lo) (c sc + lo_hi >= (c + 1) sc + lo before
+                    // the one rounding), so it still brackets the mean from above; one scalar
+                    // FADD converts the code instead of an f32x2 add with a constant pair
+                    const float2 sc2 = make_float2(sc, sc), loh = make_float2(lo, __fadd_ru(lo, sc));
+                    const float2 pm = make_float2(1.f, -1.f);
                     float2 acc2 = make_float2(acc, 0.f);
 #pragma unroll
                     for (int j = 0; j < 16; j += 2) {
@@ -825,7 +856,8 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                             const int jj = j + u;
                             const float r = __uint_as_float(__byte_perm(cw[jj >> 2], 0x4B000000u,
                                                                         (unsigned)(jj & 3) | 0x7440u));
-                            const float2 x = __ffma2_rn(__fadd2_rn(make_float2(r, r), off), sc2, lo2);
+                            const float cf = r - 8388608.f;
+                            const float2 x = __ffma2_rn(make_float2(cf, cf), sc2, loh);
                             const float2 df = __ffma2_rn(x, pm, sUL[16 * g + jj]);
                             ev[u] = fmaxf(fmaxf(df.x, df.y), 0.f);
                         }
@@ -838,12 +870,14 @@ __global__ void __launch_bounds__(MB_THREADS) paa_members_kernel(PaaArgs a) {
                     } else {
                         // the last segment has lastlen <= seg samples: remove its excess weight
                         const int sg = nseg - 1;
-                        const uint32_t lw = __ldg(reinterpret_cast<const uint32_t *>(rp) + 4 + (sg >> 2));
+                        // its code word is in this pass's group when sg >= 32 (no extra gather)
+                        const int wi = (sg >> 2) - 8;
+                        const uint32_t lw = wi < 0 ? __ldg(reinterpret_cast<const uint32_t *>(rp) + 4 + (sg >> 2))
+                                            : wi == 0 ? cg.x : wi == 1 ? cg.y : wi == 2 ? cg.z : cg.w;
                         const float cf = code_f(lw, sg & 3);
                         const float ev = fmaxf(fmaxf(fmaf(cf, sc, lo) + sUL[sg].x, sUL[sg].y - fmaf(cf + 1.f, sc, lo)), 0.f);
                         const float paa = fmaxf(fmaf(-(segf - lastlen) * ev, ev, acc * segf), 0.f) * shrink;
-                        const float2 kx = __ldg(reinterpret_cast<const float2 *>(rp) + 1);
-                        const float d0 = kx.x - q0, dl = kx.y - ql;
+                        const float d0 = h.z - q0, dl = h.w - ql;
                         const float kim = a.m >= 2 ? fmaf(dl, dl, d0 * d0) : d0 * d0;
                         if (kim > paa) key = __uint_as_float(__float_as_uint(kim * (1.f - 2.f * U32_EPS)) | 1u);
                         else key = __uint_as_float(__float_as_uint(paa) & ~1u);
