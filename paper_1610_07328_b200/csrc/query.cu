@@ -329,6 +329,7 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 // running max doubling of one padded u16 code array held in registers
 // (two codes per word, native VIMNMX.U16x2): lane owns words
@@ -384,19 +385,20 @@ struct SumArgs {
     const float *X;
     int64_t N, ld, cstride;
     int m, r, lev, pad, seg, nseg, mp, warp_bytes;
+    int single;  // one row buffer per warp: the next row streams in while the envelope codes are computed
     uint4 *rec;
     uint8_t *codes;
 };
 
 template <int WPL>
-__global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 12) ? 4 : 1) summaries_kernel(SumArgs a) {
+__global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries_kernel(SumArgs a) {
     extern __shared__ __align__(16) unsigned char xsmb[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     const int m = a.m, pad = a.pad, padw = pad >> 1;
     unsigned char *base = xsmb + (size_t)w * a.warp_bytes;
     const int mq = (m + 3) & ~3;
-    float *xbuf = reinterpret_cast<float *>(base);                    // 2 x mq samples (double buffer)
-    uint32_t *cmx = reinterpret_cast<uint32_t *>(xbuf + 2 * mq);     // pad u16: codes, 0 outside
+    float *xbuf = reinterpret_cast<float *>(base);                    // 2 x mq samples (double buffer), or 1 x mq
+    uint32_t *cmx = reinterpret_cast<uint32_t *>(xbuf + (a.single ? 1 : 2) * mq);  // pad u16: codes, 0 outside
     uint32_t *cmn = cmx + padw;                                       // pad u16: 255 - codes, 0 outside
     uint8_t *prec = reinterpret_cast<uint8_t *>(cmn + padw);          // 64-byte record staging
     uint16_t *bmx = reinterpret_cast<uint16_t *>(cmx), *bmn = reinterpret_cast<uint16_t *>(cmn);
@@ -418,9 +420,13 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 12) ? 4 : 1) summaries
     int64_t row = (int64_t)blockIdx.x * nwb + w;
     prefetch(row, xbuf);
     for (int buf = 0; row < a.N; row += nwarps, buf ^= 1) {
-        float *xs = xbuf + buf * mq;
-        prefetch(row + nwarps, xbuf + (buf ^ 1) * mq);
-        cp_async_wait1();
+        float *xs = a.single ? xbuf : xbuf + buf * mq;
+        if (a.single) {
+            cp_async_wait0();
+        } else {
+            prefetch(row + nwarps, xbuf + (buf ^ 1) * mq);
+            cp_async_wait1();
+        }
         __syncwarp();
         float vmin = INFINITY, vmax = -INFINITY;
         bool fin = true;
@@ -507,6 +513,9 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 12) ? 4 : 1) summaries
         if (lane == 0) *reinterpret_cast<float4 *>(prec) = make_float4(lo, ambiguous ? -sc : sc, xs[0], xs[m - 1]);
         __syncwarp();
         if (lane < 4) a.rec[row * 4 + lane] = reinterpret_cast<const uint4 *>(prec)[lane];
+        // long rows keep one row buffer (more resident warps): the samples are not
+        // read again, so the next row streams in under the envelope stage
+        if (a.single) prefetch(row + nwarps, xbuf);
         // running max of the codes and of their complements (= running min) over
         // [t, t + 2^lev) by byte-packed log-step doubling
         if (WPL > 0) {
@@ -564,7 +573,7 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 12) ? 4 : 1) summaries
 }
 
 struct SumGeom {
-    int seg, nseg, mp, lev, pad, warp_bytes, nwb;
+    int seg, nseg, mp, lev, pad, warp_bytes, nwb, single;
 };
 
 static int summaries_geom(const ssh_ctx *ctx, SumGeom &g) {
@@ -577,8 +586,17 @@ static int summaries_geom(const ssh_ctx *ctx, SumGeom &g) {
     // padded u16 code arrays: sample j at element j + r; the last doubling read
     // reaches element (m - 1) + 2r + 2^lev + 3; 4 pad % 16 == 0 keeps the record aligned
     g.pad = ((m + 2 * r + (1 << g.lev) + 12) + 7) & ~7;
-    g.warp_bytes = (((m + 3) & ~3) * 8 + 4 * g.pad + 64 + 15) & ~15;
+    // rows longer than 512 samples keep a single row buffer per warp (see the kernel);
+    // SSH_SUM_SINGLE=0/1 forces either form
+    g.single = m > 512;
+    if (const char *ev = getenv("SSH_SUM_SINGLE")) g.single = atoi(ev) != 0;
+    g.warp_bytes = (((m + 3) & ~3) * (g.single ? 4 : 8) + 4 * g.pad + 64 + 15) & ~15;
     g.nwb = (int)std::min<size_t>(8, (200 * 1024) / (size_t)g.warp_bytes);
+    // two or three blocks per SM when the rows are too long for 8 warps of one block
+    {
+        const int fit = (int)((200 * 1024) / (size_t)g.warp_bytes);  // warps per SM by shared memory
+        if (fit >= 10 && fit < 16) g.nwb = fit / 2;                  // two smaller blocks (registers allow it)
+    }
     SSH_REQUIRE(g.nwb >= 1, SSH_ERR_UNSUPPORTED, "series too long for the summaries kernel (m=%d, r=%d)", m, r);
     return SSH_OK;
 }
@@ -610,16 +628,19 @@ int ssh_launch_summaries_rows(ssh_ctx *ctx, ssh_index *ix, const float *X, int64
     int rc = summaries_geom(ctx, g);
     if (rc) return rc;
     const int m = ctx->p.m, r = ctx->p.radius;
-    SumArgs a{X, n, ld, ix->cstride, m, r, g.lev, g.pad, g.seg, g.nseg, g.mp, g.warp_bytes,
+    SumArgs a{X, n, ld, ix->cstride, m, r, g.lev, g.pad, g.seg, g.nseg, g.mp, g.warp_bytes, g.single,
               (uint4 *)ix->rec + r0 * 4, ix->codes + r0 * ix->cstride};
     const size_t smem = (size_t)g.warp_bytes * g.nwb;
     // envelope doubling in registers when the padded array fits 32 x WPL words
     // (zero margin of 2^(lev-1) words past padw: see env_doubling16)
     const int need = g.pad / 2 + (1 << g.lev) / 2;
-    auto kern = need <= 32 * 10 ? summaries_kernel<10>
-                : need <= 32 * 12 ? summaries_kernel<12>
-                : need <= 32 * 24 ? summaries_kernel<24>
-                : need <= 32 * 48 ? summaries_kernel<48> : summaries_kernel<0>;
+    // odd words-per-lane: lane l's chunk starts at word l * WPL, and an odd stride
+    // spreads the 32 lanes over all banks (WPL = 48 was a 16-way conflict on every
+    // shared-memory access of the doubling, 24 an 8-way one)
+    auto kern = need <= 32 * 11 ? summaries_kernel<11>
+                : need <= 32 * 13 ? summaries_kernel<13>
+                : need <= 32 * 25 ? summaries_kernel<25>
+                : need <= 32 * 49 ? summaries_kernel<49> : summaries_kernel<0>;
     SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * g.nwb, smem);
