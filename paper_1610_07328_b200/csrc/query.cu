@@ -456,17 +456,20 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries
         const float inv = 1.0f / sc;
         // sample codes, 4 per lane per 128-sample chunk (global) + padded byte arrays (smem)
         uint8_t *cr = a.codes + row * a.cstride;
-        const bool r_even = (a.r & 1) == 0;
+        // sample j sits at padded element j + rp, rp = r rounded up to even, so whole
+        // quads store as aligned u16 pairs for any radius; the window of sample i,
+        // [i - r, i + r], is the padded range [i + ro, i + ro + win) with ro = rp - r
+        const int ro = a.r & 1, rp = a.r + ro;
         for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
             uint32_t pk = 0;
-            if (i4 + 4 <= m && r_even) {
-                // whole quad: one LDS.128, codes packed as u16 pairs (4-byte aligned: r even)
+            if (i4 + 4 <= m) {
+                // whole quad: one LDS.128, codes packed as u16 pairs (4-byte aligned: rp even)
                 const float4 x4 = *reinterpret_cast<const float4 *>(xs + i4);
                 const int c0 = code_in(x4.x, lo, sc, inv), c1 = code_in(x4.y, lo, sc, inv);
                 const int c2 = code_in(x4.z, lo, sc, inv), c3 = code_in(x4.w, lo, sc, inv);
                 pk = (uint32_t)c0 | ((uint32_t)c1 << 8) | ((uint32_t)c2 << 16) | ((uint32_t)c3 << 24);
                 const uint32_t w01 = (uint32_t)c0 | ((uint32_t)c1 << 16), w23 = (uint32_t)c2 | ((uint32_t)c3 << 16);
-                const int wi = (a.r + i4) >> 1;
+                const int wi = (rp + i4) >> 1;
                 cmx[wi] = w01;
                 cmx[wi + 1] = w23;
                 cmn[wi] = 0x00FF00FFu - w01;
@@ -478,8 +481,8 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries
                     if (i < m) {
                         const int c = code_in(xs[i], lo, sc, inv);
                         pk |= (uint32_t)c << (8 * t);
-                        bmx[a.r + i] = (uint16_t)c;
-                        bmn[a.r + i] = (uint16_t)(255 - c);
+                        bmx[rp + i] = (uint16_t)c;
+                        bmn[rp + i] = (uint16_t)(255 - c);
                     }
                 }
             }
@@ -559,10 +562,11 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries
                 uint2 out = make_uint2(0x00FF00FFu, 0x00FF00FFu);  // U8 = 255, L8 = 0
                 if (i4 < m) {
                     // padded element i of sample i (window [i - r, i + r] -> [i, i + win))
-                    const uint32_t u01 = __vmaxu2(cmx[i4 >> 1], u16_word_at(cmx, i4 + shw)) + 0x00010001u;
-                    const uint32_t u23 = __vmaxu2(cmx[(i4 >> 1) + 1], u16_word_at(cmx, i4 + 2 + shw)) + 0x00010001u;
-                    const uint32_t l01 = __vmaxu2(cmn[i4 >> 1], u16_word_at(cmn, i4 + shw)) ^ 0x00FF00FFu;
-                    const uint32_t l23 = __vmaxu2(cmn[(i4 >> 1) + 1], u16_word_at(cmn, i4 + 2 + shw)) ^ 0x00FF00FFu;
+                    const int e4 = i4 + ro;  // window start of sample i4 (see rp above)
+                    const uint32_t u01 = __vmaxu2(u16_word_at(cmx, e4), u16_word_at(cmx, e4 + shw)) + 0x00010001u;
+                    const uint32_t u23 = __vmaxu2(u16_word_at(cmx, e4 + 2), u16_word_at(cmx, e4 + 2 + shw)) + 0x00010001u;
+                    const uint32_t l01 = __vmaxu2(u16_word_at(cmn, e4), u16_word_at(cmn, e4 + shw)) ^ 0x00FF00FFu;
+                    const uint32_t l23 = __vmaxu2(u16_word_at(cmn, e4 + 2), u16_word_at(cmn, e4 + 2 + shw)) ^ 0x00FF00FFu;
                     out = make_uint2(__byte_perm(u01, l01, 0x6240u), __byte_perm(u23, l23, 0x6240u));
                 }
                 *reinterpret_cast<uint2 *>(cr + a.mp + 2 * i4) = out;
@@ -585,7 +589,7 @@ static int summaries_geom(const ssh_ctx *ctx, SumGeom &g) {
     while ((2 << g.lev) <= 2 * r + 1) g.lev++;
     // padded u16 code arrays: sample j at element j + r; the last doubling read
     // reaches element (m - 1) + 2r + 2^lev + 3; 4 pad % 16 == 0 keeps the record aligned
-    g.pad = ((m + 2 * r + (1 << g.lev) + 12) + 7) & ~7;
+    g.pad = ((m + 2 * r + (1 << g.lev) + 13) + 7) & ~7;  // + 1: odd radii shift the samples by one element
     // rows longer than 512 samples keep a single row buffer per warp (see the kernel);
     // SSH_SUM_SINGLE=0/1 forces either form
     g.single = m > 512;
