@@ -865,8 +865,11 @@ static int launch_fast(ssh_ctx *ctx, const SigArgs &a, int64_t N, cudaStream_t s
 template <int MODE, int QL>
 static int launch_fast_v(ssh_ctx *ctx, const SigArgs &a, int64_t N, cudaStream_t st) {
     if (MODE == SIG_MODE_CWS_FROM_SETS) return launch_fast<MODE, QL, 1>(ctx, a, N, st);
-    const int v = a.T / 32;
-    if (v >= 16) return launch_fast<MODE, QL, 16>(ctx, a, N, st);
+    int v = a.T / 32;
+    // SSH_CWS_V caps the register-sorted part (32 V tokens; the rest merges 32 at a time): A/B switch
+    if (const char *ev = getenv("SSH_CWS_V")) v = std::min(v, std::max(1, atoi(ev)));
+    // 256 register-sorted tokens at most: at T = 643 (configs[3]) sorting 512 and merging 131
+    // measured 35.6 ms per 1M-row build against 32.0 ms for 256 + 387 (V = 4: 35.0 ms)
     if (v >= 8) return launch_fast<MODE, QL, 8>(ctx, a, N, st);
     if (v >= 4) return launch_fast<MODE, QL, 4>(ctx, a, N, st);
     if (v >= 2) return launch_fast<MODE, QL, 2>(ctx, a, N, st);
