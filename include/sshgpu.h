@@ -218,7 +218,10 @@ int ssh_probe(ssh_ctx *ctx, const ssh_index *idx, const uint64_t *qsig, int32_t 
  * n_out i32[nq], n_cand i64[nq] (|R|), counters i64[nq][5] =
  * [kim_pruned, keogh_pruned, keogh2_pruned, dtw_computed, dtw_abandoned]
  * (SearchStats, dtw.py:50-72; batch-order semantics),
- * status i32[nq] = 0 "ok", 1 "no-candidates", 2 "fallback" (index.py:99). */
+ * status i32[nq] = 0 "ok", 1 "no-candidates", 2 "fallback" (index.py:99).
+ * 1 <= k <= 16384 (larger: SSH_ERR_UNSUPPORTED); k > N answers with N entries.
+ * Any number of tied candidates is answered (the rescoring lists grow and the
+ * query slice reruns), as the reference cascade does (dtw.py:171-236). */
 #define SSH_QUERY_FALLBACK_ON_EMPTY 1 /* empty R -> exact search over the shard
                                          (query_index(fallback_on_empty=True),
                                          index.py:239-243) */
