@@ -623,10 +623,12 @@ __device__ int warp_dedup_split(const SigArgs &a, int64_t row, const WarpSmem &w
             const uint64_t bitsv = sh ? ((w0 >> sh) | (w1 << (64 - sh))) : w0;
             tok = __brev((uint32_t)bitsv & nmask) >> (32 - a.n);
         }
-        const unsigned peers = __match_any_sync(0xFFFFFFFFu, tok);
+        // every lane looks its token up and counts it with a shared-memory atomic
+        // (same-address atomics are cheap; __match_any_sync on every round was the
+        // larger part of this loop); only rounds that meet a new token take the
+        // match to insert each new token once
         bool need = false;
-        if (tok != 0xFFFFFFFFu && (peers & lt0) == 0) {
-            const uint32_t add = __popc(peers);
+        if (tok != 0xFFFFFFFFu) {
             int lo = 0, hi = Dm;  // first entry with token >= tok
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
@@ -637,12 +639,16 @@ __device__ int warp_dedup_split(const SigArgs &a, int64_t row, const WarpSmem &w
             if (lo < Dm && (w.ukey[lo] >> 12) == tok) pos = lo;
             for (int q = Dm; pos < 0 && q < D; q++)
                 if ((w.ukey[q] >> 12) == tok) pos = q;
-            if (pos >= 0) w.ukey[pos] += add;  // leaders hold distinct tokens
+            if (pos >= 0) atomicAdd(&w.ukey[pos], 1u);
             else need = true;
         }
-        const unsigned nm = __ballot_sync(0xFFFFFFFFu, need);
-        if (need) w.ukey[D + __popc(nm & lt0)] = (tok << 12) | __popc(peers);
-        D += __popc(nm);
+        if (__any_sync(0xFFFFFFFFu, need)) {
+            const unsigned peers = __match_any_sync(0xFFFFFFFFu, need ? tok : 0xFFFFFFFFu);
+            const bool lead = need && (peers & lt0) == 0;
+            const unsigned nm = __ballot_sync(0xFFFFFFFFu, lead);
+            if (lead) w.ukey[D + __popc(nm & lt0)] = (tok << 12) | __popc(peers);
+            D += __popc(nm);
+        }
         __syncwarp();
     }
     return D;
