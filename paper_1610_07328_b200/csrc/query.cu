@@ -390,15 +390,18 @@ struct SumArgs {
     uint8_t *codes;
 };
 
-template <int WPL>
+// GEN: the general form (single row buffer and / or odd radius); !GEN is the
+// even-radius, double-buffered form with those paths compiled out (configs[1])
+template <int WPL, bool GEN>
 __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries_kernel(SumArgs a) {
+    const bool single = GEN && a.single != 0;
     extern __shared__ __align__(16) unsigned char xsmb[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     const int m = a.m, pad = a.pad, padw = pad >> 1;
     unsigned char *base = xsmb + (size_t)w * a.warp_bytes;
     const int mq = (m + 3) & ~3;
     float *xbuf = reinterpret_cast<float *>(base);                    // 2 x mq samples (double buffer), or 1 x mq
-    uint32_t *cmx = reinterpret_cast<uint32_t *>(xbuf + (a.single ? 1 : 2) * mq);  // pad u16: codes, 0 outside
+    uint32_t *cmx = reinterpret_cast<uint32_t *>(xbuf + (single ? 1 : 2) * mq);  // pad u16: codes, 0 outside
     uint32_t *cmn = cmx + padw;                                       // pad u16: 255 - codes, 0 outside
     uint8_t *prec = reinterpret_cast<uint8_t *>(cmn + padw);          // 64-byte record staging
     uint16_t *bmx = reinterpret_cast<uint16_t *>(cmx), *bmn = reinterpret_cast<uint16_t *>(cmn);
@@ -420,8 +423,8 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries
     int64_t row = (int64_t)blockIdx.x * nwb + w;
     prefetch(row, xbuf);
     for (int buf = 0; row < a.N; row += nwarps, buf ^= 1) {
-        float *xs = a.single ? xbuf : xbuf + buf * mq;
-        if (a.single) {
+        float *xs = single ? xbuf : xbuf + buf * mq;
+        if (single) {
             cp_async_wait0();
         } else {
             prefetch(row + nwarps, xbuf + (buf ^ 1) * mq);
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries
         // sample j sits at padded element j + rp, rp = r rounded up to even, so whole
         // quads store as aligned u16 pairs for any radius; the window of sample i,
         // [i - r, i + r], is the padded range [i + ro, i + ro + win) with ro = rp - r
-        const int ro = a.r & 1, rp = a.r + ro;
+        const int ro = GEN ? (a.r & 1) : 0, rp = a.r + ro;
         for (int i4 = 4 * lane; i4 < a.mp; i4 += 128) {
             uint32_t pk = 0;
             if (i4 + 4 <= m) {
@@ -518,7 +521,7 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries
         if (lane < 4) a.rec[row * 4 + lane] = reinterpret_cast<const uint4 *>(prec)[lane];
         // long rows keep one row buffer (more resident warps): the samples are not
         // read again, so the next row streams in under the envelope stage
-        if (a.single) prefetch(row + nwarps, xbuf);
+        if (single) prefetch(row + nwarps, xbuf);
         // running max of the codes and of their complements (= running min) over
         // [t, t + 2^lev) by byte-packed log-step doubling
         if (WPL > 0) {
@@ -563,10 +566,18 @@ __global__ void __launch_bounds__(256, (WPL > 0 && WPL <= 13) ? 4 : 1) summaries
                 if (i4 < m) {
                     // padded element i of sample i (window [i - r, i + r] -> [i, i + win))
                     const int e4 = i4 + ro;  // window start of sample i4 (see rp above)
-                    const uint32_t u01 = __vmaxu2(u16_word_at(cmx, e4), u16_word_at(cmx, e4 + shw)) + 0x00010001u;
-                    const uint32_t u23 = __vmaxu2(u16_word_at(cmx, e4 + 2), u16_word_at(cmx, e4 + 2 + shw)) + 0x00010001u;
-                    const uint32_t l01 = __vmaxu2(u16_word_at(cmn, e4), u16_word_at(cmn, e4 + shw)) ^ 0x00FF00FFu;
-                    const uint32_t l23 = __vmaxu2(u16_word_at(cmn, e4 + 2), u16_word_at(cmn, e4 + 2 + shw)) ^ 0x00FF00FFu;
+                    uint32_t a01, a23, b01, b23;  // the words at the window start (aligned when r is even)
+                    if (ro == 0) {
+                        a01 = cmx[i4 >> 1]; a23 = cmx[(i4 >> 1) + 1];
+                        b01 = cmn[i4 >> 1]; b23 = cmn[(i4 >> 1) + 1];
+                    } else {
+                        a01 = u16_word_at(cmx, e4); a23 = u16_word_at(cmx, e4 + 2);
+                        b01 = u16_word_at(cmn, e4); b23 = u16_word_at(cmn, e4 + 2);
+                    }
+                    const uint32_t u01 = __vmaxu2(a01, u16_word_at(cmx, e4 + shw)) + 0x00010001u;
+                    const uint32_t u23 = __vmaxu2(a23, u16_word_at(cmx, e4 + 2 + shw)) + 0x00010001u;
+                    const uint32_t l01 = __vmaxu2(b01, u16_word_at(cmn, e4 + shw)) ^ 0x00FF00FFu;
+                    const uint32_t l23 = __vmaxu2(b23, u16_word_at(cmn, e4 + 2 + shw)) ^ 0x00FF00FFu;
                     out = make_uint2(__byte_perm(u01, l01, 0x6240u), __byte_perm(u23, l23, 0x6240u));
                 }
                 *reinterpret_cast<uint2 *>(cr + a.mp + 2 * i4) = out;
@@ -589,7 +600,7 @@ static int summaries_geom(const ssh_ctx *ctx, SumGeom &g) {
     while ((2 << g.lev) <= 2 * r + 1) g.lev++;
     // padded u16 code arrays: sample j at element j + r; the last doubling read
     // reaches element (m - 1) + 2r + 2^lev + 3; 4 pad % 16 == 0 keeps the record aligned
-    g.pad = ((m + 2 * r + (1 << g.lev) + 13) + 7) & ~7;  // + 1: odd radii shift the samples by one element
+    g.pad = ((m + 2 * r + (1 << g.lev) + 12 + (r & 1)) + 7) & ~7;  // + 1: odd radii shift the samples by one element
     // rows longer than 512 samples keep a single row buffer per warp (see the kernel);
     // SSH_SUM_SINGLE=0/1 forces either form
     g.single = m > 512;
@@ -641,10 +652,12 @@ int ssh_launch_summaries_rows(ssh_ctx *ctx, ssh_index *ix, const float *X, int64
     // odd words-per-lane: lane l's chunk starts at word l * WPL, and an odd stride
     // spreads the 32 lanes over all banks (WPL = 48 was a 16-way conflict on every
     // shared-memory access of the doubling, 24 an 8-way one)
-    auto kern = need <= 32 * 11 ? summaries_kernel<11>
-                : need <= 32 * 13 ? summaries_kernel<13>
-                : need <= 32 * 25 ? summaries_kernel<25>
-                : need <= 32 * 49 ? summaries_kernel<49> : summaries_kernel<0>;
+    const bool gen = g.single || (r & 1);
+    auto kern = need <= 32 * 10 ? (gen ? summaries_kernel<10, true> : summaries_kernel<10, false>)
+                : need <= 32 * 11 ? (gen ? summaries_kernel<11, true> : summaries_kernel<11, false>)
+                : need <= 32 * 13 ? (gen ? summaries_kernel<13, true> : summaries_kernel<13, false>)
+                : need <= 32 * 25 ? summaries_kernel<25, true>
+                : need <= 32 * 49 ? summaries_kernel<49, true> : summaries_kernel<0, true>;
     SSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * g.nwb, smem);
