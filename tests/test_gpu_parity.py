@@ -321,6 +321,35 @@ def test_duplicates_tie_break_by_id(cuda):
     assert res[0].ids[:3] == [7, 57, 107]
 
 
+@pytest.mark.parametrize("m,band,N", [(514, 0.05, 700), (1022, 0.05, 300), (600, 0.085, 500), (2050, 0.1, 90),
+                                      (777, 0.033, 400), (1500, 0.02, 150)])
+def test_odd_shapes_vs_oracle(cuda, m, band, N):
+    """Row lengths that are not multiples of 4, odd and even radii on the
+    long-row (single buffer) and short-row summaries forms, rows longer than
+    512 with few series: signatures, |R|, ids and squared distances equal to
+    the oracle's."""
+    import paper_1610_07328_b200 as ssh
+    from fixture_data import perturbed_queries, random_walks
+
+    X = random_walks(N, m, 4000 + m)
+    Q, _ = perturbed_queries(X, 5, 77 + m)
+    p = params(band, K=2)
+    idx = ssh.build_index(ssh.Dataset(X), p)
+    oidx = O.build_index(X, 80, 3, 15, 20, 2, 0, band)
+    assert np.array_equal(idx.signatures, oidx.sig)
+    ores = O.query_batch(oidx, Q, 7)
+    for i, r in enumerate(ssh.query_index_batch(idx, Q, 7)):
+        n = int(ores["n"][i])
+        assert r.stats.candidates == int(ores["n_cand"][i]), i
+        assert r.ids == ores["ids"][i][:n].tolist(), i
+        assert r.distances == np.sqrt(ores["d2"][i][:n]).tolist(), i
+    # exact search (R = the whole shard) exercises every summary row
+    xres = ssh.exact_search_batch(ssh.Dataset(X), Q, 7, ssh.WarpingParams(band=band))
+    for q, r in zip(Q, xres):
+        oi, od = O.brute_force_topk_over(X, np.arange(N), q, O.radius(band, m), 7)
+        assert r.ids == oi.tolist() and r.distances == np.sqrt(od).tolist()
+
+
 def test_massive_ties_beyond_rescoring_lists(cuda):
     """6,000 copies of one series: every copy ties at distance 0 with the query,
     far more than the rescoring lists (4096 + 4k) hold.  The reference cascade
